@@ -1,0 +1,173 @@
+/*
+ * cavs.h — C-ABI of the B200-native level-batched vertex-function engine.
+ *
+ * The hot path of Cavs (Zhang et al., arXiv 1712.04048; PAPER.md = the paper's
+ * LaTeX at /root/reference/PAPER.md, "P:Lnnn" = its line nnn): a static vertex
+ * function F is declared once and evaluated, forward and backward, over a
+ * minibatch of K instance-specific input graphs G (§1; Fig. 1c P:L120-125;
+ * P:L226-234 §3), batching all "activated" vertices of all K graphs into one
+ * task per step (Algorithm 1, §3.2).
+ *
+ * Calls, in order:  cavs_create -> cavs_workspace_bytes -> cavs_set_workspace
+ *   -> per batch: cavs_load_graphs -> cavs_schedule -> cavs_forward -> cavs_backward
+ *
+ * Conventions
+ *  - Every call returns a cavs_status; CAVS_OK == 0.  No exceptions, abort or
+ *    exit cross this boundary.  cavs_last_error() gives a message.
+ *  - All device work is enqueued on the context's CUDA stream (cavs_create /
+ *    cavs_set_stream) and is asynchronous, EXCEPT cavs_schedule, which reads
+ *    back a small header (status word, T, level_ptr[0..T]) and synchronises the
+ *    stream once, and the *_host entry points, which synchronise at the end.
+ *  - The library never allocates device memory: all scratch is carved from one
+ *    caller-owned device buffer (cavs_set_workspace).  The caller (PyTorch in
+ *    this repo) owns memory, streams and process groups.
+ *  - A context is single-threaded; use one per GPU / rank.
+ *  - "Global vertex id" of local vertex u of graph k = graph_ptr[k] + u
+ *    (SPEC S:L251).  The child order inside a CSR row is the gather index k of
+ *    Fig. 5 (`gather(k)`) — reading Z3 of DESIGN.md.
+ *
+ * Packed fp32 parameters (caller memory, same layout for dparams):
+ *  Tree-LSTM / LSTM (cell CAVS_CELL_TREE_LSTM; LSTM is N = 1), Fig. 5 P:L321-328:
+ *     W[4h x d] rows (i,f,o,u) | U_iou[3h x h] rows (i,o,u) | U_f[h x h] | b[4h] (i,f,o,u)
+ *     (child-sum form with one U_f shared by all k, reading Z6)
+ *  Tree-FC (CAVS_CELL_TREE_FC, N = 2), "a single fully-connected layer" P:L608,
+ *  reading Z7: h = tanh(W_c [h_l ; h_r] + W_x x + b):
+ *     W_c[h x 2h] (cols h_l | h_r) | W_x[h x d] | b[h]
+ *  Row-major everywhere.
+ */
+#ifndef CAVS_H_
+#define CAVS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum cavs_status {
+  CAVS_OK = 0,
+  CAVS_E_INVALID = 1,     /* bad argument / malformed graph (K<1, empty graph, id out of range, sizes) */
+  CAVS_E_ARITY = 2,       /* a vertex has more than N children */
+  CAVS_E_CYCLE = 3,       /* G is not a DAG: some vertex is never activated */
+  CAVS_E_FANOUT = 4,      /* a vertex has more than one parent: DAG fan-out is not supported
+                             in this version (forests only) */
+  CAVS_E_STATE = 5,       /* call out of order (e.g. backward before forward) */
+  CAVS_E_CAPACITY = 6,    /* batch exceeds the context's max_* or the workspace is too small */
+  CAVS_E_CUDA = 7,        /* a CUDA runtime/driver error; see cavs_last_error */
+  CAVS_E_UNSUPPORTED = 8  /* e.g. bf16 tensor-core mode with h or d not a multiple of 64 */
+} cavs_status;
+
+typedef enum cavs_cell { CAVS_CELL_TREE_LSTM = 0, CAVS_CELL_TREE_FC = 1 } cavs_cell;
+
+typedef enum cavs_precision {
+  CAVS_FP32 = 0,   /* fp32 operands, FFMA GEMMs, accurate expf/tanhf: parity 1e-5 */
+  CAVS_BF16 = 1    /* bf16 GEMM operands (RN-even), fp32 accumulate on tcgen05 tensor
+                      cores, all elementwise math and state in fp32: parity 2e-2 */
+} cavs_precision;
+
+typedef struct cavs_desc {
+  int32_t cell;          /* cavs_cell */
+  int32_t N;             /* arity: max children per vertex (gather slots); Tree-FC requires 2 */
+  int32_t h;             /* hidden size */
+  int32_t d;             /* input (pull) size */
+  int32_t precision;     /* cavs_precision */
+  int32_t max_graphs;    /* capacity: K per batch */
+  int32_t max_vertices;  /* capacity: V per batch (sum over graphs) */
+  int32_t max_x;         /* capacity: pull records n_x per batch */
+} cavs_desc;
+
+typedef struct cavs_ctx cavs_ctx;
+
+/* Number of fp32 entries of the packed parameter vector (layout above). */
+size_t cavs_param_count(int32_t cell, int32_t N, int32_t h, int32_t d);
+
+/* Fix F (cell, N, h, d, precision) and capacities ("declared ... and optimized once").
+ * `cuda_stream` is a cudaStream_t (NULL = legacy default stream).  The context
+ * owns no device memory until cavs_set_workspace.
+ * Errors: CAVS_E_INVALID (N<1, h<1, d<1, unknown cell/precision, capacities < 1),
+ *         CAVS_E_UNSUPPORTED (BF16 with h % 64 or d % 64 != 0; Tree-FC with N != 2),
+ *         CAVS_E_CUDA (bad device). */
+cavs_status cavs_create(const cavs_desc* desc, int device, void* cuda_stream, cavs_ctx** out);
+
+/* Change the stream subsequent calls are enqueued on. */
+cavs_status cavs_set_stream(cavs_ctx* ctx, void* cuda_stream);
+
+/* Bytes of device scratch the context needs for its capacities (all arenas of
+ * the dynamic-tensor plan, Fig. 7, plus schedule arrays and weight copies). */
+size_t cavs_workspace_bytes(const cavs_ctx* ctx);
+
+/* Hand the context its scratch: `dev` must be device memory of >= cavs_workspace_bytes,
+ * 256-byte aligned, kept alive (and not used by anyone else) until cavs_destroy.
+ * The buffer is zeroed here (stream-ordered).  Errors: CAVS_E_CAPACITY, CAVS_E_INVALID. */
+cavs_status cavs_set_workspace(cavs_ctx* ctx, void* dev, size_t bytes);
+
+/* Load the K input graphs of one minibatch as CSR child lists per instance
+ * ("reads training samples and their associated graphs", §4).
+ *   graph_ptr [K+1]: global vertex offsets, graph_ptr[0] = 0, graph_ptr[K] = V
+ *   child_ptr [V+1]: CSR row pointers over global vertices, child_ptr[V] = E
+ *   child_idx [E]  : children as INSTANCE-LOCAL ids (0 .. n_k-1); row order = gather index k
+ * `on_device` != 0: the three arrays are device pointers, else host pointers.  They are
+ * copied (stream-ordered) and only borrowed until that copy completes.
+ * Host-side checks: K, V, E within capacity (CAVS_E_CAPACITY), K >= 1 (CAVS_E_INVALID).
+ * Content checks run on the device and are reported by cavs_schedule.
+ * Resets the state to LOADED. */
+cavs_status cavs_load_graphs(cavs_ctx* ctx, int32_t K, int32_t V, int32_t E,
+                             const int32_t* graph_ptr, const int32_t* child_ptr,
+                             const int32_t* child_idx, int on_device);
+
+/* Algorithm 1's task partition on the device: level(v) = 0 without
+ * children, else 1 + max over children; V_t = {v : level(v) = t} ordered by ascending
+ * global id; T = number of tasks.  Also builds the dynamic-tensor plan (positions,
+ * child/parent slots; Fig. 7, Alg. 2).  Validates the graphs.
+ * Synchronises the stream once (reads back status, T and level_ptr).
+ * `T_out` may be NULL.
+ * Errors: CAVS_E_STATE (nothing loaded), CAVS_E_INVALID, CAVS_E_ARITY, CAVS_E_CYCLE,
+ *         CAVS_E_FANOUT, CAVS_E_CUDA. */
+cavs_status cavs_schedule(cavs_ctx* ctx, int32_t* T_out);
+
+/* Copy the schedule into HOST buffers (any may be NULL):
+ *   level [V], level_ptr [T+1], order [V] (position -> global vertex id).  Synchronous. */
+cavs_status cavs_get_schedule(cavs_ctx* ctx, int32_t* level, int32_t* level_ptr, int32_t* order);
+
+/* Forward pass over all K graphs (Alg. 1 FORWARD + Alg. 2): the eager pull/input
+ * projection for all vertices with a record, then one batched task per level
+ * t = 0..T-1 (gather -> cell -> scatter/push fused in one kernel per level).
+ *   params  [P]      device fp32, packed layout above
+ *   x       [n_x, d] device fp32 pull records
+ *   x_row   [V]      device int32: record of each global vertex, -1 = none (pull() -> 0)
+ *   h_out   [V, h]   device fp32 output: push(h) of every vertex, global id order (Fig. 5)
+ * Activations stay in the workspace for cavs_backward.
+ * Errors: CAVS_E_STATE (not scheduled), CAVS_E_CAPACITY (n_x > max_x), CAVS_E_INVALID (NULL). */
+cavs_status cavs_forward(cavs_ctx* ctx, const float* params, int32_t n_x, const float* x,
+                         const int32_t* x_row, float* h_out);
+
+/* Backward pass (Alg. 1 BACKWARD): tasks in reverse order, gradients
+ * ADDED; scatter is gather's adjoint, push is pull's; parameter
+ * gradients are lazily batched over all vertices once after the level loop (§3.5).
+ *   dh_out  [V, h]   device fp32: dL/d(push h) of every vertex (the external loss's cotangent)
+ *   dparams [P]      device fp32, OVERWRITTEN with dL/dparams summed over all K graphs
+ *   dx      [n_x, d] device fp32, OVERWRITTEN with dL/dx (may be NULL)
+ * Errors: CAVS_E_STATE (no forward since the last schedule), CAVS_E_INVALID. */
+cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dparams, float* dx);
+
+/* One whole training step from HOST buffers (the end-to-end entry point): stages the
+ * CSR, params, x, x_row and dh_out host->device, runs load/schedule/forward/backward,
+ * and copies dparams (and dx if non-NULL, and h_out if non-NULL) device->host.
+ * Host buffers should be pinned for asynchronous copies.  Synchronises at the end. */
+cavs_status cavs_train_step_host(cavs_ctx* ctx, int32_t K, int32_t V, int32_t E,
+                                 const int32_t* graph_ptr, const int32_t* child_ptr,
+                                 const int32_t* child_idx, const float* params, int32_t n_x,
+                                 const float* x, const int32_t* x_row, const float* dh_out,
+                                 float* dparams, float* dx, float* h_out);
+
+/* Number of kernels the library launched since the context was created (diagnostic). */
+int64_t cavs_kernel_launches(const cavs_ctx* ctx);
+
+const char* cavs_last_error(const cavs_ctx* ctx);
+void cavs_destroy(cavs_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CAVS_H_ */

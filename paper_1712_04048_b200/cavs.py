@@ -1,0 +1,196 @@
+"""Thin ctypes binding of the C-ABI in include/cavs.h (argument marshalling only).
+
+Every step of the hot path runs inside libcavs.so (hand-written CUDA for sm_100a);
+this module only converts tensors to pointers.  PyTorch is used for device memory
+(the workspace and the caller's arrays) and for the CUDA stream — plumbing only.
+There is no CPU fallback: if the library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcavs.so")
+
+TREE_LSTM, TREE_FC = 0, 1
+FP32, BF16 = 0, 1
+CELLS = {"tree_lstm": TREE_LSTM, "tree_fc": TREE_FC}
+PRECISIONS = {"fp32": FP32, "bf16": BF16}
+STATUS = {0: "OK", 1: "E_INVALID", 2: "E_ARITY", 3: "E_CYCLE", 4: "E_FANOUT", 5: "E_STATE",
+          6: "E_CAPACITY", 7: "E_CUDA", 8: "E_UNSUPPORTED"}
+
+
+class CavsError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.name = STATUS.get(code, str(code))
+
+
+class _Desc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("cell", "N", "h", "d", "precision", "max_graphs", "max_vertices", "max_x")]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1712_04048_b200.build` "
+                          "(there is no fallback path)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, SZ, S = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctypes.c_int
+    sig = {
+        "cavs_param_count": (SZ, [I32, I32, I32, I32]),
+        "cavs_create": (S, [ctypes.POINTER(_Desc), ctypes.c_int, P, ctypes.POINTER(P)]),
+        "cavs_set_stream": (S, [P, P]),
+        "cavs_workspace_bytes": (SZ, [P]),
+        "cavs_set_workspace": (S, [P, P, SZ]),
+        "cavs_load_graphs": (S, [P, I32, I32, I32, P, P, P, ctypes.c_int]),
+        "cavs_schedule": (S, [P, ctypes.POINTER(I32)]),
+        "cavs_get_schedule": (S, [P, P, P, P]),
+        "cavs_forward": (S, [P, P, I32, P, P, P]),
+        "cavs_backward": (S, [P, P, P, P]),
+        "cavs_train_step_host": (S, [P, I32, I32, I32, P, P, P, P, I32, P, P, P, P, P, P]),
+        "cavs_kernel_launches": (I64, [P]),
+        "cavs_last_error": (ctypes.c_char_p, [P]),
+        "cavs_destroy": (None, [P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = _load()
+EXPORTS = ["cavs_param_count", "cavs_create", "cavs_set_stream", "cavs_workspace_bytes",
+           "cavs_set_workspace", "cavs_load_graphs", "cavs_schedule", "cavs_get_schedule",
+           "cavs_forward", "cavs_backward", "cavs_train_step_host", "cavs_kernel_launches",
+           "cavs_last_error", "cavs_destroy"]
+
+
+def lib():
+    return _lib
+
+
+def param_count(cell, N, h, d) -> int:
+    return int(_lib.cavs_param_count(CELLS.get(cell, cell), N, h, d))
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"]
+        return a.ctypes.data
+    assert a.is_contiguous(), "tensors must be contiguous"
+    return a.data_ptr()
+
+
+class Context:
+    """One engine instance: F fixed at creation (cell, N, h, d, precision), capacities fixed."""
+
+    def __init__(self, cell, N, h, d, precision="fp32", max_graphs=256, max_vertices=1 << 16,
+                 max_x=None, device=0, stream=None):
+        import torch
+        self._torch = torch
+        self.cell, self.N, self.h, self.d = cell, N, h, d
+        self.precision = precision
+        self.device = torch.device("cuda", device)
+        desc = _Desc(CELLS.get(cell, cell), N, h, d, PRECISIONS.get(precision, precision), max_graphs,
+                     max_vertices, max_vertices if max_x is None else max_x)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        out = ctypes.c_void_p()
+        st = _lib.cavs_create(ctypes.byref(desc), device, ctypes.c_void_p(stream.cuda_stream), ctypes.byref(out))
+        if st != 0:
+            raise CavsError(st, "cavs_create failed")
+        self._ctx = out
+        nbytes = int(_lib.cavs_workspace_bytes(self._ctx))
+        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        base = self.workspace.data_ptr()
+        aligned = (base + 255) & ~255
+        self._check(_lib.cavs_set_workspace(self._ctx, ctypes.c_void_p(aligned), nbytes))
+        self.P = param_count(cell, N, h, d)
+        self.V = 0
+        self.T = 0
+
+    def _check(self, st):
+        if st != 0:
+            raise CavsError(st, (_lib.cavs_last_error(self._ctx) or b"").decode())
+
+    def set_stream(self, stream):
+        self.stream = stream
+        self._check(_lib.cavs_set_stream(self._ctx, ctypes.c_void_p(stream.cuda_stream)))
+
+    @property
+    def launches(self) -> int:
+        return int(_lib.cavs_kernel_launches(self._ctx))
+
+    def load_graphs(self, graph_ptr, child_ptr, child_idx):
+        """CSR child lists per instance; numpy (host) or torch CUDA int32 arrays."""
+        on_dev = not isinstance(graph_ptr, np.ndarray)
+        K = int(graph_ptr.shape[0]) - 1
+        V = int(child_ptr.shape[0]) - 1
+        E = int(child_idx.shape[0])
+        self._keep = (graph_ptr, child_ptr, child_idx)
+        self._check(_lib.cavs_load_graphs(self._ctx, K, V, E, _ptr(graph_ptr), _ptr(child_ptr),
+                                          _ptr(child_idx) if E else None, 1 if on_dev else 0))
+        self.V, self.K = V, K
+
+    def schedule(self) -> int:
+        T = ctypes.c_int32()
+        self._check(_lib.cavs_schedule(self._ctx, ctypes.byref(T)))
+        self.T = int(T.value)
+        return self.T
+
+    def get_schedule(self):
+        level = np.empty(self.V, np.int32)
+        level_ptr = np.empty(self.T + 1, np.int32)
+        order = np.empty(self.V, np.int32)
+        self._check(_lib.cavs_get_schedule(self._ctx, level.ctypes.data, level_ptr.ctypes.data, order.ctypes.data))
+        return level, level_ptr, order
+
+    def forward(self, params, x, x_row, h_out=None):
+        torch = self._torch
+        if h_out is None:
+            h_out = torch.empty(self.V, self.h, dtype=torch.float32, device=self.device)
+        self._fwd_keep = (params, x, x_row, h_out)
+        self._check(_lib.cavs_forward(self._ctx, _ptr(params), int(x.shape[0]), _ptr(x), _ptr(x_row), _ptr(h_out)))
+        return h_out
+
+    def backward(self, dh_out, dparams=None, dx=None, want_dx=True):
+        torch = self._torch
+        if dparams is None:
+            dparams = torch.empty(self.P, dtype=torch.float32, device=self.device)
+        if dx is None and want_dx:
+            x = self._fwd_keep[1]
+            dx = torch.empty(x.shape[0], self.d, dtype=torch.float32, device=self.device)
+        self._bwd_keep = (dh_out, dparams, dx)
+        self._check(_lib.cavs_backward(self._ctx, _ptr(dh_out), _ptr(dparams), _ptr(dx)))
+        return dparams, dx
+
+    def train_step_host(self, graph_ptr, child_ptr, child_idx, params, x, x_row, dh_out,
+                        dparams, dx=None, h_out=None):
+        """Whole step from HOST arrays (numpy or pinned CPU tensors); synchronous."""
+        K = int(graph_ptr.shape[0]) - 1
+        V = int(child_ptr.shape[0]) - 1
+        E = int(child_idx.shape[0])
+        self._check(_lib.cavs_train_step_host(
+            self._ctx, K, V, E, _ptr(graph_ptr), _ptr(child_ptr), _ptr(child_idx), _ptr(params),
+            int(x.shape[0]), _ptr(x), _ptr(x_row), _ptr(dh_out), _ptr(dparams), _ptr(dx), _ptr(h_out)))
+        self.V, self.K = V, K
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            _lib.cavs_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,430 @@
+// cavs_api.cu — the C-ABI (include/cavs.h): context, state machine, workspace carve-up
+// (the dynamic-tensor memory plan, Fig. 7) and launch orchestration
+// of Algorithm 1: schedule -> forward tasks t = 0..T-1 -> backward tasks
+// t = T-1..1 -> lazily batched parameter gradients (§3.5).
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "tc.h"
+
+using namespace cavs;
+
+enum { S_CREATED = 0, S_READY, S_LOADED, S_SCHEDULED, S_FORWARDED };
+
+struct cavs_ctx {
+  cavs_desc desc{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  int state = S_CREATED;
+  Dev D{};
+  std::vector<int> lp;          // host copy of level_ptr[0..T]
+  int T = 0, n_roots = 0;
+  int* h_hdr = nullptr;         // pinned readback buffer
+  std::string err;
+  int64_t launches = 0;
+  // lazy scratch layout
+  float* lazy_db = nullptr;
+  int split = 1;
+  // staging for cavs_train_step_host
+  float *s_params = nullptr, *s_x = nullptr, *s_dh = nullptr, *s_dp = nullptr, *s_dx = nullptr, *s_hout = nullptr;
+  int *s_xrow = nullptr, *s_gp = nullptr, *s_cp = nullptr, *s_ci = nullptr;
+  TcState* tc = nullptr;        // tensor-core (BF16) path state: TMA descriptors
+};
+
+static constexpr int kHdrWords = 4;
+static constexpr int kReadback = 1024;
+
+static cavs_status fail(cavs_ctx* c, cavs_status s, const std::string& m) {
+  if (c) c->err = m;
+  return s;
+}
+
+static cavs_status cuda_check(cavs_ctx* c, cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return CAVS_OK;
+  return fail(c, CAVS_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CK(expr) do { cavs_status _s = cuda_check(ctx, (expr), #expr); if (_s) return _s; } while (0)
+
+static bool is_lstm(const cavs_desc& d) { return d.cell == CAVS_CELL_TREE_LSTM; }
+static int gates(const cavs_desc& d) { return is_lstm(d) ? 3 + d.N : 1; }
+static size_t esize(const cavs_desc& d) { return d.precision == CAVS_BF16 ? 2 : 4; }
+
+// Lazy fp32 scratch: [S x main GEMM outputs] + db partials.
+static size_t lazy_main_floats(const cavs_desc& d, int S) {
+  const size_t h = d.h, dd = d.d;
+  if (is_lstm(d)) return (size_t)S * (3 * h * h + h * h + gates(d) * h * dd);
+  return (size_t)S * (2 * h * h + h * dd);
+}
+
+// Carve the workspace; with base == nullptr only computes the size.
+static size_t carve(cavs_ctx* c, char* base) {
+  const cavs_desc& d = c->desc;
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> char* {
+    off = (off + 255) & ~(size_t)255;
+    char* p = base ? base + off : nullptr;
+    off += bytes;
+    return p;
+  };
+  const size_t V = d.max_vertices, K = d.max_graphs, X = d.max_x, N = d.N, h = d.h, dd = d.d;
+  const size_t Vp = V + kPadRows, G = gates(d), es = esize(d);
+  Dev& D = c->D;
+  auto I = [&](size_t n) { return reinterpret_cast<int*>(take(n * 4)); };
+  auto F = [&](size_t n) { return reinterpret_cast<float*>(take(n * 4)); };
+  D.graph_ptr = I(K + 1); D.child_ptr = I(V + 1); D.child_idx = I(V + 1);
+  D.level = I(V); D.pos = I(V); D.graph_of = I(V); D.parent_v = I(V); D.slot_v = I(V);
+  D.pending = I(V); D.queue = I(V);
+  D.hdr = I(kHdrWords + V + 1); D.level_ptr = base ? D.hdr + kHdrWords : nullptr;
+  D.roots = I(V); D.cnt = I(V + 1);
+  D.order = I(V); D.child_pos = I(V * N); D.parent_pos = I(V); D.slot = I(V); D.deg = I(V);
+  D.xrow_pos = I(Vp); D.tile_x = I(Vp / 64 + 2);
+  D.Hk = take(Vp * N * h * es);
+  D.Hs = (is_lstm(d) && N >= 2) ? (void*)take(Vp * h * es) : nullptr;
+  D.Xp = take(Vp * dd * es);
+  D.dZ = take(Vp * G * h * es);
+  D.Ck = is_lstm(d) ? F(Vp * N * h) : nullptr;
+  D.XW = F(Vp * (is_lstm(d) ? 4 : 1) * h);
+  D.gates = F(Vp * G * h);
+  D.cst = is_lstm(d) ? F(Vp * h) : nullptr;
+  D.dcb = is_lstm(d) ? F(Vp * h) : nullptr;
+  D.bias = F(4 * h);
+  if (is_lstm(d)) {
+    D.Wa = take(4 * h * h * es); D.Wb = take(4 * h * dd * es); D.Wc = take(3 * h * h * es);
+    D.Wd = take(h * h * es); D.We = take(dd * G * h * es);
+  } else {
+    D.Wa = take(2 * h * h * es); D.Wb = take(h * dd * es); D.Wc = take(2 * h * h * es);
+    D.Wd = nullptr; D.We = take(dd * h * es);
+  }
+  D.lazy = F(lazy_main_floats(d, kSplitMax));
+  c->lazy_db = F((size_t)kDbChunks * G * h);
+  const size_t P = cavs_param_count(d.cell, d.N, d.h, d.d);
+  c->s_params = F(P); c->s_dp = F(P);
+  c->s_x = F(X * dd); c->s_dx = F(X * dd);
+  c->s_dh = F(V * h); c->s_hout = F(V * h);
+  c->s_xrow = I(V); c->s_gp = I(K + 1); c->s_cp = I(V + 1); c->s_ci = I(V + 1);
+  return (off + 255) & ~(size_t)255;
+}
+
+#define CAVS_API extern "C" __attribute__((visibility("default")))
+
+CAVS_API size_t cavs_param_count(int32_t cell, int32_t N, int32_t h, int32_t d) {
+  (void)N;
+  const size_t H = h, Dd = d;
+  if (cell == CAVS_CELL_TREE_LSTM) return 4 * H * Dd + 3 * H * H + H * H + 4 * H;
+  if (cell == CAVS_CELL_TREE_FC) return 2 * H * H + H * Dd + H;
+  return 0;
+}
+
+CAVS_API cavs_status cavs_create(const cavs_desc* desc, int device, void* stream, cavs_ctx** out) {
+  if (!desc || !out) return CAVS_E_INVALID;
+  *out = nullptr;
+  const cavs_desc& d = *desc;
+  if ((d.cell != CAVS_CELL_TREE_LSTM && d.cell != CAVS_CELL_TREE_FC) || d.N < 1 || d.h < 1 || d.d < 1 ||
+      (d.precision != CAVS_FP32 && d.precision != CAVS_BF16) || d.max_graphs < 1 || d.max_vertices < 1 ||
+      d.max_x < 0)
+    return CAVS_E_INVALID;
+  if (d.N > kMaxN) return CAVS_E_UNSUPPORTED;
+  if (d.cell == CAVS_CELL_TREE_FC && d.N != 2) return CAVS_E_UNSUPPORTED;
+  if (d.precision == CAVS_BF16 && ((d.h % 64) || (d.d % 64))) return CAVS_E_UNSUPPORTED;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return CAVS_E_CUDA;
+  cavs_ctx* c = new cavs_ctx();
+  c->desc = d;
+  c->device = device;
+  c->stream = reinterpret_cast<cudaStream_t>(stream);
+  c->D.cell = d.cell; c->D.N = d.N; c->D.h = d.h; c->D.d = d.d; c->D.prec = d.precision;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaMallocHost(&c->h_hdr, sizeof(int) * (kHdrWords + kReadback)) != cudaSuccess) {
+    delete c;
+    return CAVS_E_CUDA;
+  }
+  c->ws_bytes = carve(c, nullptr);
+  *out = c;
+  return CAVS_OK;
+}
+
+CAVS_API cavs_status cavs_set_stream(cavs_ctx* ctx, void* stream) {
+  if (!ctx) return CAVS_E_INVALID;
+  ctx->stream = reinterpret_cast<cudaStream_t>(stream);
+  return CAVS_OK;
+}
+
+CAVS_API size_t cavs_workspace_bytes(const cavs_ctx* ctx) { return ctx ? ctx->ws_bytes : 0; }
+
+CAVS_API cavs_status cavs_set_workspace(cavs_ctx* ctx, void* dev, size_t bytes) {
+  if (!ctx || !dev) return fail(ctx, CAVS_E_INVALID, "null workspace");
+  if ((reinterpret_cast<uintptr_t>(dev) & 255) != 0) return fail(ctx, CAVS_E_INVALID, "workspace not 256B aligned");
+  if (bytes < ctx->ws_bytes) return fail(ctx, CAVS_E_CAPACITY, "workspace too small");
+  CK(cudaSetDevice(ctx->device));
+  ctx->ws = reinterpret_cast<char*>(dev);
+  carve(ctx, ctx->ws);
+  CK(cudaMemsetAsync(ctx->ws, 0, ctx->ws_bytes, ctx->stream));   // arenas start finite (zero)
+  if (ctx->desc.precision == CAVS_BF16) {
+    cavs_status s = tc_init(ctx->D, ctx->desc.max_vertices, &ctx->tc, &ctx->err);
+    if (s) return s;
+  }
+  ctx->state = S_READY;
+  return CAVS_OK;
+}
+
+CAVS_API cavs_status cavs_load_graphs(cavs_ctx* ctx, int32_t K, int32_t V, int32_t E, const int32_t* graph_ptr,
+                             const int32_t* child_ptr, const int32_t* child_idx, int on_device) {
+  if (!ctx) return CAVS_E_INVALID;
+  if (ctx->state < S_READY) return fail(ctx, CAVS_E_STATE, "set_workspace first");
+  if (K < 1 || V < 1 || E < 0 || !graph_ptr || !child_ptr || (E > 0 && !child_idx))
+    return fail(ctx, CAVS_E_INVALID, "bad sizes or null pointers");
+  if (K > ctx->desc.max_graphs || V > ctx->desc.max_vertices || E > ctx->desc.max_vertices)
+    return fail(ctx, CAVS_E_CAPACITY, "batch exceeds context capacity");
+  CK(cudaSetDevice(ctx->device));
+  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  Dev& D = ctx->D;
+  CK(cudaMemcpyAsync((void*)D.graph_ptr, graph_ptr, sizeof(int) * (K + 1), kind, ctx->stream));
+  CK(cudaMemcpyAsync((void*)D.child_ptr, child_ptr, sizeof(int) * (V + 1), kind, ctx->stream));
+  if (E > 0) CK(cudaMemcpyAsync((void*)D.child_idx, child_idx, sizeof(int) * E, kind, ctx->stream));
+  D.K = K; D.V = V; D.E = E;
+  ctx->state = S_LOADED;
+  return CAVS_OK;
+}
+
+CAVS_API cavs_status cavs_schedule(cavs_ctx* ctx, int32_t* T_out) {
+  if (!ctx) return CAVS_E_INVALID;
+  if (ctx->state < S_LOADED) return fail(ctx, CAVS_E_STATE, "no graphs loaded");
+  CK(cudaSetDevice(ctx->device));
+  Dev& D = ctx->D;
+  CK(cudaMemsetAsync(D.hdr, 0, sizeof(int) * kHdrWords, ctx->stream));
+  CK(cudaMemsetAsync(D.cnt, 0, sizeof(int) * (D.V + 1), ctx->stream));
+  launch_schedule(D, ctx->stream);
+  ctx->launches += 5;
+  CK(cudaGetLastError());
+  const int nread = kHdrWords + std::min(D.V + 1, kReadback);
+  CK(cudaMemcpyAsync(ctx->h_hdr, D.hdr, sizeof(int) * nread, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const int st = ctx->h_hdr[0];
+  if (st) {
+    ctx->state = S_LOADED;
+    if (st & ST_INVALID) return fail(ctx, CAVS_E_INVALID, "malformed graph (range/shape)");
+    if (st & ST_ARITY) return fail(ctx, CAVS_E_ARITY, "a vertex has more than N children");
+    if (st & ST_FANOUT) return fail(ctx, CAVS_E_FANOUT, "a vertex has more than one parent");
+    return fail(ctx, CAVS_E_CYCLE, "input graph has a cycle");
+  }
+  const int T = ctx->h_hdr[1];
+  ctx->T = T;
+  ctx->n_roots = ctx->h_hdr[2];
+  ctx->lp.assign(T + 1, 0);
+  if (T + 1 <= nread - kHdrWords) {
+    std::memcpy(ctx->lp.data(), ctx->h_hdr + kHdrWords, sizeof(int) * (T + 1));
+  } else {
+    CK(cudaMemcpy(ctx->lp.data(), D.level_ptr, sizeof(int) * (T + 1), cudaMemcpyDeviceToHost));
+  }
+  D.T = T;
+  D.lp1 = T > 1 ? ctx->lp[1] : D.V;
+  ctx->state = S_SCHEDULED;
+  if (T_out) *T_out = T;
+  return CAVS_OK;
+}
+
+CAVS_API cavs_status cavs_get_schedule(cavs_ctx* ctx, int32_t* level, int32_t* level_ptr, int32_t* order) {
+  if (!ctx) return CAVS_E_INVALID;
+  if (ctx->state < S_SCHEDULED) return fail(ctx, CAVS_E_STATE, "not scheduled");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const Dev& D = ctx->D;
+  if (level) CK(cudaMemcpy(level, D.level, sizeof(int) * D.V, cudaMemcpyDeviceToHost));
+  if (level_ptr) std::memcpy(level_ptr, ctx->lp.data(), sizeof(int) * (ctx->T + 1));
+  if (order) CK(cudaMemcpy(order, D.order, sizeof(int) * D.V, cudaMemcpyDeviceToHost));
+  return CAVS_OK;
+}
+
+// --------------------------------------------------------------------------- forward
+template <class OpT>
+static void forward_simt(cavs_ctx* ctx) {
+  Dev& D = ctx->D;
+  const int h = D.h, d = D.d, N = D.N;
+  cudaStream_t s = ctx->stream;
+  SegListI L{};
+  if (D.cell == CAVS_CELL_TREE_LSTM) {
+    L.n = 4;
+    for (int g = 0; g < 4; ++g) L.s[g] = SegI{D.Wb, d, g * h, B_XP, 0, d, d, g};
+    simt_typeI<OpT>(D, EPI_LSTM_XPROJ, L, 0, D.V, h, s);
+    ctx->launches++;
+    SegListI F{};
+    F.n = 3 + N;
+    for (int g = 0; g < 3; ++g) F.s[g] = SegI{D.Wa, h, g * h, N >= 2 ? B_HSUM : B_HK, 0, N * h, h, g};
+    for (int k = 0; k < N; ++k) F.s[3 + k] = SegI{D.Wa, h, 3 * h, B_HK, k * h, N * h, h, 3 + k};
+    for (int t = 1; t < ctx->T; ++t) {
+      simt_typeI<OpT>(D, EPI_LSTM_FWD, F, ctx->lp[t], ctx->lp[t + 1], h, s);
+      ctx->launches++;
+    }
+  } else {
+    L.n = 1;
+    L.s[0] = SegI{D.Wb, d, 0, B_XP, 0, d, d, 0};
+    simt_typeI<OpT>(D, EPI_FC_XPROJ, L, 0, D.V, h, s);
+    ctx->launches++;
+    SegListI F{};
+    F.n = 1;
+    F.s[0] = SegI{D.Wa, 2 * h, 0, B_HK, 0, 2 * h, 2 * h, 0};
+    for (int t = 1; t < ctx->T; ++t) {
+      simt_typeI<OpT>(D, EPI_FC_FWD, F, ctx->lp[t], ctx->lp[t + 1], h, s);
+      ctx->launches++;
+    }
+  }
+}
+
+CAVS_API cavs_status cavs_forward(cavs_ctx* ctx, const float* params, int32_t n_x, const float* x,
+                         const int32_t* x_row, float* h_out) {
+  if (!ctx) return CAVS_E_INVALID;
+  if (ctx->state < S_SCHEDULED) return fail(ctx, CAVS_E_STATE, "cavs_schedule first");
+  if (!params || !x_row || !h_out || (n_x > 0 && !x)) return fail(ctx, CAVS_E_INVALID, "null pointer");
+  if (n_x < 0 || n_x > ctx->desc.max_x) return fail(ctx, CAVS_E_CAPACITY, "n_x exceeds max_x");
+  CK(cudaSetDevice(ctx->device));
+  Dev& D = ctx->D;
+  D.params = params; D.x = x; D.x_row = x_row; D.h_out = h_out; D.n_x = n_x;
+  launch_prep(D, ctx->stream);
+  launch_pull(D, ctx->stream);
+  ctx->launches += 2;
+  if (D.prec == CAVS_BF16) {
+    ctx->launches += tc_forward(D, ctx->tc, ctx->lp, ctx->stream);
+  } else {
+    forward_simt<float>(ctx);
+  }
+  CK(cudaGetLastError());
+  ctx->state = S_FORWARDED;
+  return CAVS_OK;
+}
+
+// --------------------------------------------------------------------------- backward
+template <class OpT>
+static void backward_simt(cavs_ctx* ctx) {
+  Dev& D = ctx->D;
+  const int h = D.h, d = D.d, N = D.N, G = gates(ctx->desc);
+  cudaStream_t s = ctx->stream;
+  SegListI B{};
+  int epi;
+  if (D.cell == CAVS_CELL_TREE_LSTM) {
+    B.n = 1 + N;
+    B.s[0] = SegI{D.Wc, 3 * h, 0, B_DZ, 0, G * h, 3 * h, 0};
+    for (int k = 0; k < N; ++k) B.s[1 + k] = SegI{D.Wd, h, 0, B_DZ, (3 + k) * h, G * h, h, 1 + k};
+    epi = EPI_LSTM_BWD;
+  } else {
+    B.n = 2;
+    for (int k = 0; k < 2; ++k) B.s[k] = SegI{D.Wc, h, k * h, B_DZ, 0, h, h, k};
+    epi = EPI_FC_BWD;
+  }
+  for (int t = ctx->T - 1; t >= 1; --t) {
+    simt_typeI<OpT>(D, epi, B, ctx->lp[t], ctx->lp[t + 1], h, s);
+    ctx->launches++;
+  }
+  // lazy batching of the parameter gradients over ALL vertices
+  float* lz = D.lazy;
+  const int lp1 = D.lp1, V = D.V;
+  if (D.cell == CAVS_CELL_TREE_LSTM) {
+    float* u4 = lz; float* uf = u4 + (size_t)3 * h * h; float* w = uf + (size_t)h * h;
+    SegListII A{};
+    A.n = 1;
+    A.s[0] = SegII{D.dZ, G * h, 0, N >= 2 ? D.Hs : D.Hk, N >= 2 ? h : N * h, 0, lp1, V, 0};
+    simt_typeII<OpT>(D, A, u4, 3 * h, h, h, s);
+    SegListII Bf{};
+    Bf.n = N;
+    for (int k = 0; k < N; ++k) Bf.s[k] = SegII{D.dZ, G * h, (3 + k) * h, D.Hk, N * h, k * h, lp1, V, 0};
+    simt_typeII<OpT>(D, Bf, uf, h, h, h, s);
+    SegListII Cw{};
+    Cw.n = 1;
+    Cw.s[0] = SegII{D.dZ, G * h, 0, D.Xp, d, 0, 0, V, 1};
+    simt_typeII<OpT>(D, Cw, w, G * h, d, d, s);
+    ctx->launches += 3;
+    SegListII dummy{};
+    (void)dummy;
+    SegListI X{};
+    X.n = 1;
+    X.s[0] = SegI{D.We, G * h, 0, B_DZ, 0, G * h, G * h, 0};
+    if (D.dx) { simt_typeI<OpT>(D, EPI_DX, X, 0, V, d, s); ctx->launches++; }
+  } else {
+    float* wc = lz; float* wx = wc + (size_t)2 * h * h;
+    SegListII A{};
+    A.n = 1;
+    A.s[0] = SegII{D.dZ, h, 0, D.Hk, 2 * h, 0, lp1, V, 0};
+    simt_typeII<OpT>(D, A, wc, h, 2 * h, 2 * h, s);
+    SegListII Cw{};
+    Cw.n = 1;
+    Cw.s[0] = SegII{D.dZ, h, 0, D.Xp, d, 0, 0, V, 1};
+    simt_typeII<OpT>(D, Cw, wx, h, d, d, s);
+    ctx->launches += 2;
+    SegListI X{};
+    X.n = 1;
+    X.s[0] = SegI{D.We, h, 0, B_DZ, 0, h, h, 0};
+    if (D.dx) { simt_typeI<OpT>(D, EPI_DX, X, 0, V, d, s); ctx->launches++; }
+  }
+}
+
+CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dparams, float* dx) {
+  if (!ctx) return CAVS_E_INVALID;
+  if (ctx->state < S_FORWARDED) return fail(ctx, CAVS_E_STATE, "cavs_forward first");
+  if (!dh_out || !dparams) return fail(ctx, CAVS_E_INVALID, "null pointer");
+  CK(cudaSetDevice(ctx->device));
+  Dev& D = ctx->D;
+  D.dh_out = dh_out; D.dparams = dparams; D.dx = dx;
+  launch_roots(D, ctx->n_roots, D.roots, ctx->stream);
+  ctx->launches++;
+  int split = 1;
+  if (D.prec == CAVS_BF16) {
+    ctx->launches += tc_backward(D, ctx->tc, ctx->lp, ctx->stream, &split);
+  } else {
+    backward_simt<float>(ctx);
+  }
+  launch_colsum(D, ctx->lazy_db, ctx->stream);
+  launch_pack(D, D.lazy, split, ctx->lazy_db, ctx->stream);
+  ctx->launches += 2;
+  CK(cudaGetLastError());
+  return CAVS_OK;
+}
+
+CAVS_API cavs_status cavs_train_step_host(cavs_ctx* ctx, int32_t K, int32_t V, int32_t E, const int32_t* graph_ptr,
+                                 const int32_t* child_ptr, const int32_t* child_idx, const float* params,
+                                 int32_t n_x, const float* x, const int32_t* x_row, const float* dh_out,
+                                 float* dparams, float* dx, float* h_out) {
+  if (!ctx) return CAVS_E_INVALID;
+  if (ctx->state < S_READY) return fail(ctx, CAVS_E_STATE, "set_workspace first");
+  if (n_x < 0 || n_x > ctx->desc.max_x || V > ctx->desc.max_vertices || V < 1)
+    return fail(ctx, CAVS_E_CAPACITY, "batch exceeds capacity");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const cavs_desc& d = ctx->desc;
+  const size_t P = cavs_param_count(d.cell, d.N, d.h, d.d);
+  cavs_status st = cavs_load_graphs(ctx, K, V, E, graph_ptr, child_ptr, child_idx, 0);
+  if (st) return st;
+  CK(cudaMemcpyAsync(ctx->s_params, params, sizeof(float) * P, cudaMemcpyHostToDevice, s));
+  if (n_x) CK(cudaMemcpyAsync(ctx->s_x, x, sizeof(float) * n_x * d.d, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->s_xrow, x_row, sizeof(int) * V, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->s_dh, dh_out, sizeof(float) * V * d.h, cudaMemcpyHostToDevice, s));
+  st = cavs_schedule(ctx, nullptr);
+  if (st) return st;
+  st = cavs_forward(ctx, ctx->s_params, n_x, ctx->s_x, ctx->s_xrow, ctx->s_hout);
+  if (st) return st;
+  st = cavs_backward(ctx, ctx->s_dh, ctx->s_dp, dx ? ctx->s_dx : nullptr);
+  if (st) return st;
+  CK(cudaMemcpyAsync(dparams, ctx->s_dp, sizeof(float) * P, cudaMemcpyDeviceToHost, s));
+  if (dx && n_x) CK(cudaMemcpyAsync(dx, ctx->s_dx, sizeof(float) * n_x * d.d, cudaMemcpyDeviceToHost, s));
+  if (h_out) CK(cudaMemcpyAsync(h_out, ctx->s_hout, sizeof(float) * V * d.h, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return CAVS_OK;
+}
+
+CAVS_API int64_t cavs_kernel_launches(const cavs_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+CAVS_API const char* cavs_last_error(const cavs_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+CAVS_API void cavs_destroy(cavs_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream); else cudaDeviceSynchronize();
+  tc_destroy(ctx->tc);
+  if (ctx->h_hdr) cudaFreeHost(ctx->h_hdr);
+  delete ctx;
+}
+

@@ -1,0 +1,66 @@
+// common.cuh — shared device/host definitions of the Cavs B200 engine (internal).
+//
+// Data layout in HBM: every per-vertex tensor of F is a
+// "dynamic tensor" (Fig. 7) laid out in POSITION order: the
+// vertices of task V_0 first, then V_1, ..., each task contiguous (offset of task t =
+// level_ptr[t] rows, bs = M_t).  Gather buffers are PARENT-slot arenas: a child's
+// scatter writes its state straight into row pos(parent), slot k of the gather arena
+// (Hk/Ck), so a task's gather operand is a contiguous row block.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/cavs.h"
+
+namespace cavs {
+
+enum : int { ST_INVALID = 1, ST_ARITY = 2, ST_CYCLE = 4, ST_FANOUT = 8 };
+
+// Device view of one context: sizes + every arena pointer.  Passed by value.
+struct Dev {
+  int cell, N, h, d, prec;
+  int K, V, E, n_x, T, lp1;          // lp1 = level_ptr[1] (first internal position), host copy
+  // loaded graphs (global CSR, instance-local child ids)
+  const int* graph_ptr; const int* child_ptr; const int* child_idx;
+  // schedule (vid-indexed)
+  int* level; int* pos; int* graph_of; int* parent_v; int* slot_v; int* pending; int* queue;
+  // schedule (position-indexed)
+  int* order; int* level_ptr; int* child_pos; int* parent_pos; int* slot; int* deg; int* xrow_pos;
+  int* tile_x;                      // per 64-position tile: 1 if any vertex has a pull record
+  int* hdr;                         // [0] status bits, [1] T, [2] #roots, [3] -, [4..] level_ptr
+  int* roots;                       // positions of vertices without a parent
+  int* cnt;                         // level histogram scratch [V+1]
+  // arenas (OpT = float in FP32 mode, __nv_bfloat16 in BF16 mode)
+  void* Hk;      // [Vp, N*h] gather slots of child h (written by the child's scatter)
+  void* Hs;      // [Vp, h]   child-sum h~ (Tree-LSTM, N >= 2)
+  void* Xp;      // [Vp, d]   pulled x in position order (zero rows: no record)
+  void* dZ;      // [Vp, G*h] gate-preactivation gradients (G = 3+N Tree-LSTM, 1 Tree-FC)
+  float* Ck;     // [Vp, N*h] gather slots of child c (Tree-LSTM)
+  float* XW;     // [Vp, Gx*h] eager x-projection for x-vertices above level 0
+  float* gates;  // [Vp, G*h] Tree-LSTM activations (i,o,u,f_1..f_N); Tree-FC: h
+  float* cst;    // [Vp, h]   Tree-LSTM memory cell c
+  float* dcb;    // [Vp, h]   Tree-LSTM dc-bar
+  float* bias;   // internal gate order (i,o,u,f) / (b)
+  // weight copies (OpT), see prep kernel
+  void* Wa; void* Wb; void* Wc; void* Wd; void* We;
+  // lazy outputs (fp32 scratch)
+  float* lazy;
+  // caller buffers of the current call
+  const float* params; const float* x; const int* x_row; const float* dh_out;
+  float* h_out; float* dparams; float* dx;
+};
+
+constexpr int kPadRows = 128;   // extra zero rows after V for TMA/K-block over-reach
+
+__host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+__device__ __forceinline__ float sigm(float z) { return 1.0f / (1.0f + expf(-z)); }
+
+template <class T> __device__ __forceinline__ T to_op(float v);
+template <> __device__ __forceinline__ float to_op<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 to_op<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+__device__ __forceinline__ float from_op(float v) { return v; }
+__device__ __forceinline__ float from_op(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+}  // namespace cavs

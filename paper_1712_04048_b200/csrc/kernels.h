@@ -1,0 +1,45 @@
+// kernels.h — internal launcher declarations (host side of the engine).
+#pragma once
+#include "common.cuh"
+
+namespace cavs {
+
+constexpr int kMaxN = 4;          // max arity supported by the kernels
+constexpr int kDbChunks = 32;     // row chunks of the deterministic db column reduction
+constexpr int kSplitMax = 8;      // max split-K of the lazy tensor-core GEMMs
+
+enum Epi : int { EPI_LSTM_FWD = 0, EPI_LSTM_XPROJ, EPI_LSTM_BWD, EPI_FC_FWD, EPI_FC_XPROJ, EPI_FC_BWD, EPI_DX };
+
+enum BSrc : int { B_HK = 0, B_XP = 1, B_DZ = 2, B_HSUM = 3 };
+
+// One type-I segment: acc[acc] += A[a_row + j, 0:klen] . B[p, b_col : b_col+klen]
+struct SegI {
+  const void* A; int lda; int a_row;
+  int b_src; int b_col; int ldb;
+  int klen; int acc;
+};
+struct SegListI { int n; SegI s[6]; };
+
+// One type-II segment: out[m, n] += sum_{q in [k_lo,k_hi)} A[q, a_col+m] * B[q, b_col+n]
+struct SegII {
+  const void* A; int lda; int a_col;
+  const void* B; int ldb; int b_col;
+  int k_lo, k_hi; int skip_no_x;
+};
+struct SegListII { int n; SegII s[4]; };
+
+void launch_schedule(const Dev& D, cudaStream_t s);
+
+template <class OpT>
+void simt_typeI(const Dev& D, int epi, const SegListI& L, int row_lo, int row_hi, int units, cudaStream_t s);
+template <class OpT>
+void simt_typeII(const Dev& D, const SegListII& L, float* out, int M, int Ncols, int ldo, cudaStream_t s);
+
+// ops.cu
+void launch_prep(const Dev& D, cudaStream_t s);
+void launch_pull(const Dev& D, cudaStream_t s);
+void launch_roots(const Dev& D, int n_roots, const int* roots, cudaStream_t s);
+void launch_colsum(const Dev& D, float* part, cudaStream_t s);
+void launch_pack(const Dev& D, const float* lazy_main, int split, const float* db_part, cudaStream_t s);
+
+}  // namespace cavs

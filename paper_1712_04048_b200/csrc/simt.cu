@@ -1,0 +1,171 @@
+// simt.cu — FP32 mode: FFMA (SIMT) level kernels with the fused cell epilogue, and the
+// lazily batched weight-gradient GEMMs (§3.5 lazy batching).
+//
+// Type I  ("weights x task rows"): out[unit j, position p] = sum_seg A_seg[a_row + j, :] . B_seg[p, :]
+//          over the positions of one task V_t, accumulators fed to the cell epilogue (cells.cuh).
+// Type II ("lazy reduction over positions"): out[m, n] = sum_seg sum_p A_seg[p, a_col+m] * B_seg[p, b_col+n].
+#include "cells.cuh"
+#include "kernels.h"
+
+namespace cavs {
+
+constexpr int ST = 32;   // tile edge
+
+template <class OpT>
+__device__ __forceinline__ float load_b(const Dev& D, const SegI& s, int p, int k) {
+  if (s.b_src == B_HSUM) {
+    const OpT* hk = reinterpret_cast<const OpT*>(D.Hk) + (size_t)p * D.N * D.h + k;
+    float v = 0.f;
+    for (int q = 0; q < D.N; ++q) v += from_op(hk[q * D.h]);
+    return v;
+  }
+  const OpT* base = reinterpret_cast<const OpT*>(s.b_src == B_HK ? D.Hk : s.b_src == B_XP ? D.Xp : D.dZ);
+  return from_op(base[(size_t)p * s.ldb + s.b_col + k]);
+}
+
+template <class OpT, int NACC, int E>
+__global__ void __launch_bounds__(256) k_simt_typeI(Dev D, SegListI L, int row_lo, int row_hi, int units) {
+  __shared__ float As[ST][ST + 1];   // [k][unit]
+  __shared__ float Bs[ST][ST + 1];   // [pos][k]
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int j0 = blockIdx.x * ST, p0 = row_lo + blockIdx.y * ST;
+  // tile skipping: no row of this tile needs the epilogue
+  {
+    bool act = false;
+    if (threadIdx.x < ST) { const int p = p0 + threadIdx.x; act = p < row_hi && row_active<E>(D, p); }
+    if (!__syncthreads_or(act)) return;
+  }
+  float acc[NACC][4];
+#pragma unroll
+  for (int a = 0; a < NACC; ++a)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) acc[a][r] = 0.f;
+
+  for (int si = 0; si < L.n; ++si) {
+    const SegI s = L.s[si];
+    const OpT* A = reinterpret_cast<const OpT*>(s.A);
+    float t[4] = {0.f, 0.f, 0.f, 0.f};
+    const bool write_hs = (s.b_src == B_HSUM) && blockIdx.x == 0 && D.Hs != nullptr;
+    for (int k0 = 0; k0 < s.klen; k0 += ST) {
+      for (int e = threadIdx.x; e < ST * ST; e += 256) {
+        const int u = e >> 5, k = e & 31;
+        const int j = j0 + u;
+        As[k][u] = (j < units && k0 + k < s.klen) ? from_op(A[(size_t)(s.a_row + j) * s.lda + k0 + k]) : 0.f;
+        const int p = p0 + u;
+        float bv = 0.f;
+        if (p < row_hi && k0 + k < s.klen) {
+          bv = load_b<OpT>(D, s, p, k0 + k);
+          if (write_hs) reinterpret_cast<OpT*>(D.Hs)[(size_t)p * D.h + k0 + k] = to_op<OpT>(bv);
+        }
+        Bs[u][k] = bv;
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int k = 0; k < ST; ++k) {
+        const float a = As[k][tx];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) t[r] = fmaf(a, Bs[ty + 8 * r][k], t[r]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < NACC; ++a)
+      if (a == s.acc)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[a][r] += t[r];
+  }
+  const int j = j0 + tx;
+  if (j >= units) return;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int p = p0 + ty + 8 * r;
+    if (p >= row_hi || !row_active<E>(D, p)) continue;
+    float v[NACC];
+#pragma unroll
+    for (int a = 0; a < NACC; ++a) v[a] = acc[a][r];
+    epilogue<E, OpT>(D, j, p, v);
+  }
+}
+
+template <class OpT>
+__global__ void __launch_bounds__(256) k_simt_typeII(Dev D, SegListII L, float* out, int M, int Ncols, int ldo) {
+  __shared__ float As[ST][ST + 1];   // [pos][m]
+  __shared__ float Bs[ST][ST + 1];   // [pos][n]
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int m0 = blockIdx.x * ST, n0 = blockIdx.y * ST;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int si = 0; si < L.n; ++si) {
+    const SegII s = L.s[si];
+    const OpT* A = reinterpret_cast<const OpT*>(s.A);
+    const OpT* B = reinterpret_cast<const OpT*>(s.B);
+    for (int q0 = s.k_lo; q0 < s.k_hi; q0 += ST) {
+      if (s.skip_no_x) {
+        const int t0 = q0 >> 6, t1 = min(q0 + ST - 1, s.k_hi - 1) >> 6;
+        if (!D.tile_x[t0] && !D.tile_x[t1]) continue;        // uniform across the CTA
+      }
+      for (int e = threadIdx.x; e < ST * ST; e += 256) {
+        const int r = e >> 5, c = e & 31;
+        const int q = q0 + r;
+        const bool ok = q < s.k_hi;
+        As[r][c] = (ok && m0 + c < M) ? from_op(A[(size_t)q * s.lda + s.a_col + m0 + c]) : 0.f;
+        Bs[r][c] = (ok && n0 + c < Ncols) ? from_op(B[(size_t)q * s.ldb + s.b_col + n0 + c]) : 0.f;
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int k = 0; k < ST; ++k) {
+        const float a = As[k][tx];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[r] = fmaf(a, Bs[k][ty + 8 * r], acc[r]);
+      }
+      __syncthreads();
+    }
+  }
+  const int m = m0 + tx;
+  if (m >= M) return;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int n = n0 + ty + 8 * r;
+    if (n < Ncols) out[(size_t)m * ldo + n] = acc[r];
+  }
+}
+
+template <class OpT, int NACC, int E>
+static void typeI(const Dev& D, const SegListI& L, int row_lo, int row_hi, int units, cudaStream_t s) {
+  if (row_hi <= row_lo) return;
+  dim3 grid(cdiv(units, ST), cdiv(row_hi - row_lo, ST));
+  k_simt_typeI<OpT, NACC, E><<<grid, 256, 0, s>>>(D, L, row_lo, row_hi, units);
+}
+
+template <class OpT>
+void simt_typeI(const Dev& D, int epi, const SegListI& L, int row_lo, int row_hi, int units, cudaStream_t s) {
+  switch (epi) {
+    case EPI_LSTM_XPROJ: typeI<OpT, 4, EPI_LSTM_XPROJ>(D, L, row_lo, row_hi, units, s); break;
+    case EPI_LSTM_FWD:
+      if (D.N == 1) typeI<OpT, 4, EPI_LSTM_FWD>(D, L, row_lo, row_hi, units, s);
+      else if (D.N == 2) typeI<OpT, 5, EPI_LSTM_FWD>(D, L, row_lo, row_hi, units, s);
+      else typeI<OpT, 3 + kMaxN, EPI_LSTM_FWD>(D, L, row_lo, row_hi, units, s);
+      break;
+    case EPI_LSTM_BWD:
+      if (D.N == 1) typeI<OpT, 2, EPI_LSTM_BWD>(D, L, row_lo, row_hi, units, s);
+      else if (D.N == 2) typeI<OpT, 3, EPI_LSTM_BWD>(D, L, row_lo, row_hi, units, s);
+      else typeI<OpT, 1 + kMaxN, EPI_LSTM_BWD>(D, L, row_lo, row_hi, units, s);
+      break;
+    case EPI_FC_XPROJ: typeI<OpT, 1, EPI_FC_XPROJ>(D, L, row_lo, row_hi, units, s); break;
+    case EPI_FC_FWD: typeI<OpT, 1, EPI_FC_FWD>(D, L, row_lo, row_hi, units, s); break;
+    case EPI_FC_BWD: typeI<OpT, 2, EPI_FC_BWD>(D, L, row_lo, row_hi, units, s); break;
+    default: typeI<OpT, 1, EPI_DX>(D, L, row_lo, row_hi, units, s); break;
+  }
+}
+
+template <class OpT>
+void simt_typeII(const Dev& D, const SegListII& L, float* out, int M, int Ncols, int ldo, cudaStream_t s) {
+  dim3 grid(cdiv(M, ST), cdiv(Ncols, ST));
+  k_simt_typeII<OpT><<<grid, 256, 0, s>>>(D, L, out, M, Ncols, ldo);
+}
+
+template void simt_typeI<float>(const Dev&, int, const SegListI&, int, int, int, cudaStream_t);
+template void simt_typeI<__nv_bfloat16>(const Dev&, int, const SegListI&, int, int, int, cudaStream_t);
+template void simt_typeII<float>(const Dev&, const SegListII&, float*, int, int, int, cudaStream_t);
+template void simt_typeII<__nv_bfloat16>(const Dev&, const SegListII&, float*, int, int, int, cudaStream_t);
+
+}  // namespace cavs

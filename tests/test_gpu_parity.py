@@ -1,0 +1,231 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, on the same
+seeded inputs.  Schedules bit-exact; fp32 mode within 1e-5 and bf16 mode within 2e-2
+relative (BASELINE.json north_star), plus a tight check of the bf16 path against the
+bf16-emulating oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle.cavs_oracle import global_children
+from workloads import gen
+
+from gpu_harness import compare, make_ctx, rel, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+BF16_TOL = 2e-2
+BF16_EMU_TOL = 2e-3
+
+
+def _sched_check(b, precision="fp32"):
+    ctx = make_ctx(b, precision)
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    ctx.load_graphs(t(b.graph_ptr), t(b.child_ptr), t(b.child_idx))
+    T = ctx.schedule()
+    level, level_ptr, order = ctx.get_schedule()
+    ch = global_children(b.graph_ptr, b.child_ptr, b.child_idx)
+    rl, rlp, ro = oracle.schedule(ch)
+    assert T == len(rlp) - 1
+    assert np.array_equal(level, rl)
+    assert np.array_equal(level_ptr, rlp)
+    assert np.array_equal(order, ro)
+    return T
+
+
+# ------------------------------------------------------------------ schedule
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+def test_schedule_bit_exact_configs(cfg):
+    for seed in (0, 1):
+        b = gen.make_config_batch(cfg, seed=seed, h=64) if cfg != "cfg5" else gen.make_config_batch(cfg, seed=seed, h=64)
+        _sched_check(b)
+
+
+@pytest.mark.parametrize("graphs", [
+    "chain4096", "singletons", "forest", "star4", "mixed_spec", "deep_shallow"])
+def test_schedule_adversarial(graphs):
+    rng = np.random.default_rng(5)
+    N = 2
+    if graphs == "chain4096":
+        g = [gen.permute(gen.chain(4096), rng), gen.chain(1)]
+        N = 1
+    elif graphs == "singletons":
+        g = [[[]] for _ in range(37)]
+    elif graphs == "forest":
+        g = [[[], [], [0, 1], [], [3], [], [5]] for _ in range(5)]   # several roots per instance
+    elif graphs == "star4":
+        g = [[[1, 2, 3, 4], [], [], [], []]]
+        N = 4
+    elif graphs == "mixed_spec":
+        g = [gen.chain(3), [[], [], [0, 1]]]
+    else:
+        g = [gen.permute(gen.chain(300), rng)] + [gen.permute(gen.remy_tree(5, rng), rng) for _ in range(50)]
+        N = 2
+    b = gen.batch_from_graphs(g, cell="tree_lstm", N=N, h=64, d=64, seed=1)
+    _sched_check(b)
+
+
+def test_schedule_mixed_batch_tasks():
+    b = gen.batch_from_graphs([gen.chain(3), [[], [], [0, 1]]], cell="tree_lstm", N=2, h=64, d=64, seed=0)
+    _sched_check(b)
+    ctx = make_ctx(b, "fp32")
+    ctx.load_graphs(b.graph_ptr, b.child_ptr, b.child_idx)
+    assert ctx.schedule() == 3
+    _, lp, order = ctx.get_schedule()
+    assert [sorted(order[lp[t]:lp[t + 1]].tolist()) for t in range(3)] == [[0, 3, 4], [1, 5], [2]]
+
+
+# ------------------------------------------------------------------ errors
+@pytest.mark.parametrize("graphs,N,code", [
+    ([[[1], [0]]], 2, "E_CYCLE"),
+    ([[[0]]], 2, "E_CYCLE"),
+    ([[[], [0, 2], [1]]], 2, "E_CYCLE"),
+    ([[[1, 2, 3], [], [], []]], 2, "E_ARITY"),
+    ([[[5], []]], 2, "E_INVALID"),
+    ([[[1, 1], []]], 2, "E_FANOUT"),
+])
+def test_schedule_errors(graphs, N, code):
+    from paper_1712_04048_b200 import CavsError
+    b = gen.batch_from_graphs(graphs, cell="tree_lstm", N=N, h=64, d=64, seed=0)
+    ctx = make_ctx(b, "fp32")
+    ctx.load_graphs(b.graph_ptr, b.child_ptr, b.child_idx)
+    with pytest.raises(CavsError) as e:
+        ctx.schedule()
+    assert e.value.name == code
+    # a valid batch afterwards still works on the same context
+    ok = gen.batch_from_graphs([gen.chain(2)], cell="tree_lstm", N=N, h=64, d=64, seed=0)
+    ctx.load_graphs(ok.graph_ptr, ok.child_ptr, ok.child_idx)
+    assert ctx.schedule() == 2
+
+
+def test_call_order_errors():
+    from paper_1712_04048_b200 import CavsError
+    b = gen.make_config_batch("cfg1", seed=0)
+    ctx = make_ctx(b, "fp32")
+    dev = torch.device("cuda", 0)
+    with pytest.raises(CavsError) as e:
+        ctx.schedule()
+    assert e.value.name == "E_STATE"
+    ctx.load_graphs(b.graph_ptr, b.child_ptr, b.child_idx)
+    ctx.schedule()
+    with pytest.raises(CavsError) as e:
+        ctx.backward(torch.zeros(b.V, b.h, device=dev), torch.zeros(ctx.P, device=dev), want_dx=False)
+    assert e.value.name == "E_STATE"
+    big = gen.make_config_batch("cfg1", seed=0, K=8)
+    with pytest.raises(CavsError) as e:
+        ctx.load_graphs(big.graph_ptr, big.child_ptr, big.child_idx)
+    assert e.value.name == "E_CAPACITY"
+
+
+# ------------------------------------------------------------------ fp32 numerics
+FP32_CASES = {
+    "cfg1_tree_fc": lambda: gen.make_config_batch("cfg1", seed=0),
+    "cfg1_seed3": lambda: gen.make_config_batch("cfg1", seed=3),
+    "tree_lstm_sst": lambda: gen.make_batch("tree_lstm", 2, 48, 40, "sst_tree", 24, seed=2),
+    "lstm_chain": lambda: gen.make_batch("tree_lstm", 1, 40, 24, "sst_chain", 12, seed=3),
+    "fixed_lstm": lambda: gen.make_batch("tree_lstm", 1, 32, 32, "chain64", 4, seed=4),
+    "tree_fc_cbt": lambda: gen.make_batch("tree_fc", 2, 40, 24, "cbt32", 5, seed=5),
+    "tree_lstm_N3": lambda: gen.batch_from_graphs(
+        [[[], [], [], [0, 1, 2], [3], [], [4, 5]] for _ in range(3)] + [[[]]],
+        cell="tree_lstm", N=3, h=24, d=16, seed=6, x_at="all", loss_at="all"),
+    "tree_lstm_unary_forest": lambda: gen.batch_from_graphs(
+        [[[], [], [0, 1], [], [3], [2, 4], [], [6]]] * 4, cell="tree_lstm", N=2, h=33, d=17, seed=7,
+        x_at="all", loss_at="all"),
+}
+
+
+@pytest.mark.parametrize("case", list(FP32_CASES))
+def test_fp32_parity(case):
+    b = FP32_CASES[case]()
+    g = run_gpu(b, "fp32")
+    r = run_oracle(b)
+    compare(b, g, r, FP32_TOL, case)
+
+
+def test_host_and_device_inputs_agree():
+    b = gen.make_config_batch("cfg1", seed=1)
+    g1 = run_gpu(b, "fp32", on_device=True)
+    g2 = run_gpu(b, "fp32", on_device=False)
+    assert np.array_equal(g1["h_out"], g2["h_out"])
+    assert np.array_equal(g1["dparams"], g2["dparams"])
+
+
+def test_context_reuse_across_batches():
+    """Capacity sized for the largest batch; smaller/different batches reuse the arenas."""
+    b0 = gen.make_batch("tree_lstm", 2, 32, 32, "sst_tree", 20, seed=8)
+    b1 = gen.make_batch("tree_lstm", 2, 32, 32, "sst_tree", 7, seed=9)
+    b1.params = b0.params
+    ctx = make_ctx(b0, "fp32", max_vertices=b0.V + b1.V, max_graphs=40, max_x=b0.n_x + b1.n_x)
+    for b in (b0, b1, b0):
+        g = run_gpu(b, "fp32", ctx=ctx)
+        compare(b, g, run_oracle(b), FP32_TOL, "reuse")
+
+
+def test_train_step_host_matches_device_path():
+    b = gen.make_batch("tree_lstm", 2, 32, 32, "sst_tree", 10, seed=10)
+    g = run_gpu(b, "fp32")
+    ctx = make_ctx(b, "fp32")
+    dp = np.empty_like(b.params)
+    dx = np.empty_like(b.x)
+    ho = np.empty((b.V, b.h), np.float32)
+    ctx.train_step_host(b.graph_ptr, b.child_ptr, b.child_idx, b.params, b.x, b.x_row, b.gamma, dp, dx, ho)
+    assert np.array_equal(dp, g["dparams"])
+    assert np.array_equal(dx, g["dx"])
+    assert np.array_equal(ho, g["h_out"])
+
+
+# ------------------------------------------------------------------ bf16 numerics
+BF16_CASES = {
+    "tree_lstm_sst_h64": lambda: gen.make_batch("tree_lstm", 2, 64, 64, "sst_tree", 24, seed=11),
+    "tree_lstm_sst_h128_d64": lambda: gen.make_batch("tree_lstm", 2, 128, 64, "sst_tree", 40, seed=12),
+    "lstm_chain_h64": lambda: gen.make_batch("tree_lstm", 1, 64, 64, "sst_chain", 16, seed=13),
+    "tree_fc_cbt_h64": lambda: gen.make_batch("tree_fc", 2, 64, 128, "cbt32", 6, seed=14),
+    "tree_lstm_unary_h64": lambda: gen.batch_from_graphs(
+        [[[], [], [0, 1], [], [3], [2, 4], [], [6]]] * 9, cell="tree_lstm", N=2, h=64, d=64, seed=15,
+        x_at="all", loss_at="all"),
+}
+
+
+@pytest.mark.parametrize("case", list(BF16_CASES))
+def test_bf16_parity(case):
+    b = BF16_CASES[case]()
+    g = run_gpu(b, "bf16")
+    compare(b, g, run_oracle(b), BF16_TOL, case + " vs fp64 oracle")
+    compare(b, g, run_oracle(b, emulate_bf16=True), BF16_EMU_TOL, case + " vs bf16-emulating oracle")
+
+
+# ------------------------------------------------------------------ full-size, sampled
+@pytest.mark.parametrize("cfg,precision,sample", [("cfg4", "bf16", [0, 77, 255]), ("cfg4", "fp32", [3, 200]),
+                                                   ("cfg2", "bf16", [5]), ("cfg5", "bf16", [9])])
+def test_full_size_sampled(cfg, precision, sample):
+    """BASELINE sizes in the bench's launch configuration.  Graphs are independent, so the
+    h of sampled graphs is checked row by row; Gamma is zeroed outside the sample, so the
+    full-batch dparams equal the oracle's dparams over the sampled graphs alone."""
+    b = gen.make_config_batch(cfg, seed=0)
+    keep = np.zeros(b.V, bool)
+    for k in sample:
+        keep[b.graph_ptr[k]:b.graph_ptr[k + 1]] = True
+    b.gamma[~keep] = 0
+    g = run_gpu(b, precision)
+    graphs_ch = global_children(b.graph_ptr, b.child_ptr, b.child_idx)
+    sub = []
+    for k in sample:
+        lo = int(b.graph_ptr[k])
+        sub.append([[c - lo for c in graphs_ch[v]] for v in range(lo, int(b.graph_ptr[k + 1]))])
+    sb = gen.batch_from_graphs(sub, cell=b.cell, N=b.N, h=b.h, d=b.d, seed=0, params=b.params,
+                               x_at="all" if b.is_chain else "leaves", loss_at="all" if b.is_chain else "roots")
+    rows = np.concatenate([np.arange(b.graph_ptr[k], b.graph_ptr[k + 1]) for k in sample])
+    xr = b.x_row[rows]
+    sb.x = b.x[xr[xr >= 0]]
+    sb.x_row = np.where(xr >= 0, np.cumsum(xr >= 0) - 1, -1).astype(np.int32)
+    sb.gamma = b.gamma[rows]
+    r = run_oracle(sb)
+    tol = FP32_TOL if precision == "fp32" else BF16_TOL
+    assert rel(g["h_out"][rows], r["h_out"]) <= tol
+    from gpu_harness import param_blocks
+    for name, sl in param_blocks(b):
+        e = rel(g["dparams"][sl], r["dparams"][sl])
+        assert e <= tol, (name, e)
+    assert rel(g["dx"][xr[xr >= 0]], r["dx"]) <= tol
