@@ -30,7 +30,6 @@ struct cavs_ctx {
   int64_t launches = 0;
   // lazy scratch layout
   float* lazy_db = nullptr;
-  int split = 1;
   // staging for cavs_train_step_host
   float *s_params = nullptr, *s_x = nullptr, *s_dh = nullptr, *s_dp = nullptr, *s_dx = nullptr, *s_hout = nullptr;
   int *s_xrow = nullptr, *s_gp = nullptr, *s_cp = nullptr, *s_ci = nullptr;
@@ -54,13 +53,6 @@ static cavs_status cuda_check(cavs_ctx* c, cudaError_t e, const char* where) {
 static bool is_lstm(const cavs_desc& d) { return d.cell == CAVS_CELL_TREE_LSTM; }
 static int gates(const cavs_desc& d) { return is_lstm(d) ? 3 + d.N : 1; }
 static size_t esize(const cavs_desc& d) { return d.precision == CAVS_BF16 ? 2 : 4; }
-
-// Lazy fp32 scratch: [S x main GEMM outputs] + db partials.
-static size_t lazy_main_floats(const cavs_desc& d, int S) {
-  const size_t h = d.h, dd = d.d;
-  if (is_lstm(d)) return (size_t)S * (3 * h * h + h * h + gates(d) * h * dd);
-  return (size_t)S * (2 * h * h + h * dd);
-}
 
 // Carve the workspace; with base == nullptr only computes the size.
 static size_t carve(cavs_ctx* c, char* base) {
@@ -101,7 +93,7 @@ static size_t carve(cavs_ctx* c, char* base) {
     D.Wa = take(2 * h * h * es); D.Wb = take(h * dd * es); D.Wc = take(2 * h * h * es);
     D.Wd = nullptr; D.We = take(dd * h * es);
   }
-  D.lazy = F(lazy_main_floats(d, kSplitMax));
+  D.lazy = F(lazy_floats(D));
   c->lazy_db = F((size_t)kDbChunks * G * h);
   const size_t P = cavs_param_count(d.cell, d.N, d.h, d.d);
   c->s_params = F(P); c->s_dp = F(P);
@@ -242,40 +234,6 @@ CAVS_API cavs_status cavs_get_schedule(cavs_ctx* ctx, int32_t* level, int32_t* l
 }
 
 // --------------------------------------------------------------------------- forward
-template <class OpT>
-static void forward_simt(cavs_ctx* ctx) {
-  Dev& D = ctx->D;
-  const int h = D.h, d = D.d, N = D.N;
-  cudaStream_t s = ctx->stream;
-  SegListI L{};
-  if (D.cell == CAVS_CELL_TREE_LSTM) {
-    L.n = 4;
-    for (int g = 0; g < 4; ++g) L.s[g] = SegI{D.Wb, d, g * h, B_XP, 0, d, d, g};
-    simt_typeI<OpT>(D, EPI_LSTM_XPROJ, L, 0, D.V, h, s);
-    ctx->launches++;
-    SegListI F{};
-    F.n = 3 + N;
-    for (int g = 0; g < 3; ++g) F.s[g] = SegI{D.Wa, h, g * h, N >= 2 ? B_HSUM : B_HK, 0, N * h, h, g};
-    for (int k = 0; k < N; ++k) F.s[3 + k] = SegI{D.Wa, h, 3 * h, B_HK, k * h, N * h, h, 3 + k};
-    for (int t = 1; t < ctx->T; ++t) {
-      simt_typeI<OpT>(D, EPI_LSTM_FWD, F, ctx->lp[t], ctx->lp[t + 1], h, s);
-      ctx->launches++;
-    }
-  } else {
-    L.n = 1;
-    L.s[0] = SegI{D.Wb, d, 0, B_XP, 0, d, d, 0};
-    simt_typeI<OpT>(D, EPI_FC_XPROJ, L, 0, D.V, h, s);
-    ctx->launches++;
-    SegListI F{};
-    F.n = 1;
-    F.s[0] = SegI{D.Wa, 2 * h, 0, B_HK, 0, 2 * h, 2 * h, 0};
-    for (int t = 1; t < ctx->T; ++t) {
-      simt_typeI<OpT>(D, EPI_FC_FWD, F, ctx->lp[t], ctx->lp[t + 1], h, s);
-      ctx->launches++;
-    }
-  }
-}
-
 CAVS_API cavs_status cavs_forward(cavs_ctx* ctx, const float* params, int32_t n_x, const float* x,
                          const int32_t* x_row, float* h_out) {
   if (!ctx) return CAVS_E_INVALID;
@@ -291,7 +249,7 @@ CAVS_API cavs_status cavs_forward(cavs_ctx* ctx, const float* params, int32_t n_
   if (D.prec == CAVS_BF16) {
     ctx->launches += tc_forward(D, ctx->tc, ctx->lp, ctx->stream);
   } else {
-    forward_simt<float>(ctx);
+    ctx->launches += simt_forward<float>(D, ctx->lp, ctx->stream);
   }
   CK(cudaGetLastError());
   ctx->state = S_FORWARDED;
@@ -299,69 +257,6 @@ CAVS_API cavs_status cavs_forward(cavs_ctx* ctx, const float* params, int32_t n_
 }
 
 // --------------------------------------------------------------------------- backward
-template <class OpT>
-static void backward_simt(cavs_ctx* ctx) {
-  Dev& D = ctx->D;
-  const int h = D.h, d = D.d, N = D.N, G = gates(ctx->desc);
-  cudaStream_t s = ctx->stream;
-  SegListI B{};
-  int epi;
-  if (D.cell == CAVS_CELL_TREE_LSTM) {
-    B.n = 1 + N;
-    B.s[0] = SegI{D.Wc, 3 * h, 0, B_DZ, 0, G * h, 3 * h, 0};
-    for (int k = 0; k < N; ++k) B.s[1 + k] = SegI{D.Wd, h, 0, B_DZ, (3 + k) * h, G * h, h, 1 + k};
-    epi = EPI_LSTM_BWD;
-  } else {
-    B.n = 2;
-    for (int k = 0; k < 2; ++k) B.s[k] = SegI{D.Wc, h, k * h, B_DZ, 0, h, h, k};
-    epi = EPI_FC_BWD;
-  }
-  for (int t = ctx->T - 1; t >= 1; --t) {
-    simt_typeI<OpT>(D, epi, B, ctx->lp[t], ctx->lp[t + 1], h, s);
-    ctx->launches++;
-  }
-  // lazy batching of the parameter gradients over ALL vertices
-  float* lz = D.lazy;
-  const int lp1 = D.lp1, V = D.V;
-  if (D.cell == CAVS_CELL_TREE_LSTM) {
-    float* u4 = lz; float* uf = u4 + (size_t)3 * h * h; float* w = uf + (size_t)h * h;
-    SegListII A{};
-    A.n = 1;
-    A.s[0] = SegII{D.dZ, G * h, 0, N >= 2 ? D.Hs : D.Hk, N >= 2 ? h : N * h, 0, lp1, V, 0};
-    simt_typeII<OpT>(D, A, u4, 3 * h, h, h, s);
-    SegListII Bf{};
-    Bf.n = N;
-    for (int k = 0; k < N; ++k) Bf.s[k] = SegII{D.dZ, G * h, (3 + k) * h, D.Hk, N * h, k * h, lp1, V, 0};
-    simt_typeII<OpT>(D, Bf, uf, h, h, h, s);
-    SegListII Cw{};
-    Cw.n = 1;
-    Cw.s[0] = SegII{D.dZ, G * h, 0, D.Xp, d, 0, 0, V, 1};
-    simt_typeII<OpT>(D, Cw, w, G * h, d, d, s);
-    ctx->launches += 3;
-    SegListII dummy{};
-    (void)dummy;
-    SegListI X{};
-    X.n = 1;
-    X.s[0] = SegI{D.We, G * h, 0, B_DZ, 0, G * h, G * h, 0};
-    if (D.dx) { simt_typeI<OpT>(D, EPI_DX, X, 0, V, d, s); ctx->launches++; }
-  } else {
-    float* wc = lz; float* wx = wc + (size_t)2 * h * h;
-    SegListII A{};
-    A.n = 1;
-    A.s[0] = SegII{D.dZ, h, 0, D.Hk, 2 * h, 0, lp1, V, 0};
-    simt_typeII<OpT>(D, A, wc, h, 2 * h, 2 * h, s);
-    SegListII Cw{};
-    Cw.n = 1;
-    Cw.s[0] = SegII{D.dZ, h, 0, D.Xp, d, 0, 0, V, 1};
-    simt_typeII<OpT>(D, Cw, wx, h, d, d, s);
-    ctx->launches += 2;
-    SegListI X{};
-    X.n = 1;
-    X.s[0] = SegI{D.We, h, 0, B_DZ, 0, h, h, 0};
-    if (D.dx) { simt_typeI<OpT>(D, EPI_DX, X, 0, V, d, s); ctx->launches++; }
-  }
-}
-
 CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dparams, float* dx) {
   if (!ctx) return CAVS_E_INVALID;
   if (ctx->state < S_FORWARDED) return fail(ctx, CAVS_E_STATE, "cavs_forward first");
@@ -371,14 +266,14 @@ CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dp
   D.dh_out = dh_out; D.dparams = dparams; D.dx = dx;
   launch_roots(D, ctx->n_roots, D.roots, ctx->stream);
   ctx->launches++;
-  int split = 1;
+  int split[3] = {1, 1, 1};
   if (D.prec == CAVS_BF16) {
-    ctx->launches += tc_backward(D, ctx->tc, ctx->lp, ctx->stream, &split);
+    ctx->launches += tc_backward(D, ctx->tc, ctx->lp, ctx->stream, split);
   } else {
-    backward_simt<float>(ctx);
+    ctx->launches += simt_backward<float>(D, ctx->lp, ctx->stream);
   }
   launch_colsum(D, ctx->lazy_db, ctx->stream);
-  launch_pack(D, D.lazy, split, ctx->lazy_db, ctx->stream);
+  launch_pack(D, split, ctx->lazy_db, ctx->stream);
   ctx->launches += 2;
   CK(cudaGetLastError());
   return CAVS_OK;

@@ -1,5 +1,7 @@
 // kernels.h — internal launcher declarations (host side of the engine).
 #pragma once
+#include <vector>
+
 #include "common.cuh"
 
 namespace cavs {
@@ -28,7 +30,21 @@ struct SegII {
 };
 struct SegListII { int n; SegII s[4]; };
 
+// Lazy fp32 scratch: kSplitMax partial slots per GEMM output (float offsets into D.lazy).
+struct LazyLayout { size_t u4, uf, w, su4, suf, sw; };
+inline LazyLayout lazy_layout(const Dev& D) {
+  const size_t h = D.h, d = D.d;
+  LazyLayout L{};
+  if (D.cell == CAVS_CELL_TREE_LSTM) { L.su4 = 3 * h * h; L.suf = h * h; L.sw = (3 + D.N) * h * d; }
+  else { L.su4 = 2 * h * h; L.suf = 0; L.sw = h * d; }
+  L.u4 = 0; L.uf = kSplitMax * L.su4; L.w = L.uf + kSplitMax * L.suf;
+  return L;
+}
+inline size_t lazy_floats(const Dev& D) { const LazyLayout L = lazy_layout(D); return L.w + kSplitMax * L.sw; }
+
 void launch_schedule(const Dev& D, cudaStream_t s);
+template <class OpT> int simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s);
+template <class OpT> int simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s);
 
 template <class OpT>
 void simt_typeI(const Dev& D, int epi, const SegListI& L, int row_lo, int row_hi, int units, cudaStream_t s);
@@ -40,6 +56,6 @@ void launch_prep(const Dev& D, cudaStream_t s);
 void launch_pull(const Dev& D, cudaStream_t s);
 void launch_roots(const Dev& D, int n_roots, const int* roots, cudaStream_t s);
 void launch_colsum(const Dev& D, float* part, cudaStream_t s);
-void launch_pack(const Dev& D, const float* lazy_main, int split, const float* db_part, cudaStream_t s);
+void launch_pack(const Dev& D, const int* split /*[3]*/, const float* db_part, cudaStream_t s);
 
 }  // namespace cavs

@@ -124,15 +124,16 @@ __global__ void k_colsum(Dev D, float* part, int cols) {
   part[(size_t)blockIdx.y * cols + col] = s;
 }
 
-__global__ void k_pack(Dev D, const float* lz, int S, const float* dbp) {
+__global__ void k_pack(Dev D, LazyLayout Z, int Su4, int Suf, int Sw, const float* dbp) {
   const int h = D.h, d = D.d, N = D.N;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   float* out = D.dparams;
+  const float* u4 = D.lazy + Z.u4;
+  const float* uf = D.lazy + Z.uf;
+  const float* w = D.lazy + Z.w;
   if (D.cell == CAVS_CELL_TREE_LSTM) {
     const int G = 3 + N;
-    const size_t su4 = (size_t)3 * h * h, suf = (size_t)h * h, sw = (size_t)G * h * d;
-    const float* u4 = lz; const float* uf = u4 + S * su4; const float* w = uf + S * suf;
     const size_t nW = (size_t)4 * h * d, nU = (size_t)3 * h * h, nUf = (size_t)h * h;
     const int intern[4] = {0, 3, 1, 2};         // packed (i,f,o,u) -> internal row block (f: 3..3+N-1)
     for (size_t i = i0; i < nW + nU + nUf + 4 * h; i += stride) {
@@ -140,14 +141,14 @@ __global__ void k_pack(Dev D, const float* lz, int S, const float* dbp) {
       if (i < nW) {
         const int pg = (int)(i / ((size_t)h * d)); const size_t rest = i % ((size_t)h * d);
         const int nb = pg == 1 ? N : 1;
-        for (int s = 0; s < S; ++s)
-          for (int q = 0; q < nb; ++q) v += w[s * sw + (size_t)(intern[pg] + q) * h * d + rest];
+        for (int s = 0; s < Sw; ++s)
+          for (int q = 0; q < nb; ++q) v += w[s * Z.sw + (size_t)(intern[pg] + q) * h * d + rest];
       } else if (i < nW + nU) {
         const size_t r = i - nW;
-        for (int s = 0; s < S; ++s) v += u4[s * su4 + r];
+        for (int s = 0; s < Su4; ++s) v += u4[s * Z.su4 + r];
       } else if (i < nW + nU + nUf) {
         const size_t r = i - nW - nU;
-        for (int s = 0; s < S; ++s) v += uf[s * suf + r];
+        for (int s = 0; s < Suf; ++s) v += uf[s * Z.suf + r];
       } else {
         const size_t r = i - nW - nU - nUf;
         const int pg = (int)(r / h), m = (int)(r % h);
@@ -158,12 +159,11 @@ __global__ void k_pack(Dev D, const float* lz, int S, const float* dbp) {
       out[i] = v;
     }
   } else {
-    const size_t swc = (size_t)2 * h * h, swx = (size_t)h * d;
-    const float* wc = lz; const float* wx = wc + S * swc;
+    const size_t swc = Z.su4, swx = Z.sw;
     for (size_t i = i0; i < swc + swx + h; i += stride) {
       float v = 0.f;
-      if (i < swc) { for (int s = 0; s < S; ++s) v += wc[s * swc + i]; }
-      else if (i < swc + swx) { for (int s = 0; s < S; ++s) v += wx[s * swx + (i - swc)]; }
+      if (i < swc) { for (int s = 0; s < Su4; ++s) v += u4[s * swc + i]; }
+      else if (i < swc + swx) { for (int s = 0; s < Sw; ++s) v += w[s * swx + (i - swc)]; }
       else { for (int c = 0; c < kDbChunks; ++c) v += dbp[(size_t)c * h + (i - swc - swx)]; }
       out[i] = v;
     }
@@ -196,9 +196,9 @@ void launch_colsum(const Dev& D, float* part, cudaStream_t s) {
   else k_colsum<float><<<grid, 128, 0, s>>>(D, part, cols);
 }
 
-void launch_pack(const Dev& D, const float* lazy_main, int split, const float* db_part, cudaStream_t s) {
+void launch_pack(const Dev& D, const int* split, const float* db_part, cudaStream_t s) {
   const size_t n = (size_t)4 * D.h * D.d + (size_t)4 * D.h * D.h + 4 * D.h;
-  k_pack<<<grid_for(n, 256), 256, 0, s>>>(D, lazy_main, split, db_part);
+  k_pack<<<grid_for(n, 256), 256, 0, s>>>(D, lazy_layout(D), split[0], split[1], split[2], db_part);
 }
 
 }  // namespace cavs

@@ -12,7 +12,7 @@ struct TcState;
 cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* err);
 // Returns the number of kernels launched.
 int tc_forward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s);
-int tc_backward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, int* split);
+int tc_backward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, int* split /*[3]*/);
 void tc_destroy(TcState* tc);
 
 }  // namespace cavs

@@ -89,7 +89,7 @@ def test_schedule_mixed_batch_tasks():
 def test_schedule_errors(graphs, N, code):
     from paper_1712_04048_b200 import CavsError
     b = gen.batch_from_graphs(graphs, cell="tree_lstm", N=N, h=64, d=64, seed=0)
-    ctx = make_ctx(b, "fp32")
+    ctx = make_ctx(b, "fp32", max_vertices=16, max_graphs=4, max_x=16)
     ctx.load_graphs(b.graph_ptr, b.child_ptr, b.child_idx)
     with pytest.raises(CavsError) as e:
         ctx.schedule()
@@ -229,3 +229,15 @@ def test_full_size_sampled(cfg, precision, sample):
         e = rel(g["dparams"][sl], r["dparams"][sl])
         assert e <= tol, (name, e)
     assert rel(g["dx"][xr[xr >= 0]], r["dx"]) <= tol
+
+
+@pytest.mark.parametrize("case", ["tree_lstm_sst_h128_d64", "lstm_chain_h64", "tree_fc_cbt_h64"])
+def test_tcgen05_matches_simt_bf16(case, monkeypatch):
+    """Same bf16 rounding points on both paths; only the accumulation order differs."""
+    b = BF16_CASES[case]()
+    monkeypatch.setenv("CAVS_BF16_SIMT", "1")
+    s = run_gpu(b, "bf16")
+    monkeypatch.setenv("CAVS_BF16_SIMT", "0")
+    t = run_gpu(b, "bf16")
+    from gpu_harness import compare
+    compare(b, t, s, BF16_EMU_TOL, case + " tcgen05 vs simt-bf16")
