@@ -164,6 +164,28 @@ cavs_status cavs_train_step_host(cavs_ctx* ctx, int32_t K, int32_t V, int32_t E,
 /* Number of kernels the library launched since the context was created (diagnostic). */
 int64_t cavs_kernel_launches(const cavs_ctx* ctx);
 
+/* Per-phase device timing: with profiling on, the library records one CUDA event on its
+ * stream at every phase boundary of schedule/forward/backward (no extra synchronisation)
+ * and accumulates, per phase, the elapsed time, the kernel launches and the ALGORITHMIC
+ * FLOPs / bytes of that phase.
+ * cavs_profile(ctx, 1) resets the accumulators and starts recording; (ctx, 0) stops.
+ * cavs_profile_read synchronises the stream and returns the totals of one phase. */
+typedef enum cavs_phase {
+  CAVS_PH_SCHEDULE = 0,   /* graph validation + level sweep + task lists (Alg. 1) */
+  CAVS_PH_PREP = 1,       /* parameter repack + pull gather */
+  CAVS_PH_XPROJ = 2,      /* eager pull projection fused with task 0 */
+  CAVS_PH_FWD_LEVELS = 3, /* forward tasks t = 1..T-1 (level GEMM + fused cell) */
+  CAVS_PH_BWD_ROOTS = 4,  /* dF at the roots */
+  CAVS_PH_BWD_LEVELS = 5, /* backward tasks t = T-1..1 (dH GEMM + fused dF of the children) */
+  CAVS_PH_LAZY = 6,       /* lazily batched weight-gradient GEMMs */
+  CAVS_PH_DX = 7,         /* pull's adjoint dx */
+  CAVS_PH_REDUCE = 8,     /* db column sums + dparams packing */
+  CAVS_PH_COUNT = 9
+} cavs_phase;
+cavs_status cavs_profile(cavs_ctx* ctx, int enable);
+cavs_status cavs_profile_read(cavs_ctx* ctx, int32_t phase, double* ms, double* flops, double* bytes,
+                              int64_t* launches);
+
 const char* cavs_last_error(const cavs_ctx* ctx);
 void cavs_destroy(cavs_ctx* ctx);
 

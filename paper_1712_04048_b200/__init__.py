@@ -5,6 +5,7 @@ forward and backward, behind the C-ABI in include/cavs.h.
 Importing this package loads libcavs.so and fails loudly if it is missing.
 """
 from .cavs import (  # noqa: F401
+    PHASES,
     BF16,
     CELLS,
     Context,

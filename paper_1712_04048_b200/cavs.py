@@ -55,6 +55,9 @@ def _load():
         "cavs_train_step_host": (S, [P, I32, I32, I32, P, P, P, P, I32, P, P, P, P, P, P]),
         "cavs_kernel_launches": (I64, [P]),
         "cavs_last_error": (ctypes.c_char_p, [P]),
+        "cavs_profile": (S, [P, ctypes.c_int]),
+        "cavs_profile_read": (S, [P, I32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)]),
         "cavs_destroy": (None, [P]),
     }
     for name, (res, args) in sig.items():
@@ -68,7 +71,8 @@ _lib = _load()
 EXPORTS = ["cavs_param_count", "cavs_create", "cavs_set_stream", "cavs_workspace_bytes",
            "cavs_set_workspace", "cavs_load_graphs", "cavs_schedule", "cavs_get_schedule",
            "cavs_forward", "cavs_backward", "cavs_train_step_host", "cavs_kernel_launches",
-           "cavs_last_error", "cavs_destroy"]
+           "cavs_last_error", "cavs_destroy", "cavs_profile", "cavs_profile_read"]
+PHASES = ["schedule", "prep", "xproj", "fwd_levels", "bwd_roots", "bwd_levels", "lazy", "dx", "reduce"]
 
 
 def lib():
@@ -129,6 +133,21 @@ class Context:
     @property
     def launches(self) -> int:
         return int(_lib.cavs_kernel_launches(self._ctx))
+
+    def profile(self, enable: bool = True):
+        """Reset the per-phase accumulators and (de)activate phase timing."""
+        self._check(_lib.cavs_profile(self._ctx, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        """{phase: dict(ms, flops, bytes, launches)} accumulated since profile(True)."""
+        out = {}
+        for i, name in enumerate(PHASES):
+            ms, fl, by = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+            ln = ctypes.c_int64()
+            self._check(_lib.cavs_profile_read(self._ctx, i, ctypes.byref(ms), ctypes.byref(fl),
+                                               ctypes.byref(by), ctypes.byref(ln)))
+            out[name] = dict(ms=ms.value, flops=fl.value, bytes=by.value, launches=int(ln.value))
+        return out
 
     def load_graphs(self, graph_ptr, child_ptr, child_idx):
         """CSR child lists per instance; numpy (host) or torch CUDA int32 arrays."""

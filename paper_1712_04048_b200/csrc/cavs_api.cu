@@ -27,7 +27,7 @@ struct cavs_ctx {
   int T = 0, n_roots = 0;
   int* h_hdr = nullptr;         // pinned readback buffer
   std::string err;
-  int64_t launches = 0;
+  Prof prof;                    // phase marks + launch counts
   // lazy scratch layout
   float* lazy_db = nullptr;
   // staging for cavs_train_step_host
@@ -191,8 +191,10 @@ CAVS_API cavs_status cavs_schedule(cavs_ctx* ctx, int32_t* T_out) {
   Dev& D = ctx->D;
   CK(cudaMemsetAsync(D.hdr, 0, sizeof(int) * kHdrWords, ctx->stream));
   CK(cudaMemsetAsync(D.cnt, 0, sizeof(int) * (D.V + 1), ctx->stream));
+  ctx->prof.mark(CAVS_PH_SCHEDULE, ctx->stream);
   launch_schedule(D, ctx->stream);
-  ctx->launches += 5;
+  ctx->prof.count(5);
+  ctx->prof.mark(-1, ctx->stream);
   CK(cudaGetLastError());
   const int nread = kHdrWords + std::min(D.V + 1, kReadback);
   CK(cudaMemcpyAsync(ctx->h_hdr, D.hdr, sizeof(int) * nread, cudaMemcpyDeviceToHost, ctx->stream));
@@ -233,6 +235,56 @@ CAVS_API cavs_status cavs_get_schedule(cavs_ctx* ctx, int32_t* level, int32_t* l
   return CAVS_OK;
 }
 
+// --------------------------------------------------------------------------- roofline accounting
+// ALGORITHMIC work per phase: FLOPs of the contractions the
+// method must do (2 per MAC; a vertex with c children needs U h~ (3h^2 MACs, Tree-LSTM) and
+// one U_f h_k per existing child; leaves no recurrent term), bytes = minimal HBM traffic of
+// the phase's operands/results in the precision they are stored in.
+static void account_forward(cavs_ctx* ctx) {
+  Prof& P = ctx->prof;
+  const Dev& D = ctx->D;
+  const double h = D.h, d = D.d, I = D.V - D.lp1, E = D.E, nx = D.n_x, O = esize(ctx->desc), S = 4;
+  const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
+  const double G = lstm ? 3 + D.N : 1;
+  if (lstm) {
+    P.flops[CAVS_PH_XPROJ] += 2.0 * 4 * h * d * nx;
+    P.flops[CAVS_PH_FWD_LEVELS] += 2.0 * h * h * (3 * I + E);
+    // read child h (O) and c (S) per edge; write c, gates, h_out, parent slot h (O) + c (S), h~ (O)
+    P.bytes[CAVS_PH_FWD_LEVELS] += E * h * (O + S) + I * h * (S + G * S + S + O + S + O) +
+                                   (ctx->T - 1) * 4 * h * h * O;
+    P.bytes[CAVS_PH_XPROJ] += nx * d * O + 4 * h * d * O + nx * h * (S + G * S + S + O + S);
+  } else {
+    P.flops[CAVS_PH_XPROJ] += 2.0 * h * d * nx;
+    P.flops[CAVS_PH_FWD_LEVELS] += 2.0 * h * h * E;
+    P.bytes[CAVS_PH_FWD_LEVELS] += E * h * O + I * h * (S + S + O) + (ctx->T - 1) * 2 * h * h * O;
+    P.bytes[CAVS_PH_XPROJ] += nx * d * O + h * d * O + nx * h * (S + S + O);
+  }
+}
+
+static void account_backward(cavs_ctx* ctx) {
+  Prof& P = ctx->prof;
+  const Dev& D = ctx->D;
+  const double h = D.h, d = D.d, I = D.V - D.lp1, E = D.E, nx = D.n_x, O = esize(ctx->desc), S = 4;
+  const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
+  const double G = lstm ? 3 + D.N : 1;
+  if (lstm) {
+    P.flops[CAVS_PH_BWD_LEVELS] += 2.0 * h * h * (3 * I + E);
+    P.flops[CAVS_PH_LAZY] += 2.0 * h * h * (3 * I + E) + 2.0 * 4 * h * d * nx;
+    P.flops[CAVS_PH_DX] += 2.0 * 4 * h * d * nx;
+    // read parent dZ (O), dc-bar, gates; per child: dh_out, gates, c, child c slots; write child dZ, dc-bar
+    P.bytes[CAVS_PH_BWD_LEVELS] += I * h * (G * O + S + G * S) + E * h * (S + G * S + S + D.N * S + G * O + S) +
+                                   (ctx->T - 1) * 4 * h * h * O;
+    P.bytes[CAVS_PH_LAZY] += I * h * (3 * O + O) + E * h * 2 * O + nx * (G * h + d) * O +
+                             (3 * h * h + h * h + G * h * d) * S;
+  } else {
+    P.flops[CAVS_PH_BWD_LEVELS] += 2.0 * h * h * E;
+    P.flops[CAVS_PH_LAZY] += 2.0 * h * h * E + 2.0 * h * d * nx;
+    P.flops[CAVS_PH_DX] += 2.0 * h * d * nx;
+    P.bytes[CAVS_PH_BWD_LEVELS] += I * h * O + E * h * (S + S + O) + (ctx->T - 1) * 2 * h * h * O;
+    P.bytes[CAVS_PH_LAZY] += I * h * (O + 2 * O) + nx * (h + d) * O + (2 * h * h + h * d) * S;
+  }
+}
+
 // --------------------------------------------------------------------------- forward
 CAVS_API cavs_status cavs_forward(cavs_ctx* ctx, const float* params, int32_t n_x, const float* x,
                          const int32_t* x_row, float* h_out) {
@@ -243,14 +295,16 @@ CAVS_API cavs_status cavs_forward(cavs_ctx* ctx, const float* params, int32_t n_
   CK(cudaSetDevice(ctx->device));
   Dev& D = ctx->D;
   D.params = params; D.x = x; D.x_row = x_row; D.h_out = h_out; D.n_x = n_x;
+  Prof& P = ctx->prof;
+  P.mark(CAVS_PH_PREP, ctx->stream);
   launch_prep(D, ctx->stream);
   launch_pull(D, ctx->stream);
-  ctx->launches += 2;
-  if (D.prec == CAVS_BF16) {
-    ctx->launches += tc_forward(D, ctx->tc, ctx->lp, ctx->stream);
-  } else {
-    ctx->launches += simt_forward<float>(D, ctx->lp, ctx->stream);
-  }
+  P.count(2);
+  P.mark(CAVS_PH_XPROJ, ctx->stream);
+  if (D.prec == CAVS_BF16) tc_forward(D, ctx->tc, ctx->lp, ctx->stream, P);
+  else simt_forward<float>(D, ctx->lp, ctx->stream, P);
+  P.mark(-1, ctx->stream);
+  account_forward(ctx);
   CK(cudaGetLastError());
   ctx->state = S_FORWARDED;
   return CAVS_OK;
@@ -264,17 +318,23 @@ CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dp
   CK(cudaSetDevice(ctx->device));
   Dev& D = ctx->D;
   D.dh_out = dh_out; D.dparams = dparams; D.dx = dx;
+  Prof& P = ctx->prof;
+  P.mark(CAVS_PH_BWD_ROOTS, ctx->stream);
   launch_roots(D, ctx->n_roots, D.roots, ctx->stream);
-  ctx->launches++;
+  P.count(1);
+  P.mark(CAVS_PH_BWD_LEVELS, ctx->stream);
   int split[3] = {1, 1, 1};
   if (D.prec == CAVS_BF16) {
-    ctx->launches += tc_backward(D, ctx->tc, ctx->lp, ctx->stream, split);
+    tc_backward(D, ctx->tc, ctx->lp, ctx->stream, split, P);
   } else {
-    ctx->launches += simt_backward<float>(D, ctx->lp, ctx->stream);
+    simt_backward<float>(D, ctx->lp, ctx->stream, P);
   }
+  P.mark(CAVS_PH_REDUCE, ctx->stream);
   launch_colsum(D, ctx->lazy_db, ctx->stream);
   launch_pack(D, split, ctx->lazy_db, ctx->stream);
-  ctx->launches += 2;
+  P.count(2);
+  P.mark(-1, ctx->stream);
+  account_backward(ctx);
   CK(cudaGetLastError());
   return CAVS_OK;
 }
@@ -310,7 +370,45 @@ CAVS_API cavs_status cavs_train_step_host(cavs_ctx* ctx, int32_t K, int32_t V, i
   return CAVS_OK;
 }
 
-CAVS_API int64_t cavs_kernel_launches(const cavs_ctx* ctx) { return ctx ? ctx->launches : 0; }
+CAVS_API int64_t cavs_kernel_launches(const cavs_ctx* ctx) { return ctx ? ctx->prof.total : 0; }
+
+static void drain_marks(cavs_ctx* ctx) {
+  Prof& P = ctx->prof;
+  if (P.marks.empty()) return;
+  cudaStreamSynchronize(ctx->stream);
+  for (size_t i = 0; i + 1 < P.marks.size(); ++i) {
+    const int ph = P.marks[i].first;
+    if (ph < 0) continue;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, P.marks[i].second, P.marks[i + 1].second);
+    P.ms[ph] += ms;
+  }
+  for (auto& m : P.marks) cudaEventDestroy(m.second);
+  P.marks.clear();
+}
+
+CAVS_API cavs_status cavs_profile(cavs_ctx* ctx, int enable) {
+  if (!ctx) return CAVS_E_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  drain_marks(ctx);
+  Prof& P = ctx->prof;
+  for (int i = 0; i < CAVS_PH_COUNT; ++i) { P.ms[i] = 0; P.flops[i] = 0; P.bytes[i] = 0; P.launches[i] = 0; }
+  P.on = enable != 0;
+  return CAVS_OK;
+}
+
+CAVS_API cavs_status cavs_profile_read(cavs_ctx* ctx, int32_t phase, double* ms, double* flops, double* bytes,
+                                       int64_t* launches) {
+  if (!ctx || phase < 0 || phase >= CAVS_PH_COUNT) return CAVS_E_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  drain_marks(ctx);
+  const Prof& P = ctx->prof;
+  if (ms) *ms = P.ms[phase];
+  if (flops) *flops = P.flops[phase];
+  if (bytes) *bytes = P.bytes[phase];
+  if (launches) *launches = P.launches[phase];
+  return CAVS_OK;
+}
 
 CAVS_API const char* cavs_last_error(const cavs_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 

@@ -42,9 +42,28 @@ inline LazyLayout lazy_layout(const Dev& D) {
 }
 inline size_t lazy_floats(const Dev& D) { const LazyLayout L = lazy_layout(D); return L.w + kSplitMax * L.sw; }
 
+// Phase marks (one CUDA event per phase boundary when profiling) + launch counting.
+struct Prof {
+  bool on = false;
+  int cur = -1;
+  std::vector<std::pair<int, cudaEvent_t>> marks;
+  double ms[CAVS_PH_COUNT] = {}, flops[CAVS_PH_COUNT] = {}, bytes[CAVS_PH_COUNT] = {};
+  int64_t launches[CAVS_PH_COUNT] = {};
+  int64_t total = 0;
+  void mark(int phase, cudaStream_t s) {
+    cur = phase;
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    marks.push_back({phase, e});
+  }
+  void count(int n) { if (cur >= 0) launches[cur] += n; total += n; }
+};
+
 void launch_schedule(const Dev& D, cudaStream_t s);
-template <class OpT> int simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s);
-template <class OpT> int simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s);
+template <class OpT> void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P);
+template <class OpT> void simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P);
 
 template <class OpT>
 void simt_typeI(const Dev& D, int epi, const SegListI& L, int row_lo, int row_hi, int units, cudaStream_t s);

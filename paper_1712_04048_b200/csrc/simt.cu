@@ -165,35 +165,34 @@ void simt_typeII(const Dev& D, const SegListII& L, float* out, int M, int Ncols,
 
 // ---- whole passes (FP32 mode; BF16 operands when CAVS_BF16_SIMT=1 for A/B checks) ----
 template <class OpT>
-int simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s) {
+void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
   const int h = D.h, d = D.d, N = D.N, T = (int)lp.size() - 1;
-  int n = 0;
   SegListI L{}, F{};
   if (D.cell == CAVS_CELL_TREE_LSTM) {
     L.n = 4;
     for (int g = 0; g < 4; ++g) L.s[g] = SegI{D.Wb, d, g * h, B_XP, 0, d, d, g};
-    simt_typeI<OpT>(D, EPI_LSTM_XPROJ, L, 0, D.V, h, s); ++n;
+    simt_typeI<OpT>(D, EPI_LSTM_XPROJ, L, 0, D.V, h, s); P.count(1);
+    P.mark(CAVS_PH_FWD_LEVELS, s);
     F.n = 3 + N;
     for (int g = 0; g < 3; ++g) F.s[g] = SegI{D.Wa, h, g * h, N >= 2 ? B_HSUM : B_HK, 0, N * h, h, g};
     for (int k = 0; k < N; ++k) F.s[3 + k] = SegI{D.Wa, h, 3 * h, B_HK, k * h, N * h, h, 3 + k};
-    for (int t = 1; t < T; ++t) { simt_typeI<OpT>(D, EPI_LSTM_FWD, F, lp[t], lp[t + 1], h, s); ++n; }
+    for (int t = 1; t < T; ++t) { simt_typeI<OpT>(D, EPI_LSTM_FWD, F, lp[t], lp[t + 1], h, s); P.count(1); }
   } else {
     L.n = 1;
     L.s[0] = SegI{D.Wb, d, 0, B_XP, 0, d, d, 0};
-    simt_typeI<OpT>(D, EPI_FC_XPROJ, L, 0, D.V, h, s); ++n;
+    simt_typeI<OpT>(D, EPI_FC_XPROJ, L, 0, D.V, h, s); P.count(1);
+    P.mark(CAVS_PH_FWD_LEVELS, s);
     F.n = 1;
     F.s[0] = SegI{D.Wa, 2 * h, 0, B_HK, 0, 2 * h, 2 * h, 0};
-    for (int t = 1; t < T; ++t) { simt_typeI<OpT>(D, EPI_FC_FWD, F, lp[t], lp[t + 1], h, s); ++n; }
+    for (int t = 1; t < T; ++t) { simt_typeI<OpT>(D, EPI_FC_FWD, F, lp[t], lp[t + 1], h, s); P.count(1); }
   }
-  return n;
 }
 
 template <class OpT>
-int simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s) {
+void simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
   const int h = D.h, d = D.d, N = D.N, T = (int)lp.size() - 1;
   const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
   const int G = lstm ? 3 + N : 1;
-  int n = 0;
   SegListI B{};
   int epi;
   if (lstm) {
@@ -206,7 +205,8 @@ int simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s) {
     for (int k = 0; k < 2; ++k) B.s[k] = SegI{D.Wc, h, k * h, B_DZ, 0, h, h, k};
     epi = EPI_FC_BWD;
   }
-  for (int t = T - 1; t >= 1; --t) { simt_typeI<OpT>(D, epi, B, lp[t], lp[t + 1], h, s); ++n; }
+  for (int t = T - 1; t >= 1; --t) { simt_typeI<OpT>(D, epi, B, lp[t], lp[t + 1], h, s); P.count(1); }
+  P.mark(CAVS_PH_LAZY, s);
   // lazy batching of the parameter gradients over ALL vertices; one partial each
   const LazyLayout Z = lazy_layout(D);
   const int lp1 = D.lp1, V = D.V;
@@ -220,7 +220,7 @@ int simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s) {
     SegListII Cw{}; Cw.n = 1;
     Cw.s[0] = SegII{D.dZ, G * h, 0, D.Xp, d, 0, 0, V, 1};
     simt_typeII<OpT>(D, Cw, D.lazy + Z.w, G * h, d, d, s);
-    n += 3;
+    P.count(3);
   } else {
     SegListII A{}; A.n = 1;
     A.s[0] = SegII{D.dZ, h, 0, D.Hk, 2 * h, 0, lp1, V, 0};
@@ -228,20 +228,20 @@ int simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s) {
     SegListII Cw{}; Cw.n = 1;
     Cw.s[0] = SegII{D.dZ, h, 0, D.Xp, d, 0, 0, V, 1};
     simt_typeII<OpT>(D, Cw, D.lazy + Z.w, h, d, d, s);
-    n += 2;
+    P.count(2);
   }
+  P.mark(CAVS_PH_DX, s);
   if (D.dx) {
     SegListI X{}; X.n = 1;
     X.s[0] = SegI{D.We, G * h, 0, B_DZ, 0, G * h, G * h, 0};
-    simt_typeI<OpT>(D, EPI_DX, X, 0, V, d, s); ++n;
+    simt_typeI<OpT>(D, EPI_DX, X, 0, V, d, s); P.count(1);
   }
-  return n;
 }
 
-template int simt_forward<float>(Dev&, const std::vector<int>&, cudaStream_t);
-template int simt_forward<__nv_bfloat16>(Dev&, const std::vector<int>&, cudaStream_t);
-template int simt_backward<float>(Dev&, const std::vector<int>&, cudaStream_t);
-template int simt_backward<__nv_bfloat16>(Dev&, const std::vector<int>&, cudaStream_t);
+template void simt_forward<float>(Dev&, const std::vector<int>&, cudaStream_t, Prof&);
+template void simt_forward<__nv_bfloat16>(Dev&, const std::vector<int>&, cudaStream_t, Prof&);
+template void simt_backward<float>(Dev&, const std::vector<int>&, cudaStream_t, Prof&);
+template void simt_backward<__nv_bfloat16>(Dev&, const std::vector<int>&, cudaStream_t, Prof&);
 
 template void simt_typeI<float>(const Dev&, int, const SegListI&, int, int, int, cudaStream_t);
 template void simt_typeI<__nv_bfloat16>(const Dev&, int, const SegListI&, int, int, int, cudaStream_t);

@@ -435,10 +435,9 @@ static Bundle one(int map_a, int a_row, int a_col0, int b_col, int nk, int acc) 
 }
 
 
-int tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s) {
-  if (t->use_simt) return simt_forward<__nv_bfloat16>(D, lp, s);
+void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
+  if (t->use_simt) { simt_forward<__nv_bfloat16>(D, lp, s, P); return; }
   const int h = D.h, d = D.d, N = D.N, T = (int)lp.size() - 1;
-  int n = 0;
   if (D.cell == CAVS_CELL_TREE_LSTM) {
     // eager pull projection + level 0: A = W4 (gates i,o,u,f), B = Xp
     PlanI X{};
@@ -447,7 +446,8 @@ int tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s) {
     b.map_a = 0; b.nA = 4; for (int g = 0; g < 4; ++g) b.a_row[g] = g * h; b.a_col0 = 0;
     b.nB = 1; b.b_col[0] = 0; b.sum = 0; b.nk = d / BK;
     b.nmma = 4; for (int g = 0; g < 4; ++g) { b.mma_a[g] = g; b.mma_b[g] = 0; b.mma_acc[g] = g; }
-    launch_I<EPI_LSTM_XPROJ, 4>(t, t->A[1], t->A[1], t->B_xp, D, X, 0, D.V, h, s); ++n;
+    launch_I<EPI_LSTM_XPROJ, 4>(t, t->A[1], t->A[1], t->B_xp, D, X, 0, D.V, h, s); P.count(1);
+    P.mark(CAVS_PH_FWD_LEVELS, s);
     // levels t >= 1: A = U4, B = child slots of the task's rows; h~ formed in smem
     PlanI F{};
     F.nb = 1;
@@ -463,22 +463,22 @@ int tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s) {
       else if (N == 2) launch_I<EPI_LSTM_FWD, 5>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       else if (N == 3) launch_I<EPI_LSTM_FWD, 6>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       else launch_I<EPI_LSTM_FWD, 7>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
-      ++n;
+      P.count(1);
     }
   } else {
     PlanI X{};
     X.nb = 1;
     X.b[0] = one(0, 0, 0, 0, d / BK, 0);
-    launch_I<EPI_FC_XPROJ, 1>(t, t->A[1], t->A[1], t->B_xp, D, X, 0, D.V, h, s); ++n;
+    launch_I<EPI_FC_XPROJ, 1>(t, t->A[1], t->A[1], t->B_xp, D, X, 0, D.V, h, s); P.count(1);
+    P.mark(CAVS_PH_FWD_LEVELS, s);
     PlanI F{};
     F.nb = 1;
     F.b[0] = one(0, 0, 0, 0, 2 * h / BK, 0);
     for (int tt = 1; tt < T; ++tt) {
       launch_I<EPI_FC_FWD, 1>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
-      ++n;
+      P.count(1);
     }
   }
-  return n;
 }
 
 static int launch_II(const CUtensorMap& a, const CUtensorMap& b, const Dev& D, PlanII P, float* out,
@@ -499,13 +499,12 @@ static int launch_II(const CUtensorMap& a, const CUtensorMap& b, const Dev& D, P
   return P.split;
 }
 
-int tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, int* split) {
+void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, int* split, Prof& P) {
   split[0] = split[1] = split[2] = 1;
-  if (t->use_simt) return simt_backward<__nv_bfloat16>(D, lp, s);
+  if (t->use_simt) { simt_backward<__nv_bfloat16>(D, lp, s, P); return; }
   const int h = D.h, d = D.d, N = D.N, T = (int)lp.size() - 1;
   const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
   const int G = lstm ? 3 + N : 1;
-  int n = 0;
   // rows past V of dZ are read by the lazy GEMMs' last k-block: keep them zero
   cudaMemsetAsync(reinterpret_cast<__nv_bfloat16*>(D.dZ) + (size_t)D.V * G * h, 0, (size_t)64 * G * h * 2, s);
   if (lstm) {
@@ -518,7 +517,7 @@ int tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
       else if (N == 2) launch_I<EPI_LSTM_BWD, 3>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       else if (N == 3) launch_I<EPI_LSTM_BWD, 4>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       else launch_I<EPI_LSTM_BWD, 5>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
-      ++n;
+      P.count(1);
     }
   } else {
     PlanI B{};
@@ -526,9 +525,10 @@ int tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
     for (int k = 0; k < 2; ++k) B.b[k] = one(0, k * h, 0, 0, h / BK, k);   // WcT rows k*h x dZ
     for (int tt = T - 1; tt >= 1; --tt) {
       launch_I<EPI_FC_BWD, 2>(t, t->A[2], t->A[2], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
-      ++n;
+      P.count(1);
     }
   }
+  P.mark(CAVS_PH_LAZY, s);
   // ---- lazy batching of the parameter gradients ----
   const size_t su4 = lstm ? (size_t)3 * h * h : (size_t)2 * h * h;
   const size_t suf = lstm ? (size_t)h * h : 0;
@@ -542,24 +542,25 @@ int tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
     A.nseg = 1;
     A.s[0] = SegT2{0, 0, lp1, V, 0};
     A.M = 3 * h; A.Ncols = h; A.ldo = h; A.split_stride = su4;
-    if (lp1 < V) { split[0] = launch_II(t->M_dz, N >= 2 ? t->M_hs : t->M_hk, D, A, u4, s); ++n; }
+    if (lp1 < V) { split[0] = launch_II(t->M_dz, N >= 2 ? t->M_hs : t->M_hk, D, A, u4, s); P.count(1); }
     else cudaMemsetAsync(u4, 0, sizeof(float) * su4, s);
     PlanII Bf{};
     Bf.nseg = N;
     for (int k = 0; k < N; ++k) Bf.s[k] = SegT2{(3 + k) * h, k * h, lp1, V, 0};
     Bf.M = h; Bf.Ncols = h; Bf.ldo = h; Bf.split_stride = suf;
-    if (lp1 < V) { split[1] = launch_II(t->M_dz, t->M_hk, D, Bf, uf, s); ++n; }
+    if (lp1 < V) { split[1] = launch_II(t->M_dz, t->M_hk, D, Bf, uf, s); P.count(1); }
     else cudaMemsetAsync(uf, 0, sizeof(float) * suf, s);
     PlanII Cw{};
     Cw.nseg = 1;
     Cw.s[0] = SegT2{0, 0, 0, V, 1};
     Cw.M = G * h; Cw.Ncols = d; Cw.ldo = d; Cw.split_stride = sw;
-    split[2] = launch_II(t->M_dz, t->M_xp, D, Cw, w, s); ++n;
+    split[2] = launch_II(t->M_dz, t->M_xp, D, Cw, w, s); P.count(1);
+    P.mark(CAVS_PH_DX, s);
     if (D.dx) {
       PlanI X{};
       X.nb = 1;
       X.b[0] = one(0, 0, 0, 0, G * h / BK, 0);
-      launch_I<EPI_DX, 1>(t, t->A[4], t->A[4], t->B_dz, D, X, 0, V, d, s); ++n;
+      launch_I<EPI_DX, 1>(t, t->A[4], t->A[4], t->B_dz, D, X, 0, V, d, s); P.count(1);
     }
   } else {
     float* wc = u4;
@@ -568,21 +569,21 @@ int tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
     A.nseg = 1;
     A.s[0] = SegT2{0, 0, lp1, V, 0};
     A.M = h; A.Ncols = 2 * h; A.ldo = 2 * h; A.split_stride = su4;
-    if (lp1 < V) { split[0] = launch_II(t->M_dz, t->M_hk, D, A, wc, s); ++n; }
+    if (lp1 < V) { split[0] = launch_II(t->M_dz, t->M_hk, D, A, wc, s); P.count(1); }
     else cudaMemsetAsync(wc, 0, sizeof(float) * su4, s);
     PlanII Cw{};
     Cw.nseg = 1;
     Cw.s[0] = SegT2{0, 0, 0, V, 1};
     Cw.M = h; Cw.Ncols = d; Cw.ldo = d; Cw.split_stride = (size_t)h * d;
-    split[2] = launch_II(t->M_dz, t->M_xp, D, Cw, wx, s); ++n;
+    split[2] = launch_II(t->M_dz, t->M_xp, D, Cw, wx, s); P.count(1);
+    P.mark(CAVS_PH_DX, s);
     if (D.dx) {
       PlanI X{};
       X.nb = 1;
       X.b[0] = one(0, 0, 0, 0, h / BK, 0);
-      launch_I<EPI_DX, 1>(t, t->A[4], t->A[4], t->B_dz, D, X, 0, V, d, s); ++n;
+      launch_I<EPI_DX, 1>(t, t->A[4], t->A[4], t->B_dz, D, X, 0, V, d, s); P.count(1);
     }
   }
-  return n;
 }
 
 }  // namespace cavs

@@ -3,16 +3,16 @@
 #include <string>
 #include <vector>
 
-#include "common.cuh"
+#include "kernels.h"
 
 namespace cavs {
 
 struct TcState;
 
 cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* err);
-// Returns the number of kernels launched.
-int tc_forward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s);
-int tc_backward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, int* split /*[3]*/);
+// Launches are counted into P; phase marks XPROJ -> FWD_LEVELS and BWD_LEVELS -> LAZY -> DX.
+void tc_forward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, Prof& P);
+void tc_backward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, int* split /*[3]*/, Prof& P);
 void tc_destroy(TcState* tc);
 
 }  // namespace cavs
