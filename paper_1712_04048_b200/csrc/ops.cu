@@ -104,10 +104,7 @@ template <class OpT>
 __global__ void k_roots(Dev D, int n_roots, const int* roots) {
   const size_t n = (size_t)n_roots * D.h;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const int p = roots[i / D.h], j = (int)(i % D.h);
-    const float dh = D.dh_out[(size_t)D.order[p] * D.h + j];
-    if (D.cell == CAVS_CELL_TREE_LSTM) lstm_elem_bwd<OpT>(D, j, p, dh, 0.f);
-    else fc_elem_bwd<OpT>(D, j, p, dh);
+    root_bwd<OpT>(D, (int)(i % D.h), roots[i / D.h]);
   }
 }
 

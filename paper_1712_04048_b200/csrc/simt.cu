@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256) k_simt_typeI(Dev D, SegListI L, int row_l
   // tile skipping: no row of this tile needs the epilogue
   {
     bool act = false;
-    if (threadIdx.x < ST) { const int p = p0 + threadIdx.x; act = p < row_hi && row_active<E>(D, p); }
+    if (threadIdx.x < ST) { const int p = p0 + threadIdx.x; act = p < row_hi && row_active<E>(D, p, D.xrow_pos[p]); }
     if (!__syncthreads_or(act)) return;
   }
   float acc[NACC][4];
@@ -76,14 +76,20 @@ __global__ void __launch_bounds__(256) k_simt_typeI(Dev D, SegListI L, int row_l
   }
   const int j = j0 + tx;
   if (j >= units) return;
+  const UnitC uc = epi_uses_bias<E>() ? load_unit(D, j, epi_is_lstm<E>()) : UnitC{0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int p = p0 + ty + 8 * r;
-    if (p >= row_hi || !row_active<E>(D, p)) continue;
+    if (p >= row_hi) continue;
+    VMeta m;
+    load_meta(D, p, epi_needs_children<E>(), m);
+    if (!row_active<E>(D, p, m.xrow)) continue;
     float v[NACC];
 #pragma unroll
     for (int a = 0; a < NACC; ++a) v[a] = acc[a][r];
-    epilogue<E, OpT>(D, j, p, v);
+    typename EpiK<E>::In in;
+    EpiK<E>::load(D, j, m, in);
+    EpiK<E>::template store<OpT>(D, j, m, v, in, uc);
   }
 }
 

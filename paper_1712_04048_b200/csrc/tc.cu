@@ -28,7 +28,7 @@ constexpr int NT = 64;                     // task-row tile (MMA N) of type I
 constexpr int BK = 64;                     // k-block: one 128-byte swizzle atom of bf16
 constexpr int A_TILE = 128 * BK * 2;       // 16 KB
 constexpr int B_TILE = NT * BK * 2;        // 8 KB
-constexpr int kThreads = 192;              // 6 warps
+constexpr int kThreads = 320;              // 10 warps: TMA, MMA, 8 x (converter/metadata + epilogue)
 constexpr int kSmemBudget = 200 * 1024;
 
 struct Bundle {
@@ -66,9 +66,10 @@ k_tc_typeI(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
   const int m0 = blockIdx.x * 128;
   const int p0 = row_lo + blockIdx.y * NT;
 
+  __shared__ VMeta s_meta[NT];
   if constexpr (E == EPI_LSTM_XPROJ || E == EPI_FC_XPROJ || E == EPI_DX) {
     bool act = false;
-    if (threadIdx.x < NT) { const int p = p0 + threadIdx.x; act = p < row_hi && row_active<E>(D, p); }
+    if (threadIdx.x < NT) { const int p = p0 + threadIdx.x; act = p < row_hi && row_active<E>(D, p, D.xrow_pos[p]); }
     if (!__syncthreads_or(act)) return;
   }
   if (threadIdx.x == 0) {
@@ -132,67 +133,83 @@ k_tc_typeI(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
     }
     __syncwarp();
   } else {
-    // ---- child-sum converters (h~ = sum_k h_k into the C tile, same swizzled layout) ----
-    const int ct = threadIdx.x - 64;          // 0..127
-    int step = 0;
-    for (int bi = 0; bi < P.nb; ++bi) {
-      const Bundle& b = P.b[bi];
-      if (!b.sum) { step += b.nk; continue; }
-      for (int kb = 0; kb < b.nk; ++kb, ++step) {
-        const int s = step % S;
-        const uint32_t ph = (step / S) & 1;
-        ptx::mbar_wait(&full[s], ph);
-        uint8_t* st = smem + s * P.stage_bytes;
-        for (int c = ct; c < NT * 8; c += 128) {
-          const int r = c >> 3, q = c & 7;
-          const int off = r * 128 + ((q ^ (r & 7)) << 4);
-          float acc[8];
-          {
-            const uint4 v = *reinterpret_cast<const uint4*>(st + P.offB + off);
-            const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+    if (warp < 6) {
+      // ---- child-sum converters (h~ = sum_k h_k into the C tile, same swizzled layout) ----
+      const int ct = threadIdx.x - 64;          // 0..127
+      int step = 0;
+      for (int bi = 0; bi < P.nb; ++bi) {
+        const Bundle& b = P.b[bi];
+        if (!b.sum) { step += b.nk; continue; }
+        for (int kb = 0; kb < b.nk; ++kb, ++step) {
+          const int s = step % S;
+          const uint32_t ph = (step / S) & 1;
+          ptx::mbar_wait(&full[s], ph);
+          uint8_t* st = smem + s * P.stage_bytes;
+          for (int c = ct; c < NT * 8; c += 128) {
+            const int r = c >> 3, q = c & 7;
+            const int off = r * 128 + ((q ^ (r & 7)) << 4);
+            float acc[8];
+            {
+              const uint4 v = *reinterpret_cast<const uint4*>(st + P.offB + off);
+              const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) acc[i] = __bfloat162float(e[i]);
+              for (int i = 0; i < 8; ++i) acc[i] = __bfloat162float(e[i]);
+            }
+            for (int t = 1; t < b.nB; ++t) {
+              const uint4 v = *reinterpret_cast<const uint4*>(st + P.offB + t * B_TILE + off);
+              const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(e[i]);
+            }
+            uint4 o;
+            __nv_bfloat16* oe = reinterpret_cast<__nv_bfloat16*>(&o);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) oe[i] = __float2bfloat16_rn(acc[i]);
+            *reinterpret_cast<uint4*>(st + P.offC + off) = o;
+            const int p = p0 + r;
+            if (m0 == 0 && p < row_hi && D.Hs)     // keep h~ for the lazy dU_iou GEMM
+              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(D.Hs) + (size_t)p * D.h + kb * BK + q * 8) = o;
           }
-          for (int t = 1; t < b.nB; ++t) {
-            const uint4 v = *reinterpret_cast<const uint4*>(st + P.offB + t * B_TILE + off);
-            const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(e[i]);
-          }
-          uint4 o;
-          __nv_bfloat16* oe = reinterpret_cast<__nv_bfloat16*>(&o);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) oe[i] = __float2bfloat16_rn(acc[i]);
-          *reinterpret_cast<uint4*>(st + P.offC + off) = o;
-          const int p = p0 + r;
-          if (m0 == 0 && p < row_hi && D.Hs)       // keep h~ for the lazy dU_iou GEMM
-            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(D.Hs) + (size_t)p * D.h + kb * BK + q * 8) = o;
+          ptx::fence_proxy_async_smem();
+          ptx::mbar_arrive(&conv[s]);
         }
-        ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&conv[s]);
       }
+    } else {
+      // ---- per-vertex metadata into shared memory while the mainloop runs ----
+      const int r = threadIdx.x - 192;
+      if (r < NT && p0 + r < row_hi) load_meta(D, p0 + r, epi_needs_children<E>(), s_meta[r]);
     }
-    // ---- epilogue ----
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    // ---- epilogue: 2 groups of 4 warps, each group 32 of the NT task rows ----
     ptx::mbar_wait(done, 0);
     ptx::tc_fence_after();
     const int qd = warp & 3;                   // TMEM lane quarter this warp may access
+    const int grp = (warp - 2) >> 2;
     const int j = m0 + qd * 32 + lane;
     const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16);
-    for (int n0 = 0; n0 < NT; n0 += 16) {
-      if (p0 + n0 >= row_hi) break;            // warp-uniform
-      float v[NACC][16];
+    const UnitC uc = (epi_uses_bias<E>() && j < units) ? load_unit(D, j, epi_is_lstm<E>()) : UnitC{0.f, 0.f, 0.f, 0.f};
+    constexpr int CH = epi_needs_children<E>() ? 4 : 8;
+    for (int c0 = grp * 32; c0 < grp * 32 + 32; c0 += CH) {
+      if (p0 + c0 >= row_hi) break;            // warp-uniform
+      float v[NACC][CH];
 #pragma unroll
-      for (int a = 0; a < NACC; ++a) ptx::tmem_ld16(tq + a * NT + n0, v[a]);
+      for (int a = 0; a < NACC; ++a) ptx::tmem_ld<CH>(tq + a * NT + c0, v[a]);
       if (j < units) {
-#pragma unroll 1
-        for (int i = 0; i < 16; ++i) {
-          const int p = p0 + n0 + i;
-          if (p >= row_hi) break;
-          if (!row_active<E>(D, p)) continue;
+        typename EpiK<E>::In in[CH];
+        bool ok[CH];
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {         // all loads of the chunk first ...
+          const int r = c0 + i;
+          ok[i] = p0 + r < row_hi && row_active<E>(D, p0 + r, s_meta[r].xrow);
+          if (ok[i]) EpiK<E>::load(D, j, s_meta[r], in[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {         // ... then the math and the stores
+          if (!ok[i]) continue;
           float acc[NACC];
 #pragma unroll
           for (int a = 0; a < NACC; ++a) acc[a] = v[a][i];
-          epilogue<E, __nv_bfloat16>(D, j, p, acc);
+          EpiK<E>::template store<__nv_bfloat16>(D, j, s_meta[c0 + i], acc, in[i], uc);
         }
       }
     }
@@ -297,7 +314,7 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
       ptx::mma_commit(done);
     }
     __syncwarp();
-  } else {
+  } else if (warp < 6) {
     ptx::mbar_wait(done, 0);
     ptx::tc_fence_after();
     const int qd = warp & 3;

@@ -197,13 +197,18 @@ def test_bf16_parity(case):
 
 
 # ------------------------------------------------------------------ full-size, sampled
-@pytest.mark.parametrize("cfg,precision,sample", [("cfg4", "bf16", [0, 77, 255]), ("cfg4", "fp32", [3, 200]),
-                                                   ("cfg2", "bf16", [5]), ("cfg5", "bf16", [9])])
-def test_full_size_sampled(cfg, precision, sample):
+@pytest.mark.parametrize("cfg,precision,sample,pscale", [
+    ("cfg4", "bf16", [0, 77, 255], 1.0), ("cfg4", "fp32", [3, 200], 1.0), ("cfg2", "bf16", [5], 1.0),
+    ("cfg3", "bf16", [17, 200], 1.0), ("cfg4_h1024", "bf16", [31], 1.0),
+    # cfg5 (h = 2048, fan-in 4096) with the U(-0.1,0.1) init is chaotic: bf16 rounding alone moves
+    # dW by ~23% (reading R-bf16).  Same shapes/launches with a contracting init:
+    ("cfg5", "bf16", [9], 0.1), ("cfg5", "fp32", [40], 0.1)])
+def test_full_size_sampled(cfg, precision, sample, pscale):
     """BASELINE sizes in the bench's launch configuration.  Graphs are independent, so the
     h of sampled graphs is checked row by row; Gamma is zeroed outside the sample, so the
     full-batch dparams equal the oracle's dparams over the sampled graphs alone."""
     b = gen.make_config_batch(cfg, seed=0)
+    b.params = (b.params * pscale).astype(np.float32)
     keep = np.zeros(b.V, bool)
     for k in sample:
         keep[b.graph_ptr[k]:b.graph_ptr[k + 1]] = True
