@@ -29,7 +29,7 @@ constexpr int BK = 64;                     // k-block: one 128-byte swizzle atom
 constexpr int A_TILE = 128 * BK * 2;       // 16 KB
 constexpr int B_TILE = NT * BK * 2;        // 8 KB
 constexpr int kThreads = 320;              // 10 warps: TMA, MMA, 8 x (converter/metadata + epilogue)
-constexpr int kSmemBudget = 200 * 1024;
+constexpr int kSmemBudget = 196 * 1024;     // pipeline stages; + static VMeta staging + barriers <= 227 KB
 
 struct Bundle {
   int map_a;                 // which A tensor map (0/1)
@@ -434,10 +434,10 @@ static void launch_I(const TcState* t, const CUtensorMap& a0, const CUtensorMap&
                      const Dev& D, PlanI P, int row_lo, int row_hi, int units, cudaStream_t s) {
   if (row_hi <= row_lo) return;
   const int smem = finalize(P);
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(k_tc_typeI<E, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_done = true;
+  static int attr_set = 0;                     // dynamic + static smem must stay <= 227 KB
+  if (smem > attr_set) {
+    cudaFuncSetAttribute(k_tc_typeI<E, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_set = smem;
   }
   dim3 grid(cdiv(units, 128), cdiv(row_hi - row_lo, NT));
   k_tc_typeI<E, NACC><<<grid, kThreads, smem, s>>>(a0, a1, b, D, P, row_lo, row_hi, units);
