@@ -117,6 +117,7 @@ class Context:
         self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
         base = self.workspace.data_ptr()
         aligned = (base + 255) & ~255
+        self._ws_off, self._ws_bytes = aligned - base, nbytes
         self._check(_lib.cavs_set_workspace(self._ctx, ctypes.c_void_p(aligned), nbytes))
         self.P = param_count(cell, N, h, d)
         self.V = 0

@@ -4,6 +4,7 @@
 // t = T-1..1 -> lazily batched parameter gradients (§3.5).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -137,6 +138,8 @@ CAVS_API cavs_status cavs_create(const cavs_desc* desc, int device, void* stream
     return CAVS_E_CUDA;
   }
   c->ws_bytes = carve(c, nullptr);
+  const char* tr = std::getenv("CAVS_TRACE");
+  if (tr && tr[0] == '1') c->ws_bytes += 4u << 20;     // debug trace ring at the end of the workspace
   *out = c;
   return CAVS_OK;
 }
@@ -156,6 +159,9 @@ CAVS_API cavs_status cavs_set_workspace(cavs_ctx* ctx, void* dev, size_t bytes) 
   CK(cudaSetDevice(ctx->device));
   ctx->ws = reinterpret_cast<char*>(dev);
   carve(ctx, ctx->ws);
+  const char* tr = std::getenv("CAVS_TRACE");
+  ctx->D.trace = (tr && tr[0] == '1') ? reinterpret_cast<unsigned long long*>(ctx->ws + ctx->ws_bytes - (4u << 20))
+                                      : nullptr;
   CK(cudaMemsetAsync(ctx->ws, 0, ctx->ws_bytes, ctx->stream));   // arenas start finite (zero)
   if (ctx->desc.precision == CAVS_BF16) {
     cavs_status s = tc_init(ctx->D, ctx->desc.max_vertices, &ctx->tc, &ctx->err);

@@ -26,6 +26,23 @@ namespace cavs {
 
 template <class OpT> __device__ __forceinline__ OpT* op(void* p) { return reinterpret_cast<OpT*>(p); }
 
+// Activations.  FP32 mode: accurate expf/tanhf (parity 1e-5).  BF16 mode: the MUFU tanh
+// (tanh.approx.f32, rel. err <= 2^-10.99), sigmoid(z) = 0.5 tanh(z/2) + 0.5 — an order of
+// magnitude below the bf16 operand rounding the mode already accepts (reading Z11).
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+template <class OpT> __device__ __forceinline__ float act_sig(float z) {
+  if constexpr (sizeof(OpT) == 2) return fmaf(0.5f, tanh_fast(0.5f * z), 0.5f);
+  else return sigm(z);
+}
+template <class OpT> __device__ __forceinline__ float act_tanh(float z) {
+  if constexpr (sizeof(OpT) == 2) return tanh_fast(z);
+  else return tanhf(z);
+}
+
 struct VMeta {
   int p, vid, par, slot, deg, xrow;
   int ch[kMaxN], ch_vid[kMaxN], ch_deg[kMaxN];
@@ -61,17 +78,17 @@ template <class OpT>
 __device__ __forceinline__ void lstm_finish(const Dev& D, int j, const VMeta& m, float zi, float zo, float zu,
                                             const float* zf, const float* ck) {
   const int h = D.h, N = D.N, G = 3 + N;
-  const float i = sigm(zi), o = sigm(zo), u = tanhf(zu);
+  const float i = act_sig<OpT>(zi), o = act_sig<OpT>(zo), u = act_tanh<OpT>(zu);
   float c = i * u;
   float* g = D.gates + (size_t)m.p * G * h;
 #pragma unroll
   for (int k = 0; k < kMaxN; ++k) {
     if (k >= N) break;
-    const float f = sigm(zf[k]);
+    const float f = act_sig<OpT>(zf[k]);
     g[(3 + k) * h + j] = f;
     if (k < m.deg) c += f * ck[k];               // missing children: c_k = 0 (Z1)
   }
-  const float hv = o * tanhf(c);
+  const float hv = o * act_tanh<OpT>(c);
   g[j] = i; g[h + j] = o; g[2 * h + j] = u;
   D.cst[(size_t)m.p * h + j] = c;
   D.h_out[(size_t)m.vid * h + j] = hv;           // push(h)
@@ -104,7 +121,7 @@ template <class OpT>
 __device__ __forceinline__ void lstm_child_store(const Dev& D, int j, int c, int c_deg, float dh, float dc,
                                                  const LstmChildIn& in) {
   const int h = D.h, N = D.N, G = 3 + N;
-  const float tc = tanhf(in.cc);
+  const float tc = act_tanh<OpT>(in.cc);
   const float dzo = dh * tc * in.o * (1.f - in.o);
   const float dcb = dc + dh * in.o * (1.f - tc * tc);
   const float dzi = dcb * in.u * in.i * (1.f - in.i);
@@ -200,7 +217,7 @@ template <> struct EpiK<EPI_LSTM_BWD> {
 template <class OpT>
 __device__ __forceinline__ void fc_finish(const Dev& D, int j, const VMeta& m, float z) {
   const int h = D.h;
-  const float hv = tanhf(z);
+  const float hv = act_tanh<OpT>(z);
   D.gates[(size_t)m.p * h + j] = hv;
   D.h_out[(size_t)m.vid * h + j] = hv;
   if (m.par >= 0) op<OpT>(D.Hk)[(size_t)m.par * 2 * h + (size_t)m.slot * h + j] = to_op<OpT>(hv);

@@ -46,6 +46,7 @@ struct Dev {
   void* Wa; void* Wb; void* Wc; void* Wd; void* We;
   // lazy outputs (fp32 scratch)
   float* lazy;
+  unsigned long long* trace;   // debug (CAVS_TRACE=1): per-CTA globaltimer records, else null
   // caller buffers of the current call
   const float* params; const float* x; const int* x_row; const float* dh_out;
   float* h_out; float* dparams; float* dx;
@@ -54,6 +55,12 @@ struct Dev {
 constexpr int kPadRows = 128;   // extra zero rows after V for TMA/K-block over-reach
 
 __host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ float sigm(float z) { return 1.0f / (1.0f + expf(-z)); }
 

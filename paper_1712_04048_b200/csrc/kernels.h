@@ -9,6 +9,7 @@ namespace cavs {
 constexpr int kMaxN = 4;          // max arity supported by the kernels
 constexpr int kDbChunks = 32;     // row chunks of the deterministic db column reduction
 constexpr int kSplitMax = 8;      // max split-K of the lazy tensor-core GEMMs
+constexpr int kSkinnyMax = 32;    // tasks with at most this many vertices use the skinny level kernel
 
 enum Epi : int { EPI_LSTM_FWD = 0, EPI_LSTM_XPROJ, EPI_LSTM_BWD, EPI_FC_FWD, EPI_FC_XPROJ, EPI_FC_BWD, EPI_DX };
 
@@ -67,6 +68,11 @@ template <class OpT> void simt_backward(Dev& D, const std::vector<int>& lp, cuda
 
 template <class OpT>
 void simt_typeI(const Dev& D, int epi, const SegListI& L, int row_lo, int row_hi, int units, cudaStream_t s);
+template <class OpT>
+void skinny_typeI(const Dev& D, int epi, const SegListI& L, int row_lo, int row_hi, int units, cudaStream_t s);
+// FFMA segment lists of the level kernels (shared by the SIMT, skinny and BF16 paths)
+SegListI fwd_segments(const Dev& D);
+SegListI bwd_segments(const Dev& D);
 template <class OpT>
 void simt_typeII(const Dev& D, const SegListII& L, float* out, int M, int Ncols, int ldo, cudaStream_t s);
 

@@ -17,7 +17,7 @@ __device__ __forceinline__ float load_b(const Dev& D, const SegI& s, int p, int 
     const OpT* hk = reinterpret_cast<const OpT*>(D.Hk) + (size_t)p * D.N * D.h + k;
     float v = 0.f;
     for (int q = 0; q < D.N; ++q) v += from_op(hk[q * D.h]);
-    return v;
+    return from_op(to_op<OpT>(v));               // h~ is an operand: rounded like the tensor-core path
   }
   const OpT* base = reinterpret_cast<const OpT*>(s.b_src == B_HK ? D.Hk : s.b_src == B_XP ? D.Xp : D.dZ);
   return from_op(base[(size_t)p * s.ldb + s.b_col + k]);
@@ -169,6 +169,35 @@ void simt_typeII(const Dev& D, const SegListII& L, float* out, int M, int Ncols,
   k_simt_typeII<OpT><<<grid, 256, 0, s>>>(D, L, out, M, Ncols, ldo);
 }
 
+SegListI fwd_segments(const Dev& D) {
+  const int h = D.h, N = D.N;
+  SegListI F{};
+  if (D.cell == CAVS_CELL_TREE_LSTM) {
+    F.n = 3 + N;
+    for (int g = 0; g < 3; ++g) F.s[g] = SegI{D.Wa, h, g * h, N >= 2 ? B_HSUM : B_HK, 0, N * h, h, g};
+    for (int k = 0; k < N; ++k) F.s[3 + k] = SegI{D.Wa, h, 3 * h, B_HK, k * h, N * h, h, 3 + k};
+  } else {
+    F.n = 1;
+    F.s[0] = SegI{D.Wa, 2 * h, 0, B_HK, 0, 2 * h, 2 * h, 0};
+  }
+  return F;
+}
+
+SegListI bwd_segments(const Dev& D) {
+  const int h = D.h, N = D.N;
+  SegListI B{};
+  if (D.cell == CAVS_CELL_TREE_LSTM) {
+    const int G = 3 + N;
+    B.n = 1 + N;
+    B.s[0] = SegI{D.Wc, 3 * h, 0, B_DZ, 0, G * h, 3 * h, 0};
+    for (int k = 0; k < N; ++k) B.s[1 + k] = SegI{D.Wd, h, 0, B_DZ, (3 + k) * h, G * h, h, 1 + k};
+  } else {
+    B.n = 2;
+    for (int k = 0; k < 2; ++k) B.s[k] = SegI{D.Wc, h, k * h, B_DZ, 0, h, h, k};
+  }
+  return B;
+}
+
 // ---- whole passes (FP32 mode; BF16 operands when CAVS_BF16_SIMT=1 for A/B checks) ----
 template <class OpT>
 void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
@@ -182,7 +211,11 @@ void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
     F.n = 3 + N;
     for (int g = 0; g < 3; ++g) F.s[g] = SegI{D.Wa, h, g * h, N >= 2 ? B_HSUM : B_HK, 0, N * h, h, g};
     for (int k = 0; k < N; ++k) F.s[3 + k] = SegI{D.Wa, h, 3 * h, B_HK, k * h, N * h, h, 3 + k};
-    for (int t = 1; t < T; ++t) { simt_typeI<OpT>(D, EPI_LSTM_FWD, F, lp[t], lp[t + 1], h, s); P.count(1); }
+    for (int t = 1; t < T; ++t) {
+      if (lp[t + 1] - lp[t] <= kSkinnyMax) skinny_typeI<OpT>(D, EPI_LSTM_FWD, F, lp[t], lp[t + 1], h, s);
+      else simt_typeI<OpT>(D, EPI_LSTM_FWD, F, lp[t], lp[t + 1], h, s);
+      P.count(1);
+    }
   } else {
     L.n = 1;
     L.s[0] = SegI{D.Wb, d, 0, B_XP, 0, d, d, 0};
@@ -190,7 +223,11 @@ void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
     P.mark(CAVS_PH_FWD_LEVELS, s);
     F.n = 1;
     F.s[0] = SegI{D.Wa, 2 * h, 0, B_HK, 0, 2 * h, 2 * h, 0};
-    for (int t = 1; t < T; ++t) { simt_typeI<OpT>(D, EPI_FC_FWD, F, lp[t], lp[t + 1], h, s); P.count(1); }
+    for (int t = 1; t < T; ++t) {
+      if (lp[t + 1] - lp[t] <= kSkinnyMax) skinny_typeI<OpT>(D, EPI_FC_FWD, F, lp[t], lp[t + 1], h, s);
+      else simt_typeI<OpT>(D, EPI_FC_FWD, F, lp[t], lp[t + 1], h, s);
+      P.count(1);
+    }
   }
 }
 
@@ -211,7 +248,11 @@ void simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) 
     for (int k = 0; k < 2; ++k) B.s[k] = SegI{D.Wc, h, k * h, B_DZ, 0, h, h, k};
     epi = EPI_FC_BWD;
   }
-  for (int t = T - 1; t >= 1; --t) { simt_typeI<OpT>(D, epi, B, lp[t], lp[t + 1], h, s); P.count(1); }
+  for (int t = T - 1; t >= 1; --t) {
+    if (lp[t + 1] - lp[t] <= kSkinnyMax) skinny_typeI<OpT>(D, epi, B, lp[t], lp[t + 1], h, s);
+    else simt_typeI<OpT>(D, epi, B, lp[t], lp[t + 1], h, s);
+    P.count(1);
+  }
   P.mark(CAVS_PH_LAZY, s);
   // lazy batching of the parameter gradients over ALL vertices; one partial each
   const LazyLayout Z = lazy_layout(D);

@@ -65,6 +65,8 @@ k_tc_typeI(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * 128;
   const int p0 = row_lo + blockIdx.y * NT;
+  __shared__ unsigned long long s_tr[6];
+  if (D.trace && threadIdx.x == 0) s_tr[0] = gtime();
 
   __shared__ VMeta s_meta[NT];
   if constexpr (E == EPI_LSTM_XPROJ || E == EPI_FC_XPROJ || E == EPI_DX) {
@@ -82,6 +84,7 @@ k_tc_typeI(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (D.trace && threadIdx.x == 0) s_tr[1] = gtime();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -183,6 +186,7 @@ k_tc_typeI(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
     // ---- epilogue: 2 groups of 4 warps, each group 32 of the NT task rows ----
     ptx::mbar_wait(done, 0);
     ptx::tc_fence_after();
+    if (D.trace && threadIdx.x == 64) s_tr[2] = gtime();
     const int qd = warp & 3;                   // TMEM lane quarter this warp may access
     const int grp = (warp - 2) >> 2;
     const int j = m0 + qd * 32 + lane;
@@ -216,6 +220,15 @@ k_tc_typeI(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (D.trace && threadIdx.x == 0) {
+    const unsigned long long t = gtime();
+    const unsigned long long at = 8 + 8 * atomicAdd(D.trace, 1ull);
+    if (at + 8 < (4u << 20) / 8) {
+      D.trace[at] = E; D.trace[at + 1] = blockIdx.x + 1000ull * blockIdx.y; D.trace[at + 2] = row_lo;
+      D.trace[at + 3] = s_tr[0]; D.trace[at + 4] = s_tr[1]; D.trace[at + 5] = s_tr[2]; D.trace[at + 6] = t;
+      D.trace[at + 7] = row_hi;
+    }
+  }
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem);
@@ -475,8 +488,10 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
     f.nmma = 3 + N;
     for (int g = 0; g < 3; ++g) { f.mma_a[g] = g; f.mma_b[g] = N >= 2 ? 3 : 0; f.mma_acc[g] = g; }
     for (int k = 0; k < N; ++k) { f.mma_a[3 + k] = 3; f.mma_b[3 + k] = k; f.mma_acc[3 + k] = 3 + k; }
+    const SegListI Fs = fwd_segments(D);
     for (int tt = 1; tt < T; ++tt) {
-      if (N == 1) launch_I<EPI_LSTM_FWD, 4>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
+      if (lp[tt + 1] - lp[tt] <= kSkinnyMax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_FWD, Fs, lp[tt], lp[tt + 1], h, s);
+      else if (N == 1) launch_I<EPI_LSTM_FWD, 4>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       else if (N == 2) launch_I<EPI_LSTM_FWD, 5>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       else if (N == 3) launch_I<EPI_LSTM_FWD, 6>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       else launch_I<EPI_LSTM_FWD, 7>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
@@ -491,8 +506,10 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
     PlanI F{};
     F.nb = 1;
     F.b[0] = one(0, 0, 0, 0, 2 * h / BK, 0);
+    const SegListI Fs = fwd_segments(D);
     for (int tt = 1; tt < T; ++tt) {
-      launch_I<EPI_FC_FWD, 1>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
+      if (lp[tt + 1] - lp[tt] <= kSkinnyMax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_FWD, Fs, lp[tt], lp[tt + 1], h, s);
+      else launch_I<EPI_FC_FWD, 1>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       P.count(1);
     }
   }
@@ -529,8 +546,10 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
     B.nb = 1 + N;
     B.b[0] = one(0, 0, 0, 0, 3 * h / BK, 0);                          // UTiou x dZ_iou
     for (int k = 0; k < N; ++k) B.b[1 + k] = one(1, 0, 0, (3 + k) * h, h / BK, 1 + k);   // UTf x dZ_fk
+    const SegListI Bs = bwd_segments(D);
     for (int tt = T - 1; tt >= 1; --tt) {
-      if (N == 1) launch_I<EPI_LSTM_BWD, 2>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
+      if (lp[tt + 1] - lp[tt] <= kSkinnyMax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_BWD, Bs, lp[tt], lp[tt + 1], h, s);
+      else if (N == 1) launch_I<EPI_LSTM_BWD, 2>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       else if (N == 2) launch_I<EPI_LSTM_BWD, 3>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       else if (N == 3) launch_I<EPI_LSTM_BWD, 4>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       else launch_I<EPI_LSTM_BWD, 5>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
@@ -540,8 +559,10 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
     PlanI B{};
     B.nb = 2;
     for (int k = 0; k < 2; ++k) B.b[k] = one(0, k * h, 0, 0, h / BK, k);   // WcT rows k*h x dZ
+    const SegListI Bs = bwd_segments(D);
     for (int tt = T - 1; tt >= 1; --tt) {
-      launch_I<EPI_FC_BWD, 2>(t, t->A[2], t->A[2], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
+      if (lp[tt + 1] - lp[tt] <= kSkinnyMax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_BWD, Bs, lp[tt], lp[tt + 1], h, s);
+      else launch_I<EPI_FC_BWD, 2>(t, t->A[2], t->A[2], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       P.count(1);
     }
   }
