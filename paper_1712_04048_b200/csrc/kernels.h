@@ -68,6 +68,7 @@ template <class OpT> void simt_backward(Dev& D, const std::vector<int>& lp, cuda
 
 template <class OpT>
 void simt_typeI(const Dev& D, int epi, const SegListI& L, int row_lo, int row_hi, int units, cudaStream_t s);
+int skinny_max(const Dev& D);   // largest task handled by the skinny kernel (0: unsupported shape)
 template <class OpT>
 void skinny_typeI(const Dev& D, int epi, const SegListI& L, int row_lo, int row_hi, int units, cudaStream_t s);
 // FFMA segment lists of the level kernels (shared by the SIMT, skinny and BF16 paths)

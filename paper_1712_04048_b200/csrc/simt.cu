@@ -201,6 +201,7 @@ SegListI bwd_segments(const Dev& D) {
 // ---- whole passes (FP32 mode; BF16 operands when CAVS_BF16_SIMT=1 for A/B checks) ----
 template <class OpT>
 void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
+  const int skmax = skinny_max(D);
   const int h = D.h, d = D.d, N = D.N, T = (int)lp.size() - 1;
   SegListI L{}, F{};
   if (D.cell == CAVS_CELL_TREE_LSTM) {
@@ -212,7 +213,7 @@ void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
     for (int g = 0; g < 3; ++g) F.s[g] = SegI{D.Wa, h, g * h, N >= 2 ? B_HSUM : B_HK, 0, N * h, h, g};
     for (int k = 0; k < N; ++k) F.s[3 + k] = SegI{D.Wa, h, 3 * h, B_HK, k * h, N * h, h, 3 + k};
     for (int t = 1; t < T; ++t) {
-      if (lp[t + 1] - lp[t] <= kSkinnyMax) skinny_typeI<OpT>(D, EPI_LSTM_FWD, F, lp[t], lp[t + 1], h, s);
+      if (lp[t + 1] - lp[t] <= skmax) skinny_typeI<OpT>(D, EPI_LSTM_FWD, F, lp[t], lp[t + 1], h, s);
       else simt_typeI<OpT>(D, EPI_LSTM_FWD, F, lp[t], lp[t + 1], h, s);
       P.count(1);
     }
@@ -224,7 +225,7 @@ void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
     F.n = 1;
     F.s[0] = SegI{D.Wa, 2 * h, 0, B_HK, 0, 2 * h, 2 * h, 0};
     for (int t = 1; t < T; ++t) {
-      if (lp[t + 1] - lp[t] <= kSkinnyMax) skinny_typeI<OpT>(D, EPI_FC_FWD, F, lp[t], lp[t + 1], h, s);
+      if (lp[t + 1] - lp[t] <= skmax) skinny_typeI<OpT>(D, EPI_FC_FWD, F, lp[t], lp[t + 1], h, s);
       else simt_typeI<OpT>(D, EPI_FC_FWD, F, lp[t], lp[t + 1], h, s);
       P.count(1);
     }
@@ -233,6 +234,7 @@ void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
 
 template <class OpT>
 void simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
+  const int skmax = skinny_max(D);
   const int h = D.h, d = D.d, N = D.N, T = (int)lp.size() - 1;
   const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
   const int G = lstm ? 3 + N : 1;
@@ -249,7 +251,7 @@ void simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) 
     epi = EPI_FC_BWD;
   }
   for (int t = T - 1; t >= 1; --t) {
-    if (lp[t + 1] - lp[t] <= kSkinnyMax) skinny_typeI<OpT>(D, epi, B, lp[t], lp[t + 1], h, s);
+    if (lp[t + 1] - lp[t] <= skmax) skinny_typeI<OpT>(D, epi, B, lp[t], lp[t + 1], h, s);
     else simt_typeI<OpT>(D, epi, B, lp[t], lp[t + 1], h, s);
     P.count(1);
   }

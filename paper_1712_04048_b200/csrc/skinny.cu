@@ -3,10 +3,10 @@
 // A task of a few vertices is bound by streaming F's weights (2-8 MB) through the SMs, not by
 // math: the tensor-core kernel puts 128 units per CTA, i.e. only h/128 CTAs each pulling
 // 0.5-1 MB.  Here a CTA owns kUnits = 4 units of every gate, so the weights spread over h/4
-// CTAs (~16 KB each, read once from L2), the task's operand rows are staged in shared memory
-// and the K loop is split across lanes/warps with fp32 accumulation and a shuffle reduction.
-// Numerics are those of the selected precision (bf16 operands incl. the bf16 child sum h~,
-// fp32 accumulate), so results match the tensor-core path up to summation order.  The fused
+// CTAs (~16 KB each, read once from L2).  Each CTA stages the task's operand rows once in
+// shared memory (16-byte vector loads; the child sum h~ is formed there, rounded like the
+// tensor-core path), every warp loads its whole weight rows up front (one latency), and
+// the K dot products run with fp32 accumulation and a shuffle reduction.  The fused
 // epilogue is the same cells.cuh code as every other level kernel.
 #include "cells.cuh"
 #include "kernels.h"
@@ -14,92 +14,161 @@
 namespace cavs {
 
 constexpr int kUnits = 4;          // units of each gate per CTA
-constexpr int kKC = 256;           // K chunk staged in shared memory (static smem < 48 KB)
-constexpr int kSkThreads = 256;    // 8 warps: warp w -> row (w % 4), K half (w / 4)
+constexpr int kSkThreads = 256;    // 8 warps
 
-template <class OpT, int NACC, int E>
-__global__ void __launch_bounds__(kSkThreads) k_skinny(Dev D, SegListI L, int row_lo, int row_hi, int units) {
-  __shared__ float Bs[kSkinnyMax][kKC + 1];
-  __shared__ float part[2][kUnits][kSkinnyMax];
-  __shared__ float out[NACC][kUnits][kSkinnyMax];
-  __shared__ VMeta s_meta[kSkinnyMax];
+template <class OpT> struct Vec;   // 16-byte vector of operands
+template <> struct Vec<float> { static constexpr int n = 4; };
+template <> struct Vec<__nv_bfloat16> { static constexpr int n = 8; };
+
+template <class OpT>
+__device__ __forceinline__ void unpack16(const uint4& u, float* f) {
+  if constexpr (sizeof(OpT) == 4) {
+    f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y); f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
+  } else {
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { const float2 t = __bfloat1622float2(b[i]); f[2 * i] = t.x; f[2 * i + 1] = t.y; }
+  }
+}
+
+// Staged operand layout (per vertex row, in OpT): [B source columns 0..W) | h~ (h columns, HSUM)]
+template <class OpT, int NACC, int E, int MV>
+__global__ void __launch_bounds__(kSkThreads) k_skinny(Dev D, SegListI L, int row_lo, int row_hi, int units,
+                                                      int bsrc, int W, int ldb, int with_hsum) {
+  constexpr int VE = Vec<OpT>::n;
+  extern __shared__ __align__(16) uint8_t sk_smem[];
+  const int SW = W + (with_hsum ? D.h : 0);                     // staged row width (elements)
+  OpT* Bs = reinterpret_cast<OpT*>(sk_smem);                    // [MV][SW]
+  float* out = reinterpret_cast<float*>(sk_smem + (size_t)MV * SW * sizeof(OpT));   // [NACC][kUnits][MV]
+  __shared__ VMeta s_meta[MV];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u0 = blockIdx.x * kUnits;
   const int M = row_hi - row_lo;
   if (threadIdx.x < M) load_meta(D, row_lo + threadIdx.x, epi_needs_children<E>(), s_meta[threadIdx.x]);
-  for (int i = threadIdx.x; i < NACC * kUnits * kSkinnyMax; i += kSkThreads) (&out[0][0][0])[i] = 0.f;
-  const int row = warp & (kUnits - 1), khalf = warp >> 2;
-  for (int si = 0; si < L.n; ++si) {
-    const SegI s = L.s[si];
-    const OpT* A = reinterpret_cast<const OpT*>(s.A);
-    const bool write_hs = s.b_src == B_HSUM && blockIdx.x == 0 && D.Hs != nullptr;
-    float acc[kSkinnyMax];
-#pragma unroll
-    for (int v = 0; v < kSkinnyMax; ++v) acc[v] = 0.f;
-    const int j = u0 + row;
-    for (int k0 = 0; k0 < s.klen; k0 += kKC) {
-      const int kc = min(kKC, s.klen - k0);
-      __syncthreads();
-      for (int e = threadIdx.x; e < M * kc; e += kSkThreads) {
-        const int v = e / kc, k = e % kc, p = row_lo + v;
-        float b;
-        if (s.b_src == B_HSUM) {                 // child sum h~ as the tensor-core path forms it
-          const OpT* hk = reinterpret_cast<const OpT*>(D.Hk) + (size_t)p * D.N * D.h + k0 + k;
-          float t = 0.f;
-          for (int q = 0; q < D.N; ++q) t += from_op(hk[q * D.h]);
-          const OpT r = to_op<OpT>(t);
-          b = from_op(r);
-          if (write_hs) reinterpret_cast<OpT*>(D.Hs)[(size_t)p * D.h + k0 + k] = r;
-        } else {
-          const OpT* base = reinterpret_cast<const OpT*>(s.b_src == B_HK ? D.Hk : s.b_src == B_XP ? D.Xp : D.dZ);
-          b = from_op(base[(size_t)p * s.ldb + s.b_col + k0 + k]);
-        }
-        Bs[v][k] = b;
-      }
-      __syncthreads();
-      if (j < units) {
-        const OpT* a = A + (size_t)(s.a_row + j) * s.lda + k0;
-        for (int k = khalf * 32 + lane; k < kc; k += 64) {
-          const float w = from_op(a[k]);
-#pragma unroll
-          for (int v = 0; v < kSkinnyMax; ++v) acc[v] = fmaf(w, Bs[v][k], acc[v]);
-        }
-      }
-    }
-    // reduce over lanes, then over the two K halves
-#pragma unroll
-    for (int v = 0; v < kSkinnyMax; ++v) {
-      float x = acc[v];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane == 0) part[khalf][row][v] = x;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kUnits * kSkinnyMax; i += kSkThreads) {
-      const int r = i / kSkinnyMax, v = i % kSkinnyMax;
-      out[s.acc][r][v] += part[0][r][v] + part[1][r][v];
+  for (int i = threadIdx.x; i < NACC * kUnits * MV; i += kSkThreads) out[i] = 0.f;
+  // ---- stage the task's operand rows (one pass, 16-byte vectors) ----
+  {
+    const OpT* src = reinterpret_cast<const OpT*>(bsrc == B_HK ? D.Hk : bsrc == B_XP ? D.Xp : D.dZ);
+    const int nv = W / VE;
+    for (int e = threadIdx.x; e < MV * nv; e += kSkThreads) {
+      const int v = e / nv, c = e % nv;
+      uint4 val = make_uint4(0, 0, 0, 0);
+      if (v < M) val = *reinterpret_cast<const uint4*>(src + (size_t)(row_lo + v) * ldb + c * VE);
+      *reinterpret_cast<uint4*>(Bs + (size_t)v * SW + c * VE) = val;
     }
   }
   __syncthreads();
-  // fused epilogue: thread -> (unit r, vertex v)
+  if (with_hsum) {                                              // h~ = sum_k h_k, rounded to the operand type
+    const int h = D.h;
+    for (int e = threadIdx.x; e < MV * h; e += kSkThreads) {
+      const int v = e / h, k = e % h;
+      float t = 0.f;
+      for (int q = 0; q < D.N; ++q) t += from_op(Bs[(size_t)v * SW + q * h + k]);
+      const OpT r = to_op<OpT>(t);
+      Bs[(size_t)v * SW + W + k] = r;
+      if (blockIdx.x == 0 && v < M && D.Hs) reinterpret_cast<OpT*>(D.Hs)[(size_t)(row_lo + v) * h + k] = r;
+    }
+    __syncthreads();
+  }
+  // ---- dot products: row = (segment, unit); warps take rows round-robin ----
+  const int nrows = L.n * kUnits;
+  for (int rr = warp; rr < nrows; rr += kSkThreads / 32) {
+    const SegI s = L.s[rr / kUnits];
+    const int r = rr % kUnits, j = u0 + r;
+    if (j >= units) continue;                                   // warp-uniform
+    const OpT* a = reinterpret_cast<const OpT*>(s.A) + (size_t)(s.a_row + j) * s.lda;
+    const int bcol = s.b_src == B_HSUM ? W : s.b_col;
+    float acc[MV];
+#pragma unroll
+    for (int v = 0; v < MV; ++v) acc[v] = 0.f;
+    constexpr int KMAX = 12;                                    // vectors per lane kept in flight
+    for (int kb = 0; kb < s.klen; kb += 32 * VE * KMAX) {
+      uint4 av[KMAX];
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i) {
+        const int k = kb + (i * 32 + lane) * VE;
+        av[i] = k < s.klen ? *reinterpret_cast<const uint4*>(a + k) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i) {
+        const int k = kb + (i * 32 + lane) * VE;
+        if (k >= s.klen) break;
+        float w[VE];
+        unpack16<OpT>(av[i], w);
+#pragma unroll
+        for (int v = 0; v < MV; ++v) {
+          float b[VE];
+          unpack16<OpT>(*reinterpret_cast<const uint4*>(Bs + (size_t)v * SW + bcol + k), b);
+#pragma unroll
+          for (int e = 0; e < VE; ++e) acc[v] = fmaf(w[e], b[e], acc[v]);
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < MV; ++v) {
+      float x = acc[v];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) atomicAdd(&out[(s.acc * kUnits + r) * MV + v], x);   // smem; segments may share an acc
+    }
+  }
+  __syncthreads();
+  // ---- fused epilogue: thread -> (unit r, vertex v) ----
   for (int i = threadIdx.x; i < kUnits * M; i += kSkThreads) {
     const int r = i / M, v = i % M;
     const int j = u0 + r;
     const int p = row_lo + v;
     if (j >= units || !row_active<E>(D, p, s_meta[v].xrow)) continue;
     const UnitC uc = epi_uses_bias<E>() ? load_unit(D, j, epi_is_lstm<E>()) : UnitC{0.f, 0.f, 0.f, 0.f};
-    float a[NACC];
+    float av[NACC];
 #pragma unroll
-    for (int q = 0; q < NACC; ++q) a[q] = out[q][r][v];
+    for (int q = 0; q < NACC; ++q) av[q] = out[(q * kUnits + r) * MV + v];
     typename EpiK<E>::In in;
     EpiK<E>::load(D, j, s_meta[v], in);
-    EpiK<E>::template store<OpT>(D, j, s_meta[v], a, in, uc);
+    EpiK<E>::template store<OpT>(D, j, s_meta[v], av, in, uc);
   }
+}
+
+template <class OpT, int NACC, int E, int MV>
+static void sk_mv(const Dev& D, const SegListI& L, int row_lo, int row_hi, int units, cudaStream_t s) {
+  // staged source: the union of the segments' B columns (all segments of a level kernel read one arena)
+  int bsrc = B_DZ, W = 0, ldb = 0, with_hsum = 0;
+  for (int i = 0; i < L.n; ++i) {
+    const SegI& g = L.s[i];
+    if (g.b_src == B_HSUM) { with_hsum = 1; bsrc = B_HK; ldb = g.ldb; W = std::max(W, D.N * D.h); }
+    else { bsrc = g.b_src; ldb = g.ldb; W = std::max(W, g.b_col + g.klen); }
+  }
+  const int SW = W + (with_hsum ? D.h : 0);
+  const size_t smem = (size_t)MV * SW * sizeof(OpT) + (size_t)NACC * kUnits * MV * sizeof(float);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaFuncSetAttribute(k_skinny<OpT, NACC, E, MV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  k_skinny<OpT, NACC, E, MV><<<cdiv(units, kUnits), kSkThreads, smem, s>>>(D, L, row_lo, row_hi, units, bsrc, W,
+                                                                            ldb, with_hsum);
 }
 
 template <class OpT, int NACC, int E>
 static void sk(const Dev& D, const SegListI& L, int row_lo, int row_hi, int units, cudaStream_t s) {
-  k_skinny<OpT, NACC, E><<<cdiv(units, kUnits), kSkThreads, 0, s>>>(D, L, row_lo, row_hi, units);
+  const int M = row_hi - row_lo;
+  if (M <= 4) sk_mv<OpT, NACC, E, 4>(D, L, row_lo, row_hi, units, s);
+  else if (M <= 8) sk_mv<OpT, NACC, E, 8>(D, L, row_lo, row_hi, units, s);
+  else if (M <= 16) sk_mv<OpT, NACC, E, 16>(D, L, row_lo, row_hi, units, s);
+  else sk_mv<OpT, NACC, E, 32>(D, L, row_lo, row_hi, units, s);
+}
+
+int skinny_max(const Dev& D) {
+  // 16-byte vector access needs every row width / column offset to be a multiple of the vector
+  const int es = D.prec == CAVS_BF16 ? 2 : 4;
+  const int ve = 16 / es;
+  if (D.h % ve || D.d % ve) return 0;
+  // staged rows must fit shared memory: widest source row (+ h~) x MV operands
+  const int G = D.cell == CAVS_CELL_TREE_LSTM ? 3 + D.N : 1;
+  const int W = std::max(D.N * D.h + D.h, G * D.h);
+  int mv = kSkinnyMax;
+  while (mv > 4 && (size_t)mv * W * es > 180 * 1024) mv /= 2;
+  return mv;
 }
 
 template <class OpT>

@@ -466,6 +466,7 @@ static Bundle one(int map_a, int a_row, int a_col0, int b_col, int nk, int acc) 
 
 
 void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
+  const int skmax = skinny_max(D);
   if (t->use_simt) { simt_forward<__nv_bfloat16>(D, lp, s, P); return; }
   const int h = D.h, d = D.d, N = D.N, T = (int)lp.size() - 1;
   if (D.cell == CAVS_CELL_TREE_LSTM) {
@@ -490,7 +491,7 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
     for (int k = 0; k < N; ++k) { f.mma_a[3 + k] = 3; f.mma_b[3 + k] = k; f.mma_acc[3 + k] = 3 + k; }
     const SegListI Fs = fwd_segments(D);
     for (int tt = 1; tt < T; ++tt) {
-      if (lp[tt + 1] - lp[tt] <= kSkinnyMax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_FWD, Fs, lp[tt], lp[tt + 1], h, s);
+      if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_FWD, Fs, lp[tt], lp[tt + 1], h, s);
       else if (N == 1) launch_I<EPI_LSTM_FWD, 4>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       else if (N == 2) launch_I<EPI_LSTM_FWD, 5>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       else if (N == 3) launch_I<EPI_LSTM_FWD, 6>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
@@ -508,7 +509,7 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
     F.b[0] = one(0, 0, 0, 0, 2 * h / BK, 0);
     const SegListI Fs = fwd_segments(D);
     for (int tt = 1; tt < T; ++tt) {
-      if (lp[tt + 1] - lp[tt] <= kSkinnyMax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_FWD, Fs, lp[tt], lp[tt + 1], h, s);
+      if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_FWD, Fs, lp[tt], lp[tt + 1], h, s);
       else launch_I<EPI_FC_FWD, 1>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       P.count(1);
     }
@@ -534,6 +535,7 @@ static int launch_II(const CUtensorMap& a, const CUtensorMap& b, const Dev& D, P
 }
 
 void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, int* split, Prof& P) {
+  const int skmax = skinny_max(D);
   split[0] = split[1] = split[2] = 1;
   if (t->use_simt) { simt_backward<__nv_bfloat16>(D, lp, s, P); return; }
   const int h = D.h, d = D.d, N = D.N, T = (int)lp.size() - 1;
@@ -548,7 +550,7 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
     for (int k = 0; k < N; ++k) B.b[1 + k] = one(1, 0, 0, (3 + k) * h, h / BK, 1 + k);   // UTf x dZ_fk
     const SegListI Bs = bwd_segments(D);
     for (int tt = T - 1; tt >= 1; --tt) {
-      if (lp[tt + 1] - lp[tt] <= kSkinnyMax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_BWD, Bs, lp[tt], lp[tt + 1], h, s);
+      if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_BWD, Bs, lp[tt], lp[tt + 1], h, s);
       else if (N == 1) launch_I<EPI_LSTM_BWD, 2>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       else if (N == 2) launch_I<EPI_LSTM_BWD, 3>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       else if (N == 3) launch_I<EPI_LSTM_BWD, 4>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
@@ -561,7 +563,7 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
     for (int k = 0; k < 2; ++k) B.b[k] = one(0, k * h, 0, 0, h / BK, k);   // WcT rows k*h x dZ
     const SegListI Bs = bwd_segments(D);
     for (int tt = T - 1; tt >= 1; --tt) {
-      if (lp[tt + 1] - lp[tt] <= kSkinnyMax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_BWD, Bs, lp[tt], lp[tt + 1], h, s);
+      if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_BWD, Bs, lp[tt], lp[tt + 1], h, s);
       else launch_I<EPI_FC_BWD, 2>(t, t->A[2], t->A[2], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       P.count(1);
     }

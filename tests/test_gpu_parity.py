@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 FP32_TOL = 1e-5
 BF16_TOL = 2e-2
-BF16_EMU_TOL = 2e-3
+BF16_EMU_TOL = 5e-3   # bf16-emulating oracle has exact activations; the GPU uses MUFU tanh (2^-11)
 
 
 def _sched_check(b, precision="fp32"):
