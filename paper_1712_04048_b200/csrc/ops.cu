@@ -73,7 +73,7 @@ __global__ void k_prep(Dev D) {
   }
 }
 
-// One CTA per 64-position tile.
+// One CTA per 64-position tile; 4 consecutive x values per thread and step (16-byte loads).
 template <class OpT>
 __global__ void k_pull(Dev D) {
   const int p0 = blockIdx.x * 64;
@@ -92,11 +92,23 @@ __global__ void k_pull(Dev D) {
   if (threadIdx.x == 0) D.tile_x[blockIdx.x] = any;
   OpT* X = op<OpT>(D.Xp);
   const int d = D.d;
-  for (int e = threadIdx.x; e < 64 * d; e += blockDim.x) {
-    const int rr = e / d, k = e % d, p = p0 + rr;
-    if (p >= D.V) break;
-    const int r = s_r[rr];
-    X[(size_t)p * d + k] = to_op<OpT>(r >= 0 ? D.x[(size_t)r * d + k] : 0.f);
+  if ((d & 3) == 0) {
+    const int d4 = d >> 2;
+    for (int e = threadIdx.x; e < 64 * d4; e += blockDim.x) {
+      const int rr = e / d4, k = (e % d4) * 4, p = p0 + rr;
+      if (p >= D.V) break;
+      const int r = s_r[rr];
+      const float4 v = r >= 0 ? *reinterpret_cast<const float4*>(D.x + (size_t)r * d + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+      OpT* o = X + (size_t)p * d + k;
+      o[0] = to_op<OpT>(v.x); o[1] = to_op<OpT>(v.y); o[2] = to_op<OpT>(v.z); o[3] = to_op<OpT>(v.w);
+    }
+  } else {
+    for (int e = threadIdx.x; e < 64 * d; e += blockDim.x) {
+      const int rr = e / d, k = e % d, p = p0 + rr;
+      if (p >= D.V) break;
+      const int r = s_r[rr];
+      X[(size_t)p * d + k] = to_op<OpT>(r >= 0 ? D.x[(size_t)r * d + k] : 0.f);
+    }
   }
 }
 
@@ -116,9 +128,16 @@ __global__ void k_colsum(Dev D, float* part, int cols) {
   const int chunk = cdiv(D.V, gridDim.y);
   const int r0 = blockIdx.y * chunk, r1 = min(D.V, r0 + chunk);
   const OpT* dz = op<OpT>(D.dZ);
-  float s = 0.f;
-  for (int r = r0; r < r1; ++r) s += from_op(dz[(size_t)r * cols + col]);
-  part[(size_t)blockIdx.y * cols + col] = s;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  int r = r0;
+  for (; r + 3 < r1; r += 4) {
+    s0 += from_op(dz[(size_t)r * cols + col]);
+    s1 += from_op(dz[(size_t)(r + 1) * cols + col]);
+    s2 += from_op(dz[(size_t)(r + 2) * cols + col]);
+    s3 += from_op(dz[(size_t)(r + 3) * cols + col]);
+  }
+  for (; r < r1; ++r) s0 += from_op(dz[(size_t)r * cols + col]);
+  part[(size_t)blockIdx.y * cols + col] = (s0 + s1) + (s2 + s3);
 }
 
 __global__ void k_pack(Dev D, LazyLayout Z, int Su4, int Suf, int Sw, const float* dbp) {
@@ -188,7 +207,7 @@ void launch_roots(const Dev& D, int n_roots, const int* roots, cudaStream_t s) {
 
 void launch_colsum(const Dev& D, float* part, cudaStream_t s) {
   const int cols = (D.cell == CAVS_CELL_TREE_LSTM ? 3 + D.N : 1) * D.h;
-  dim3 grid(cdiv(cols, 128), kDbChunks);
+  dim3 grid(cdiv(cols, 128), kDbChunks);   // 32 deterministic row chunks
   if (D.prec == CAVS_BF16) k_colsum<__nv_bfloat16><<<grid, 128, 0, s>>>(D, part, cols);
   else k_colsum<float><<<grid, 128, 0, s>>>(D, part, cols);
 }

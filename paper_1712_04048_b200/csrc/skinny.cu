@@ -46,16 +46,22 @@ __global__ void __launch_bounds__(kSkThreads) k_skinny(Dev D, SegListI L, int ro
   const int M = row_hi - row_lo;
   if (threadIdx.x < M) load_meta(D, row_lo + threadIdx.x, epi_needs_children<E>(), s_meta[threadIdx.x]);
   for (int i = threadIdx.x; i < NACC * kUnits * MV; i += kSkThreads) out[i] = 0.f;
-  // ---- stage the task's operand rows (one pass, 16-byte vectors) ----
+  // ---- stage the task's operand rows: all 16-byte copies in flight at once (cp.async) ----
   {
     const OpT* src = reinterpret_cast<const OpT*>(bsrc == B_HK ? D.Hk : bsrc == B_XP ? D.Xp : D.dZ);
     const int nv = W / VE;
     for (int e = threadIdx.x; e < MV * nv; e += kSkThreads) {
       const int v = e / nv, c = e % nv;
-      uint4 val = make_uint4(0, 0, 0, 0);
-      if (v < M) val = *reinterpret_cast<const uint4*>(src + (size_t)(row_lo + v) * ldb + c * VE);
-      *reinterpret_cast<uint4*>(Bs + (size_t)v * SW + c * VE) = val;
+      OpT* dst = Bs + (size_t)v * SW + c * VE;
+      if (v < M) {
+        const OpT* g = src + (size_t)(row_lo + v) * ldb + c * VE;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                     "l"(g) : "memory");
+      } else {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+      }
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   }
   __syncthreads();
   if (with_hsum) {                                              // h~ = sum_k h_k, rounded to the operand type

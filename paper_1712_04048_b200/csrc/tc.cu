@@ -35,11 +35,12 @@ struct Bundle {
   int map_a;                 // which A tensor map (0/1)
   int nA; int a_row[4];      // A row offsets (added to the CTA's unit base m0)
   int a_col0;                // A column (k) base
-  int nB; int b_col[3];      // B column bases in the arena
+  int nB; int b_col[4];      // B column bases in the arena
   int sum;                   // C = sum of the nB B tiles (child-sum h~)
   int nk;                    // k-blocks
-  int nmma; int mma_a[6], mma_b[6], mma_acc[6];   // mma_b: 0..2 B tile, 3 = C
+  int nmma; int mma_a[6], mma_b[6], mma_acc[6];   // mma_b: 0..3 B tile, kC = the child-sum tile
 };
+constexpr int kC = 7;
 struct PlanI { int nb; Bundle b[4]; int stages; int stage_bytes; int offB; int offC; };
 
 struct SegT2 { int a_col; int b_col; int k_lo, k_hi; int skip_no_x; };
@@ -121,7 +122,7 @@ k_tc_typeI(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
           const uint32_t st = ptx::smem_u32(smem + s * P.stage_bytes);
           for (int m = 0; m < b.nmma; ++m) {
             const uint32_t a = st + b.mma_a[m] * A_TILE;
-            const uint32_t bb = b.mma_b[m] == 3 ? st + P.offC : st + P.offB + b.mma_b[m] * B_TILE;
+            const uint32_t bb = b.mma_b[m] == kC ? st + P.offC : st + P.offB + b.mma_b[m] * B_TILE;
             const uint32_t d = tmem + b.mma_acc[m] * NT;
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
@@ -354,6 +355,238 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
   }
 }
 
+
+// ------------------------------------------------------------------------------------
+// Gate-split cluster level kernel.  A cluster of 4 CTAs covers one 128-unit block of one
+// 64-row task tile; rank r streams only its gate's weights (forward: U_i / U_o / U_u / U_f;
+// backward and dX: the K columns of gate r), so each CTA pulls ~1/4 of the weights of the
+// monolithic kernel.  After the mainloop every CTA stages its accumulators in its own shared
+// memory, the cluster synchronises, and rank r runs the fused cell epilogue for task columns
+// [16r, 16r+16), reading the other ranks' accumulators through distributed shared memory.
+constexpr int kCluster = 4;
+constexpr int kOwn = NT / kCluster;   // task columns per CTA in the epilogue
+
+struct RankPlan { int nb; Bundle b[3]; int nacc; int stages; int stage_bytes; int offB; int offC; };
+struct PlanGS { RankPlan r[kCluster]; int comb[8][kCluster]; int bar_off; };
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t d;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(saddr), "r"(rank));
+  return d;
+}
+__device__ __forceinline__ float ld_dsmem(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+template <int E, int NACC>
+__global__ void __launch_bounds__(kThreads, 1)
+k_tc_gs(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
+        const __grid_constant__ CUtensorMap mB, Dev D, PlanGS P, int row_lo, int row_hi, int units) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  const uint32_t rank = cluster_rank();
+  const RankPlan& R = P.r[rank];
+  const int S = R.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P.bar_off);
+  uint64_t* empty = full + 6;
+  uint64_t* conv = empty + 6;
+  uint64_t* done = conv + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  float* xs = reinterpret_cast<float*>(smem);                    // [nacc][NT][128] after the mainloop
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = (blockIdx.x / kCluster) * 128;
+  const int p0 = row_lo + blockIdx.y * NT;
+  __shared__ VMeta s_meta[kOwn];
+
+  if constexpr (E == EPI_LSTM_XPROJ || E == EPI_FC_XPROJ || E == EPI_DX) {
+    bool act = false;                                            // uniform across the cluster
+    if (threadIdx.x < NT) { const int p = p0 + threadIdx.x; act = p < row_hi && row_active<E>(D, p, D.xrow_pos[p]); }
+    if (!__syncthreads_or(act)) return;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); ptx::mbar_init(&conv[s], 128); }
+    ptx::mbar_init(done, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<256>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::tma_prefetch(&mA0); ptx::tma_prefetch(&mA1); ptx::tma_prefetch(&mB);
+      int step = 0;
+      for (int bi = 0; bi < R.nb; ++bi) {
+        const Bundle& b = R.b[bi];
+        const CUtensorMap* ma = b.map_a ? &mA1 : &mA0;
+        for (int kb = 0; kb < b.nk; ++kb, ++step) {
+          const int s = step % S;
+          const uint32_t ph = (step / S) & 1;
+          ptx::mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * R.stage_bytes;
+          ptx::mbar_arrive_expect_tx(&full[s], b.nA * A_TILE + b.nB * B_TILE);
+          for (int i = 0; i < b.nA; ++i)
+            ptx::tma_load_2d(st + i * A_TILE, ma, b.a_col0 + kb * BK, b.a_row[i] + m0, &full[s]);
+          for (int i = 0; i < b.nB; ++i)
+            ptx::tma_load_2d(st + R.offB + i * B_TILE, &mB, b.b_col[i] + kb * BK, p0, &full[s]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16(128, NT, 0, 0);
+      uint32_t written = 0;                                      // accumulators already initialised
+      int step = 0;
+      for (int bi = 0; bi < R.nb; ++bi) {
+        const Bundle& b = R.b[bi];
+        for (int kb = 0; kb < b.nk; ++kb, ++step) {
+          const int s = step % S;
+          const uint32_t ph = (step / S) & 1;
+          ptx::mbar_wait(&full[s], ph);
+          if (b.sum) ptx::mbar_wait(&conv[s], ph);
+          ptx::tc_fence_after();
+          const uint32_t st = ptx::smem_u32(smem + s * R.stage_bytes);
+          for (int m = 0; m < b.nmma; ++m) {
+            const uint32_t a = st + b.mma_a[m] * A_TILE;
+            const uint32_t bb = b.mma_b[m] == kC ? st + R.offC : st + R.offB + b.mma_b[m] * B_TILE;
+            const int acc = b.mma_acc[m];
+            const uint32_t d = tmem + acc * NT;
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              ptx::mma_bf16(d, ptx::sdesc_sw128(a + kk * 32, 16, 1024), ptx::sdesc_sw128(bb + kk * 32, 16, 1024),
+                            idesc, ((written >> acc) & 1u) | (kk > 0 ? 1u : 0u));
+            }
+            written |= 1u << acc;
+          }
+          ptx::mma_commit(&empty[s]);
+        }
+      }
+      ptx::mma_commit(done);
+    }
+    __syncwarp();
+  } else if (warp < 6) {
+    // ---- child-sum converters ----
+    const int ct = threadIdx.x - 64;
+    int step = 0;
+    for (int bi = 0; bi < R.nb; ++bi) {
+      const Bundle& b = R.b[bi];
+      if (!b.sum) { step += b.nk; continue; }
+      for (int kb = 0; kb < b.nk; ++kb, ++step) {
+        const int s = step % S;
+        const uint32_t ph = (step / S) & 1;
+        ptx::mbar_wait(&full[s], ph);
+        uint8_t* st = smem + s * R.stage_bytes;
+        for (int c = ct; c < NT * 8; c += 128) {
+          const int r = c >> 3, q = c & 7;
+          const int off = r * 128 + ((q ^ (r & 7)) << 4);
+          float acc[8];
+          {
+            const uint4 v = *reinterpret_cast<const uint4*>(st + R.offB + off);
+            const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = __bfloat162float(e[i]);
+          }
+          for (int t = 1; t < b.nB; ++t) {
+            const uint4 v = *reinterpret_cast<const uint4*>(st + R.offB + t * B_TILE + off);
+            const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(e[i]);
+          }
+          uint4 o;
+          __nv_bfloat16* oe = reinterpret_cast<__nv_bfloat16*>(&o);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) oe[i] = __float2bfloat16_rn(acc[i]);
+          *reinterpret_cast<uint4*>(st + R.offC + off) = o;
+          const int p = p0 + r;
+          if (m0 == 0 && rank == 0 && p < row_hi && D.Hs)        // keep h~ for the lazy dU_iou GEMM
+            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(D.Hs) + (size_t)p * D.h + kb * BK + q * 8) = o;
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(&conv[s]);
+      }
+    }
+  } else {
+    // ---- metadata of this CTA's epilogue columns ----
+    const int r = threadIdx.x - 192;
+    const int p = p0 + (int)rank * kOwn + r;
+    if (r < kOwn && p < row_hi) load_meta(D, p, epi_needs_children<E>(), s_meta[r]);
+  }
+  // ---- stage own accumulators in shared memory ----
+  const int qd = warp & 3;
+  if (warp >= 2) {
+    ptx::mbar_wait(done, 0);
+    ptx::tc_fence_after();
+    const int grp = (warp - 2) >> 2;
+    const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16);
+    for (int a = 0; a < R.nacc; ++a) {
+      for (int c0 = grp * 32; c0 < grp * 32 + 32; c0 += 8) {
+        float v[8];
+        ptx::tmem_ld<8>(tq + a * NT + c0, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xs[((size_t)a * NT + c0 + i) * 128 + qd * 32 + lane] = v[i];
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  cluster_sync_all();
+  // ---- fused epilogue over this CTA's kOwn columns (two groups of 8) ----
+  if (warp >= 2) {
+    const int grp = (warp - 2) >> 2;
+    const int j = m0 + qd * 32 + lane;
+    const UnitC uc = (epi_uses_bias<E>() && j < units) ? load_unit(D, j, epi_is_lstm<E>()) : UnitC{0.f, 0.f, 0.f, 0.f};
+    const uint32_t xs_base = ptx::smem_u32(xs) + (uint32_t)(qd * 32 + lane) * 4u;
+    constexpr int CH = epi_needs_children<E>() ? 2 : 8;        // vertices whose loads are batched
+#pragma unroll 1
+    for (int c0 = 0; c0 < kOwn / 2; c0 += CH) {
+      float acc[CH][NACC];
+      typename EpiK<E>::In in[CH];
+      bool ok[CH];
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        const int r = grp * (kOwn / 2) + c0 + i;               // own-column index
+        const int c = (int)rank * kOwn + r;                    // task column in the tile
+        const int p = p0 + c;
+        ok[i] = j < units && p < row_hi && row_active<E>(D, p, s_meta[r].xrow);
+        if (!ok[i]) continue;
+#pragma unroll
+        for (int e = 0; e < NACC; ++e) {
+          float sum = 0.f;
+#pragma unroll
+          for (int q = 0; q < kCluster; ++q) {
+            const int ai = P.comb[e][q];
+            if (ai >= 0) sum += ld_dsmem(mapa_rank(xs_base + (uint32_t)((ai * NT + c) * 128) * 4u, q));
+          }
+          acc[i][e] = sum;
+        }
+        EpiK<E>::load(D, j, s_meta[r], in[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < CH; ++i)
+        if (ok[i]) EpiK<E>::template store<__nv_bfloat16>(D, j, s_meta[grp * (kOwn / 2) + c0 + i], acc[i], in[i], uc);
+    }
+  }
+  cluster_sync_all();                                          // remote reads done before smem is released
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<256>(tmem);
+  }
+}
+
 // =====================================================================================
 // host side
 // =====================================================================================
@@ -363,6 +596,7 @@ struct TcState {
   CUtensorMap B_hk, B_xp, B_dz;
   CUtensorMap M_dz, M_hs, M_hk, M_xp;
   bool use_simt = false;
+  bool mono = false;            // CAVS_TC_MONO=1: one CTA per 128-unit block (A/B checks)
 };
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -383,6 +617,8 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
   TcState* t = new TcState();
   const char* env = std::getenv("CAVS_BF16_SIMT");
   t->use_simt = env && env[0] == '1';
+  const char* mono = std::getenv("CAVS_TC_MONO");
+  t->mono = mono && mono[0] == '1';
   if (!g_encode) {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
@@ -465,6 +701,163 @@ static Bundle one(int map_a, int a_row, int a_col0, int b_col, int nk, int acc) 
 }
 
 
+
+// ---- gate-split plans ------------------------------------------------------------------
+static Bundle bundle(int map_a, int a_row, int a_col0, int nB, const int* b_cols, int sum, int nk) {
+  Bundle b{};
+  b.map_a = map_a; b.nA = 1; b.a_row[0] = a_row; b.a_col0 = a_col0;
+  b.nB = nB; for (int i = 0; i < nB; ++i) b.b_col[i] = b_cols[i];
+  b.sum = sum; b.nk = nk;
+  return b;
+}
+
+static int gs_finalize(PlanGS& P) {
+  int pipe = 0, xs = 0;
+  for (int r = 0; r < kCluster; ++r) {
+    RankPlan& R = P.r[r];
+    int maxB = 0, sum = 0;
+    for (int i = 0; i < R.nb; ++i) { maxB = std::max(maxB, R.b[i].nB); sum |= R.b[i].sum; }
+    R.offB = A_TILE;
+    R.offC = R.offB + maxB * B_TILE;
+    R.stage_bytes = R.offC + (sum ? B_TILE : 0);
+    R.stages = std::max(1, std::min(6, kSmemBudget / R.stage_bytes));
+    pipe = std::max(pipe, R.stages * R.stage_bytes);
+    xs = std::max(xs, R.nacc * NT * 128 * 4);
+  }
+  P.bar_off = (std::max(pipe, xs) + 1023) & ~1023;
+  return 1024 + P.bar_off + 3 * 6 * 8 + 16 + 64;
+}
+
+// K range [0, nkb) k-blocks split over the cluster ranks (contiguous, balanced).
+static void ksplit(int nkb, int r, int* kb0, int* nk) {
+  const int q = nkb / kCluster, rem = nkb % kCluster;
+  *kb0 = r * q + std::min(r, rem);
+  *nk = q + (r < rem ? 1 : 0);
+}
+
+// all ranks: one bundle over their K share of (A rows a_row, A cols a_col, B cols b_col) -> acc
+static void gs_add_ksplit(PlanGS& P, int map_a, int a_row, int a_col, int b_col, int K, int acc) {
+  const int nkb = K / BK;
+  for (int r = 0; r < kCluster; ++r) {
+    int kb0, nk;
+    ksplit(nkb, r, &kb0, &nk);
+    RankPlan& R = P.r[r];
+    if (nk == 0) continue;
+    const int bc = b_col + kb0 * BK;
+    Bundle b = bundle(map_a, a_row, a_col + kb0 * BK, 1, &bc, 0, nk);
+    b.nmma = 1; b.mma_a[0] = 0; b.mma_b[0] = 0; b.mma_acc[0] = R.nacc;
+    R.b[R.nb++] = b;
+    P.comb[acc][r] = R.nacc;
+    R.nacc++;
+  }
+}
+
+static PlanGS gs_empty() {
+  PlanGS P{};
+  for (int e = 0; e < 8; ++e) for (int r = 0; r < kCluster; ++r) P.comb[e][r] = -1;
+  return P;
+}
+
+// Tree-LSTM forward task: rank g < 3 -> gate g over h~; rank 3 -> U_f over every child slot.
+static PlanGS gs_lstm_fwd(int h, int N) {
+  PlanGS P = gs_empty();
+  int cols[4];
+  for (int k = 0; k < N; ++k) cols[k] = k * h;
+  for (int g = 0; g < 3; ++g) {
+    RankPlan& R = P.r[g];
+    Bundle b = bundle(0, g * h, 0, N, cols, N >= 2, h / BK);
+    b.nmma = 1; b.mma_a[0] = 0; b.mma_b[0] = N >= 2 ? kC : 0; b.mma_acc[0] = 0;
+    R.b[0] = b; R.nb = 1; R.nacc = 1;
+    P.comb[g][g] = 0;
+  }
+  RankPlan& R = P.r[3];
+  Bundle b = bundle(0, 3 * h, 0, N, cols, 0, h / BK);
+  b.nmma = N;
+  for (int k = 0; k < N; ++k) { b.mma_a[k] = 0; b.mma_b[k] = k; b.mma_acc[k] = k; P.comb[3 + k][3] = k; }
+  R.b[0] = b; R.nb = 1; R.nacc = N;
+  return P;
+}
+
+// Tree-LSTM eager pull projection: rank g -> gate g of W4 over Xp.
+static PlanGS gs_lstm_xproj(int h, int d) {
+  PlanGS P = gs_empty();
+  const int zero = 0;
+  for (int g = 0; g < 4; ++g) {
+    RankPlan& R = P.r[g];
+    Bundle b = bundle(0, g * h, 0, 1, &zero, 0, d / BK);
+    b.nmma = 1; b.mma_a[0] = 0; b.mma_b[0] = 0; b.mma_acc[0] = 0;
+    R.b[0] = b; R.nb = 1; R.nacc = 1;
+    P.comb[g][g] = 0;
+  }
+  return P;
+}
+
+// Tree-LSTM backward task: rank g < 3 -> U_g^T dz_g (K = gate g); rank 3 -> U_f^T dz_fk per slot.
+static PlanGS gs_lstm_bwd(int h, int N) {
+  PlanGS P = gs_empty();
+  for (int g = 0; g < 3; ++g) {
+    RankPlan& R = P.r[g];
+    const int bc = g * h;
+    Bundle b = bundle(0, 0, g * h, 1, &bc, 0, h / BK);
+    b.nmma = 1; b.mma_a[0] = 0; b.mma_b[0] = 0; b.mma_acc[0] = 0;
+    R.b[0] = b; R.nb = 1; R.nacc = 1;
+    P.comb[0][g] = 0;
+  }
+  RankPlan& R = P.r[3];
+  int cols[4];
+  for (int k = 0; k < N; ++k) cols[k] = (3 + k) * h;
+  Bundle b = bundle(1, 0, 0, N, cols, 0, h / BK);
+  b.nmma = N;
+  for (int k = 0; k < N; ++k) { b.mma_a[k] = 0; b.mma_b[k] = k; b.mma_acc[k] = k; P.comb[1 + k][3] = k; }
+  R.b[0] = b; R.nb = 1; R.nacc = N;
+  return P;
+}
+
+// Tree-LSTM dX: rank g < 3 -> W_g^T dz_g; rank 3 -> W_f^T sum_k dz_fk (one acc).
+static PlanGS gs_lstm_dx(int h, int N) {
+  PlanGS P = gs_empty();
+  for (int g = 0; g < 3; ++g) {
+    RankPlan& R = P.r[g];
+    const int bc = g * h;
+    Bundle b = bundle(0, 0, g * h, 1, &bc, 0, h / BK);
+    b.nmma = 1; b.mma_a[0] = 0; b.mma_b[0] = 0; b.mma_acc[0] = 0;
+    R.b[0] = b; R.nb = 1; R.nacc = 1;
+    P.comb[0][g] = 0;
+  }
+  RankPlan& R = P.r[3];
+  int cols[4];
+  for (int k = 0; k < N; ++k) cols[k] = (3 + k) * h;
+  Bundle b = bundle(0, 0, 3 * h, N, cols, 0, h / BK);
+  b.nmma = N;
+  for (int k = 0; k < N; ++k) { b.mma_a[k] = 0; b.mma_b[k] = k; b.mma_acc[k] = 0; }
+  R.b[0] = b; R.nb = 1; R.nacc = 1;
+  P.comb[0][3] = 0;
+  return P;
+}
+
+template <int E, int NACC>
+static void launch_gs(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const Dev& D, PlanGS P,
+                      int row_lo, int row_hi, int units, cudaStream_t s) {
+  if (row_hi <= row_lo) return;
+  const int smem = gs_finalize(P);
+  static int attr_set = 0;
+  if (smem > attr_set) {
+    cudaFuncSetAttribute(k_tc_gs<E, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_set = smem;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kCluster * cdiv(units, 128), cdiv(row_hi - row_lo, NT), 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kCluster; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_tc_gs<E, NACC>, a0, a1, b, D, P, row_lo, row_hi, units);
+}
+
 void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
   const int skmax = skinny_max(D);
   if (t->use_simt) { simt_forward<__nv_bfloat16>(D, lp, s, P); return; }
@@ -477,7 +870,9 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
     b.map_a = 0; b.nA = 4; for (int g = 0; g < 4; ++g) b.a_row[g] = g * h; b.a_col0 = 0;
     b.nB = 1; b.b_col[0] = 0; b.sum = 0; b.nk = d / BK;
     b.nmma = 4; for (int g = 0; g < 4; ++g) { b.mma_a[g] = g; b.mma_b[g] = 0; b.mma_acc[g] = g; }
-    launch_I<EPI_LSTM_XPROJ, 4>(t, t->A[1], t->A[1], t->B_xp, D, X, 0, D.V, h, s); P.count(1);
+    if (t->mono) launch_I<EPI_LSTM_XPROJ, 4>(t, t->A[1], t->A[1], t->B_xp, D, X, 0, D.V, h, s);
+    else launch_gs<EPI_LSTM_XPROJ, 4>(t->A[1], t->A[1], t->B_xp, D, gs_lstm_xproj(h, d), 0, D.V, h, s);
+    P.count(1);
     P.mark(CAVS_PH_FWD_LEVELS, s);
     // levels t >= 1: A = U4, B = child slots of the task's rows; h~ formed in smem
     PlanI F{};
@@ -487,12 +882,18 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
     f.nB = N; for (int k = 0; k < N; ++k) f.b_col[k] = k * h;
     f.sum = N >= 2; f.nk = h / BK;
     f.nmma = 3 + N;
-    for (int g = 0; g < 3; ++g) { f.mma_a[g] = g; f.mma_b[g] = N >= 2 ? 3 : 0; f.mma_acc[g] = g; }
+    for (int g = 0; g < 3; ++g) { f.mma_a[g] = g; f.mma_b[g] = N >= 2 ? kC : 0; f.mma_acc[g] = g; }
     for (int k = 0; k < N; ++k) { f.mma_a[3 + k] = 3; f.mma_b[3 + k] = k; f.mma_acc[3 + k] = 3 + k; }
     const SegListI Fs = fwd_segments(D);
+    const PlanGS G = gs_lstm_fwd(h, N);
     for (int tt = 1; tt < T; ++tt) {
       if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_FWD, Fs, lp[tt], lp[tt + 1], h, s);
-      else if (N == 1) launch_I<EPI_LSTM_FWD, 4>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
+      else if (!t->mono) {
+        if (N == 1) launch_gs<EPI_LSTM_FWD, 4>(t->A[0], t->A[0], t->B_hk, D, G, lp[tt], lp[tt + 1], h, s);
+        else if (N == 2) launch_gs<EPI_LSTM_FWD, 5>(t->A[0], t->A[0], t->B_hk, D, G, lp[tt], lp[tt + 1], h, s);
+        else if (N == 3) launch_gs<EPI_LSTM_FWD, 6>(t->A[0], t->A[0], t->B_hk, D, G, lp[tt], lp[tt + 1], h, s);
+        else launch_gs<EPI_LSTM_FWD, 7>(t->A[0], t->A[0], t->B_hk, D, G, lp[tt], lp[tt + 1], h, s);
+      } else if (N == 1) launch_I<EPI_LSTM_FWD, 4>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       else if (N == 2) launch_I<EPI_LSTM_FWD, 5>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       else if (N == 3) launch_I<EPI_LSTM_FWD, 6>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       else launch_I<EPI_LSTM_FWD, 7>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
@@ -502,14 +903,23 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
     PlanI X{};
     X.nb = 1;
     X.b[0] = one(0, 0, 0, 0, d / BK, 0);
-    launch_I<EPI_FC_XPROJ, 1>(t, t->A[1], t->A[1], t->B_xp, D, X, 0, D.V, h, s); P.count(1);
+    if (t->mono) launch_I<EPI_FC_XPROJ, 1>(t, t->A[1], t->A[1], t->B_xp, D, X, 0, D.V, h, s);
+    else {
+      PlanGS G = gs_empty();
+      gs_add_ksplit(G, 0, 0, 0, 0, d, 0);
+      launch_gs<EPI_FC_XPROJ, 1>(t->A[1], t->A[1], t->B_xp, D, G, 0, D.V, h, s);
+    }
+    P.count(1);
     P.mark(CAVS_PH_FWD_LEVELS, s);
     PlanI F{};
     F.nb = 1;
     F.b[0] = one(0, 0, 0, 0, 2 * h / BK, 0);
     const SegListI Fs = fwd_segments(D);
+    PlanGS G = gs_empty();
+    gs_add_ksplit(G, 0, 0, 0, 0, 2 * h, 0);
     for (int tt = 1; tt < T; ++tt) {
       if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_FWD, Fs, lp[tt], lp[tt + 1], h, s);
+      else if (!t->mono) launch_gs<EPI_FC_FWD, 1>(t->A[0], t->A[0], t->B_hk, D, G, lp[tt], lp[tt + 1], h, s);
       else launch_I<EPI_FC_FWD, 1>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       P.count(1);
     }
@@ -549,9 +959,15 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
     B.b[0] = one(0, 0, 0, 0, 3 * h / BK, 0);                          // UTiou x dZ_iou
     for (int k = 0; k < N; ++k) B.b[1 + k] = one(1, 0, 0, (3 + k) * h, h / BK, 1 + k);   // UTf x dZ_fk
     const SegListI Bs = bwd_segments(D);
+    const PlanGS G = gs_lstm_bwd(h, N);
     for (int tt = T - 1; tt >= 1; --tt) {
       if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_BWD, Bs, lp[tt], lp[tt + 1], h, s);
-      else if (N == 1) launch_I<EPI_LSTM_BWD, 2>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
+      else if (!t->mono) {
+        if (N == 1) launch_gs<EPI_LSTM_BWD, 2>(t->A[2], t->A[3], t->B_dz, D, G, lp[tt], lp[tt + 1], h, s);
+        else if (N == 2) launch_gs<EPI_LSTM_BWD, 3>(t->A[2], t->A[3], t->B_dz, D, G, lp[tt], lp[tt + 1], h, s);
+        else if (N == 3) launch_gs<EPI_LSTM_BWD, 4>(t->A[2], t->A[3], t->B_dz, D, G, lp[tt], lp[tt + 1], h, s);
+        else launch_gs<EPI_LSTM_BWD, 5>(t->A[2], t->A[3], t->B_dz, D, G, lp[tt], lp[tt + 1], h, s);
+      } else if (N == 1) launch_I<EPI_LSTM_BWD, 2>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       else if (N == 2) launch_I<EPI_LSTM_BWD, 3>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       else if (N == 3) launch_I<EPI_LSTM_BWD, 4>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       else launch_I<EPI_LSTM_BWD, 5>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
@@ -562,8 +978,11 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
     B.nb = 2;
     for (int k = 0; k < 2; ++k) B.b[k] = one(0, k * h, 0, 0, h / BK, k);   // WcT rows k*h x dZ
     const SegListI Bs = bwd_segments(D);
+    PlanGS G = gs_empty();
+    for (int k = 0; k < 2; ++k) gs_add_ksplit(G, 0, k * h, 0, 0, h, k);
     for (int tt = T - 1; tt >= 1; --tt) {
       if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_BWD, Bs, lp[tt], lp[tt + 1], h, s);
+      else if (!t->mono) launch_gs<EPI_FC_BWD, 2>(t->A[2], t->A[2], t->B_dz, D, G, lp[tt], lp[tt + 1], h, s);
       else launch_I<EPI_FC_BWD, 2>(t, t->A[2], t->A[2], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       P.count(1);
     }
@@ -600,7 +1019,9 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
       PlanI X{};
       X.nb = 1;
       X.b[0] = one(0, 0, 0, 0, G * h / BK, 0);
-      launch_I<EPI_DX, 1>(t, t->A[4], t->A[4], t->B_dz, D, X, 0, V, d, s); P.count(1);
+      if (t->mono) launch_I<EPI_DX, 1>(t, t->A[4], t->A[4], t->B_dz, D, X, 0, V, d, s);
+      else launch_gs<EPI_DX, 1>(t->A[4], t->A[4], t->B_dz, D, gs_lstm_dx(h, N), 0, V, d, s);
+      P.count(1);
     }
   } else {
     float* wc = u4;
@@ -621,7 +1042,13 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
       PlanI X{};
       X.nb = 1;
       X.b[0] = one(0, 0, 0, 0, h / BK, 0);
-      launch_I<EPI_DX, 1>(t, t->A[4], t->A[4], t->B_dz, D, X, 0, V, d, s); P.count(1);
+      if (t->mono) launch_I<EPI_DX, 1>(t, t->A[4], t->A[4], t->B_dz, D, X, 0, V, d, s);
+      else {
+        PlanGS Gx = gs_empty();
+        gs_add_ksplit(Gx, 0, 0, 0, 0, h, 0);
+        launch_gs<EPI_DX, 1>(t->A[4], t->A[4], t->B_dz, D, Gx, 0, V, d, s);
+      }
+      P.count(1);
     }
   }
 }

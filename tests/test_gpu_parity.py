@@ -255,3 +255,16 @@ def test_tcgen05_matches_simt_bf16(case, monkeypatch):
     t = run_gpu(b, "bf16")
     from gpu_harness import compare
     compare(b, t, s, BF16_EMU_TOL, case + " tcgen05 vs simt-bf16")
+
+
+@pytest.mark.parametrize("case", ["tree_lstm_sst_h128_d64", "lstm_chain_h64", "tree_fc_cbt_h64", "tree_lstm_unary_h64"])
+def test_gate_split_cluster_matches_monolithic(case, monkeypatch):
+    """The 4-CTA gate-split cluster kernels against the one-CTA-per-unit-block kernels:
+    identical operands and rounding points, different fp32 summation order only."""
+    b = BF16_CASES[case]()
+    monkeypatch.setenv("CAVS_TC_MONO", "1")
+    m = run_gpu(b, "bf16")
+    monkeypatch.setenv("CAVS_TC_MONO", "0")
+    g = run_gpu(b, "bf16")
+    from gpu_harness import compare
+    compare(b, g, m, 1e-3, case + " gate-split vs monolithic")
