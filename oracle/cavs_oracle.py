@@ -262,16 +262,10 @@ def forward(cell, N, h, d, theta, graph_ptr, child_ptr, child_idx, x_row, x, emu
             hk = [st[c]["h"] for c in ch[v]] + [np.zeros(h)] * (N - len(ch[v]))
             ck = [st[c]["c"] for c in ch[v]] + [np.zeros(h)] * (N - len(ch[v]))
             hkq = [q(a) for a in hk]
-            if emulate_bf16:
-                if N == 1:
-                    hs = hkq[0]
-                else:                  # fp32 running sum of the bf16 slots, then bf16
-                    acc = hkq[0]
-                    for a in hkq[1:]:
-                        acc = f32(acc + a)
-                    hs = q(acc)
-            else:
-                hs = sum(hk)           # h~ = sum_k h_k   (Fig. 5)
+            # h~ = sum_k h_k (Fig. 5).  In bf16 mode the GPU never rounds h~ itself: it
+            # accumulates U h~ as sum_k U bf16(h_k) (reading Z11), i.e. U applied to the exact
+            # sum of the bf16 slots.
+            hs = sum(hkq) if emulate_bf16 else sum(hk)
             i = sigmoid(Pq["W_i"] @ xv + Pq["U_i"] @ hs + P["b_i"])
             f = [sigmoid(Pq["W_f"] @ xv + Pq["U_f"] @ hkq[k] + P["b_f"]) for k in range(N)]
             o = sigmoid(Pq["W_o"] @ xv + Pq["U_o"] @ hs + P["b_o"])

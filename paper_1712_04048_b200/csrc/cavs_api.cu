@@ -78,7 +78,7 @@ static size_t carve(cavs_ctx* c, char* base) {
   D.order = I(V); D.child_pos = I(V * N); D.parent_pos = I(V); D.slot = I(V); D.deg = I(V);
   D.xrow_pos = I(Vp); D.tile_x = I(Vp / 64 + 2);
   D.Hk = take(Vp * N * h * es);
-  D.Hs = (is_lstm(d) && N >= 2) ? (void*)take(Vp * h * es) : nullptr;
+  D.Hs = nullptr;                              // U h~ is accumulated as sum_k U h_k: no h~ arena
   D.Xp = take(Vp * dd * es);
   D.dZ = take(Vp * G * h * es);
   D.Ck = is_lstm(d) ? F(Vp * N * h) : nullptr;

@@ -1,21 +1,22 @@
-// cells.cuh — the vertex function F and its derivative dF as per-(unit j, position p)
-// epilogues, shared by the FP32 (FFMA) and BF16 (tcgen05) level kernels.
+// cells.cuh — the vertex function F and its derivative dF as per-(units j..j+VW-1, position p)
+// epilogues, shared by every level kernel (FFMA tiles, skinny, tcgen05).
 //
 // Tree-LSTM, N-ary child-sum (Fig. 5):
 //   h~ = sum_k h_k; i = s(W_i x + U_i h~ + b_i); f_k = s(W_f x + U_f h_k + b_f);
 //   o = s(W_o x + U_o h~ + b_o); u = tanh(W_u x + U_u h~ + b_u);
 //   c = i*u + sum_k f_k*c_k; h = o*tanh(c); scatter [c,h]; push h.
+//   (U h~ is accumulated as sum_k U h_k by the GEMMs — the same number in exact arithmetic,
+//   reading Z11 of DESIGN.md.)
 // Tree-FC (reading Z7): h = tanh(W_c [h_l; h_r] + W_x x + b).
 // Backward: hand-derived dF (checked by FD in tests/test_oracle_pins.py);
 // gradients flowing to children are written by the unique parent (forests), i.e. the
 // "added" of P:L447 is a plain store because every child has exactly one adder.
 //
-// Every epilogue is split into load() (all global reads of one vertex, into registers)
-// and store() (math + all writes), so a kernel can issue the loads of several vertices
-// before the first store: the reads never alias the writes of the same launch (a task's
-// own rows vs. its parents' / children's rows), and batching them turns a latency chain
-// into memory-level parallelism.  Per-vertex metadata (VMeta) comes from shared memory
-// in the tensor-core kernels.
+// Every epilogue is split into load() (all global reads of one vertex, into registers) and
+// store() (math + all writes), so kernels issue the loads of several vertices before the
+// first store: the reads never alias the writes of the same launch (a task's own rows vs.
+// its parents' / children's rows).  VW consecutive units are handled per call (VW = 4 in
+// the tensor-core kernels: 16-byte accesses); all VW-wide rows are contiguous.
 //
 // Internal gate order of every per-vertex row: (i, o, u, f_1..f_N); weights/bias are
 // repacked to it by k_prep (see ops.cu).
@@ -43,6 +44,39 @@ template <class OpT> __device__ __forceinline__ float act_tanh(float z) {
   else return tanhf(z);
 }
 
+// ---- VW-wide vector helpers (VW in {1, 4}) ----------------------------------------------
+template <int VW> struct FV { float v[VW]; };
+
+template <int VW> __device__ __forceinline__ FV<VW> ldv(const float* p) {
+  FV<VW> r;
+  if constexpr (VW == 4) { const float4 t = *reinterpret_cast<const float4*>(p); r.v[0] = t.x; r.v[1] = t.y; r.v[2] = t.z; r.v[3] = t.w; }
+  else r.v[0] = *p;
+  return r;
+}
+template <int VW> __device__ __forceinline__ void stv(float* p, const FV<VW>& a) {
+  if constexpr (VW == 4) *reinterpret_cast<float4*>(p) = make_float4(a.v[0], a.v[1], a.v[2], a.v[3]);
+  else *p = a.v[0];
+}
+template <class OpT, int VW> __device__ __forceinline__ void stv_op(OpT* p, const FV<VW>& a) {
+  if constexpr (VW == 4 && sizeof(OpT) == 2) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(a.v[0], a.v[1]), hi = __floats2bfloat162_rn(a.v[2], a.v[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&lo);
+    u.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(p) = u;
+  } else if constexpr (VW == 4) {
+    stv<4>(reinterpret_cast<float*>(p), a);
+  } else {
+    *p = to_op<OpT>(a.v[0]);
+  }
+}
+template <int VW> __device__ __forceinline__ FV<VW> zerov() {
+  FV<VW> r;
+#pragma unroll
+  for (int i = 0; i < VW; ++i) r.v[i] = 0.f;
+  return r;
+}
+
 struct VMeta {
   int p, vid, par, slot, deg, xrow;
   int ch[kMaxN], ch_vid[kMaxN], ch_deg[kMaxN];
@@ -65,76 +99,96 @@ __device__ __forceinline__ void load_meta(const Dev& D, int p, bool children, VM
 }
 
 // Per-unit constants (bias in the internal gate order), loaded once per thread.
-struct UnitC { float b0, b1, b2, b3; };
-__device__ __forceinline__ UnitC load_unit(const Dev& D, int j, bool lstm) {
-  UnitC u;
-  if (lstm) { u.b0 = D.bias[j]; u.b1 = D.bias[D.h + j]; u.b2 = D.bias[2 * D.h + j]; u.b3 = D.bias[3 * D.h + j]; }
-  else { u.b0 = D.bias[j]; u.b1 = u.b2 = u.b3 = 0.f; }
+template <int VW> struct UnitC { FV<VW> b0, b1, b2, b3; };
+template <int VW> __device__ __forceinline__ UnitC<VW> load_unit(const Dev& D, int j, bool lstm) {
+  UnitC<VW> u;
+  u.b0 = ldv<VW>(D.bias + j);
+  if (lstm) { u.b1 = ldv<VW>(D.bias + D.h + j); u.b2 = ldv<VW>(D.bias + 2 * D.h + j); u.b3 = ldv<VW>(D.bias + 3 * D.h + j); }
+  else { u.b1 = u.b2 = u.b3 = zerov<VW>(); }
   return u;
 }
 
 // ---- Tree-LSTM helpers -----------------------------------------------------------
-template <class OpT>
-__device__ __forceinline__ void lstm_finish(const Dev& D, int j, const VMeta& m, float zi, float zo, float zu,
-                                            const float* zf, const float* ck) {
+// Finish F at (j.., p) given gate pre-activations (bias included) and the children's c.
+template <class OpT, int VW, int NM>
+__device__ __forceinline__ void lstm_finish(const Dev& D, int j, const VMeta& m, const FV<VW>& zi, const FV<VW>& zo,
+                                            const FV<VW>& zu, const FV<VW>* zf, const FV<VW>* ck) {
   const int h = D.h, N = D.N, G = 3 + N;
-  const float i = act_sig<OpT>(zi), o = act_sig<OpT>(zo), u = act_tanh<OpT>(zu);
-  float c = i * u;
-  float* g = D.gates + (size_t)m.p * G * h;
+  FV<VW> i, o, u, c, hv;
 #pragma unroll
-  for (int k = 0; k < kMaxN; ++k) {
-    if (k >= N) break;
-    const float f = act_sig<OpT>(zf[k]);
-    g[(3 + k) * h + j] = f;
-    if (k < m.deg) c += f * ck[k];               // missing children: c_k = 0 (Z1)
+  for (int e = 0; e < VW; ++e) {
+    i.v[e] = act_sig<OpT>(zi.v[e]); o.v[e] = act_sig<OpT>(zo.v[e]); u.v[e] = act_tanh<OpT>(zu.v[e]);
+    c.v[e] = i.v[e] * u.v[e];
   }
-  const float hv = o * act_tanh<OpT>(c);
-  g[j] = i; g[h + j] = o; g[2 * h + j] = u;
-  D.cst[(size_t)m.p * h + j] = c;
-  D.h_out[(size_t)m.vid * h + j] = hv;           // push(h)
-  if (m.par >= 0) {                              // scatter([c,h]) into the parent's gather slot
+  float* g = D.gates + (size_t)m.p * G * h + j;
+#pragma unroll
+  for (int k = 0; k < NM; ++k) {
+    if (k >= N) break;
+    FV<VW> f;
+#pragma unroll
+    for (int e = 0; e < VW; ++e) {
+      f.v[e] = act_sig<OpT>(zf[k].v[e]);
+      if (k < m.deg) c.v[e] = fmaf(f.v[e], ck[k].v[e], c.v[e]);   // missing children: c_k = 0 (Z1)
+    }
+    stv<VW>(g + (3 + k) * h, f);
+  }
+#pragma unroll
+  for (int e = 0; e < VW; ++e) hv.v[e] = o.v[e] * act_tanh<OpT>(c.v[e]);
+  stv<VW>(g, i); stv<VW>(g + h, o); stv<VW>(g + 2 * h, u);
+  stv<VW>(D.cst + (size_t)m.p * h + j, c);
+  stv<VW>(D.h_out + (size_t)m.vid * h + j, hv);                   // push(h)
+  if (m.par >= 0) {                                                // scatter([c,h]) into the parent's gather slot
     const size_t at = (size_t)m.par * N * h + (size_t)m.slot * h + j;
-    op<OpT>(D.Hk)[at] = to_op<OpT>(hv);
-    D.Ck[at] = c;
+    stv_op<OpT, VW>(op<OpT>(D.Hk) + at, hv);
+    stv<VW>(D.Ck + at, c);
   }
 }
 
-// dF at child c (unit j): inputs already loaded.
-struct LstmChildIn { float dho, i, o, u, cc; float f[kMaxN]; float ck[kMaxN]; };
+// dF at child c (units j..): inputs already loaded.
+template <int VW, int NM> struct LstmChildIn { FV<VW> dho, i, o, u, cc; FV<VW> f[NM]; FV<VW> ck[NM]; };
 
-__device__ __forceinline__ void lstm_child_load(const Dev& D, int j, int c, int c_vid, int c_deg, LstmChildIn& in) {
+template <int VW, int NM>
+__device__ __forceinline__ void lstm_child_load(const Dev& D, int j, int c, int c_vid, int c_deg, LstmChildIn<VW, NM>& in) {
   const int h = D.h, N = D.N, G = 3 + N;
-  const float* g = D.gates + (size_t)c * G * h;
-  in.dho = D.dh_out[(size_t)c_vid * h + j];
-  in.i = g[j]; in.o = g[h + j]; in.u = g[2 * h + j];
-  in.cc = D.cst[(size_t)c * h + j];
-  const float* ck = D.Ck + (size_t)c * N * h;
+  const float* g = D.gates + (size_t)c * G * h + j;
+  in.dho = ldv<VW>(D.dh_out + (size_t)c_vid * h + j);
+  in.i = ldv<VW>(g); in.o = ldv<VW>(g + h); in.u = ldv<VW>(g + 2 * h);
+  in.cc = ldv<VW>(D.cst + (size_t)c * h + j);
+  const float* ck = D.Ck + (size_t)c * N * h + j;
 #pragma unroll
-  for (int k = 0; k < kMaxN; ++k) {
+  for (int k = 0; k < NM; ++k) {
     const bool have = k < c_deg;
-    in.f[k] = have ? g[(3 + k) * h + j] : 0.f;
-    in.ck[k] = have ? ck[k * h + j] : 0.f;
+    in.f[k] = have ? ldv<VW>(g + (3 + k) * h) : zerov<VW>();
+    in.ck[k] = have ? ldv<VW>(ck + k * h) : zerov<VW>();
   }
 }
 
-template <class OpT>
-__device__ __forceinline__ void lstm_child_store(const Dev& D, int j, int c, int c_deg, float dh, float dc,
-                                                 const LstmChildIn& in) {
+template <class OpT, int VW, int NM>
+__device__ __forceinline__ void lstm_child_store(const Dev& D, int j, int c, int c_deg, const FV<VW>& dh,
+                                                 const FV<VW>& dc, const LstmChildIn<VW, NM>& in) {
   const int h = D.h, N = D.N, G = 3 + N;
-  const float tc = act_tanh<OpT>(in.cc);
-  const float dzo = dh * tc * in.o * (1.f - in.o);
-  const float dcb = dc + dh * in.o * (1.f - tc * tc);
-  const float dzi = dcb * in.u * in.i * (1.f - in.i);
-  const float dzu = dcb * in.i * (1.f - in.u * in.u);
-  OpT* dz = op<OpT>(D.dZ) + (size_t)c * G * h;
-  dz[j] = to_op<OpT>(dzi); dz[h + j] = to_op<OpT>(dzo); dz[2 * h + j] = to_op<OpT>(dzu);
+  FV<VW> dzi, dzo, dzu, dcb;
 #pragma unroll
-  for (int k = 0; k < kMaxN; ++k) {
-    if (k >= N) break;
-    const float v = k < c_deg ? dcb * in.ck[k] * in.f[k] * (1.f - in.f[k]) : 0.f;
-    dz[(3 + k) * h + j] = to_op<OpT>(v);
+  for (int e = 0; e < VW; ++e) {
+    const float tc = act_tanh<OpT>(in.cc.v[e]);
+    const float o = in.o.v[e], i = in.i.v[e], u = in.u.v[e];
+    dzo.v[e] = dh.v[e] * tc * o * (1.f - o);
+    dcb.v[e] = dc.v[e] + dh.v[e] * o * (1.f - tc * tc);
+    dzi.v[e] = dcb.v[e] * u * i * (1.f - i);
+    dzu.v[e] = dcb.v[e] * i * (1.f - u * u);
   }
-  D.dcb[(size_t)c * h + j] = dcb;
+  OpT* dz = op<OpT>(D.dZ) + (size_t)c * G * h + j;
+  stv_op<OpT, VW>(dz, dzi); stv_op<OpT, VW>(dz + h, dzo); stv_op<OpT, VW>(dz + 2 * h, dzu);
+#pragma unroll
+  for (int k = 0; k < NM; ++k) {
+    if (k >= N) break;
+    FV<VW> v;
+#pragma unroll
+    for (int e = 0; e < VW; ++e)
+      v.v[e] = k < c_deg ? dcb.v[e] * in.ck[k].v[e] * in.f[k].v[e] * (1.f - in.f[k].v[e]) : 0.f;
+    stv_op<OpT, VW>(dz + (3 + k) * h, v);
+  }
+  stv<VW>(D.dcb + (size_t)c * h + j, dcb);
 }
 
 // ---- epilogue kinds ----------------------------------------------------------------
@@ -142,25 +196,34 @@ template <int E> struct EpiK;
 
 // Level kernel, t >= 1: acc = (U_i h~, U_o h~, U_u h~, U_f h_1..U_f h_N).
 template <> struct EpiK<EPI_LSTM_FWD> {
-  struct In { float ck[kMaxN]; float xi, xo, xu, xf; };
-  static __device__ __forceinline__ void load(const Dev& D, int j, const VMeta& m, In& in) {
+  template <int VW, int NM = kMaxN> struct In { FV<VW> ck[NM]; FV<VW> xi, xo, xu, xf; };
+  template <int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void load(const Dev& D, int j, const VMeta& m, In<VW, NM>& in) {
     const int h = D.h, N = D.N;
-    const float* ck = D.Ck + (size_t)m.p * N * h;
+    const float* ck = D.Ck + (size_t)m.p * N * h + j;
 #pragma unroll
-    for (int k = 0; k < kMaxN; ++k) in.ck[k] = k < m.deg ? ck[k * h + j] : 0.f;
-    in.xi = in.xo = in.xu = in.xf = 0.f;
+    for (int k = 0; k < NM; ++k) in.ck[k] = k < m.deg ? ldv<VW>(ck + k * h) : zerov<VW>();
+    in.xi = in.xo = in.xu = in.xf = zerov<VW>();
     if (m.xrow >= 0) {                           // eager pull projection
-      const float* xw = D.XW + (size_t)m.p * 4 * h;
-      in.xi = xw[j]; in.xo = xw[h + j]; in.xu = xw[2 * h + j]; in.xf = xw[3 * h + j];
+      const float* xw = D.XW + (size_t)m.p * 4 * h + j;
+      in.xi = ldv<VW>(xw); in.xo = ldv<VW>(xw + h); in.xu = ldv<VW>(xw + 2 * h); in.xf = ldv<VW>(xw + 3 * h);
     }
   }
-  template <class OpT>
-  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const float* acc, const In& in,
-                                               const UnitC& b) {
-    float zf[kMaxN];
+  template <class OpT, int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const FV<VW>* acc,
+                                               const In<VW, NM>& in, const UnitC<VW>& b) {
+    FV<VW> zi, zo, zu, zf[NM];
 #pragma unroll
-    for (int k = 0; k < kMaxN; ++k) zf[k] = (k < D.N ? acc[3 + k] : 0.f) + in.xf + b.b3;
-    lstm_finish<OpT>(D, j, m, acc[0] + in.xi + b.b0, acc[1] + in.xo + b.b1, acc[2] + in.xu + b.b2, zf, in.ck);
+    for (int e = 0; e < VW; ++e) {
+      zi.v[e] = acc[0].v[e] + in.xi.v[e] + b.b0.v[e];
+      zo.v[e] = acc[1].v[e] + in.xo.v[e] + b.b1.v[e];
+      zu.v[e] = acc[2].v[e] + in.xu.v[e] + b.b2.v[e];
+    }
+#pragma unroll
+    for (int k = 0; k < NM; ++k)
+#pragma unroll
+      for (int e = 0; e < VW; ++e) zf[k].v[e] = (k < D.N ? acc[3 + k].v[e] : 0.f) + in.xf.v[e] + b.b3.v[e];
+    lstm_finish<OpT, VW, NM>(D, j, m, zi, zo, zu, zf, in.ck);
   }
 };
 
@@ -168,20 +231,28 @@ template <> struct EpiK<EPI_LSTM_FWD> {
 // children, no recurrent term) are finished here; x-vertices above level 0 keep their
 // projection for their own task.
 template <> struct EpiK<EPI_LSTM_XPROJ> {
-  struct In {};
-  static __device__ __forceinline__ void load(const Dev&, int, const VMeta&, In&) {}
-  template <class OpT>
-  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const float* acc, const In&,
-                                               const UnitC& b) {
+  template <int VW, int NM = kMaxN> struct In {};
+  template <int VW, int NM = kMaxN> static __device__ __forceinline__ void load(const Dev&, int, const VMeta&, In<VW, NM>&) {}
+  template <class OpT, int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const FV<VW>* acc,
+                                               const In<VW, NM>&, const UnitC<VW>& b) {
     const int h = D.h;
     if (m.p < D.lp1) {
-      float zf[kMaxN], ck[kMaxN];
+      FV<VW> zi, zo, zu, zf[NM], ck[NM];
 #pragma unroll
-      for (int k = 0; k < kMaxN; ++k) { zf[k] = acc[3] + b.b3; ck[k] = 0.f; }
-      lstm_finish<OpT>(D, j, m, acc[0] + b.b0, acc[1] + b.b1, acc[2] + b.b2, zf, ck);
+      for (int e = 0; e < VW; ++e) {
+        zi.v[e] = acc[0].v[e] + b.b0.v[e]; zo.v[e] = acc[1].v[e] + b.b1.v[e]; zu.v[e] = acc[2].v[e] + b.b2.v[e];
+      }
+#pragma unroll
+      for (int k = 0; k < NM; ++k) {
+        ck[k] = zerov<VW>();
+#pragma unroll
+        for (int e = 0; e < VW; ++e) zf[k].v[e] = acc[3].v[e] + b.b3.v[e];
+      }
+      lstm_finish<OpT, VW, NM>(D, j, m, zi, zo, zu, zf, ck);
     } else if (m.xrow >= 0) {
-      float* xw = D.XW + (size_t)m.p * 4 * h;
-      xw[j] = acc[0]; xw[h + j] = acc[1]; xw[2 * h + j] = acc[2]; xw[3 * h + j] = acc[3];
+      float* xw = D.XW + (size_t)m.p * 4 * h + j;
+      stv<VW>(xw, acc[0]); stv<VW>(xw + h, acc[1]); stv<VW>(xw + 2 * h, acc[2]); stv<VW>(xw + 3 * h, acc[3]);
     }
   }
 };
@@ -190,91 +261,113 @@ template <> struct EpiK<EPI_LSTM_XPROJ> {
 // Gather's adjoint: child k receives dh~ + U_f^T dz_fk (+ its push cotangent) and
 // dc-bar * f_k; then dF of the child runs here (the child's own task needs its dZ).
 template <> struct EpiK<EPI_LSTM_BWD> {
-  struct In { float dcbp; float fp[kMaxN]; LstmChildIn c[kMaxN]; };
-  static __device__ __forceinline__ void load(const Dev& D, int j, const VMeta& m, In& in) {
+  template <int VW, int NM = kMaxN> struct In { FV<VW> dcbp; FV<VW> fp[NM]; LstmChildIn<VW, NM> c[NM]; };
+  template <int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void load(const Dev& D, int j, const VMeta& m, In<VW, NM>& in) {
     const int h = D.h, N = D.N;
-    in.dcbp = D.dcb[(size_t)m.p * h + j];
-    const float* g = D.gates + (size_t)m.p * (3 + N) * h;
+    in.dcbp = ldv<VW>(D.dcb + (size_t)m.p * h + j);
+    const float* g = D.gates + (size_t)m.p * (3 + N) * h + j;
 #pragma unroll
-    for (int k = 0; k < kMaxN; ++k) {
-      in.fp[k] = k < m.deg ? g[(3 + k) * h + j] : 0.f;
-      if (k < m.deg) lstm_child_load(D, j, m.ch[k], m.ch_vid[k], m.ch_deg[k], in.c[k]);
+    for (int k = 0; k < NM; ++k) {
+      in.fp[k] = k < m.deg ? ldv<VW>(g + (3 + k) * h) : zerov<VW>();
+      if (k < m.deg) lstm_child_load<VW, NM>(D, j, m.ch[k], m.ch_vid[k], m.ch_deg[k], in.c[k]);
     }
   }
-  template <class OpT>
-  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const float* acc, const In& in,
-                                               const UnitC&) {
+  template <class OpT, int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const FV<VW>* acc,
+                                               const In<VW, NM>& in, const UnitC<VW>&) {
 #pragma unroll
-    for (int k = 0; k < kMaxN; ++k) {
+    for (int k = 0; k < NM; ++k) {
       if (k >= m.deg) break;
-      const float dh = acc[0] + acc[1 + k] + in.c[k].dho;
-      lstm_child_store<OpT>(D, j, m.ch[k], m.ch_deg[k], dh, in.dcbp * in.fp[k], in.c[k]);
+      FV<VW> dh, dc;
+#pragma unroll
+      for (int e = 0; e < VW; ++e) {
+        dh.v[e] = acc[0].v[e] + acc[1 + k].v[e] + in.c[k].dho.v[e];
+        dc.v[e] = in.dcbp.v[e] * in.fp[k].v[e];
+      }
+      lstm_child_store<OpT, VW, NM>(D, j, m.ch[k], m.ch_deg[k], dh, dc, in.c[k]);
     }
   }
 };
 
 // ---- Tree-FC ------------------------------------------------------------------------
-template <class OpT>
-__device__ __forceinline__ void fc_finish(const Dev& D, int j, const VMeta& m, float z) {
+template <class OpT, int VW>
+__device__ __forceinline__ void fc_finish(const Dev& D, int j, const VMeta& m, const FV<VW>& z) {
   const int h = D.h;
-  const float hv = act_tanh<OpT>(z);
-  D.gates[(size_t)m.p * h + j] = hv;
-  D.h_out[(size_t)m.vid * h + j] = hv;
-  if (m.par >= 0) op<OpT>(D.Hk)[(size_t)m.par * 2 * h + (size_t)m.slot * h + j] = to_op<OpT>(hv);
+  FV<VW> hv;
+#pragma unroll
+  for (int e = 0; e < VW; ++e) hv.v[e] = act_tanh<OpT>(z.v[e]);
+  stv<VW>(D.gates + (size_t)m.p * h + j, hv);
+  stv<VW>(D.h_out + (size_t)m.vid * h + j, hv);
+  if (m.par >= 0) stv_op<OpT, VW>(op<OpT>(D.Hk) + (size_t)m.par * 2 * h + (size_t)m.slot * h + j, hv);
 }
 
 template <> struct EpiK<EPI_FC_FWD> {
-  struct In { float xw; };
-  static __device__ __forceinline__ void load(const Dev& D, int j, const VMeta& m, In& in) {
-    in.xw = m.xrow >= 0 ? D.XW[(size_t)m.p * D.h + j] : 0.f;
+  template <int VW, int NM = kMaxN> struct In { FV<VW> xw; };
+  template <int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void load(const Dev& D, int j, const VMeta& m, In<VW, NM>& in) {
+    in.xw = m.xrow >= 0 ? ldv<VW>(D.XW + (size_t)m.p * D.h + j) : zerov<VW>();
   }
-  template <class OpT>
-  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const float* acc, const In& in,
-                                               const UnitC& b) {
-    fc_finish<OpT>(D, j, m, acc[0] + in.xw + b.b0);
+  template <class OpT, int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const FV<VW>* acc,
+                                               const In<VW, NM>& in, const UnitC<VW>& b) {
+    FV<VW> z;
+#pragma unroll
+    for (int e = 0; e < VW; ++e) z.v[e] = acc[0].v[e] + in.xw.v[e] + b.b0.v[e];
+    fc_finish<OpT, VW>(D, j, m, z);
   }
 };
 
 template <> struct EpiK<EPI_FC_XPROJ> {
-  struct In {};
-  static __device__ __forceinline__ void load(const Dev&, int, const VMeta&, In&) {}
-  template <class OpT>
-  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const float* acc, const In&,
-                                               const UnitC& b) {
-    if (m.p < D.lp1) fc_finish<OpT>(D, j, m, acc[0] + b.b0);
-    else if (m.xrow >= 0) D.XW[(size_t)m.p * D.h + j] = acc[0];
+  template <int VW, int NM = kMaxN> struct In {};
+  template <int VW, int NM = kMaxN> static __device__ __forceinline__ void load(const Dev&, int, const VMeta&, In<VW, NM>&) {}
+  template <class OpT, int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const FV<VW>* acc,
+                                               const In<VW, NM>&, const UnitC<VW>& b) {
+    if (m.p < D.lp1) {
+      FV<VW> z;
+#pragma unroll
+      for (int e = 0; e < VW; ++e) z.v[e] = acc[0].v[e] + b.b0.v[e];
+      fc_finish<OpT, VW>(D, j, m, z);
+    } else if (m.xrow >= 0) {
+      stv<VW>(D.XW + (size_t)m.p * D.h + j, acc[0]);
+    }
   }
 };
 
 // acc[k] = W_{l|r}^T dz  (k = 0: left, 1: right); dz_child = (acc[k] + push cotangent) * (1 - h^2)
 template <> struct EpiK<EPI_FC_BWD> {
-  struct In { float dho[2], hc[2]; };
-  static __device__ __forceinline__ void load(const Dev& D, int j, const VMeta& m, In& in) {
+  template <int VW, int NM = kMaxN> struct In { FV<VW> dho[2], hc[2]; };
+  template <int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void load(const Dev& D, int j, const VMeta& m, In<VW, NM>& in) {
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      in.dho[k] = k < m.deg ? D.dh_out[(size_t)m.ch_vid[k] * D.h + j] : 0.f;
-      in.hc[k] = k < m.deg ? D.gates[(size_t)m.ch[k] * D.h + j] : 0.f;
+      in.dho[k] = k < m.deg ? ldv<VW>(D.dh_out + (size_t)m.ch_vid[k] * D.h + j) : zerov<VW>();
+      in.hc[k] = k < m.deg ? ldv<VW>(D.gates + (size_t)m.ch[k] * D.h + j) : zerov<VW>();
     }
   }
-  template <class OpT>
-  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const float* acc, const In& in,
-                                               const UnitC&) {
+  template <class OpT, int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const FV<VW>* acc,
+                                               const In<VW, NM>& in, const UnitC<VW>&) {
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       if (k >= m.deg) break;
-      op<OpT>(D.dZ)[(size_t)m.ch[k] * D.h + j] = to_op<OpT>((acc[k] + in.dho[k]) * (1.f - in.hc[k] * in.hc[k]));
+      FV<VW> dz;
+#pragma unroll
+      for (int e = 0; e < VW; ++e) dz.v[e] = (acc[k].v[e] + in.dho[k].v[e]) * (1.f - in.hc[k].v[e] * in.hc[k].v[e]);
+      stv_op<OpT, VW>(op<OpT>(D.dZ) + (size_t)m.ch[k] * D.h + j, dz);
     }
   }
 };
 
 // pull's adjoint: dx[record] = W^T dz
 template <> struct EpiK<EPI_DX> {
-  struct In {};
-  static __device__ __forceinline__ void load(const Dev&, int, const VMeta&, In&) {}
-  template <class OpT>
-  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const float* acc, const In&,
-                                               const UnitC&) {
-    if (m.xrow >= 0) D.dx[(size_t)m.xrow * D.d + j] = acc[0];
+  template <int VW, int NM = kMaxN> struct In {};
+  template <int VW, int NM = kMaxN> static __device__ __forceinline__ void load(const Dev&, int, const VMeta&, In<VW, NM>&) {}
+  template <class OpT, int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const FV<VW>* acc,
+                                               const In<VW, NM>&, const UnitC<VW>&) {
+    if (m.xrow >= 0) stv<VW>(D.dx + (size_t)m.xrow * D.d + j, acc[0]);
   }
 };
 
@@ -296,15 +389,27 @@ __device__ __forceinline__ bool row_active(const Dev& D, int p, int xrow) {
   else return true;
 }
 
+// Scalar entry used by the FFMA / skinny kernels: acc has NACC entries.
+template <int E, class OpT, int NACC>
+__device__ __forceinline__ void epilogue1(const Dev& D, int j, const VMeta& m, const float* acc) {
+  const UnitC<1> uc = epi_uses_bias<E>() ? load_unit<1>(D, j, epi_is_lstm<E>()) : UnitC<1>{};
+  FV<1> a[NACC];
+#pragma unroll
+  for (int q = 0; q < NACC; ++q) a[q].v[0] = acc[q];
+  typename EpiK<E>::template In<1, kMaxN> in;
+  EpiK<E>::template load<1, kMaxN>(D, j, m, in);
+  EpiK<E>::template store<OpT, 1, kMaxN>(D, j, m, a, in, uc);
+}
+
 // dF entry at vertices without a parent: only push's adjoint arrives (dh = Gamma, dc = 0).
 template <class OpT>
 __device__ __forceinline__ void root_bwd(const Dev& D, int j, int p) {
   const int vid = D.order[p];
   if (D.cell == CAVS_CELL_TREE_LSTM) {
-    LstmChildIn in;
+    LstmChildIn<1, kMaxN> in;
     const int deg = D.deg[p];
-    lstm_child_load(D, j, p, vid, deg, in);
-    lstm_child_store<OpT>(D, j, p, deg, in.dho, 0.f, in);
+    lstm_child_load<1, kMaxN>(D, j, p, vid, deg, in);
+    lstm_child_store<OpT, 1, kMaxN>(D, j, p, deg, in.dho, zerov<1>(), in);
   } else {
     const float hv = D.gates[(size_t)p * D.h + j];
     op<OpT>(D.dZ)[(size_t)p * D.h + j] = to_op<OpT>(D.dh_out[(size_t)vid * D.h + j] * (1.f - hv * hv));

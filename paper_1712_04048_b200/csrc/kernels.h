@@ -13,7 +13,7 @@ constexpr int kSkinnyMax = 32;    // tasks with at most this many vertices use t
 
 enum Epi : int { EPI_LSTM_FWD = 0, EPI_LSTM_XPROJ, EPI_LSTM_BWD, EPI_FC_FWD, EPI_FC_XPROJ, EPI_FC_BWD, EPI_DX };
 
-enum BSrc : int { B_HK = 0, B_XP = 1, B_DZ = 2, B_HSUM = 3 };
+enum BSrc : int { B_HK = 0, B_XP = 1, B_DZ = 2 };
 
 // One type-I segment: acc[acc] += A[a_row + j, 0:klen] . B[p, b_col : b_col+klen]
 struct SegI {
@@ -21,7 +21,7 @@ struct SegI {
   int b_src; int b_col; int ldb;
   int klen; int acc;
 };
-struct SegListI { int n; SegI s[6]; };
+struct SegListI { int n; SegI s[16]; };
 
 // One type-II segment: out[m, n] += sum_{q in [k_lo,k_hi)} A[q, a_col+m] * B[q, b_col+n]
 struct SegII {

@@ -13,12 +13,6 @@ constexpr int ST = 32;   // tile edge
 
 template <class OpT>
 __device__ __forceinline__ float load_b(const Dev& D, const SegI& s, int p, int k) {
-  if (s.b_src == B_HSUM) {
-    const OpT* hk = reinterpret_cast<const OpT*>(D.Hk) + (size_t)p * D.N * D.h + k;
-    float v = 0.f;
-    for (int q = 0; q < D.N; ++q) v += from_op(hk[q * D.h]);
-    return from_op(to_op<OpT>(v));               // h~ is an operand: rounded like the tensor-core path
-  }
   const OpT* base = reinterpret_cast<const OpT*>(s.b_src == B_HK ? D.Hk : s.b_src == B_XP ? D.Xp : D.dZ);
   return from_op(base[(size_t)p * s.ldb + s.b_col + k]);
 }
@@ -45,7 +39,6 @@ __global__ void __launch_bounds__(256) k_simt_typeI(Dev D, SegListI L, int row_l
     const SegI s = L.s[si];
     const OpT* A = reinterpret_cast<const OpT*>(s.A);
     float t[4] = {0.f, 0.f, 0.f, 0.f};
-    const bool write_hs = (s.b_src == B_HSUM) && blockIdx.x == 0 && D.Hs != nullptr;
     for (int k0 = 0; k0 < s.klen; k0 += ST) {
       for (int e = threadIdx.x; e < ST * ST; e += 256) {
         const int u = e >> 5, k = e & 31;
@@ -53,10 +46,7 @@ __global__ void __launch_bounds__(256) k_simt_typeI(Dev D, SegListI L, int row_l
         As[k][u] = (j < units && k0 + k < s.klen) ? from_op(A[(size_t)(s.a_row + j) * s.lda + k0 + k]) : 0.f;
         const int p = p0 + u;
         float bv = 0.f;
-        if (p < row_hi && k0 + k < s.klen) {
-          bv = load_b<OpT>(D, s, p, k0 + k);
-          if (write_hs) reinterpret_cast<OpT*>(D.Hs)[(size_t)p * D.h + k0 + k] = to_op<OpT>(bv);
-        }
+        if (p < row_hi && k0 + k < s.klen) bv = load_b<OpT>(D, s, p, k0 + k);
         Bs[u][k] = bv;
       }
       __syncthreads();
@@ -76,7 +66,6 @@ __global__ void __launch_bounds__(256) k_simt_typeI(Dev D, SegListI L, int row_l
   }
   const int j = j0 + tx;
   if (j >= units) return;
-  const UnitC uc = epi_uses_bias<E>() ? load_unit(D, j, epi_is_lstm<E>()) : UnitC{0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int p = p0 + ty + 8 * r;
@@ -87,9 +76,7 @@ __global__ void __launch_bounds__(256) k_simt_typeI(Dev D, SegListI L, int row_l
     float v[NACC];
 #pragma unroll
     for (int a = 0; a < NACC; ++a) v[a] = acc[a][r];
-    typename EpiK<E>::In in;
-    EpiK<E>::load(D, j, m, in);
-    EpiK<E>::template store<OpT>(D, j, m, v, in, uc);
+    epilogue1<E, OpT, NACC>(D, j, m, v);
   }
 }
 
@@ -173,9 +160,11 @@ SegListI fwd_segments(const Dev& D) {
   const int h = D.h, N = D.N;
   SegListI F{};
   if (D.cell == CAVS_CELL_TREE_LSTM) {
-    F.n = 3 + N;
-    for (int g = 0; g < 3; ++g) F.s[g] = SegI{D.Wa, h, g * h, N >= 2 ? B_HSUM : B_HK, 0, N * h, h, g};
-    for (int k = 0; k < N; ++k) F.s[3 + k] = SegI{D.Wa, h, 3 * h, B_HK, k * h, N * h, h, 3 + k};
+    // U_g h~ = sum_k U_g h_k (linearity, reading Z11): one segment per (gate, child slot)
+    F.n = 0;
+    for (int g = 0; g < 3; ++g)
+      for (int k = 0; k < N; ++k) F.s[F.n++] = SegI{D.Wa, h, g * h, B_HK, k * h, N * h, h, g};
+    for (int k = 0; k < N; ++k) F.s[F.n++] = SegI{D.Wa, h, 3 * h, B_HK, k * h, N * h, h, 3 + k};
   } else {
     F.n = 1;
     F.s[0] = SegI{D.Wa, 2 * h, 0, B_HK, 0, 2 * h, 2 * h, 0};
@@ -209,9 +198,7 @@ void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
     for (int g = 0; g < 4; ++g) L.s[g] = SegI{D.Wb, d, g * h, B_XP, 0, d, d, g};
     simt_typeI<OpT>(D, EPI_LSTM_XPROJ, L, 0, D.V, h, s); P.count(1);
     P.mark(CAVS_PH_FWD_LEVELS, s);
-    F.n = 3 + N;
-    for (int g = 0; g < 3; ++g) F.s[g] = SegI{D.Wa, h, g * h, N >= 2 ? B_HSUM : B_HK, 0, N * h, h, g};
-    for (int k = 0; k < N; ++k) F.s[3 + k] = SegI{D.Wa, h, 3 * h, B_HK, k * h, N * h, h, 3 + k};
+    F = fwd_segments(D);
     for (int t = 1; t < T; ++t) {
       if (lp[t + 1] - lp[t] <= skmax) skinny_typeI<OpT>(D, EPI_LSTM_FWD, F, lp[t], lp[t + 1], h, s);
       else simt_typeI<OpT>(D, EPI_LSTM_FWD, F, lp[t], lp[t + 1], h, s);
@@ -222,8 +209,7 @@ void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
     L.s[0] = SegI{D.Wb, d, 0, B_XP, 0, d, d, 0};
     simt_typeI<OpT>(D, EPI_FC_XPROJ, L, 0, D.V, h, s); P.count(1);
     P.mark(CAVS_PH_FWD_LEVELS, s);
-    F.n = 1;
-    F.s[0] = SegI{D.Wa, 2 * h, 0, B_HK, 0, 2 * h, 2 * h, 0};
+    F = fwd_segments(D);
     for (int t = 1; t < T; ++t) {
       if (lp[t + 1] - lp[t] <= skmax) skinny_typeI<OpT>(D, EPI_FC_FWD, F, lp[t], lp[t + 1], h, s);
       else simt_typeI<OpT>(D, EPI_FC_FWD, F, lp[t], lp[t + 1], h, s);
@@ -260,8 +246,8 @@ void simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) 
   const LazyLayout Z = lazy_layout(D);
   const int lp1 = D.lp1, V = D.V;
   if (lstm) {
-    SegListII A{}; A.n = 1;
-    A.s[0] = SegII{D.dZ, G * h, 0, N >= 2 ? D.Hs : D.Hk, N >= 2 ? h : N * h, 0, lp1, V, 0};
+    SegListII A{}; A.n = N;                      // dU_iou = sum_k dZ_iou^T H_k
+    for (int k = 0; k < N; ++k) A.s[k] = SegII{D.dZ, G * h, 0, D.Hk, N * h, k * h, lp1, V, 0};
     simt_typeII<OpT>(D, A, D.lazy + Z.u4, 3 * h, h, h, s);
     SegListII Bf{}; Bf.n = N;
     for (int k = 0; k < N; ++k) Bf.s[k] = SegII{D.dZ, G * h, (3 + k) * h, D.Hk, N * h, k * h, lp1, V, 0};

@@ -31,28 +31,28 @@ __device__ __forceinline__ void unpack16(const uint4& u, float* f) {
   }
 }
 
-// Staged operand layout (per vertex row, in OpT): [B source columns 0..W) | h~ (h columns, HSUM)]
+// Staged operand layout (per vertex row, in OpT): the B source columns [0, W).
 template <class OpT, int NACC, int E, int MV>
 __global__ void __launch_bounds__(kSkThreads) k_skinny(Dev D, SegListI L, int row_lo, int row_hi, int units,
-                                                      int bsrc, int W, int ldb, int with_hsum) {
+                                                      int bsrc, int W, int ldb) {
   constexpr int VE = Vec<OpT>::n;
   extern __shared__ __align__(16) uint8_t sk_smem[];
-  const int SW = W + (with_hsum ? D.h : 0);                     // staged row width (elements)
-  OpT* Bs = reinterpret_cast<OpT*>(sk_smem);                    // [MV][SW]
-  float* out = reinterpret_cast<float*>(sk_smem + (size_t)MV * SW * sizeof(OpT));   // [NACC][kUnits][MV]
+  OpT* Bs = reinterpret_cast<OpT*>(sk_smem);                    // [MV][W]
+  float* out = reinterpret_cast<float*>(sk_smem + (size_t)MV * W * sizeof(OpT));   // [NACC][kUnits][MV]
   __shared__ VMeta s_meta[MV];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u0 = blockIdx.x * kUnits;
   const int M = row_hi - row_lo;
+  unsigned long long t_0 = 0, t_1 = 0, t_2 = 0;
+  if (D.trace && threadIdx.x == 0) t_0 = gtime();
   if (threadIdx.x < M) load_meta(D, row_lo + threadIdx.x, epi_needs_children<E>(), s_meta[threadIdx.x]);
-  for (int i = threadIdx.x; i < NACC * kUnits * MV; i += kSkThreads) out[i] = 0.f;
   // ---- stage the task's operand rows: all 16-byte copies in flight at once (cp.async) ----
   {
     const OpT* src = reinterpret_cast<const OpT*>(bsrc == B_HK ? D.Hk : bsrc == B_XP ? D.Xp : D.dZ);
     const int nv = W / VE;
     for (int e = threadIdx.x; e < MV * nv; e += kSkThreads) {
       const int v = e / nv, c = e % nv;
-      OpT* dst = Bs + (size_t)v * SW + c * VE;
+      OpT* dst = Bs + (size_t)v * W + c * VE;
       if (v < M) {
         const OpT* g = src + (size_t)(row_lo + v) * ldb + c * VE;
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
@@ -64,49 +64,39 @@ __global__ void __launch_bounds__(kSkThreads) k_skinny(Dev D, SegListI L, int ro
     asm volatile("cp.async.wait_all;" ::: "memory");
   }
   __syncthreads();
-  if (with_hsum) {                                              // h~ = sum_k h_k, rounded to the operand type
-    const int h = D.h;
-    for (int e = threadIdx.x; e < MV * h; e += kSkThreads) {
-      const int v = e / h, k = e % h;
-      float t = 0.f;
-      for (int q = 0; q < D.N; ++q) t += from_op(Bs[(size_t)v * SW + q * h + k]);
-      const OpT r = to_op<OpT>(t);
-      Bs[(size_t)v * SW + W + k] = r;
-      if (blockIdx.x == 0 && v < M && D.Hs) reinterpret_cast<OpT*>(D.Hs)[(size_t)(row_lo + v) * h + k] = r;
-    }
-    __syncthreads();
-  }
-  // ---- dot products: row = (segment, unit); warps take rows round-robin ----
-  const int nrows = L.n * kUnits;
-  for (int rr = warp; rr < nrows; rr += kSkThreads / 32) {
-    const SegI s = L.s[rr / kUnits];
-    const int r = rr % kUnits, j = u0 + r;
+  if (D.trace && threadIdx.x == 0) t_1 = gtime();
+  // ---- dot products: row = (accumulator, unit); one warp sums all segments of its row ----
+  for (int rr = warp; rr < NACC * kUnits; rr += kSkThreads / 32) {
+    const int acc_id = rr / kUnits, r = rr % kUnits, j = u0 + r;
     if (j >= units) continue;                                   // warp-uniform
-    const OpT* a = reinterpret_cast<const OpT*>(s.A) + (size_t)(s.a_row + j) * s.lda;
-    const int bcol = s.b_src == B_HSUM ? W : s.b_col;
     float acc[MV];
 #pragma unroll
     for (int v = 0; v < MV; ++v) acc[v] = 0.f;
-    constexpr int KMAX = 12;                                    // vectors per lane kept in flight
-    for (int kb = 0; kb < s.klen; kb += 32 * VE * KMAX) {
-      uint4 av[KMAX];
+    for (int si = 0; si < L.n; ++si) {
+      const SegI s = L.s[si];
+      if (s.acc != acc_id) continue;
+      const OpT* a = reinterpret_cast<const OpT*>(s.A) + (size_t)(s.a_row + j) * s.lda;
+      constexpr int KMAX = 12;                                  // vectors per lane kept in flight
+      for (int kb = 0; kb < s.klen; kb += 32 * VE * KMAX) {
+        uint4 av[KMAX];
 #pragma unroll
-      for (int i = 0; i < KMAX; ++i) {
-        const int k = kb + (i * 32 + lane) * VE;
-        av[i] = k < s.klen ? *reinterpret_cast<const uint4*>(a + k) : make_uint4(0, 0, 0, 0);
-      }
+        for (int i = 0; i < KMAX; ++i) {
+          const int k = kb + (i * 32 + lane) * VE;
+          av[i] = k < s.klen ? *reinterpret_cast<const uint4*>(a + k) : make_uint4(0, 0, 0, 0);
+        }
 #pragma unroll
-      for (int i = 0; i < KMAX; ++i) {
-        const int k = kb + (i * 32 + lane) * VE;
-        if (k >= s.klen) break;
-        float w[VE];
-        unpack16<OpT>(av[i], w);
+        for (int i = 0; i < KMAX; ++i) {
+          const int k = kb + (i * 32 + lane) * VE;
+          if (k >= s.klen) break;
+          float w[VE];
+          unpack16<OpT>(av[i], w);
 #pragma unroll
-        for (int v = 0; v < MV; ++v) {
-          float b[VE];
-          unpack16<OpT>(*reinterpret_cast<const uint4*>(Bs + (size_t)v * SW + bcol + k), b);
+          for (int v = 0; v < MV; ++v) {
+            float b[VE];
+            unpack16<OpT>(*reinterpret_cast<const uint4*>(Bs + (size_t)v * W + s.b_col + k), b);
 #pragma unroll
-          for (int e = 0; e < VE; ++e) acc[v] = fmaf(w[e], b[e], acc[v]);
+            for (int e = 0; e < VE; ++e) acc[v] = fmaf(w[e], b[e], acc[v]);
+          }
         }
       }
     }
@@ -115,44 +105,51 @@ __global__ void __launch_bounds__(kSkThreads) k_skinny(Dev D, SegListI L, int ro
       float x = acc[v];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane == 0) atomicAdd(&out[(s.acc * kUnits + r) * MV + v], x);   // smem; segments may share an acc
+      if (lane == 0) out[(acc_id * kUnits + r) * MV + v] = x;
     }
   }
   __syncthreads();
+  if (D.trace && threadIdx.x == 0) t_2 = gtime();
   // ---- fused epilogue: thread -> (unit r, vertex v) ----
   for (int i = threadIdx.x; i < kUnits * M; i += kSkThreads) {
     const int r = i / M, v = i % M;
     const int j = u0 + r;
     const int p = row_lo + v;
     if (j >= units || !row_active<E>(D, p, s_meta[v].xrow)) continue;
-    const UnitC uc = epi_uses_bias<E>() ? load_unit(D, j, epi_is_lstm<E>()) : UnitC{0.f, 0.f, 0.f, 0.f};
     float av[NACC];
 #pragma unroll
     for (int q = 0; q < NACC; ++q) av[q] = out[(q * kUnits + r) * MV + v];
-    typename EpiK<E>::In in;
-    EpiK<E>::load(D, j, s_meta[v], in);
-    EpiK<E>::template store<OpT>(D, j, s_meta[v], av, in, uc);
+    epilogue1<E, OpT, NACC>(D, j, s_meta[v], av);
+  }
+  if (D.trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned long long at = 8 + 8 * atomicAdd(D.trace, 1ull);
+      if (at + 8 < (4u << 20) / 8) {
+        D.trace[at] = 200 + E; D.trace[at + 1] = blockIdx.x; D.trace[at + 2] = row_lo;
+        D.trace[at + 3] = t_0; D.trace[at + 4] = t_1; D.trace[at + 5] = t_2; D.trace[at + 6] = gtime();
+        D.trace[at + 7] = row_hi;
+      }
+    }
   }
 }
 
 template <class OpT, int NACC, int E, int MV>
 static void sk_mv(const Dev& D, const SegListI& L, int row_lo, int row_hi, int units, cudaStream_t s) {
   // staged source: the union of the segments' B columns (all segments of a level kernel read one arena)
-  int bsrc = B_DZ, W = 0, ldb = 0, with_hsum = 0;
+  int bsrc = B_DZ, W = 0, ldb = 0;
   for (int i = 0; i < L.n; ++i) {
     const SegI& g = L.s[i];
-    if (g.b_src == B_HSUM) { with_hsum = 1; bsrc = B_HK; ldb = g.ldb; W = std::max(W, D.N * D.h); }
-    else { bsrc = g.b_src; ldb = g.ldb; W = std::max(W, g.b_col + g.klen); }
+    bsrc = g.b_src; ldb = g.ldb; W = std::max(W, g.b_col + g.klen);
   }
-  const int SW = W + (with_hsum ? D.h : 0);
-  const size_t smem = (size_t)MV * SW * sizeof(OpT) + (size_t)NACC * kUnits * MV * sizeof(float);
+  const size_t smem = (size_t)MV * W * sizeof(OpT) + (size_t)NACC * kUnits * MV * sizeof(float);
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
     cudaFuncSetAttribute(k_skinny<OpT, NACC, E, MV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
   }
   k_skinny<OpT, NACC, E, MV><<<cdiv(units, kUnits), kSkThreads, smem, s>>>(D, L, row_lo, row_hi, units, bsrc, W,
-                                                                            ldb, with_hsum);
+                                                                            ldb);
 }
 
 template <class OpT, int NACC, int E>
@@ -171,7 +168,7 @@ int skinny_max(const Dev& D) {
   if (D.h % ve || D.d % ve) return 0;
   // staged rows must fit shared memory: widest source row (+ h~) x MV operands
   const int G = D.cell == CAVS_CELL_TREE_LSTM ? 3 + D.N : 1;
-  const int W = std::max(D.N * D.h + D.h, G * D.h);
+  const int W = std::max(D.N * D.h, G * D.h);
   int mv = kSkinnyMax;
   while (mv > 4 && (size_t)mv * W * es > 180 * 1024) mv /= 2;
   return mv;

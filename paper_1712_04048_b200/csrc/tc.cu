@@ -3,14 +3,20 @@
 // Type I ("level kernel"): one launch per batching task V_t (Alg. 1).
 //   D[unit j, vertex n] = sum_k A[j, k] * B[n, k]  with A = weights (K-major, TMA),
 //   B = the task's contiguous rows of a position-ordered arena (K-major, TMA) — swap-AB,
-//   so the tensor-core M side (128) is the gate units and the small, ragged task size M_t
-//   is the N side (tile NT = 64).  Several accumulators per CTA (one per gate) live in
-//   TMEM, so the epilogue sees i, o, u, f_1..f_N of the same (unit, vertex) and runs the
-//   whole cell (cells.cuh) — gates, activations, child-sum, scatter, push — fused (§3.5
-//   "automatic kernel fusion", done by hand).  For the child-sum Tree-LSTM the
-//   h~ = sum_k h_k operand is formed in shared memory from the TMA-loaded child slots.
+//   so the tensor-core M side (128) is gate units and the small, ragged task size M_t is
+//   the N side (tile NT = 64).  Accumulators live in TMEM; the epilogue stages them in
+//   shared memory, transposed so one thread owns 4 consecutive units of one vertex, and
+//   runs the whole cell (cells.cuh: gates, activations, child-sum, scatter, push) with
+//   16-byte accesses — §3.5's kernel fusion done by hand across the GEMM.
+//   U h~ = sum_k U h_k is accumulated in TMEM (reading Z11), so no h~ operand is formed.
+//   Two variants:
+//   * CL = 1 (monolithic): one CTA = 128 units x all gates (the large x-projection / dX);
+//   * CL = 4 (gate split): a 4-CTA cluster splits a 128-unit block by gate (forward
+//     i/o/u/f, backward and dX the K columns of each gate), so each CTA streams 1/4 of the
+//     weights; accumulators are exchanged through distributed shared memory and rank r
+//     finishes task columns [16r, 16r+16) (the per-level tasks).
 //   Warp roles: w0 TMA producer, w1 TMEM allocator + single-thread MMA issuer,
-//   w2..w5 child-sum converters, then epilogue (TMEM -> registers -> cell -> HBM).
+//   w2..w9 per-vertex metadata, then epilogue.
 // Type II ("lazy GEMM"): the deferred parameter gradients batched over ALL vertices
 //   (lazy batching): out[m, n] = sum_p A[p, m] B[p, n] with both operands
 //   MN-major straight from the position-ordered arenas, split-K across CTAs.
@@ -28,20 +34,22 @@ constexpr int NT = 64;                     // task-row tile (MMA N) of type I
 constexpr int BK = 64;                     // k-block: one 128-byte swizzle atom of bf16
 constexpr int A_TILE = 128 * BK * 2;       // 16 KB
 constexpr int B_TILE = NT * BK * 2;        // 8 KB
-constexpr int kThreads = 320;              // 10 warps: TMA, MMA, 8 x (converter/metadata + epilogue)
-constexpr int kSmemBudget = 196 * 1024;     // pipeline stages; + static VMeta staging + barriers <= 227 KB
+constexpr int kThreads = 320;              // 10 warps
+constexpr int kSmemBudget = 196 * 1024;    // pipeline stages (+ static metadata <= 227 KB)
+constexpr int kCluster = 4;
 
 struct Bundle {
   int map_a;                 // which A tensor map (0/1)
   int nA; int a_row[4];      // A row offsets (added to the CTA's unit base m0)
   int a_col0;                // A column (k) base
   int nB; int b_col[4];      // B column bases in the arena
-  int sum;                   // C = sum of the nB B tiles (child-sum h~)
   int nk;                    // k-blocks
-  int nmma; int mma_a[6], mma_b[6], mma_acc[6];   // mma_b: 0..3 B tile, kC = the child-sum tile
+  int nmma; int mma_a[8], mma_b[8], mma_acc[8];
 };
-constexpr int kC = 7;
-struct PlanI { int nb; Bundle b[4]; int stages; int stage_bytes; int offB; int offC; };
+struct RankPlan { int nb; Bundle b[3]; int nacc; int stages; int stage_bytes; int offB; };
+// CL = 1: rank 0 only; CL = kCluster: one plan per rank.  comb[e][r] = accumulator of rank r
+// summed into epilogue slot e (-1: none).
+struct PlanT { RankPlan r[kCluster]; int comb[8][kCluster]; int bar_off; };
 
 struct SegT2 { int a_col; int b_col; int k_lo, k_hi; int skip_no_x; };
 struct PlanII { int nseg; SegT2 s[4]; int M, Ncols, ldo; int split; size_t split_stride; int stages; };
@@ -49,34 +57,58 @@ struct PlanII { int nseg; SegT2 s[4]; int M, Ncols, ldo; int split; size_t split
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~(uintptr_t)1023);
 }
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t d;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(saddr), "r"(rank));
+  return d;
+}
+__device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr) : "memory");
+  return v;
+}
 
 // ------------------------------------------------------------------------------------
-template <int E, int NACC>
+// Type-I kernel.  CL = 1 (monolithic) or kCluster (gate split).
+template <int E, int NACC, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
-k_tc_typeI(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
-           const __grid_constant__ CUtensorMap mB, Dev D, PlanI P, int row_lo, int row_hi, int units) {
+k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
+           const __grid_constant__ CUtensorMap mB, Dev D, PlanT P, int row_lo, int row_hi, int units) {
+  constexpr int COLS = NT / CL;                        // task columns finished by this CTA
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  const int S = P.stages;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * P.stage_bytes);
-  uint64_t* empty = full + S;
-  uint64_t* conv = empty + S;
-  uint64_t* done = conv + S;
+  const uint32_t rank = CL > 1 ? cluster_rank() : 0;
+  const RankPlan& R = P.r[rank];
+  const int S = R.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P.bar_off);
+  uint64_t* empty = full + 6;
+  uint64_t* done = empty + 6;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  float* xs = reinterpret_cast<float*>(smem);          // [nacc][NT][128] after the mainloop
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * 128;
+  const int m0 = (blockIdx.x / CL) * 128;
   const int p0 = row_lo + blockIdx.y * NT;
-  __shared__ unsigned long long s_tr[6];
+  const int c_own = (int)rank * COLS;                  // first task column finished here
+  __shared__ VMeta s_meta[COLS];
+  __shared__ unsigned long long s_tr[3];
   if (D.trace && threadIdx.x == 0) s_tr[0] = gtime();
 
-  __shared__ VMeta s_meta[NT];
   if constexpr (E == EPI_LSTM_XPROJ || E == EPI_FC_XPROJ || E == EPI_DX) {
-    bool act = false;
+    bool act = false;                                  // uniform across a cluster (same task tile)
     if (threadIdx.x < NT) { const int p = p0 + threadIdx.x; act = p < row_hi && row_active<E>(D, p, D.xrow_pos[p]); }
     if (!__syncthreads_or(act)) return;
   }
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); ptx::mbar_init(&conv[s], 128); }
+    for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
     ptx::mbar_init(done, 1);
     ptx::fence_mbar_init();
   }
@@ -85,50 +117,51 @@ k_tc_typeI(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (D.trace && threadIdx.x == 0) s_tr[1] = gtime();
 
   if (warp == 0) {
     if (lane == 0) {
       ptx::tma_prefetch(&mA0); ptx::tma_prefetch(&mA1); ptx::tma_prefetch(&mB);
       int step = 0;
-      for (int bi = 0; bi < P.nb; ++bi) {
-        const Bundle& b = P.b[bi];
+      for (int bi = 0; bi < R.nb; ++bi) {
+        const Bundle& b = R.b[bi];
         const CUtensorMap* ma = b.map_a ? &mA1 : &mA0;
         for (int kb = 0; kb < b.nk; ++kb, ++step) {
           const int s = step % S;
           const uint32_t ph = (step / S) & 1;
           ptx::mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* st = smem + s * P.stage_bytes;
+          uint8_t* st = smem + s * R.stage_bytes;
           ptx::mbar_arrive_expect_tx(&full[s], b.nA * A_TILE + b.nB * B_TILE);
           for (int i = 0; i < b.nA; ++i)
             ptx::tma_load_2d(st + i * A_TILE, ma, b.a_col0 + kb * BK, b.a_row[i] + m0, &full[s]);
           for (int i = 0; i < b.nB; ++i)
-            ptx::tma_load_2d(st + P.offB + i * B_TILE, &mB, b.b_col[i] + kb * BK, p0, &full[s]);
+            ptx::tma_load_2d(st + R.offB + i * B_TILE, &mB, b.b_col[i] + kb * BK, p0, &full[s]);
         }
       }
     }
+    __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_bf16(128, NT, 0, 0);
+      uint32_t written = 0;                            // accumulators already initialised
       int step = 0;
-      for (int bi = 0; bi < P.nb; ++bi) {
-        const Bundle& b = P.b[bi];
+      for (int bi = 0; bi < R.nb; ++bi) {
+        const Bundle& b = R.b[bi];
         for (int kb = 0; kb < b.nk; ++kb, ++step) {
           const int s = step % S;
           const uint32_t ph = (step / S) & 1;
           ptx::mbar_wait(&full[s], ph);
-          if (b.sum) ptx::mbar_wait(&conv[s], ph);
           ptx::tc_fence_after();
-          const uint32_t st = ptx::smem_u32(smem + s * P.stage_bytes);
+          const uint32_t st = ptx::smem_u32(smem + s * R.stage_bytes);
           for (int m = 0; m < b.nmma; ++m) {
             const uint32_t a = st + b.mma_a[m] * A_TILE;
-            const uint32_t bb = b.mma_b[m] == kC ? st + P.offC : st + P.offB + b.mma_b[m] * B_TILE;
-            const uint32_t d = tmem + b.mma_acc[m] * NT;
+            const uint32_t bb = st + R.offB + b.mma_b[m] * B_TILE;
+            const int acc = b.mma_acc[m];
+            const uint32_t d = tmem + acc * NT;
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {
+            for (int kk = 0; kk < BK / 16; ++kk)
               ptx::mma_bf16(d, ptx::sdesc_sw128(a + kk * 32, 16, 1024), ptx::sdesc_sw128(bb + kk * 32, 16, 1024),
-                            idesc, (kb > 0 || kk > 0) ? 1u : 0u);
-            }
+                            idesc, ((written >> acc) & 1u) | (kk > 0 ? 1u : 0u));
+            written |= 1u << acc;
           }
           ptx::mma_commit(&empty[s]);
         }
@@ -137,96 +170,82 @@ k_tc_typeI(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
     }
     __syncwarp();
   } else {
-    if (warp < 6) {
-      // ---- child-sum converters (h~ = sum_k h_k into the C tile, same swizzled layout) ----
-      const int ct = threadIdx.x - 64;          // 0..127
-      int step = 0;
-      for (int bi = 0; bi < P.nb; ++bi) {
-        const Bundle& b = P.b[bi];
-        if (!b.sum) { step += b.nk; continue; }
-        for (int kb = 0; kb < b.nk; ++kb, ++step) {
-          const int s = step % S;
-          const uint32_t ph = (step / S) & 1;
-          ptx::mbar_wait(&full[s], ph);
-          uint8_t* st = smem + s * P.stage_bytes;
-          for (int c = ct; c < NT * 8; c += 128) {
-            const int r = c >> 3, q = c & 7;
-            const int off = r * 128 + ((q ^ (r & 7)) << 4);
-            float acc[8];
-            {
-              const uint4 v = *reinterpret_cast<const uint4*>(st + P.offB + off);
-              const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) acc[i] = __bfloat162float(e[i]);
-            }
-            for (int t = 1; t < b.nB; ++t) {
-              const uint4 v = *reinterpret_cast<const uint4*>(st + P.offB + t * B_TILE + off);
-              const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(e[i]);
-            }
-            uint4 o;
-            __nv_bfloat16* oe = reinterpret_cast<__nv_bfloat16*>(&o);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) oe[i] = __float2bfloat16_rn(acc[i]);
-            *reinterpret_cast<uint4*>(st + P.offC + off) = o;
-            const int p = p0 + r;
-            if (m0 == 0 && p < row_hi && D.Hs)     // keep h~ for the lazy dU_iou GEMM
-              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(D.Hs) + (size_t)p * D.h + kb * BK + q * 8) = o;
-          }
-          ptx::fence_proxy_async_smem();
-          ptx::mbar_arrive(&conv[s]);
-        }
-      }
-    } else {
-      // ---- per-vertex metadata into shared memory while the mainloop runs ----
-      const int r = threadIdx.x - 192;
-      if (r < NT && p0 + r < row_hi) load_meta(D, p0 + r, epi_needs_children<E>(), s_meta[r]);
+    // ---- per-vertex metadata of this CTA's columns, while the mainloop runs ----
+    for (int r = threadIdx.x - 64; r < COLS; r += kThreads - 64) {
+      const int p = p0 + c_own + r;
+      if (p < row_hi) load_meta(D, p, epi_needs_children<E>(), s_meta[r]);
     }
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    // ---- epilogue: 2 groups of 4 warps, each group 32 of the NT task rows ----
+    // ---- stage all accumulators in shared memory: xs[a][col][unit] ----
     ptx::mbar_wait(done, 0);
     ptx::tc_fence_after();
-    if (D.trace && threadIdx.x == 64) s_tr[2] = gtime();
-    const int qd = warp & 3;                   // TMEM lane quarter this warp may access
-    const int grp = (warp - 2) >> 2;
-    const int j = m0 + qd * 32 + lane;
+    if (D.trace && threadIdx.x == 64) s_tr[1] = gtime();
+    const int qd = warp & 3, grp = (warp - 2) >> 2;
     const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16);
-    const UnitC uc = (epi_uses_bias<E>() && j < units) ? load_unit(D, j, epi_is_lstm<E>()) : UnitC{0.f, 0.f, 0.f, 0.f};
-    constexpr int CH = epi_needs_children<E>() ? 4 : 8;
-    for (int c0 = grp * 32; c0 < grp * 32 + 32; c0 += CH) {
-      if (p0 + c0 >= row_hi) break;            // warp-uniform
-      float v[NACC][CH];
+    for (int a = 0; a < R.nacc; ++a) {
 #pragma unroll
-      for (int a = 0; a < NACC; ++a) ptx::tmem_ld<CH>(tq + a * NT + c0, v[a]);
-      if (j < units) {
-        typename EpiK<E>::In in[CH];
-        bool ok[CH];
+      for (int c0 = grp * 32; c0 < grp * 32 + 32; c0 += 8) {
+        float v[8];
+        ptx::tmem_ld<8>(tq + a * NT + c0, v);
 #pragma unroll
-        for (int i = 0; i < CH; ++i) {         // all loads of the chunk first ...
-          const int r = c0 + i;
-          ok[i] = p0 + r < row_hi && row_active<E>(D, p0 + r, s_meta[r].xrow);
-          if (ok[i]) EpiK<E>::load(D, j, s_meta[r], in[i]);
-        }
-#pragma unroll
-        for (int i = 0; i < CH; ++i) {         // ... then the math and the stores
-          if (!ok[i]) continue;
-          float acc[NACC];
-#pragma unroll
-          for (int a = 0; a < NACC; ++a) acc[a] = v[a][i];
-          EpiK<E>::template store<__nv_bfloat16>(D, j, s_meta[c0 + i], acc, in[i], uc);
-        }
+        for (int i = 0; i < 8; ++i) xs[((size_t)a * NT + c0 + i) * 128 + qd * 32 + lane] = v[i];
       }
     }
   }
   ptx::tc_fence_before();
+  if constexpr (CL > 1) cluster_sync_all();
+  else __syncthreads();
+  // ---- fused cell epilogue: thread -> (4 consecutive units, columns) ----
+  if (warp >= 2) {
+    const int t = threadIdx.x - 64;                    // 0..255
+    const int uq = t & 31, cg = t >> 5;                // unit quad, column group
+    const int j = m0 + uq * 4;
+    const UnitC<4> uc = (epi_uses_bias<E>() && j < units) ? load_unit<4>(D, j, epi_is_lstm<E>()) : UnitC<4>{};
+    const uint32_t xs_base = ptx::smem_u32(xs) + (uint32_t)(uq * 4) * 4u;
+    constexpr int CPT = COLS / 8;                      // columns per thread
+    constexpr int CH = epi_needs_children<E>() ? 1 : (CPT < 4 ? CPT : 4);
+    // children per vertex the epilogue state is sized for
+    constexpr int NM = E == EPI_LSTM_FWD ? NACC - 3 : E == EPI_LSTM_BWD ? NACC - 1 : 1;
+#pragma unroll 1
+    for (int i0 = 0; i0 < CPT; i0 += CH) {
+      FV<4> acc[CH][NACC];
+      typename EpiK<E>::template In<4, NM> in[CH];
+      bool ok[CH];
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {                   // gather accumulators + all loads first ...
+        const int r = cg + 8 * (i0 + i);               // own column index
+        const int c = c_own + r;                       // column in the task tile
+        const int p = p0 + c;
+        ok[i] = j < units && p < row_hi && row_active<E>(D, p, s_meta[r].xrow);
+        if (!ok[i]) continue;
+#pragma unroll
+        for (int e = 0; e < NACC; ++e) {
+          float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int q = 0; q < CL; ++q) {
+            const int ai = P.comb[e][q];
+            if (ai < 0) continue;
+            float4 x;
+            if constexpr (CL > 1) x = ld_dsmem4(mapa_rank(xs_base + (uint32_t)((ai * NT + c) * 128) * 4u, q));
+            else x = *reinterpret_cast<const float4*>(xs + (size_t)(ai * NT + c) * 128 + uq * 4);
+            sum.x += x.x; sum.y += x.y; sum.z += x.z; sum.w += x.w;
+          }
+          acc[i][e].v[0] = sum.x; acc[i][e].v[1] = sum.y; acc[i][e].v[2] = sum.z; acc[i][e].v[3] = sum.w;
+        }
+        EpiK<E>::template load<4, NM>(D, j, s_meta[r], in[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < CH; ++i)                     // ... then the math and the stores
+        if (ok[i]) EpiK<E>::template store<__nv_bfloat16, 4, NM>(D, j, s_meta[cg + 8 * (i0 + i)], acc[i], in[i], uc);
+    }
+  }
+  if constexpr (CL > 1) cluster_sync_all();            // remote reads done before smem is released
+  ptx::tc_fence_before();
   __syncthreads();
   if (D.trace && threadIdx.x == 0) {
-    const unsigned long long t = gtime();
     const unsigned long long at = 8 + 8 * atomicAdd(D.trace, 1ull);
     if (at + 8 < (4u << 20) / 8) {
-      D.trace[at] = E; D.trace[at + 1] = blockIdx.x + 1000ull * blockIdx.y; D.trace[at + 2] = row_lo;
-      D.trace[at + 3] = s_tr[0]; D.trace[at + 4] = s_tr[1]; D.trace[at + 5] = s_tr[2]; D.trace[at + 6] = t;
+      D.trace[at] = 100 * CL + E; D.trace[at + 1] = blockIdx.x + 1000ull * blockIdx.y; D.trace[at + 2] = row_lo;
+      D.trace[at + 3] = s_tr[0]; D.trace[at + 4] = s_tr[0]; D.trace[at + 5] = s_tr[1]; D.trace[at + 6] = gtime();
       D.trace[at + 7] = row_hi;
     }
   }
@@ -258,7 +277,6 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
   int* s_count = reinterpret_cast<int*>(tmem_slot + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * 128, n0 = blockIdx.y * 128, z = blockIdx.z;
-  // global k-block range of this split
   int nkb_total = 0;
   for (int i = 0; i < P.nseg; ++i) nkb_total += cdiv(P.s[i].k_hi - P.s[i].k_lo, 64);
   const int per = cdiv(nkb_total, P.split);
@@ -300,6 +318,7 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
         }
       }
     }
+    __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_bf16(128, 128, 1, 1);
@@ -355,238 +374,6 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
   }
 }
 
-
-// ------------------------------------------------------------------------------------
-// Gate-split cluster level kernel.  A cluster of 4 CTAs covers one 128-unit block of one
-// 64-row task tile; rank r streams only its gate's weights (forward: U_i / U_o / U_u / U_f;
-// backward and dX: the K columns of gate r), so each CTA pulls ~1/4 of the weights of the
-// monolithic kernel.  After the mainloop every CTA stages its accumulators in its own shared
-// memory, the cluster synchronises, and rank r runs the fused cell epilogue for task columns
-// [16r, 16r+16), reading the other ranks' accumulators through distributed shared memory.
-constexpr int kCluster = 4;
-constexpr int kOwn = NT / kCluster;   // task columns per CTA in the epilogue
-
-struct RankPlan { int nb; Bundle b[3]; int nacc; int stages; int stage_bytes; int offB; int offC; };
-struct PlanGS { RankPlan r[kCluster]; int comb[8][kCluster]; int bar_off; };
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
-  uint32_t d;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(saddr), "r"(rank));
-  return d;
-}
-__device__ __forceinline__ float ld_dsmem(uint32_t addr) {
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
-  return v;
-}
-
-template <int E, int NACC>
-__global__ void __launch_bounds__(kThreads, 1)
-k_tc_gs(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
-        const __grid_constant__ CUtensorMap mB, Dev D, PlanGS P, int row_lo, int row_hi, int units) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = align1024(smem_raw);
-  const uint32_t rank = cluster_rank();
-  const RankPlan& R = P.r[rank];
-  const int S = R.stages;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P.bar_off);
-  uint64_t* empty = full + 6;
-  uint64_t* conv = empty + 6;
-  uint64_t* done = conv + 6;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-  float* xs = reinterpret_cast<float*>(smem);                    // [nacc][NT][128] after the mainloop
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = (blockIdx.x / kCluster) * 128;
-  const int p0 = row_lo + blockIdx.y * NT;
-  __shared__ VMeta s_meta[kOwn];
-
-  if constexpr (E == EPI_LSTM_XPROJ || E == EPI_FC_XPROJ || E == EPI_DX) {
-    bool act = false;                                            // uniform across the cluster
-    if (threadIdx.x < NT) { const int p = p0 + threadIdx.x; act = p < row_hi && row_active<E>(D, p, D.xrow_pos[p]); }
-    if (!__syncthreads_or(act)) return;
-  }
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); ptx::mbar_init(&conv[s], 128); }
-    ptx::mbar_init(done, 1);
-    ptx::fence_mbar_init();
-  }
-  if (warp == 1) ptx::tmem_alloc<256>(tmem_slot);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      ptx::tma_prefetch(&mA0); ptx::tma_prefetch(&mA1); ptx::tma_prefetch(&mB);
-      int step = 0;
-      for (int bi = 0; bi < R.nb; ++bi) {
-        const Bundle& b = R.b[bi];
-        const CUtensorMap* ma = b.map_a ? &mA1 : &mA0;
-        for (int kb = 0; kb < b.nk; ++kb, ++step) {
-          const int s = step % S;
-          const uint32_t ph = (step / S) & 1;
-          ptx::mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* st = smem + s * R.stage_bytes;
-          ptx::mbar_arrive_expect_tx(&full[s], b.nA * A_TILE + b.nB * B_TILE);
-          for (int i = 0; i < b.nA; ++i)
-            ptx::tma_load_2d(st + i * A_TILE, ma, b.a_col0 + kb * BK, b.a_row[i] + m0, &full[s]);
-          for (int i = 0; i < b.nB; ++i)
-            ptx::tma_load_2d(st + R.offB + i * B_TILE, &mB, b.b_col[i] + kb * BK, p0, &full[s]);
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16(128, NT, 0, 0);
-      uint32_t written = 0;                                      // accumulators already initialised
-      int step = 0;
-      for (int bi = 0; bi < R.nb; ++bi) {
-        const Bundle& b = R.b[bi];
-        for (int kb = 0; kb < b.nk; ++kb, ++step) {
-          const int s = step % S;
-          const uint32_t ph = (step / S) & 1;
-          ptx::mbar_wait(&full[s], ph);
-          if (b.sum) ptx::mbar_wait(&conv[s], ph);
-          ptx::tc_fence_after();
-          const uint32_t st = ptx::smem_u32(smem + s * R.stage_bytes);
-          for (int m = 0; m < b.nmma; ++m) {
-            const uint32_t a = st + b.mma_a[m] * A_TILE;
-            const uint32_t bb = b.mma_b[m] == kC ? st + R.offC : st + R.offB + b.mma_b[m] * B_TILE;
-            const int acc = b.mma_acc[m];
-            const uint32_t d = tmem + acc * NT;
-#pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {
-              ptx::mma_bf16(d, ptx::sdesc_sw128(a + kk * 32, 16, 1024), ptx::sdesc_sw128(bb + kk * 32, 16, 1024),
-                            idesc, ((written >> acc) & 1u) | (kk > 0 ? 1u : 0u));
-            }
-            written |= 1u << acc;
-          }
-          ptx::mma_commit(&empty[s]);
-        }
-      }
-      ptx::mma_commit(done);
-    }
-    __syncwarp();
-  } else if (warp < 6) {
-    // ---- child-sum converters ----
-    const int ct = threadIdx.x - 64;
-    int step = 0;
-    for (int bi = 0; bi < R.nb; ++bi) {
-      const Bundle& b = R.b[bi];
-      if (!b.sum) { step += b.nk; continue; }
-      for (int kb = 0; kb < b.nk; ++kb, ++step) {
-        const int s = step % S;
-        const uint32_t ph = (step / S) & 1;
-        ptx::mbar_wait(&full[s], ph);
-        uint8_t* st = smem + s * R.stage_bytes;
-        for (int c = ct; c < NT * 8; c += 128) {
-          const int r = c >> 3, q = c & 7;
-          const int off = r * 128 + ((q ^ (r & 7)) << 4);
-          float acc[8];
-          {
-            const uint4 v = *reinterpret_cast<const uint4*>(st + R.offB + off);
-            const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc[i] = __bfloat162float(e[i]);
-          }
-          for (int t = 1; t < b.nB; ++t) {
-            const uint4 v = *reinterpret_cast<const uint4*>(st + R.offB + t * B_TILE + off);
-            const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(e[i]);
-          }
-          uint4 o;
-          __nv_bfloat16* oe = reinterpret_cast<__nv_bfloat16*>(&o);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) oe[i] = __float2bfloat16_rn(acc[i]);
-          *reinterpret_cast<uint4*>(st + R.offC + off) = o;
-          const int p = p0 + r;
-          if (m0 == 0 && rank == 0 && p < row_hi && D.Hs)        // keep h~ for the lazy dU_iou GEMM
-            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(D.Hs) + (size_t)p * D.h + kb * BK + q * 8) = o;
-        }
-        ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&conv[s]);
-      }
-    }
-  } else {
-    // ---- metadata of this CTA's epilogue columns ----
-    const int r = threadIdx.x - 192;
-    const int p = p0 + (int)rank * kOwn + r;
-    if (r < kOwn && p < row_hi) load_meta(D, p, epi_needs_children<E>(), s_meta[r]);
-  }
-  // ---- stage own accumulators in shared memory ----
-  const int qd = warp & 3;
-  if (warp >= 2) {
-    ptx::mbar_wait(done, 0);
-    ptx::tc_fence_after();
-    const int grp = (warp - 2) >> 2;
-    const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16);
-    for (int a = 0; a < R.nacc; ++a) {
-      for (int c0 = grp * 32; c0 < grp * 32 + 32; c0 += 8) {
-        float v[8];
-        ptx::tmem_ld<8>(tq + a * NT + c0, v);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) xs[((size_t)a * NT + c0 + i) * 128 + qd * 32 + lane] = v[i];
-      }
-    }
-  }
-  ptx::tc_fence_before();
-  cluster_sync_all();
-  // ---- fused epilogue over this CTA's kOwn columns (two groups of 8) ----
-  if (warp >= 2) {
-    const int grp = (warp - 2) >> 2;
-    const int j = m0 + qd * 32 + lane;
-    const UnitC uc = (epi_uses_bias<E>() && j < units) ? load_unit(D, j, epi_is_lstm<E>()) : UnitC{0.f, 0.f, 0.f, 0.f};
-    const uint32_t xs_base = ptx::smem_u32(xs) + (uint32_t)(qd * 32 + lane) * 4u;
-    constexpr int CH = epi_needs_children<E>() ? 2 : 8;        // vertices whose loads are batched
-#pragma unroll 1
-    for (int c0 = 0; c0 < kOwn / 2; c0 += CH) {
-      float acc[CH][NACC];
-      typename EpiK<E>::In in[CH];
-      bool ok[CH];
-#pragma unroll
-      for (int i = 0; i < CH; ++i) {
-        const int r = grp * (kOwn / 2) + c0 + i;               // own-column index
-        const int c = (int)rank * kOwn + r;                    // task column in the tile
-        const int p = p0 + c;
-        ok[i] = j < units && p < row_hi && row_active<E>(D, p, s_meta[r].xrow);
-        if (!ok[i]) continue;
-#pragma unroll
-        for (int e = 0; e < NACC; ++e) {
-          float sum = 0.f;
-#pragma unroll
-          for (int q = 0; q < kCluster; ++q) {
-            const int ai = P.comb[e][q];
-            if (ai >= 0) sum += ld_dsmem(mapa_rank(xs_base + (uint32_t)((ai * NT + c) * 128) * 4u, q));
-          }
-          acc[i][e] = sum;
-        }
-        EpiK<E>::load(D, j, s_meta[r], in[i]);
-      }
-#pragma unroll
-      for (int i = 0; i < CH; ++i)
-        if (ok[i]) EpiK<E>::template store<__nv_bfloat16>(D, j, s_meta[grp * (kOwn / 2) + c0 + i], acc[i], in[i], uc);
-    }
-  }
-  cluster_sync_all();                                          // remote reads done before smem is released
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<256>(tmem);
-  }
-}
-
 // =====================================================================================
 // host side
 // =====================================================================================
@@ -594,9 +381,9 @@ struct TcState {
   // K-major A (weights, box 64 x 128), K-major B (arenas, box 64 x NT), MN-major (box 64 x 64)
   CUtensorMap A[5];
   CUtensorMap B_hk, B_xp, B_dz;
-  CUtensorMap M_dz, M_hs, M_hk, M_xp;
+  CUtensorMap M_dz, M_hk, M_xp;
   bool use_simt = false;
-  bool mono = false;            // CAVS_TC_MONO=1: one CTA per 128-unit block (A/B checks)
+  bool mono = false;            // CAVS_TC_MONO=1: one CTA per 128-unit block for the levels too
 };
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -652,7 +439,6 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
   ok &= encode(&t->M_dz, D.dZ, G * h, Vp, G * h, 64, 64);
   ok &= encode(&t->M_hk, D.Hk, N * h, Vp, N * h, 64, 64);
   ok &= encode(&t->M_xp, D.Xp, d, Vp, d, 64, 64);
-  if (D.Hs) ok &= encode(&t->M_hs, D.Hs, h, Vp, h, 64, 64);
   if (!ok) {
     *err = "cuTensorMapEncodeTiled failed";
     delete t;
@@ -664,68 +450,42 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
 
 void tc_destroy(TcState* tc) { delete tc; }
 
-static int finalize(PlanI& P) {
-  int maxA = 0, maxB = 0, sum = 0;
-  for (int i = 0; i < P.nb; ++i) {
-    maxA = std::max(maxA, P.b[i].nA);
-    maxB = std::max(maxB, P.b[i].nB);
-    sum |= P.b[i].sum;
-  }
-  P.offB = maxA * A_TILE;
-  P.offC = P.offB + maxB * B_TILE;
-  P.stage_bytes = P.offC + (sum ? B_TILE : 0);
-  P.stages = std::max(1, std::min(6, kSmemBudget / P.stage_bytes));
-  return P.stages * P.stage_bytes + 1024 + 3 * 8 * P.stages + 64;
+// ---- type-I plans ---------------------------------------------------------------------
+static PlanT plan_empty() {
+  PlanT P{};
+  for (int e = 0; e < 8; ++e)
+    for (int r = 0; r < kCluster; ++r) P.comb[e][r] = -1;
+  return P;
 }
 
-template <int E, int NACC>
-static void launch_I(const TcState* t, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
-                     const Dev& D, PlanI P, int row_lo, int row_hi, int units, cudaStream_t s) {
-  if (row_hi <= row_lo) return;
-  const int smem = finalize(P);
-  static int attr_set = 0;                     // dynamic + static smem must stay <= 227 KB
-  if (smem > attr_set) {
-    cudaFuncSetAttribute(k_tc_typeI<E, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_set = smem;
-  }
-  dim3 grid(cdiv(units, 128), cdiv(row_hi - row_lo, NT));
-  k_tc_typeI<E, NACC><<<grid, kThreads, smem, s>>>(a0, a1, b, D, P, row_lo, row_hi, units);
-}
-
-static Bundle one(int map_a, int a_row, int a_col0, int b_col, int nk, int acc) {
+static Bundle bundle(int map_a, int nA, const int* a_rows, int a_col0, int nB, const int* b_cols, int nk) {
   Bundle b{};
-  b.map_a = map_a; b.nA = 1; b.a_row[0] = a_row; b.a_col0 = a_col0;
-  b.nB = 1; b.b_col[0] = b_col; b.sum = 0; b.nk = nk;
-  b.nmma = 1; b.mma_a[0] = 0; b.mma_b[0] = 0; b.mma_acc[0] = acc;
+  b.map_a = map_a; b.nA = nA;
+  for (int i = 0; i < nA; ++i) b.a_row[i] = a_rows[i];
+  b.a_col0 = a_col0;
+  b.nB = nB;
+  for (int i = 0; i < nB; ++i) b.b_col[i] = b_cols[i];
+  b.nk = nk;
   return b;
 }
-
-
-
-// ---- gate-split plans ------------------------------------------------------------------
-static Bundle bundle(int map_a, int a_row, int a_col0, int nB, const int* b_cols, int sum, int nk) {
-  Bundle b{};
-  b.map_a = map_a; b.nA = 1; b.a_row[0] = a_row; b.a_col0 = a_col0;
-  b.nB = nB; for (int i = 0; i < nB; ++i) b.b_col[i] = b_cols[i];
-  b.sum = sum; b.nk = nk;
-  return b;
+static void add_mma(Bundle& b, int a, int bt, int acc) {
+  b.mma_a[b.nmma] = a; b.mma_b[b.nmma] = bt; b.mma_acc[b.nmma] = acc; ++b.nmma;
 }
 
-static int gs_finalize(PlanGS& P) {
+static int plan_finalize(PlanT& P, int CL) {
   int pipe = 0, xs = 0;
-  for (int r = 0; r < kCluster; ++r) {
+  for (int r = 0; r < CL; ++r) {
     RankPlan& R = P.r[r];
-    int maxB = 0, sum = 0;
-    for (int i = 0; i < R.nb; ++i) { maxB = std::max(maxB, R.b[i].nB); sum |= R.b[i].sum; }
-    R.offB = A_TILE;
-    R.offC = R.offB + maxB * B_TILE;
-    R.stage_bytes = R.offC + (sum ? B_TILE : 0);
+    int maxA = 1, maxB = 1;
+    for (int i = 0; i < R.nb; ++i) { maxA = std::max(maxA, R.b[i].nA); maxB = std::max(maxB, R.b[i].nB); }
+    R.offB = maxA * A_TILE;
+    R.stage_bytes = R.offB + maxB * B_TILE;
     R.stages = std::max(1, std::min(6, kSmemBudget / R.stage_bytes));
     pipe = std::max(pipe, R.stages * R.stage_bytes);
     xs = std::max(xs, R.nacc * NT * 128 * 4);
   }
   P.bar_off = (std::max(pipe, xs) + 1023) & ~1023;
-  return 1024 + P.bar_off + 3 * 6 * 8 + 16 + 64;
+  return 1024 + P.bar_off + 2 * 6 * 8 + 16 + 64;
 }
 
 // K range [0, nkb) k-blocks split over the cluster ranks (contiguous, balanced).
@@ -735,192 +495,191 @@ static void ksplit(int nkb, int r, int* kb0, int* nk) {
   *nk = q + (r < rem ? 1 : 0);
 }
 
-// all ranks: one bundle over their K share of (A rows a_row, A cols a_col, B cols b_col) -> acc
-static void gs_add_ksplit(PlanGS& P, int map_a, int a_row, int a_col, int b_col, int K, int acc) {
+// gate split: every rank takes its K share of (A rows a_row, A col a_col, B col b_col) -> slot e
+static void gs_add_ksplit(PlanT& P, int map_a, int a_row, int a_col, int b_col, int K, int e) {
   const int nkb = K / BK;
   for (int r = 0; r < kCluster; ++r) {
     int kb0, nk;
     ksplit(nkb, r, &kb0, &nk);
-    RankPlan& R = P.r[r];
     if (nk == 0) continue;
+    RankPlan& R = P.r[r];
     const int bc = b_col + kb0 * BK;
-    Bundle b = bundle(map_a, a_row, a_col + kb0 * BK, 1, &bc, 0, nk);
-    b.nmma = 1; b.mma_a[0] = 0; b.mma_b[0] = 0; b.mma_acc[0] = R.nacc;
+    Bundle b = bundle(map_a, 1, &a_row, a_col + kb0 * BK, 1, &bc, nk);
+    add_mma(b, 0, 0, R.nacc);
     R.b[R.nb++] = b;
-    P.comb[acc][r] = R.nacc;
-    R.nacc++;
+    P.comb[e][r] = R.nacc++;
   }
 }
 
-static PlanGS gs_empty() {
-  PlanGS P{};
-  for (int e = 0; e < 8; ++e) for (int r = 0; r < kCluster; ++r) P.comb[e][r] = -1;
-  return P;
-}
-
-// Tree-LSTM forward task: rank g < 3 -> gate g over h~; rank 3 -> U_f over every child slot.
-static PlanGS gs_lstm_fwd(int h, int N) {
-  PlanGS P = gs_empty();
+// ---- Tree-LSTM, forward task: gate g over every child slot (U h~ = sum_k U h_k) ----
+static PlanT mono_lstm_fwd(int h, int N) {
+  PlanT P = plan_empty();
+  const int rows[4] = {0, h, 2 * h, 3 * h};
   int cols[4];
   for (int k = 0; k < N; ++k) cols[k] = k * h;
-  for (int g = 0; g < 3; ++g) {
-    RankPlan& R = P.r[g];
-    Bundle b = bundle(0, g * h, 0, N, cols, N >= 2, h / BK);
-    b.nmma = 1; b.mma_a[0] = 0; b.mma_b[0] = N >= 2 ? kC : 0; b.mma_acc[0] = 0;
-    R.b[0] = b; R.nb = 1; R.nacc = 1;
-    P.comb[g][g] = 0;
-  }
-  RankPlan& R = P.r[3];
-  Bundle b = bundle(0, 3 * h, 0, N, cols, 0, h / BK);
-  b.nmma = N;
-  for (int k = 0; k < N; ++k) { b.mma_a[k] = 0; b.mma_b[k] = k; b.mma_acc[k] = k; P.comb[3 + k][3] = k; }
-  R.b[0] = b; R.nb = 1; R.nacc = N;
+  Bundle b = bundle(0, 4, rows, 0, N, cols, h / BK);
+  for (int g = 0; g < 3; ++g)
+    for (int k = 0; k < N; ++k) add_mma(b, g, k, g);
+  for (int k = 0; k < N; ++k) add_mma(b, 3, k, 3 + k);
+  RankPlan& R = P.r[0];
+  R.b[0] = b; R.nb = 1; R.nacc = 3 + N;
+  for (int e = 0; e < 3 + N; ++e) P.comb[e][0] = e;
   return P;
 }
-
-// Tree-LSTM eager pull projection: rank g -> gate g of W4 over Xp.
-static PlanGS gs_lstm_xproj(int h, int d) {
-  PlanGS P = gs_empty();
-  const int zero = 0;
+static PlanT gs_lstm_fwd(int h, int N) {
+  PlanT P = plan_empty();
+  int cols[4];
+  for (int k = 0; k < N; ++k) cols[k] = k * h;
   for (int g = 0; g < 4; ++g) {
+    const int row = g * h;
+    Bundle b = bundle(0, 1, &row, 0, N, cols, h / BK);
     RankPlan& R = P.r[g];
-    Bundle b = bundle(0, g * h, 0, 1, &zero, 0, d / BK);
-    b.nmma = 1; b.mma_a[0] = 0; b.mma_b[0] = 0; b.mma_acc[0] = 0;
-    R.b[0] = b; R.nb = 1; R.nacc = 1;
-    P.comb[g][g] = 0;
+    if (g < 3) {
+      for (int k = 0; k < N; ++k) add_mma(b, 0, k, 0);
+      R.nacc = 1;
+      P.comb[g][g] = 0;
+    } else {
+      for (int k = 0; k < N; ++k) { add_mma(b, 0, k, k); P.comb[3 + k][3] = k; }
+      R.nacc = N;
+    }
+    R.b[0] = b; R.nb = 1;
   }
   return P;
 }
-
-// Tree-LSTM backward task: rank g < 3 -> U_g^T dz_g (K = gate g); rank 3 -> U_f^T dz_fk per slot.
-static PlanGS gs_lstm_bwd(int h, int N) {
-  PlanGS P = gs_empty();
-  for (int g = 0; g < 3; ++g) {
-    RankPlan& R = P.r[g];
-    const int bc = g * h;
-    Bundle b = bundle(0, 0, g * h, 1, &bc, 0, h / BK);
-    b.nmma = 1; b.mma_a[0] = 0; b.mma_b[0] = 0; b.mma_acc[0] = 0;
-    R.b[0] = b; R.nb = 1; R.nacc = 1;
-    P.comb[0][g] = 0;
-  }
-  RankPlan& R = P.r[3];
+// ---- Tree-LSTM eager pull projection: gates of W4 over Xp ----
+static PlanT mono_lstm_xproj(int h, int d) {
+  PlanT P = plan_empty();
+  const int rows[4] = {0, h, 2 * h, 3 * h};
+  const int zero = 0;
+  Bundle b = bundle(0, 4, rows, 0, 1, &zero, d / BK);
+  for (int g = 0; g < 4; ++g) { add_mma(b, g, 0, g); P.comb[g][0] = g; }
+  P.r[0].b[0] = b; P.r[0].nb = 1; P.r[0].nacc = 4;
+  return P;
+}
+// ---- Tree-LSTM backward task: slot 0 = U_iou^T dz_iou, slot 1+k = U_f^T dz_fk ----
+static PlanT mono_lstm_bwd(int h, int N) {
+  PlanT P = plan_empty();
+  RankPlan& R = P.r[0];
+  const int zero = 0;
+  R.b[0] = bundle(0, 1, &zero, 0, 1, &zero, 3 * h / BK);
+  add_mma(R.b[0], 0, 0, 0);
   int cols[4];
   for (int k = 0; k < N; ++k) cols[k] = (3 + k) * h;
-  Bundle b = bundle(1, 0, 0, N, cols, 0, h / BK);
-  b.nmma = N;
-  for (int k = 0; k < N; ++k) { b.mma_a[k] = 0; b.mma_b[k] = k; b.mma_acc[k] = k; P.comb[1 + k][3] = k; }
-  R.b[0] = b; R.nb = 1; R.nacc = N;
+  R.b[1] = bundle(1, 1, &zero, 0, N, cols, h / BK);
+  for (int k = 0; k < N; ++k) add_mma(R.b[1], 0, k, 1 + k);
+  R.nb = 2; R.nacc = 1 + N;
+  for (int e = 0; e < 1 + N; ++e) P.comb[e][0] = e;
   return P;
 }
-
-// Tree-LSTM dX: rank g < 3 -> W_g^T dz_g; rank 3 -> W_f^T sum_k dz_fk (one acc).
-static PlanGS gs_lstm_dx(int h, int N) {
-  PlanGS P = gs_empty();
+static PlanT gs_lstm_bwd(int h, int N) {
+  PlanT P = plan_empty();
+  const int zero = 0;
   for (int g = 0; g < 3; ++g) {
-    RankPlan& R = P.r[g];
     const int bc = g * h;
-    Bundle b = bundle(0, 0, g * h, 1, &bc, 0, h / BK);
-    b.nmma = 1; b.mma_a[0] = 0; b.mma_b[0] = 0; b.mma_acc[0] = 0;
-    R.b[0] = b; R.nb = 1; R.nacc = 1;
+    Bundle b = bundle(0, 1, &zero, g * h, 1, &bc, h / BK);
+    add_mma(b, 0, 0, 0);
+    P.r[g].b[0] = b; P.r[g].nb = 1; P.r[g].nacc = 1;
     P.comb[0][g] = 0;
   }
-  RankPlan& R = P.r[3];
   int cols[4];
   for (int k = 0; k < N; ++k) cols[k] = (3 + k) * h;
-  Bundle b = bundle(0, 0, 3 * h, N, cols, 0, h / BK);
-  b.nmma = N;
-  for (int k = 0; k < N; ++k) { b.mma_a[k] = 0; b.mma_b[k] = k; b.mma_acc[k] = 0; }
-  R.b[0] = b; R.nb = 1; R.nacc = 1;
-  P.comb[0][3] = 0;
+  Bundle b = bundle(1, 1, &zero, 0, N, cols, h / BK);
+  for (int k = 0; k < N; ++k) { add_mma(b, 0, k, k); P.comb[1 + k][3] = k; }
+  P.r[3].b[0] = b; P.r[3].nb = 1; P.r[3].nacc = N;
+  return P;
+}
+// ---- Tree-LSTM dX: W^T over dZ (the f blocks of W^T all hold W_f) ----
+static PlanT mono_lstm_dx(int h, int N) {
+  PlanT P = plan_empty();
+  const int zero = 0;
+  Bundle b = bundle(0, 1, &zero, 0, 1, &zero, (3 + N) * h / BK);
+  add_mma(b, 0, 0, 0);
+  P.r[0].b[0] = b; P.r[0].nb = 1; P.r[0].nacc = 1;
+  P.comb[0][0] = 0;
+  return P;
+}
+// ---- single-rank plan: slot e = A rows a_rows[e] x B cols b_cols[e] over K ----
+static PlanT mono_one(int K, int e_count, const int* a_rows, const int* b_cols) {
+  PlanT P = plan_empty();
+  RankPlan& R = P.r[0];
+  for (int e = 0; e < e_count; ++e) {
+    Bundle b = bundle(0, 1, &a_rows[e], 0, 1, &b_cols[e], K / BK);
+    add_mma(b, 0, 0, e);
+    R.b[R.nb++] = b;
+    P.comb[e][0] = e;
+  }
+  R.nacc = e_count;
   return P;
 }
 
-template <int E, int NACC>
-static void launch_gs(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const Dev& D, PlanGS P,
-                      int row_lo, int row_hi, int units, cudaStream_t s) {
+template <int E, int NACC, int CL>
+static void launch_level(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const Dev& D, PlanT P,
+                         int row_lo, int row_hi, int units, cudaStream_t s) {
   if (row_hi <= row_lo) return;
-  const int smem = gs_finalize(P);
-  static int attr_set = 0;
+  const int smem = plan_finalize(P, CL);
+  static int attr_set = 0;                             // dynamic + static smem must stay <= 227 KB
   if (smem > attr_set) {
-    cudaFuncSetAttribute(k_tc_gs<E, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_tc_level<E, NACC, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr_set = smem;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(kCluster * cdiv(units, 128), cdiv(row_hi - row_lo, NT), 1);
+  cfg.gridDim = dim3(CL * cdiv(units, 128), cdiv(row_hi - row_lo, NT), 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = kCluster; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_tc_gs<E, NACC>, a0, a1, b, D, P, row_lo, row_hi, units);
+  cfg.numAttrs = CL > 1 ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k_tc_level<E, NACC, CL>, a0, a1, b, D, P, row_lo, row_hi, units);
+}
+
+// per-task dispatch on the arity N (NACC = BASE + N)
+template <int E, int BASE>
+static void level_N(bool gs, int N, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const Dev& D,
+                    const PlanT& P, int lo, int hi, int units, cudaStream_t s) {
+  switch (N) {
+    case 1: gs ? launch_level<E, BASE + 1, kCluster>(a0, a1, b, D, P, lo, hi, units, s)
+               : launch_level<E, BASE + 1, 1>(a0, a1, b, D, P, lo, hi, units, s); break;
+    case 2: gs ? launch_level<E, BASE + 2, kCluster>(a0, a1, b, D, P, lo, hi, units, s)
+               : launch_level<E, BASE + 2, 1>(a0, a1, b, D, P, lo, hi, units, s); break;
+    case 3: gs ? launch_level<E, BASE + 3, kCluster>(a0, a1, b, D, P, lo, hi, units, s)
+               : launch_level<E, BASE + 3, 1>(a0, a1, b, D, P, lo, hi, units, s); break;
+    default: gs ? launch_level<E, BASE + 4, kCluster>(a0, a1, b, D, P, lo, hi, units, s)
+                : launch_level<E, BASE + 4, 1>(a0, a1, b, D, P, lo, hi, units, s); break;
+  }
 }
 
 void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
   const int skmax = skinny_max(D);
   if (t->use_simt) { simt_forward<__nv_bfloat16>(D, lp, s, P); return; }
   const int h = D.h, d = D.d, N = D.N, T = (int)lp.size() - 1;
+  const bool gs = !t->mono;
+  const SegListI Fs = fwd_segments(D);
+  const int zero = 0;
   if (D.cell == CAVS_CELL_TREE_LSTM) {
-    // eager pull projection + level 0: A = W4 (gates i,o,u,f), B = Xp
-    PlanI X{};
-    X.nb = 1;
-    Bundle& b = X.b[0];
-    b.map_a = 0; b.nA = 4; for (int g = 0; g < 4; ++g) b.a_row[g] = g * h; b.a_col0 = 0;
-    b.nB = 1; b.b_col[0] = 0; b.sum = 0; b.nk = d / BK;
-    b.nmma = 4; for (int g = 0; g < 4; ++g) { b.mma_a[g] = g; b.mma_b[g] = 0; b.mma_acc[g] = g; }
-    if (t->mono) launch_I<EPI_LSTM_XPROJ, 4>(t, t->A[1], t->A[1], t->B_xp, D, X, 0, D.V, h, s);
-    else launch_gs<EPI_LSTM_XPROJ, 4>(t->A[1], t->A[1], t->B_xp, D, gs_lstm_xproj(h, d), 0, D.V, h, s);
+    // eager pull projection fused with task 0 (large: monolithic CTAs reuse the x tile for 4 gates)
+    launch_level<EPI_LSTM_XPROJ, 4, 1>(t->A[1], t->A[1], t->B_xp, D, mono_lstm_xproj(h, d), 0, D.V, h, s);
     P.count(1);
     P.mark(CAVS_PH_FWD_LEVELS, s);
-    // levels t >= 1: A = U4, B = child slots of the task's rows; h~ formed in smem
-    PlanI F{};
-    F.nb = 1;
-    Bundle& f = F.b[0];
-    f.map_a = 0; f.nA = 4; for (int g = 0; g < 4; ++g) f.a_row[g] = g * h; f.a_col0 = 0;
-    f.nB = N; for (int k = 0; k < N; ++k) f.b_col[k] = k * h;
-    f.sum = N >= 2; f.nk = h / BK;
-    f.nmma = 3 + N;
-    for (int g = 0; g < 3; ++g) { f.mma_a[g] = g; f.mma_b[g] = N >= 2 ? kC : 0; f.mma_acc[g] = g; }
-    for (int k = 0; k < N; ++k) { f.mma_a[3 + k] = 3; f.mma_b[3 + k] = k; f.mma_acc[3 + k] = 3 + k; }
-    const SegListI Fs = fwd_segments(D);
-    const PlanGS G = gs_lstm_fwd(h, N);
+    const PlanT F = gs ? gs_lstm_fwd(h, N) : mono_lstm_fwd(h, N);
     for (int tt = 1; tt < T; ++tt) {
       if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_FWD, Fs, lp[tt], lp[tt + 1], h, s);
-      else if (!t->mono) {
-        if (N == 1) launch_gs<EPI_LSTM_FWD, 4>(t->A[0], t->A[0], t->B_hk, D, G, lp[tt], lp[tt + 1], h, s);
-        else if (N == 2) launch_gs<EPI_LSTM_FWD, 5>(t->A[0], t->A[0], t->B_hk, D, G, lp[tt], lp[tt + 1], h, s);
-        else if (N == 3) launch_gs<EPI_LSTM_FWD, 6>(t->A[0], t->A[0], t->B_hk, D, G, lp[tt], lp[tt + 1], h, s);
-        else launch_gs<EPI_LSTM_FWD, 7>(t->A[0], t->A[0], t->B_hk, D, G, lp[tt], lp[tt + 1], h, s);
-      } else if (N == 1) launch_I<EPI_LSTM_FWD, 4>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
-      else if (N == 2) launch_I<EPI_LSTM_FWD, 5>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
-      else if (N == 3) launch_I<EPI_LSTM_FWD, 6>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
-      else launch_I<EPI_LSTM_FWD, 7>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
+      else level_N<EPI_LSTM_FWD, 3>(gs, N, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       P.count(1);
     }
   } else {
-    PlanI X{};
-    X.nb = 1;
-    X.b[0] = one(0, 0, 0, 0, d / BK, 0);
-    if (t->mono) launch_I<EPI_FC_XPROJ, 1>(t, t->A[1], t->A[1], t->B_xp, D, X, 0, D.V, h, s);
-    else {
-      PlanGS G = gs_empty();
-      gs_add_ksplit(G, 0, 0, 0, 0, d, 0);
-      launch_gs<EPI_FC_XPROJ, 1>(t->A[1], t->A[1], t->B_xp, D, G, 0, D.V, h, s);
-    }
+    launch_level<EPI_FC_XPROJ, 1, 1>(t->A[1], t->A[1], t->B_xp, D, mono_one(d, 1, &zero, &zero), 0, D.V, h, s);
     P.count(1);
     P.mark(CAVS_PH_FWD_LEVELS, s);
-    PlanI F{};
-    F.nb = 1;
-    F.b[0] = one(0, 0, 0, 0, 2 * h / BK, 0);
-    const SegListI Fs = fwd_segments(D);
-    PlanGS G = gs_empty();
-    gs_add_ksplit(G, 0, 0, 0, 0, 2 * h, 0);
+    PlanT F;
+    if (gs) { F = plan_empty(); gs_add_ksplit(F, 0, 0, 0, 0, 2 * h, 0); }
+    else F = mono_one(2 * h, 1, &zero, &zero);
     for (int tt = 1; tt < T; ++tt) {
       if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_FWD, Fs, lp[tt], lp[tt + 1], h, s);
-      else if (!t->mono) launch_gs<EPI_FC_FWD, 1>(t->A[0], t->A[0], t->B_hk, D, G, lp[tt], lp[tt + 1], h, s);
-      else launch_I<EPI_FC_FWD, 1>(t, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
+      else if (gs) launch_level<EPI_FC_FWD, 1, kCluster>(t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
+      else launch_level<EPI_FC_FWD, 1, 1>(t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       P.count(1);
     }
   }
@@ -951,103 +710,75 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
   const int h = D.h, d = D.d, N = D.N, T = (int)lp.size() - 1;
   const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
   const int G = lstm ? 3 + N : 1;
+  const bool gs = !t->mono;
+  const SegListI Bs = bwd_segments(D);
   // rows past V of dZ are read by the lazy GEMMs' last k-block: keep them zero
   cudaMemsetAsync(reinterpret_cast<__nv_bfloat16*>(D.dZ) + (size_t)D.V * G * h, 0, (size_t)64 * G * h * 2, s);
   if (lstm) {
-    PlanI B{};
-    B.nb = 1 + N;
-    B.b[0] = one(0, 0, 0, 0, 3 * h / BK, 0);                          // UTiou x dZ_iou
-    for (int k = 0; k < N; ++k) B.b[1 + k] = one(1, 0, 0, (3 + k) * h, h / BK, 1 + k);   // UTf x dZ_fk
-    const SegListI Bs = bwd_segments(D);
-    const PlanGS G = gs_lstm_bwd(h, N);
+    const PlanT B = gs ? gs_lstm_bwd(h, N) : mono_lstm_bwd(h, N);
     for (int tt = T - 1; tt >= 1; --tt) {
       if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_BWD, Bs, lp[tt], lp[tt + 1], h, s);
-      else if (!t->mono) {
-        if (N == 1) launch_gs<EPI_LSTM_BWD, 2>(t->A[2], t->A[3], t->B_dz, D, G, lp[tt], lp[tt + 1], h, s);
-        else if (N == 2) launch_gs<EPI_LSTM_BWD, 3>(t->A[2], t->A[3], t->B_dz, D, G, lp[tt], lp[tt + 1], h, s);
-        else if (N == 3) launch_gs<EPI_LSTM_BWD, 4>(t->A[2], t->A[3], t->B_dz, D, G, lp[tt], lp[tt + 1], h, s);
-        else launch_gs<EPI_LSTM_BWD, 5>(t->A[2], t->A[3], t->B_dz, D, G, lp[tt], lp[tt + 1], h, s);
-      } else if (N == 1) launch_I<EPI_LSTM_BWD, 2>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
-      else if (N == 2) launch_I<EPI_LSTM_BWD, 3>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
-      else if (N == 3) launch_I<EPI_LSTM_BWD, 4>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
-      else launch_I<EPI_LSTM_BWD, 5>(t, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
+      else level_N<EPI_LSTM_BWD, 1>(gs, N, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       P.count(1);
     }
   } else {
-    PlanI B{};
-    B.nb = 2;
-    for (int k = 0; k < 2; ++k) B.b[k] = one(0, k * h, 0, 0, h / BK, k);   // WcT rows k*h x dZ
-    const SegListI Bs = bwd_segments(D);
-    PlanGS G = gs_empty();
-    for (int k = 0; k < 2; ++k) gs_add_ksplit(G, 0, k * h, 0, 0, h, k);
+    PlanT B;
+    const int rows[2] = {0, h}, zeros[2] = {0, 0};
+    if (gs) { B = plan_empty(); for (int k = 0; k < 2; ++k) gs_add_ksplit(B, 0, k * h, 0, 0, h, k); }
+    else B = mono_one(h, 2, rows, zeros);
     for (int tt = T - 1; tt >= 1; --tt) {
       if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_BWD, Bs, lp[tt], lp[tt + 1], h, s);
-      else if (!t->mono) launch_gs<EPI_FC_BWD, 2>(t->A[2], t->A[2], t->B_dz, D, G, lp[tt], lp[tt + 1], h, s);
-      else launch_I<EPI_FC_BWD, 2>(t, t->A[2], t->A[2], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
+      else if (gs) launch_level<EPI_FC_BWD, 2, kCluster>(t->A[2], t->A[2], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
+      else launch_level<EPI_FC_BWD, 2, 1>(t->A[2], t->A[2], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       P.count(1);
     }
   }
   P.mark(CAVS_PH_LAZY, s);
   // ---- lazy batching of the parameter gradients ----
-  const size_t su4 = lstm ? (size_t)3 * h * h : (size_t)2 * h * h;
-  const size_t suf = lstm ? (size_t)h * h : 0;
-  const size_t sw = (size_t)G * h * d;
-  float* u4 = D.lazy;
-  float* uf = u4 + kSplitMax * su4;
-  float* w = uf + kSplitMax * suf;
+  const LazyLayout Z = lazy_layout(D);
+  float* u4 = D.lazy + Z.u4;
+  float* uf = D.lazy + Z.uf;
+  float* w = D.lazy + Z.w;
   const int lp1 = D.lp1, V = D.V;
+  const int zero = 0;
   if (lstm) {
-    PlanII A{};
-    A.nseg = 1;
-    A.s[0] = SegT2{0, 0, lp1, V, 0};
-    A.M = 3 * h; A.Ncols = h; A.ldo = h; A.split_stride = su4;
-    if (lp1 < V) { split[0] = launch_II(t->M_dz, N >= 2 ? t->M_hs : t->M_hk, D, A, u4, s); P.count(1); }
-    else cudaMemsetAsync(u4, 0, sizeof(float) * su4, s);
-    PlanII Bf{};
+    PlanII A{};                                         // dU_iou = sum_k dZ_iou^T H_k  (h~ by linearity)
+    A.nseg = N;
+    for (int k = 0; k < N; ++k) A.s[k] = SegT2{0, k * h, lp1, V, 0};
+    A.M = 3 * h; A.Ncols = h; A.ldo = h; A.split_stride = Z.su4;
+    if (lp1 < V) { split[0] = launch_II(t->M_dz, t->M_hk, D, A, u4, s); P.count(1); }
+    else cudaMemsetAsync(u4, 0, sizeof(float) * Z.su4, s);
+    PlanII Bf{};                                        // dU_f = sum_k dZ_fk^T H_k
     Bf.nseg = N;
     for (int k = 0; k < N; ++k) Bf.s[k] = SegT2{(3 + k) * h, k * h, lp1, V, 0};
-    Bf.M = h; Bf.Ncols = h; Bf.ldo = h; Bf.split_stride = suf;
+    Bf.M = h; Bf.Ncols = h; Bf.ldo = h; Bf.split_stride = Z.suf;
     if (lp1 < V) { split[1] = launch_II(t->M_dz, t->M_hk, D, Bf, uf, s); P.count(1); }
-    else cudaMemsetAsync(uf, 0, sizeof(float) * suf, s);
-    PlanII Cw{};
+    else cudaMemsetAsync(uf, 0, sizeof(float) * Z.suf, s);
+    PlanII Cw{};                                        // dW = dZ^T X over the pull records
     Cw.nseg = 1;
     Cw.s[0] = SegT2{0, 0, 0, V, 1};
-    Cw.M = G * h; Cw.Ncols = d; Cw.ldo = d; Cw.split_stride = sw;
+    Cw.M = G * h; Cw.Ncols = d; Cw.ldo = d; Cw.split_stride = Z.sw;
     split[2] = launch_II(t->M_dz, t->M_xp, D, Cw, w, s); P.count(1);
     P.mark(CAVS_PH_DX, s);
     if (D.dx) {
-      PlanI X{};
-      X.nb = 1;
-      X.b[0] = one(0, 0, 0, 0, G * h / BK, 0);
-      if (t->mono) launch_I<EPI_DX, 1>(t, t->A[4], t->A[4], t->B_dz, D, X, 0, V, d, s);
-      else launch_gs<EPI_DX, 1>(t->A[4], t->A[4], t->B_dz, D, gs_lstm_dx(h, N), 0, V, d, s);
+      launch_level<EPI_DX, 1, 1>(t->A[4], t->A[4], t->B_dz, D, mono_lstm_dx(h, N), 0, V, d, s);
       P.count(1);
     }
   } else {
-    float* wc = u4;
-    float* wx = w;
     PlanII A{};
     A.nseg = 1;
     A.s[0] = SegT2{0, 0, lp1, V, 0};
-    A.M = h; A.Ncols = 2 * h; A.ldo = 2 * h; A.split_stride = su4;
-    if (lp1 < V) { split[0] = launch_II(t->M_dz, t->M_hk, D, A, wc, s); P.count(1); }
-    else cudaMemsetAsync(wc, 0, sizeof(float) * su4, s);
+    A.M = h; A.Ncols = 2 * h; A.ldo = 2 * h; A.split_stride = Z.su4;
+    if (lp1 < V) { split[0] = launch_II(t->M_dz, t->M_hk, D, A, u4, s); P.count(1); }
+    else cudaMemsetAsync(u4, 0, sizeof(float) * Z.su4, s);
     PlanII Cw{};
     Cw.nseg = 1;
     Cw.s[0] = SegT2{0, 0, 0, V, 1};
-    Cw.M = h; Cw.Ncols = d; Cw.ldo = d; Cw.split_stride = (size_t)h * d;
-    split[2] = launch_II(t->M_dz, t->M_xp, D, Cw, wx, s); P.count(1);
+    Cw.M = h; Cw.Ncols = d; Cw.ldo = d; Cw.split_stride = Z.sw;
+    split[2] = launch_II(t->M_dz, t->M_xp, D, Cw, w, s); P.count(1);
     P.mark(CAVS_PH_DX, s);
     if (D.dx) {
-      PlanI X{};
-      X.nb = 1;
-      X.b[0] = one(0, 0, 0, 0, h / BK, 0);
-      if (t->mono) launch_I<EPI_DX, 1>(t, t->A[4], t->A[4], t->B_dz, D, X, 0, V, d, s);
-      else {
-        PlanGS Gx = gs_empty();
-        gs_add_ksplit(Gx, 0, 0, 0, 0, h, 0);
-        launch_gs<EPI_DX, 1>(t->A[4], t->A[4], t->B_dz, D, Gx, 0, V, d, s);
-      }
+      launch_level<EPI_DX, 1, 1>(t->A[4], t->A[4], t->B_dz, D, mono_one(h, 1, &zero, &zero), 0, V, d, s);
       P.count(1);
     }
   }

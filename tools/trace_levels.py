@@ -9,8 +9,8 @@ b = gen.make_config_batch(sys.argv[1] if len(sys.argv) > 1 else "cfg4", seed=0)
 dev = torch.device("cuda", 0)
 t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
 ctx = Context(b.cell, b.N, b.h, b.d, precision="bf16", max_graphs=b.K, max_vertices=b.V, max_x=b.n_x)
-for it in range(3):
-    ws = ctx.workspace[ctx._ws_off + ctx._ws_bytes - (4 << 20): ctx._ws_off + ctx._ws_bytes]
+ws = ctx.workspace[ctx._ws_off + ctx._ws_bytes - (4 << 20): ctx._ws_off + ctx._ws_bytes]
+for it in range(20):
     torch.cuda.synchronize()
     ws.zero_()
     ctx.load_graphs(t(b.graph_ptr), t(b.child_ptr), t(b.child_idx)); ctx.schedule()
@@ -21,7 +21,15 @@ n = tail[0]
 rec = tail[8:8 + 8 * n].reshape(n, 8)
 t0 = rec[:, 3].min()
 print("records", n)
-print("kind block row_lo rows | start setup(us) done(us) end(us) | since first start")
-for r in rec[np.argsort(rec[:, 3])][:400]:
-    print(r[0], r[1], r[2], r[7] - r[2], "|", "%.2f %.2f %.2f" % ((r[4] - r[3]) / 1e3, (r[5] - r[3]) / 1e3, (r[6] - r[3]) / 1e3),
-          "| %.2f" % ((r[3] - t0) / 1e3))
+# per launch (kind, row_lo): CTAs, first start, last end, max per-CTA phase times
+import collections
+L = collections.OrderedDict()
+for r in rec[np.argsort(rec[:, 3])]:
+    L.setdefault((int(r[0]), int(r[2]), int(r[7])), []).append(r)
+print("kind row_lo rows ctas | launch_us | max setup / done / end per CTA (us) | start since t0 (us)")
+for (k, lo, hi), rs in L.items():
+    rs = np.array(rs)
+    st, en = rs[:, 3].min(), rs[:, 6].max()
+    print(k, lo, hi - lo, len(rs), "| %.2f |" % ((en - st) / 1e3),
+          "%.2f %.2f %.2f" % (((rs[:, 4] - rs[:, 3]).max()) / 1e3, ((rs[:, 5] - rs[:, 3]).max()) / 1e3,
+                              ((rs[:, 6] - rs[:, 3]).max()) / 1e3), "| %.2f" % ((st - t0) / 1e3))
