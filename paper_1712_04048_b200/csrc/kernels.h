@@ -9,7 +9,7 @@ namespace cavs {
 constexpr int kMaxN = 4;          // max arity supported by the kernels
 constexpr int kDbChunks = 32;     // row chunks of the deterministic db column reduction
 constexpr int kSplitMax = 8;      // max split-K of the lazy tensor-core GEMMs
-constexpr int kSkinnyMax = 32;    // tasks with at most this many vertices use the skinny level kernel
+constexpr int kSkinnyMax = 8;     // tasks with at most this many vertices use the skinny level kernel
 
 enum Epi : int { EPI_LSTM_FWD = 0, EPI_LSTM_XPROJ, EPI_LSTM_BWD, EPI_FC_FWD, EPI_FC_XPROJ, EPI_FC_BWD, EPI_DX };
 

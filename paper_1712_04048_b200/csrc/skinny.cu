@@ -46,6 +46,8 @@ __global__ void __launch_bounds__(kSkThreads) k_skinny(Dev D, SegListI L, int ro
   unsigned long long t_0 = 0, t_1 = 0, t_2 = 0;
   if (D.trace && threadIdx.x == 0) t_0 = gtime();
   if (threadIdx.x < M) load_meta(D, row_lo + threadIdx.x, epi_needs_children<E>(), s_meta[threadIdx.x]);
+  asm volatile("griddepcontrol.wait;" ::: "memory");          // PDL: previous task complete + visible
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // ---- stage the task's operand rows: all 16-byte copies in flight at once (cp.async) ----
   {
     const OpT* src = reinterpret_cast<const OpT*>(bsrc == B_HK ? D.Hk : bsrc == B_XP ? D.Xp : D.dZ);
@@ -148,8 +150,17 @@ static void sk_mv(const Dev& D, const SegListI& L, int row_lo, int row_hi, int u
     cudaFuncSetAttribute(k_skinny<OpT, NACC, E, MV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
   }
-  k_skinny<OpT, NACC, E, MV><<<cdiv(units, kUnits), kSkThreads, smem, s>>>(D, L, row_lo, row_hi, units, bsrc, W,
-                                                                            ldb);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cdiv(units, kUnits), 1, 1);
+  cfg.blockDim = dim3(kSkThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL: overlap with the previous task
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_skinny<OpT, NACC, E, MV>, D, L, row_lo, row_hi, units, bsrc, W, ldb);
 }
 
 template <class OpT, int NACC, int E>

@@ -121,6 +121,22 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
   if (warp == 0) {
     if (lane == 0) {
       ptx::tma_prefetch(&mA0); ptx::tma_prefetch(&mA1); ptx::tma_prefetch(&mB);
+      // Weight tiles of the first S stages do not depend on the previous task: under PDL they
+      // stream in while the previous task's kernel is still finishing.
+      int pre = 0;
+      for (int bi = 0, step = 0; bi < R.nb && step < S; ++bi) {
+        const Bundle& b = R.b[bi];
+        const CUtensorMap* ma = b.map_a ? &mA1 : &mA0;
+        for (int kb = 0; kb < b.nk && step < S; ++kb, ++step) {
+          uint8_t* st = smem + step * R.stage_bytes;
+          ptx::mbar_arrive_expect_tx(&full[step], b.nA * A_TILE + b.nB * B_TILE);
+          for (int i = 0; i < b.nA; ++i)
+            ptx::tma_load_2d(st + i * A_TILE, ma, b.a_col0 + kb * BK, b.a_row[i] + m0, &full[step]);
+          pre = step + 1;
+        }
+      }
+      ptx::griddep_wait();                             // the task's operand rows are now final
+      ptx::griddep_launch();
       int step = 0;
       for (int bi = 0; bi < R.nb; ++bi) {
         const Bundle& b = R.b[bi];
@@ -128,11 +144,13 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
         for (int kb = 0; kb < b.nk; ++kb, ++step) {
           const int s = step % S;
           const uint32_t ph = (step / S) & 1;
-          ptx::mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * R.stage_bytes;
-          ptx::mbar_arrive_expect_tx(&full[s], b.nA * A_TILE + b.nB * B_TILE);
-          for (int i = 0; i < b.nA; ++i)
-            ptx::tma_load_2d(st + i * A_TILE, ma, b.a_col0 + kb * BK, b.a_row[i] + m0, &full[s]);
+          if (step >= pre) {
+            ptx::mbar_wait(&empty[s], ph ^ 1);
+            ptx::mbar_arrive_expect_tx(&full[s], b.nA * A_TILE + b.nB * B_TILE);
+            for (int i = 0; i < b.nA; ++i)
+              ptx::tma_load_2d(st + i * A_TILE, ma, b.a_col0 + kb * BK, b.a_row[i] + m0, &full[s]);
+          }
           for (int i = 0; i < b.nB; ++i)
             ptx::tma_load_2d(st + R.offB + i * B_TILE, &mB, b.b_col[i] + kb * BK, p0, &full[s]);
         }
@@ -178,6 +196,7 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
     // ---- stage all accumulators in shared memory: xs[a][col][unit] ----
     ptx::mbar_wait(done, 0);
     ptx::tc_fence_after();
+    ptx::griddep_wait();                               // (already satisfied: orders the epilogue's reads)
     if (D.trace && threadIdx.x == 64) s_tr[1] = gtime();
     const int qd = warp & 3, grp = (warp - 2) >> 2;
     const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16);
@@ -630,8 +649,14 @@ static void launch_level(const CUtensorMap& a0, const CUtensorMap& a1, const CUt
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = CL > 1 ? 1 : 0;
+  cudaLaunchAttribute at2[2];
+  int na = 0;
+  if (CL > 1) at2[na++] = at[0];
+  at2[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL: overlap with the previous task
+  at2[na].val.programmaticStreamSerializationAllowed = 1;
+  ++na;
+  cfg.attrs = at2;
+  cfg.numAttrs = na;
   cudaLaunchKernelEx(&cfg, k_tc_level<E, NACC, CL>, a0, a1, b, D, P, row_lo, row_hi, units);
 }
 
