@@ -121,40 +121,8 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
   if (warp == 0) {
     if (lane == 0) {
       ptx::tma_prefetch(&mA0); ptx::tma_prefetch(&mA1); ptx::tma_prefetch(&mB);
-      // Weight tiles of the first S stages do not depend on the previous task: under PDL they
-      // stream in while the previous task's kernel is still finishing.
-      int pre = 0;
-      for (int bi = 0, step = 0; bi < R.nb && step < S; ++bi) {
-        const Bundle& b = R.b[bi];
-        const CUtensorMap* ma = b.map_a ? &mA1 : &mA0;
-        for (int kb = 0; kb < b.nk && step < S; ++kb, ++step) {
-          uint8_t* st = smem + step * R.stage_bytes;
-          ptx::mbar_arrive_expect_tx(&full[step], b.nA * A_TILE + b.nB * B_TILE);
-          for (int i = 0; i < b.nA; ++i)
-            ptx::tma_load_2d(st + i * A_TILE, ma, b.a_col0 + kb * BK, b.a_row[i] + m0, &full[step]);
-          pre = step + 1;
-        }
-      }
-      ptx::griddep_wait();                             // the task's operand rows are now final
-      ptx::griddep_launch();
-      int step = 0;
-      for (int bi = 0; bi < R.nb; ++bi) {
-        const Bundle& b = R.b[bi];
-        const CUtensorMap* ma = b.map_a ? &mA1 : &mA0;
-        for (int kb = 0; kb < b.nk; ++kb, ++step) {
-          const int s = step % S;
-          const uint32_t ph = (step / S) & 1;
-          uint8_t* st = smem + s * R.stage_bytes;
-          if (step >= pre) {
-            ptx::mbar_wait(&empty[s], ph ^ 1);
-            ptx::mbar_arrive_expect_tx(&full[s], b.nA * A_TILE + b.nB * B_TILE);
-            for (int i = 0; i < b.nA; ++i)
-              ptx::tma_load_2d(st + i * A_TILE, ma, b.a_col0 + kb * BK, b.a_row[i] + m0, &full[s]);
-          }
-          for (int i = 0; i < b.nB; ++i)
-            ptx::tma_load_2d(st + R.offB + i * B_TILE, &mB, b.b_col[i] + kb * BK, p0, &full[s]);
-        }
-      }
+      ptx::griddep_wait();
+      ptx::griddep_launch();                           // PDL: let the next task's CTAs start their prologue
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -188,11 +156,38 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
     }
     __syncwarp();
   } else {
-    // ---- per-vertex metadata of this CTA's columns, while the mainloop runs ----
-    for (int r = threadIdx.x - 64; r < COLS; r += kThreads - 64) {
-      const int p = p0 + c_own + r;
-      if (p < row_hi) load_meta(D, p, epi_needs_children<E>(), s_meta[r]);
+    if (lane == 0) {
+      // ---- TMA issue, spread over 8 warps (a single issuing thread serialises its boxes) ----
+      // Step st goes to warp 2 + st % 8.  Weight (A) tiles do not depend on the previous task, so
+      // under PDL they stream in before griddepcontrol.wait; the task's rows (B) after it.
+      const int w = warp - 2;
+      bool waited = false;
+      int step = 0;
+      for (int bi = 0; bi < R.nb; ++bi) {
+        const Bundle& b = R.b[bi];
+        const CUtensorMap* ma = b.map_a ? &mA1 : &mA0;
+        for (int kb = 0; kb < b.nk; ++kb, ++step) {
+          if ((step & 7) != w) continue;
+          const int s = step % S;
+          const uint32_t ph = (step / S) & 1;
+          uint8_t* st = smem + s * R.stage_bytes;
+          if (step >= S) ptx::mbar_wait(&empty[s], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[s], b.nA * A_TILE + b.nB * B_TILE);
+          for (int i = 0; i < b.nA; ++i)
+            ptx::tma_load_2d(st + i * A_TILE, ma, b.a_col0 + kb * BK, b.a_row[i] + m0, &full[s]);
+          if (!waited) { ptx::griddep_wait(); waited = true; }
+          for (int i = 0; i < b.nB; ++i)
+            ptx::tma_load_2d(st + R.offB + i * B_TILE, &mB, b.b_col[i] + kb * BK, p0, &full[s]);
+        }
+      }
+    } else {
+      // ---- per-vertex metadata of this CTA's columns, meanwhile (lanes 1..31) ----
+      for (int r = (warp - 2) * 31 + lane - 1; r < COLS; r += 8 * 31) {
+        const int p = p0 + c_own + r;
+        if (p < row_hi) load_meta(D, p, epi_needs_children<E>(), s_meta[r]);
+      }
     }
+    __syncwarp();
     // ---- stage all accumulators in shared memory: xs[a][col][unit] ----
     ptx::mbar_wait(done, 0);
     ptx::tc_fence_after();
@@ -314,29 +309,7 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      ptx::tma_prefetch(&mA); ptx::tma_prefetch(&mB);
-      int step = 0, g = 0;
-      for (int si = 0; si < P.nseg; ++si) {
-        const SegT2 sg = P.s[si];
-        const int nkb = cdiv(sg.k_hi - sg.k_lo, 64);
-        for (int kb = 0; kb < nkb; ++kb, ++g) {
-          if (g < g_lo || g >= g_hi) continue;
-          const int r0 = sg.k_lo + kb * 64;
-          if (sg.skip_no_x && !kb_has_x(D, r0)) continue;
-          const int s = step % S;
-          const uint32_t ph = (step / S) & 1;
-          ptx::mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* st = smem + s * STAGE;
-          ptx::mbar_arrive_expect_tx(&full[s], STAGE);
-          ptx::tma_load_2d(st, &mA, sg.a_col + m0, r0, &full[s]);
-          ptx::tma_load_2d(st + T2_TILE / 2, &mA, sg.a_col + m0 + 64, r0, &full[s]);
-          ptx::tma_load_2d(st + T2_TILE, &mB, sg.b_col + n0, r0, &full[s]);
-          ptx::tma_load_2d(st + T2_TILE + T2_TILE / 2, &mB, sg.b_col + n0 + 64, r0, &full[s]);
-          ++step;
-        }
-      }
-    }
+    if (lane == 0) { ptx::tma_prefetch(&mA); ptx::tma_prefetch(&mB); }
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
@@ -366,21 +339,50 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
       ptx::mma_commit(done);
     }
     __syncwarp();
-  } else if (warp < 6) {
-    ptx::mbar_wait(done, 0);
-    ptx::tc_fence_after();
-    const int qd = warp & 3;
-    const int m = m0 + qd * 32 + lane;
-    const bool any = *s_count > 0;
-    float* o = out + (size_t)z * P.split_stride;
-    const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16);
-    for (int c = 0; c < 128; c += 16) {
-      float v[16];
-      ptx::tmem_ld16(tq + c, v);
-      if (m < P.M) {
-        for (int i = 0; i < 16; ++i) {
-          const int n = n0 + c + i;
-          if (n < P.Ncols) o[(size_t)m * P.ldo + n] = any ? v[i] : 0.f;
+  } else {
+    if (lane == 0) {
+      // ---- TMA issue spread over warps 2..9: k-step st goes to warp 2 + st % 8 ----
+      const int w = warp - 2;
+      int step = 0, g = 0;
+      for (int si = 0; si < P.nseg; ++si) {
+        const SegT2 sg = P.s[si];
+        const int nkb = cdiv(sg.k_hi - sg.k_lo, 64);
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          if (g < g_lo || g >= g_hi) continue;
+          const int r0 = sg.k_lo + kb * 64;
+          if (sg.skip_no_x && !kb_has_x(D, r0)) continue;
+          if ((step & 7) == w) {
+            const int s = step % S;
+            const uint32_t ph = (step / S) & 1;
+            if (step >= S) ptx::mbar_wait(&empty[s], ph ^ 1);
+            uint8_t* st = smem + s * STAGE;
+            ptx::mbar_arrive_expect_tx(&full[s], STAGE);
+            ptx::tma_load_2d(st, &mA, sg.a_col + m0, r0, &full[s]);
+            ptx::tma_load_2d(st + T2_TILE / 2, &mA, sg.a_col + m0 + 64, r0, &full[s]);
+            ptx::tma_load_2d(st + T2_TILE, &mB, sg.b_col + n0, r0, &full[s]);
+            ptx::tma_load_2d(st + T2_TILE + T2_TILE / 2, &mB, sg.b_col + n0 + 64, r0, &full[s]);
+          }
+          ++step;
+        }
+      }
+    }
+    __syncwarp();
+    if (warp < 6) {
+      ptx::mbar_wait(done, 0);
+      ptx::tc_fence_after();
+      const int qd = warp & 3;
+      const int m = m0 + qd * 32 + lane;
+      const bool any = *s_count > 0;
+      float* o = out + (size_t)z * P.split_stride;
+      const uint32_t tq = tmem + ((uint32_t)(qd * 32) << 16);
+      for (int c = 0; c < 128; c += 16) {
+        float v[16];
+        ptx::tmem_ld16(tq + c, v);
+        if (m < P.M) {
+          for (int i = 0; i < 16; ++i) {
+            const int n = n0 + c + i;
+            if (n < P.Ncols) o[(size_t)m * P.ldo + n] = any ? v[i] : 0.f;
+          }
         }
       }
     }
