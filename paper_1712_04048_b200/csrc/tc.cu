@@ -157,8 +157,9 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
     __syncwarp();
   } else {
     if (lane == 0) {
-      // ---- TMA issue, spread over 8 warps (a single issuing thread serialises its boxes) ----
-      // Step st goes to warp 2 + st % 8.  Weight (A) tiles do not depend on the previous task, so
+      // ---- TMA issue, one warp per pipeline stage (a single issuing thread serialises its
+      // boxes): stage s = warp - 2 owns steps s, s+S, ... so each stage's barrier phases
+      // advance strictly in order.  Weight (A) tiles do not depend on the previous task, so
       // under PDL they stream in before griddepcontrol.wait; the task's rows (B) after it.
       const int w = warp - 2;
       bool waited = false;
@@ -167,7 +168,7 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
         const Bundle& b = R.b[bi];
         const CUtensorMap* ma = b.map_a ? &mA1 : &mA0;
         for (int kb = 0; kb < b.nk; ++kb, ++step) {
-          if ((step & 7) != w) continue;
+          if (step % S != w) continue;
           const int s = step % S;
           const uint32_t ph = (step / S) & 1;
           uint8_t* st = smem + s * R.stage_bytes;
@@ -341,7 +342,7 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
     __syncwarp();
   } else {
     if (lane == 0) {
-      // ---- TMA issue spread over warps 2..9: k-step st goes to warp 2 + st % 8 ----
+      // ---- TMA issue, one warp per pipeline stage (warp 2 + s owns stage s) ----
       const int w = warp - 2;
       int step = 0, g = 0;
       for (int si = 0; si < P.nseg; ++si) {
@@ -351,7 +352,7 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
           if (g < g_lo || g >= g_hi) continue;
           const int r0 = sg.k_lo + kb * 64;
           if (sg.skip_no_x && !kb_has_x(D, r0)) continue;
-          if ((step & 7) == w) {
+          if (step % S == w) {
             const int s = step % S;
             const uint32_t ph = (step / S) & 1;
             if (step >= S) ptx::mbar_wait(&empty[s], ph ^ 1);
