@@ -122,6 +122,7 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
     if (lane == 0) {
       ptx::tma_prefetch(&mA0); ptx::tma_prefetch(&mA1); ptx::tma_prefetch(&mB);
       ptx::griddep_wait();
+      if (D.trace) s_tr[2] = gtime();
       ptx::griddep_launch();                           // PDL: let the next task's CTAs start their prologue
     }
     __syncwarp();
@@ -260,7 +261,7 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
     const unsigned long long at = 8 + 8 * atomicAdd(D.trace, 1ull);
     if (at + 8 < (4u << 20) / 8) {
       D.trace[at] = 100 * CL + E; D.trace[at + 1] = blockIdx.x + 1000ull * blockIdx.y; D.trace[at + 2] = row_lo;
-      D.trace[at + 3] = s_tr[0]; D.trace[at + 4] = s_tr[0]; D.trace[at + 5] = s_tr[1]; D.trace[at + 6] = gtime();
+      D.trace[at + 3] = s_tr[0]; D.trace[at + 4] = s_tr[2]; D.trace[at + 5] = s_tr[1]; D.trace[at + 6] = gtime();
       D.trace[at + 7] = row_hi;
     }
   }
