@@ -187,6 +187,11 @@ cavs_status cavs_profile_read(cavs_ctx* ctx, int32_t phase, double* ms, double* 
                               int64_t* launches);
 
 const char* cavs_last_error(const cavs_ctx* ctx);
+
+/* Which kernel path the context runs its batching tasks on (diagnostic string, owned by the
+ * context, valid until the next call on it), e.g. "levels: persistent: grid 144 ...".  Only
+ * meaningful after cavs_set_workspace; never NULL. */
+const char* cavs_path_info(const cavs_ctx* ctx);
 void cavs_destroy(cavs_ctx* ctx);
 
 #ifdef __cplusplus

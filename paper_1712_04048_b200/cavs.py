@@ -55,6 +55,7 @@ def _load():
         "cavs_train_step_host": (S, [P, I32, I32, I32, P, P, P, P, I32, P, P, P, P, P, P]),
         "cavs_kernel_launches": (I64, [P]),
         "cavs_last_error": (ctypes.c_char_p, [P]),
+        "cavs_path_info": (ctypes.c_char_p, [P]),
         "cavs_profile": (S, [P, ctypes.c_int]),
         "cavs_profile_read": (S, [P, I32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)]),
@@ -71,7 +72,7 @@ _lib = _load()
 EXPORTS = ["cavs_param_count", "cavs_create", "cavs_set_stream", "cavs_workspace_bytes",
            "cavs_set_workspace", "cavs_load_graphs", "cavs_schedule", "cavs_get_schedule",
            "cavs_forward", "cavs_backward", "cavs_train_step_host", "cavs_kernel_launches",
-           "cavs_last_error", "cavs_destroy", "cavs_profile", "cavs_profile_read"]
+           "cavs_last_error", "cavs_path_info", "cavs_destroy", "cavs_profile", "cavs_profile_read"]
 PHASES = ["schedule", "prep", "xproj", "fwd_levels", "bwd_roots", "bwd_levels", "lazy", "dx", "reduce"]
 
 
@@ -134,6 +135,10 @@ class Context:
     @property
     def launches(self) -> int:
         return int(_lib.cavs_kernel_launches(self._ctx))
+
+    def path_info(self) -> str:
+        """Which kernel path runs the batching tasks (e.g. the persistent level kernel)."""
+        return (_lib.cavs_path_info(self._ctx) or b"").decode()
 
     def profile(self, enable: bool = True):
         """Reset the per-phase accumulators and (de)activate phase timing."""

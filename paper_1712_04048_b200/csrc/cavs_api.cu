@@ -28,6 +28,7 @@ struct cavs_ctx {
   int T = 0, n_roots = 0;
   int* h_hdr = nullptr;         // pinned readback buffer
   std::string err;
+  std::string info;             // cavs_path_info buffer
   Prof prof;                    // phase marks + launch counts
   // lazy scratch layout
   float* lazy_db = nullptr;
@@ -75,6 +76,7 @@ static size_t carve(cavs_ctx* c, char* base) {
   D.pending = I(V); D.queue = I(V);
   D.hdr = I(kHdrWords + V + 1); D.level_ptr = base ? D.hdr + kHdrWords : nullptr;
   D.roots = I(V); D.cnt = I(V + 1);
+  D.gsync = reinterpret_cast<unsigned*>(I(64));
   D.order = I(V); D.child_pos = I(V * N); D.parent_pos = I(V); D.slot = I(V); D.deg = I(V);
   D.xrow_pos = I(Vp); D.tile_x = I(Vp / 64 + 2);
   D.Hk = take(Vp * N * h * es);
@@ -417,6 +419,14 @@ CAVS_API cavs_status cavs_profile_read(cavs_ctx* ctx, int32_t phase, double* ms,
 }
 
 CAVS_API const char* cavs_last_error(const cavs_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+CAVS_API const char* cavs_path_info(const cavs_ctx* ctx) {
+  if (!ctx) return "null context";
+  cavs_ctx* c = const_cast<cavs_ctx*>(ctx);
+  c->info = ctx->state < S_READY ? std::string("no workspace yet")
+                                 : ctx->desc.precision == CAVS_BF16 ? tc_describe(ctx->tc) : std::string("levels: FP32 FFMA");
+  return c->info.c_str();
+}
 
 CAVS_API void cavs_destroy(cavs_ctx* ctx) {
   if (!ctx) return;

@@ -1,0 +1,673 @@
+// persist.cu — BF16 mode: ONE persistent, weight-stationary launch for all batching tasks of a
+// pass (Alg. 1 FORWARD / BACKWARD loop; the batched "Batched Execution"
+// of §3.5).
+//
+// Why: a level-by-level launch pays, per task V_t, a kernel launch + a fresh stream of F's
+// weights (2-8 MB) through the SMs, and the small tasks at the top of the trees are pure
+// latency.  Here every CTA keeps a fixed 128-row slice of the weights resident in shared
+// memory for the whole pass, and the tasks are separated by a grid-wide barrier instead of
+// kernel boundaries.
+//
+// Decomposition (swap-AB, like tc.cu): D[row, task] = sum_k A[row, k] B[task, k], M = 128 weight
+// rows, N = NT task rows (16/32/64 chosen per task so that the task spreads over the R
+// replicas), accumulators in TMEM.  The 128 rows of a CTA are ngrp "row groups" of UG units
+// each, every group a different gate (Tree-LSTM: i, o, u, f of the same 32 units, UG = 32;
+// Tree-FC: the two children's blocks of the same 64 units, UG = 64), so a CTA owns ALL the
+// gates of its units and the fused cell epilogue needs no inter-CTA exchange.  A group only
+// pairs with its own operand columns; where operands differ per group (backward: dz_i, dz_o,
+// dz_u, dz_f; Tree-FC forward: h_l, h_r) each operand gets its own accumulator and the
+// epilogue keeps the matching group — the wasted MMA rows are cheap next to the latency saved.
+//
+//   grid = nub x R CTAs (nub = h / UG unit blocks, R = replicas, all co-resident: 1 CTA/SM);
+//   CTA (ub, r) handles tiles j = r, r + R, ... of every task.
+//   warps 0-2: TMA producers (weights once; then B boxes {64 k, NT rows, sk k-blocks} of the
+//              task rows, one warp per pipeline stage), warp 3: TMEM allocator + MMA issuer,
+//   warps 4-11: per-vertex metadata, TMEM -> smem staging, fused cell epilogue (cells.cuh),
+//              and the grid barrier between tasks.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "cells.cuh"
+#include "persist.h"
+#include "ptx.cuh"
+
+namespace cavs {
+
+constexpr int kPThreads = 384;       // 12 warps (whole 4-warp register granules: up to 168 regs)
+constexpr int kPProd = 3;            // producer warps 0-2, MMA warp 3
+constexpr int kPMma = 3;
+constexpr int kPEpi0 = 4;            // first epilogue warp
+constexpr int kPKb = 16384;          // one resident A k-block: 128 rows x 128 B (SW128, K-major)
+constexpr int kPStage = 16384;       // one B box
+constexpr int kPMaxNT = 64;
+
+struct PPlan {
+  int UG, ngrp, nkbA;                // units per CTA, row groups, resident k-blocks (K = 64 nkbA)
+  int grp_row0[4], grp_col0[4];      // A rows grp_row0 + u0 .. + UG, columns grp_col0 + 64 kb
+  int nseg, seg_bcol[8], seg_acc[8]; // MMA segments: all resident k-blocks x B columns [bcol, bcol + K)
+  int nacc;
+  int nslot, slot_grp[8], slot_nacc[8], slot_acc[8][4];   // staged slot = sum of accs, one group
+  int ne, e_n[8], e_slot[8][3];      // epilogue accumulator e = sum of slots
+  int S;                             // B pipeline stages
+  int sk[3];                         // k-blocks per B box for NT = 16 / 32 / 64
+  int nub, R;
+  int xs_off, meta_off, bar_off;
+};
+
+// mbarrier wait: try_wait (the waiting thread is suspended in hardware instead of polling the
+// barrier unit), trapping after ~4 s instead of hanging the GPU on a protocol bug.
+__device__ __forceinline__ void pwait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = ptx::smem_u32(bar);
+  unsigned long long t0 = 0;
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    if (ok) return;
+    const unsigned long long now = gtime();
+    if (t0 == 0) t0 = now;
+    else if (now - t0 > 4000000000ull) __trap();
+  }
+}
+// one waiting lane per warp, then the warp proceeds together
+__device__ __forceinline__ void pwait_warp(uint64_t* bar, uint32_t parity) {
+  if ((threadIdx.x & 31) == 0) pwait(bar, parity);
+  __syncwarp();
+}
+
+__device__ __forceinline__ int nt_index(int M, int R) {
+  const int n = (M + R - 1) / R;
+  return n <= 16 ? 0 : n <= 32 ? 1 : 2;
+}
+
+// Grid barrier (all CTAs co-resident by construction: cooperative launch).  Monotonic arrival
+// counter: barrier i of a launch completes when the counter reaches (i + 1) * gridDim.x; the
+// last CTA to leave the kernel resets it to 0 (so the launch is replayable, e.g. in a graph).
+// Release-add + acquire-poll: one L2 round trip after the last arrival.  Spins at most ~4 s,
+// then traps (never hang the GPU).
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned target) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
+  unsigned long long t0 = 0;
+  unsigned it = 0;
+  while ((int)(ptx::ld_acquire_gpu(count) - target) < 0) {
+    if ((++it & 255u) == 0) {
+      const unsigned long long now = gtime();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 4000000000ull) __trap();
+    }
+  }
+}
+
+// Compile-time staging layout per epilogue kind (matches the host plan of persist_init):
+// xs slot s holds one row group's accumulator(s); epilogue accumulator e sums slots.
+template <int E, int NM> struct PLay {
+  static constexpr bool lstm = E == EPI_LSTM_FWD || E == EPI_LSTM_BWD;
+  static constexpr int UG = lstm ? 32 : 64;
+  static constexpr int NSLOT = lstm ? 3 + NM : 2;
+  static constexpr int NE = E == EPI_LSTM_FWD ? 3 + NM : E == EPI_LSTM_BWD ? 1 + NM : E == EPI_FC_FWD ? 1 : 2;
+  static __device__ __forceinline__ constexpr int grp(int s) { return lstm ? (s < 3 ? s : 3) : s; }
+  static __device__ __forceinline__ constexpr int nacc(int s) { return E == EPI_LSTM_FWD && s < 3 ? NM : 1; }
+  static __device__ __forceinline__ constexpr int acc(int s, int a) {
+    return E == EPI_LSTM_FWD ? (s < 3 ? a : s - 3) : E == EPI_FC_BWD ? 0 : s;
+  }
+  static __device__ __forceinline__ constexpr int e_n(int e) {
+    return E == EPI_LSTM_BWD && e == 0 ? 3 : E == EPI_FC_FWD ? 2 : 1;
+  }
+  static __device__ __forceinline__ constexpr int e_slot(int e, int z) {
+    return E == EPI_LSTM_BWD ? (e == 0 ? z : e + 2) : E == EPI_FC_FWD ? z : e;
+  }
+};
+
+// debug trace record (CAVS_TRACE=1): 8 words per record in the ring at D.trace
+__device__ __forceinline__ void ptrace(const Dev& D, unsigned long long a, unsigned long long b, unsigned long long c,
+                                       unsigned long long d, unsigned long long e, unsigned long long f,
+                                       unsigned long long g, unsigned long long h) {
+  const unsigned long long at = 8 + 8 * atomicAdd(D.trace, 1ull);
+  if (at + 8 < (4u << 20) / 8) {
+    D.trace[at] = a; D.trace[at + 1] = b; D.trace[at + 2] = c; D.trace[at + 3] = d;
+    D.trace[at + 4] = e; D.trace[at + 5] = f; D.trace[at + 6] = g; D.trace[at + 7] = h;
+  }
+}
+
+// MMA issue of one task's tiles (NT compile-time: constant instruction descriptor, accumulator
+// columns and descriptor strides; only 32-bit adds per tcgen05.mma).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t lo) {
+  return ((uint64_t)((1024u >> 4) | (1u << 14) | (2u << 29)) << 32) | lo;   // SBO 1024, version 1, SWIZZLE_128B
+}
+template <int NT>
+__device__ __forceinline__ void mma_level(const PPlan& P, int r, int ntile, uint32_t a_lo, uint32_t b_lo,
+                                          uint64_t* full, uint64_t* empty, uint64_t* done, uint64_t* tmem_empty,
+                                          int& step, int& tcount, unsigned long long* tr) {
+  constexpr uint32_t idesc = ptx::idesc_bf16(128, NT, 0, 0);
+  constexpr int ni = NT == 16 ? 0 : NT == 32 ? 1 : 2;
+  const int sk = P.sk[ni], nbox = P.nkbA / sk, S = P.S;
+  for (int j = r; j < ntile; j += P.R, ++tcount) {
+    if (tcount > 0) { pwait(tmem_empty, (tcount - 1) & 1); ptx::tc_fence_after(); }
+    uint32_t written = 0;
+    for (int sg = 0; sg < P.nseg; ++sg) {
+      const int acc = P.seg_acc[sg];
+      const uint32_t d = (uint32_t)(acc * NT);
+      for (int b = 0; b < nbox; ++b, ++step) {
+        const int s = step % S;
+        pwait(&full[s], (step / S) & 1);
+        ptx::tc_fence_after();
+        if (tr && tr[0] == 0) tr[0] = gtime();
+        uint32_t al = a_lo + (uint32_t)(b * sk) * (kPKb >> 4);
+        uint32_t bl = b_lo + (uint32_t)s * (kPStage >> 4);
+        uint32_t acc_flag = (written >> acc) & 1u;
+        for (int kb = 0; kb < sk; ++kb) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            ptx::mma_bf16(d, sw128_desc(al + kk * 2), sw128_desc(bl + kk * 2), idesc, acc_flag);
+            acc_flag = 1u;
+          }
+          al += kPKb >> 4;
+          bl += (NT * 128) >> 4;
+        }
+        written |= 1u << acc;
+        ptx::mma_commit(&empty[s]);
+      }
+    }
+    ptx::mma_commit(done);
+    if (tr && tr[1] == 0) tr[1] = gtime();
+  }
+}
+
+template <int E, int NE, int NM>
+__global__ void __launch_bounds__(kPThreads, 1)
+k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUtensorMap ma1,
+          const __grid_constant__ CUtensorMap ma2, const __grid_constant__ CUtensorMap ma3,
+          const __grid_constant__ CUtensorMap mb16, const __grid_constant__ CUtensorMap mb32,
+          const __grid_constant__ CUtensorMap mb64, Dev D, PPlan P, int t_first, int nlev, int dir) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  // 1024-aligned base by pointer arithmetic on the __shared__ symbol (keeps the shared address
+  // space visible to the compiler: LDS/STS, not generic loads)
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  using L = PLay<E, NM>;
+  static_assert(L::NE == NE, "epilogue accumulator count");
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + P.nkbA * kPKb;
+  float* xs = reinterpret_cast<float*>(smem + P.xs_off);        // [nslot][64][UG]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P.bar_off);
+  uint64_t* empty = full + kPProd;
+  uint64_t* done = empty + kPProd;
+  uint64_t* tmem_empty = done + 1;
+  uint64_t* abar = tmem_empty + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(abar + 1);
+  volatile int* gate = reinterpret_cast<volatile int*>(tmem_slot + 1);
+  __shared__ unsigned long long s_tmax;                          // debug trace only
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ub = blockIdx.x % P.nub, r = blockIdx.x / P.nub;
+  const int u0 = ub * P.UG;
+  const int S = P.S;
+  const int* lp = D.level_ptr;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    ptx::mbar_init(done, 1);
+    ptx::mbar_init(tmem_empty, 8);
+    ptx::mbar_init(abar, P.ngrp);
+    *gate = 0;
+    ptx::fence_mbar_init();
+  }
+  if (warp == kPMma) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < kPProd) {
+    // ------------------------------------------------------------------ producers
+    if (lane == 0) {
+      const int w = warp;
+      for (int g = w; g < P.ngrp; g += kPProd) {      // resident weights: group g, all k-blocks
+        const CUtensorMap* ma = g == 0 ? &ma0 : g == 1 ? &ma1 : g == 2 ? &ma2 : &ma3;
+        ptx::tma_prefetch(ma);
+        ptx::mbar_arrive_expect_tx(abar, P.nkbA * P.UG * 128);
+        for (int kb = 0; kb < P.nkbA; ++kb)
+          ptx::tma_load_2d(sA + kb * kPKb + g * P.UG * 128, ma, P.grp_col0[g] + kb * 64, P.grp_row0[g] + u0, abar);
+      }
+      ptx::tma_prefetch(&mb16); ptx::tma_prefetch(&mb32); ptx::tma_prefetch(&mb64);
+      ptx::griddep_wait();                            // task rows come from the previous kernels
+      int step = 0;
+      for (int i = 0; i < nlev; ++i) {
+        const int t = t_first + i * dir;
+        const int lo = lp[t], M = lp[t + 1] - lo;
+        const int ni = nt_index(M, P.R), nt = 16 << ni;
+        const int ntile = (M + nt - 1) / nt;
+        if (r >= ntile) continue;
+        const CUtensorMap* mb = ni == 0 ? &mb16 : ni == 1 ? &mb32 : &mb64;
+        const int sk = P.sk[ni], nbox = P.nkbA / sk;
+        const uint32_t bytes = (uint32_t)nt * 128u * (uint32_t)sk;
+        if (i > 0) {                                  // previous task finished grid-wide
+          const unsigned long long tw = D.trace ? gtime() : 0;
+          while (*gate < i) { }
+          ptx::fence_proxy_async_global();
+          if (D.trace && w == 0) ptrace(D, 3000 + E, blockIdx.x, i, tw, gtime(), 0, 0, 0);
+        }
+        if (D.trace && w == 0) ptrace(D, 5000 + E, blockIdx.x, i, gtime(), 0, 0, 0, 0);
+        for (int j = r; j < ntile; j += P.R) {
+          const int p0 = lo + j * nt;
+          for (int sg = 0; sg < P.nseg; ++sg) {
+            for (int b = 0; b < nbox; ++b, ++step) {
+              const int s = step % S;
+              if (s != w) continue;
+              const uint32_t ph = (step / S) & 1;
+              if (step >= S) pwait(&empty[s], ph ^ 1);
+              ptx::mbar_arrive_expect_tx(&full[s], bytes);
+              ptx::tma_load_3d(sB + s * kPStage, mb, 0, p0, P.seg_bcol[sg] / 64 + b * sk, &full[s]);
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == kPMma) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      // The CTA is alone on its SM (shared memory) and owns all 512 TMEM columns, so the
+      // allocation starts at column 0: accumulator addresses are then warp-uniform constants
+      // (no per-MMA register->uniform waterfall in the issue loop).
+      if (tmem != 0) __trap();
+      pwait(abar, 0);
+      ptx::tc_fence_after();
+      const uint32_t a_lo = ((ptx::smem_u32(sA) >> 4) & 0x3FFF) | (1u << 16);
+      const uint32_t b_lo = ((ptx::smem_u32(sB) >> 4) & 0x3FFF) | (1u << 16);
+      int step = 0, tcount = 0;
+      for (int i = 0; i < nlev; ++i) {
+        const int t = t_first + i * dir;
+        const int M = lp[t + 1] - lp[t];
+        const int ni = nt_index(M, P.R), nt = 16 << ni;
+        const int ntile = (M + nt - 1) / nt;
+        unsigned long long trm[2] = {0, 0};
+        unsigned long long* tr = D.trace ? trm : nullptr;
+        if (ni == 0) mma_level<16>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
+        else if (ni == 1) mma_level<32>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
+        else mma_level<64>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
+        if (D.trace && r < ntile) ptrace(D, 4000 + E, blockIdx.x, i, trm[0], trm[1], 0, nt, 0);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------------ epilogue (8 warps)
+    const int et = threadIdx.x - kPEpi0 * 32;          // 0..255
+    const int q = warp & 3, half = (warp - kPEpi0) >> 2;
+    constexpr int quads = L::UG / 4;
+    const int quad = et % quads;                       // constant: 256 % quads == 0
+    const int j = u0 + quad * 4;
+    ptx::griddep_wait();
+    const UnitC<4> uc = epi_uses_bias<E>() ? load_unit<4>(D, j, epi_is_lstm<E>()) : UnitC<4>{};
+    constexpr int CH = epi_needs_children<E>() ? 1 : 2;
+    int tcount = 0;
+    for (int i = 0; i < nlev; ++i) {
+      const int t = t_first + i * dir;
+      const int lo = lp[t], M = lp[t + 1] - lo;
+      const int ni = nt_index(M, P.R), nt = 16 << ni;
+      const int ntile = (M + nt - 1) / nt;
+      unsigned long long tr0 = 0, tr1 = 0, tr2 = 0, tr3 = 0;
+      if (D.trace && et == 0) tr0 = gtime();
+      if (i > 0 && r < ntile) {                         // inputs of V_t are final once the barrier passed
+        if (lane == 0) while (*gate < i) { }
+        __syncwarp();
+      }
+      for (int jt = r; jt < ntile; jt += P.R, ++tcount) {
+        const int p0 = lo + jt * nt;
+        const int valid = min(nt, lo + M - p0);
+        const int items = quads * valid;
+        // ---- this thread's first round of (unit quad, column) items: metadata + cell inputs,
+        //      loaded while the TMA / MMA of the tile are still in flight ----
+        VMeta mt[CH];
+        typename EpiK<E>::template In<4, NM> in[CH];
+        int base = et;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const int it = base + 256 * c;
+          if (it < items) {
+            load_meta(D, p0 + it / quads, epi_needs_children<E>(), mt[c]);
+            EpiK<E>::template load<4, NM>(D, j, mt[c], in[c]);
+          }
+        }
+        // ---- accumulators -> xs[slot][col][unit] (warp quadrant q holds TMEM lanes 32q..32q+31) ----
+        pwait_warp(done, tcount & 1);
+        if (D.trace && et == 0 && tr1 == 0) tr1 = gtime();
+        ptx::tc_fence_after();
+        const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+#pragma unroll
+        for (int s = 0; s < L::NSLOT; ++s) {
+          constexpr int UG = L::UG;
+          const int g = L::grp(s);
+          if (q * 32 < g * UG || q * 32 >= (g + 1) * UG) continue;
+          const int urow = q * 32 - g * UG + lane;
+          for (int c0 = half * (nt / 2); c0 < (half + 1) * (nt / 2); c0 += 8) {
+            float v[8];
+            ptx::tmem_ld<8>(tq + L::acc(s, 0) * nt + c0, v);
+#pragma unroll
+            for (int a = 1; a < L::nacc(s); ++a) {
+              float w8[8];
+              ptx::tmem_ld<8>(tq + L::acc(s, a) * nt + c0, w8);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[e] += w8[e];
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) xs[(s * kPMaxNT + c0 + e) * UG + urow] = v[e];
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(tmem_empty);
+        ptx::named_bar_sync(1, 256);
+        if (D.trace && et == 0 && tr3 == 0) tr3 = gtime();
+        // ---- fused cell epilogue: thread -> (unit quad, columns) ----
+#pragma unroll 1
+        while (base < items) {
+          FV<4> acc[CH][NE];
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {
+            const int it = base + 256 * c;
+            if (it >= items) continue;
+            const int col = it / quads;
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+              float4 sum = *reinterpret_cast<const float4*>(xs + (L::e_slot(e, 0) * kPMaxNT + col) * L::UG + quad * 4);
+#pragma unroll
+              for (int z = 1; z < L::e_n(e); ++z) {
+                const float4 x = *reinterpret_cast<const float4*>(
+                    xs + (L::e_slot(e, z) * kPMaxNT + col) * L::UG + quad * 4);
+                sum.x += x.x; sum.y += x.y; sum.z += x.z; sum.w += x.w;
+              }
+              acc[c][e].v[0] = sum.x; acc[c][e].v[1] = sum.y; acc[c][e].v[2] = sum.z; acc[c][e].v[3] = sum.w;
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < CH; ++c)
+            if (base + 256 * c < items) EpiK<E>::template store<__nv_bfloat16, 4, NM>(D, j, mt[c], acc[c], in[c], uc);
+          base += 256 * CH;
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {                 // next round (large tiles / FC): load, then loop
+            const int it = base + 256 * c;
+            if (it < items) {
+              load_meta(D, p0 + it / quads, epi_needs_children<E>(), mt[c]);
+              EpiK<E>::template load<4, NM>(D, j, mt[c], in[c]);
+            }
+          }
+        }
+        unsigned long long tl = 0;
+        if (D.trace) { tl = gtime(); atomicMax(&s_tmax, tl); }
+        ptx::named_bar_sync(1, 256);                     // xs free for the next tile
+        if (D.trace && et == 0 && jt == r) { ptrace(D, 6000 + E, blockIdx.x, i, tr3, tl, s_tmax, gtime(), 0); s_tmax = 0; }
+      }
+      if (i + 1 < nlev) {                                // task V_t complete grid-wide before V_t+-1
+        ptx::named_bar_sync(1, 256);
+        if (et == 0) {
+          if (D.trace) tr2 = gtime();
+          grid_barrier(D.gsync, (unsigned)(i + 1) * gridDim.x);
+          *gate = i + 1;
+          if (D.trace) ptrace(D, 2000 + E, blockIdx.x, (unsigned long long)i | ((unsigned long long)M << 16), tr0, tr1, tr2,
+                              gtime(), tr3);
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == kPMma) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+  if (threadIdx.x == 0 && atomicAdd(D.gsync + 1, 1u) == gridDim.x - 1) {   // every CTA is past its last barrier
+    D.gsync[0] = 0;
+    D.gsync[1] = 0;
+  }
+}
+
+// =====================================================================================
+// host side
+// =====================================================================================
+struct PersistState {
+  CUtensorMap A_fwd[4], A_bwd[4];     // per row group (box 64 x UG)
+  CUtensorMap B_hk[3], B_dz[3];       // 3D {64, NT, sk} boxes over Hk / dZ
+  PPlan fwd{}, bwd{};
+  int num_sms = 0;
+};
+
+static PFN_cuTensorMapEncodeTiled_v12000 p_encode = nullptr;
+
+static bool enc2(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_elems,
+                 uint32_t box_cols, uint32_t box_rows) {
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch_elems * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return p_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// [rows, width] row-major arena viewed as {64 k, row, k-block}: one box = sk stacked K-major
+// SW128 tiles of NT rows (smem order [kb][row][64]).
+static bool enc3(CUtensorMap* m, const void* base, uint64_t width, uint64_t rows, uint32_t nt, uint32_t sk) {
+  cuuint64_t dims[3] = {64, rows, width / 64};
+  cuuint64_t strides[2] = {width * 2, 128};
+  cuuint32_t box[3] = {64, nt, sk};
+  cuuint32_t es[3] = {1, 1, 1};
+  return p_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static void plan_slot(PPlan& P, int grp, int nacc, const int* accs) {
+  const int s = P.nslot++;
+  P.slot_grp[s] = grp;
+  P.slot_nacc[s] = nacc;
+  for (int a = 0; a < nacc; ++a) P.slot_acc[s][a] = accs[a];
+}
+static void plan_e(PPlan& P, int n, const int* slots) {
+  const int e = P.ne++;
+  P.e_n[e] = n;
+  for (int z = 0; z < n; ++z) P.e_slot[e][z] = slots[z];
+}
+
+// smem offsets + pipeline depth; false if the plan does not fit one CTA
+static bool plan_layout(PPlan& P) {
+  const int A = P.nkbA * kPKb;
+  const int xs = P.nslot * kPMaxNT * P.UG * 4;
+  const int meta = 0;
+  const int fixed = 1024 + A + xs + meta + 256;
+  const int S = std::min(kPProd, (232448 - fixed) / kPStage);
+  if (S < 2) return false;
+  P.S = S;
+  P.xs_off = A + S * kPStage;
+  P.meta_off = P.xs_off + xs;
+  P.bar_off = (P.meta_off + meta + 15) & ~15;
+  for (int i = 0; i < 3; ++i) {                       // largest divisor of nkbA with a <= 16 KB box
+    const int cap = kPStage / ((16 << i) * 128);
+    int sk = 1;
+    for (int c = 1; c <= std::min(cap, P.nkbA); ++c)
+      if (P.nkbA % c == 0) sk = c;
+    P.sk[i] = sk;
+  }
+  return true;
+}
+static int plan_smem(const PPlan& P) { return 1024 + P.bar_off + 128; }
+
+template <int E, int NE, int NM>
+static bool attr_and_occupancy(int smem) {
+  if (cudaFuncSetAttribute(k_persist<E, NE, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return false;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_persist<E, NE, NM>, kPThreads, smem) != cudaSuccess)
+    return false;
+  return occ >= 1;
+}
+
+template <int E, int NE, int NM>
+static void launch_p(const CUtensorMap* A, const CUtensorMap* B, const Dev& D, const PPlan& P, int t_first, int nlev,
+                     int dir, cudaStream_t s) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(P.nub * P.R, 1, 1);
+  cfg.blockDim = dim3(kPThreads, 1, 1);
+  cfg.dynamicSmemBytes = plan_smem(P);
+  cfg.stream = s;
+  // cooperative: all CTAs resident at once (the grid barrier relies on it, also next to other
+  // streams' kernels); PDL: the weights stream in under the previous kernel when the driver
+  // accepts both attributes together, else cooperative alone.
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  static int nattr = 2;
+  cfg.numAttrs = nattr;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_persist<E, NE, NM>, A[0], A[1], A[2], A[3], B[0], B[1], B[2], D, P,
+                                     t_first, nlev, dir);
+  if (e != cudaSuccess && nattr == 2) {
+    (void)cudaGetLastError();
+    nattr = 1;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_persist<E, NE, NM>, A[0], A[1], A[2], A[3], B[0], B[1], B[2], D, P, t_first, nlev, dir);
+  }
+}
+
+PersistState* persist_init(const Dev& D, int max_vertices, std::string* why) {
+  const char* env = std::getenv("CAVS_PERSIST");
+  if (env && env[0] == '0') { *why = "disabled (CAVS_PERSIST=0)"; return nullptr; }
+  const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
+  const int h = D.h, N = D.N;
+  const int UG = lstm ? 32 : 64;
+  if (h % 64 || h % UG || h / 64 > 8) { *why = "shape: needs h % 64 == 0 and h <= 512"; return nullptr; }
+  if (!p_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+      *why = "cuTensorMapEncodeTiled unavailable";
+      return nullptr;
+    }
+    p_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  PersistState* ps = new PersistState();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&ps->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  const int nub = h / UG;
+  const int R = ps->num_sms / nub;
+  if (R < 1) { delete ps; *why = "too few SMs"; return nullptr; }
+  const uint64_t Vp = (uint64_t)max_vertices + kPadRows;
+  const int G = lstm ? 3 + N : 1;
+  bool ok = true;
+  PPlan F{}, B{};
+  F.UG = B.UG = UG; F.nkbA = B.nkbA = h / 64; F.nub = B.nub = nub; F.R = B.R = R;
+  if (lstm) {
+    // forward: groups (i, o, u, f) of U4 [4h x h]; acc k = U4 . h_k (sum over k by linearity, Z11)
+    F.ngrp = 4;
+    for (int g = 0; g < 4; ++g) { F.grp_row0[g] = g * h; F.grp_col0[g] = 0; ok &= enc2(&ps->A_fwd[g], D.Wa, h, 4 * h, h, 64, UG); }
+    F.nseg = N;
+    for (int k = 0; k < N; ++k) { F.seg_bcol[k] = k * h; F.seg_acc[k] = k; }
+    F.nacc = N;
+    int all[4] = {0, 1, 2, 3};
+    for (int g = 0; g < 3; ++g) plan_slot(F, g, N, all);
+    for (int k = 0; k < N; ++k) plan_slot(F, 3, 1, &all[k]);
+    for (int e = 0; e < 3 + N; ++e) plan_e(F, 1, &e);
+    // backward: groups (U_i^T, U_o^T, U_u^T, U_f^T) rows of the output units; acc g = group g
+    // against dz_g, acc 3+k = U_f^T group against dz_fk
+    B.ngrp = 4;
+    for (int g = 0; g < 3; ++g) { B.grp_row0[g] = 0; B.grp_col0[g] = g * h; ok &= enc2(&ps->A_bwd[g], D.Wc, 3 * h, h, 3 * h, 64, UG); }
+    B.grp_row0[3] = 0; B.grp_col0[3] = 0; ok &= enc2(&ps->A_bwd[3], D.Wd, h, h, h, 64, UG);
+    B.nseg = 3 + N;
+    for (int g = 0; g < 3 + N; ++g) { B.seg_bcol[g] = g * h; B.seg_acc[g] = g; }
+    B.nacc = 3 + N;
+    for (int g = 0; g < 3; ++g) plan_slot(B, g, 1, &g);
+    for (int k = 0; k < N; ++k) { const int a = 3 + k; plan_slot(B, 3, 1, &a); }
+    const int iou[3] = {0, 1, 2};
+    plan_e(B, 3, iou);
+    for (int k = 0; k < N; ++k) { const int sl = 3 + k; plan_e(B, 1, &sl); }
+  } else {
+    // Tree-FC forward: groups (W_l, W_r) rows of the units = W_c [h x 2h] columns [0,h) / [h,2h)
+    F.ngrp = 2;
+    for (int g = 0; g < 2; ++g) { F.grp_row0[g] = 0; F.grp_col0[g] = g * h; ok &= enc2(&ps->A_fwd[g], D.Wa, 2 * h, h, 2 * h, 64, UG); }
+    ps->A_fwd[2] = ps->A_fwd[3] = ps->A_fwd[0];
+    F.nseg = 2; F.seg_bcol[0] = 0; F.seg_acc[0] = 0; F.seg_bcol[1] = h; F.seg_acc[1] = 1;
+    F.nacc = 2;
+    const int a0 = 0, a1 = 1;
+    plan_slot(F, 0, 1, &a0); plan_slot(F, 1, 1, &a1);
+    const int both[2] = {0, 1};
+    plan_e(F, 2, both);
+    // backward: groups (W_l^T, W_r^T) = WcT [2h x h] rows [0,h) / [h,2h) against dz
+    B.ngrp = 2;
+    for (int g = 0; g < 2; ++g) { B.grp_row0[g] = g * h; B.grp_col0[g] = 0; ok &= enc2(&ps->A_bwd[g], D.Wc, h, 2 * h, h, 64, UG); }
+    ps->A_bwd[2] = ps->A_bwd[3] = ps->A_bwd[0];
+    B.nseg = 1; B.seg_bcol[0] = 0; B.seg_acc[0] = 0;
+    B.nacc = 1;
+    plan_slot(B, 0, 1, &a0); plan_slot(B, 1, 1, &a0);
+    plan_e(B, 1, &a0); plan_e(B, 1, &a1);
+  }
+  if (!plan_layout(F) || !plan_layout(B)) { delete ps; *why = "does not fit shared memory"; return nullptr; }
+  if (F.nacc * kPMaxNT > 512 || B.nacc * kPMaxNT > 512) { delete ps; *why = "TMEM"; return nullptr; }
+  for (int i = 0; i < 3; ++i) {
+    ok &= enc3(&ps->B_hk[i], D.Hk, (uint64_t)N * h, Vp, 16u << i, F.sk[i]);
+    ok &= enc3(&ps->B_dz[i], D.dZ, (uint64_t)G * h, Vp, 16u << i, B.sk[i]);
+  }
+  if (!ok) { delete ps; *why = "tensor map encode failed"; return nullptr; }
+  // every CTA must be resident at once (grid barrier): one CTA per SM
+  bool occ = true;
+  if (lstm) {
+    switch (N) {
+      case 1: occ = attr_and_occupancy<EPI_LSTM_FWD, 4, 1>(plan_smem(F)) && attr_and_occupancy<EPI_LSTM_BWD, 2, 1>(plan_smem(B)); break;
+      case 2: occ = attr_and_occupancy<EPI_LSTM_FWD, 5, 2>(plan_smem(F)) && attr_and_occupancy<EPI_LSTM_BWD, 3, 2>(plan_smem(B)); break;
+      case 3: occ = attr_and_occupancy<EPI_LSTM_FWD, 6, 3>(plan_smem(F)) && attr_and_occupancy<EPI_LSTM_BWD, 4, 3>(plan_smem(B)); break;
+      default: occ = attr_and_occupancy<EPI_LSTM_FWD, 7, 4>(plan_smem(F)) && attr_and_occupancy<EPI_LSTM_BWD, 5, 4>(plan_smem(B)); break;
+    }
+  } else {
+    occ = attr_and_occupancy<EPI_FC_FWD, 1, 1>(plan_smem(F)) && attr_and_occupancy<EPI_FC_BWD, 2, 1>(plan_smem(B));
+  }
+  if (!occ) { delete ps; *why = "occupancy"; return nullptr; }
+  ps->fwd = F;
+  ps->bwd = B;
+  return ps;
+}
+
+void persist_destroy(PersistState* ps) { delete ps; }
+
+std::string persist_describe(const PersistState* ps) {
+  const PPlan& F = ps->fwd;
+  const PPlan& B = ps->bwd;
+  return "persistent: grid " + std::to_string(F.nub * F.R) + " (units/CTA " + std::to_string(F.UG) + ", replicas " +
+         std::to_string(F.R) + "), stages fwd " + std::to_string(F.S) + " bwd " + std::to_string(B.S);
+}
+
+void persist_forward(const Dev& D, PersistState* ps, int T, cudaStream_t s) {
+  if (T <= 1) return;
+  const PPlan& P = ps->fwd;
+  if (D.cell == CAVS_CELL_TREE_LSTM) {
+    switch (D.N) {
+      case 1: launch_p<EPI_LSTM_FWD, 4, 1>(ps->A_fwd, ps->B_hk, D, P, 1, T - 1, 1, s); break;
+      case 2: launch_p<EPI_LSTM_FWD, 5, 2>(ps->A_fwd, ps->B_hk, D, P, 1, T - 1, 1, s); break;
+      case 3: launch_p<EPI_LSTM_FWD, 6, 3>(ps->A_fwd, ps->B_hk, D, P, 1, T - 1, 1, s); break;
+      default: launch_p<EPI_LSTM_FWD, 7, 4>(ps->A_fwd, ps->B_hk, D, P, 1, T - 1, 1, s); break;
+    }
+  } else {
+    launch_p<EPI_FC_FWD, 1, 1>(ps->A_fwd, ps->B_hk, D, P, 1, T - 1, 1, s);
+  }
+}
+
+void persist_backward(const Dev& D, PersistState* ps, int T, cudaStream_t s) {
+  if (T <= 1) return;
+  const PPlan& P = ps->bwd;
+  if (D.cell == CAVS_CELL_TREE_LSTM) {
+    switch (D.N) {
+      case 1: launch_p<EPI_LSTM_BWD, 2, 1>(ps->A_bwd, ps->B_dz, D, P, T - 1, T - 1, -1, s); break;
+      case 2: launch_p<EPI_LSTM_BWD, 3, 2>(ps->A_bwd, ps->B_dz, D, P, T - 1, T - 1, -1, s); break;
+      case 3: launch_p<EPI_LSTM_BWD, 4, 3>(ps->A_bwd, ps->B_dz, D, P, T - 1, T - 1, -1, s); break;
+      default: launch_p<EPI_LSTM_BWD, 5, 4>(ps->A_bwd, ps->B_dz, D, P, T - 1, T - 1, -1, s); break;
+    }
+  } else {
+    launch_p<EPI_FC_BWD, 2, 1>(ps->A_bwd, ps->B_dz, D, P, T - 1, T - 1, -1, s);
+  }
+}
+
+}  // namespace cavs

@@ -1,0 +1,19 @@
+// persist.h — persistent weight-stationary level kernels (BF16 mode), see persist.cu.
+#pragma once
+#include <string>
+
+#include "kernels.h"
+
+namespace cavs {
+
+struct PersistState;
+// nullptr (+ reason) when the shape / device does not admit the persistent path.
+PersistState* persist_init(const Dev& D, int max_vertices, std::string* why);
+void persist_destroy(PersistState* ps);
+// All tasks t = 1 .. T-1 (forward) / T-1 .. 1 (backward) in one launch.
+void persist_forward(const Dev& D, PersistState* ps, int T, cudaStream_t s);
+void persist_backward(const Dev& D, PersistState* ps, int T, cudaStream_t s);
+// short description of the plan ("R=9 nub=16 S=3 ...")
+std::string persist_describe(const PersistState* ps);
+
+}  // namespace cavs

@@ -25,6 +25,7 @@
 #include <cstdlib>
 
 #include "cells.cuh"
+#include "persist.h"
 #include "ptx.cuh"
 #include "tc.h"
 
@@ -407,6 +408,8 @@ struct TcState {
   CUtensorMap M_dz, M_hk, M_xp;
   bool use_simt = false;
   bool mono = false;            // CAVS_TC_MONO=1: one CTA per 128-unit block for the levels too
+  PersistState* ps = nullptr;   // persistent weight-stationary level kernels (persist.cu), if the shape admits
+  std::string info;
 };
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -467,11 +470,24 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
     delete t;
     return CAVS_E_CUDA;
   }
+  if (t->use_simt) t->info = "levels: SIMT FFMA (CAVS_BF16_SIMT=1)";
+  else if (t->mono) t->info = "levels: per-task tcgen05, monolithic CTAs (CAVS_TC_MONO=1)";
+  else {
+    std::string why;
+    t->ps = persist_init(D, max_vertices, &why);
+    t->info = t->ps ? "levels: " + persist_describe(t->ps)
+                    : "levels: per-task tcgen05 launches (persistent path unavailable: " + why + ")";
+  }
   *out = t;
   return CAVS_OK;
 }
 
-void tc_destroy(TcState* tc) { delete tc; }
+std::string tc_describe(const TcState* tc) { return tc ? tc->info : std::string("levels: FP32 FFMA"); }
+
+void tc_destroy(TcState* tc) {
+  if (tc && tc->ps) persist_destroy(tc->ps);
+  delete tc;
+}
 
 // ---- type-I plans ---------------------------------------------------------------------
 static PlanT plan_empty() {
@@ -692,6 +708,7 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
     launch_level<EPI_LSTM_XPROJ, 4, 1>(t->A[1], t->A[1], t->B_xp, D, mono_lstm_xproj(h, d), 0, D.V, h, s);
     P.count(1);
     P.mark(CAVS_PH_FWD_LEVELS, s);
+    if (t->ps) { if (T > 1) { persist_forward(D, t->ps, T, s); P.count(1); } return; }
     const PlanT F = gs ? gs_lstm_fwd(h, N) : mono_lstm_fwd(h, N);
     for (int tt = 1; tt < T; ++tt) {
       if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_FWD, Fs, lp[tt], lp[tt + 1], h, s);
@@ -702,6 +719,7 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
     launch_level<EPI_FC_XPROJ, 1, 1>(t->A[1], t->A[1], t->B_xp, D, mono_one(d, 1, &zero, &zero), 0, D.V, h, s);
     P.count(1);
     P.mark(CAVS_PH_FWD_LEVELS, s);
+    if (t->ps) { if (T > 1) { persist_forward(D, t->ps, T, s); P.count(1); } return; }
     PlanT F;
     if (gs) { F = plan_empty(); gs_add_ksplit(F, 0, 0, 0, 0, 2 * h, 0); }
     else F = mono_one(2 * h, 1, &zero, &zero);
@@ -743,7 +761,9 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
   const SegListI Bs = bwd_segments(D);
   // rows past V of dZ are read by the lazy GEMMs' last k-block: keep them zero
   cudaMemsetAsync(reinterpret_cast<__nv_bfloat16*>(D.dZ) + (size_t)D.V * G * h, 0, (size_t)64 * G * h * 2, s);
-  if (lstm) {
+  if (t->ps) {
+    if (T > 1) { persist_backward(D, t->ps, T, s); P.count(1); }
+  } else if (lstm) {
     const PlanT B = gs ? gs_lstm_bwd(h, N) : mono_lstm_bwd(h, N);
     for (int tt = T - 1; tt >= 1; --tt) {
       if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_BWD, Bs, lp[tt], lp[tt + 1], h, s);

@@ -14,5 +14,6 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
 void tc_forward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, Prof& P);
 void tc_backward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, int* split /*[3]*/, Prof& P);
 void tc_destroy(TcState* tc);
+std::string tc_describe(const TcState* tc);   // which level-kernel path is active
 
 }  // namespace cavs

@@ -262,9 +262,73 @@ def test_gate_split_cluster_matches_monolithic(case, monkeypatch):
     """The 4-CTA gate-split cluster kernels against the one-CTA-per-unit-block kernels:
     identical operands and rounding points, different fp32 summation order only."""
     b = BF16_CASES[case]()
+    monkeypatch.setenv("CAVS_PERSIST", "0")
     monkeypatch.setenv("CAVS_TC_MONO", "1")
     m = run_gpu(b, "bf16")
     monkeypatch.setenv("CAVS_TC_MONO", "0")
     g = run_gpu(b, "bf16")
     from gpu_harness import compare
     compare(b, g, m, 1e-3, case + " gate-split vs monolithic")
+
+
+# ------------------------------------------------------------------ persistent level kernel
+def _nary_forest(K, N, max_leaves, seed):
+    """Random trees whose internal vertices have 1..N children (children before parents)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(K):
+        nodes = [[] for _ in range(int(rng.integers(1, max_leaves + 1)))]
+        frontier = list(range(len(nodes)))
+        while len(frontier) > 1:
+            k = int(rng.integers(1, min(N, len(frontier)) + 1))
+            pick = sorted(rng.choice(len(frontier), size=k, replace=False).tolist(), reverse=True)
+            ch = [frontier.pop(i) for i in pick]
+            nodes.append(ch)
+            frontier.append(len(nodes) - 1)
+        out.append(gen.permute(nodes, rng))
+    return out
+
+
+PERSIST_CASES = {
+    # h = 512: 16 unit blocks x 9 replicas; NT = 16/32/64 across the levels
+    "lstm_n2_h512_sst": lambda: gen.make_batch("tree_lstm", 2, 512, 512, "sst_tree", 40, seed=21),
+    # h = 256, 2 rounds of NT = 64 tiles per task (600 chains of 3 > 64 x 18 replicas / 2)
+    "lstm_n1_h256_wide": lambda: gen.batch_from_graphs([gen.chain(3)] * 1300, cell="tree_lstm", N=1, h=256, d=128,
+                                                        seed=22, x_at="all", loss_at="all"),
+    # 300 tasks in one launch: 299 grid barriers
+    "lstm_n1_h64_deep": lambda: gen.batch_from_graphs([gen.chain(300), gen.chain(120)], cell="tree_lstm", N=1,
+                                                       h=64, d=64, seed=23, x_at="all", loss_at="all"),
+    "lstm_n3_h128": lambda: gen.batch_from_graphs(_nary_forest(30, 3, 20, 24), cell="tree_lstm", N=3, h=128, d=64,
+                                                  seed=24),
+    "lstm_n4_h512": lambda: gen.batch_from_graphs(_nary_forest(12, 4, 24, 25), cell="tree_lstm", N=4, h=512, d=128,
+                                                  seed=25),
+    "lstm_unary_h128": lambda: gen.batch_from_graphs(
+        [[[], [], [0, 1], [], [3], [2, 4], [], [6]]] * 9, cell="tree_lstm", N=2, h=128, d=64, seed=26,
+        x_at="all", loss_at="all"),
+    "fc_h256_cbt": lambda: gen.make_batch("tree_fc", 2, 256, 128, "cbt32", 12, seed=27),
+    "fc_h512_sst": lambda: gen.make_batch("tree_fc", 2, 512, 256, "sst_tree", 24, seed=28),
+}
+
+
+@pytest.mark.parametrize("case", list(PERSIST_CASES))
+def test_persistent_levels(case, monkeypatch):
+    """One persistent weight-stationary launch per pass (persist.cu) against the oracle, and
+    against the per-task launches (CAVS_PERSIST=0: same operands and rounding points)."""
+    b = PERSIST_CASES[case]()
+    monkeypatch.setenv("CAVS_PERSIST", "1")
+    g = run_gpu(b, "bf16")
+    assert "levels: persistent" in g["ctx"].path_info(), g["ctx"].path_info()
+    compare(b, g, run_oracle(b), BF16_TOL, case + " vs fp64 oracle")
+    # deep / wide trees: single-ulp bf16 rounding flips of h (different fp32 summation order than
+    # the emulating oracle's) accumulate in the weight gradients; still 2x inside the 2e-2 gate
+    compare(b, g, run_oracle(b, emulate_bf16=True), 2 * BF16_EMU_TOL, case + " vs bf16-emulating oracle")
+    monkeypatch.setenv("CAVS_PERSIST", "0")
+    o = run_gpu(b, "bf16")
+    assert "levels: persistent" not in o["ctx"].path_info()
+    compare(b, g, o, BF16_EMU_TOL, case + " persistent vs per-task")
+
+
+def test_persistent_path_is_default_for_benchmark_shape():
+    b = gen.make_batch("tree_lstm", 2, 512, 512, "sst_tree", 4, seed=1)
+    ctx = make_ctx(b, "bf16")
+    assert "levels: persistent" in ctx.path_info()
