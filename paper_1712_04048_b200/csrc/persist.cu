@@ -42,6 +42,7 @@ constexpr int kPEpi0 = 4;            // first epilogue warp
 constexpr int kPKb = 16384;          // one resident A k-block: 128 rows x 128 B (SW128, K-major)
 constexpr int kPStage = 16384;       // one B box
 constexpr int kPMaxNT = 64;
+constexpr int kPMaxS = 12;           // B pipeline stages (TMEM-resident weights free the smem)
 
 struct PPlan {
   int UG, ngrp, nkbA;                // units per CTA, row groups, resident k-blocks (K = 64 nkbA)
@@ -52,6 +53,9 @@ struct PPlan {
   int ne, e_n[8], e_slot[8][3];      // epilogue accumulator e = sum of slots
   int S;                             // B pipeline stages
   int sk[3];                         // k-blocks per B box for NT = 16 / 32 / 64
+  int tsA;                           // 1: weights resident in TMEM (A operand from TMEM), 0: in smem
+  int acc0;                          // first TMEM column of the accumulators
+  int max_ni;                        // largest task tile index (NT = 16 << ni) the TMEM budget admits
   int nub, R;
   int xs_off, meta_off, bar_off;
 };
@@ -80,9 +84,9 @@ __device__ __forceinline__ void pwait_warp(uint64_t* bar, uint32_t parity) {
   __syncwarp();
 }
 
-__device__ __forceinline__ int nt_index(int M, int R) {
+__device__ __forceinline__ int nt_index(int M, int R, int max_ni) {
   const int n = (M + R - 1) / R;
-  return n <= 16 ? 0 : n <= 32 ? 1 : 2;
+  return min(max_ni, n <= 16 ? 0 : n <= 32 ? 1 : 2);
 }
 
 // Grid barrier (all CTAs co-resident by construction: cooperative launch).  Monotonic arrival
@@ -139,41 +143,50 @@ __device__ __forceinline__ void ptrace(const Dev& D, unsigned long long a, unsig
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t lo) {
   return ((uint64_t)((1024u >> 4) | (1u << 14) | (2u << 29)) << 32) | lo;   // SBO 1024, version 1, SWIZZLE_128B
 }
-template <int NT>
+template <int NT, bool TS>
 __device__ __forceinline__ void mma_level(const PPlan& P, int r, int ntile, uint32_t a_lo, uint32_t b_lo,
                                           uint64_t* full, uint64_t* empty, uint64_t* done, uint64_t* tmem_empty,
                                           int& step, int& tcount, unsigned long long* tr) {
+  // Whole warp runs the loop (warp-uniform operands live in uniform registers); one elected
+  // lane issues each box's MMAs + commit.
   constexpr uint32_t idesc = ptx::idesc_bf16(128, NT, 0, 0);
   constexpr int ni = NT == 16 ? 0 : NT == 32 ? 1 : 2;
   const int sk = P.sk[ni], nbox = P.nkbA / sk, S = P.S;
   for (int j = r; j < ntile; j += P.R, ++tcount) {
-    if (tcount > 0) { pwait(tmem_empty, (tcount - 1) & 1); ptx::tc_fence_after(); }
+    if (tcount > 0) { pwait_warp(tmem_empty, (tcount - 1) & 1); ptx::tc_fence_after(); }
     uint32_t written = 0;
     for (int sg = 0; sg < P.nseg; ++sg) {
       const int acc = P.seg_acc[sg];
-      const uint32_t d = (uint32_t)(acc * NT);
+      const uint32_t d = (uint32_t)(P.acc0 + acc * NT);
       for (int b = 0; b < nbox; ++b, ++step) {
         const int s = step % S;
-        pwait(&full[s], (step / S) & 1);
+        pwait_warp(&full[s], (step / S) & 1);
         ptx::tc_fence_after();
         if (tr && tr[0] == 0) tr[0] = gtime();
-        uint32_t al = a_lo + (uint32_t)(b * sk) * (kPKb >> 4);
-        uint32_t bl = b_lo + (uint32_t)s * (kPStage >> 4);
-        uint32_t acc_flag = (written >> acc) & 1u;
-        for (int kb = 0; kb < sk; ++kb) {
+        if (ptx::elect_one()) {
+          uint32_t al = a_lo + (uint32_t)(b * sk) * (kPKb >> 4);
+          uint32_t bl = b_lo + (uint32_t)s * (kPStage >> 4);
+          uint32_t acc_flag = (written >> acc) & 1u;
+          uint32_t at = (uint32_t)(b * sk) * 32u;             // TMEM column of the weights' k-block
+          for (int kb = 0; kb < sk; ++kb) {
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            ptx::mma_bf16(d, sw128_desc(al + kk * 2), sw128_desc(bl + kk * 2), idesc, acc_flag);
-            acc_flag = 1u;
+            for (int kk = 0; kk < 4; ++kk) {
+              if constexpr (TS) ptx::mma_bf16_ts(d, at + kk * 8, sw128_desc(bl + kk * 2), idesc, acc_flag);
+              else ptx::mma_bf16(d, sw128_desc(al + kk * 2), sw128_desc(bl + kk * 2), idesc, acc_flag);
+              acc_flag = 1u;
+            }
+            al += kPKb >> 4;
+            at += 32;
+            bl += (NT * 128) >> 4;
           }
-          al += kPKb >> 4;
-          bl += (NT * 128) >> 4;
+          ptx::mma_commit(&empty[s]);
         }
+        __syncwarp();
         written |= 1u << acc;
-        ptx::mma_commit(&empty[s]);
       }
     }
-    ptx::mma_commit(done);
+    if (ptx::elect_one()) ptx::mma_commit(done);
+    __syncwarp();
     if (tr && tr[1] == 0) tr[1] = gtime();
   }
 }
@@ -190,15 +203,16 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   using L = PLay<E, NM>;
   static_assert(L::NE == NE, "epilogue accumulator count");
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + P.nkbA * kPKb;
+  uint8_t* sA = smem;                                           // weights as loaded by TMA
+  uint8_t* sB = P.tsA ? smem : smem + P.nkbA * kPKb;            // TMEM weights: stages reuse sA
   float* xs = reinterpret_cast<float*>(smem + P.xs_off);        // [nslot][64][UG]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + P.bar_off);
-  uint64_t* empty = full + kPProd;
-  uint64_t* done = empty + kPProd;
+  uint64_t* empty = full + kPMaxS;
+  uint64_t* done = empty + kPMaxS;
   uint64_t* tmem_empty = done + 1;
   uint64_t* abar = tmem_empty + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(abar + 1);
+  uint64_t* acopy = abar + 1;                                   // weights copied smem -> TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acopy + 1);
   volatile int* gate = reinterpret_cast<volatile int*>(tmem_slot + 1);
   __shared__ unsigned long long s_tmax;                          // debug trace only
 
@@ -213,6 +227,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
     ptx::mbar_init(done, 1);
     ptx::mbar_init(tmem_empty, 8);
     ptx::mbar_init(abar, P.ngrp);
+    ptx::mbar_init(acopy, 1);
     *gate = 0;
     ptx::fence_mbar_init();
   }
@@ -234,12 +249,13 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
           ptx::tma_load_2d(sA + kb * kPKb + g * P.UG * 128, ma, P.grp_col0[g] + kb * 64, P.grp_row0[g] + u0, abar);
       }
       ptx::tma_prefetch(&mb16); ptx::tma_prefetch(&mb32); ptx::tma_prefetch(&mb64);
+      if (P.tsA) pwait(acopy, 0);                     // stages overlay the weights' staging area
       ptx::griddep_wait();                            // task rows come from the previous kernels
       int step = 0;
       for (int i = 0; i < nlev; ++i) {
         const int t = t_first + i * dir;
         const int lo = lp[t], M = lp[t + 1] - lo;
-        const int ni = nt_index(M, P.R), nt = 16 << ni;
+        const int ni = nt_index(M, P.R, P.max_ni), nt = 16 << ni;
         const int ntile = (M + nt - 1) / nt;
         if (r >= ntile) continue;
         const CUtensorMap* mb = ni == 0 ? &mb16 : ni == 1 ? &mb32 : &mb64;
@@ -257,7 +273,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
           for (int sg = 0; sg < P.nseg; ++sg) {
             for (int b = 0; b < nbox; ++b, ++step) {
               const int s = step % S;
-              if (s != w) continue;
+              if (s % kPProd != w) continue;
               const uint32_t ph = (step / S) & 1;
               if (step >= S) pwait(&empty[s], ph ^ 1);
               ptx::mbar_arrive_expect_tx(&full[s], bytes);
@@ -270,27 +286,46 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
     __syncwarp();
   } else if (warp == kPMma) {
     // ------------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    {
       // The CTA is alone on its SM (shared memory) and owns all 512 TMEM columns, so the
       // allocation starts at column 0: accumulator addresses are then warp-uniform constants
       // (no per-MMA register->uniform waterfall in the issue loop).
       if (tmem != 0) __trap();
-      pwait(abar, 0);
+      pwait_warp(abar, 0);
       ptx::tc_fence_after();
+      if (P.tsA) {                                    // weights -> TMEM columns [0, 32 nkbA)
+        if (ptx::elect_one()) {
+          for (int kb = 0; kb < P.nkbA; ++kb)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              ptx::tmem_cp_128x256b((uint32_t)(kb * 32 + kk * 8),
+                                    sw128_desc(((ptx::smem_u32(sA + kb * kPKb + kk * 32) >> 4) & 0x3FFF) | (1u << 16)));
+          ptx::mma_commit(acopy);
+        }
+        __syncwarp();
+        pwait_warp(acopy, 0);
+        ptx::tc_fence_after();
+      }
       const uint32_t a_lo = ((ptx::smem_u32(sA) >> 4) & 0x3FFF) | (1u << 16);
       const uint32_t b_lo = ((ptx::smem_u32(sB) >> 4) & 0x3FFF) | (1u << 16);
       int step = 0, tcount = 0;
       for (int i = 0; i < nlev; ++i) {
         const int t = t_first + i * dir;
         const int M = lp[t + 1] - lp[t];
-        const int ni = nt_index(M, P.R), nt = 16 << ni;
+        const int ni = nt_index(M, P.R, P.max_ni), nt = 16 << ni;
         const int ntile = (M + nt - 1) / nt;
         unsigned long long trm[2] = {0, 0};
         unsigned long long* tr = D.trace ? trm : nullptr;
-        if (ni == 0) mma_level<16>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
-        else if (ni == 1) mma_level<32>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
-        else mma_level<64>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
-        if (D.trace && r < ntile) ptrace(D, 4000 + E, blockIdx.x, i, trm[0], trm[1], 0, nt, 0);
+        if (P.tsA) {
+          if (ni == 0) mma_level<16, true>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
+          else if (ni == 1) mma_level<32, true>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
+          else mma_level<64, true>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
+        } else {
+          if (ni == 0) mma_level<16, false>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
+          else if (ni == 1) mma_level<32, false>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
+          else mma_level<64, false>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
+        }
+        if (D.trace && r < ntile && lane == 0) ptrace(D, 4000 + E, blockIdx.x, i, trm[0], trm[1], 0, nt, 0);
       }
     }
     __syncwarp();
@@ -308,7 +343,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
     for (int i = 0; i < nlev; ++i) {
       const int t = t_first + i * dir;
       const int lo = lp[t], M = lp[t + 1] - lo;
-      const int ni = nt_index(M, P.R), nt = 16 << ni;
+      const int ni = nt_index(M, P.R, P.max_ni), nt = 16 << ni;
       const int ntile = (M + nt - 1) / nt;
       unsigned long long tr0 = 0, tr1 = 0, tr2 = 0, tr3 = 0;
       if (D.trace && et == 0) tr0 = gtime();
@@ -337,7 +372,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
         pwait_warp(done, tcount & 1);
         if (D.trace && et == 0 && tr1 == 0) tr1 = gtime();
         ptx::tc_fence_after();
-        const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+        const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)P.acc0;
 #pragma unroll
         for (int s = 0; s < L::NSLOT; ++s) {
           constexpr int UG = L::UG;
@@ -472,18 +507,33 @@ static void plan_e(PPlan& P, int n, const int* slots) {
   for (int z = 0; z < n; ++z) P.e_slot[e][z] = slots[z];
 }
 
-// smem offsets + pipeline depth; false if the plan does not fit one CTA
-static bool plan_layout(PPlan& P) {
+// smem offsets, pipeline depth, TMEM budget; false if the plan does not fit one CTA.
+// tsA: the weights are staged once through smem and copied into TMEM columns [0, 32 nkbA),
+// the accumulators follow; the B stages then reuse the staging area.
+static bool plan_layout(PPlan& P, bool tsA) {
   const int A = P.nkbA * kPKb;
   const int xs = P.nslot * kPMaxNT * P.UG * 4;
-  const int meta = 0;
-  const int fixed = 1024 + A + xs + meta + 256;
-  const int S = std::min(kPProd, (232448 - fixed) / kPStage);
+  const int avail = 232448 - 1024 - xs - 256 - 2 * kPMaxS * 8 - 64;
+  P.tsA = tsA ? 1 : 0;
+  int S;
+  if (tsA) {
+    S = std::min(kPMaxS, avail / kPStage);
+    if (S * kPStage < A) return false;
+    P.acc0 = P.nkbA * 32;
+    P.xs_off = S * kPStage;
+  } else {
+    S = std::min(kPProd, (avail - A) / kPStage);
+    P.acc0 = 0;
+    P.xs_off = A + S * kPStage;
+  }
   if (S < 2) return false;
   P.S = S;
-  P.xs_off = A + S * kPStage;
+  P.max_ni = -1;
+  for (int i = 0; i < 3; ++i)
+    if (P.acc0 + P.nacc * (16 << i) <= 512) P.max_ni = i;
+  if (P.max_ni < 0) return false;
   P.meta_off = P.xs_off + xs;
-  P.bar_off = (P.meta_off + meta + 15) & ~15;
+  P.bar_off = (P.meta_off + 15) & ~15;
   for (int i = 0; i < 3; ++i) {                       // largest divisor of nkbA with a <= 16 KB box
     const int cap = kPStage / ((16 << i) * 128);
     int sk = 1;
@@ -493,7 +543,7 @@ static bool plan_layout(PPlan& P) {
   }
   return true;
 }
-static int plan_smem(const PPlan& P) { return 1024 + P.bar_off + 128; }
+static int plan_smem(const PPlan& P) { return 1024 + P.bar_off + 2 * kPMaxS * 8 + 64; }
 
 template <int E, int NE, int NM>
 static bool attr_and_occupancy(int smem) {
@@ -606,8 +656,9 @@ PersistState* persist_init(const Dev& D, int max_vertices, std::string* why) {
     plan_slot(B, 0, 1, &a0); plan_slot(B, 1, 1, &a0);
     plan_e(B, 1, &a0); plan_e(B, 1, &a1);
   }
-  if (!plan_layout(F) || !plan_layout(B)) { delete ps; *why = "does not fit shared memory"; return nullptr; }
-  if (F.nacc * kPMaxNT > 512 || B.nacc * kPMaxNT > 512) { delete ps; *why = "TMEM"; return nullptr; }
+  const char* ss = std::getenv("CAVS_PERSIST_SS");    // 1: weights in smem (SS MMA) instead of TMEM
+  const bool tsA = !(ss && ss[0] == '1');
+  if (!plan_layout(F, tsA) || !plan_layout(B, tsA)) { delete ps; *why = "does not fit shared memory / TMEM"; return nullptr; }
   for (int i = 0; i < 3; ++i) {
     ok &= enc3(&ps->B_hk[i], D.Hk, (uint64_t)N * h, Vp, 16u << i, F.sk[i]);
     ok &= enc3(&ps->B_dz[i], D.dZ, (uint64_t)G * h, Vp, 16u << i, B.sk[i]);
@@ -637,7 +688,9 @@ std::string persist_describe(const PersistState* ps) {
   const PPlan& F = ps->fwd;
   const PPlan& B = ps->bwd;
   return "persistent: grid " + std::to_string(F.nub * F.R) + " (units/CTA " + std::to_string(F.UG) + ", replicas " +
-         std::to_string(F.R) + "), stages fwd " + std::to_string(F.S) + " bwd " + std::to_string(B.S);
+         std::to_string(F.R) + "), weights in " + (F.tsA ? "TMEM" : "smem") + ", stages fwd " + std::to_string(F.S) +
+         " bwd " + std::to_string(B.S) + ", max task tile fwd " + std::to_string(16 << F.max_ni) + " bwd " +
+         std::to_string(16 << B.max_ni);
 }
 
 void persist_forward(const Dev& D, PersistState* ps, int T, cudaStream_t s) {
