@@ -240,7 +240,7 @@ def main():
         p = pool[i % len(pool)]
         V = p["cp"].shape[0] - 1
         ctx.load_graphs(p["gp"], p["cp"], p["ci"])
-        ctx.schedule()
+        ctx.schedule(wait=False)            # header consumed inside forward, overlapping the pull
         ctx.forward(params, p["x"], p["xr"], h_out[:V])
         ctx.backward(p["g"], dparams, dx[:p["x"].shape[0]])
         if world > 1:

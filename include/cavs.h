@@ -15,9 +15,11 @@
  *  - Every call returns a cavs_status; CAVS_OK == 0.  No exceptions, abort or
  *    exit cross this boundary.  cavs_last_error() gives a message.
  *  - All device work is enqueued on the context's CUDA stream (cavs_create /
- *    cavs_set_stream) and is asynchronous, EXCEPT cavs_schedule, which reads
- *    back a small header (status word, T, level_ptr[0..T]) and synchronises the
- *    stream once, and the *_host entry points, which synchronise at the end.
+ *    cavs_set_stream) and is asynchronous, EXCEPT: cavs_schedule with T_out != NULL
+ *    waits for a small header (status word, T, level_ptr[0..T]) read back from the
+ *    device; with T_out == NULL the header is read back asynchronously and consumed by
+ *    the next cavs_forward (after it has enqueued the pull, so the wait overlaps device
+ *    work) or cavs_get_schedule; the *_host entry points synchronise at the end.
  *  - The library never allocates device memory: all scratch is carved from one
  *    caller-owned device buffer (cavs_set_workspace).  The caller (PyTorch in
  *    this repo) owns memory, streams and process groups.
@@ -120,8 +122,10 @@ cavs_status cavs_load_graphs(cavs_ctx* ctx, int32_t K, int32_t V, int32_t E,
  * children, else 1 + max over children; V_t = {v : level(v) = t} ordered by ascending
  * global id; T = number of tasks.  Also builds the dynamic-tensor plan (positions,
  * child/parent slots; Fig. 7, Alg. 2).  Validates the graphs.
- * Synchronises the stream once (reads back status, T and level_ptr).
- * `T_out` may be NULL.
+ * T_out != NULL: waits for the header (status, T, level_ptr) and returns T and the graphs'
+ * validation errors here.  T_out == NULL: returns after enqueueing; the validation errors
+ * are then returned by the next cavs_forward / cavs_get_schedule (which consume the header)
+ * and the context falls back to LOADED.
  * Errors: CAVS_E_STATE (nothing loaded), CAVS_E_INVALID, CAVS_E_ARITY, CAVS_E_CYCLE,
  *         CAVS_E_FANOUT, CAVS_E_CUDA. */
 cavs_status cavs_schedule(cavs_ctx* ctx, int32_t* T_out);

@@ -166,7 +166,13 @@ class Context:
                                           _ptr(child_idx) if E else None, 1 if on_dev else 0))
         self.V, self.K = V, K
 
-    def schedule(self) -> int:
+    def schedule(self, wait: bool = True):
+        """Algorithm 1's task partition.  wait=True returns T (and raises on invalid graphs);
+        wait=False only enqueues — T and validation errors surface at the next forward()."""
+        if not wait:
+            self._check(_lib.cavs_schedule(self._ctx, None))
+            self.T = None
+            return None
         T = ctypes.c_int32()
         self._check(_lib.cavs_schedule(self._ctx, ctypes.byref(T)))
         self.T = int(T.value)

@@ -36,6 +36,8 @@ struct cavs_ctx {
   float *s_params = nullptr, *s_x = nullptr, *s_dh = nullptr, *s_dp = nullptr, *s_dx = nullptr, *s_hout = nullptr;
   int *s_xrow = nullptr, *s_gp = nullptr, *s_cp = nullptr, *s_ci = nullptr;
   TcState* tc = nullptr;        // tensor-core (BF16) path state: TMA descriptors
+  cudaEvent_t ev_hdr = nullptr; // recorded after the schedule header's device->host copy
+  bool hdr_pending = false;     // header copied asynchronously, not parsed yet
 };
 
 static constexpr int kHdrWords = 4;
@@ -189,24 +191,18 @@ CAVS_API cavs_status cavs_load_graphs(cavs_ctx* ctx, int32_t K, int32_t V, int32
   if (E > 0) CK(cudaMemcpyAsync((void*)D.child_idx, child_idx, sizeof(int) * E, kind, ctx->stream));
   D.K = K; D.V = V; D.E = E;
   ctx->state = S_LOADED;
+  ctx->hdr_pending = false;
   return CAVS_OK;
 }
 
-CAVS_API cavs_status cavs_schedule(cavs_ctx* ctx, int32_t* T_out) {
-  if (!ctx) return CAVS_E_INVALID;
-  if (ctx->state < S_LOADED) return fail(ctx, CAVS_E_STATE, "no graphs loaded");
-  CK(cudaSetDevice(ctx->device));
+// Wait for the schedule header (status, T, #roots, level_ptr) copied by cavs_schedule and
+// parse it; reports the graphs' validation errors.  No-op when already parsed.
+static cavs_status finish_schedule(cavs_ctx* ctx) {
+  if (!ctx->hdr_pending) return CAVS_OK;
+  ctx->hdr_pending = false;
+  CK(cudaEventSynchronize(ctx->ev_hdr));
   Dev& D = ctx->D;
-  CK(cudaMemsetAsync(D.hdr, 0, sizeof(int) * kHdrWords, ctx->stream));
-  CK(cudaMemsetAsync(D.cnt, 0, sizeof(int) * (D.V + 1), ctx->stream));
-  ctx->prof.mark(CAVS_PH_SCHEDULE, ctx->stream);
-  launch_schedule(D, ctx->stream);
-  ctx->prof.count(5);
-  ctx->prof.mark(-1, ctx->stream);
-  CK(cudaGetLastError());
   const int nread = kHdrWords + std::min(D.V + 1, kReadback);
-  CK(cudaMemcpyAsync(ctx->h_hdr, D.hdr, sizeof(int) * nread, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
   const int st = ctx->h_hdr[0];
   if (st) {
     ctx->state = S_LOADED;
@@ -226,8 +222,32 @@ CAVS_API cavs_status cavs_schedule(cavs_ctx* ctx, int32_t* T_out) {
   }
   D.T = T;
   D.lp1 = T > 1 ? ctx->lp[1] : D.V;
+  return CAVS_OK;
+}
+
+CAVS_API cavs_status cavs_schedule(cavs_ctx* ctx, int32_t* T_out) {
+  if (!ctx) return CAVS_E_INVALID;
+  if (ctx->state < S_LOADED) return fail(ctx, CAVS_E_STATE, "no graphs loaded");
+  CK(cudaSetDevice(ctx->device));
+  Dev& D = ctx->D;
+  CK(cudaMemsetAsync(D.hdr, 0, sizeof(int) * kHdrWords, ctx->stream));
+  CK(cudaMemsetAsync(D.cnt, 0, sizeof(int) * (D.V + 1), ctx->stream));
+  ctx->prof.mark(CAVS_PH_SCHEDULE, ctx->stream);
+  launch_schedule(D, ctx->stream);
+  ctx->prof.count(5);
+  ctx->prof.mark(-1, ctx->stream);
+  CK(cudaGetLastError());
+  const int nread = kHdrWords + std::min(D.V + 1, kReadback);
+  CK(cudaMemcpyAsync(ctx->h_hdr, D.hdr, sizeof(int) * nread, cudaMemcpyDeviceToHost, ctx->stream));
+  if (!ctx->ev_hdr) CK(cudaEventCreateWithFlags(&ctx->ev_hdr, cudaEventDisableTiming));
+  CK(cudaEventRecord(ctx->ev_hdr, ctx->stream));
+  ctx->hdr_pending = true;
   ctx->state = S_SCHEDULED;
-  if (T_out) *T_out = T;
+  if (T_out) {
+    const cavs_status st = finish_schedule(ctx);
+    if (st) return st;
+    *T_out = ctx->T;
+  }
   return CAVS_OK;
 }
 
@@ -235,6 +255,8 @@ CAVS_API cavs_status cavs_get_schedule(cavs_ctx* ctx, int32_t* level, int32_t* l
   if (!ctx) return CAVS_E_INVALID;
   if (ctx->state < S_SCHEDULED) return fail(ctx, CAVS_E_STATE, "not scheduled");
   CK(cudaSetDevice(ctx->device));
+  const cavs_status st = finish_schedule(ctx);
+  if (st) return st;
   CK(cudaStreamSynchronize(ctx->stream));
   const Dev& D = ctx->D;
   if (level) CK(cudaMemcpy(level, D.level, sizeof(int) * D.V, cudaMemcpyDeviceToHost));
@@ -308,6 +330,10 @@ CAVS_API cavs_status cavs_forward(cavs_ctx* ctx, const float* params, int32_t n_
   launch_prep(D, ctx->stream);
   launch_pull(D, ctx->stream);
   P.count(2);
+  {  // a deferred schedule header is consumed here, while prep / pull run on the device
+    const cavs_status st = finish_schedule(ctx);
+    if (st) return st;
+  }
   P.mark(CAVS_PH_XPROJ, ctx->stream);
   if (D.prec == CAVS_BF16) tc_forward(D, ctx->tc, ctx->lp, ctx->stream, P);
   else simt_forward<float>(D, ctx->lp, ctx->stream, P);
@@ -433,6 +459,7 @@ CAVS_API void cavs_destroy(cavs_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream); else cudaDeviceSynchronize();
   tc_destroy(ctx->tc);
+  if (ctx->ev_hdr) cudaEventDestroy(ctx->ev_hdr);
   if (ctx->h_hdr) cudaFreeHost(ctx->h_hdr);
   delete ctx;
 }

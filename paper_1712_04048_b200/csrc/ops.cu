@@ -13,63 +13,66 @@
 
 namespace cavs {
 
+// Parameter repack as a list of jobs, one launch: blockIdx.y = job.  A copy job converts a
+// contiguous fp32 range; a transpose job writes dst[c][r] = src[r][c] (32 x 32 smem tiles, both
+// sides coalesced).  The internal layouts are plain concatenations / transposes of the packed
+// blocks (internal gate order (i, o, u, f); packed W/b order (i, f, o, u)).
+struct PrepJob {
+  const float* src; int rows, cols, spitch;    // source block (row-major fp32)
+  int dst_sel; size_t dst_off; int dpitch;     // destination arena (0..4: Wa..We, 5: bias fp32)
+  int transpose;
+};
+struct PrepJobs { int n; PrepJob j[20]; };
+
 template <class OpT>
-__global__ void k_prep(Dev D) {
-  const int h = D.h, d = D.d, N = D.N;
-  const float* t = D.params;
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
-  const size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (D.cell == CAVS_CELL_TREE_LSTM) {
-    // packed: W[4h x d] rows (i,f,o,u) | U_iou[3h x h] (i,o,u) | U_f[h x h] | b[4h] (i,f,o,u)
-    const float* W = t;
-    const float* Uiou = t + (size_t)4 * h * d;
-    const float* Uf = Uiou + (size_t)3 * h * h;
-    const float* b = Uf + (size_t)h * h;
-    const int blkW[4] = {0, 2, 3, 1};           // internal gate (i,o,u,f) -> packed W/b block
-    OpT* U4 = op<OpT>(D.Wa); OpT* W4 = op<OpT>(D.Wb); OpT* UTiou = op<OpT>(D.Wc);
-    OpT* UTf = op<OpT>(D.Wd); OpT* WT = op<OpT>(D.We);
-    const int G = 3 + N;
-    for (size_t i = i0; i < (size_t)4 * h * h; i += stride) {      // U4[g*h+m][k]
-      const int r = (int)(i / h), k = (int)(i % h), g = r / h, m = r % h;
-      U4[i] = to_op<OpT>(g < 3 ? Uiou[(size_t)(g * h + m) * h + k] : Uf[(size_t)m * h + k]);
-    }
-    for (size_t i = i0; i < (size_t)4 * h * d; i += stride) {      // W4[g*h+m][k]
-      const int r = (int)(i / d), k = (int)(i % d), g = r / h, m = r % h;
-      W4[i] = to_op<OpT>(W[(size_t)(blkW[g] * h + m) * d + k]);
-    }
-    for (size_t i = i0; i < (size_t)3 * h * h; i += stride) {      // UTiou[j][g*h+m] = U_g[m][j]
-      const int j = (int)(i / (3 * h)), c = (int)(i % (3 * h));
-      UTiou[i] = to_op<OpT>(Uiou[(size_t)c * h + j]);
-    }
-    for (size_t i = i0; i < (size_t)h * h; i += stride) {          // UTf[j][m] = U_f[m][j]
-      const int j = (int)(i / h), m = (int)(i % h);
-      UTf[i] = to_op<OpT>(Uf[(size_t)m * h + j]);
-    }
-    for (size_t i = i0; i < (size_t)d * G * h; i += stride) {      // WT[j][g*h+m] = W_g[m][j]
-      const int j = (int)(i / (G * h)), c = (int)(i % (G * h)), g = c / h, m = c % h;
-      WT[i] = to_op<OpT>(W[(size_t)(blkW[g < 3 ? g : 3] * h + m) * d + j]);
-    }
-    for (size_t i = i0; i < (size_t)4 * h; i += stride) {
-      const int g = (int)(i / h), m = (int)(i % h);
-      D.bias[i] = b[blkW[g] * h + m];
+__device__ __forceinline__ OpT* prep_dst(const Dev& D, int sel) {
+  return sel == 0 ? op<OpT>(D.Wa) : sel == 1 ? op<OpT>(D.Wb) : sel == 2 ? op<OpT>(D.Wc) : sel == 3 ? op<OpT>(D.Wd)
+                                                                                          : op<OpT>(D.We);
+}
+
+template <class OpT>
+__global__ void __launch_bounds__(256) k_prep(Dev D, PrepJobs J) {
+  const PrepJob& jb = J.j[blockIdx.y];
+  __shared__ float tile[32][33];
+  if (jb.transpose) {
+    const int tr = cdiv(jb.rows, 32), tc = cdiv(jb.cols, 32);
+    OpT* dst = prep_dst<OpT>(D, jb.dst_sel) + jb.dst_off;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;        // 32 x 8
+    for (int t = blockIdx.x; t < tr * tc; t += gridDim.x) {
+      const int r0 = (t / tc) * 32, c0 = (t % tc) * 32;
+#pragma unroll
+      for (int k = 0; k < 32; k += 8) {
+        const int r = r0 + ty + k, c = c0 + tx;
+        tile[ty + k][tx] = (r < jb.rows && c < jb.cols) ? jb.src[(size_t)r * jb.spitch + c] : 0.f;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 32; k += 8) {
+        const int c = c0 + ty + k, r = r0 + tx;                    // dst row = source column
+        if (r < jb.rows && c < jb.cols) dst[(size_t)c * jb.dpitch + r] = to_op<OpT>(tile[tx][ty + k]);
+      }
+      __syncthreads();
     }
   } else {
-    // packed: W_c[h x 2h] | W_x[h x d] | b[h]
-    const float* Wcp = t;
-    const float* Wx = t + (size_t)2 * h * h;
-    const float* b = Wx + (size_t)h * d;
-    OpT* Wc = op<OpT>(D.Wa); OpT* Wxo = op<OpT>(D.Wb); OpT* WcT = op<OpT>(D.Wc); OpT* WxT = op<OpT>(D.We);
-    for (size_t i = i0; i < (size_t)2 * h * h; i += stride) {
-      Wc[i] = to_op<OpT>(Wcp[i]);
-      const int r = (int)(i / h), m = (int)(i % h);              // WcT[k*h+j][m] = Wc[m][k*h+j]
-      WcT[i] = to_op<OpT>(Wcp[(size_t)m * 2 * h + r]);
+    const size_t n = (size_t)jb.rows * jb.cols;                  // contiguous (spitch == cols)
+    if (jb.dst_sel == 5) {
+      for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        D.bias[jb.dst_off + i] = jb.src[i];
+      return;
     }
-    for (size_t i = i0; i < (size_t)h * d; i += stride) {
-      Wxo[i] = to_op<OpT>(Wx[i]);
-      const int j = (int)(i / h), m = (int)(i % h);              // WxT[j][m] = Wx[m][j]
-      WxT[i] = to_op<OpT>(Wx[(size_t)m * d + j]);
+    OpT* dst = prep_dst<OpT>(D, jb.dst_sel) + jb.dst_off;
+    if ((n & 3) == 0 && ((jb.dst_off & 3) == 0)) {
+      const float4* s4 = reinterpret_cast<const float4*>(jb.src);
+      for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += (size_t)gridDim.x * blockDim.x) {
+        const float4 v = s4[i];
+        FV<4> f;
+        f.v[0] = v.x; f.v[1] = v.y; f.v[2] = v.z; f.v[3] = v.w;
+        stv_op<OpT, 4>(dst + 4 * i, f);
+      }
+    } else {
+      for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = to_op<OpT>(jb.src[i]);
     }
-    for (size_t i = i0; i < (size_t)h; i += stride) D.bias[i] = b[i];
   }
 }
 
@@ -93,14 +96,24 @@ __global__ void k_pull(Dev D) {
   OpT* X = op<OpT>(D.Xp);
   const int d = D.d;
   if ((d & 3) == 0) {
-    const int d4 = d >> 2;
-    for (int e = threadIdx.x; e < 64 * d4; e += blockDim.x) {
-      const int rr = e / d4, k = (e % d4) * 4, p = p0 + rr;
-      if (p >= D.V) break;
-      const int r = s_r[rr];
-      const float4 v = r >= 0 ? *reinterpret_cast<const float4*>(D.x + (size_t)r * d + k) : make_float4(0.f, 0.f, 0.f, 0.f);
-      OpT* o = X + (size_t)p * d + k;
-      o[0] = to_op<OpT>(v.x); o[1] = to_op<OpT>(v.y); o[2] = to_op<OpT>(v.z); o[3] = to_op<OpT>(v.w);
+    // 8 independent 16-byte loads in flight per thread (the copy is latency-bound otherwise)
+    const int d4 = d >> 2, n = 64 * d4;
+    for (int e0 = threadIdx.x; e0 < n; e0 += 8 * blockDim.x) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * blockDim.x, rr = e / d4, k = (e % d4) * 4;
+        const int r = (e < n && p0 + rr < D.V) ? s_r[rr] : -1;
+        v[u] = r >= 0 ? *reinterpret_cast<const float4*>(D.x + (size_t)r * d + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * blockDim.x, rr = e / d4, k = (e % d4) * 4;
+        if (e >= n || p0 + rr >= D.V) continue;
+        FV<4> f;
+        f.v[0] = v[u].x; f.v[1] = v[u].y; f.v[2] = v[u].z; f.v[3] = v[u].w;
+        stv_op<OpT, 4>(X + (size_t)(p0 + rr) * d + k, f);
+      }
     }
   } else {
     for (int e = threadIdx.x; e < 64 * d; e += blockDim.x) {
@@ -120,68 +133,92 @@ __global__ void k_roots(Dev D, int n_roots, const int* roots) {
   }
 }
 
-// part[c][col] = sum over rows of chunk c of dZ[row][col]
+// part[c][col] = sum over rows of chunk c of dZ[row][col].  CTA = 8 warps x 256 columns; a lane
+// owns 8 consecutive columns (one 16-byte bf16 load per row), warp w takes rows w, w+8, ... of
+// the chunk; the 8 warp partials are added in a fixed order (deterministic).
 template <class OpT>
-__global__ void k_colsum(Dev D, float* part, int cols) {
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= cols) return;
+__global__ void __launch_bounds__(256) k_colsum(Dev D, float* part, int cols) {
+  __shared__ float red[8][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = blockIdx.x * 256 + lane * 8;
   const int chunk = cdiv(D.V, gridDim.y);
   const int r0 = blockIdx.y * chunk, r1 = min(D.V, r0 + chunk);
   const OpT* dz = op<OpT>(D.dZ);
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-  int r = r0;
-  for (; r + 3 < r1; r += 4) {
-    s0 += from_op(dz[(size_t)r * cols + col]);
-    s1 += from_op(dz[(size_t)(r + 1) * cols + col]);
-    s2 += from_op(dz[(size_t)(r + 2) * cols + col]);
-    s3 += from_op(dz[(size_t)(r + 3) * cols + col]);
-  }
-  for (; r < r1; ++r) s0 += from_op(dz[(size_t)r * cols + col]);
-  part[(size_t)blockIdx.y * cols + col] = (s0 + s1) + (s2 + s3);
-}
-
-__global__ void k_pack(Dev D, LazyLayout Z, int Su4, int Suf, int Sw, const float* dbp) {
-  const int h = D.h, d = D.d, N = D.N;
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
-  const size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  float* out = D.dparams;
-  const float* u4 = D.lazy + Z.u4;
-  const float* uf = D.lazy + Z.uf;
-  const float* w = D.lazy + Z.w;
-  if (D.cell == CAVS_CELL_TREE_LSTM) {
-    const int G = 3 + N;
-    const size_t nW = (size_t)4 * h * d, nU = (size_t)3 * h * h, nUf = (size_t)h * h;
-    const int intern[4] = {0, 3, 1, 2};         // packed (i,f,o,u) -> internal row block (f: 3..3+N-1)
-    for (size_t i = i0; i < nW + nU + nUf + 4 * h; i += stride) {
-      float v = 0.f;
-      if (i < nW) {
-        const int pg = (int)(i / ((size_t)h * d)); const size_t rest = i % ((size_t)h * d);
-        const int nb = pg == 1 ? N : 1;
-        for (int s = 0; s < Sw; ++s)
-          for (int q = 0; q < nb; ++q) v += w[s * Z.sw + (size_t)(intern[pg] + q) * h * d + rest];
-      } else if (i < nW + nU) {
-        const size_t r = i - nW;
-        for (int s = 0; s < Su4; ++s) v += u4[s * Z.su4 + r];
-      } else if (i < nW + nU + nUf) {
-        const size_t r = i - nW - nU;
-        for (int s = 0; s < Suf; ++s) v += uf[s * Z.suf + r];
-      } else {
-        const size_t r = i - nW - nU - nUf;
-        const int pg = (int)(r / h), m = (int)(r % h);
-        const int nb = pg == 1 ? N : 1;
-        for (int c = 0; c < kDbChunks; ++c)
-          for (int q = 0; q < nb; ++q) v += dbp[(size_t)c * G * h + (size_t)(intern[pg] + q) * h + m];
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  if (c0 + 8 <= cols && sizeof(OpT) == 2) {
+    int r = r0 + warp;
+    for (; r + 24 < r1; r += 32) {                  // 4 rows in flight
+      uint4 u[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) u[k] = *reinterpret_cast<const uint4*>(dz + (size_t)(r + 8 * k) * cols + c0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u[k]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) { const float2 f = __bfloat1622float2(b[e]); acc[2 * e] += f.x; acc[2 * e + 1] += f.y; }
       }
-      out[i] = v;
+    }
+    for (; r < r1; r += 8) {
+      const uint4 u = *reinterpret_cast<const uint4*>(dz + (size_t)r * cols + c0);
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) { const float2 f = __bfloat1622float2(b[e]); acc[2 * e] += f.x; acc[2 * e + 1] += f.y; }
+    }
+  } else if (c0 + 8 <= cols) {
+    for (int r = r0 + warp; r < r1; r += 8) {
+      const OpT* rowp = dz + (size_t)r * cols + c0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += from_op(rowp[e]);
     }
   } else {
-    const size_t swc = Z.su4, swx = Z.sw;
-    for (size_t i = i0; i < swc + swx + h; i += stride) {
-      float v = 0.f;
-      if (i < swc) { for (int s = 0; s < Su4; ++s) v += u4[s * swc + i]; }
-      else if (i < swc + swx) { for (int s = 0; s < Sw; ++s) v += w[s * swx + (i - swc)]; }
-      else { for (int c = 0; c < kDbChunks; ++c) v += dbp[(size_t)c * h + (i - swc - swx)]; }
-      out[i] = v;
+    for (int r = r0 + warp; r < r1; r += 8)
+      for (int e = 0; e < 8 && c0 + e < cols; ++e) acc[e] += from_op(dz[(size_t)r * cols + c0 + e]);
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) red[warp][lane * 8 + e] = acc[e];
+  __syncthreads();
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c < cols) {
+    float v = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
+    part[(size_t)blockIdx.y * cols + c] = v;
+  }
+}
+
+// Packing as segments: out[o0 + e] = sum_{s < S} sum_{q < nb} src[s * sstride + soff + q * qstride + e]
+struct PackSeg { const float* src; size_t sstride, soff, qstride, o0; int S, nb, len; };
+struct PackSegs { int n; PackSeg s[10]; };
+
+__global__ void __launch_bounds__(256) k_pack(Dev D, PackSegs P) {
+  const PackSeg& g = P.s[blockIdx.y];
+  float* out = D.dparams + g.o0;
+  // 4 consecutive outputs per thread and step, float4 loads when aligned; partials of a slot
+  // are loaded together before they are added (fixed order: deterministic)
+  const bool vec = ((g.len | g.sstride | g.soff | g.qstride | g.o0) & 3) == 0;
+  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) * 4; e < g.len; e += gridDim.x * blockDim.x * 4) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < g.S; ++s)
+      for (int q = 0; q < g.nb; ++q) {
+        const float* src = g.src + s * g.sstride + g.soff + q * g.qstride + e;
+        if (vec) {
+          const float4 x = *reinterpret_cast<const float4*>(src);
+          v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
+        } else {
+          v.x += src[0];
+          if (e + 1 < g.len) v.y += src[1];
+          if (e + 2 < g.len) v.z += src[2];
+          if (e + 3 < g.len) v.w += src[3];
+        }
+      }
+    if (vec) *reinterpret_cast<float4*>(out + e) = v;
+    else {
+      out[e] = v.x;
+      if (e + 1 < g.len) out[e + 1] = v.y;
+      if (e + 2 < g.len) out[e + 2] = v.z;
+      if (e + 3 < g.len) out[e + 3] = v.w;
     }
   }
 }
@@ -189,9 +226,40 @@ __global__ void k_pack(Dev D, LazyLayout Z, int Su4, int Suf, int Sw, const floa
 static int grid_for(size_t n, int block) { return (int)std::min<size_t>((n + block - 1) / block, 148 * 16); }
 
 void launch_prep(const Dev& D, cudaStream_t s) {
-  const size_t n = (size_t)4 * D.h * std::max(D.h, D.d) + (size_t)D.d * (3 + D.N) * D.h;
-  if (D.prec == CAVS_BF16) k_prep<__nv_bfloat16><<<grid_for(n, 256), 256, 0, s>>>(D);
-  else k_prep<float><<<grid_for(n, 256), 256, 0, s>>>(D);
+  const size_t h = D.h, d = D.d;
+  const int N = D.N;
+  PrepJobs J{};
+  auto add = [&](const float* src, int rows, int cols, int spitch, int sel, size_t off, int dpitch, int tr) {
+    J.j[J.n++] = PrepJob{src, rows, cols, spitch, sel, off, dpitch, tr};
+  };
+  const float* t = D.params;
+  if (D.cell == CAVS_CELL_TREE_LSTM) {
+    const int G = 3 + N;
+    const float* W = t;                       // [4h x d] blocks (i, f, o, u)
+    const float* Uiou = t + 4 * h * d;        // [3h x h] (i, o, u)
+    const float* Uf = Uiou + 3 * h * h;       // [h x h]
+    const float* b = Uf + h * h;              // [4h] (i, f, o, u)
+    const int blkW[4] = {0, 2, 3, 1};         // internal gate (i, o, u, f) -> packed block
+    add(Uiou, 1, (int)(4 * h * h), 0, 0, 0, 0, 0);                                   // U4 = [U_iou; U_f]
+    for (int g = 0; g < 4; ++g) add(W + blkW[g] * h * d, 1, (int)(h * d), 0, 1, g * h * d, 0, 0);   // W4
+    add(Uiou, (int)(3 * h), (int)h, (int)h, 2, 0, (int)(3 * h), 1);                  // UTiou = U_iou^T
+    add(Uf, (int)h, (int)h, (int)h, 3, 0, (int)h, 1);                                // UTf = U_f^T
+    for (int g = 0; g < G; ++g)                                                      // WT[:, g h] = W_g^T
+      add(W + blkW[g < 3 ? g : 3] * h * d, (int)h, (int)d, (int)d, 4, g * h, G * (int)h, 1);
+    for (int g = 0; g < 4; ++g) add(b + blkW[g] * h, 1, (int)h, 0, 5, g * h, 0, 0);
+  } else {
+    const float* Wc = t;                      // [h x 2h]
+    const float* Wx = t + 2 * h * h;          // [h x d]
+    const float* b = Wx + h * d;
+    add(Wc, 1, (int)(2 * h * h), 0, 0, 0, 0, 0);
+    add(Wx, 1, (int)(h * d), 0, 1, 0, 0, 0);
+    add(Wc, (int)h, (int)(2 * h), (int)(2 * h), 2, 0, (int)h, 1);                    // WcT = W_c^T [2h x h]
+    add(Wx, (int)h, (int)d, (int)d, 4, 0, (int)h, 1);                                // WxT = W_x^T [d x h]
+    add(b, 1, (int)h, 0, 5, 0, 0, 0);
+  }
+  dim3 grid(148, J.n);
+  if (D.prec == CAVS_BF16) k_prep<__nv_bfloat16><<<grid, 256, 0, s>>>(D, J);
+  else k_prep<float><<<grid, 256, 0, s>>>(D, J);
 }
 
 void launch_pull(const Dev& D, cudaStream_t s) {
@@ -207,14 +275,41 @@ void launch_roots(const Dev& D, int n_roots, const int* roots, cudaStream_t s) {
 
 void launch_colsum(const Dev& D, float* part, cudaStream_t s) {
   const int cols = (D.cell == CAVS_CELL_TREE_LSTM ? 3 + D.N : 1) * D.h;
-  dim3 grid(cdiv(cols, 128), kDbChunks);   // 32 deterministic row chunks
-  if (D.prec == CAVS_BF16) k_colsum<__nv_bfloat16><<<grid, 128, 0, s>>>(D, part, cols);
-  else k_colsum<float><<<grid, 128, 0, s>>>(D, part, cols);
+  dim3 grid(cdiv(cols, 256), kDbChunks);   // 32 deterministic row chunks
+  if (D.prec == CAVS_BF16) k_colsum<__nv_bfloat16><<<grid, 256, 0, s>>>(D, part, cols);
+  else k_colsum<float><<<grid, 256, 0, s>>>(D, part, cols);
 }
 
-void launch_pack(const Dev& D, const int* split, const float* db_part, cudaStream_t s) {
-  const size_t n = (size_t)4 * D.h * D.d + (size_t)4 * D.h * D.h + 4 * D.h;
-  k_pack<<<grid_for(n, 256), 256, 0, s>>>(D, lazy_layout(D), split[0], split[1], split[2], db_part);
+void launch_pack(const Dev& D, const int* split, const float* dbp, cudaStream_t s) {
+  const LazyLayout Z = lazy_layout(D);
+  const size_t h = D.h, d = D.d;
+  const int N = D.N;
+  PackSegs P{};
+  const float* u4 = D.lazy + Z.u4;
+  const float* uf = D.lazy + Z.uf;
+  const float* w = D.lazy + Z.w;
+  int maxlen = 0;
+  auto add = [&](const float* src, size_t sstride, size_t soff, size_t qstride, size_t o0, int S, int nb, size_t len) {
+    P.s[P.n++] = PackSeg{src, sstride, soff, qstride, o0, S, nb, (int)len};
+    maxlen = std::max(maxlen, (int)len);
+  };
+  if (D.cell == CAVS_CELL_TREE_LSTM) {
+    const int G = 3 + N;
+    const int intern[4] = {0, 3, 1, 2};      // packed (i, f, o, u) -> internal row block (f: 3..3+N-1)
+    const size_t nW = 4 * h * d, nU = 3 * h * h, nUf = h * h;
+    for (int pg = 0; pg < 4; ++pg)           // W blocks: sum over split slots (and the N f-blocks)
+      add(w, Z.sw, intern[pg] * h * d, h * d, pg * h * d, split[2], pg == 1 ? N : 1, h * d);
+    add(u4, Z.su4, 0, 0, nW, split[0], 1, nU);
+    add(uf, Z.suf, 0, 0, nW + nU, split[1], 1, nUf);
+    for (int pg = 0; pg < 4; ++pg)           // b: sum of the db chunk partials (and the N f-blocks)
+      add(dbp, (size_t)G * h, intern[pg] * h, h, nW + nU + nUf + pg * h, kDbChunks, pg == 1 ? N : 1, h);
+  } else {
+    add(u4, Z.su4, 0, 0, 0, split[0], 1, 2 * h * h);
+    add(w, Z.sw, 0, 0, 2 * h * h, split[2], 1, h * d);
+    add(dbp, h, 0, 0, 2 * h * h + h * d, kDbChunks, 1, h);
+  }
+  dim3 grid(std::min(148, cdiv(maxlen, 256 * 4)), P.n);
+  k_pack<<<grid, 256, 0, s>>>(D, P);
 }
 
 }  // namespace cavs

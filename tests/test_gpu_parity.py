@@ -100,6 +100,40 @@ def test_schedule_errors(graphs, N, code):
     assert ctx.schedule() == 2
 
 
+@pytest.mark.parametrize("graphs,N,code", [
+    ([[[1], [0]]], 1, "E_CYCLE"),
+    ([[[1, 2, 3], [], [], []]], 2, "E_ARITY"),
+])
+def test_deferred_schedule_errors_surface_at_forward(graphs, N, code):
+    """schedule(wait=False) only enqueues; the validation error is returned by forward()."""
+    from paper_1712_04048_b200 import CavsError
+    dev = torch.device("cuda", 0)
+    b = gen.batch_from_graphs(graphs, cell="tree_lstm", N=N, h=64, d=64, seed=0)
+    ctx = make_ctx(b, "bf16", max_vertices=16, max_graphs=4, max_x=16)
+    ctx.load_graphs(b.graph_ptr, b.child_ptr, b.child_idx)
+    assert ctx.schedule(wait=False) is None
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    with pytest.raises(CavsError) as e:
+        ctx.forward(t(b.params), t(b.x), t(b.x_row))
+    assert e.value.name == code
+
+
+def test_deferred_schedule_matches_synchronous():
+    b = BF16_CASES["tree_lstm_sst_h128_d64"]()
+    g = run_gpu(b, "bf16")
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    ctx = make_ctx(b, "bf16")
+    ctx.load_graphs(t(b.graph_ptr), t(b.child_ptr), t(b.child_idx))
+    ctx.schedule(wait=False)
+    h = ctx.forward(t(b.params), t(b.x), t(b.x_row))
+    dp, dx = ctx.backward(t(b.gamma))
+    torch.cuda.synchronize()
+    assert np.array_equal(h.cpu().numpy(), g["h_out"])
+    assert np.array_equal(dp.cpu().numpy(), g["dparams"])
+    assert np.array_equal(dx.cpu().numpy(), g["dx"])
+
+
 def test_call_order_errors():
     from paper_1712_04048_b200 import CavsError
     b = gen.make_config_batch("cfg1", seed=0)
