@@ -1,0 +1,85 @@
+// tools/mma_rate.cu — microbenchmark: cycles per tcgen05.mma (kind::f16, M = 128, K = 16) vs N,
+// with A from shared memory (SS) or from TMEM (TS), B from shared memory; one CTA per SM.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1712_04048_b200/csrc tools/mma_rate.cu -o tools/mma_rate
+#include <cuda_runtime.h>
+#include <cstdio>
+
+#include "ptx.cuh"
+
+using namespace cavs;
+
+__device__ __forceinline__ uint64_t desc(uint32_t saddr) {
+  return ((uint64_t)((1024u >> 4) | (1u << 14) | (2u << 29)) << 32) | (((saddr >> 4) & 0x3FFF) | (1u << 16));
+}
+
+template <int N, bool TS>
+__global__ void k_rate(int iters, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) { ptx::mbar_init(&bar, 1); ptx::fence_mbar_init(); }
+  if (warp == 0) ptx::tmem_alloc<512>(&slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = slot;
+  // A: 128 x 64 bf16 tile (16 KB) at smem, B: N x 64 (N*128 B) after it; contents irrelevant
+  const uint32_t a = ptx::smem_u32(smem), b = a + 16384;
+  constexpr uint32_t idesc = ptx::idesc_bf16(128, N, 0, 0);
+  unsigned long long t0 = 0, t1 = 0;
+  if (warp == 0) {
+    if (TS && ptx::elect_one()) {
+      for (int kk = 0; kk < 4; ++kk) ptx::tmem_cp_128x256b(tmem + 256 + kk * 8, desc(a + kk * 32));
+      ptx::mma_commit(&bar);
+    }
+    __syncwarp();
+    if (TS) { ptx::mbar_wait(&bar, 0); ptx::tc_fence_after(); }
+    const uint32_t ph = TS ? 1 : 0;
+    if (ptx::elect_one()) {
+      t0 = clock64();
+      for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          if constexpr (TS) ptx::mma_bf16_ts(tmem, tmem + 256 + kk * 8, desc(b + kk * 32), idesc, it | kk ? 1u : 0u);
+          else ptx::mma_bf16(tmem, desc(a + kk * 32), desc(b + kk * 32), idesc, it | kk ? 1u : 0u);
+        }
+      }
+      ptx::mma_commit(&bar);
+    }
+    __syncwarp();
+    ptx::mbar_wait(&bar, ph);
+    if (threadIdx.x == 0) { t1 = clock64(); out[blockIdx.x] = t1 - t0; }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { ptx::tc_fence_after(); ptx::tmem_dealloc<512>(tmem); }
+}
+
+template <int N, bool TS>
+void run(int grid) {
+  unsigned long long* d;
+  cudaMalloc(&d, 148 * 8);
+  const int smem = 16384 + N * 128 + 1024;
+  cudaFuncSetAttribute(k_rate<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int iters = 256;
+  k_rate<N, TS><<<grid, 128, smem>>>(iters, d);
+  k_rate<N, TS><<<grid, 128, smem>>>(iters, d);
+  cudaDeviceSynchronize();
+  unsigned long long h[148];
+  cudaMemcpy(h, d, grid * 8, cudaMemcpyDeviceToHost);
+  unsigned long long mx = 0;
+  for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
+  const double per = (double)mx / (iters * 4);
+  printf("%s N=%3d grid=%3d : %6.1f cycles/MMA  (%5.0f MAC/cycle/SM, %.0f%% of 4096)  err=%s\n", TS ? "TS" : "SS", N, grid,
+         per, 128.0 * N * 16 / per, 100.0 * 128.0 * N * 16 / per / 4096, cudaGetErrorString(cudaGetLastError()));
+  cudaFree(d);
+}
+
+int main() {
+  for (int grid : {1, 148}) {
+    run<16, false>(grid); run<32, false>(grid); run<64, false>(grid); run<128, false>(grid); run<256, false>(grid);
+    run<16, true>(grid); run<32, true>(grid); run<64, true>(grid); run<128, true>(grid); run<256, true>(grid);
+  }
+  return 0;
+}
