@@ -40,7 +40,7 @@ constexpr int kPProd = 3;            // producer warps 0-2, MMA warp 3
 constexpr int kPMma = 3;
 constexpr int kPEpi0 = 4;            // first epilogue warp
 constexpr int kPKb = 16384;          // one resident A k-block: 128 rows x 128 B (SW128, K-major)
-constexpr int kPStage = 16384;       // one B box
+constexpr int kPStageMin = 16384;    // B stage granularity (one 16-row x 8 k-block box)
 constexpr int kPMaxNT = 64;
 constexpr int kPMaxS = 12;           // B pipeline stages (TMEM-resident weights free the smem)
 
@@ -48,11 +48,13 @@ struct PPlan {
   int UG, ngrp, nkbA;                // units per CTA, row groups, resident k-blocks (K = 64 nkbA)
   int grp_row0[4], grp_col0[4];      // A rows grp_row0 + u0 .. + UG, columns grp_col0 + 64 kb
   int nseg, seg_bcol[8], seg_acc[8]; // MMA segments: all resident k-blocks x B columns [bcol, bcol + K)
+  int seg_init[8];                   // 1: the segment is the first one writing its accumulator
   int nacc;
   int nslot, slot_grp[8], slot_nacc[8], slot_acc[8][4];   // staged slot = sum of accs, one group
   int ne, e_n[8], e_slot[8][3];      // epilogue accumulator e = sum of slots
   int S;                             // B pipeline stages
-  int sk[3];                         // k-blocks per B box for NT = 16 / 32 / 64
+  int sk[3];                         // k-blocks per B box (= per stage) for NT = 16 / 32 / 64
+  int stage;                         // bytes per B stage (one box); boxes span segments (contiguous B columns)
   int tsA;                           // 1: weights resident in TMEM (A operand from TMEM), 0: in smem
   int acc0;                          // first TMEM column of the accumulators
   int max_ni;                        // largest task tile index (NT = 16 << ni) the TMEM budget admits
@@ -151,39 +153,40 @@ __device__ __forceinline__ void mma_level(const PPlan& P, int r, int ntile, uint
   // lane issues each box's MMAs + commit.
   constexpr uint32_t idesc = ptx::idesc_bf16(128, NT, 0, 0);
   constexpr int ni = NT == 16 ? 0 : NT == 32 ? 1 : 2;
-  const int sk = P.sk[ni], nbox = P.nkbA / sk, S = P.S;
+  const int sk = P.sk[ni], S = P.S;
+  const int nkb = P.nseg * P.nkbA;                  // the tile's k-blocks, segment-major
+  const int nbox = (nkb + sk - 1) / sk;
   for (int j = r; j < ntile; j += P.R, ++tcount) {
     if (tcount > 0) { pwait_warp(tmem_empty, (tcount - 1) & 1); ptx::tc_fence_after(); }
-    uint32_t written = 0;
-    for (int sg = 0; sg < P.nseg; ++sg) {
-      const int acc = P.seg_acc[sg];
-      const uint32_t d = (uint32_t)(P.acc0 + acc * NT);
-      for (int b = 0; b < nbox; ++b, ++step) {
-        const int s = step % S;
-        pwait_warp(&full[s], (step / S) & 1);
-        ptx::tc_fence_after();
-        if (tr && tr[0] == 0) tr[0] = gtime();
-        if (ptx::elect_one()) {
-          uint32_t al = a_lo + (uint32_t)(b * sk) * (kPKb >> 4);
-          uint32_t bl = b_lo + (uint32_t)s * (kPStage >> 4);
-          uint32_t acc_flag = (written >> acc) & 1u;
-          uint32_t at = (uint32_t)(b * sk) * 32u;             // TMEM column of the weights' k-block
-          for (int kb = 0; kb < sk; ++kb) {
+    int sg = 0, kba = 0;                              // (segment, weight k-block) of the next k-block
+    for (int b = 0; b < nbox; ++b, ++step) {
+      const int s = step % S;
+      pwait_warp(&full[s], (step / S) & 1);
+      ptx::tc_fence_after();
+      if (tr && tr[0] == 0) tr[0] = gtime();
+      const int g1 = min(nkb, (b + 1) * sk);
+      if (ptx::elect_one()) {
+        uint32_t bl = b_lo + (uint32_t)s * (uint32_t)(P.stage >> 4);
+        int sgi = sg, kbi = kba;
+        for (int g = b * sk; g < g1; ++g) {
+          const uint32_t d = (uint32_t)(P.acc0 + P.seg_acc[sgi] * NT);
+          const uint32_t first = (P.seg_init[sgi] && kbi == 0) ? 1u : 0u;   // first product into the accumulator
+          const uint32_t al = a_lo + (uint32_t)kbi * (kPKb >> 4);
+          const uint32_t at = (uint32_t)kbi * 32u;     // TMEM column of the weights' k-block
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              if constexpr (TS) ptx::mma_bf16_ts(d, at + kk * 8, sw128_desc(bl + kk * 2), idesc, acc_flag);
-              else ptx::mma_bf16(d, sw128_desc(al + kk * 2), sw128_desc(bl + kk * 2), idesc, acc_flag);
-              acc_flag = 1u;
-            }
-            al += kPKb >> 4;
-            at += 32;
-            bl += (NT * 128) >> 4;
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t acc_flag = (kk == 0 && first) ? 0u : 1u;
+            if constexpr (TS) ptx::mma_bf16_ts(d, at + kk * 8, sw128_desc(bl + kk * 2), idesc, acc_flag);
+            else ptx::mma_bf16(d, sw128_desc(al + kk * 2), sw128_desc(bl + kk * 2), idesc, acc_flag);
           }
-          ptx::mma_commit(&empty[s]);
+          bl += (NT * 128) >> 4;
+          if (++kbi == P.nkbA) { kbi = 0; ++sgi; }
         }
-        __syncwarp();
-        written |= 1u << acc;
+        ptx::mma_commit(&empty[s]);
       }
+      __syncwarp();
+      kba += g1 - b * sk;                             // advance (all lanes, uniform)
+      while (kba >= P.nkbA) { kba -= P.nkbA; ++sg; }
     }
     if (ptx::elect_one()) ptx::mma_commit(done);
     __syncwarp();
@@ -259,7 +262,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
         const int ntile = (M + nt - 1) / nt;
         if (r >= ntile) continue;
         const CUtensorMap* mb = ni == 0 ? &mb16 : ni == 1 ? &mb32 : &mb64;
-        const int sk = P.sk[ni], nbox = P.nkbA / sk;
+        const int sk = P.sk[ni], nbox = (P.nseg * P.nkbA + sk - 1) / sk;
         const uint32_t bytes = (uint32_t)nt * 128u * (uint32_t)sk;
         if (i > 0) {                                  // previous task finished grid-wide
           const unsigned long long tw = D.trace ? gtime() : 0;
@@ -270,15 +273,13 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
         if (D.trace && w == 0) ptrace(D, 5000 + E, blockIdx.x, i, gtime(), 0, 0, 0, 0);
         for (int j = r; j < ntile; j += P.R) {
           const int p0 = lo + j * nt;
-          for (int sg = 0; sg < P.nseg; ++sg) {
-            for (int b = 0; b < nbox; ++b, ++step) {
-              const int s = step % S;
-              if (s % kPProd != w) continue;
-              const uint32_t ph = (step / S) & 1;
-              if (step >= S) pwait(&empty[s], ph ^ 1);
-              ptx::mbar_arrive_expect_tx(&full[s], bytes);
-              ptx::tma_load_3d(sB + s * kPStage, mb, 0, p0, P.seg_bcol[sg] / 64 + b * sk, &full[s]);
-            }
+          for (int b = 0; b < nbox; ++b, ++step) {   // one box = sk consecutive k-blocks of the row block
+            const int s = step % S;
+            if (s % kPProd != w) continue;
+            const uint32_t ph = (step / S) & 1;
+            if (step >= S) pwait(&empty[s], ph ^ 1);
+            ptx::mbar_arrive_expect_tx(&full[s], bytes);
+            ptx::tma_load_3d(sB + s * P.stage, mb, 0, p0, P.seg_bcol[0] / 64 + b * sk, &full[s]);
           }
         }
       }
@@ -514,33 +515,41 @@ static bool plan_layout(PPlan& P, bool tsA) {
   const int A = P.nkbA * kPKb;
   const int xs = P.nslot * kPMaxNT * P.UG * 4;
   const int avail = 232448 - 1024 - xs - 256 - 2 * kPMaxS * 8 - 64;
+  // segments must be contiguous B columns (one box may span several)
+  for (int sg = 1; sg < P.nseg; ++sg)
+    if (P.seg_bcol[sg] != P.seg_bcol[0] + sg * P.nkbA * 64) return false;
+  for (int sg = 0; sg < P.nseg; ++sg) {
+    P.seg_init[sg] = 1;
+    for (int e = 0; e < sg; ++e)
+      if (P.seg_acc[e] == P.seg_acc[sg]) P.seg_init[sg] = 0;
+  }
+  // stage size: a 16-row tile of the task in one or two boxes (fewer, larger TMA boxes: the
+  // boxes of one SM are serviced one after another), multiple of 8 KB, <= 48 KB
+  const int tile16 = 16 * 128 * P.nseg * P.nkbA;
+  int stage = tile16 <= 32768 ? tile16 : (tile16 / 2 + 8191) / 8192 * 8192;
+  stage = std::max(kPStageMin, std::min(stage, 49152));
   P.tsA = tsA ? 1 : 0;
   int S;
   if (tsA) {
-    S = std::min(kPMaxS, avail / kPStage);
-    if (S * kPStage < A) return false;
+    S = std::min(kPMaxS, avail / stage);
+    if (S * stage < A) return false;
     P.acc0 = P.nkbA * 32;
-    P.xs_off = S * kPStage;
+    P.xs_off = S * stage;
   } else {
-    S = std::min(kPProd, (avail - A) / kPStage);
+    S = std::min(kPProd, (avail - A) / stage);
     P.acc0 = 0;
-    P.xs_off = A + S * kPStage;
+    P.xs_off = A + S * stage;
   }
   if (S < 2) return false;
   P.S = S;
+  P.stage = stage;
   P.max_ni = -1;
   for (int i = 0; i < 3; ++i)
     if (P.acc0 + P.nacc * (16 << i) <= 512) P.max_ni = i;
   if (P.max_ni < 0) return false;
   P.meta_off = P.xs_off + xs;
   P.bar_off = (P.meta_off + 15) & ~15;
-  for (int i = 0; i < 3; ++i) {                       // largest divisor of nkbA with a <= 16 KB box
-    const int cap = kPStage / ((16 << i) * 128);
-    int sk = 1;
-    for (int c = 1; c <= std::min(cap, P.nkbA); ++c)
-      if (P.nkbA % c == 0) sk = c;
-    P.sk[i] = sk;
-  }
+  for (int i = 0; i < 3; ++i) P.sk[i] = stage / ((16 << i) * 128);   // k-blocks per box (<= 256)
   return true;
 }
 static int plan_smem(const PPlan& P) { return 1024 + P.bar_off + 2 * kPMaxS * 8 + 64; }
