@@ -25,6 +25,7 @@
 #include <cstdlib>
 
 #include "cells.cuh"
+#include "gemm.h"
 #include "persist.h"
 #include "ptx.cuh"
 #include "tc.h"
@@ -409,6 +410,7 @@ struct TcState {
   bool use_simt = false;
   bool mono = false;            // CAVS_TC_MONO=1: one CTA per 128-unit block for the levels too
   PersistState* ps = nullptr;   // persistent weight-stationary level kernels (persist.cu), if the shape admits
+  GemmState* gs = nullptr;      // row-tiled x-projection / dX GEMMs (gemm.cu)
   std::string info;
 };
 
@@ -470,6 +472,7 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
     delete t;
     return CAVS_E_CUDA;
   }
+  if (!t->use_simt) t->gs = gemm_init(D, max_vertices);
   if (t->use_simt) t->info = "levels: SIMT FFMA (CAVS_BF16_SIMT=1)";
   else if (t->mono) t->info = "levels: per-task tcgen05, monolithic CTAs (CAVS_TC_MONO=1)";
   else {
@@ -486,6 +489,7 @@ std::string tc_describe(const TcState* tc) { return tc ? tc->info : std::string(
 
 void tc_destroy(TcState* tc) {
   if (tc && tc->ps) persist_destroy(tc->ps);
+  if (tc && tc->gs) gemm_destroy(tc->gs);
   delete tc;
 }
 
@@ -705,7 +709,8 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
   const int zero = 0;
   if (D.cell == CAVS_CELL_TREE_LSTM) {
     // eager pull projection fused with task 0 (large: monolithic CTAs reuse the x tile for 4 gates)
-    launch_level<EPI_LSTM_XPROJ, 4, 1>(t->A[1], t->A[1], t->B_xp, D, mono_lstm_xproj(h, d), 0, D.V, h, s);
+    if (!gemm_xproj(D, t->gs, s))
+      launch_level<EPI_LSTM_XPROJ, 4, 1>(t->A[1], t->A[1], t->B_xp, D, mono_lstm_xproj(h, d), 0, D.V, h, s);
     P.count(1);
     P.mark(CAVS_PH_FWD_LEVELS, s);
     if (t->ps) { if (T > 1) { persist_forward(D, t->ps, T, s); P.count(1); } return; }
@@ -716,7 +721,8 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
       P.count(1);
     }
   } else {
-    launch_level<EPI_FC_XPROJ, 1, 1>(t->A[1], t->A[1], t->B_xp, D, mono_one(d, 1, &zero, &zero), 0, D.V, h, s);
+    if (!gemm_xproj(D, t->gs, s))
+      launch_level<EPI_FC_XPROJ, 1, 1>(t->A[1], t->A[1], t->B_xp, D, mono_one(d, 1, &zero, &zero), 0, D.V, h, s);
     P.count(1);
     P.mark(CAVS_PH_FWD_LEVELS, s);
     if (t->ps) { if (T > 1) { persist_forward(D, t->ps, T, s); P.count(1); } return; }
@@ -810,7 +816,8 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
     split[2] = launch_II(t->M_dz, t->M_xp, D, Cw, w, s); P.count(1);
     P.mark(CAVS_PH_DX, s);
     if (D.dx) {
-      launch_level<EPI_DX, 1, 1>(t->A[4], t->A[4], t->B_dz, D, mono_lstm_dx(h, N), 0, V, d, s);
+      if (!gemm_dx(D, t->gs, s))
+        launch_level<EPI_DX, 1, 1>(t->A[4], t->A[4], t->B_dz, D, mono_lstm_dx(h, N), 0, V, d, s);
       P.count(1);
     }
   } else {
@@ -827,7 +834,8 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
     split[2] = launch_II(t->M_dz, t->M_xp, D, Cw, w, s); P.count(1);
     P.mark(CAVS_PH_DX, s);
     if (D.dx) {
-      launch_level<EPI_DX, 1, 1>(t->A[4], t->A[4], t->B_dz, D, mono_one(h, 1, &zero, &zero), 0, V, d, s);
+      if (!gemm_dx(D, t->gs, s))
+        launch_level<EPI_DX, 1, 1>(t->A[4], t->A[4], t->B_dz, D, mono_one(h, 1, &zero, &zero), 0, V, d, s);
       P.count(1);
     }
   }
