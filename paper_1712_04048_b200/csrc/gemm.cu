@@ -196,7 +196,7 @@ static bool genc(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows,
 // Tree-LSTM x-projection: BN = 128 = 4 gates x 32 units; Tree-FC: BN = 128 units; dX: BN = 128.
 constexpr int kXpBN = 128;
 constexpr int kDxBN = 128;
-constexpr int kGS = 6;                                     // pipeline stages (32 KB each)
+constexpr int kGS = 3;                                     // pipeline stages (32 KB each): 2 CTAs per SM
 
 template <int E, int BN, int NG>
 static void launch_rows(const CUtensorMap& a, const CUtensorMap& b, const Dev& D, int K, int a_col0, int gate_stride,
