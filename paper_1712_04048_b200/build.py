@@ -1,7 +1,7 @@
 """Build the C-ABI shared library `libcavs.so` in-tree with nvcc for sm_100a.
 
-    python -m paper_1712_04048_b200.build          # incremental
-    python -m paper_1712_04048_b200.build --force  # rebuild everything
+    python paper_1712_04048_b200/build.py          # incremental (or __graft_entry__.build())
+    python paper_1712_04048_b200/build.py --force  # rebuild everything
 """
 from __future__ import annotations
 

@@ -37,7 +37,7 @@ class _Desc(ctypes.Structure):
 
 def _load():
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1712_04048_b200.build` "
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_1712_04048_b200/build.py` or `__graft_entry__.build()` "
                           "(there is no fallback path)")
     lib = ctypes.CDLL(LIB_PATH)
     P, I32, I64, SZ, S = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctypes.c_int
