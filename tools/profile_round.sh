@@ -1,14 +1,25 @@
 #!/bin/bash
-# Round profile capture (run on the GPU box via gpurun).  Produces, under gpurun_out/:
-#   launches.csv      ncu launch list (gpu__time_duration.sum, --clock-control none) of the bench command
-#   levels.ncu-rep    ncu --set full of one forward+backward pass worth of level kernels (warm caches)
-#   bench.json        the bench line of the same command (no profiler attached)
+# Round capture (run on the GPU box via gpurun).  Produces, under gpurun_out/:
+#   pytest_gpu.log    the -m gpu parity suite
+#   bench.json        the bench line (no profiler attached)
+#   launches.csv      ncu launch list (gpu__time_duration.sum, --clock-control none) of a short bench
+#   persist.ncu-rep   ncu --set full of the persistent level kernels (one forward + one backward pass)
+#   rows.ncu-rep      ncu --set full of the row GEMMs and the lazy (type-II) GEMMs
 set -x
+mkdir -p gpurun_out
 ARGS="--steps 2 --warmup 1 --no-e2e --no-cpu-baseline --pool 2 ${BENCH_ARGS}"
-python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err
-ncu --metrics gpu__time_duration.sum --clock-control none -c 500 --csv --log-file gpurun_out/launches.csv \
+if [ -z "${SKIP_TESTS}" ]; then
+  timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
+  tail -3 gpurun_out/pytest_gpu.log
+fi
+timeout 600 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
+tail -c 600 gpurun_out/bench.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 500 --csv --log-file gpurun_out/launches.csv \
     python bench.py $ARGS > gpurun_out/launches_bench.log 2>&1
-ncu --set full --cache-control none --clock-control none --import-source on \
-    -k regex:"k_tc_level|k_skinny|k_tc_typeII" -s ${SKIP:-60} -c ${COUNT:-60} \
-    -o gpurun_out/levels -f python bench.py $ARGS > gpurun_out/levels.log 2>&1
+timeout 600 ncu --set full --cache-control none --clock-control none --import-source on \
+    -k regex:"k_persist" -s ${SKIP:-2} -c ${COUNT:-2} \
+    -o gpurun_out/persist -f python bench.py $ARGS > gpurun_out/persist.log 2>&1
+timeout 600 ncu --set full --cache-control none --clock-control none --import-source on \
+    -k regex:"k_gemm_rows|k_tc_typeII" -s 4 -c 5 \
+    -o gpurun_out/rows -f python bench.py $ARGS > gpurun_out/rows.log 2>&1
 ls -la gpurun_out

@@ -26,6 +26,12 @@ def kclass(name):
         if m:
             return f"tc_level[{epi.get(m.group(1), m.group(1))},CL={m.group(3)}]"
         return "tc_level"
+    if "k_persist" in n:
+        m = re.search(r"k_persist<(?:\(int\))?(\d+)", n)
+        return "persist[" + {"0": "fwd", "2": "bwd", "3": "fc_fwd", "5": "fc_bwd"}.get(m.group(1) if m else "", "?") + "]"
+    if "k_gemm_rows" in n:
+        m = re.search(r"k_gemm_rows<(?:\(int\))?(\d+)", n)
+        return "gemm_rows[" + {"1": "xproj", "4": "fc_xproj", "6": "dx"}.get(m.group(1) if m else "", m.group(1) if m else "?") + "]"
     if "k_skinny" in n:
         m = re.search(r"k_skinny<[^,]+, (?:\(int\))?(\d+), (?:\(int\))?(\d+)", n)
         return "skinny[" + ("fwd" if m and m.group(2) == "0" else "bwd") + "]"
@@ -92,9 +98,9 @@ def main():
     for c, (t, n) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
         lines.append(f"| {c} | {n} | {t / 1e3:.1f} | {100 * t / tot:.1f}% |")
     # full capture of the level kernels
-    rep = os.path.join(a.src, "levels.ncu-rep")
     traffic = {}
-    if os.path.exists(rep):
+    reps = [os.path.join(a.src, r) for r in ("levels.ncu-rep", "persist.ncu-rep", "rows.ncu-rep")]
+    for rep in [r for r in reps if os.path.exists(r)]:
         hdr, data = raw_metrics(rep)
         ix = {n: i for i, n in enumerate(hdr)}
 
@@ -103,7 +109,7 @@ def main():
                 return float(r[ix[n]])
             except Exception:
                 return float("nan")
-        lines += ["", "## ncu --set full of consecutive level kernels (warm caches, `--cache-control none`)", "",
+        lines += ["", f"## ncu --set full: {os.path.basename(rep)} (warm caches, `--cache-control none`)", "",
                   "| kernel | grid | us | DRAM read MB | DRAM write MB | L2 hit % | tensor pipe % | issued IPC | regs |",
                   "|---|---|---|---|---|---|---|---|---|"]
         per = defaultdict(list)
@@ -119,12 +125,15 @@ def main():
                          f"{g(r, 'sm__inst_issued.avg.per_cycle_active'):.2f} | "
                          f"{g(r, 'launch__registers_per_thread'):.0f} |")
             per[c].append((rd + wr) * 1e6)
-        fwd = per.get("tc_level[fwd,CL=4]", []) + per.get("skinny[fwd]", [])
-        bwd = per.get("tc_level[bwd,CL=4]", []) + per.get("skinny[bwd]", [])
+        fwd = per.get("tc_level[fwd,CL=4]", []) + per.get("skinny[fwd]", []) + per.get("persist[fwd]", [])
+        bwd = per.get("tc_level[bwd,CL=4]", []) + per.get("skinny[bwd]", []) + per.get("persist[bwd]", [])
+        lazy = per.get("k_tc_typeII", [])
         if fwd:
             traffic[f"{a.config}:fwd_levels"] = sum(fwd) / len(fwd)
         if bwd:
             traffic[f"{a.config}:bwd_levels"] = sum(bwd) / len(bwd)
+        if lazy:
+            traffic[f"{a.config}:lazy"] = sum(lazy) / len(lazy)
         lines += ["", "DRAM units as reported by ncu (MB).  traffic.json holds bytes per launch, averaged over "
                   "the captured launches of each pass."]
     bj = os.path.join(a.src, "bench.json")
