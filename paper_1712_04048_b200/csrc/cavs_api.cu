@@ -79,6 +79,7 @@ static size_t carve(cavs_ctx* c, char* base) {
   D.hdr = I(kHdrWords + V + 1); D.level_ptr = base ? D.hdr + kHdrWords : nullptr;
   D.roots = I(V); D.cnt = I(V + 1);
   D.gsync = reinterpret_cast<unsigned*>(I(64));
+  D.tile_cnt = I(kLazyMaxTiles + kDbMaxBlocks);
   D.order = I(V); D.child_pos = I(V * N); D.parent_pos = I(V); D.slot = I(V); D.deg = I(V);
   D.xrow_pos = I(Vp); D.tile_x = I(Vp / 64 + 2);
   D.Hk = take(Vp * N * h * es);
@@ -128,6 +129,7 @@ CAVS_API cavs_status cavs_create(const cavs_desc* desc, int device, void* stream
     return CAVS_E_INVALID;
   if (d.N > kMaxN) return CAVS_E_UNSUPPORTED;
   if (d.cell == CAVS_CELL_TREE_FC && d.N != 2) return CAVS_E_UNSUPPORTED;
+  if ((int64_t)4 * d.h > 256 * kDbMaxBlocks) return CAVS_E_UNSUPPORTED;     // db column blocks (k_colsum)
   if (d.precision == CAVS_BF16 && ((d.h % 64) || (d.d % 64))) return CAVS_E_UNSUPPORTED;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return CAVS_E_CUDA;
@@ -364,9 +366,12 @@ CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dp
     simt_backward<float>(D, ctx->lp, ctx->stream, P);
   }
   P.mark(CAVS_PH_REDUCE, ctx->stream);
-  launch_colsum(D, ctx->lazy_db, ctx->stream);
-  launch_pack(D, split, ctx->lazy_db, ctx->stream);
-  P.count(2);
+  if (split[0] >= 0) {                         // split-K slots of the fallback lazy GEMMs -> dparams
+    launch_pack(D, split, ctx->stream);
+    P.count(1);
+  }
+  launch_colsum(D, ctx->lazy_db, ctx->stream);  // db -> dparams
+  P.count(1);
   P.mark(-1, ctx->stream);
   account_backward(ctx);
   CK(cudaGetLastError());

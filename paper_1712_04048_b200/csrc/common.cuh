@@ -32,6 +32,7 @@ struct Dev {
   int* roots;                       // positions of vertices without a parent
   int* cnt;                         // level histogram scratch [V+1]
   unsigned* gsync;                  // [0] barrier arrivals, [1] exits: grid barrier of the persistent level kernels
+  int* tile_cnt;                    // arrival counters (zero between launches): lazy tiles, then db column blocks
   // arenas (OpT = float in FP32 mode, __nv_bfloat16 in BF16 mode)
   void* Hk;      // [Vp, N*h] gather slots of child h (written by the child's scatter)
   void* Hs;      // [Vp, h]   child-sum h~ (Tree-LSTM, N >= 2)

@@ -9,6 +9,8 @@ namespace cavs {
 constexpr int kMaxN = 4;          // max arity supported by the kernels
 constexpr int kDbChunks = 32;     // row chunks of the deterministic db column reduction
 constexpr int kSplitMax = 8;      // max split-K of the lazy tensor-core GEMMs
+constexpr int kLazyMaxTiles = 1024;   // arrival counters of the stream-K lazy kernel (lazy.cu)
+constexpr int kDbMaxBlocks = 64;      // arrival counters of the db column blocks (k_colsum)
 constexpr int kSkinnyMax = 8;     // tasks with at most this many vertices use the skinny level kernel
 
 enum Epi : int { EPI_LSTM_FWD = 0, EPI_LSTM_XPROJ, EPI_LSTM_BWD, EPI_FC_FWD, EPI_FC_XPROJ, EPI_FC_BWD, EPI_DX };
@@ -81,7 +83,7 @@ void simt_typeII(const Dev& D, const SegListII& L, float* out, int M, int Ncols,
 void launch_prep(const Dev& D, cudaStream_t s);
 void launch_pull(const Dev& D, cudaStream_t s);
 void launch_roots(const Dev& D, int n_roots, const int* roots, cudaStream_t s);
-void launch_colsum(const Dev& D, float* part, cudaStream_t s);
-void launch_pack(const Dev& D, const int* split /*[3]*/, const float* db_part, cudaStream_t s);
+void launch_colsum(const Dev& D, float* part, cudaStream_t s);   // db straight into D.dparams
+void launch_pack(const Dev& D, const int* split /*[3]*/, cudaStream_t s);   // split-K slots -> dU, dW
 
 }  // namespace cavs

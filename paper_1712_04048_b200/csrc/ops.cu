@@ -133,59 +133,100 @@ __global__ void k_roots(Dev D, int n_roots, const int* roots) {
   }
 }
 
-// part[c][col] = sum over rows of chunk c of dZ[row][col].  CTA = 8 warps x 256 columns; a lane
-// owns 8 consecutive columns (one 16-byte bf16 load per row), warp w takes rows w, w+8, ... of
-// the chunk; the 8 warp partials are added in a fixed order (deterministic).
+// db (P:L541-542 lazy batching of the bias gradient): db_g = sum over all vertices of dz_g.
+// Logical columns L = (i, o, u, f) x h for Tree-LSTM (f summed over the N child slots: the
+// shared U_f / b_f of Z6) or h for Tree-FC.  part[c][L] = sum over the rows of chunk c; CTA = 8
+// warps x 256 logical columns, a lane owns 8 consecutive columns (16-byte loads per row in BF16
+// mode), warp w takes rows w, w+8, ... of the chunk, the 8 warp partials are added in a fixed
+// order.  The last CTA of a column block (arrival counter) sums the kDbChunks partials in chunk
+// order and writes the packed db block of dparams (deterministic).
 template <class OpT>
-__global__ void __launch_bounds__(256) k_colsum(Dev D, float* part, int cols) {
+__global__ void __launch_bounds__(256) k_colsum(Dev D, float* part, int lcols) {
   __shared__ float red[8][256];
+  __shared__ int s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c0 = blockIdx.x * 256 + lane * 8;
+  const int h = D.h;
+  const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
+  const int cols = lstm ? (3 + D.N) * h : h;                 // physical dZ row width
+  const int L0 = blockIdx.x * 256 + lane * 8;
   const int chunk = cdiv(D.V, gridDim.y);
   const int r0 = blockIdx.y * chunk, r1 = min(D.V, r0 + chunk);
   const OpT* dz = op<OpT>(D.dZ);
   float acc[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-  if (c0 + 8 <= cols && sizeof(OpT) == 2) {
-    int r = r0 + warp;
-    for (; r + 24 < r1; r += 32) {                  // 4 rows in flight
-      uint4 u[4];
+  if (L0 + 8 <= lcols && (h & 7) == 0) {                     // 8 columns inside one gate
+    const int gl = L0 / h, j = L0 - gl * h;
+    const int nk = (lstm && gl == 3) ? D.N : 1;
+    const int pc = (lstm && gl == 3) ? 3 * h + j : gl * h + j;
+    for (int k = 0; k < nk; ++k) {
+      const OpT* col = dz + pc + k * h;
+      if constexpr (sizeof(OpT) == 2) {
+        int r = r0 + warp;
+        for (; r + 24 < r1; r += 32) {                      // 4 rows in flight
+          uint4 u[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) u[k] = *reinterpret_cast<const uint4*>(dz + (size_t)(r + 8 * k) * cols + c0);
+          for (int q = 0; q < 4; ++q) u[q] = *reinterpret_cast<const uint4*>(col + (size_t)(r + 8 * q) * cols);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u[k]);
+          for (int q = 0; q < 4; ++q) {
+            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u[q]);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) { const float2 f = __bfloat1622float2(b[e]); acc[2 * e] += f.x; acc[2 * e + 1] += f.y; }
+            for (int e = 0; e < 4; ++e) { const float2 f = __bfloat1622float2(b2[e]); acc[2 * e] += f.x; acc[2 * e + 1] += f.y; }
+          }
+        }
+        for (; r < r1; r += 8) {
+          const uint4 u = *reinterpret_cast<const uint4*>(col + (size_t)r * cols);
+          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) { const float2 f = __bfloat1622float2(b2[e]); acc[2 * e] += f.x; acc[2 * e + 1] += f.y; }
+        }
+      } else {
+        for (int r = r0 + warp; r < r1; r += 8) {
+          const OpT* rowp = col + (size_t)r * cols;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] += from_op(rowp[e]);
+        }
       }
     }
-    for (; r < r1; r += 8) {
-      const uint4 u = *reinterpret_cast<const uint4*>(dz + (size_t)r * cols + c0);
-      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) { const float2 f = __bfloat1622float2(b[e]); acc[2 * e] += f.x; acc[2 * e + 1] += f.y; }
-    }
-  } else if (c0 + 8 <= cols) {
-    for (int r = r0 + warp; r < r1; r += 8) {
-      const OpT* rowp = dz + (size_t)r * cols + c0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] += from_op(rowp[e]);
-    }
   } else {
-    for (int r = r0 + warp; r < r1; r += 8)
-      for (int e = 0; e < 8 && c0 + e < cols; ++e) acc[e] += from_op(dz[(size_t)r * cols + c0 + e]);
+    for (int e = 0; e < 8 && L0 + e < lcols; ++e) {
+      const int L = L0 + e, gl = L / h, j = L - gl * h;
+      const int nk = (lstm && gl == 3) ? D.N : 1;
+      const int pc = (lstm && gl == 3) ? 3 * h + j : gl * h + j;
+      for (int k = 0; k < nk; ++k)
+        for (int r = r0 + warp; r < r1; r += 8) acc[e] += from_op(dz[(size_t)r * cols + pc + k * h]);
+    }
   }
 #pragma unroll
   for (int e = 0; e < 8; ++e) red[warp][lane * 8 + e] = acc[e];
   __syncthreads();
-  const int c = blockIdx.x * 256 + threadIdx.x;
-  if (c < cols) {
+  const int L = blockIdx.x * 256 + threadIdx.x;
+  if (L < lcols) {
     float v = 0.f;
 #pragma unroll
     for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
-    part[(size_t)blockIdx.y * cols + c] = v;
+    part[(size_t)blockIdx.y * lcols + L] = v;
   }
+  __threadfence();
+  __syncthreads();
+  int* cnt = D.tile_cnt + kLazyMaxTiles + blockIdx.x;
+  if (threadIdx.x == 0) s_last = atomicAdd(cnt, 1) == (int)gridDim.y - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (L < lcols) {
+    float v = 0.f;
+    for (int c = 0; c < (int)gridDim.y; ++c) v += __ldcg(part + (size_t)c * lcols + L);
+    const size_t H = h, Dd = D.d;
+    if (lstm) {
+      const int gl = L / h, j = L - gl * h;
+      const int blk[4] = {0, 2, 3, 1};                       // internal (i, o, u, f) -> packed (i, f, o, u)
+      D.dparams[4 * H * Dd + 4 * H * H + (size_t)blk[gl] * H + j] = v;
+    } else {
+      D.dparams[2 * H * H + H * Dd + L] = v;
+    }
+  }
+  if (threadIdx.x == 0) *cnt = 0;                             // replayable
 }
 
 // Packing as segments: out[o0 + e] = sum_{s < S} sum_{q < nb} src[s * sstride + soff + q * qstride + e]
@@ -274,13 +315,13 @@ void launch_roots(const Dev& D, int n_roots, const int* roots, cudaStream_t s) {
 }
 
 void launch_colsum(const Dev& D, float* part, cudaStream_t s) {
-  const int cols = (D.cell == CAVS_CELL_TREE_LSTM ? 3 + D.N : 1) * D.h;
-  dim3 grid(cdiv(cols, 256), kDbChunks);   // 32 deterministic row chunks
-  if (D.prec == CAVS_BF16) k_colsum<__nv_bfloat16><<<grid, 256, 0, s>>>(D, part, cols);
-  else k_colsum<float><<<grid, 256, 0, s>>>(D, part, cols);
+  const int lcols = (D.cell == CAVS_CELL_TREE_LSTM ? 4 : 1) * D.h;
+  dim3 grid(cdiv(lcols, 256), kDbChunks);   // 32 deterministic row chunks
+  if (D.prec == CAVS_BF16) k_colsum<__nv_bfloat16><<<grid, 256, 0, s>>>(D, part, lcols);
+  else k_colsum<float><<<grid, 256, 0, s>>>(D, part, lcols);
 }
 
-void launch_pack(const Dev& D, const int* split, const float* dbp, cudaStream_t s) {
+void launch_pack(const Dev& D, const int* split, cudaStream_t s) {
   const LazyLayout Z = lazy_layout(D);
   const size_t h = D.h, d = D.d;
   const int N = D.N;
@@ -301,12 +342,9 @@ void launch_pack(const Dev& D, const int* split, const float* dbp, cudaStream_t 
       add(w, Z.sw, intern[pg] * h * d, h * d, pg * h * d, split[2], pg == 1 ? N : 1, h * d);
     add(u4, Z.su4, 0, 0, nW, split[0], 1, nU);
     add(uf, Z.suf, 0, 0, nW + nU, split[1], 1, nUf);
-    for (int pg = 0; pg < 4; ++pg)           // b: sum of the db chunk partials (and the N f-blocks)
-      add(dbp, (size_t)G * h, intern[pg] * h, h, nW + nU + nUf + pg * h, kDbChunks, pg == 1 ? N : 1, h);
   } else {
     add(u4, Z.su4, 0, 0, 0, split[0], 1, 2 * h * h);
     add(w, Z.sw, 0, 0, 2 * h * h, split[2], 1, h * d);
-    add(dbp, h, 0, 0, 2 * h * h + h * d, kDbChunks, 1, h);
   }
   dim3 grid(std::min(148, cdiv(maxlen, 256 * 4)), P.n);
   k_pack<<<grid, 256, 0, s>>>(D, P);

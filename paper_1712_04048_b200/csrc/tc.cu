@@ -26,6 +26,7 @@
 
 #include "cells.cuh"
 #include "gemm.h"
+#include "lazy.h"
 #include "persist.h"
 #include "ptx.cuh"
 #include "tc.h"
@@ -411,6 +412,7 @@ struct TcState {
   bool mono = false;            // CAVS_TC_MONO=1: one CTA per 128-unit block for the levels too
   PersistState* ps = nullptr;   // persistent weight-stationary level kernels (persist.cu), if the shape admits
   GemmState* gs = nullptr;      // row-tiled x-projection / dX GEMMs (gemm.cu)
+  LazyState* ls = nullptr;      // stream-K lazy weight-gradient GEMMs (lazy.cu)
   std::string info;
 };
 
@@ -473,6 +475,7 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
     return CAVS_E_CUDA;
   }
   if (!t->use_simt) t->gs = gemm_init(D, max_vertices);
+  if (!t->use_simt) t->ls = lazy_init(D, max_vertices);
   if (t->use_simt) t->info = "levels: SIMT FFMA (CAVS_BF16_SIMT=1)";
   else if (t->mono) t->info = "levels: per-task tcgen05, monolithic CTAs (CAVS_TC_MONO=1)";
   else {
@@ -481,6 +484,7 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
     t->info = t->ps ? "levels: " + persist_describe(t->ps)
                     : "levels: per-task tcgen05 launches (persistent path unavailable: " + why + ")";
   }
+  t->info += t->ls ? "; lazy: stream-K tcgen05 (one launch)" : "; lazy: split-K tcgen05 + pack";
   *out = t;
   return CAVS_OK;
 }
@@ -490,6 +494,7 @@ std::string tc_describe(const TcState* tc) { return tc ? tc->info : std::string(
 void tc_destroy(TcState* tc) {
   if (tc && tc->ps) persist_destroy(tc->ps);
   if (tc && tc->gs) gemm_destroy(tc->gs);
+  if (tc && tc->ls) lazy_destroy(tc->ls);
   delete tc;
 }
 
@@ -796,7 +801,10 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
   float* w = D.lazy + Z.w;
   const int lp1 = D.lp1, V = D.V;
   const int zero = 0;
-  if (lstm) {
+  if (lazy_grads(D, t->ls, s)) {                      // every dU / dW block straight into dparams
+    P.count(1);
+    split[0] = -1;
+  } else if (lstm) {
     PlanII A{};                                         // dU_iou = sum_k dZ_iou^T H_k  (h~ by linearity)
     A.nseg = N;
     for (int k = 0; k < N; ++k) A.s[k] = SegT2{0, k * h, lp1, V, 0};
@@ -814,12 +822,6 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
     Cw.s[0] = SegT2{0, 0, 0, V, 1};
     Cw.M = G * h; Cw.Ncols = d; Cw.ldo = d; Cw.split_stride = Z.sw;
     split[2] = launch_II(t->M_dz, t->M_xp, D, Cw, w, s); P.count(1);
-    P.mark(CAVS_PH_DX, s);
-    if (D.dx) {
-      if (!gemm_dx(D, t->gs, s))
-        launch_level<EPI_DX, 1, 1>(t->A[4], t->A[4], t->B_dz, D, mono_lstm_dx(h, N), 0, V, d, s);
-      P.count(1);
-    }
   } else {
     PlanII A{};
     A.nseg = 1;
@@ -832,12 +834,14 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
     Cw.s[0] = SegT2{0, 0, 0, V, 1};
     Cw.M = h; Cw.Ncols = d; Cw.ldo = d; Cw.split_stride = Z.sw;
     split[2] = launch_II(t->M_dz, t->M_xp, D, Cw, w, s); P.count(1);
-    P.mark(CAVS_PH_DX, s);
-    if (D.dx) {
-      if (!gemm_dx(D, t->gs, s))
-        launch_level<EPI_DX, 1, 1>(t->A[4], t->A[4], t->B_dz, D, mono_one(h, 1, &zero, &zero), 0, V, d, s);
-      P.count(1);
+  }
+  P.mark(CAVS_PH_DX, s);
+  if (D.dx) {                                         // pull's adjoint: dX = dZ W
+    if (!gemm_dx(D, t->gs, s)) {
+      if (lstm) launch_level<EPI_DX, 1, 1>(t->A[4], t->A[4], t->B_dz, D, mono_lstm_dx(h, N), 0, V, d, s);
+      else launch_level<EPI_DX, 1, 1>(t->A[4], t->A[4], t->B_dz, D, mono_one(h, 1, &zero, &zero), 0, V, d, s);
     }
+    P.count(1);
   }
 }
 

@@ -366,3 +366,40 @@ def test_persistent_path_is_default_for_benchmark_shape():
     b = gen.make_batch("tree_lstm", 2, 512, 512, "sst_tree", 4, seed=1)
     ctx = make_ctx(b, "bf16")
     assert "levels: persistent" in ctx.path_info()
+
+
+# ------------------------------------------------------------------ stream-K lazy gradients
+LAZY_CASES = {
+    "lstm_n2_h512_sst": lambda: gen.make_batch("tree_lstm", 2, 512, 512, "sst_tree", 40, seed=31),
+    "lstm_n1_h256_chain": lambda: gen.batch_from_graphs([gen.chain(n) for n in (40, 17, 3, 60)], cell="tree_lstm",
+                                                         N=1, h=256, d=128, seed=32, x_at="all", loss_at="all"),
+    "lstm_n3_h128": lambda: gen.batch_from_graphs(_nary_forest(30, 3, 20, 33), cell="tree_lstm", N=3, h=128, d=192,
+                                                  seed=33),
+    # no internal vertex: every dU tile is a zero-work piece
+    "lstm_leaves_only": lambda: gen.batch_from_graphs([[[]]] * 70, cell="tree_lstm", N=2, h=128, d=64, seed=34,
+                                                      loss_at="all"),
+    # no pull record: every dW tile is a zero-work piece
+    "lstm_no_x": lambda: gen.batch_from_graphs(_nary_forest(20, 2, 12, 35), cell="tree_lstm", N=2, h=128, d=64,
+                                               seed=35, x_at="none"),
+    "fc_h256_cbt": lambda: gen.make_batch("tree_fc", 2, 256, 128, "cbt32", 12, seed=36),
+    "fc_h512_sst": lambda: gen.make_batch("tree_fc", 2, 512, 256, "sst_tree", 60, seed=37),
+}
+
+
+@pytest.mark.parametrize("case", list(LAZY_CASES))
+def test_lazy_streamk(case, monkeypatch):
+    """The one-launch stream-K lazy kernel (lazy.cu) against the oracle and against the split-K
+    type-II kernels + pack (CAVS_LAZY=0): same bf16 operands, fp32 sums in another order; and
+    bit-identical results when the same context runs the same batch twice (fixed-order in-kernel
+    split-K reduction)."""
+    b = LAZY_CASES[case]()
+    monkeypatch.setenv("CAVS_LAZY", "1")
+    g = run_gpu(b, "bf16")
+    assert "lazy: stream-K" in g["ctx"].path_info(), g["ctx"].path_info()
+    compare(b, g, run_oracle(b), BF16_TOL, case + " vs fp64 oracle")
+    g2 = run_gpu(b, "bf16", ctx=g["ctx"])
+    assert np.array_equal(g["dparams"], g2["dparams"]), "stream-K lazy gradients not deterministic"
+    monkeypatch.setenv("CAVS_LAZY", "0")
+    o = run_gpu(b, "bf16")
+    assert "lazy: split-K" in o["ctx"].path_info()
+    compare(b, g, o, 1e-5, case + " stream-K vs split-K")
