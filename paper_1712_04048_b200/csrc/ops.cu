@@ -216,7 +216,13 @@ __global__ void __launch_bounds__(256) k_colsum(Dev D, float* part, int lcols) {
   __threadfence();
   if (L < lcols) {
     float v = 0.f;
-    for (int c = 0; c < (int)gridDim.y; ++c) v += __ldcg(part + (size_t)c * lcols + L);
+    for (int c0 = 0; c0 < (int)gridDim.y; c0 += 8) {        // 8 partials in flight, summed in chunk order
+      float t[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) t[e] = c0 + e < (int)gridDim.y ? __ldcg(part + (size_t)(c0 + e) * lcols + L) : 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v += t[e];
+    }
     const size_t H = h, Dd = D.d;
     if (lstm) {
       const int gl = L / h, j = L - gl * h;
@@ -316,7 +322,7 @@ void launch_roots(const Dev& D, int n_roots, const int* roots, cudaStream_t s) {
 
 void launch_colsum(const Dev& D, float* part, cudaStream_t s) {
   const int lcols = (D.cell == CAVS_CELL_TREE_LSTM ? 4 : 1) * D.h;
-  dim3 grid(cdiv(lcols, 256), kDbChunks);   // 32 deterministic row chunks
+  dim3 grid(cdiv(lcols, 256), kDbChunks);   // deterministic row chunks (one wave of CTAs)
   if (D.prec == CAVS_BF16) k_colsum<__nv_bfloat16><<<grid, 256, 0, s>>>(D, part, lcols);
   else k_colsum<float><<<grid, 256, 0, s>>>(D, part, lcols);
 }
