@@ -80,6 +80,7 @@ static size_t carve(cavs_ctx* c, char* base) {
   D.roots = I(V); D.cnt = I(V + 1);
   D.gsync = reinterpret_cast<unsigned*>(I(64));
   D.tile_cnt = I(kLazyMaxTiles + kDbMaxBlocks);
+  D.crow = I((V + 1) * (kMaxClusters + 1));
   D.order = I(V); D.child_pos = I(V * N); D.parent_pos = I(V); D.slot = I(V); D.deg = I(V);
   D.xrow_pos = I(Vp); D.tile_x = I(Vp / 64 + 2);
   D.Hk = take(Vp * N * h * es);
@@ -172,6 +173,7 @@ CAVS_API cavs_status cavs_set_workspace(cavs_ctx* ctx, void* dev, size_t bytes) 
   if (ctx->desc.precision == CAVS_BF16) {
     cavs_status s = tc_init(ctx->D, ctx->desc.max_vertices, &ctx->tc, &ctx->err);
     if (s) return s;
+    ctx->D.ncl = tc_clusters(ctx->tc);
   }
   ctx->state = S_READY;
   return CAVS_OK;

@@ -32,6 +32,8 @@ struct Dev {
   int* roots;                       // positions of vertices without a parent
   int* cnt;                         // level histogram scratch [V+1]
   unsigned* gsync;                  // [0] barrier arrivals, [1] exits: grid barrier of the persistent level kernels
+  int ncl;                          // clusters of the persistent level kernels (0: none)
+  int* crow;                        // [T][ncl + 1]: first position of task t owned by cluster >= r
   int* tile_cnt;                    // arrival counters (zero between launches): lazy tiles, then db column blocks
   // arenas (OpT = float in FP32 mode, __nv_bfloat16 in BF16 mode)
   void* Hk;      // [Vp, N*h] gather slots of child h (written by the child's scatter)

@@ -91,22 +91,42 @@ __device__ __forceinline__ int nt_index(int M, int R, int max_ni) {
   return min(max_ni, n <= 16 ? 0 : n <= 32 ? 1 : 2);
 }
 
-// Grid barrier (all CTAs co-resident by construction: cooperative launch).  Monotonic arrival
-// counter: barrier i of a launch completes when the counter reaches (i + 1) * gridDim.x; the
-// last CTA to leave the kernel resets it to 0 (so the launch is replayable, e.g. in a graph).
-// Release-add + acquire-poll: one L2 round trip after the last arrival.  Spins at most ~4 s,
-// then traps (never hang the GPU).
-__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned target) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
+// Cluster-local task barrier.  The graphs of a batch are independent, so each
+// cluster owns a contiguous range of graphs (their rows of every task V_t are contiguous: positions
+// inside a task are graph-major) and only its own CTAs -- the unit blocks of the same rows -- need
+// to agree that V_t is done before V_t+-1 starts.  One mbarrier per CTA counts one remote arrival
+// per CTA of the cluster (DSMEM, release at cluster scope); the waiter acquires at cluster scope.
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// release-arrive on CTA c's barrier (the release covers this CTA's task writes: the caller passed
+// a CTA barrier after them)
+__device__ __forceinline__ void cluster_arrive(uint64_t* bar, int c) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(ptx::smem_u32(bar)), "r"(c));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+__device__ __forceinline__ void cluster_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = ptx::smem_u32(bar);
   unsigned long long t0 = 0;
-  unsigned it = 0;
-  while ((int)(ptx::ld_acquire_gpu(count) - target) < 0) {
-    if ((++it & 255u) == 0) {
-      const unsigned long long now = gtime();
-      if (t0 == 0) t0 = now;
-      else if (now - t0 > 4000000000ull) __trap();
-    }
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    if (ok) return;
+    const unsigned long long now = gtime();
+    if (t0 == 0) t0 = now;
+    else if (now - t0 > 4000000000ull) __trap();
   }
+}
+// rows of task t owned by cluster r: [crow[t][r], crow[t][r + 1]) (k_build_maps)
+__device__ __forceinline__ void cl_rows(const Dev& D, int t, int r, int& lo, int& M) {
+  const int* c = D.crow + (size_t)t * (D.ncl + 1) + r;
+  lo = c[0];
+  M = c[1] - lo;
 }
 
 // Compile-time staging layout per epilogue kind (matches the host plan of persist_init):
@@ -146,7 +166,7 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t lo) {
   return ((uint64_t)((1024u >> 4) | (1u << 14) | (2u << 29)) << 32) | lo;   // SBO 1024, version 1, SWIZZLE_128B
 }
 template <int NT, bool TS>
-__device__ __forceinline__ void mma_level(const PPlan& P, int r, int ntile, uint32_t a_lo, uint32_t b_lo,
+__device__ __forceinline__ void mma_level(const PPlan& P, int ntile, uint32_t a_lo, uint32_t b_lo,
                                           uint64_t* full, uint64_t* empty, uint64_t* done, uint64_t* tmem_empty,
                                           int& step, int& tcount, unsigned long long* tr) {
   // Whole warp runs the loop (warp-uniform operands live in uniform registers); one elected
@@ -156,7 +176,7 @@ __device__ __forceinline__ void mma_level(const PPlan& P, int r, int ntile, uint
   const int sk = P.sk[ni], S = P.S;
   const int nkb = P.nseg * P.nkbA;                  // the tile's k-blocks, segment-major
   const int nbox = (nkb + sk - 1) / sk;
-  for (int j = r; j < ntile; j += P.R, ++tcount) {
+  for (int j = 0; j < ntile; ++j, ++tcount) {
     if (tcount > 0) { pwait_warp(tmem_empty, (tcount - 1) & 1); ptx::tc_fence_after(); }
     int sg = 0, kba = 0;                              // (segment, weight k-block) of the next k-block
     for (int b = 0; b < nbox; ++b, ++step) {
@@ -215,15 +235,15 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
   uint64_t* tmem_empty = done + 1;
   uint64_t* abar = tmem_empty + 1;
   uint64_t* acopy = abar + 1;                                   // weights copied smem -> TMEM
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acopy + 1);
+  uint64_t* cbar = acopy + 1;                                   // cluster task barrier
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbar + 1);
   volatile int* gate = reinterpret_cast<volatile int*>(tmem_slot + 1);
   __shared__ unsigned long long s_tmax;                          // debug trace only
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ub = blockIdx.x % P.nub, r = blockIdx.x / P.nub;
+  const int ub = blockIdx.x % P.nub, r = blockIdx.x / P.nub;   // cluster rank = unit block, cluster = r
   const int u0 = ub * P.UG;
   const int S = P.S;
-  const int* lp = D.level_ptr;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
@@ -231,12 +251,13 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
     ptx::mbar_init(tmem_empty, 8);
     ptx::mbar_init(abar, P.ngrp);
     ptx::mbar_init(acopy, 1);
+    ptx::mbar_init(cbar, P.nub);
     *gate = 0;
-    ptx::fence_mbar_init();
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kPMma) ptx::tmem_alloc<512>(tmem_slot);
   ptx::tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();                                 // peers' barriers initialised before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -257,10 +278,11 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
       int step = 0;
       for (int i = 0; i < nlev; ++i) {
         const int t = t_first + i * dir;
-        const int lo = lp[t], M = lp[t + 1] - lo;
-        const int ni = nt_index(M, P.R, P.max_ni), nt = 16 << ni;
+        int lo, M;
+        cl_rows(D, t, r, lo, M);
+        const int ni = nt_index(M, 1, P.max_ni), nt = 16 << ni;
         const int ntile = (M + nt - 1) / nt;
-        if (r >= ntile) continue;
+        if (ntile == 0) continue;
         const CUtensorMap* mb = ni == 0 ? &mb16 : ni == 1 ? &mb32 : &mb64;
         const int sk = P.sk[ni], nbox = (P.nseg * P.nkbA + sk - 1) / sk;
         const uint32_t bytes = (uint32_t)nt * 128u * (uint32_t)sk;
@@ -271,7 +293,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
           if (D.trace && w == 0) ptrace(D, 3000 + E, blockIdx.x, i, tw, gtime(), 0, 0, 0);
         }
         if (D.trace && w == 0) ptrace(D, 5000 + E, blockIdx.x, i, gtime(), 0, 0, 0, 0);
-        for (int j = r; j < ntile; j += P.R) {
+        for (int j = 0; j < ntile; ++j) {
           const int p0 = lo + j * nt;
           for (int b = 0; b < nbox; ++b, ++step) {   // one box = sk consecutive k-blocks of the row block
             const int s = step % S;
@@ -312,21 +334,22 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
       int step = 0, tcount = 0;
       for (int i = 0; i < nlev; ++i) {
         const int t = t_first + i * dir;
-        const int M = lp[t + 1] - lp[t];
-        const int ni = nt_index(M, P.R, P.max_ni), nt = 16 << ni;
+        int lo, M;
+        cl_rows(D, t, r, lo, M);
+        const int ni = nt_index(M, 1, P.max_ni), nt = 16 << ni;
         const int ntile = (M + nt - 1) / nt;
         unsigned long long trm[2] = {0, 0};
         unsigned long long* tr = D.trace ? trm : nullptr;
         if (P.tsA) {
-          if (ni == 0) mma_level<16, true>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
-          else if (ni == 1) mma_level<32, true>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
-          else mma_level<64, true>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
+          if (ni == 0) mma_level<16, true>(P, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
+          else if (ni == 1) mma_level<32, true>(P, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
+          else mma_level<64, true>(P, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
         } else {
-          if (ni == 0) mma_level<16, false>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
-          else if (ni == 1) mma_level<32, false>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
-          else mma_level<64, false>(P, r, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
+          if (ni == 0) mma_level<16, false>(P, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
+          else if (ni == 1) mma_level<32, false>(P, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
+          else mma_level<64, false>(P, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
         }
-        if (D.trace && r < ntile && lane == 0) ptrace(D, 4000 + E, blockIdx.x, i, trm[0], trm[1], 0, nt, 0);
+        if (D.trace && ntile > 0 && lane == 0) ptrace(D, 4000 + E, blockIdx.x, i, trm[0], trm[1], 0, nt, 0);
       }
     }
     __syncwarp();
@@ -340,19 +363,20 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
     ptx::griddep_wait();
     const UnitC<4> uc = epi_uses_bias<E>() ? load_unit<4>(D, j, epi_is_lstm<E>()) : UnitC<4>{};
     constexpr int CH = epi_needs_children<E>() ? 1 : 2;
-    int tcount = 0;
+    int tcount = 0, nbar = 0;
     for (int i = 0; i < nlev; ++i) {
       const int t = t_first + i * dir;
-      const int lo = lp[t], M = lp[t + 1] - lo;
-      const int ni = nt_index(M, P.R, P.max_ni), nt = 16 << ni;
+      int lo, M;
+      cl_rows(D, t, r, lo, M);
+      const int ni = nt_index(M, 1, P.max_ni), nt = 16 << ni;
       const int ntile = (M + nt - 1) / nt;
       unsigned long long tr0 = 0, tr1 = 0, tr2 = 0, tr3 = 0;
       if (D.trace && et == 0) tr0 = gtime();
-      if (i > 0 && r < ntile) {                         // inputs of V_t are final once the barrier passed
+      if (i > 0 && ntile > 0) {                         // inputs of V_t are final once the barrier passed
         if (lane == 0) while (*gate < i) { }
         __syncwarp();
       }
-      for (int jt = r; jt < ntile; jt += P.R, ++tcount) {
+      for (int jt = 0; jt < ntile; ++jt, ++tcount) {
         const int p0 = lo + jt * nt;
         const int valid = min(nt, lo + M - p0);
         const int items = quads * valid;
@@ -436,16 +460,22 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
         unsigned long long tl = 0;
         if (D.trace) { tl = gtime(); atomicMax(&s_tmax, tl); }
         ptx::named_bar_sync(1, 256);                     // xs free for the next tile
-        if (D.trace && et == 0 && jt == r) { ptrace(D, 6000 + E, blockIdx.x, i, tr3, tl, s_tmax, gtime(), 0); s_tmax = 0; }
+        if (D.trace && et == 0 && jt == 0) { ptrace(D, 6000 + E, blockIdx.x, i, tr3, tl, s_tmax, gtime(), 0); s_tmax = 0; }
       }
-      if (i + 1 < nlev) {                                // task V_t complete grid-wide before V_t+-1
+      if (i + 1 < nlev) {                                // task V_t complete cluster-wide before V_t+-1
         ptx::named_bar_sync(1, 256);
-        if (et == 0) {
-          if (D.trace) tr2 = gtime();
-          grid_barrier(D.gsync, (unsigned)(i + 1) * gridDim.x);
-          *gate = i + 1;
-          if (D.trace) ptrace(D, 2000 + E, blockIdx.x, (unsigned long long)i | ((unsigned long long)M << 16), tr0, tr1, tr2,
-                              gtime(), tr3);
+        if (et < 32) {
+          if (D.trace && et == 0) tr2 = gtime();
+          if (ntile > 0) {                               // cluster-uniform: same rows for every unit block
+            if (et < P.nub) cluster_arrive(cbar, et);    // one warp instruction: all peers at once
+            if (et == 0) cluster_wait(cbar, (uint32_t)(nbar & 1));
+            ++nbar;
+          }
+          if (et == 0) {
+            *gate = i + 1;
+            if (D.trace) ptrace(D, 2000 + E, blockIdx.x, (unsigned long long)i | ((unsigned long long)M << 16), tr0, tr1,
+                                tr2, gtime(), tr3);
+          }
         }
       }
     }
@@ -456,10 +486,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem);
   }
-  if (threadIdx.x == 0 && atomicAdd(D.gsync + 1, 1u) == gridDim.x - 1) {   // every CTA is past its last barrier
-    D.gsync[0] = 0;
-    D.gsync[1] = 0;
-  }
+  cluster_sync_all();                                 // no peer touches this CTA's barrier after exit
 }
 
 // =====================================================================================
@@ -554,14 +581,28 @@ static bool plan_layout(PPlan& P, bool tsA) {
 }
 static int plan_smem(const PPlan& P) { return 1024 + P.bar_off + 2 * kPMaxS * 8 + 64; }
 
+// smem attribute + how many clusters of nub CTAs (1 CTA per SM) can be resident at once
 template <int E, int NE, int NM>
-static bool attr_and_occupancy(int smem) {
+static int attr_and_clusters(int smem, int nub) {
   if (cudaFuncSetAttribute(k_persist<E, NE, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return false;
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_persist<E, NE, NM>, kPThreads, smem) != cudaSuccess)
-    return false;
-  return occ >= 1;
+    return 0;
+  if (nub > 8 && cudaFuncSetAttribute(k_persist<E, NE, NM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    return 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(nub * kMaxClusters, 1, 1);
+  cfg.blockDim = dim3(kPThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = nub; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_persist<E, NE, NM>, &cfg) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  return n;
 }
 
 template <int E, int NE, int NM>
@@ -572,12 +613,11 @@ static void launch_p(const CUtensorMap* A, const CUtensorMap* B, const Dev& D, c
   cfg.blockDim = dim3(kPThreads, 1, 1);
   cfg.dynamicSmemBytes = plan_smem(P);
   cfg.stream = s;
-  // cooperative: all CTAs resident at once (the grid barrier relies on it, also next to other
-  // streams' kernels); PDL: the weights stream in under the previous kernel when the driver
-  // accepts both attributes together, else cooperative alone.
+  // one cluster of nub unit-block CTAs per graph range; PDL: the weights stream in under the
+  // previous kernel
   cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = P.nub; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
@@ -614,8 +654,8 @@ PersistState* persist_init(const Dev& D, int max_vertices, std::string* why) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&ps->num_sms, cudaDevAttrMultiProcessorCount, dev);
   const int nub = h / UG;
-  const int R = ps->num_sms / nub;
-  if (R < 1) { delete ps; *why = "too few SMs"; return nullptr; }
+  if (nub > 16) { delete ps; *why = "more than 16 unit blocks (cluster size)"; return nullptr; }
+  int R = kMaxClusters;                               // clusters (graph ranges), set from occupancy below
   const uint64_t Vp = (uint64_t)max_vertices + kPadRows;
   const int G = lstm ? 3 + N : 1;
   bool ok = true;
@@ -673,19 +713,24 @@ PersistState* persist_init(const Dev& D, int max_vertices, std::string* why) {
     ok &= enc3(&ps->B_dz[i], D.dZ, (uint64_t)G * h, Vp, 16u << i, B.sk[i]);
   }
   if (!ok) { delete ps; *why = "tensor map encode failed"; return nullptr; }
-  // every CTA must be resident at once (grid barrier): one CTA per SM
-  bool occ = true;
+  // clusters of nub CTAs, one CTA per SM (TMEM, shared memory); every cluster runs its own graph
+  // range through all tasks, so only a cluster's own CTAs need to be co-resident
+  int nc = kMaxClusters;
+  auto occ = [&](int a, int b) { nc = std::min(nc, std::min(a, b)); };
   if (lstm) {
     switch (N) {
-      case 1: occ = attr_and_occupancy<EPI_LSTM_FWD, 4, 1>(plan_smem(F)) && attr_and_occupancy<EPI_LSTM_BWD, 2, 1>(plan_smem(B)); break;
-      case 2: occ = attr_and_occupancy<EPI_LSTM_FWD, 5, 2>(plan_smem(F)) && attr_and_occupancy<EPI_LSTM_BWD, 3, 2>(plan_smem(B)); break;
-      case 3: occ = attr_and_occupancy<EPI_LSTM_FWD, 6, 3>(plan_smem(F)) && attr_and_occupancy<EPI_LSTM_BWD, 4, 3>(plan_smem(B)); break;
-      default: occ = attr_and_occupancy<EPI_LSTM_FWD, 7, 4>(plan_smem(F)) && attr_and_occupancy<EPI_LSTM_BWD, 5, 4>(plan_smem(B)); break;
+      case 1: occ(attr_and_clusters<EPI_LSTM_FWD, 4, 1>(plan_smem(F), nub), attr_and_clusters<EPI_LSTM_BWD, 2, 1>(plan_smem(B), nub)); break;
+      case 2: occ(attr_and_clusters<EPI_LSTM_FWD, 5, 2>(plan_smem(F), nub), attr_and_clusters<EPI_LSTM_BWD, 3, 2>(plan_smem(B), nub)); break;
+      case 3: occ(attr_and_clusters<EPI_LSTM_FWD, 6, 3>(plan_smem(F), nub), attr_and_clusters<EPI_LSTM_BWD, 4, 3>(plan_smem(B), nub)); break;
+      default: occ(attr_and_clusters<EPI_LSTM_FWD, 7, 4>(plan_smem(F), nub), attr_and_clusters<EPI_LSTM_BWD, 5, 4>(plan_smem(B), nub)); break;
     }
   } else {
-    occ = attr_and_occupancy<EPI_FC_FWD, 1, 1>(plan_smem(F)) && attr_and_occupancy<EPI_FC_BWD, 2, 1>(plan_smem(B));
+    occ(attr_and_clusters<EPI_FC_FWD, 1, 1>(plan_smem(F), nub), attr_and_clusters<EPI_FC_BWD, 2, 1>(plan_smem(B), nub));
   }
-  if (!occ) { delete ps; *why = "occupancy"; return nullptr; }
+  const char* cenv = std::getenv("CAVS_PERSIST_CLUSTERS");    // debug / A-B: fewer clusters
+  if (cenv && std::atoi(cenv) > 0) nc = std::min(nc, std::atoi(cenv));
+  if (nc < 1) { delete ps; *why = "no cluster of " + std::to_string(nub) + " CTAs fits"; return nullptr; }
+  F.R = B.R = R = nc;
   ps->fwd = F;
   ps->bwd = B;
   return ps;
@@ -693,11 +738,13 @@ PersistState* persist_init(const Dev& D, int max_vertices, std::string* why) {
 
 void persist_destroy(PersistState* ps) { delete ps; }
 
+int persist_clusters(const PersistState* ps) { return ps ? ps->fwd.R : 0; }
+
 std::string persist_describe(const PersistState* ps) {
   const PPlan& F = ps->fwd;
   const PPlan& B = ps->bwd;
-  return "persistent: grid " + std::to_string(F.nub * F.R) + " (units/CTA " + std::to_string(F.UG) + ", replicas " +
-         std::to_string(F.R) + "), weights in " + (F.tsA ? "TMEM" : "smem") + ", stages fwd " + std::to_string(F.S) +
+  return "persistent: grid " + std::to_string(F.nub * F.R) + " (units/CTA " + std::to_string(F.UG) + ", " +
+         std::to_string(F.R) + " clusters of " + std::to_string(F.nub) + " over graph ranges), weights in " + (F.tsA ? "TMEM" : "smem") + ", stages fwd " + std::to_string(F.S) +
          " bwd " + std::to_string(B.S) + ", max task tile fwd " + std::to_string(16 << F.max_ni) + " bwd " +
          std::to_string(16 << B.max_ni);
 }

@@ -167,6 +167,21 @@ __global__ void k_build_maps(Dev D) {
     D.parent_pos[p] = pv >= 0 ? D.pos[pv] : -1;
     D.slot[p] = pv >= 0 ? D.slot_v[v] : 0;
     if (pv < 0) D.roots[atomicAdd(&D.hdr[2], 1)] = p;
+    if (D.ncl > 0) {
+      // graph range of a cluster: cl(g) = graph_ptr[g] * ncl / V (balanced by vertices, monotone
+      // in g); inside task t positions are graph-major, so cluster r owns the contiguous rows
+      // [crow[t][r], crow[t][r + 1]).  Each entry is written by exactly one vertex: the first of
+      // its task whose cluster reaches r, or the task's last vertex for the clusters past it.
+      const int t = D.level[v];
+      const int t0 = D.level_ptr[t], t1 = D.level_ptr[t + 1];
+      const int nc = D.ncl;
+      int* row = D.crow + (size_t)t * (nc + 1);
+      const int c = (int)((long long)lo * nc / D.V);
+      const int cp = p > t0 ? (int)((long long)D.graph_ptr[D.graph_of[D.order[p - 1]]] * nc / D.V) : -1;
+      for (int r = cp + 1; r <= c; ++r) row[r] = p;
+      if (p == t1 - 1)
+        for (int r = c + 1; r <= nc; ++r) row[r] = t1;
+    }
     // an internal vertex with fewer than N children reads zero in its missing slots (Z1)
     if (deg > 0 && deg < D.N) {
       OpT* hk = reinterpret_cast<OpT*>(D.Hk) + (size_t)p * D.N * D.h;

@@ -491,6 +491,8 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
 
 std::string tc_describe(const TcState* tc) { return tc ? tc->info : std::string("levels: FP32 FFMA"); }
 
+int tc_clusters(const TcState* tc) { return tc && tc->ps ? persist_clusters(tc->ps) : 0; }
+
 void tc_destroy(TcState* tc) {
   if (tc && tc->ps) persist_destroy(tc->ps);
   if (tc && tc->gs) gemm_destroy(tc->gs);

@@ -15,5 +15,6 @@ void tc_forward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s,
 void tc_backward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, int* split /*[3]*/, Prof& P);
 void tc_destroy(TcState* tc);
 std::string tc_describe(const TcState* tc);   // which level-kernel path is active
+int tc_clusters(const TcState* tc);           // graph-range clusters of the persistent level kernels (0: none)
 
 }  // namespace cavs
