@@ -39,6 +39,12 @@ BATCH_DESC = {
     "cfg4_h1024": "Tree-LSTM, synthetic SST-shaped binarised parse trees, hidden 1024, batch 256",
     "cfg5": "Tree-FC, complete binary trees of 256 leaves, hidden 2048, batch 64",
 }
+def _desc(cfg, h):
+    """Workload description with the hidden size actually run (--h overrides the config's)."""
+    import re
+    return re.sub(r"hidden \d+", f"hidden {h}", BATCH_DESC.get(cfg, ""))
+
+
 TENSOR_PHASES = ("xproj", "fwd_levels", "bwd_levels", "lazy", "dx")
 
 
@@ -190,7 +196,7 @@ def run_reference(args, rank, world):
         else "Tree-FC train samples/s (fwd+bwd)",
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": f"{args.config}: {BATCH_DESC.get(args.config, '')}",
+        "data": "synthetic", "config": {"workload": f"{args.config}: {_desc(args.config, b.h)}",
                                         "h": b.h, "batch": b.K, "sample_graphs_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": used, "kind": "oracle",
                          "sample": f"{per_step} graphs of {args.config} batch seed 0 per step"},
@@ -348,7 +354,7 @@ def main():
             "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": args.precision, "data": "synthetic",
-            "config": {"workload": f"{args.config}: {BATCH_DESC.get(args.config, '')}", "h": b0.h, "d": b0.d,
+            "config": {"workload": f"{args.config}: {_desc(args.config, b0.h)}", "h": b0.h, "d": b0.d,
                        "batch_per_gpu": b0.K, "global_batch": samples, "precision": args.precision,
                        "batch_pool": args.pool, "l2_flush": not args.no_flush, "parallelism": f"dp{world}",
                        "mean_vertices": float(np.mean([b.V for b in batches])),

@@ -1,0 +1,410 @@
+// rows.cu — BF16 mode: row-tiled tcgen05 level GEMMs for LARGE tasks when the weights of F do
+// not fit the persistent weight-stationary kernel (h > 512; Alg. 1 FORWARD/BACKWARD
+// task loop P:L362-380, one launch per task V_t, fused cell epilogue as in Fig. 5).
+//
+// A large task (M_t rows) is a plain dense contraction: Z[rows, units] = A[rows, K] W[units, K]^T
+// with A = the task's contiguous rows of the gather arena Hk (forward) or of dZ (backward),
+// K-major, and W = F's weights, K-major.  Unlike the per-task swap-AB kernel (tc.cu: 128 weight
+// rows x 64 task rows, 45 FLOP/B of operand traffic) the tile here is 128 task rows x 256
+// weight rows (87 FLOP/B), so the k-loop is not bound by L2 bandwidth.  The kernel is
+// persistent over the task's (row tile, unit tile) pairs; two TMEM accumulator buffers where
+// they fit, so the cell epilogue of one tile overlaps the next tile's k-loop.
+//
+// MMA segments (host plan): segment s multiplies A columns [a_col, a_col + 64 nkb) with the B
+// boxes of weight rows {b_row0[g] + u0} into TMEM columns [acc_col, acc_col + n):
+//   Tree-FC fwd : 1 segment,  A = Hk [h_l | h_r] (K = 2h), B = W_c rows u0..u0+255   -> z
+//   Tree-FC bwd : 1 segment,  A = dZ (K = h), B = W_c^T rows {u0, h + u0} (2 x 128) -> dh_l, dh_r
+//   Tree-LSTM fwd: N segments, A = Hk slot k (K = h), B = U rows {i, o, u, f} x 64 units
+//                  -> block k = (U_iou h_k, U_f h_k); the epilogue sums the iou parts over k
+//                  (U h~ = sum_k U h_k, linearity, Z11)
+//   Tree-LSTM bwd: 1 + N segments, A = dZ_iou (K = 3h) x U_iou^T rows u0..u0+127 -> dh~,
+//                  A = dZ_fk (K = h) x U_f^T rows -> U_f^T dz_fk
+// Epilogue: thread = task row (TMEM lane) x half of the tile's units; per 4-unit quad the
+// accumulators are read straight from TMEM and the cell (cells.cuh EpiK) runs in registers.
+//   warp 0: TMA producer, warp 1: TMEM allocator + MMA issuer, warps 2-9: epilogue.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "cells.cuh"
+#include "ptx.cuh"
+#include "rows.h"
+
+namespace cavs {
+
+constexpr int kRThreads = 320;
+constexpr int kRS = 4;                 // pipeline stages
+constexpr int kRA = 128 * 128;         // A stage: 128 rows x 64 k (bf16) = 16 KB
+
+struct RSeg { int a_col, bmap, nbox, box_rows, b_row0[4], nkb, acc_col; };
+struct RPlan {
+  int nseg;
+  RSeg seg[5];
+  int UG;          // units per tile
+  int n;           // MMA N (nbox * box_rows), the same for every segment
+  int stage;       // bytes per stage
+  int acc_cols;    // TMEM columns per accumulator buffer
+  int nbuf;        // accumulator buffers (1 or 2)
+  int lo, hi;      // task rows
+  int nut, ntiles; // unit tiles, tiles
+};
+
+__device__ __forceinline__ void rwait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = ptx::smem_u32(bar);
+  unsigned long long t0 = 0;
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    if (ok) return;
+    const unsigned long long now = gtime();
+    if (t0 == 0) t0 = now;
+    else if (now - t0 > 4000000000ull) __trap();
+  }
+}
+
+__device__ __forceinline__ uint64_t r_desc(uint32_t saddr) {   // K-major SW128, SBO 1 KB
+  return ((uint64_t)((1024u >> 4) | (1u << 14) | (2u << 29)) << 32) | (((saddr >> 4) & 0x3FFF) | (1u << 16));
+}
+
+// 4 consecutive TMEM columns of this thread's lane, no wait (the caller waits once)
+__device__ __forceinline__ void tld4(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(taddr));
+}
+__device__ __forceinline__ void tld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+template <int E> struct RAcc { static constexpr int NE = 1; };
+template <> struct RAcc<EPI_FC_BWD> { static constexpr int NE = 2; };
+
+// accumulators of the quad at unit offset u (within the tile) -> acc[NE]
+template <int E, int NM>
+__device__ __forceinline__ void fetch_acc(uint32_t tb, int UG, int u, FV<4>* acc) {
+  if constexpr (E == EPI_FC_FWD) {
+    uint32_t r[4];
+    tld4(tb + u, r);
+    tld_wait();
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[0].v[e] = __uint_as_float(r[e]);
+  } else if constexpr (E == EPI_FC_BWD) {
+    uint32_t r[2][4];
+    tld4(tb + u, r[0]);
+    tld4(tb + UG + u, r[1]);
+    tld_wait();
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[a].v[e] = __uint_as_float(r[a][e]);
+  } else if constexpr (E == EPI_LSTM_FWD) {
+    uint32_t r[NM][4][4];
+#pragma unroll
+    for (int k = 0; k < NM; ++k)
+#pragma unroll
+      for (int g = 0; g < 4; ++g) tld4(tb + (uint32_t)(k * 4 * UG + g * UG + u), r[k][g]);
+    tld_wait();
+#pragma unroll
+    for (int g = 0; g < 3; ++g)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < NM; ++k) s += __uint_as_float(r[k][g][e]);
+        acc[g].v[e] = s;
+      }
+#pragma unroll
+    for (int k = 0; k < NM; ++k)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[3 + k].v[e] = __uint_as_float(r[k][3][e]);
+  } else {   // EPI_LSTM_BWD: acc 0 = U_iou^T dz_iou, acc 1 + k = U_f^T dz_fk
+    uint32_t r[1 + NM][4];
+#pragma unroll
+    for (int a = 0; a < 1 + NM; ++a) tld4(tb + (uint32_t)(a * UG + u), r[a]);
+    tld_wait();
+#pragma unroll
+    for (int a = 0; a < 1 + NM; ++a)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[a].v[e] = __uint_as_float(r[a][e]);
+  }
+}
+
+template <int E, int NM, int QB>
+__global__ void __launch_bounds__(kRThreads, 1)
+k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB0,
+       const __grid_constant__ CUtensorMap mB1, Dev D, const __grid_constant__ RPlan P) {
+  constexpr int NE = E == EPI_LSTM_FWD ? 3 + NM : E == EPI_LSTM_BWD ? 1 + NM : RAcc<E>::NE;
+  extern __shared__ __align__(16) uint8_t r_raw[];
+  uint8_t* smem = r_raw + ((1024u - (ptx::smem_u32(r_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRS * P.stage);
+  uint64_t* empty = full + kRS;
+  uint64_t* accf = empty + kRS;
+  uint64_t* acce = accf + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRS; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { ptx::mbar_init(&accf[b], 1); ptx::mbar_init(&acce[b], 256); }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---- TMA producer ----
+    if (lane == 0) {
+      ptx::tma_prefetch(&mA); ptx::tma_prefetch(&mB0); ptx::tma_prefetch(&mB1);
+      ptx::griddep_wait();                               // task rows come from the previous kernels
+      int step = 0;
+      for (int j = blockIdx.x; j < P.ntiles; j += gridDim.x) {
+        const int p0 = P.lo + (j / P.nut) * 128, u0 = (j % P.nut) * P.UG;
+        for (int sg = 0; sg < P.nseg; ++sg) {
+          const RSeg& S = P.seg[sg];
+          const CUtensorMap* mb = S.bmap ? &mB1 : &mB0;
+          for (int kb = 0; kb < S.nkb; ++kb, ++step) {
+            const int s = step % kRS;
+            if (step >= kRS) rwait(&empty[s], ((step / kRS) & 1) ^ 1);
+            uint8_t* st = smem + s * P.stage;
+            ptx::mbar_arrive_expect_tx(&full[s], P.stage);
+            ptx::tma_load_2d(st, &mA, S.a_col + kb * 64, p0, &full[s]);
+            for (int g = 0; g < S.nbox; ++g)
+              ptx::tma_load_2d(st + kRA + g * S.box_rows * 128, mb, kb * 64, S.b_row0[g] + u0, &full[s]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---- MMA issuer ----
+    if (lane == 0) {
+      const uint32_t idesc = ptx::idesc_bf16(128, P.n, 0, 0);
+      int step = 0;
+      for (int j = blockIdx.x, k = 0; j < P.ntiles; j += gridDim.x, ++k) {
+        const int buf = P.nbuf == 2 ? (k & 1) : 0;
+        const int use = P.nbuf == 2 ? (k >> 1) : k;       // earlier uses of this buffer
+        if (use > 0) rwait(&acce[buf], (use - 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t tb = tmem + (uint32_t)(buf * P.acc_cols);
+        for (int sg = 0; sg < P.nseg; ++sg) {
+          const RSeg& S = P.seg[sg];
+          for (int kb = 0; kb < S.nkb; ++kb, ++step) {
+            const int s = step % kRS;
+            rwait(&full[s], (step / kRS) & 1);
+            ptx::tc_fence_after();
+            const uint32_t a = ptx::smem_u32(smem + s * P.stage), b = a + kRA;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              ptx::mma_bf16(tb + (uint32_t)S.acc_col, r_desc(a + kk * 32), r_desc(b + kk * 32), idesc,
+                            (kb | kk) ? 1u : 0u);
+            ptx::mma_commit(&empty[s]);
+          }
+        }
+        ptx::mma_commit(&accf[buf]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---- epilogue: thread = task row (TMEM lane 32q + lane) x half of the tile's units ----
+    const int q = warp & 3, hh = (warp - 2) >> 2;
+    const int r = q * 32 + lane;
+    const int qpt = P.UG / 8;                            // quads per thread
+    ptx::griddep_wait();
+    for (int j = blockIdx.x, k = 0; j < P.ntiles; j += gridDim.x, ++k) {
+      const int p0 = P.lo + (j / P.nut) * 128, u0 = (j % P.nut) * P.UG;
+      const int p = p0 + r;
+      const bool valid = p < P.hi;
+      VMeta m;
+      if (valid) load_meta(D, p, epi_needs_children<E>(), m);
+      const int buf = P.nbuf == 2 ? (k & 1) : 0;
+      const int use = P.nbuf == 2 ? (k >> 1) : k;
+      rwait(&accf[buf], use & 1);
+      ptx::tc_fence_after();
+      const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * P.acc_cols);
+      const int ub = hh * (P.UG / 2);                    // this thread's first unit within the tile
+#pragma unroll 1
+      for (int qb = 0; qb < qpt; qb += QB) {
+        typename EpiK<E>::template In<4, NM> in[QB];
+        UnitC<4> uc[QB];
+        if (valid) {
+#pragma unroll
+          for (int b = 0; b < QB; ++b) {
+            const int jj = u0 + ub + (qb + b) * 4;
+            EpiK<E>::template load<4, NM>(D, jj, m, in[b]);
+            uc[b] = epi_uses_bias<E>() ? load_unit<4>(D, jj, epi_is_lstm<E>()) : UnitC<4>{};
+          }
+        }
+        FV<4> acc[QB][NE];
+#pragma unroll
+        for (int b = 0; b < QB; ++b) fetch_acc<E, NM>(tb, P.UG, ub + (qb + b) * 4, acc[b]);
+        if (valid) {
+#pragma unroll
+          for (int b = 0; b < QB; ++b)
+            EpiK<E>::template store<__nv_bfloat16, 4, NM>(D, u0 + ub + (qb + b) * 4, m, acc[b], in[b], uc[b]);
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&acce[buf]);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+// =====================================================================================
+// host side
+// =====================================================================================
+struct RowsState {
+  CUtensorMap A_hk, A_dz;
+  CUtensorMap B_fwd, B_bwd0, B_bwd1;
+  RPlan fwd{}, bwd{};
+  int num_sms = 148;
+};
+
+static PFN_cuTensorMapEncodeTiled_v12000 r_enc = nullptr;
+
+static bool renc(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return r_enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static RSeg rseg(int a_col, int bmap, int nbox, int box_rows, const int* rows0, int nkb, int acc_col) {
+  RSeg S{};
+  S.a_col = a_col; S.bmap = bmap; S.nbox = nbox; S.box_rows = box_rows;
+  for (int g = 0; g < nbox; ++g) S.b_row0[g] = rows0[g];
+  S.nkb = nkb; S.acc_col = acc_col;
+  return S;
+}
+
+static int r_smem(const RPlan& P) { return 1024 + kRS * P.stage + (2 * kRS + 4) * 8 + 16; }
+
+template <int E, int NM, int QB>
+static bool r_attr(const RPlan& P) {
+  return cudaFuncSetAttribute(k_rows<E, NM, QB>, cudaFuncAttributeMaxDynamicSharedMemorySize, r_smem(P)) == cudaSuccess;
+}
+
+RowsState* rows_init(const Dev& D, int max_vertices) {
+  const char* env = std::getenv("CAVS_ROWS");
+  if (env && env[0] == '0') return nullptr;
+  const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
+  const int h = D.h, N = D.N;
+  if (lstm && (h % 128 || N > 2)) return nullptr;
+  if (!lstm && h % 256) return nullptr;
+  if (!r_enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return nullptr;
+    r_enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  RowsState* rs = new RowsState();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&rs->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t Vp = (uint64_t)max_vertices + kPadRows, G = lstm ? 3 + N : 1;
+  bool ok = renc(&rs->A_hk, D.Hk, (uint64_t)N * h, Vp, 128) && renc(&rs->A_dz, D.dZ, G * h, Vp, 128);
+  RPlan& F = rs->fwd;
+  RPlan& B = rs->bwd;
+  if (lstm) {
+    // forward: block k (4 x 64 columns) = (U_i, U_o, U_u, U_f) h_k for 64 units
+    F.UG = 64; F.n = 256; F.nseg = N;
+    const int rows4[4] = {0, h, 2 * h, 3 * h};
+    for (int k = 0; k < N; ++k) F.seg[k] = rseg(k * h, 0, 4, 64, rows4, h / 64, k * 256);
+    F.acc_cols = 256 * N;
+    ok = ok && renc(&rs->B_fwd, D.Wa, h, 4 * (uint64_t)h, 64);                  // U4 [4h x h]
+    // backward: acc 0 = U_iou^T dz_iou (K = 3h), acc 1 + k = U_f^T dz_fk (K = h); 128 units
+    B.UG = 128; B.n = 128; B.nseg = 1 + N;
+    const int r0[1] = {0};
+    B.seg[0] = rseg(0, 0, 1, 128, r0, 3 * h / 64, 0);
+    for (int k = 0; k < N; ++k) B.seg[1 + k] = rseg((3 + k) * h, 1, 1, 128, r0, h / 64, (1 + k) * 128);
+    B.acc_cols = 128 * (1 + N);
+    ok = ok && renc(&rs->B_bwd0, D.Wc, 3 * (uint64_t)h, h, 128) && renc(&rs->B_bwd1, D.Wd, h, h, 128);
+  } else {
+    // forward: z = [h_l | h_r] W_c^T for 256 units
+    F.UG = 256; F.n = 256; F.nseg = 1;
+    const int r0[1] = {0};
+    F.seg[0] = rseg(0, 0, 1, 256, r0, 2 * h / 64, 0);
+    F.acc_cols = 256;
+    ok = ok && renc(&rs->B_fwd, D.Wa, 2 * (uint64_t)h, h, 256);                 // W_c [h x 2h]
+    // backward: (dh_l, dh_r) = dz W_c for 128 units: W_c^T rows u0 and h + u0
+    B.UG = 128; B.n = 256; B.nseg = 1;
+    const int r2[2] = {0, h};
+    B.seg[0] = rseg(0, 0, 2, 128, r2, h / 64, 0);
+    B.acc_cols = 256;
+    ok = ok && renc(&rs->B_bwd0, D.Wc, h, 2 * (uint64_t)h, 128);                // W_c^T [2h x h]
+    rs->B_bwd1 = rs->B_bwd0;
+  }
+  for (RPlan* P : {&F, &B}) {
+    P->stage = kRA + P->n * 128;
+    P->nbuf = 2 * P->acc_cols <= 512 ? 2 : 1;
+    P->nut = h / P->UG;
+  }
+  if (lstm) {
+    ok = ok && (N == 1 ? r_attr<EPI_LSTM_FWD, 1, 2>(F) && r_attr<EPI_LSTM_BWD, 1, 2>(B)
+                       : r_attr<EPI_LSTM_FWD, 2, 2>(F) && r_attr<EPI_LSTM_BWD, 2, 2>(B));
+  } else {
+    ok = ok && r_attr<EPI_FC_FWD, 1, 4>(F) && r_attr<EPI_FC_BWD, 1, 4>(B);
+  }
+  if (!ok) { delete rs; return nullptr; }
+  return rs;
+}
+
+void rows_destroy(RowsState* rs) { delete rs; }
+
+int rows_tiles(const RowsState* rs, bool backward, int rows) {
+  return rs ? cdiv(rows, 128) * (backward ? rs->bwd.nut : rs->fwd.nut) : 0;
+}
+
+template <int E, int NM, int QB>
+static void r_launch(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const Dev& D, const RPlan& P,
+                     int grid, cudaStream_t s) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kRThreads, 1, 1);
+  cfg.dynamicSmemBytes = r_smem(P);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_rows<E, NM, QB>, a, b0, b1, D, P);
+}
+
+bool rows_level(const Dev& D, RowsState* rs, bool backward, int lo, int hi, cudaStream_t s) {
+  if (!rs || hi <= lo) return false;
+  RPlan P = backward ? rs->bwd : rs->fwd;
+  P.lo = lo; P.hi = hi;
+  P.ntiles = cdiv(hi - lo, 128) * P.nut;
+  const int grid = std::min(P.ntiles, rs->num_sms);
+  const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
+  if (lstm) {
+    if (!backward) {
+      if (D.N == 1) r_launch<EPI_LSTM_FWD, 1, 2>(rs->A_hk, rs->B_fwd, rs->B_fwd, D, P, grid, s);
+      else r_launch<EPI_LSTM_FWD, 2, 2>(rs->A_hk, rs->B_fwd, rs->B_fwd, D, P, grid, s);
+    } else {
+      if (D.N == 1) r_launch<EPI_LSTM_BWD, 1, 2>(rs->A_dz, rs->B_bwd0, rs->B_bwd1, D, P, grid, s);
+      else r_launch<EPI_LSTM_BWD, 2, 2>(rs->A_dz, rs->B_bwd0, rs->B_bwd1, D, P, grid, s);
+    }
+  } else {
+    if (!backward) r_launch<EPI_FC_FWD, 1, 4>(rs->A_hk, rs->B_fwd, rs->B_fwd, D, P, grid, s);
+    else r_launch<EPI_FC_BWD, 1, 4>(rs->A_dz, rs->B_bwd0, rs->B_bwd1, D, P, grid, s);
+  }
+  return true;
+}
+
+}  // namespace cavs

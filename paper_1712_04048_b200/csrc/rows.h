@@ -1,0 +1,14 @@
+// rows.h — row-tiled tcgen05 level GEMMs for large tasks at h > 512 (fused cell epilogues), see rows.cu.
+#pragma once
+#include "kernels.h"
+
+namespace cavs {
+
+struct RowsState;
+RowsState* rows_init(const Dev& D, int max_vertices);   // nullptr: shape not supported / disabled
+void rows_destroy(RowsState* rs);
+int rows_tiles(const RowsState* rs, bool backward, int rows);   // tiles of a task of `rows` rows
+// one task V_t = rows [lo, hi) of the forward (or backward) level step; false: caller falls back
+bool rows_level(const Dev& D, RowsState* rs, bool backward, int lo, int hi, cudaStream_t s);
+
+}  // namespace cavs

@@ -27,6 +27,7 @@
 #include "cells.cuh"
 #include "gemm.h"
 #include "lazy.h"
+#include "rows.h"
 #include "persist.h"
 #include "ptx.cuh"
 #include "tc.h"
@@ -413,6 +414,8 @@ struct TcState {
   PersistState* ps = nullptr;   // persistent weight-stationary level kernels (persist.cu), if the shape admits
   GemmState* gs = nullptr;      // row-tiled x-projection / dX GEMMs (gemm.cu)
   LazyState* ls = nullptr;      // stream-K lazy weight-gradient GEMMs (lazy.cu)
+  RowsState* rs = nullptr;      // row-tiled level GEMMs for large tasks when the persistent path is off (rows.cu)
+  int rows_min_tiles = 64;      // a task uses the row-tiled kernel from this many tiles on
   std::string info;
 };
 
@@ -483,6 +486,12 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
     t->ps = persist_init(D, max_vertices, &why);
     t->info = t->ps ? "levels: " + persist_describe(t->ps)
                     : "levels: per-task tcgen05 launches (persistent path unavailable: " + why + ")";
+    if (!t->ps) {
+      t->rs = rows_init(D, max_vertices);
+      const char* mt = std::getenv("CAVS_ROWS_MIN_TILES");
+      if (mt) t->rows_min_tiles = std::atoi(mt);
+      if (t->rs) t->info += "; large tasks: row-tiled tcgen05 (>= " + std::to_string(t->rows_min_tiles) + " tiles)";
+    }
   }
   t->info += t->ls ? "; lazy: stream-K tcgen05 (one launch)" : "; lazy: split-K tcgen05 + pack";
   *out = t;
@@ -497,6 +506,7 @@ void tc_destroy(TcState* tc) {
   if (tc && tc->ps) persist_destroy(tc->ps);
   if (tc && tc->gs) gemm_destroy(tc->gs);
   if (tc && tc->ls) lazy_destroy(tc->ls);
+  if (tc && tc->rs) rows_destroy(tc->rs);
   delete tc;
 }
 
@@ -723,7 +733,9 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
     if (t->ps) { if (T > 1) { persist_forward(D, t->ps, T, s); P.count(1); } return; }
     const PlanT F = gs ? gs_lstm_fwd(h, N) : mono_lstm_fwd(h, N);
     for (int tt = 1; tt < T; ++tt) {
-      if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_FWD, Fs, lp[tt], lp[tt + 1], h, s);
+      const int M = lp[tt + 1] - lp[tt];
+      if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_FWD, Fs, lp[tt], lp[tt + 1], h, s);
+      else if (rows_tiles(t->rs, false, M) >= t->rows_min_tiles && rows_level(D, t->rs, false, lp[tt], lp[tt + 1], s)) {}
       else level_N<EPI_LSTM_FWD, 3>(gs, N, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       P.count(1);
     }
@@ -737,7 +749,9 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
     if (gs) { F = plan_empty(); gs_add_ksplit(F, 0, 0, 0, 0, 2 * h, 0); }
     else F = mono_one(2 * h, 1, &zero, &zero);
     for (int tt = 1; tt < T; ++tt) {
-      if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_FWD, Fs, lp[tt], lp[tt + 1], h, s);
+      const int M = lp[tt + 1] - lp[tt];
+      if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_FWD, Fs, lp[tt], lp[tt + 1], h, s);
+      else if (rows_tiles(t->rs, false, M) >= t->rows_min_tiles && rows_level(D, t->rs, false, lp[tt], lp[tt + 1], s)) {}
       else if (gs) launch_level<EPI_FC_FWD, 1, kCluster>(t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       else launch_level<EPI_FC_FWD, 1, 1>(t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       P.count(1);
@@ -779,7 +793,9 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
   } else if (lstm) {
     const PlanT B = gs ? gs_lstm_bwd(h, N) : mono_lstm_bwd(h, N);
     for (int tt = T - 1; tt >= 1; --tt) {
-      if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_BWD, Bs, lp[tt], lp[tt + 1], h, s);
+      const int M = lp[tt + 1] - lp[tt];
+      if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_BWD, Bs, lp[tt], lp[tt + 1], h, s);
+      else if (rows_tiles(t->rs, true, M) >= t->rows_min_tiles && rows_level(D, t->rs, true, lp[tt], lp[tt + 1], s)) {}
       else level_N<EPI_LSTM_BWD, 1>(gs, N, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       P.count(1);
     }
@@ -789,7 +805,9 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
     if (gs) { B = plan_empty(); for (int k = 0; k < 2; ++k) gs_add_ksplit(B, 0, k * h, 0, 0, h, k); }
     else B = mono_one(h, 2, rows, zeros);
     for (int tt = T - 1; tt >= 1; --tt) {
-      if (lp[tt + 1] - lp[tt] <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_BWD, Bs, lp[tt], lp[tt + 1], h, s);
+      const int M = lp[tt + 1] - lp[tt];
+      if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_BWD, Bs, lp[tt], lp[tt + 1], h, s);
+      else if (rows_tiles(t->rs, true, M) >= t->rows_min_tiles && rows_level(D, t->rs, true, lp[tt], lp[tt + 1], s)) {}
       else if (gs) launch_level<EPI_FC_BWD, 2, kCluster>(t->A[2], t->A[2], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       else launch_level<EPI_FC_BWD, 2, 1>(t->A[2], t->A[2], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       P.count(1);

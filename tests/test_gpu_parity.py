@@ -403,3 +403,33 @@ def test_lazy_streamk(case, monkeypatch):
     o = run_gpu(b, "bf16")
     assert "lazy: split-K" in o["ctx"].path_info()
     compare(b, g, o, 1e-5, case + " stream-K vs split-K")
+
+
+# ------------------------------------------------------------------ row-tiled large-task kernels
+ROWS_CASES = {
+    "lstm_n2_h256_sst": lambda: gen.make_batch("tree_lstm", 2, 256, 128, "sst_tree", 48, seed=41),
+    "lstm_n1_h128_chain": lambda: gen.batch_from_graphs([gen.chain(n) for n in (30, 200, 7)] * 60, cell="tree_lstm",
+                                                         N=1, h=128, d=128, seed=42, x_at="all", loss_at="all"),
+    "lstm_n2_h128_unary": lambda: gen.batch_from_graphs(_nary_forest(60, 2, 30, 43), cell="tree_lstm", N=2, h=128,
+                                                        d=64, seed=43),
+    "fc_h256_cbt": lambda: gen.make_batch("tree_fc", 2, 256, 128, "cbt32", 40, seed=44),
+    "fc_h512_sst": lambda: gen.make_batch("tree_fc", 2, 512, 256, "sst_tree", 60, seed=45),
+}
+
+
+@pytest.mark.parametrize("case", list(ROWS_CASES))
+def test_rows_level_kernels(case, monkeypatch):
+    """Row-tiled tcgen05 level GEMMs (rows.cu; forced onto every non-skinny task) against the oracle
+    and against the per-task swap-AB kernels (CAVS_ROWS=0): same bf16 operands and rounding
+    points, another fp32 summation order."""
+    b = ROWS_CASES[case]()
+    monkeypatch.setenv("CAVS_PERSIST", "0")
+    monkeypatch.setenv("CAVS_ROWS_MIN_TILES", "1")
+    g = run_gpu(b, "bf16")
+    assert "large tasks: row-tiled" in g["ctx"].path_info(), g["ctx"].path_info()
+    compare(b, g, run_oracle(b), BF16_TOL, case + " vs fp64 oracle")
+    compare(b, g, run_oracle(b, emulate_bf16=True), 2 * BF16_EMU_TOL, case + " vs bf16-emulating oracle")
+    monkeypatch.setenv("CAVS_ROWS", "0")
+    o = run_gpu(b, "bf16")
+    assert "row-tiled" not in o["ctx"].path_info()
+    compare(b, g, o, BF16_EMU_TOL, case + " row-tiled vs per-task")
