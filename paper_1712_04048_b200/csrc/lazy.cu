@@ -400,10 +400,14 @@ bool lazy_grads(const Dev& D, LazyState* l, cudaStream_t s) {
   struct T { int job, ltile; long long w; };
   std::vector<T> tiles;
   long long W = 0;
-  for (int j = 0; j < nj; ++j) {
+  for (int j = 0; j < nj; ++j) {                       // tm fastest: CTAs of one wave share B column blocks
     const LJob& J = P.job[j];
-    const int nt = cdiv(J.M, kLBM) * J.ntn;
-    for (int t = 0; t < nt; ++t) { tiles.push_back({j, t, (long long)J.nseg * J.nkb}); W += (long long)J.nseg * J.nkb; }
+    const int ntm = cdiv(J.M, kLBM);
+    for (int tn = 0; tn < J.ntn; ++tn)
+      for (int tm = 0; tm < ntm; ++tm) {
+        tiles.push_back({j, tm * J.ntn + tn, (long long)J.nseg * J.nkb});
+        W += (long long)J.nseg * J.nkb;
+      }
   }
   if ((int)tiles.size() > kLazyMaxTiles) return false;
   const int grid = (int)std::max<long long>(1, std::min<long long>(kLMaxCta, W / kLMinPiece));
@@ -412,7 +416,18 @@ bool lazy_grads(const Dev& D, LazyState* l, cudaStream_t s) {
   int nitems = 0;
   int zt = 0;
   long long T0 = 0;
-  for (int ti = 0; ti < (int)tiles.size(); ++ti) {
+  // At least a full wave of tiles (large h): whole-K tiles, tile i on CTA i mod grid.  The CTAs of
+  // a wave then walk the same k-blocks in step and share their A / B blocks in L2 (a stream-K
+  // split would start every CTA at another k and stream the operands from DRAM once per tile).
+  const bool waves = (int)tiles.size() >= grid && grid == kLMaxCta;
+  for (int ti = 0; waves && ti < (int)tiles.size(); ++ti) {
+    LItem it{};
+    it.gtile = (unsigned short)ti; it.ltile = (unsigned short)tiles[ti].ltile; it.job = (unsigned char)tiles[ti].job;
+    it.npiece = 1; it.g0 = 0; it.g1 = (int)tiles[ti].w;
+    per[ti % grid].push_back(it);
+    ++nitems;
+  }
+  for (int ti = 0; !waves && ti < (int)tiles.size(); ++ti) {
     const T& t = tiles[ti];
     LItem it{};
     it.gtile = (unsigned short)ti; it.ltile = (unsigned short)t.ltile; it.job = (unsigned char)t.job;

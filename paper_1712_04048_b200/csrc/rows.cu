@@ -158,9 +158,11 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
 
   if (warp == 0) {
     // ---- TMA producer ----
-    if (lane == 0) {
-      ptx::tma_prefetch(&mA); ptx::tma_prefetch(&mB0); ptx::tma_prefetch(&mB1);
-      ptx::griddep_wait();                               // task rows come from the previous kernels
+    // one box per lane (lane 0: A, lanes 1..nbox: B): boxes issued by one thread are serviced
+    // one after another, boxes of different threads in parallel
+    if (lane == 0) { ptx::tma_prefetch(&mA); ptx::tma_prefetch(&mB0); ptx::tma_prefetch(&mB1); }
+    ptx::griddep_wait();                                 // task rows come from the previous kernels
+    if (lane <= 4) {
       int step = 0;
       for (int j = blockIdx.x; j < P.ntiles; j += gridDim.x) {
         const int p0 = P.lo + (j / P.nut) * 128, u0 = (j % P.nut) * P.UG;
@@ -169,12 +171,16 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
           const CUtensorMap* mb = S.bmap ? &mB1 : &mB0;
           for (int kb = 0; kb < S.nkb; ++kb, ++step) {
             const int s = step % kRS;
+            if (lane > S.nbox) continue;
             if (step >= kRS) rwait(&empty[s], ((step / kRS) & 1) ^ 1);
             uint8_t* st = smem + s * P.stage;
-            ptx::mbar_arrive_expect_tx(&full[s], P.stage);
-            ptx::tma_load_2d(st, &mA, S.a_col + kb * 64, p0, &full[s]);
-            for (int g = 0; g < S.nbox; ++g)
+            if (lane == 0) {
+              ptx::mbar_arrive_expect_tx(&full[s], P.stage);
+              ptx::tma_load_2d(st, &mA, S.a_col + kb * 64, p0, &full[s]);
+            } else {
+              const int g = lane - 1;
               ptx::tma_load_2d(st + kRA + g * S.box_rows * 128, mb, kb * 64, S.b_row0[g] + u0, &full[s]);
+            }
           }
         }
       }
@@ -336,10 +342,10 @@ RowsState* rows_init(const Dev& D, int max_vertices) {
   } else {
     // forward: z = [h_l | h_r] W_c^T for 256 units
     F.UG = 256; F.n = 256; F.nseg = 1;
-    const int r0[1] = {0};
-    F.seg[0] = rseg(0, 0, 1, 256, r0, 2 * h / 64, 0);
+    const int r01[2] = {0, 128};
+    F.seg[0] = rseg(0, 0, 2, 128, r01, 2 * h / 64, 0);
     F.acc_cols = 256;
-    ok = ok && renc(&rs->B_fwd, D.Wa, 2 * (uint64_t)h, h, 256);                 // W_c [h x 2h]
+    ok = ok && renc(&rs->B_fwd, D.Wa, 2 * (uint64_t)h, h, 128);                 // W_c [h x 2h]
     // backward: (dh_l, dh_r) = dz W_c for 128 units: W_c^T rows u0 and h + u0
     B.UG = 128; B.n = 256; B.nseg = 1;
     const int r2[2] = {0, h};
