@@ -77,9 +77,9 @@ static size_t carve(cavs_ctx* c, char* base) {
   D.level = I(V); D.pos = I(V); D.graph_of = I(V); D.parent_v = I(V); D.slot_v = I(V);
   D.pending = I(V); D.queue = I(V);
   D.hdr = I(kHdrWords + V + 1); D.level_ptr = base ? D.hdr + kHdrWords : nullptr;
-  D.roots = I(V); D.cnt = I(V + 1);
+  D.roots = I(V); D.cnt = I(V + 1); D.lrank = I(V); D.goff = I(V + 1); D.gT = I(K); D.lcount = I(V + 1);
   D.gsync = reinterpret_cast<unsigned*>(I(64));
-  D.tile_cnt = I(kLazyMaxTiles + kDbMaxBlocks);
+  D.tile_cnt = I(kLazyMaxTiles + kDbMaxBlocks + 1);   // + the schedule's last-CTA counter
   D.crow = I((V + 1) * (kMaxClusters + 1));
   D.order = I(V); D.child_pos = I(V * N); D.parent_pos = I(V); D.slot = I(V); D.deg = I(V);
   D.xrow_pos = I(Vp); D.tile_x = I(Vp / 64 + 2);
@@ -235,10 +235,9 @@ CAVS_API cavs_status cavs_schedule(cavs_ctx* ctx, int32_t* T_out) {
   CK(cudaSetDevice(ctx->device));
   Dev& D = ctx->D;
   CK(cudaMemsetAsync(D.hdr, 0, sizeof(int) * kHdrWords, ctx->stream));
-  CK(cudaMemsetAsync(D.cnt, 0, sizeof(int) * (D.V + 1), ctx->stream));
   ctx->prof.mark(CAVS_PH_SCHEDULE, ctx->stream);
   launch_schedule(D, ctx->stream);
-  ctx->prof.count(5);
+  ctx->prof.count(3);
   ctx->prof.mark(-1, ctx->stream);
   CK(cudaGetLastError());
   const int nread = kHdrWords + std::min(D.V + 1, kReadback);

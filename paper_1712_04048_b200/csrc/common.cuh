@@ -30,7 +30,11 @@ struct Dev {
   int* tile_x;                      // per 64-position tile: 1 if any vertex has a pull record
   int* hdr;                         // [0] status bits, [1] T, [2] #roots, [3] -, [4..] level_ptr
   int* roots;                       // positions of vertices without a parent
-  int* cnt;                         // level histogram scratch [V+1]
+  int* cnt;                         // per-graph level histograms: cnt[graph_ptr[g] + t] (t < T_g)
+  int* lrank;                       // rank of a vertex among the vertices of its graph and level
+  int* goff;                        // goff[graph_ptr[g] + t]: rows of earlier graphs in task t
+  int* gT;                          // levels of graph g
+  int* lcount;                      // |V_t|
   unsigned* gsync;                  // [0] barrier arrivals, [1] exits: grid barrier of the persistent level kernels
   int ncl;                          // clusters of the persistent level kernels (0: none)
   int* crow;                        // [T][ncl + 1]: first position of task t owned by cluster >= r

@@ -8,30 +8,44 @@
 // (reading Z5).  Tasks are then materialised as level-contiguous position lists.
 #include <algorithm>
 
-#include "common.cuh"
+#include "kernels.h"
 
 namespace cavs {
 
-// One CTA per graph.  Validates (ranges, arity, fan-out), records parents, sweeps.
-__global__ void k_graph_levels(Dev D) {
+constexpr int kSchedCap = 2048;      // vertices of a graph swept in shared memory (larger: global scratch)
+
+// K1 — one CTA per graph: validation (ranges, arity, fan-out), parents, the frontier sweep
+// (level = task id), the graph's level histogram and every vertex's rank among the vertices of
+// its graph and level in ascending id (reading Z4).  State lives in shared memory for graphs
+// of <= kSchedCap vertices (every BASELINE config), else in the graph's slices of the global
+// scratch arrays; local ids throughout.
+__global__ void __launch_bounds__(256) k_graph_sched(Dev D) {
+  extern __shared__ int sm[];
   const int k = blockIdx.x;
   int* st = D.hdr;
-  __shared__ int s_bad, s_head, s_tail, s_done, s_round;
+  __shared__ int s_bad, s_head, s_tail;
   const int lo = D.graph_ptr[k], hi = D.graph_ptr[k + 1];
-  if (threadIdx.x == 0) { s_bad = 0; s_head = 0; s_tail = 0; s_done = 0; s_round = 0; }
+  if (threadIdx.x == 0) { s_bad = 0; s_head = 0; s_tail = 0; }
   __syncthreads();
   if (lo < 0 || hi > D.V || hi <= lo || (k == 0 && lo != 0) || (k == D.K - 1 && hi != D.V)) {
     if (threadIdx.x == 0) atomicOr(st, ST_INVALID);
     return;
   }
   const int n = hi - lo;
-  // pass 1: degrees, arity, child ranges; parents (fan-out check)
-  for (int v = lo + threadIdx.x; v < hi; v += blockDim.x) {
-    D.parent_v[v] = -1;
-    D.graph_of[v] = k;
+  const bool in_smem = n <= kSchedCap;
+  int* par = in_smem ? sm : D.parent_v + lo;                     // local parent id, -1: root
+  int* pend = in_smem ? sm + kSchedCap : D.pending + lo;         // children not yet finished
+  int* lev = in_smem ? sm + 2 * kSchedCap : D.level + lo;
+  int* q = in_smem ? sm + 3 * kSchedCap : D.queue + lo;          // frontier queue (level order)
+  int* cnt = in_smem ? sm + 4 * kSchedCap : D.cnt + lo;          // per-level counters (levels < n)
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    par[i] = -1;
+    cnt[i] = 0;
+    D.graph_of[lo + i] = k;
   }
   __syncthreads();
-  for (int v = lo + threadIdx.x; v < hi; v += blockDim.x) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int v = lo + i;
     const int a = D.child_ptr[v], b = D.child_ptr[v + 1];
     int bad = 0;
     if (a < 0 || b < a || b > D.E) bad |= ST_INVALID;
@@ -40,40 +54,35 @@ __global__ void k_graph_levels(Dev D) {
       for (int e = a; e < b; ++e) {
         const int c = D.child_idx[e];
         if (c < 0 || c >= n) { bad |= ST_INVALID; break; }
-        if (atomicCAS(&D.parent_v[lo + c], -1, v) != -1) bad |= ST_FANOUT;
+        if (atomicCAS(&par[c], -1, i) != -1) bad |= ST_FANOUT;
         else D.slot_v[lo + c] = e - a;
       }
     }
-    D.pending[v] = (bad ? 0 : b - a);
-    if (bad) { atomicOr(&s_bad, bad); }
+    pend[i] = bad ? 0 : b - a;
+    if (bad) atomicOr(&s_bad, bad);
   }
   __syncthreads();
   if (s_bad) {
     if (threadIdx.x == 0) atomicOr(st, s_bad);
     return;
   }
-  // frontier sweep: queue lives in the graph's own slice [lo, hi) of D.queue
-  int* q = D.queue + lo;
-  for (int v = lo + threadIdx.x; v < hi; v += blockDim.x) {
-    if (D.pending[v] == 0) {
-      const int at = atomicAdd(&s_tail, 1);
-      q[at] = v;
-      D.level[v] = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (pend[i] == 0) {
+      q[atomicAdd(&s_tail, 1)] = i;
+      lev[i] = 0;
     }
   }
   __syncthreads();
   int round = 0;
-  while (true) {
+  while (true) {                                     // round r activates exactly the level-r vertices
     const int qs = s_head, qe = s_tail;
     if (qs == qe) break;
     __syncthreads();
     for (int i = qs + threadIdx.x; i < qe; i += blockDim.x) {
-      const int v = q[i];
-      const int p = D.parent_v[v];
-      if (p >= 0 && atomicSub(&D.pending[p], 1) == 1) {
-        D.level[p] = round + 1;
-        const int at = atomicAdd(&s_tail, 1);
-        q[at] = p;
+      const int p = par[q[i]];
+      if (p >= 0 && atomicSub(&pend[p], 1) == 1) {
+        lev[p] = round + 1;
+        q[atomicAdd(&s_tail, 1)] = p;
       }
     }
     __syncthreads();
@@ -81,107 +90,142 @@ __global__ void k_graph_levels(Dev D) {
     ++round;
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    if (s_tail != n) atomicOr(st, ST_CYCLE);      // some vertex never activated
-    else atomicMax(&st[1], round);               // rounds == depth + 1 == this graph's T
+  if (s_tail != n) {                                 // some vertex never activated
+    if (threadIdx.x == 0) atomicOr(st, ST_CYCLE);
+    return;
   }
-}
-
-__global__ void k_level_hist(Dev D) {
-  if (D.hdr[0]) return;
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < D.V; v += gridDim.x * blockDim.x)
-    atomicAdd(&D.cnt[D.level[v]], 1);
-}
-
-// Single CTA: exclusive scan of the level histogram -> level_ptr[0..T].
-__global__ void k_level_scan(Dev D) {
-  if (D.hdr[0]) return;
-  const int T = D.hdr[1];
-  __shared__ int s_warp[32];
-  __shared__ int s_carry;
-  if (threadIdx.x == 0) s_carry = 0;
+  // ranks inside (graph, level) in ascending id: one warp walks the ids 32 at a time
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (int b0 = 0; b0 < n; b0 += 32) {
+      const int i = b0 + lane;
+      const int l = i < n ? lev[i] : -1;
+      const unsigned m = __match_any_sync(~0u, l);
+      const int leader = __ffs(m) - 1;
+      int base = (lane == leader && l >= 0) ? cnt[l] : 0;
+      base = __shfl_sync(~0u, base, leader);
+      if (i < n) D.lrank[lo + i] = base + __popc(m & ((1u << lane) - 1u));
+      __syncwarp();
+      if (lane == leader && l >= 0) cnt[l] = base + __popc(m);
+      __syncwarp();
+    }
+  }
   __syncthreads();
-  for (int base = 0; base < T; base += blockDim.x) {
-    const int l = base + threadIdx.x;
-    const int c = l < T ? D.cnt[l] : 0;
-    int x = c;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int o = 1; o < 32; o <<= 1) { int y = __shfl_up_sync(~0u, x, o); if (lane >= o) x += y; }
-    if (lane == 31) s_warp[w] = x;
-    __syncthreads();
-    if (w == 0) {
-      int y = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
-      for (int o = 1; o < 32; o <<= 1) { int z = __shfl_up_sync(~0u, y, o); if (lane >= o) y += z; }
-      s_warp[lane] = y;
-    }
-    __syncthreads();
-    const int incl = x + (w ? s_warp[w - 1] : 0) + s_carry;
-    if (l < T) D.level_ptr[l] = incl - c;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) s_carry = incl;
-    __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (in_smem) D.level[lo + i] = lev[i];
+    const int p = par[i];
+    D.parent_v[lo + i] = p >= 0 ? lo + p : -1;       // global ids from here on
   }
-  if (threadIdx.x == 0) D.level_ptr[T] = D.V;
+  if (in_smem)
+    for (int l = threadIdx.x; l < round; l += blockDim.x) D.cnt[lo + l] = cnt[l];
+  if (threadIdx.x == 0) {
+    D.gT[k] = round;                                 // rounds == depth + 1 == this graph's T
+    atomicMax(&st[1], round);
+  }
 }
 
-// CTAs stride over levels; each ranks its level's vertices by ascending global id
-// (reading Z4) with a block-wide ballot scan over all V vertices.
-__global__ void k_level_rank(Dev D) {
-  if (D.hdr[0]) return;
-  const int T = D.hdr[1];
-  __shared__ int s_warp[32];
+// Block-wide exclusive scan of one int per thread (blockDim.x multiple of 32, <= 1024).
+__device__ __forceinline__ int block_excl_scan(int x, int* s_warp, int& total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int l = blockIdx.x; l < T; l += gridDim.x) {
-    int running = D.level_ptr[l];
-    for (int base = 0; base < D.V; base += blockDim.x) {
-      const int v = base + threadIdx.x;
-      const bool f = v < D.V && D.level[v] == l;
-      const unsigned m = __ballot_sync(~0u, f);
-      if (lane == 0) s_warp[w] = __popc(m);
-      __syncthreads();
-      int before = 0, total = 0;
-      for (int i = 0; i < nw; ++i) { const int c = s_warp[i]; if (i < w) before += c; total += c; }
-      if (f) {
-        const int p = running + before + __popc(m & ((1u << lane) - 1));
-        D.pos[v] = p;
-        D.order[p] = v;
+  int v = x;
+  for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(~0u, v, o); if (lane >= o) v += y; }
+  if (lane == 31) s_warp[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int y = lane < nw ? s_warp[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) { const int z = __shfl_up_sync(~0u, y, o); if (lane >= o) y += z; }
+    s_warp[lane] = y;
+  }
+  __syncthreads();
+  total = s_warp[nw - 1];
+  const int excl = v - x + (w ? s_warp[w - 1] : 0);
+  __syncthreads();
+  return excl;
+}
+
+// K2 — per task t (CTAs stride over t): exclusive scan over the graphs of their level-t counts
+// -> goff[graph_ptr[g] + t] (rows of graph g inside V_t), the task size, and the cluster row
+// table of the persistent kernels (crow[t][r] = rows before the first graph of cluster r).  The
+// last CTA to finish scans the task sizes into level_ptr and makes crow absolute.
+__global__ void __launch_bounds__(1024) k_level_offsets(Dev D) {
+  if (D.hdr[0]) return;
+  __shared__ int s_warp[32];
+  __shared__ int s_last;
+  const int T = D.hdr[1], K = D.K, V = D.V, nc = D.ncl;
+  for (int t = blockIdx.x; t < T; t += gridDim.x) {
+    int carry = 0;
+    for (int g0 = 0; g0 < K; g0 += blockDim.x) {
+      const int g = g0 + threadIdx.x;
+      const int lo = g < K ? D.graph_ptr[g] : V;
+      const bool has = g < K && t < D.gT[g];
+      const int c = has ? D.cnt[lo + t] : 0;
+      int total;
+      const int excl = carry + block_excl_scan(c, s_warp, total);
+      if (has) D.goff[lo + t] = excl;
+      if (nc > 0 && g < K) {
+        const int cg = (int)((long long)lo * nc / V);
+        const int cp = g > 0 ? (int)((long long)D.graph_ptr[g - 1] * nc / V) : -1;
+        for (int r = cp + 1; r <= cg; ++r) D.crow[(size_t)t * (nc + 1) + r] = excl;
       }
-      running += total;
-      __syncthreads();
+      carry += total;
+    }
+    if (threadIdx.x == 0) {
+      D.lcount[t] = carry;
+      if (nc > 0) {
+        const int cl = (int)((long long)D.graph_ptr[K - 1] * nc / V);
+        for (int r = cl + 1; r <= nc; ++r) D.crow[(size_t)t * (nc + 1) + r] = carry;
+      }
     }
   }
+  __threadfence();
+  __syncthreads();
+  int* done = D.tile_cnt + kLazyMaxTiles + kDbMaxBlocks;
+  if (threadIdx.x == 0) s_last = atomicAdd(done, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  int carry = 0;
+  for (int t0 = 0; t0 < T; t0 += blockDim.x) {
+    const int t = t0 + threadIdx.x;
+    const int c = t < T ? __ldcg(D.lcount + t) : 0;
+    int total;
+    const int excl = carry + block_excl_scan(c, s_warp, total);
+    if (t < T) D.level_ptr[t] = excl;
+    carry += total;
+  }
+  if (threadIdx.x == 0) { D.level_ptr[T] = V; *done = 0; }
+  __syncthreads();
+  if (nc > 0)
+    for (int i = threadIdx.x; i < T * (nc + 1); i += blockDim.x) {
+      const size_t at = i;
+      D.crow[at] = __ldcg(D.crow + at) + D.level_ptr[i / (nc + 1)];
+    }
+}
+
+__device__ __forceinline__ int vpos(const Dev& D, int v, int lo) {
+  const int l = D.level[v];
+  return D.level_ptr[l] + D.goff[lo + l] + D.lrank[v];
 }
 
 // Per vertex: position-indexed plan (children/parent slots, degree).
+// K3 — per vertex: position (level_ptr + rows of earlier graphs in the task + rank), order, and
+// the position-indexed plan (children / parent slots, degree, roots).
 template <class OpT>
 __global__ void k_build_maps(Dev D) {
   if (D.hdr[0]) return;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < D.V; v += gridDim.x * blockDim.x) {
-    const int p = D.pos[v];
     const int lo = D.graph_ptr[D.graph_of[v]];
+    const int p = vpos(D, v, lo);
+    D.pos[v] = p;
+    D.order[p] = v;
     const int a = D.child_ptr[v], deg = D.child_ptr[v + 1] - a;
     D.deg[p] = deg;
     for (int k = 0; k < D.N; ++k)
-      D.child_pos[(size_t)p * D.N + k] = k < deg ? D.pos[lo + D.child_idx[a + k]] : -1;
+      D.child_pos[(size_t)p * D.N + k] = k < deg ? vpos(D, lo + D.child_idx[a + k], lo) : -1;
     const int pv = D.parent_v[v];
-    D.parent_pos[p] = pv >= 0 ? D.pos[pv] : -1;
+    D.parent_pos[p] = pv >= 0 ? vpos(D, pv, lo) : -1;
     D.slot[p] = pv >= 0 ? D.slot_v[v] : 0;
     if (pv < 0) D.roots[atomicAdd(&D.hdr[2], 1)] = p;
-    if (D.ncl > 0) {
-      // graph range of a cluster: cl(g) = graph_ptr[g] * ncl / V (balanced by vertices, monotone
-      // in g); inside task t positions are graph-major, so cluster r owns the contiguous rows
-      // [crow[t][r], crow[t][r + 1]).  Each entry is written by exactly one vertex: the first of
-      // its task whose cluster reaches r, or the task's last vertex for the clusters past it.
-      const int t = D.level[v];
-      const int t0 = D.level_ptr[t], t1 = D.level_ptr[t + 1];
-      const int nc = D.ncl;
-      int* row = D.crow + (size_t)t * (nc + 1);
-      const int c = (int)((long long)lo * nc / D.V);
-      const int cp = p > t0 ? (int)((long long)D.graph_ptr[D.graph_of[D.order[p - 1]]] * nc / D.V) : -1;
-      for (int r = cp + 1; r <= c; ++r) row[r] = p;
-      if (p == t1 - 1)
-        for (int r = c + 1; r <= nc; ++r) row[r] = t1;
-    }
     // an internal vertex with fewer than N children reads zero in its missing slots (Z1)
     if (deg > 0 && deg < D.N) {
       OpT* hk = reinterpret_cast<OpT*>(D.Hk) + (size_t)p * D.N * D.h;
@@ -192,11 +236,15 @@ __global__ void k_build_maps(Dev D) {
 }
 
 void launch_schedule(const Dev& D, cudaStream_t s) {
-  k_graph_levels<<<D.K, 256, 0, s>>>(D);
+  static bool attr = false;
+  constexpr int smem = 5 * kSchedCap * 4;
+  if (!attr) {
+    cudaFuncSetAttribute(k_graph_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  k_graph_sched<<<D.K, 256, smem, s>>>(D);
+  k_level_offsets<<<148, 1024, 0, s>>>(D);
   const int g = std::min(cdiv(D.V, 256), 148 * 8);
-  k_level_hist<<<g, 256, 0, s>>>(D);
-  k_level_scan<<<1, 1024, 0, s>>>(D);
-  k_level_rank<<<148, 1024, 0, s>>>(D);
   if (D.prec == CAVS_BF16) k_build_maps<__nv_bfloat16><<<g, 256, 0, s>>>(D);
   else k_build_maps<float><<<g, 256, 0, s>>>(D);
 }

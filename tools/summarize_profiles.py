@@ -35,7 +35,11 @@ def kclass(name):
     if "k_skinny" in n:
         m = re.search(r"k_skinny<[^,]+, (?:\(int\))?(\d+), (?:\(int\))?(\d+)", n)
         return "skinny[" + ("fwd" if m and m.group(2) == "0" else "bwd") + "]"
-    for k in ("k_tc_typeII", "k_graph_levels", "k_level_hist", "k_level_scan", "k_level_rank", "k_build_maps",
+    if "k_rows" in n:
+        m = re.search(r"k_rows<(?:\(int\))?(\d+)", n)
+        return "rows[" + {"0": "fwd", "2": "bwd", "3": "fc_fwd", "5": "fc_bwd"}.get(m.group(1) if m else "", "?") + "]"
+    for k in ("k_lazy", "k_tc_typeII", "k_graph_sched", "k_level_offsets", "k_graph_levels", "k_level_hist",
+              "k_level_scan", "k_level_rank", "k_build_maps",
               "k_prep", "k_pull", "k_roots", "k_colsum", "k_pack"):
         if k in n:
             return k
@@ -73,8 +77,8 @@ def main():
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
     L = launches(os.path.join(a.src, "launches.csv"))
-    # one step = from the 2nd k_graph_levels launch (warm-up excluded) to the next one
-    starts = [i for i, r in enumerate(L) if "k_graph_levels" in r[1]]
+    # one step = from the 2nd schedule launch (warm-up excluded) to the next one
+    starts = [i for i, r in enumerate(L) if "k_graph_sched" in r[1] or "k_graph_levels" in r[1]]
     s0 = starts[1] if len(starts) > 1 else 0
     s1 = starts[2] if len(starts) > 2 else len(L)
     step = [r for r in L[s0:s1] if not r[1].startswith("void at::")]
