@@ -20,6 +20,10 @@ timeout 600 ncu --set full --cache-control none --clock-control none --import-so
     -k regex:"k_persist" -s ${SKIP:-2} -c ${COUNT:-2} \
     -o gpurun_out/persist -f python bench.py $ARGS > gpurun_out/persist.log 2>&1
 timeout 600 ncu --set full --cache-control none --clock-control none --import-source on \
-    -k regex:"k_gemm_rows|k_tc_typeII" -s 4 -c 5 \
+    -k regex:"k_gemm_rows|k_lazy|k_graph_sched|k_level_offsets|k_build_maps|k_colsum" -s 6 -c 7 \
     -o gpurun_out/rows -f python bench.py $ARGS > gpurun_out/rows.log 2>&1
+timeout 600 ncu --set full --cache-control none --clock-control none --import-source on \
+    -k regex:"k_rows|k_lazy" -s 0 -c 3 \
+    -o gpurun_out/cfg5 -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --pool 2 --config cfg5 > gpurun_out/cfg5.log 2>&1
+timeout 600 python bench.py --config cfg5 --steps 10 --warmup 3 > gpurun_out/bench_cfg5.json 2> gpurun_out/bench_cfg5.err
 ls -la gpurun_out

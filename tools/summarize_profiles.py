@@ -103,7 +103,7 @@ def main():
         lines.append(f"| {c} | {n} | {t / 1e3:.1f} | {100 * t / tot:.1f}% |")
     # full capture of the level kernels
     traffic = {}
-    reps = [os.path.join(a.src, r) for r in ("levels.ncu-rep", "persist.ncu-rep", "rows.ncu-rep")]
+    reps = [os.path.join(a.src, r) for r in ("levels.ncu-rep", "persist.ncu-rep", "rows.ncu-rep", "cfg5.ncu-rep")]
     for rep in [r for r in reps if os.path.exists(r)]:
         hdr, data = raw_metrics(rep)
         ix = {n: i for i, n in enumerate(hdr)}
@@ -131,7 +131,7 @@ def main():
             per[c].append((rd + wr) * 1e6)
         fwd = per.get("tc_level[fwd,CL=4]", []) + per.get("skinny[fwd]", []) + per.get("persist[fwd]", [])
         bwd = per.get("tc_level[bwd,CL=4]", []) + per.get("skinny[bwd]", []) + per.get("persist[bwd]", [])
-        lazy = per.get("k_tc_typeII", [])
+        lazy = per.get("k_lazy", []) or per.get("k_tc_typeII", [])
         if fwd:
             traffic[f"{a.config}:fwd_levels"] = sum(fwd) / len(fwd)
         if bwd:
@@ -148,6 +148,16 @@ def main():
             json.dump(b, open(os.path.join(prof, f"{a.round}_bench.json"), "w"), indent=1)
         except Exception as e:  # noqa: BLE001
             lines += ["", f"(bench.json unreadable: {e})"]
+    b5 = os.path.join(a.src, "bench_cfg5.json")
+    if os.path.exists(b5):
+        try:
+            b = json.loads(open(b5).read().strip().splitlines()[-1])
+            json.dump(b, open(os.path.join(prof, f"{a.round}_bench_cfg5.json"), "w"), indent=1)
+            lines += ["", "## cfg5 bench line (Tree-FC h = 2048, no profiler attached)", "", "```",
+                      json.dumps({k: b[k] for k in ("value", "unit", "ms_per_step", "roofline", "phases") if k in b},
+                                 indent=1)[:4000], "```"]
+        except Exception as e:  # noqa: BLE001
+            lines += ["", f"(bench_cfg5.json unreadable: {e})"]
     open(os.path.join(prof, f"{a.round}_summary.md"), "w").write("\n".join(lines) + "\n")
     tp = os.path.join(prof, "traffic.json")
     old = json.load(open(tp)) if os.path.exists(tp) else {}
