@@ -326,12 +326,31 @@ def main():
         hdp = torch.empty(ctx.P, dtype=torch.float32).pin_memory()
         h2d = sum(v.numel() * v.element_size() for v in hp.values())
         d2h = hdp.numel() * 4
+        dv = {k: torch.empty_like(v, device=dev) for k, v in hp.items()}
+
+        def e2e_step():
+            if world == 1:                          # one C-ABI call: H2D, schedule, fwd, bwd, D2H
+                ctx.train_step_host(hp["gp"], hp["cp"], hp["ci"], hp["pr"], hp["x"], hp["xr"], hp["g"], hdp)
+                return
+            for k, v in hp.items():                 # N > 1: the same copies around the data-parallel step
+                dv[k].copy_(v, non_blocking=True)
+            V = dv["cp"].shape[0] - 1
+            ctx.load_graphs(dv["gp"], dv["cp"], dv["ci"])
+            ctx.schedule(wait=False)
+            ctx.forward(dv["pr"], dv["x"], dv["xr"], h_out[:V])
+            ctx.backward(dv["g"], dparams, dx[:dv["x"].shape[0]])
+            dp.allreduce_grads(dparams)
+            hdp.copy_(dparams, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+
         for _ in range(max(1, args.warmup)):
-            ctx.train_step_host(hp["gp"], hp["cp"], hp["ci"], hp["pr"], hp["x"], hp["xr"], hp["g"], hdp)
+            e2e_step()
         e_steps = max(3, args.steps // 2)
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(e_steps):
-            ctx.train_step_host(hp["gp"], hp["cp"], hp["ci"], hp["pr"], hp["x"], hp["xr"], hp["g"], hdp)
+            e2e_step()
         e_ms = 1000 * (time.perf_counter() - t0) / e_steps
         if world > 1:
             tt = torch.tensor([e_ms], device=dev)
@@ -339,8 +358,9 @@ def main():
             e_ms = float(tt.item())
         e2e = {"value": world * hb.K / (e_ms / 1000), "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms,
-               "note": "cavs_train_step_host: pinned host CSR/params/x/x_row/Gamma -> device, schedule, fwd, bwd, "
-                       "dparams -> host, synchronised each step (host wall clock)"}
+               "note": ("cavs_train_step_host" if world == 1 else "copies + step + NCCL all-reduce") +
+                       ": pinned host CSR/params/x/x_row/Gamma -> device, schedule, fwd, bwd, "
+                       "dparams -> host, synchronised each step (host wall clock, max over ranks)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -7,7 +7,7 @@
 namespace cavs {
 
 constexpr int kMaxN = 4;          // max arity supported by the kernels
-constexpr int kDbChunks = 128;    // row chunks of the deterministic db column reduction
+constexpr int kDbChunks = 32;     // row chunks of the deterministic db column reduction
 constexpr int kSplitMax = 8;      // max split-K of the lazy tensor-core GEMMs
 constexpr int kLazyMaxTiles = 1024;   // arrival counters of the stream-K lazy kernel (lazy.cu)
 constexpr int kMaxClusters = 16;     // graph-range clusters of the persistent level kernels (persist.cu)

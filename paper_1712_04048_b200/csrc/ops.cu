@@ -163,12 +163,12 @@ __global__ void __launch_bounds__(256) k_colsum(Dev D, float* part, int lcols) {
       const OpT* col = dz + pc + k * h;
       if constexpr (sizeof(OpT) == 2) {
         int r = r0 + warp;
-        for (; r + 24 < r1; r += 32) {                      // 4 rows in flight
-          uint4 u[4];
+        for (; r + 56 < r1; r += 64) {                      // 8 rows in flight
+          uint4 u[8];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) u[q] = *reinterpret_cast<const uint4*>(col + (size_t)(r + 8 * q) * cols);
+          for (int q = 0; q < 8; ++q) u[q] = *reinterpret_cast<const uint4*>(col + (size_t)(r + 8 * q) * cols);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < 8; ++q) {
             const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u[q]);
 #pragma unroll
             for (int e = 0; e < 4; ++e) { const float2 f = __bfloat1622float2(b2[e]); acc[2 * e] += f.x; acc[2 * e + 1] += f.y; }
@@ -216,12 +216,12 @@ __global__ void __launch_bounds__(256) k_colsum(Dev D, float* part, int lcols) {
   __threadfence();
   if (L < lcols) {
     float v = 0.f;
-    for (int c0 = 0; c0 < (int)gridDim.y; c0 += 8) {        // 8 partials in flight, summed in chunk order
-      float t[8];
+    for (int c0 = 0; c0 < (int)gridDim.y; c0 += 32) {       // 32 partials in flight, summed in chunk order
+      float t[32];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) t[e] = c0 + e < (int)gridDim.y ? __ldcg(part + (size_t)(c0 + e) * lcols + L) : 0.f;
+      for (int e = 0; e < 32; ++e) t[e] = c0 + e < (int)gridDim.y ? __ldcg(part + (size_t)(c0 + e) * lcols + L) : 0.f;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) v += t[e];
+      for (int e = 0; e < 32; ++e) v += t[e];
     }
     const size_t H = h, Dd = D.d;
     if (lstm) {

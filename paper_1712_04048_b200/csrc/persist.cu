@@ -173,9 +173,13 @@ __device__ __forceinline__ void mma_level(const PPlan& P, int ntile, uint32_t a_
   // lane issues each box's MMAs + commit.
   constexpr uint32_t idesc = ptx::idesc_bf16(128, NT, 0, 0);
   constexpr int ni = NT == 16 ? 0 : NT == 32 ? 1 : 2;
+  // plan constants hoisted into registers (no indexed constant-bank loads in the issue loop);
+  // accumulator of segment sg = acc0 + sg * NT (every plan maps segment sg to accumulator sg)
   const int sk = P.sk[ni], S = P.S;
-  const int nkb = P.nseg * P.nkbA;                  // the tile's k-blocks, segment-major
+  const int nkbA = P.nkbA;
+  const int nkb = P.nseg * nkbA;                    // the tile's k-blocks, segment-major
   const int nbox = (nkb + sk - 1) / sk;
+  const uint32_t acc0 = (uint32_t)P.acc0, stage16 = (uint32_t)(P.stage >> 4);
   for (int j = 0; j < ntile; ++j, ++tcount) {
     if (tcount > 0) { pwait_warp(tmem_empty, (tcount - 1) & 1); ptx::tc_fence_after(); }
     int sg = 0, kba = 0;                              // (segment, weight k-block) of the next k-block
@@ -183,30 +187,29 @@ __device__ __forceinline__ void mma_level(const PPlan& P, int ntile, uint32_t a_
       const int s = step % S;
       pwait_warp(&full[s], (step / S) & 1);
       ptx::tc_fence_after();
-      if (tr && tr[0] == 0) tr[0] = gtime();
-      const int g1 = min(nkb, (b + 1) * sk);
+      if (tr) { if (tr[0] == 0) tr[0] = gtime(); if (tr[1] == 0) tr[2] = gtime(); }   // first / last box of the first tile
+      const int cnt = min(nkb, (b + 1) * sk) - b * sk;
       if (ptx::elect_one()) {
-        uint32_t bl = b_lo + (uint32_t)s * (uint32_t)(P.stage >> 4);
-        int sgi = sg, kbi = kba;
-        for (int g = b * sk; g < g1; ++g) {
-          const uint32_t d = (uint32_t)(P.acc0 + P.seg_acc[sgi] * NT);
-          const uint32_t first = (P.seg_init[sgi] && kbi == 0) ? 1u : 0u;   // first product into the accumulator
-          const uint32_t al = a_lo + (uint32_t)kbi * (kPKb >> 4);
+        uint32_t bl = b_lo + (uint32_t)s * stage16;
+        int kbi = kba;
+        uint32_t d = acc0 + (uint32_t)(sg * NT);
+        for (int g = 0; g < cnt; ++g) {
           const uint32_t at = (uint32_t)kbi * 32u;     // TMEM column of the weights' k-block
+          const uint32_t al = a_lo + (uint32_t)kbi * (kPKb >> 4);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t acc_flag = (kk == 0 && first) ? 0u : 1u;
+            const uint32_t acc_flag = (kk == 0 && kbi == 0) ? 0u : 1u;   // first product into the accumulator
             if constexpr (TS) ptx::mma_bf16_ts(d, at + kk * 8, sw128_desc(bl + kk * 2), idesc, acc_flag);
             else ptx::mma_bf16(d, sw128_desc(al + kk * 2), sw128_desc(bl + kk * 2), idesc, acc_flag);
           }
           bl += (NT * 128) >> 4;
-          if (++kbi == P.nkbA) { kbi = 0; ++sgi; }
+          if (++kbi == nkbA) { kbi = 0; d += NT; }
         }
         ptx::mma_commit(&empty[s]);
       }
       __syncwarp();
-      kba += g1 - b * sk;                             // advance (all lanes, uniform)
-      while (kba >= P.nkbA) { kba -= P.nkbA; ++sg; }
+      kba += cnt;                                     // advance (all lanes, uniform)
+      while (kba >= nkbA) { kba -= nkbA; ++sg; }
     }
     if (ptx::elect_one()) ptx::mma_commit(done);
     __syncwarp();
@@ -338,7 +341,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
         cl_rows(D, t, r, lo, M);
         const int ni = nt_index(M, 1, P.max_ni), nt = 16 << ni;
         const int ntile = (M + nt - 1) / nt;
-        unsigned long long trm[2] = {0, 0};
+        unsigned long long trm[3] = {0, 0, 0};
         unsigned long long* tr = D.trace ? trm : nullptr;
         if (P.tsA) {
           if (ni == 0) mma_level<16, true>(P, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
@@ -349,7 +352,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
           else if (ni == 1) mma_level<32, false>(P, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
           else mma_level<64, false>(P, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
         }
-        if (D.trace && ntile > 0 && lane == 0) ptrace(D, 4000 + E, blockIdx.x, i, trm[0], trm[1], 0, nt, 0);
+        if (D.trace && ntile > 0 && lane == 0) ptrace(D, 4000 + E, blockIdx.x, i, trm[0], trm[1], trm[2], nt, 0);
       }
     }
     __syncwarp();
@@ -545,6 +548,8 @@ static bool plan_layout(PPlan& P, bool tsA) {
   // segments must be contiguous B columns (one box may span several)
   for (int sg = 1; sg < P.nseg; ++sg)
     if (P.seg_bcol[sg] != P.seg_bcol[0] + sg * P.nkbA * 64) return false;
+  for (int sg = 0; sg < P.nseg; ++sg)
+    if (P.seg_acc[sg] != sg) return false;           // the issue loop assumes accumulator sg for segment sg
   for (int sg = 0; sg < P.nseg; ++sg) {
     P.seg_init[sg] = 1;
     for (int e = 0; e < sg; ++e)

@@ -56,6 +56,65 @@ __global__ void k_rate(int iters, unsigned long long* out) {
   if (warp == 0) { ptx::tc_fence_after(); ptx::tmem_dealloc<512>(tmem); }
 }
 
+// persist-like issue: per tile 2 segments x 8 k-blocks x 4 MMAs (TS, N = 16), A walking 256 TMEM
+// columns, B walking a 32 KB box (16 k-blocks of 16 rows), 2 accumulators; one commit per tile.
+template <int N>
+__global__ void k_tile_issue(int iters, unsigned long long* out, int wait_each) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) { ptx::mbar_init(&bar, 1); ptx::fence_mbar_init(); }
+  if (warp == 0) ptx::tmem_alloc<512>(&slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = slot;
+  const uint32_t b = ptx::smem_u32(smem);
+  constexpr uint32_t idesc = ptx::idesc_bf16(128, N, 0, 0);
+  unsigned long long t0 = 0;
+  if (warp == 0) {
+    uint32_t ph = 0;
+    if (ptx::elect_one()) {
+      t0 = clock64();
+      for (int it = 0; it < iters; ++it) {
+        for (int g = 0; g < 16; ++g) {
+          const uint32_t d = tmem + 256 + (g >> 3) * N;
+          const uint32_t at = (uint32_t)(g & 7) * 32u;
+          const uint32_t bl = b + (uint32_t)g * N * 128;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            ptx::mma_bf16_ts(d, tmem + at + kk * 8, desc(bl + kk * 32), idesc, (g & 7) | kk ? 1u : 0u);
+        }
+        if (wait_each) { ptx::mma_commit(&bar); ptx::mbar_wait(&bar, ph); ph ^= 1; }
+      }
+      if (!wait_each) { ptx::mma_commit(&bar); ptx::mbar_wait(&bar, 0); }
+      out[blockIdx.x] = clock64() - t0;
+    }
+    __syncwarp();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { ptx::tc_fence_after(); ptx::tmem_dealloc<512>(tmem); }
+}
+
+template <int N>
+void run_tile(int wait_each) {
+  unsigned long long* d;
+  cudaMalloc(&d, 148 * 8);
+  const int smem = 16 * N * 128 + 1024;
+  cudaFuncSetAttribute(k_tile_issue<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int iters = 64;
+  k_tile_issue<N><<<1, 128, smem>>>(iters, d, wait_each);
+  k_tile_issue<N><<<1, 128, smem>>>(iters, d, wait_each);
+  cudaDeviceSynchronize();
+  unsigned long long h = 0;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  printf("tile-issue N=%3d wait_each=%d : %6.1f cycles/MMA (64 MMAs per tile)  err=%s\n", N, wait_each, (double)h / (iters * 64),
+         cudaGetErrorString(cudaGetLastError()));
+  cudaFree(d);
+}
+
 template <int N, bool TS>
 void run(int grid) {
   unsigned long long* d;
@@ -77,6 +136,7 @@ void run(int grid) {
 }
 
 int main() {
+  for (int w : {0, 1}) { run_tile<16>(w); run_tile<32>(w); run_tile<64>(w); }
   for (int grid : {1, 148}) {
     run<16, false>(grid); run<32, false>(grid); run<64, false>(grid); run<128, false>(grid); run<256, false>(grid);
     run<16, true>(grid); run<32, true>(grid); run<64, true>(grid); run<128, true>(grid); run<256, true>(grid);

@@ -58,14 +58,16 @@ for kind in sorted(set(int(k) for k in rec[:, 0] if 4000 <= k < 5000)):
     E = kind - 4000
     M_ = rec[rec[:, 0] == kind]
     P5 = rec[rec[:, 0] == 5000 + E]
-    print(f"== MMA kind {kind}: per task: nt | producer first issue -> first full (max, mean) | first full -> tile committed (max, mean) | ctas")
+    print(f"== MMA kind {kind}: per task: nt | producer first issue -> first full (max, mean) | first full -> tile committed (max, mean) | first full -> last box full (max, mean) | ctas")
     for i in sorted(set(M_[:, 2])):
         m = M_[M_[:, 2] == i]
         p = P5[P5[:, 2] == i]
         iss = {int(c): int(t) for c, t in zip(p[:, 1], p[:, 3])}
         lat = np.array([(int(r[3]) - iss[int(r[1])]) / 1e3 for r in m if int(r[1]) in iss])
         mm = (m[:, 4] - m[:, 3]) / 1e3
-        print(f"  i={i:3d} nt={int(m[0, 6]):3d} | {lat.max():6.2f} {lat.mean():6.2f} | {mm.max():6.2f} {mm.mean():6.2f} | {len(m)}")
+        lb = (m[:, 5] - m[:, 3]) / 1e3
+        print(f"  i={i:3d} nt={int(m[0, 6]):3d} | {lat.max():6.2f} {lat.mean():6.2f} | {mm.max():6.2f} {mm.mean():6.2f} | "
+              f"{lb.max():6.2f} {lb.mean():6.2f} | {len(m)}")
 
 # epilogue detail (6000+E): [cta, i, staged, et0 loop end, max thread loop end, after barrier]
 for kind in sorted(set(int(k) for k in rec[:, 0] if 6000 <= k < 7000)):
