@@ -130,7 +130,7 @@ __device__ __forceinline__ void lstm_finish(const Dev& D, int j, const VMeta& m,
       f.v[e] = act_sig<OpT>(zf[k].v[e]);
       if (k < m.deg) c.v[e] = fmaf(f.v[e], ck[k].v[e], c.v[e]);   // missing children: c_k = 0 (Z1)
     }
-    stv<VW>(g + (3 + k) * h, f);
+    if (k < m.deg) stv<VW>(g + (3 + k) * h, f);   // dF reads f_k only for present children
   }
 #pragma unroll
   for (int e = 0; e < VW; ++e) hv.v[e] = o.v[e] * act_tanh<OpT>(c.v[e]);

@@ -59,12 +59,13 @@ __global__ void k_rate(int iters, unsigned long long* out) {
 // persist-like issue: per tile 2 segments x 8 k-blocks x 4 MMAs (TS, N = 16), A walking 256 TMEM
 // columns, B walking a 32 KB box (16 k-blocks of 16 rows), 2 accumulators; one commit per tile.
 template <int N>
-__global__ void k_tile_issue(int iters, unsigned long long* out, int wait_each) {
+__global__ void k_tile_issue(int iters, unsigned long long* out, int wait_each, int noise) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
+  __shared__ int slot2;
   const int warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) { ptx::mbar_init(&bar, 1); ptx::fence_mbar_init(); }
+  if (threadIdx.x == 0) { ptx::mbar_init(&bar, 1); ptx::fence_mbar_init(); slot2 = 0; }
   if (warp == 0) ptx::tmem_alloc<512>(&slot);
   ptx::tc_fence_before();
   __syncthreads();
@@ -90,8 +91,14 @@ __global__ void k_tile_issue(int iters, unsigned long long* out, int wait_each) 
       }
       if (!wait_each) { ptx::mma_commit(&bar); ptx::mbar_wait(&bar, 0); }
       out[blockIdx.x] = clock64() - t0;
+      *(volatile int*)&slot2 = 1;
     }
     __syncwarp();
+  } else if (noise == 1) {                           // other warps spin on a shared-memory flag
+    while (*(volatile int*)&slot2 == 0) { }
+  } else if (noise == 2) {                           // other warps read TMEM (epilogue-like)
+    const uint32_t q = (uint32_t)((warp & 3) * 32) << 16;
+    while (*(volatile int*)&slot2 == 0) { uint32_t r[4]; asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(tmem + q + 400)); asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -99,18 +106,18 @@ __global__ void k_tile_issue(int iters, unsigned long long* out, int wait_each) 
 }
 
 template <int N>
-void run_tile(int wait_each) {
+void run_tile(int wait_each, int noise = 0) {
   unsigned long long* d;
   cudaMalloc(&d, 148 * 8);
   const int smem = 16 * N * 128 + 1024;
   cudaFuncSetAttribute(k_tile_issue<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 64;
-  k_tile_issue<N><<<1, 128, smem>>>(iters, d, wait_each);
-  k_tile_issue<N><<<1, 128, smem>>>(iters, d, wait_each);
+  k_tile_issue<N><<<1, noise ? 384 : 128, smem>>>(iters, d, wait_each, noise);
+  k_tile_issue<N><<<1, noise ? 384 : 128, smem>>>(iters, d, wait_each, noise);
   cudaDeviceSynchronize();
   unsigned long long h = 0;
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-  printf("tile-issue N=%3d wait_each=%d : %6.1f cycles/MMA (64 MMAs per tile)  err=%s\n", N, wait_each, (double)h / (iters * 64),
+  printf("tile-issue N=%3d wait_each=%d noise=%d : %6.1f cycles/MMA (64 MMAs per tile)  err=%s\n", N, wait_each, noise, (double)h / (iters * 64),
          cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
@@ -137,6 +144,8 @@ void run(int grid) {
 
 int main() {
   for (int w : {0, 1}) { run_tile<16>(w); run_tile<32>(w); run_tile<64>(w); }
+  for (int nz : {1, 2}) { run_tile<16>(1, nz); run_tile<32>(1, nz); }
+  return 0;
   for (int grid : {1, 148}) {
     run<16, false>(grid); run<32, false>(grid); run<64, false>(grid); run<128, false>(grid); run<256, false>(grid);
     run<16, true>(grid); run<32, true>(grid); run<64, true>(grid); run<128, true>(grid); run<256, true>(grid);
