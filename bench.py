@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--inference", action="store_true",
+                    help="forward-only (cavs_forward_inference): inference samples/s, no backward")
     return ap.parse_args()
 
 
@@ -247,6 +249,9 @@ def main():
         V = p["cp"].shape[0] - 1
         ctx.load_graphs(p["gp"], p["cp"], p["ci"])
         ctx.schedule(wait=False)            # header consumed inside forward, overlapping the pull
+        if args.inference:
+            ctx.forward_inference(params, p["x"], p["xr"], h_out[:V])
+            return
         ctx.forward(params, p["x"], p["xr"], h_out[:V])
         ctx.backward(p["g"], dparams, dx[:p["x"].shape[0]])
         if world > 1:
@@ -318,7 +323,7 @@ def main():
 
     # ---- end to end through the C-ABI with HOST buffers ----
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.inference:
         hb = batches[0]
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
         hp = dict(gp=pin(hb.graph_ptr), cp=pin(hb.child_ptr), ci=pin(hb.child_idx), pr=pin(params.cpu().numpy()),
@@ -363,14 +368,16 @@ def main():
                        "dparams -> host, synchronised each step (host wall clock, max over ranks)"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.inference:
         cpu = cpu_baseline(args, b0.K)
 
     if rank == 0:
         metric = {"tree_lstm": "Tree-LSTM train samples/s (fwd+bwd)", "tree_fc": "Tree-FC train samples/s (fwd+bwd)"}
         line = {
-            "metric": metric[b0.cell] if args.config != "cfg2" and args.config != "cfg3"
-            else "LSTM train samples/s (fwd+bwd)",
+            "metric": (metric[b0.cell] if args.config != "cfg2" and args.config != "cfg3"
+                       else "LSTM train samples/s (fwd+bwd)").replace(
+                           "train samples/s (fwd+bwd)", "inference samples/s (fwd only)" if args.inference else
+                           "train samples/s (fwd+bwd)"),
             "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": args.precision, "data": "synthetic",

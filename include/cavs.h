@@ -146,6 +146,14 @@ cavs_status cavs_get_schedule(cavs_ctx* ctx, int32_t* level, int32_t* level_ptr,
 cavs_status cavs_forward(cavs_ctx* ctx, const float* params, int32_t n_x, const float* x,
                          const int32_t* x_row, float* h_out);
 
+/* Inference-only forward: the same pass as cavs_forward (same h_out,
+ * bit for bit) without saving the activations dF needs (gates, memory cells) — only the
+ * states the next tasks gather (scatter into the parents' slots) and push(h) are written.
+ * A following cavs_backward fails with CAVS_E_STATE until a training cavs_forward ran.
+ * Arguments, layouts, ownership and errors as cavs_forward. */
+cavs_status cavs_forward_inference(cavs_ctx* ctx, const float* params, int32_t n_x, const float* x,
+                                   const int32_t* x_row, float* h_out);
+
 /* Backward pass (Alg. 1 BACKWARD): tasks in reverse order, gradients
  * ADDED; scatter is gather's adjoint, push is pull's; parameter
  * gradients are lazily batched over all vertices once after the level loop (§3.5).

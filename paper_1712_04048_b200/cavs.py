@@ -51,6 +51,7 @@ def _load():
         "cavs_schedule": (S, [P, ctypes.POINTER(I32)]),
         "cavs_get_schedule": (S, [P, P, P, P]),
         "cavs_forward": (S, [P, P, I32, P, P, P]),
+        "cavs_forward_inference": (S, [P, P, I32, P, P, P]),
         "cavs_backward": (S, [P, P, P, P]),
         "cavs_train_step_host": (S, [P, I32, I32, I32, P, P, P, P, I32, P, P, P, P, P, P]),
         "cavs_kernel_launches": (I64, [P]),
@@ -71,7 +72,7 @@ def _load():
 _lib = _load()
 EXPORTS = ["cavs_param_count", "cavs_create", "cavs_set_stream", "cavs_workspace_bytes",
            "cavs_set_workspace", "cavs_load_graphs", "cavs_schedule", "cavs_get_schedule",
-           "cavs_forward", "cavs_backward", "cavs_train_step_host", "cavs_kernel_launches",
+           "cavs_forward", "cavs_forward_inference", "cavs_backward", "cavs_train_step_host", "cavs_kernel_launches",
            "cavs_last_error", "cavs_path_info", "cavs_destroy", "cavs_profile", "cavs_profile_read"]
 PHASES = ["schedule", "prep", "xproj", "fwd_levels", "bwd_roots", "bwd_levels", "lazy", "dx", "reduce"]
 
@@ -191,6 +192,16 @@ class Context:
             h_out = torch.empty(self.V, self.h, dtype=torch.float32, device=self.device)
         self._fwd_keep = (params, x, x_row, h_out)
         self._check(_lib.cavs_forward(self._ctx, _ptr(params), int(x.shape[0]), _ptr(x), _ptr(x_row), _ptr(h_out)))
+        return h_out
+
+    def forward_inference(self, params, x, x_row, h_out=None):
+        """Inference-only forward: same h_out, no activations saved (backward needs forward())."""
+        torch = self._torch
+        if h_out is None:
+            h_out = torch.empty(self.V, self.h, dtype=torch.float32, device=self.device)
+        self._fwd_keep = (params, x, x_row, h_out)
+        self._check(_lib.cavs_forward_inference(self._ctx, _ptr(params), int(x.shape[0]), _ptr(x), _ptr(x_row),
+                                                _ptr(h_out)))
         return h_out
 
     def backward(self, dh_out, dparams=None, dx=None, want_dx=True):

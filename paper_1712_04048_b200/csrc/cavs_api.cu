@@ -319,8 +319,8 @@ static void account_backward(cavs_ctx* ctx) {
 }
 
 // --------------------------------------------------------------------------- forward
-CAVS_API cavs_status cavs_forward(cavs_ctx* ctx, const float* params, int32_t n_x, const float* x,
-                         const int32_t* x_row, float* h_out) {
+static cavs_status forward_impl(cavs_ctx* ctx, const float* params, int32_t n_x, const float* x,
+                                const int32_t* x_row, float* h_out, bool infer) {
   if (!ctx) return CAVS_E_INVALID;
   if (ctx->state < S_SCHEDULED) return fail(ctx, CAVS_E_STATE, "cavs_schedule first");
   if (!params || !x_row || !h_out || (n_x > 0 && !x)) return fail(ctx, CAVS_E_INVALID, "null pointer");
@@ -328,6 +328,7 @@ CAVS_API cavs_status cavs_forward(cavs_ctx* ctx, const float* params, int32_t n_
   CK(cudaSetDevice(ctx->device));
   Dev& D = ctx->D;
   D.params = params; D.x = x; D.x_row = x_row; D.h_out = h_out; D.n_x = n_x;
+  D.infer = infer ? 1 : 0;
   Prof& P = ctx->prof;
   P.mark(CAVS_PH_PREP, ctx->stream);
   launch_prep(D, ctx->stream);
@@ -343,8 +344,18 @@ CAVS_API cavs_status cavs_forward(cavs_ctx* ctx, const float* params, int32_t n_
   P.mark(-1, ctx->stream);
   account_forward(ctx);
   CK(cudaGetLastError());
-  ctx->state = S_FORWARDED;
+  ctx->state = infer ? S_SCHEDULED : S_FORWARDED;   // no activations for dF after an inference pass
   return CAVS_OK;
+}
+
+CAVS_API cavs_status cavs_forward(cavs_ctx* ctx, const float* params, int32_t n_x, const float* x,
+                                  const int32_t* x_row, float* h_out) {
+  return forward_impl(ctx, params, n_x, x, x_row, h_out, false);
+}
+
+CAVS_API cavs_status cavs_forward_inference(cavs_ctx* ctx, const float* params, int32_t n_x, const float* x,
+                                            const int32_t* x_row, float* h_out) {
+  return forward_impl(ctx, params, n_x, x, x_row, h_out, true);
 }
 
 // --------------------------------------------------------------------------- backward

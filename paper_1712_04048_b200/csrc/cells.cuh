@@ -130,12 +130,14 @@ __device__ __forceinline__ void lstm_finish(const Dev& D, int j, const VMeta& m,
       f.v[e] = act_sig<OpT>(zf[k].v[e]);
       if (k < m.deg) c.v[e] = fmaf(f.v[e], ck[k].v[e], c.v[e]);   // missing children: c_k = 0 (Z1)
     }
-    if (k < m.deg) stv<VW>(g + (3 + k) * h, f);   // dF reads f_k only for present children
+    if (k < m.deg && !D.infer) stv<VW>(g + (3 + k) * h, f);   // dF reads f_k only for present children
   }
 #pragma unroll
   for (int e = 0; e < VW; ++e) hv.v[e] = o.v[e] * act_tanh<OpT>(c.v[e]);
-  stv<VW>(g, i); stv<VW>(g + h, o); stv<VW>(g + 2 * h, u);
-  stv<VW>(D.cst + (size_t)m.p * h + j, c);
+  if (!D.infer) {                                                  // activations kept for dF
+    stv<VW>(g, i); stv<VW>(g + h, o); stv<VW>(g + 2 * h, u);
+    stv<VW>(D.cst + (size_t)m.p * h + j, c);
+  }
   stv<VW>(D.h_out + (size_t)m.vid * h + j, hv);                   // push(h)
   if (m.par >= 0) {                                                // scatter([c,h]) into the parent's gather slot
     const size_t at = (size_t)m.par * N * h + (size_t)m.slot * h + j;
@@ -297,7 +299,7 @@ __device__ __forceinline__ void fc_finish(const Dev& D, int j, const VMeta& m, c
   FV<VW> hv;
 #pragma unroll
   for (int e = 0; e < VW; ++e) hv.v[e] = act_tanh<OpT>(z.v[e]);
-  stv<VW>(D.gates + (size_t)m.p * h + j, hv);
+  if (!D.infer) stv<VW>(D.gates + (size_t)m.p * h + j, hv);       // h kept for dF (1 - h^2)
   stv<VW>(D.h_out + (size_t)m.vid * h + j, hv);
   if (m.par >= 0) stv_op<OpT, VW>(op<OpT>(D.Hk) + (size_t)m.par * 2 * h + (size_t)m.slot * h + j, hv);
 }

@@ -21,6 +21,7 @@ enum : int { ST_INVALID = 1, ST_ARITY = 2, ST_CYCLE = 4, ST_FANOUT = 8 };
 struct Dev {
   int cell, N, h, d, prec;
   int K, V, E, n_x, T, lp1;          // lp1 = level_ptr[1] (first internal position), host copy
+  int infer;                        // 1: inference-only forward (no activations saved for dF)
   // loaded graphs (global CSR, instance-local child ids)
   const int* graph_ptr; const int* child_ptr; const int* child_idx;
   // schedule (vid-indexed)

@@ -433,3 +433,27 @@ def test_rows_level_kernels(case, monkeypatch):
     o = run_gpu(b, "bf16")
     assert "row-tiled" not in o["ctx"].path_info()
     compare(b, g, o, BF16_EMU_TOL, case + " row-tiled vs per-task")
+
+
+# ------------------------------------------------------------------ inference-only forward
+@pytest.mark.parametrize("case", ["lstm_n2_h512_sst", "fc_h256_cbt"])
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_forward_inference(case, precision, monkeypatch):
+    """cavs_forward_inference: the same h_out as the training forward, bit for bit (the same
+    kernels minus the activation stores), and a backward right after it is a usage error."""
+    from paper_1712_04048_b200 import CavsError
+    b = LAZY_CASES[case]() if case in LAZY_CASES else PERSIST_CASES[case]()
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    ctx = make_ctx(b, precision)
+    ctx.load_graphs(t(b.graph_ptr), t(b.child_ptr), t(b.child_idx))
+    ctx.schedule()
+    h_inf = ctx.forward_inference(t(b.params), t(b.x), t(b.x_row)).cpu().numpy()
+    with pytest.raises(CavsError):
+        ctx.backward(t(b.gamma))
+    h_trn = ctx.forward(t(b.params), t(b.x), t(b.x_row)).cpu().numpy()
+    assert np.array_equal(h_inf, h_trn)
+    ref = run_oracle(b)
+    assert rel(h_inf, ref["h_out"]) <= (FP32_TOL if precision == "fp32" else BF16_TOL)
+    dp, _ = ctx.backward(t(b.gamma))                  # a training forward re-enables backward
+    torch.cuda.synchronize()
