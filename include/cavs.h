@@ -109,8 +109,11 @@ cavs_status cavs_set_workspace(cavs_ctx* ctx, void* dev, size_t bytes);
  *   graph_ptr [K+1]: global vertex offsets, graph_ptr[0] = 0, graph_ptr[K] = V
  *   child_ptr [V+1]: CSR row pointers over global vertices, child_ptr[V] = E
  *   child_idx [E]  : children as INSTANCE-LOCAL ids (0 .. n_k-1); row order = gather index k
- * `on_device` != 0: the three arrays are device pointers, else host pointers.  They are
- * copied (stream-ordered) and only borrowed until that copy completes.
+ * `on_device` != 0: the three arrays are device pointers, read (and copied into the
+ * workspace) by the first kernel of the next cavs_schedule — keep them alive and unmodified
+ * until that kernel ran (stream order), i.e. until any later call on the stream completes.
+ * `on_device` == 0: host pointers, copied host->device here (stream-ordered; borrowed until
+ * that copy completes).
  * Host-side checks: K, V, E within capacity (CAVS_E_CAPACITY), K >= 1 (CAVS_E_INVALID).
  * Content checks run on the device and are reported by cavs_schedule.
  * Resets the state to LOADED. */

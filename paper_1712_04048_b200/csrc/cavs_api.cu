@@ -188,11 +188,15 @@ CAVS_API cavs_status cavs_load_graphs(cavs_ctx* ctx, int32_t K, int32_t V, int32
   if (K > ctx->desc.max_graphs || V > ctx->desc.max_vertices || E > ctx->desc.max_vertices)
     return fail(ctx, CAVS_E_CAPACITY, "batch exceeds context capacity");
   CK(cudaSetDevice(ctx->device));
-  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   Dev& D = ctx->D;
-  CK(cudaMemcpyAsync((void*)D.graph_ptr, graph_ptr, sizeof(int) * (K + 1), kind, ctx->stream));
-  CK(cudaMemcpyAsync((void*)D.child_ptr, child_ptr, sizeof(int) * (V + 1), kind, ctx->stream));
-  if (E > 0) CK(cudaMemcpyAsync((void*)D.child_idx, child_idx, sizeof(int) * E, kind, ctx->stream));
+  if (on_device) {            // read (and copied into the workspace) by cavs_schedule's first kernel
+    D.src_gp = graph_ptr; D.src_cp = child_ptr; D.src_ci = child_idx;
+  } else {
+    CK(cudaMemcpyAsync((void*)D.graph_ptr, graph_ptr, sizeof(int) * (K + 1), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync((void*)D.child_ptr, child_ptr, sizeof(int) * (V + 1), cudaMemcpyHostToDevice, ctx->stream));
+    if (E > 0) CK(cudaMemcpyAsync((void*)D.child_idx, child_idx, sizeof(int) * E, cudaMemcpyHostToDevice, ctx->stream));
+    D.src_gp = D.graph_ptr; D.src_cp = D.child_ptr; D.src_ci = D.child_idx;
+  }
   D.K = K; D.V = V; D.E = E;
   ctx->state = S_LOADED;
   ctx->hdr_pending = false;

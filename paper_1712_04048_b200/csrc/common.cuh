@@ -24,6 +24,9 @@ struct Dev {
   int infer;                        // 1: inference-only forward (no activations saved for dF)
   // loaded graphs (global CSR, instance-local child ids)
   const int* graph_ptr; const int* child_ptr; const int* child_idx;
+  // where k_graph_sched reads the CSR: the caller's device arrays (copied into the arrays above
+  // by the same kernel) or, after a host upload, the arrays above themselves
+  const int* src_gp; const int* src_cp; const int* src_ci;
   // schedule (vid-indexed)
   int* level; int* pos; int* graph_of; int* parent_v; int* slot_v; int* pending; int* queue;
   // schedule (position-indexed)

@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(256) k_graph_sched(Dev D) {
   const int k = blockIdx.x;
   int* st = D.hdr;
   __shared__ int s_bad, s_head, s_tail;
-  const int lo = D.graph_ptr[k], hi = D.graph_ptr[k + 1];
+  const int lo = D.src_gp[k], hi = D.src_gp[k + 1];
   if (threadIdx.x == 0) { s_bad = 0; s_head = 0; s_tail = 0; }
   __syncthreads();
   if (lo < 0 || hi > D.V || hi <= lo || (k == 0 && lo != 0) || (k == D.K - 1 && hi != D.V)) {
@@ -32,6 +32,20 @@ __global__ void __launch_bounds__(256) k_graph_sched(Dev D) {
     return;
   }
   const int n = hi - lo;
+  // ingest (a1): this graph's slice of the caller's CSR into the workspace copy the later
+  // kernels read (a no-op after a host upload, which already wrote the workspace arrays)
+  const bool copy = D.src_gp != D.graph_ptr;
+  if (copy) {
+    if (threadIdx.x == 0) {
+      const_cast<int*>(D.graph_ptr)[k] = lo;
+      if (k == D.K - 1) const_cast<int*>(D.graph_ptr)[k + 1] = hi;
+    }
+    for (int i = threadIdx.x; i <= n; i += blockDim.x)
+      if (i < n || k == D.K - 1) const_cast<int*>(D.child_ptr)[lo + i] = D.src_cp[lo + i];
+    const int e0 = D.src_cp[lo], e1 = D.src_cp[hi];
+    if (e0 >= 0 && e1 <= D.E)
+      for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) const_cast<int*>(D.child_idx)[e] = D.src_ci[e];
+  }
   const bool in_smem = n <= kSchedCap;
   int* par = in_smem ? sm : D.parent_v + lo;                     // local parent id, -1: root
   int* pend = in_smem ? sm + kSchedCap : D.pending + lo;         // children not yet finished
@@ -46,13 +60,13 @@ __global__ void __launch_bounds__(256) k_graph_sched(Dev D) {
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int v = lo + i;
-    const int a = D.child_ptr[v], b = D.child_ptr[v + 1];
+    const int a = D.src_cp[v], b = D.src_cp[v + 1];
     int bad = 0;
     if (a < 0 || b < a || b > D.E) bad |= ST_INVALID;
     else if (b - a > D.N) bad |= ST_ARITY;
     else {
       for (int e = a; e < b; ++e) {
-        const int c = D.child_idx[e];
+        const int c = D.src_ci[e];
         if (c < 0 || c >= n) { bad |= ST_INVALID; break; }
         if (atomicCAS(&par[c], -1, i) != -1) bad |= ST_FANOUT;
         else D.slot_v[lo + c] = e - a;
