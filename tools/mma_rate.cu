@@ -74,8 +74,24 @@ __global__ void k_tile_issue(int iters, unsigned long long* out, int wait_each, 
   const uint32_t b = ptx::smem_u32(smem);
   constexpr uint32_t idesc = ptx::idesc_bf16(128, N, 0, 0);
   unsigned long long t0 = 0;
+  if (noise >= 3) {   // realistic operands: random bf16 in B (smem) and in A (TMEM columns 0..255)
+    uint32_t* w = reinterpret_cast<uint32_t*>(smem);
+    for (int i = threadIdx.x; i < 16 * N * 32; i += blockDim.x) {
+      uint32_t x = (uint32_t)i * 2654435761u + 12345u; x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+      w[i] = (x & 0x3fff3fffu) | 0x3c003c00u;   // bf16 pairs in [1, 2)-ish with random mantissas
+    }
+    __syncthreads();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (warp == 0 && ptx::elect_one()) {
+      for (int c = 0; c < 32; ++c) ptx::tmem_cp_128x256b(tmem + c * 8, desc(b + (c % 16) * 32 * 4));
+      ptx::mma_commit(&bar);
+    }
+    if (warp == 0) { __syncwarp(); ptx::mbar_wait(&bar, 0); ptx::tc_fence_after(); }
+    __syncthreads();
+  }
   if (warp == 0) {
-    uint32_t ph = 0;
+    uint32_t ph = noise >= 3 ? 1 : 0;
     if (ptx::elect_one()) {
       t0 = clock64();
       for (int it = 0; it < iters; ++it) {
@@ -144,7 +160,7 @@ void run(int grid) {
 
 int main() {
   for (int w : {0, 1}) { run_tile<16>(w); run_tile<32>(w); run_tile<64>(w); }
-  for (int nz : {1, 2}) { run_tile<16>(1, nz); run_tile<32>(1, nz); }
+  for (int nz : {1, 2, 3}) { run_tile<16>(1, nz); run_tile<32>(1, nz); }
   return 0;
   for (int grid : {1, 148}) {
     run<16, false>(grid); run<32, false>(grid); run<64, false>(grid); run<128, false>(grid); run<256, false>(grid);

@@ -66,8 +66,9 @@ for kind in sorted(set(int(k) for k in rec[:, 0] if 4000 <= k < 5000)):
         lat = np.array([(int(r[3]) - iss[int(r[1])]) / 1e3 for r in m if int(r[1]) in iss])
         mm = (m[:, 4] - m[:, 3]) / 1e3
         lb = (m[:, 5] - m[:, 3]) / 1e3
+        ghz = np.where(m[:, 4] > m[:, 3], m[:, 7] / np.maximum(1, m[:, 4] - m[:, 3]), 0)
         print(f"  i={i:3d} nt={int(m[0, 6]):3d} | {lat.max():6.2f} {lat.mean():6.2f} | {mm.max():6.2f} {mm.mean():6.2f} | "
-              f"{lb.max():6.2f} {lb.mean():6.2f} | {len(m)}")
+              f"{lb.max():6.2f} {lb.mean():6.2f} | {len(m)} | SM GHz during issue {ghz.mean():.2f}")
 
 # epilogue detail (6000+E): [cta, i, staged, et0 loop end, max thread loop end, after barrier]
 for kind in sorted(set(int(k) for k in rec[:, 0] if 6000 <= k < 7000)):
