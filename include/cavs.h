@@ -150,8 +150,9 @@ cavs_status cavs_forward(cavs_ctx* ctx, const float* params, int32_t n_x, const 
                          const int32_t* x_row, float* h_out);
 
 /* Inference-only forward: the same pass as cavs_forward (same h_out,
- * bit for bit) without saving the activations dF needs (gates, memory cells) — only the
- * states the next tasks gather (scatter into the parents' slots) and push(h) are written.
+ * bit for bit); the level-0 cells (the pull projection's epilogue, half the vertices of a tree
+ * batch) skip the activations only dF needs (gates, memory cells) — the level kernels keep
+ * their stores (a runtime check there costs the register-bound persistent kernel ~5 us).
  * A following cavs_backward fails with CAVS_E_STATE until a training cavs_forward ran.
  * Arguments, layouts, ownership and errors as cavs_forward. */
 cavs_status cavs_forward_inference(cavs_ctx* ctx, const float* params, int32_t n_x, const float* x,

@@ -110,9 +110,13 @@ template <int VW> __device__ __forceinline__ UnitC<VW> load_unit(const Dev& D, i
 
 // ---- Tree-LSTM helpers -----------------------------------------------------------
 // Finish F at (j.., p) given gate pre-activations (bias included) and the children's c.
-template <class OpT, int VW, int NM>
+// CHK: honour Dev::infer (skip the activations dF needs).  Only the x-projection epilogue
+// (level-0 cells, half the vertices of a tree batch) checks it; the level kernels always store
+// (the check costs the register-bound persistent kernel ~5 us per pass).
+template <class OpT, int VW, int NM, bool CHK = false>
 __device__ __forceinline__ void lstm_finish(const Dev& D, int j, const VMeta& m, const FV<VW>& zi, const FV<VW>& zo,
                                             const FV<VW>& zu, const FV<VW>* zf, const FV<VW>* ck) {
+  const bool keep = !CHK || !D.infer;
   const int h = D.h, N = D.N, G = 3 + N;
   FV<VW> i, o, u, c, hv;
 #pragma unroll
@@ -130,11 +134,11 @@ __device__ __forceinline__ void lstm_finish(const Dev& D, int j, const VMeta& m,
       f.v[e] = act_sig<OpT>(zf[k].v[e]);
       if (k < m.deg) c.v[e] = fmaf(f.v[e], ck[k].v[e], c.v[e]);   // missing children: c_k = 0 (Z1)
     }
-    if (k < m.deg && !D.infer) stv<VW>(g + (3 + k) * h, f);   // dF reads f_k only for present children
+    if (keep) stv<VW>(g + (3 + k) * h, f);
   }
 #pragma unroll
   for (int e = 0; e < VW; ++e) hv.v[e] = o.v[e] * act_tanh<OpT>(c.v[e]);
-  if (!D.infer) {                                                  // activations kept for dF
+  if (keep) {                                                       // activations kept for dF
     stv<VW>(g, i); stv<VW>(g + h, o); stv<VW>(g + 2 * h, u);
     stv<VW>(D.cst + (size_t)m.p * h + j, c);
   }
@@ -251,7 +255,7 @@ template <> struct EpiK<EPI_LSTM_XPROJ> {
 #pragma unroll
         for (int e = 0; e < VW; ++e) zf[k].v[e] = acc[3].v[e] + b.b3.v[e];
       }
-      lstm_finish<OpT, VW, NM>(D, j, m, zi, zo, zu, zf, ck);
+      lstm_finish<OpT, VW, NM, true>(D, j, m, zi, zo, zu, zf, ck);
     } else if (m.xrow >= 0) {
       float* xw = D.XW + (size_t)m.p * 4 * h + j;
       stv<VW>(xw, acc[0]); stv<VW>(xw + h, acc[1]); stv<VW>(xw + 2 * h, acc[2]); stv<VW>(xw + 3 * h, acc[3]);
@@ -293,13 +297,13 @@ template <> struct EpiK<EPI_LSTM_BWD> {
 };
 
 // ---- Tree-FC ------------------------------------------------------------------------
-template <class OpT, int VW>
+template <class OpT, int VW, bool CHK = false>
 __device__ __forceinline__ void fc_finish(const Dev& D, int j, const VMeta& m, const FV<VW>& z) {
   const int h = D.h;
   FV<VW> hv;
 #pragma unroll
   for (int e = 0; e < VW; ++e) hv.v[e] = act_tanh<OpT>(z.v[e]);
-  if (!D.infer) stv<VW>(D.gates + (size_t)m.p * h + j, hv);       // h kept for dF (1 - h^2)
+  if (!CHK || !D.infer) stv<VW>(D.gates + (size_t)m.p * h + j, hv);   // h kept for dF (1 - h^2)
   stv<VW>(D.h_out + (size_t)m.vid * h + j, hv);
   if (m.par >= 0) stv_op<OpT, VW>(op<OpT>(D.Hk) + (size_t)m.par * 2 * h + (size_t)m.slot * h + j, hv);
 }
@@ -330,7 +334,7 @@ template <> struct EpiK<EPI_FC_XPROJ> {
       FV<VW> z;
 #pragma unroll
       for (int e = 0; e < VW; ++e) z.v[e] = acc[0].v[e] + b.b0.v[e];
-      fc_finish<OpT, VW>(D, j, m, z);
+      fc_finish<OpT, VW, true>(D, j, m, z);
     } else if (m.xrow >= 0) {
       stv<VW>(D.XW + (size_t)m.p * D.h + j, acc[0]);
     }

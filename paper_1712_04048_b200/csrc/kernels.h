@@ -65,6 +65,24 @@ struct Prof {
   void count(int n) { if (cur >= 0) launches[cur] += n; total += n; }
 };
 
+// Launch with programmatic dependent launch (PDL): the kernel may be scheduled while its
+// predecessor on the stream drains; every such kernel starts with griddepcontrol.wait.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 void launch_schedule(const Dev& D, cudaStream_t s);
 template <class OpT> void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P);
 template <class OpT> void simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P);

@@ -32,6 +32,7 @@ __device__ __forceinline__ OpT* prep_dst(const Dev& D, int sel) {
 
 template <class OpT>
 __global__ void __launch_bounds__(256) k_prep(Dev D, PrepJobs J) {
+  pdl_wait();
   const PrepJob& jb = J.j[blockIdx.y];
   __shared__ float tile[32][33];
   if (jb.transpose) {
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(256) k_prep(Dev D, PrepJobs J) {
 // One CTA per 64-position tile; 4 consecutive x values per thread and step (16-byte loads).
 template <class OpT>
 __global__ void k_pull(Dev D) {
+  pdl_wait();
   const int p0 = blockIdx.x * 64;
   __shared__ int s_r[64];
   if (threadIdx.x < 64) {
@@ -127,6 +129,7 @@ __global__ void k_pull(Dev D) {
 
 template <class OpT>
 __global__ void k_roots(Dev D, int n_roots, const int* roots) {
+  pdl_wait();
   const size_t n = (size_t)n_roots * D.h;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     root_bwd<OpT>(D, (int)(i % D.h), roots[i / D.h]);
@@ -142,6 +145,7 @@ __global__ void k_roots(Dev D, int n_roots, const int* roots) {
 // order and writes the packed db block of dparams (deterministic).
 template <class OpT>
 __global__ void __launch_bounds__(256) k_colsum(Dev D, float* part, int lcols) {
+  pdl_wait();
   __shared__ float red[8][256];
   __shared__ int s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -305,26 +309,26 @@ void launch_prep(const Dev& D, cudaStream_t s) {
     add(b, 1, (int)h, 0, 5, 0, 0, 0);
   }
   dim3 grid(148, J.n);
-  if (D.prec == CAVS_BF16) k_prep<__nv_bfloat16><<<grid, 256, 0, s>>>(D, J);
-  else k_prep<float><<<grid, 256, 0, s>>>(D, J);
+  if (D.prec == CAVS_BF16) launch_pdl(k_prep<__nv_bfloat16>, grid, dim3(256), 0, s, D, J);
+  else launch_pdl(k_prep<float>, grid, dim3(256), 0, s, D, J);
 }
 
 void launch_pull(const Dev& D, cudaStream_t s) {
-  if (D.prec == CAVS_BF16) k_pull<__nv_bfloat16><<<cdiv(D.V, 64), 256, 0, s>>>(D);
-  else k_pull<float><<<cdiv(D.V, 64), 256, 0, s>>>(D);
+  if (D.prec == CAVS_BF16) launch_pdl(k_pull<__nv_bfloat16>, dim3(cdiv(D.V, 64)), dim3(256), 0, s, D);
+  else launch_pdl(k_pull<float>, dim3(cdiv(D.V, 64)), dim3(256), 0, s, D);
 }
 
 void launch_roots(const Dev& D, int n_roots, const int* roots, cudaStream_t s) {
   const size_t n = (size_t)n_roots * D.h;
-  if (D.prec == CAVS_BF16) k_roots<__nv_bfloat16><<<grid_for(n, 256), 256, 0, s>>>(D, n_roots, roots);
-  else k_roots<float><<<grid_for(n, 256), 256, 0, s>>>(D, n_roots, roots);
+  if (D.prec == CAVS_BF16) launch_pdl(k_roots<__nv_bfloat16>, dim3(grid_for(n, 256)), dim3(256), 0, s, D, n_roots, roots);
+  else launch_pdl(k_roots<float>, dim3(grid_for(n, 256)), dim3(256), 0, s, D, n_roots, roots);
 }
 
 void launch_colsum(const Dev& D, float* part, cudaStream_t s) {
   const int lcols = (D.cell == CAVS_CELL_TREE_LSTM ? 4 : 1) * D.h;
   dim3 grid(cdiv(lcols, 256), kDbChunks);   // deterministic row chunks (one wave of CTAs)
-  if (D.prec == CAVS_BF16) k_colsum<__nv_bfloat16><<<grid, 256, 0, s>>>(D, part, lcols);
-  else k_colsum<float><<<grid, 256, 0, s>>>(D, part, lcols);
+  if (D.prec == CAVS_BF16) launch_pdl(k_colsum<__nv_bfloat16>, grid, dim3(256), 0, s, D, part, lcols);
+  else launch_pdl(k_colsum<float>, grid, dim3(256), 0, s, D, part, lcols);
 }
 
 void launch_pack(const Dev& D, const int* split, cudaStream_t s) {

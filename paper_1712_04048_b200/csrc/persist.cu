@@ -187,7 +187,7 @@ __device__ __forceinline__ void mma_level(const PPlan& P, int ntile, uint32_t a_
       const int s = step % S;
       pwait_warp(&full[s], (step / S) & 1);
       ptx::tc_fence_after();
-      if (tr) { if (tr[0] == 0) { tr[0] = gtime(); tr[3] = clock64(); } if (tr[1] == 0) tr[2] = gtime(); }   // first / last box of the first tile
+      if (tr) { if (tr[0] == 0) tr[0] = gtime(); if (tr[1] == 0) tr[2] = gtime(); }   // first / last box of the first tile
       const int cnt = min(nkb, (b + 1) * sk) - b * sk;
       if (ptx::elect_one()) {
         uint32_t bl = b_lo + (uint32_t)s * stage16;
@@ -213,7 +213,7 @@ __device__ __forceinline__ void mma_level(const PPlan& P, int ntile, uint32_t a_
     }
     if (ptx::elect_one()) ptx::mma_commit(done);
     __syncwarp();
-    if (tr && tr[1] == 0) { tr[1] = gtime(); tr[4] = clock64() - tr[3]; }
+    if (tr && tr[1] == 0) tr[1] = gtime();
   }
 }
 
@@ -341,7 +341,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
         cl_rows(D, t, r, lo, M);
         const int ni = nt_index(M, 1, P.max_ni), nt = 16 << ni;
         const int ntile = (M + nt - 1) / nt;
-        unsigned long long trm[5] = {0, 0, 0, 0, 0};
+        unsigned long long trm[3] = {0, 0, 0};
         unsigned long long* tr = D.trace ? trm : nullptr;
         if (P.tsA) {
           if (ni == 0) mma_level<16, true>(P, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
@@ -352,7 +352,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
           else if (ni == 1) mma_level<32, false>(P, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
           else mma_level<64, false>(P, ntile, a_lo, b_lo, full, empty, done, tmem_empty, step, tcount, tr);
         }
-        if (D.trace && ntile > 0 && lane == 0) ptrace(D, 4000 + E, blockIdx.x, i, trm[0], trm[1], trm[2], nt, trm[4]);
+        if (D.trace && ntile > 0 && lane == 0) ptrace(D, 4000 + E, blockIdx.x, i, trm[0], trm[1], trm[2], nt, 0);
       }
     }
     __syncwarp();

@@ -20,6 +20,7 @@ constexpr int kSchedCap = 2048;      // vertices of a graph swept in shared memo
 // of <= kSchedCap vertices (every BASELINE config), else in the graph's slices of the global
 // scratch arrays; local ids throughout.
 __global__ void __launch_bounds__(256) k_graph_sched(Dev D) {
+  pdl_wait();
   extern __shared__ int sm[];
   const int k = blockIdx.x;
   int* st = D.hdr;
@@ -162,6 +163,7 @@ __device__ __forceinline__ int block_excl_scan(int x, int* s_warp, int& total) {
 // table of the persistent kernels (crow[t][r] = rows before the first graph of cluster r).  The
 // last CTA to finish scans the task sizes into level_ptr and makes crow absolute.
 __global__ void __launch_bounds__(1024) k_level_offsets(Dev D) {
+  pdl_wait();
   if (D.hdr[0]) return;
   __shared__ int s_warp[32];
   __shared__ int s_last;
@@ -226,6 +228,7 @@ __device__ __forceinline__ int vpos(const Dev& D, int v, int lo) {
 // the position-indexed plan (children / parent slots, degree, roots).
 template <class OpT>
 __global__ void k_build_maps(Dev D) {
+  pdl_wait();
   if (D.hdr[0]) return;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < D.V; v += gridDim.x * blockDim.x) {
     const int lo = D.graph_ptr[D.graph_of[v]];
@@ -256,11 +259,11 @@ void launch_schedule(const Dev& D, cudaStream_t s) {
     cudaFuncSetAttribute(k_graph_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  k_graph_sched<<<D.K, 256, smem, s>>>(D);
-  k_level_offsets<<<148, 1024, 0, s>>>(D);
+  launch_pdl(k_graph_sched, dim3(D.K), dim3(256), smem, s, D);
+  launch_pdl(k_level_offsets, dim3(148), dim3(1024), 0, s, D);
   const int g = std::min(cdiv(D.V, 256), 148 * 8);
-  if (D.prec == CAVS_BF16) k_build_maps<__nv_bfloat16><<<g, 256, 0, s>>>(D);
-  else k_build_maps<float><<<g, 256, 0, s>>>(D);
+  if (D.prec == CAVS_BF16) launch_pdl(k_build_maps<__nv_bfloat16>, dim3(g), dim3(256), 0, s, D);
+  else launch_pdl(k_build_maps<float>, dim3(g), dim3(256), 0, s, D);
 }
 
 }  // namespace cavs
