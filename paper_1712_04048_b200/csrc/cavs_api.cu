@@ -101,7 +101,7 @@ static size_t carve(cavs_ctx* c, char* base) {
     D.Wd = nullptr; D.We = take(dd * h * es);
   }
   D.lazy = F(lazy_floats(D));
-  c->lazy_db = F((size_t)kDbChunks * G * h);
+  c->lazy_db = F((size_t)kDbChunks * d.N * 4 * h);   // db partials [(slot, chunk)][logical column]
   const size_t P = cavs_param_count(d.cell, d.N, d.h, d.d);
   c->s_params = F(P); c->s_dp = F(P);
   c->s_x = F(X * dd); c->s_dx = F(X * dd);

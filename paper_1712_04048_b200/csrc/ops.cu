@@ -153,8 +153,11 @@ __global__ void __launch_bounds__(256) k_colsum(Dev D, float* part, int lcols) {
   const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
   const int cols = lstm ? (3 + D.N) * h : h;                 // physical dZ row width
   const int L0 = blockIdx.x * 256 + lane * 8;
-  const int chunk = cdiv(D.V, gridDim.y);
-  const int r0 = blockIdx.y * chunk, r1 = min(D.V, r0 + chunk);
+  // blockIdx.y = (slot k, row chunk): the N child slots of the f block are summed by different
+  // CTAs (balanced work); the other blocks' CTAs with k > 0 contribute zero partials
+  const int kk = blockIdx.y / kDbChunks, cy = blockIdx.y % kDbChunks;
+  const int chunk = cdiv(D.V, kDbChunks);
+  const int r0 = cy * chunk, r1 = min(D.V, r0 + chunk);
   const OpT* dz = op<OpT>(D.dZ);
   float acc[8];
 #pragma unroll
@@ -163,7 +166,7 @@ __global__ void __launch_bounds__(256) k_colsum(Dev D, float* part, int lcols) {
     const int gl = L0 / h, j = L0 - gl * h;
     const int nk = (lstm && gl == 3) ? D.N : 1;
     const int pc = (lstm && gl == 3) ? 3 * h + j : gl * h + j;
-    for (int k = 0; k < nk; ++k) {
+    for (int k = kk; k < min(nk, kk + 1); ++k) {
       const OpT* col = dz + pc + k * h;
       if constexpr (sizeof(OpT) == 2) {
         int r = r0 + warp;
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(256) k_colsum(Dev D, float* part, int lcols) {
       const int L = L0 + e, gl = L / h, j = L - gl * h;
       const int nk = (lstm && gl == 3) ? D.N : 1;
       const int pc = (lstm && gl == 3) ? 3 * h + j : gl * h + j;
-      for (int k = 0; k < nk; ++k)
+      for (int k = kk; k < min(nk, kk + 1); ++k)
         for (int r = r0 + warp; r < r1; r += 8) acc[e] += from_op(dz[(size_t)r * cols + pc + k * h]);
     }
   }
@@ -326,7 +329,7 @@ void launch_roots(const Dev& D, int n_roots, const int* roots, cudaStream_t s) {
 
 void launch_colsum(const Dev& D, float* part, cudaStream_t s) {
   const int lcols = (D.cell == CAVS_CELL_TREE_LSTM ? 4 : 1) * D.h;
-  dim3 grid(cdiv(lcols, 256), kDbChunks);   // deterministic row chunks (one wave of CTAs)
+  dim3 grid(cdiv(lcols, 256), kDbChunks * (D.cell == CAVS_CELL_TREE_LSTM ? D.N : 1));   // (slot, row chunk)
   if (D.prec == CAVS_BF16) launch_pdl(k_colsum<__nv_bfloat16>, grid, dim3(256), 0, s, D, part, lcols);
   else launch_pdl(k_colsum<float>, grid, dim3(256), 0, s, D, part, lcols);
 }
