@@ -55,7 +55,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="cavs", choices=["cavs", "reference"])
     ap.add_argument("--config", default="cfg4")
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--precision", default=None, choices=["bf16", "fp32"],
+                    help="default bf16; fp32 for cfg1 (BASELINE: 'hidden 16, fp32'; bf16 mode needs h % 64 == 0)")
     ap.add_argument("--h", type=int, default=None)
     ap.add_argument("--pool", type=int, default=16)
     ap.add_argument("--cpu-sample", type=int, default=48, help="graphs in the CPU-oracle baseline sample")
@@ -64,7 +65,10 @@ def parse():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--inference", action="store_true",
                     help="forward-only (cavs_forward_inference): inference samples/s, no backward")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.precision is None:
+        a.precision = "fp32" if a.config == "cfg1" else "bf16"
+    return a
 
 
 # ------------------------------------------------------------------------------ clocks
