@@ -136,13 +136,13 @@ def _noop(_):
 
 
 def _oracle_jobs(b, graphs, n_chunks):
-    from paper_1712_04048_b200 import dp
+    from workloads import gen              # never the product package: the oracle leg must not load libcavs.so
     chunks = [graphs[i::n_chunks] for i in range(n_chunks)]
     jobs = []
     for ch in chunks:
         if not ch:
             continue
-        gp, cp, ci, rows, recs, nxr = dp.subset_csr(b.graph_ptr, b.child_ptr, b.child_idx, b.x_row, ch)
+        gp, cp, ci, rows, recs, nxr = gen.subset_csr(b.graph_ptr, b.child_ptr, b.child_idx, b.x_row, ch)
         jobs.append((b.cell, b.N, b.h, b.d, b.params, gp, cp, ci, nxr, b.x[recs], b.gamma[rows]))
     return jobs
 

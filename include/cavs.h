@@ -142,7 +142,10 @@ cavs_status cavs_get_schedule(cavs_ctx* ctx, int32_t* level, int32_t* level_ptr,
  * t = 0..T-1 (gather -> cell -> scatter/push fused in one kernel per level).
  *   params  [P]      device fp32, packed layout above
  *   x       [n_x, d] device fp32 pull records
- *   x_row   [V]      device int32: record of each global vertex, -1 = none (pull() -> 0)
+ *   x_row   [V]      device int32: record of each global vertex, -1 = none (pull() -> 0).  Several
+ *                    vertices may pull the same record (an embedding row): their dx rows are ADDED.
+ *                    An entry outside [-1, n_x) is an input error found on the device: the vertex
+ *                    pulls nothing and the next cavs_sync returns CAVS_E_INVALID.
  *   h_out   [V, h]   device fp32 output: push(h) of every vertex, global id order (Fig. 5)
  * Activations stay in the workspace for cavs_backward.
  * Errors: CAVS_E_STATE (not scheduled), CAVS_E_CAPACITY (n_x > max_x), CAVS_E_INVALID (NULL). */
@@ -163,7 +166,9 @@ cavs_status cavs_forward_inference(cavs_ctx* ctx, const float* params, int32_t n
  * gradients are lazily batched over all vertices once after the level loop (§3.5).
  *   dh_out  [V, h]   device fp32: dL/d(push h) of every vertex (the external loss's cotangent)
  *   dparams [P]      device fp32, OVERWRITTEN with dL/dparams summed over all K graphs
- *   dx      [n_x, d] device fp32, OVERWRITTEN with dL/dx (may be NULL)
+ *   dx      [n_x, d] device fp32, OVERWRITTEN with dL/dx (may be NULL): zeroed, then every vertex's
+ *                    pull adjoint W^T dz is added into its record's row; records no
+ *                    vertex pulls stay 0.  Deterministic when each record is pulled at most once.
  * Errors: CAVS_E_STATE (no forward since the last schedule), CAVS_E_INVALID. */
 cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dparams, float* dx);
 
@@ -176,6 +181,11 @@ cavs_status cavs_train_step_host(cavs_ctx* ctx, int32_t K, int32_t V, int32_t E,
                                  const int32_t* child_idx, const float* params, int32_t n_x,
                                  const float* x, const int32_t* x_row, const float* dh_out,
                                  float* dparams, float* dx, float* h_out);
+
+/* Wait for all work enqueued on the context's stream and report the deferred device-side input
+ * errors of the calls since the last cavs_schedule: CAVS_E_INVALID if a forward met an x_row
+ * entry outside [-1, n_x).  CAVS_E_CUDA on a CUDA error.  cavs_train_step_host does this itself. */
+cavs_status cavs_sync(cavs_ctx* ctx);
 
 /* Number of kernels the library launched since the context was created (diagnostic). */
 int64_t cavs_kernel_launches(const cavs_ctx* ctx);

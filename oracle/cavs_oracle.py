@@ -25,9 +25,17 @@ What it computes (PAPER.md = /root/reference/PAPER.md, "P:Lnnn" = line):
     (P:L358, P:L373-380), gradients ADDED, never overwritten (P:L447);
     gather's adjoint is scatter and pull's adjoint is push.
   * fp64 throughout (the paper never states a precision, Z11).  The optional
-    `emulate_bf16=True` mode rounds exactly the GEMM operands the GPU's
-    bf16 mode rounds (params W,U; x; the gathered h_k and child-sum h~; the
-    stored dZ), RN-even via fp32 (reading Z11, pin P9).
+    `emulate_bf16=True` mode is a DIAGNOSTIC (it separates bf16 quantisation
+    from bugs; the parity gate is always the plain fp64 mode): it rounds the
+    GEMM operands of SURVEY reading Z11 (params W,U; x; the gathered h_k and
+    the child-sum h~; the stored dZ) RN-even via fp32 (pin P9).  Fig. 5 fixes
+    U h~ with h~ = sum_k h_k but no rounding point, so two bf16 readings are
+    offered:
+      bf16_hsum="rounded" (default, Z11 as written): h~ = bf16(sum_k bf16(h_k));
+      bf16_hsum="exact"   (reading R-lin): U h~ taken as sum_k U bf16(h_k) in
+                          exact arithmetic, i.e. h~ = sum_k bf16(h_k) unrounded.
+    Both equal the fp64 definition up to bf16 rounding; they coincide bit for
+    bit when no vertex has two or more children.
 
 Parity status: every function here is pinned by `tests/test_oracle_pins.py`
 (closed forms, brute force, torch.nn.LSTM, finite differences, hand-worked
@@ -233,9 +241,13 @@ class Tape:
     children: list
 
 
-def forward(cell, N, h, d, theta, graph_ptr, child_ptr, child_idx, x_row, x, emulate_bf16=False):
+def forward(cell, N, h, d, theta, graph_ptr, child_ptr, child_idx, x_row, x, emulate_bf16=False,
+            bf16_hsum="rounded"):
     """Returns (h_out[V,h] fp64, tape).  Evaluates F at every vertex after all its
-    children (Fig. 5); each vertex exactly once (memo)."""
+    children (Fig. 5); each vertex exactly once (memo).  `bf16_hsum` only
+    matters with emulate_bf16 (see the module header)."""
+    if bf16_hsum not in ("rounded", "exact"):
+        raise ValueError(bf16_hsum)
     ch = validate(graph_ptr, child_ptr, child_idx, N)
     V = len(ch)
     P = unpack(cell, N, h, d, theta)
@@ -262,10 +274,13 @@ def forward(cell, N, h, d, theta, graph_ptr, child_ptr, child_idx, x_row, x, emu
             hk = [st[c]["h"] for c in ch[v]] + [np.zeros(h)] * (N - len(ch[v]))
             ck = [st[c]["c"] for c in ch[v]] + [np.zeros(h)] * (N - len(ch[v]))
             hkq = [q(a) for a in hk]
-            # h~ = sum_k h_k (Fig. 5).  In bf16 mode the GPU never rounds h~ itself: it
-            # accumulates U h~ as sum_k U bf16(h_k) (reading Z11), i.e. U applied to the exact
-            # sum of the bf16 slots.
-            hs = sum(hkq) if emulate_bf16 else sum(hk)
+            # h~ = sum_k h_k (Fig. 5); bf16 emulation: Z11 rounds it as a GEMM operand,
+            # reading R-lin keeps the exact sum of the rounded slots
+            hs = sum(hk)
+            if emulate_bf16:
+                hs = sum(hkq)
+                if bf16_hsum == "rounded":
+                    hs = q(hs)
             i = sigmoid(Pq["W_i"] @ xv + Pq["U_i"] @ hs + P["b_i"])
             f = [sigmoid(Pq["W_f"] @ xv + Pq["U_f"] @ hkq[k] + P["b_f"]) for k in range(N)]
             o = sigmoid(Pq["W_o"] @ xv + Pq["U_o"] @ hs + P["b_o"])
@@ -355,11 +370,11 @@ def loss(h_out, gamma):
     return float(np.sum(np.asarray(h_out) * np.asarray(gamma, dtype=np.float64)))
 
 
-def run(batch, emulate_bf16=False, with_backward=True):
+def run(batch, emulate_bf16=False, with_backward=True, bf16_hsum="rounded"):
     """Convenience: forward (+ backward) on a workloads.Batch-like object."""
     h_out, tape = forward(batch.cell, batch.N, batch.h, batch.d, batch.params, batch.graph_ptr,
                           batch.child_ptr, batch.child_idx, batch.x_row, batch.x,
-                          emulate_bf16=emulate_bf16)
+                          emulate_bf16=emulate_bf16, bf16_hsum=bf16_hsum)
     if not with_backward:
         return h_out, None, None, tape
     dparams, dx = backward(batch.cell, batch.N, batch.h, batch.d, batch.params, tape, batch.x_row,

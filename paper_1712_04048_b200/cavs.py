@@ -55,6 +55,7 @@ def _load():
         "cavs_backward": (S, [P, P, P, P]),
         "cavs_train_step_host": (S, [P, I32, I32, I32, P, P, P, P, I32, P, P, P, P, P, P]),
         "cavs_kernel_launches": (I64, [P]),
+        "cavs_sync": (S, [P]),
         "cavs_last_error": (ctypes.c_char_p, [P]),
         "cavs_path_info": (ctypes.c_char_p, [P]),
         "cavs_profile": (S, [P, ctypes.c_int]),
@@ -74,7 +75,7 @@ def _load():
 _lib = _load()
 EXPORTS = ["cavs_param_count", "cavs_create", "cavs_set_stream", "cavs_workspace_bytes",
            "cavs_set_workspace", "cavs_load_graphs", "cavs_schedule", "cavs_get_schedule",
-           "cavs_forward", "cavs_forward_inference", "cavs_backward", "cavs_train_step_host", "cavs_kernel_launches",
+           "cavs_forward", "cavs_forward_inference", "cavs_backward", "cavs_train_step_host", "cavs_kernel_launches", "cavs_sync",
            "cavs_last_error", "cavs_path_info", "cavs_destroy", "cavs_profile", "cavs_profile_read"]
 PHASES = ["schedule", "prep", "xproj", "fwd_levels", "bwd_roots", "bwd_levels", "lazy", "dx", "reduce"]
 
@@ -87,13 +88,31 @@ def param_count(cell, N, h, d) -> int:
     return int(_lib.cavs_param_count(CELLS.get(cell, cell), N, h, d))
 
 
-def _ptr(a):
+def _ptr(a, kind=None, device=None, host_ok=False):
+    """Pointer of a C-contiguous numpy array or torch tensor.  `kind` in {"i32", "f32"} checks
+    the element type (int64 index arrays would be read as int32 garbage); `device` requires a
+    CUDA tensor on that device (host_ok: numpy / CPU tensors allowed, e.g. the *_host calls)."""
     if a is None:
         return None
     if isinstance(a, np.ndarray):
-        assert a.flags["C_CONTIGUOUS"]
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("arrays must be C-contiguous")
+        if kind and a.dtype != (np.int32 if kind == "i32" else np.float32):
+            raise TypeError(f"expected {kind}, got numpy {a.dtype}")
+        if device is not None and not host_ok:
+            raise TypeError("expected a CUDA tensor, got a numpy array")
         return a.ctypes.data
-    assert a.is_contiguous(), "tensors must be contiguous"
+    import torch
+    if not a.is_contiguous():
+        raise ValueError("tensors must be contiguous")
+    if kind and a.dtype != (torch.int32 if kind == "i32" else torch.float32):
+        raise TypeError(f"expected {kind}, got {a.dtype}")
+    if device is not None:
+        if a.is_cuda:
+            if a.device != device:
+                raise ValueError(f"tensor on {a.device}, context on {device}")
+        elif not host_ok:
+            raise TypeError("expected a CUDA tensor on the context's device, got a CPU tensor")
     return a.data_ptr()
 
 
@@ -165,8 +184,9 @@ class Context:
         V = int(child_ptr.shape[0]) - 1
         E = int(child_idx.shape[0])
         self._keep = (graph_ptr, child_ptr, child_idx)
-        self._check(_lib.cavs_load_graphs(self._ctx, K, V, E, _ptr(graph_ptr), _ptr(child_ptr),
-                                          _ptr(child_idx) if E else None, 1 if on_dev else 0))
+        dev = self.device if on_dev else None
+        self._check(_lib.cavs_load_graphs(self._ctx, K, V, E, _ptr(graph_ptr, "i32", dev), _ptr(child_ptr, "i32", dev),
+                                          _ptr(child_idx, "i32", dev) if E else None, 1 if on_dev else 0))
         self.V, self.K = V, K
 
     def schedule(self, wait: bool = True):
@@ -193,7 +213,9 @@ class Context:
         if h_out is None:
             h_out = torch.empty(self.V, self.h, dtype=torch.float32, device=self.device)
         self._fwd_keep = (params, x, x_row, h_out)
-        self._check(_lib.cavs_forward(self._ctx, _ptr(params), int(x.shape[0]), _ptr(x), _ptr(x_row), _ptr(h_out)))
+        dv = self.device
+        self._check(_lib.cavs_forward(self._ctx, _ptr(params, "f32", dv), int(x.shape[0]), _ptr(x, "f32", dv),
+                                      _ptr(x_row, "i32", dv), _ptr(h_out, "f32", dv)))
         return h_out
 
     def forward_inference(self, params, x, x_row, h_out=None):
@@ -202,8 +224,9 @@ class Context:
         if h_out is None:
             h_out = torch.empty(self.V, self.h, dtype=torch.float32, device=self.device)
         self._fwd_keep = (params, x, x_row, h_out)
-        self._check(_lib.cavs_forward_inference(self._ctx, _ptr(params), int(x.shape[0]), _ptr(x), _ptr(x_row),
-                                                _ptr(h_out)))
+        dv = self.device
+        self._check(_lib.cavs_forward_inference(self._ctx, _ptr(params, "f32", dv), int(x.shape[0]),
+                                                _ptr(x, "f32", dv), _ptr(x_row, "i32", dv), _ptr(h_out, "f32", dv)))
         return h_out
 
     def backward(self, dh_out, dparams=None, dx=None, want_dx=True):
@@ -214,8 +237,14 @@ class Context:
             x = self._fwd_keep[1]
             dx = torch.empty(x.shape[0], self.d, dtype=torch.float32, device=self.device)
         self._bwd_keep = (dh_out, dparams, dx)
-        self._check(_lib.cavs_backward(self._ctx, _ptr(dh_out), _ptr(dparams), _ptr(dx)))
+        dv = self.device
+        self._check(_lib.cavs_backward(self._ctx, _ptr(dh_out, "f32", dv), _ptr(dparams, "f32", dv),
+                                       _ptr(dx, "f32", dv)))
         return dparams, dx
+
+    def sync(self):
+        """Wait for the context's stream; raises on deferred device-side input errors (cavs_sync)."""
+        self._check(_lib.cavs_sync(self._ctx))
 
     def train_step_host(self, graph_ptr, child_ptr, child_idx, params, x, x_row, dh_out,
                         dparams, dx=None, h_out=None):
@@ -223,9 +252,11 @@ class Context:
         K = int(graph_ptr.shape[0]) - 1
         V = int(child_ptr.shape[0]) - 1
         E = int(child_idx.shape[0])
+        H = dict(device=self.device, host_ok=True)
         self._check(_lib.cavs_train_step_host(
-            self._ctx, K, V, E, _ptr(graph_ptr), _ptr(child_ptr), _ptr(child_idx), _ptr(params),
-            int(x.shape[0]), _ptr(x), _ptr(x_row), _ptr(dh_out), _ptr(dparams), _ptr(dx), _ptr(h_out)))
+            self._ctx, K, V, E, _ptr(graph_ptr, "i32", **H), _ptr(child_ptr, "i32", **H), _ptr(child_idx, "i32", **H),
+            _ptr(params, "f32", **H), int(x.shape[0]), _ptr(x, "f32", **H), _ptr(x_row, "i32", **H),
+            _ptr(dh_out, "f32", **H), _ptr(dparams, "f32", **H), _ptr(dx, "f32", **H), _ptr(h_out, "f32", **H)))
         self.V, self.K = V, K
 
     def close(self):

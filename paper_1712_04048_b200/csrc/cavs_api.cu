@@ -371,6 +371,7 @@ CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dp
   Dev& D = ctx->D;
   D.dh_out = dh_out; D.dparams = dparams; D.dx = dx;
   Prof& P = ctx->prof;
+  if (dx && D.n_x > 0) CK(cudaMemsetAsync(dx, 0, sizeof(float) * (size_t)D.n_x * D.d, ctx->stream));   // dx is accumulated
   P.mark(CAVS_PH_BWD_ROOTS, ctx->stream);
   launch_roots(D, ctx->n_roots, D.roots, ctx->stream);
   P.count(1);
@@ -421,7 +422,18 @@ CAVS_API cavs_status cavs_train_step_host(cavs_ctx* ctx, int32_t K, int32_t V, i
   CK(cudaMemcpyAsync(dparams, ctx->s_dp, sizeof(float) * P, cudaMemcpyDeviceToHost, s));
   if (dx && n_x) CK(cudaMemcpyAsync(dx, ctx->s_dx, sizeof(float) * n_x * d.d, cudaMemcpyDeviceToHost, s));
   if (h_out) CK(cudaMemcpyAsync(h_out, ctx->s_hout, sizeof(float) * V * d.h, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  return cavs_sync(ctx);
+}
+
+CAVS_API cavs_status cavs_sync(cavs_ctx* ctx) {
+  if (!ctx) return CAVS_E_INVALID;
+  if (ctx->state < S_READY) return CAVS_OK;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpyAsync(ctx->h_hdr + kHdrWords + kReadback - 1, ctx->D.hdr + 3, sizeof(int), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->h_hdr[kHdrWords + kReadback - 1] & ST_XROW)
+    return fail(ctx, CAVS_E_INVALID, "x_row entry outside [-1, n_x) (the vertex pulled nothing)");
   return CAVS_OK;
 }
 

@@ -366,14 +366,20 @@ template <> struct EpiK<EPI_FC_BWD> {
   }
 };
 
-// pull's adjoint: dx[record] = W^T dz
+// pull's adjoint: dx[record] += W^T dz.  ADDED, not stored: several vertices may pull
+// the same record (an embedding row); dx is zeroed by cavs_backward first.  With one vertex per
+// record every element receives exactly one add onto 0 (deterministic).
+template <int VW> __device__ __forceinline__ void addv(float* p, const FV<VW>& a) {
+  if constexpr (VW == 4) atomicAdd(reinterpret_cast<float4*>(p), make_float4(a.v[0], a.v[1], a.v[2], a.v[3]));
+  else atomicAdd(p, a.v[0]);
+}
 template <> struct EpiK<EPI_DX> {
   template <int VW, int NM = kMaxN> struct In {};
   template <int VW, int NM = kMaxN> static __device__ __forceinline__ void load(const Dev&, int, const VMeta&, In<VW, NM>&) {}
   template <class OpT, int VW, int NM = kMaxN>
   static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const FV<VW>* acc,
                                                const In<VW, NM>&, const UnitC<VW>&) {
-    if (m.xrow >= 0) stv<VW>(D.dx + (size_t)m.xrow * D.d + j, acc[0]);
+    if (m.xrow >= 0) addv<VW>(D.dx + (size_t)m.xrow * D.d + j, acc[0]);
   }
 };
 

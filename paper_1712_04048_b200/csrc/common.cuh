@@ -15,7 +15,7 @@
 
 namespace cavs {
 
-enum : int { ST_INVALID = 1, ST_ARITY = 2, ST_CYCLE = 4, ST_FANOUT = 8 };
+enum : int { ST_INVALID = 1, ST_ARITY = 2, ST_CYCLE = 4, ST_FANOUT = 8, ST_XROW = 16 };
 
 // Device view of one context: sizes + every arena pointer.  Passed by value.
 struct Dev {
@@ -32,7 +32,7 @@ struct Dev {
   // schedule (position-indexed)
   int* order; int* level_ptr; int* child_pos; int* parent_pos; int* slot; int* deg; int* xrow_pos;
   int* tile_x;                      // per 64-position tile: 1 if any vertex has a pull record
-  int* hdr;                         // [0] status bits, [1] T, [2] #roots, [3] -, [4..] level_ptr
+  int* hdr;                         // [0] status bits, [1] T, [2] #roots, [3] deferred input errors (ST_XROW), [4..] level_ptr
   int* roots;                       // positions of vertices without a parent
   int* cnt;                         // per-graph level histograms: cnt[graph_ptr[g] + t] (t < T_g)
   int* lrank;                       // rank of a vertex among the vertices of its graph and level
@@ -65,6 +65,15 @@ struct Dev {
 };
 
 constexpr int kPadRows = 128;   // extra zero rows after V for TMA/K-block over-reach
+
+// cudaFuncSetAttribute is per device: launchers cache "attribute already set" per device id.
+constexpr int kMaxDev = 64;
+inline int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 ? 0 : d % kMaxDev;
+}
+
 
 __host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 

@@ -203,10 +203,11 @@ static void launch_rows(const CUtensorMap& a, const CUtensorMap& b, const Dev& D
                         int units, cudaStream_t s) {
   constexpr int smem = 1024 + kGS * (kGA + BN * 128) + 2 * kGS * 8 + 64;
   static_assert(kGRows * (BN + 4) * 4 + kGRows * (int)sizeof(VMeta) <= kGS * (kGA + BN * 128), "epilogue staging");
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[kMaxDev] = {};
+  const int dv = cur_device();
+  if (!attr[dv]) {
     cudaFuncSetAttribute(k_gemm_rows<E, BN, NG, kGS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
+    attr[dv] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(cdiv(D.V, kGRows), cdiv(units, BN / NG), 1);

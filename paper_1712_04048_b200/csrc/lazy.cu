@@ -318,6 +318,7 @@ struct LazyState {
   CUtensorMap A_dz, B_hk, B_xp;
   size_t slots = 0;               // scratch slots available in D.lazy
   int max_act = 0;
+  LPlan plan{};                   // host staging of the kernel parameter (per context: thread-safe across contexts)
 };
 
 static PFN_cuTensorMapEncodeTiled_v12000 l_enc = nullptr;
@@ -381,7 +382,7 @@ bool lazy_grads(const Dev& D, LazyState* l, cudaStream_t s) {
   // dW rows: the 64-row blocks holding a pull record; the plan assumes they are packed (trees:
   // the leaves [0, lp1); chains: every row); the device maps the plan onto the actual count
   const int nkb_x = std::min(cdiv(V, 64), cdiv(std::max(D.n_x, 0), 64));
-  static LPlan P;                                                          // host staging (kernel parameter)
+  LPlan& P = l->plan;                                                      // host staging (kernel parameter), per context
   int nj = 0;
   const int zero4[4] = {0, 0, 0, 0};
   if (lstm) {

@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) k_prep(Dev D, PrepJobs J) {
       return;
     }
     OpT* dst = prep_dst<OpT>(D, jb.dst_sel) + jb.dst_off;
-    if ((n & 3) == 0 && ((jb.dst_off & 3) == 0)) {
+    if ((n & 3) == 0 && ((jb.dst_off & 3) == 0) && ((reinterpret_cast<uintptr_t>(jb.src) & 15) == 0)) {
       const float4* s4 = reinterpret_cast<const float4*>(jb.src);
       for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += (size_t)gridDim.x * blockDim.x) {
         const float4 v = s4[i];
@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(256) k_prep(Dev D, PrepJobs J) {
 template <class OpT>
 __global__ void k_pull(Dev D) {
   pdl_wait();
+  if (D.hdr[0]) return;                          // invalid graphs: order[] is stale, touch nothing
   const int p0 = blockIdx.x * 64;
   __shared__ int s_r[64];
   if (threadIdx.x < 64) {
@@ -88,7 +89,10 @@ __global__ void k_pull(Dev D) {
     int r = -1;
     if (p < D.V) {
       r = D.x_row[D.order[p]];
-      if (r >= D.n_x) r = -1;                    // out-of-range record: treated as absent
+      if (r < -1 || r >= D.n_x) {                // out-of-range record: deferred CAVS_E_INVALID (cavs_sync),
+        atomicOr(D.hdr + 3, ST_XROW);            // the vertex pulls nothing meanwhile
+        r = -1;
+      }
       D.xrow_pos[p] = r;
     }
     s_r[threadIdx.x] = r;

@@ -626,13 +626,11 @@ static void launch_p(const CUtensorMap* A, const CUtensorMap* B, const Dev& D, c
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  static int nattr = 2;
-  cfg.numAttrs = nattr;
+  cfg.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, k_persist<E, NE, NM>, A[0], A[1], A[2], A[3], B[0], B[1], B[2], D, P,
                                      t_first, nlev, dir);
-  if (e != cudaSuccess && nattr == 2) {
+  if (e != cudaSuccess) {                             // retry this launch without PDL
     (void)cudaGetLastError();
-    nattr = 1;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, k_persist<E, NE, NM>, A[0], A[1], A[2], A[3], B[0], B[1], B[2], D, P, t_first, nlev, dir);
   }

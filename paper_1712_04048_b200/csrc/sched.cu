@@ -253,11 +253,12 @@ __global__ void k_build_maps(Dev D) {
 }
 
 void launch_schedule(const Dev& D, cudaStream_t s) {
-  static bool attr = false;
+  static bool attr[kMaxDev] = {};
   constexpr int smem = 5 * kSchedCap * 4;
-  if (!attr) {
+  const int dv = cur_device();
+  if (!attr[dv]) {
     cudaFuncSetAttribute(k_graph_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
+    attr[dv] = true;
   }
   launch_pdl(k_graph_sched, dim3(D.K), dim3(256), smem, s, D);
   launch_pdl(k_level_offsets, dim3(148), dim3(1024), 0, s, D);

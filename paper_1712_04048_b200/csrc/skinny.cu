@@ -145,10 +145,11 @@ static void sk_mv(const Dev& D, const SegListI& L, int row_lo, int row_hi, int u
     bsrc = g.b_src; ldb = g.ldb; W = std::max(W, g.b_col + g.klen);
   }
   const size_t smem = (size_t)MV * W * sizeof(OpT) + (size_t)NACC * kUnits * MV * sizeof(float);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
+  static size_t attr[kMaxDev] = {};
+  const int dv = cur_device();
+  if (smem > 48 * 1024 && smem > attr[dv]) {
     cudaFuncSetAttribute(k_skinny<OpT, NACC, E, MV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
+    attr[dv] = smem;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(cdiv(units, kUnits), 1, 1);

@@ -677,10 +677,11 @@ static void launch_level(const CUtensorMap& a0, const CUtensorMap& a1, const CUt
                          int row_lo, int row_hi, int units, cudaStream_t s) {
   if (row_hi <= row_lo) return;
   const int smem = plan_finalize(P, CL);
-  static int attr_set = 0;                             // dynamic + static smem must stay <= 227 KB
-  if (smem > attr_set) {
+  static int attr_set[kMaxDev] = {};                   // dynamic + static smem must stay <= 227 KB
+  const int dv = cur_device();
+  if (smem > attr_set[dv]) {
     cudaFuncSetAttribute(k_tc_level<E, NACC, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_set = smem;
+    attr_set[dv] = smem;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(CL * cdiv(units, 128), cdiv(row_hi - row_lo, NT), 1);
@@ -767,10 +768,11 @@ static int launch_II(const CUtensorMap& a, const CUtensorMap& b, const Dev& D, P
   P.split = std::max(1, std::min(std::min(kSplitMax, 148 / std::max(1, tiles)), std::max(1, nkb / 4)));
   P.stages = 6;
   const int smem = P.stages * 2 * T2_TILE + 1024 + 2 * 8 * P.stages + 64;
-  static bool attr_done = false;
-  if (!attr_done) {
+  static bool attr_done[kMaxDev] = {};
+  const int dv = cur_device();
+  if (!attr_done[dv]) {
     cudaFuncSetAttribute(k_tc_typeII, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_done = true;
+    attr_done[dv] = true;
   }
   dim3 grid(cdiv(P.M, 128), cdiv(P.Ncols, 128), P.split);
   k_tc_typeII<<<grid, kThreads, smem, s>>>(a, b, D, P, out);

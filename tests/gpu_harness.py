@@ -56,17 +56,57 @@ def run_gpu(b, precision="fp32", ctx=None, on_device=True):
                 dx=dx.cpu().numpy() if dx is not None else None, ctx=ctx)
 
 
-def run_oracle(b, emulate_bf16=False):
-    h_out, dparams, dx, tape = oracle.run(b, emulate_bf16=emulate_bf16)
+def run_oracle(b, emulate_bf16=False, bf16_hsum="rounded"):
+    h_out, dparams, dx, tape = oracle.run(b, emulate_bf16=emulate_bf16, bf16_hsum=bf16_hsum)
     return dict(h_out=h_out, dparams=dparams, dx=dx, tape=tape)
 
 
-def compare(b, g, r, tol, what=""):
-    errs = {"h_out": rel(g["h_out"], r["h_out"])}
+RECORD = []        # every compare(): (what, tol, metrics) -- dumped by conftest with CAVS_PARITY_LOG
+
+
+def row_rel_max(a, r):
+    """max over rows v of ||a_v - r_v|| / ||r_v|| (rows with ||r_v|| > 0): a wrong vertex row or
+    unit column cannot hide inside a per-tensor norm."""
+    a = np.asarray(a, dtype=np.float64).reshape(len(r), -1)
+    r = np.asarray(r, dtype=np.float64).reshape(len(r), -1)
+    n = np.linalg.norm(r, axis=1)
+    m = n > 0
+    if not m.any():
+        return float(np.abs(a).max(initial=0.0))
+    return float((np.linalg.norm(a - r, axis=1)[m] / n[m]).max())
+
+
+def elem_rel_max(a, r):
+    """max |a - r| / max |r| (Z12's elementwise diagnostic, scaled by the block's largest entry)."""
+    a = np.asarray(a, dtype=np.float64)
+    r = np.asarray(r, dtype=np.float64)
+    s = np.abs(r).max(initial=0.0)
+    return float(np.abs(a - r).max(initial=0.0) / (s if s > 0 else 1.0))
+
+
+# Row-wise / elementwise gates relative to the per-tensor gate `tol` (reading Z12, DESIGN.md §2):
+# the per-tensor L2 error averages over rows, the row maximum of thousands of rows sits a few
+# times above it; the elementwise error is normalised by the block's max |entry| and sits below.
+ROW_FACTOR = 5.0
+ELEM_FACTOR = 1.0
+
+
+def compare(b, g, r, tol, what="", row_factor=ROW_FACTOR, elem_factor=ELEM_FACTOR, rows=None):
+    """Per-tensor ||gpu - ref|| / ||ref|| <= tol (Z12) for h_out, every dparams block and dx,
+    plus row-wise (h_out, dx: max_v ||d_v|| / ||ref_v||) <= row_factor * tol and elementwise
+    (max |d| / max |ref|) <= elem_factor * tol.  `rows`: compare only these h_out rows."""
+    gh = g["h_out"] if rows is None else g["h_out"][rows]
+    errs = {"h_out": rel(gh, r["h_out"]), "h_out.row": row_rel_max(gh, r["h_out"]),
+            "h_out.elem": elem_rel_max(gh, r["h_out"])}
     for name, sl in param_blocks(b):
         errs["d" + name] = rel(g["dparams"][sl], r["dparams"][sl])
-    if b.n_x:
+        errs["d" + name + ".elem"] = elem_rel_max(g["dparams"][sl], r["dparams"][sl])
+    if b.n_x and r.get("dx") is not None:
         errs["dx"] = rel(g["dx"], r["dx"])
-    bad = {k: v for k, v in errs.items() if not v <= tol}
-    assert not bad, f"{what} errors above {tol}: {bad} (all: {errs})"
+        errs["dx.row"] = row_rel_max(g["dx"], r["dx"])
+        errs["dx.elem"] = elem_rel_max(g["dx"], r["dx"])
+    lim = {k: tol * (row_factor if k.endswith(".row") else elem_factor if k.endswith(".elem") else 1.0) for k in errs}
+    RECORD.append({"what": what, "tol": tol, "errs": errs})
+    bad = {k: v for k, v in errs.items() if not v <= lim[k]}
+    assert not bad, f"{what} errors above limits: {bad} (tol {tol}; all: {errs})"
     return errs

@@ -44,3 +44,18 @@ def test_create_rejects_bad_descriptors_without_gpu():
            _Desc(0, 2, 100, 64, 1, 1, 10, 10)]
     codes = [lib.cavs_create(ctypes.byref(b), 0, None, ctypes.byref(out)) for b in bad]
     assert codes == [1, 1, 1, 8, 8]
+
+
+def test_binding_rejects_wrong_dtypes_and_devices():
+    """int64 index arrays / CPU tensors must not reach the C-ABI as raw pointers."""
+    import numpy as np
+    import torch
+    from paper_1712_04048_b200.cavs import _ptr
+    with pytest.raises(TypeError):
+        _ptr(np.zeros(4, np.int64), "i32")
+    with pytest.raises(TypeError):
+        _ptr(torch.zeros(4, dtype=torch.int64), "i32")
+    with pytest.raises(TypeError):                      # CPU tensor where a device pointer is required
+        _ptr(torch.zeros(4, dtype=torch.float32), "f32", torch.device("cuda", 0))
+    assert _ptr(np.zeros(4, np.int32), "i32") != 0
+    assert _ptr(torch.zeros(4, dtype=torch.float32), "f32", torch.device("cuda", 0), host_ok=True) != 0

@@ -17,5 +17,6 @@ from .gen import (  # noqa: F401
     n_params,
     remy_tree,
     sst_lengths,
+    subset_csr,
     batch_from_graphs,
 )
