@@ -35,7 +35,11 @@ What it computes (PAPER.md = /root/reference/PAPER.md, "P:Lnnn" = line):
       bf16_hsum="exact"   (reading R-lin): U h~ taken as sum_k U bf16(h_k) in
                           exact arithmetic, i.e. h~ = sum_k bf16(h_k) unrounded.
     Both equal the fp64 definition up to bf16 rounding; they coincide bit for
-    bit when no vertex has two or more children.
+    bit when no vertex has two or more children.  `accum="fp32"` (bf16 mode
+    only) accumulates the matrix-vector products in fp32 instead of fp64: a
+    second valid summation, whose distance from the fp64-accumulated emulation
+    measures how much a chaotic F (reading R-bf16) amplifies summation-order
+    rounding -- the conditioning-derived parity band of the cfg5 bench init.
 
 Parity status: every function here is pinned by `tests/test_oracle_pins.py`
 (closed forms, brute force, torch.nn.LSTM, finite differences, hand-worked
@@ -241,11 +245,30 @@ class Tape:
     children: list
 
 
+def _mv(accum):
+    """Matrix-vector product of the bf16 emulation: fp64 accumulation (default), or fp32
+    accumulation (`accum="fp32"`: operands are bf16-exact, so every product is exact in fp32
+    and only the running sum rounds -- the GPU's tensor-core arithmetic, in numpy's order)."""
+    if accum == "fp64":
+        return lambda A, v: A @ v
+    if accum == "fp32":
+        cache = {}                     # fp32 images of the (bf16-exact) weight matrices
+
+        def mv32(A, v):
+            key = (A.__array_interface__["data"][0], A.shape, A.strides)
+            if key not in cache:
+                cache[key] = np.asarray(A, np.float32)
+            return (cache[key] @ np.asarray(v, np.float32)).astype(np.float64)
+        return mv32
+    raise ValueError(accum)
+
+
 def forward(cell, N, h, d, theta, graph_ptr, child_ptr, child_idx, x_row, x, emulate_bf16=False,
-            bf16_hsum="rounded"):
+            bf16_hsum="rounded", accum="fp64"):
     """Returns (h_out[V,h] fp64, tape).  Evaluates F at every vertex after all its
     children (Fig. 5); each vertex exactly once (memo).  `bf16_hsum` only
-    matters with emulate_bf16 (see the module header)."""
+    matters with emulate_bf16 (see the module header); so does `accum` (_mv)."""
+    mv = _mv(accum if emulate_bf16 else "fp64")
     if bf16_hsum not in ("rounded", "exact"):
         raise ValueError(bf16_hsum)
     ch = validate(graph_ptr, child_ptr, child_idx, N)
@@ -281,10 +304,10 @@ def forward(cell, N, h, d, theta, graph_ptr, child_ptr, child_idx, x_row, x, emu
                 hs = sum(hkq)
                 if bf16_hsum == "rounded":
                     hs = q(hs)
-            i = sigmoid(Pq["W_i"] @ xv + Pq["U_i"] @ hs + P["b_i"])
-            f = [sigmoid(Pq["W_f"] @ xv + Pq["U_f"] @ hkq[k] + P["b_f"]) for k in range(N)]
-            o = sigmoid(Pq["W_o"] @ xv + Pq["U_o"] @ hs + P["b_o"])
-            u = np.tanh(Pq["W_u"] @ xv + Pq["U_u"] @ hs + P["b_u"])
+            i = sigmoid(mv(Pq["W_i"], xv) + mv(Pq["U_i"], hs) + P["b_i"])
+            f = [sigmoid(mv(Pq["W_f"], xv) + mv(Pq["U_f"], hkq[k]) + P["b_f"]) for k in range(N)]
+            o = sigmoid(mv(Pq["W_o"], xv) + mv(Pq["U_o"], hs) + P["b_o"])
+            u = np.tanh(mv(Pq["W_u"], xv) + mv(Pq["U_u"], hs) + P["b_u"])
             c = i * u + sum(f[k] * ck[k] for k in range(N))
             hv = o * np.tanh(c)
             st[v] = dict(h=hv, c=c, i=i, f=f, o=o, u=u, hs=hs, hkq=hkq, ck=ck, x=xv)
@@ -292,7 +315,7 @@ def forward(cell, N, h, d, theta, graph_ptr, child_ptr, child_idx, x_row, x, emu
             hl = st[ch[v][0]]["h"] if len(ch[v]) > 0 else np.zeros(h)
             hr = st[ch[v][1]]["h"] if len(ch[v]) > 1 else np.zeros(h)
             hlq, hrq = q(hl), q(hr)
-            z = Pq["W_l"] @ hlq + Pq["W_r"] @ hrq + Pq["W_x"] @ xv + P["b"]
+            z = mv(Pq["W_l"], hlq) + mv(Pq["W_r"], hrq) + mv(Pq["W_x"], xv) + P["b"]
             hv = np.tanh(z)
             st[v] = dict(h=hv, hkq=[hlq, hrq], x=xv)
         log.append(v)                  # scatter/push: h is published
@@ -306,9 +329,11 @@ def forward(cell, N, h, d, theta, graph_ptr, child_ptr, child_idx, x_row, x, emu
     return h_out, Tape(log=log, st=st, children=ch)
 
 
-def backward(cell, N, h, d, theta, tape, x_row, n_x, gamma, emulate_bf16=False):
+def backward(cell, N, h, d, theta, tape, x_row, n_x, gamma, emulate_bf16=False, accum="fp64"):
     """dL/dparams (packed, fp64) and dL/dx [n_x, d] for L = sum_v <Gamma_v, h_v>.
-    Reverse evaluation order (Alg. 1 BACKWARD); all gradients accumulate."""
+    Reverse evaluation order (Alg. 1 BACKWARD); all gradients accumulate.
+    `accum` (bf16 emulation only): the dH / dx products' accumulation, see _mv."""
+    mv = _mv(accum if emulate_bf16 else "fp64")
     P = unpack(cell, N, h, d, theta)
     q = bf16r if emulate_bf16 else (lambda a: a)
     Pq = {k: (q(v) if not k.startswith("b") else v) for k, v in P.items()}
@@ -331,9 +356,9 @@ def backward(cell, N, h, d, theta, tape, x_row, n_x, gamma, emulate_bf16=False):
             dz_f = [dcb * s["ck"][k] * f[k] * (1 - f[k]) for k in range(N)]
             dz_i, dz_o, dz_u = q(dz_i), q(dz_o), q(dz_u)
             dz_f = [q(a) for a in dz_f]
-            dhs = Pq["U_i"].T @ dz_i + Pq["U_o"].T @ dz_o + Pq["U_u"].T @ dz_u
+            dhs = mv(Pq["U_i"].T, dz_i) + mv(Pq["U_o"].T, dz_o) + mv(Pq["U_u"].T, dz_u)
             for k, cv in enumerate(ch[v]):           # scatter = adjoint of gather
-                dh[cv] += dhs + Pq["U_f"].T @ dz_f[k]
+                dh[cv] += dhs + mv(Pq["U_f"].T, dz_f[k])
                 dc[cv] += dcb * f[k]
             hs = s["hs"]
             G["U_i"] += np.outer(dz_i, hs); G["U_o"] += np.outer(dz_o, hs); G["U_u"] += np.outer(dz_u, hs)
@@ -347,21 +372,21 @@ def backward(cell, N, h, d, theta, tape, x_row, n_x, gamma, emulate_bf16=False):
                 G["W_u"] += np.outer(dz_u, xv)
                 for k in range(N):
                     G["W_f"] += np.outer(dz_f[k], xv)
-                dx[r] += (Pq["W_i"].T @ dz_i + Pq["W_o"].T @ dz_o + Pq["W_u"].T @ dz_u
-                          + Pq["W_f"].T @ sum(dz_f))
+                dx[r] += (mv(Pq["W_i"].T, dz_i) + mv(Pq["W_o"].T, dz_o) + mv(Pq["W_u"].T, dz_u)
+                          + mv(Pq["W_f"].T, sum(dz_f)))
         else:
             dz = q(dh[v] * (1 - s["h"] ** 2))
             hlq, hrq = s["hkq"]
             if len(ch[v]) > 0:
-                dh[ch[v][0]] += Pq["W_l"].T @ dz
+                dh[ch[v][0]] += mv(Pq["W_l"].T, dz)
             if len(ch[v]) > 1:
-                dh[ch[v][1]] += Pq["W_r"].T @ dz
+                dh[ch[v][1]] += mv(Pq["W_r"].T, dz)
             G["W_l"] += np.outer(dz, hlq)
             G["W_r"] += np.outer(dz, hrq)
             G["b"] += dz
             if r >= 0:
                 G["W_x"] += np.outer(dz, s["x"])
-                dx[r] += Pq["W_x"].T @ dz
+                dx[r] += mv(Pq["W_x"].T, dz)
     return pack(cell, N, h, d, G), dx
 
 
@@ -370,13 +395,13 @@ def loss(h_out, gamma):
     return float(np.sum(np.asarray(h_out) * np.asarray(gamma, dtype=np.float64)))
 
 
-def run(batch, emulate_bf16=False, with_backward=True, bf16_hsum="rounded"):
+def run(batch, emulate_bf16=False, with_backward=True, bf16_hsum="rounded", accum="fp64"):
     """Convenience: forward (+ backward) on a workloads.Batch-like object."""
     h_out, tape = forward(batch.cell, batch.N, batch.h, batch.d, batch.params, batch.graph_ptr,
                           batch.child_ptr, batch.child_idx, batch.x_row, batch.x,
-                          emulate_bf16=emulate_bf16, bf16_hsum=bf16_hsum)
+                          emulate_bf16=emulate_bf16, bf16_hsum=bf16_hsum, accum=accum)
     if not with_backward:
         return h_out, None, None, tape
     dparams, dx = backward(batch.cell, batch.N, batch.h, batch.d, batch.params, tape, batch.x_row,
-                           batch.x.shape[0], batch.gamma, emulate_bf16=emulate_bf16)
+                           batch.x.shape[0], batch.gamma, emulate_bf16=emulate_bf16, accum=accum)
     return h_out, dparams, dx, tape

@@ -56,8 +56,8 @@ def run_gpu(b, precision="fp32", ctx=None, on_device=True):
                 dx=dx.cpu().numpy() if dx is not None else None, ctx=ctx)
 
 
-def run_oracle(b, emulate_bf16=False, bf16_hsum="rounded"):
-    h_out, dparams, dx, tape = oracle.run(b, emulate_bf16=emulate_bf16, bf16_hsum=bf16_hsum)
+def run_oracle(b, emulate_bf16=False, bf16_hsum="rounded", accum="fp64"):
+    h_out, dparams, dx, tape = oracle.run(b, emulate_bf16=emulate_bf16, bf16_hsum=bf16_hsum, accum=accum)
     return dict(h_out=h_out, dparams=dparams, dx=dx, tape=tape)
 
 
@@ -91,10 +91,8 @@ ROW_FACTOR = 5.0
 ELEM_FACTOR = 1.0
 
 
-def compare(b, g, r, tol, what="", row_factor=ROW_FACTOR, elem_factor=ELEM_FACTOR, rows=None):
-    """Per-tensor ||gpu - ref|| / ||ref|| <= tol (Z12) for h_out, every dparams block and dx,
-    plus row-wise (h_out, dx: max_v ||d_v|| / ||ref_v||) <= row_factor * tol and elementwise
-    (max |d| / max |ref|) <= elem_factor * tol.  `rows`: compare only these h_out rows."""
+def errors(b, g, r, rows=None):
+    """Per-tensor, row-wise and elementwise errors of g against r (see compare)."""
     gh = g["h_out"] if rows is None else g["h_out"][rows]
     errs = {"h_out": rel(gh, r["h_out"]), "h_out.row": row_rel_max(gh, r["h_out"]),
             "h_out.elem": elem_rel_max(gh, r["h_out"])}
@@ -105,6 +103,14 @@ def compare(b, g, r, tol, what="", row_factor=ROW_FACTOR, elem_factor=ELEM_FACTO
         errs["dx"] = rel(g["dx"], r["dx"])
         errs["dx.row"] = row_rel_max(g["dx"], r["dx"])
         errs["dx.elem"] = elem_rel_max(g["dx"], r["dx"])
+    return errs
+
+
+def compare(b, g, r, tol, what="", row_factor=ROW_FACTOR, elem_factor=ELEM_FACTOR, rows=None):
+    """Per-tensor ||gpu - ref|| / ||ref|| <= tol (Z12) for h_out, every dparams block and dx,
+    plus row-wise (h_out, dx: max_v ||d_v|| / ||ref_v||) <= row_factor * tol and elementwise
+    (max |d| / max |ref|) <= elem_factor * tol.  `rows`: compare only these h_out rows."""
+    errs = errors(b, g, r, rows)
     lim = {k: tol * (row_factor if k.endswith(".row") else elem_factor if k.endswith(".elem") else 1.0) for k in errs}
     RECORD.append({"what": what, "tol": tol, "errs": errs})
     bad = {k: v for k, v in errs.items() if not v <= lim[k]}

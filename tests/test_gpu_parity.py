@@ -349,7 +349,21 @@ def test_full_size_cfg5(precision, pscale):
         return
     q = run_oracle(sb, emulate_bf16=True)
     if pscale == 1.0:
-        compare(b, g_s, q, BF16_TOL, "cfg5 bf16 bench init vs bf16-emulating oracle")
+        # chaotic F (reading R-bf16): any change of fp32 summation order flips bf16 roundings that
+        # the dynamics amplify.  The band is the problem's own conditioning: the distance between
+        # two equally valid emulations (fp64- vs fp32-accumulated products, same rounding points),
+        # times 4 (the GPU's MUFU tanh, rel. 2^-11, perturbs more than fp32 summation does), and
+        # never tighter than the bf16 gate.
+        q32 = run_oracle(sb, emulate_bf16=True, accum="fp32")
+        from gpu_harness import errors, RECORD
+        spread = errors(b, q32, q)
+        g_err = errors(b, g_s, q)
+        RECORD.append({"what": "cfg5 bf16 bench init: emulation spread (fp32 vs fp64 accumulation)", "tol": None,
+                       "errs": spread})
+        RECORD.append({"what": "cfg5 bf16 bench init vs bf16-emulating oracle", "tol": None, "errs": g_err})
+        bad = {k: (v, spread[k]) for k, v in g_err.items() if not v <= max(BF16_TOL, 4 * spread[k])}
+        assert not bad, f"cfg5 bench init: GPU vs emulation beyond 4x the emulation spread: {bad}"
+        assert max(spread.values()) > BF16_TOL / 4, "R-bf16: the bench init should be ill-conditioned"
     else:
         r = run_oracle(sb)
         assert _quant(q, r, b) <= 1e-2

@@ -317,6 +317,24 @@ def test_bf16_emulation_close_to_exact():
     assert rel(dpr, dp) < 2e-2
 
 
+def test_bf16_fp32_accumulation_is_a_rounding_of_the_fp64_accumulation():
+    """accum="fp32" (bf16 emulation): every product of bf16 operands is exact in fp32, so the
+    fp32-accumulated emulation differs from the fp64-accumulated one only by the running sum's
+    rounding -- on a contracting (well-conditioned) case by ~2^-24 * sqrt(K) relative, never more
+    than a few 1e-6, and it does differ (the flag is live).  Without emulation it is ignored."""
+    b = gen.make_batch("tree_lstm", 2, 32, 32, "sst_tree", 6, seed=5)
+    a = oracle.run(b, emulate_bf16=True)
+    f = oracle.run(b, emulate_bf16=True, accum="fp32")
+    rel = lambda x, r: np.linalg.norm(x - r) / np.linalg.norm(r)
+    for x, y in zip(f[:3], a[:3]):
+        assert rel(x, y) < 5e-6
+    assert rel(f[0], a[0]) > 0
+    e = oracle.run(b, accum="fp32")
+    p = oracle.run(b)
+    for x, y in zip(e[:3], p[:3]):
+        assert np.array_equal(x, y)
+
+
 def test_bf16_hsum_readings_coincide_without_fan_in():
     """R-lin vs Z11: h~ = h_1 when no vertex has two children, and bf16 rounding is
     idempotent, so both readings must give bit-identical results on chains / unary trees."""
