@@ -35,11 +35,11 @@ What it computes (PAPER.md = /root/reference/PAPER.md, "P:Lnnn" = line):
       bf16_hsum="exact"   (reading R-lin): U h~ taken as sum_k U bf16(h_k) in
                           exact arithmetic, i.e. h~ = sum_k bf16(h_k) unrounded.
     Both equal the fp64 definition up to bf16 rounding; they coincide bit for
-    bit when no vertex has two or more children.  `accum="fp32"` (bf16 mode
-    only) accumulates the matrix-vector products in fp32 instead of fp64: a
-    second valid summation, whose distance from the fp64-accumulated emulation
-    measures how much a chaotic F (reading R-bf16) amplifies summation-order
-    rounding -- the conditioning-derived parity band of the cfg5 bench init.
+    bit when no vertex has two or more children.
+  * `accum="fp32"` (diagnostic, any mode) evaluates the matrix-vector products
+    in fp32 instead of fp64: a second valid evaluation, whose distance from the
+    fp64 one measures how much a chaotic F (reading R-chaos) amplifies rounding
+    -- the conditioning-derived parity band of the cfg5 bench init.
 
 Parity status: every function here is pinned by `tests/test_oracle_pins.py`
 (closed forms, brute force, torch.nn.LSTM, finite differences, hand-worked
@@ -246,9 +246,11 @@ class Tape:
 
 
 def _mv(accum):
-    """Matrix-vector product of the bf16 emulation: fp64 accumulation (default), or fp32
-    accumulation (`accum="fp32"`: operands are bf16-exact, so every product is exact in fp32
-    and only the running sum rounds -- the GPU's tensor-core arithmetic, in numpy's order)."""
+    """Matrix-vector product: fp64 (default), or `accum="fp32"`: operands rounded to fp32 and the
+    sum accumulated in fp32 (numpy's order) -- a second valid fp32 evaluation.  With the bf16
+    emulation the operands are bf16-exact, so every product is exact and only the running sum
+    rounds (the tensor cores' arithmetic).  Diagnostic only: it measures how much F amplifies
+    summation-order rounding (reading R-chaos)."""
     if accum == "fp64":
         return lambda A, v: A @ v
     if accum == "fp32":
@@ -267,8 +269,8 @@ def forward(cell, N, h, d, theta, graph_ptr, child_ptr, child_idx, x_row, x, emu
             bf16_hsum="rounded", accum="fp64"):
     """Returns (h_out[V,h] fp64, tape).  Evaluates F at every vertex after all its
     children (Fig. 5); each vertex exactly once (memo).  `bf16_hsum` only
-    matters with emulate_bf16 (see the module header); so does `accum` (_mv)."""
-    mv = _mv(accum if emulate_bf16 else "fp64")
+    matters with emulate_bf16 (see the module header); `accum` selects _mv."""
+    mv = _mv(accum)
     if bf16_hsum not in ("rounded", "exact"):
         raise ValueError(bf16_hsum)
     ch = validate(graph_ptr, child_ptr, child_idx, N)
@@ -332,8 +334,8 @@ def forward(cell, N, h, d, theta, graph_ptr, child_ptr, child_idx, x_row, x, emu
 def backward(cell, N, h, d, theta, tape, x_row, n_x, gamma, emulate_bf16=False, accum="fp64"):
     """dL/dparams (packed, fp64) and dL/dx [n_x, d] for L = sum_v <Gamma_v, h_v>.
     Reverse evaluation order (Alg. 1 BACKWARD); all gradients accumulate.
-    `accum` (bf16 emulation only): the dH / dx products' accumulation, see _mv."""
-    mv = _mv(accum if emulate_bf16 else "fp64")
+    `accum`: the dH / dx products' arithmetic, see _mv."""
+    mv = _mv(accum)
     P = unpack(cell, N, h, d, theta)
     q = bf16r if emulate_bf16 else (lambda a: a)
     Pq = {k: (q(v) if not k.startswith("b") else v) for k, v in P.items()}

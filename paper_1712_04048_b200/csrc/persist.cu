@@ -29,9 +29,8 @@
 #include <algorithm>
 #include <cstdlib>
 
-#include "cells.cuh"
 #include "persist.h"
-#include "ptx.cuh"
+#include "persist_common.cuh"
 
 namespace cavs {
 
@@ -62,73 +61,6 @@ struct PPlan {
   int xs_off, meta_off, bar_off;
 };
 
-// mbarrier wait: try_wait (the waiting thread is suspended in hardware instead of polling the
-// barrier unit), trapping after ~4 s instead of hanging the GPU on a protocol bug.
-__device__ __forceinline__ void pwait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = ptx::smem_u32(bar);
-  unsigned long long t0 = 0;
-  for (;;) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred P;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
-        "selp.b32 %0, 1, 0, P;\n\t}"
-        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
-    if (ok) return;
-    const unsigned long long now = gtime();
-    if (t0 == 0) t0 = now;
-    else if (now - t0 > 4000000000ull) __trap();
-  }
-}
-// one waiting lane per warp, then the warp proceeds together
-__device__ __forceinline__ void pwait_warp(uint64_t* bar, uint32_t parity) {
-  if ((threadIdx.x & 31) == 0) pwait(bar, parity);
-  __syncwarp();
-}
-
-__device__ __forceinline__ int nt_index(int M, int R, int max_ni) {
-  const int n = (M + R - 1) / R;
-  return min(max_ni, n <= 16 ? 0 : n <= 32 ? 1 : 2);
-}
-
-// Cluster-local task barrier.  The graphs of a batch are independent, so each
-// cluster owns a contiguous range of graphs (their rows of every task V_t are contiguous: positions
-// inside a task are graph-major) and only its own CTAs -- the unit blocks of the same rows -- need
-// to agree that V_t is done before V_t+-1 starts.  One mbarrier per CTA counts one remote arrival
-// per CTA of the cluster (DSMEM, release at cluster scope); the waiter acquires at cluster scope.
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// release-arrive on CTA c's barrier (the release covers this CTA's task writes: the caller passed
-// a CTA barrier after them)
-__device__ __forceinline__ void cluster_arrive(uint64_t* bar, int c) {
-  uint32_t ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(ptx::smem_u32(bar)), "r"(c));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
-}
-__device__ __forceinline__ void cluster_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = ptx::smem_u32(bar);
-  unsigned long long t0 = 0;
-  for (;;) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred P;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
-        "selp.b32 %0, 1, 0, P;\n\t}"
-        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
-    if (ok) return;
-    const unsigned long long now = gtime();
-    if (t0 == 0) t0 = now;
-    else if (now - t0 > 4000000000ull) __trap();
-  }
-}
-// rows of task t owned by cluster r: [crow[t][r], crow[t][r + 1]) (k_build_maps)
-__device__ __forceinline__ void cl_rows(const Dev& D, int t, int r, int& lo, int& M) {
-  const int* c = D.crow + (size_t)t * (D.ncl + 1) + r;
-  lo = c[0];
-  M = c[1] - lo;
-}
-
 // Compile-time staging layout per epilogue kind (matches the host plan of persist_init):
 // xs slot s holds one row group's accumulator(s); epilogue accumulator e sums slots.
 template <int E, int NM> struct PLay {
@@ -149,22 +81,8 @@ template <int E, int NM> struct PLay {
   }
 };
 
-// debug trace record (CAVS_TRACE=1): 8 words per record in the ring at D.trace
-__device__ __forceinline__ void ptrace(const Dev& D, unsigned long long a, unsigned long long b, unsigned long long c,
-                                       unsigned long long d, unsigned long long e, unsigned long long f,
-                                       unsigned long long g, unsigned long long h) {
-  const unsigned long long at = 8 + 8 * atomicAdd(D.trace, 1ull);
-  if (at + 8 < (4u << 20) / 8) {
-    D.trace[at] = a; D.trace[at + 1] = b; D.trace[at + 2] = c; D.trace[at + 3] = d;
-    D.trace[at + 4] = e; D.trace[at + 5] = f; D.trace[at + 6] = g; D.trace[at + 7] = h;
-  }
-}
-
 // MMA issue of one task's tiles (NT compile-time: constant instruction descriptor, accumulator
 // columns and descriptor strides; only 32-bit adds per tcgen05.mma).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t lo) {
-  return ((uint64_t)((1024u >> 4) | (1u << 14) | (2u << 29)) << 32) | lo;   // SBO 1024, version 1, SWIZZLE_128B
-}
 template <int NT, bool TS>
 __device__ __forceinline__ void mma_level(const PPlan& P, int ntile, uint32_t a_lo, uint32_t b_lo,
                                           uint64_t* full, uint64_t* empty, uint64_t* done, uint64_t* tmem_empty,
@@ -240,7 +158,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
   uint64_t* acopy = abar + 1;                                   // weights copied smem -> TMEM
   uint64_t* cbar = acopy + 1;                                   // cluster task barrier
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbar + 1);
-  volatile int* gate = reinterpret_cast<volatile int*>(tmem_slot + 1);
+  int* gate = reinterpret_cast<int*>(tmem_slot + 1);
   __shared__ unsigned long long s_tmax;                          // debug trace only
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -291,8 +209,8 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
         const uint32_t bytes = (uint32_t)nt * 128u * (uint32_t)sk;
         if (i > 0) {                                  // previous task finished grid-wide
           const unsigned long long tw = D.trace ? gtime() : 0;
-          while (*gate < i) { }
-          ptx::fence_proxy_async_global();
+          while (gate_get(gate) < i) { }         // acquire: the cluster's task writes are visible
+          ptx::fence_proxy_async_global();     // ... to this thread's TMA (async proxy) reads
           if (D.trace && w == 0) ptrace(D, 3000 + E, blockIdx.x, i, tw, gtime(), 0, 0, 0);
         }
         if (D.trace && w == 0) ptrace(D, 5000 + E, blockIdx.x, i, gtime(), 0, 0, 0, 0);
@@ -376,7 +294,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
       unsigned long long tr0 = 0, tr1 = 0, tr2 = 0, tr3 = 0;
       if (D.trace && et == 0) tr0 = gtime();
       if (i > 0 && ntile > 0) {                         // inputs of V_t are final once the barrier passed
-        if (lane == 0) while (*gate < i) { }
+        if (lane == 0) while (gate_get(gate) < i) { }
         __syncwarp();
       }
       for (int jt = 0; jt < ntile; ++jt, ++tcount) {
@@ -475,7 +393,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
             ++nbar;
           }
           if (et == 0) {
-            *gate = i + 1;
+            gate_set(gate, i + 1);
             if (D.trace) ptrace(D, 2000 + E, blockIdx.x, (unsigned long long)i | ((unsigned long long)M << 16), tr0, tr1,
                                 tr2, gtime(), tr3);
           }
@@ -499,6 +417,8 @@ struct PersistState {
   CUtensorMap A_fwd[4], A_bwd[4];     // per row group (box 64 x UG)
   CUtensorMap B_hk[3], B_dz[3];       // 3D {64, NT, sk} boxes over Hk / dZ
   PPlan fwd{}, bwd{};
+  PbwdState* kbwd = nullptr;          // Tree-LSTM backward: K-split kernel (persist_bwd.cu)
+  std::string kbwd_why;
   int num_sms = 0;
 };
 
@@ -730,18 +650,34 @@ PersistState* persist_init(const Dev& D, int max_vertices, std::string* why) {
   } else {
     occ(attr_and_clusters<EPI_FC_FWD, 1, 1>(plan_smem(F), nub), attr_and_clusters<EPI_FC_BWD, 2, 1>(plan_smem(B), nub));
   }
+  if (lstm) {                                          // the K-split backward shares the cluster table
+    int kc = 0;
+    ps->kbwd = pbwd_init(D, max_vertices, &kc, &ps->kbwd_why);
+    if (ps->kbwd) nc = std::min(nc, kc);
+  }
   const char* cenv = std::getenv("CAVS_PERSIST_CLUSTERS");    // debug / A-B: fewer clusters
   if (cenv && std::atoi(cenv) > 0) nc = std::min(nc, std::atoi(cenv));
-  if (nc < 1) { delete ps; *why = "no cluster of " + std::to_string(nub) + " CTAs fits"; return nullptr; }
+  if (nc < 1) {
+    if (ps->kbwd) pbwd_destroy(ps->kbwd);
+    delete ps;
+    *why = "no cluster of " + std::to_string(nub) + " CTAs fits";
+    return nullptr;
+  }
   F.R = B.R = R = nc;
+  if (ps->kbwd) pbwd_set_clusters(ps->kbwd, nc);
   ps->fwd = F;
   ps->bwd = B;
   return ps;
 }
 
-void persist_destroy(PersistState* ps) { delete ps; }
+void persist_destroy(PersistState* ps) {
+  if (ps && ps->kbwd) pbwd_destroy(ps->kbwd);
+  delete ps;
+}
 
 int persist_clusters(const PersistState* ps) { return ps ? ps->fwd.R : 0; }
+
+static bool D_is_lstm(const PersistState* ps) { return ps->fwd.ngrp == 4; }
 
 std::string persist_describe(const PersistState* ps) {
   const PPlan& F = ps->fwd;
@@ -749,7 +685,9 @@ std::string persist_describe(const PersistState* ps) {
   return "persistent: grid " + std::to_string(F.nub * F.R) + " (units/CTA " + std::to_string(F.UG) + ", " +
          std::to_string(F.R) + " clusters of " + std::to_string(F.nub) + " over graph ranges), weights in " + (F.tsA ? "TMEM" : "smem") + ", stages fwd " + std::to_string(F.S) +
          " bwd " + std::to_string(B.S) + ", max task tile fwd " + std::to_string(16 << F.max_ni) + " bwd " +
-         std::to_string(16 << B.max_ni);
+         std::to_string(16 << B.max_ni) +
+         (ps->kbwd ? "; " + pbwd_describe(ps->kbwd)
+                   : (D_is_lstm(ps) ? "; bwd gate-grouped (K-split unavailable: " + ps->kbwd_why + ")" : std::string()));
 }
 
 void persist_forward(const Dev& D, PersistState* ps, int T, cudaStream_t s) {
@@ -769,6 +707,7 @@ void persist_forward(const Dev& D, PersistState* ps, int T, cudaStream_t s) {
 
 void persist_backward(const Dev& D, PersistState* ps, int T, cudaStream_t s) {
   if (T <= 1) return;
+  if (ps->kbwd) { pbwd_launch(D, ps->kbwd, T, s); return; }
   const PPlan& P = ps->bwd;
   if (D.cell == CAVS_CELL_TREE_LSTM) {
     switch (D.N) {
