@@ -5,12 +5,13 @@
                     [--config cfg4] [--precision bf16|fp32] [--h H]
 
 Workload (BASELINE.json metric "Tree-LSTM train samples/s (fwd+bwd)"): cfg4 = Tree-LSTM on
-synthetic SST-shaped binarised parse trees, h = d = 512, 256 trees per GPU (weak scaling,
-one independent batch per rank; the only exchange is the NCCL all-reduce of the weight
-gradients).  A step = cavs_load_graphs (device-resident CSR) + cavs_schedule +
-cavs_forward + cavs_backward (+ all-reduce for N > 1) over one batch of a pool of 16
-pre-generated batches, so the schedule changes every step.  L2 is flushed (256 MiB write)
-between timed steps, outside the per-step CUDA events.
+synthetic SST-shaped binarised parse trees, h = d = 512, a GLOBAL batch of 256 trees (strong
+scaling: at N > 1 the batch is sharded over the ranks by vertex count, dp.shard_batch; --weak
+gives every rank its own 256 trees).  A step = cavs_load_graphs (device-resident CSR) +
+cavs_schedule + cavs_forward + cavs_backward (+ the bucketed NCCL all-reduce of the weight
+gradients for N > 1, overlapped with dX / db) over one batch of a pool of 16 pre-generated
+batches, so the schedule changes every step.  L2 is flushed (256 MiB write) between timed steps,
+outside the per-step CUDA events.
 
 The roofline object is computed live from the library's per-phase CUDA events and its
 algorithmic FLOP counts; `traffic` comes from the
@@ -63,6 +64,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: an independent batch of the config's size per rank (default: strong "
+                         "scaling, ONE global batch sharded over the ranks by dp.shard_batch)")
     ap.add_argument("--inference", action="store_true",
                     help="forward-only (cavs_forward_inference): inference samples/s, no backward")
     a = ap.parse_args()
@@ -201,7 +205,7 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": "Tree-LSTM train samples/s (fwd+bwd)" if b.cell == "tree_lstm"
         else "Tree-FC train samples/s (fwd+bwd)",
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": f"{args.config}: {_desc(args.config, b.h)}",
                                         "h": b.h, "batch": b.K, "sample_graphs_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": used, "kind": "oracle",
@@ -234,7 +238,17 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     # ---- inputs: a pool of batches resident in HBM before the timed region ----
-    batches = [gen.make_config_batch(args.config, seed=rank * args.pool + i, h=args.h) for i in range(args.pool)]
+    # strong scaling (default): pool batch i is ONE global batch (seed i, same on every rank), sharded
+    # over the ranks by vertex count (dp.shard_batch; the graphs are independent);
+    # weak scaling (--weak): every rank draws its own full-size batches (seeds rank * pool + i)
+    if args.weak or world == 1:
+        glob = [gen.make_config_batch(args.config, seed=(rank if args.weak else 0) * args.pool + i, h=args.h)
+                for i in range(args.pool)]
+        batches = glob
+    else:
+        glob = [gen.make_config_batch(args.config, seed=i, h=args.h) for i in range(args.pool)]
+        batches = [dp.shard_batch(g, world, rank)[0] for g in glob]
+    depth_T = float(np.mean([max(dp.graph_depths(g.graph_ptr, g.child_ptr, g.child_idx)) for g in glob]))
     b0 = batches[0]
     params = torch.from_numpy(gen.make_config_batch(args.config, seed=0, h=args.h).params).to(dev)
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
@@ -242,11 +256,14 @@ def main():
             for b in batches]
     maxV = max(b.V for b in batches)
     maxX = max(b.n_x for b in batches)
-    ctx = Context(b0.cell, b0.N, b0.h, b0.d, precision=args.precision, max_graphs=b0.K, max_vertices=maxV,
-                  max_x=maxX, device=local)
+    ctx = Context(b0.cell, b0.N, b0.h, b0.d, precision=args.precision, max_graphs=max(b.K for b in batches),
+                  max_vertices=maxV, max_x=maxX, device=local)
     h_out = torch.empty(maxV, b0.h, device=dev)
     dparams = torch.empty(ctx.P, device=dev)
     dx = torch.empty(maxX, b0.d, device=dev)
+    # N > 1: weight blocks all-reduced on a side stream as soon as the lazy GEMMs finish (overlapping
+    # dX and db), the bias block after the backward (dp.BucketedAllReduce)
+    allreduce = dp.BucketedAllReduce(ctx, dparams, dp.bias_floats(b0.cell, b0.N, b0.h)) if world > 1 else None
 
     def step(i):
         p = pool[i % len(pool)]
@@ -258,8 +275,9 @@ def main():
             return
         ctx.forward(params, p["x"], p["xr"], h_out[:V])
         ctx.backward(p["g"], dparams, dx[:p["x"].shape[0]])
-        if world > 1:
-            dp.allreduce_grads(dparams)
+        if allreduce is not None:
+            allreduce.launch()
+            allreduce.wait()
 
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for i in range(args.warmup):
@@ -294,7 +312,7 @@ def main():
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    samples = world * b0.K
+    samples = world * b0.K if args.weak else glob[0].K      # graphs the whole job processed per step
     value = samples / (ms / 1000.0)
 
     # ---- roofline of the dominant tensor-core phase (per launch = totals / launches) ----
@@ -348,7 +366,8 @@ def main():
             ctx.schedule(wait=False)
             ctx.forward(dv["pr"], dv["x"], dv["xr"], h_out[:V])
             ctx.backward(dv["g"], dparams, dx[:dv["x"].shape[0]])
-            dp.allreduce_grads(dparams)
+            allreduce.launch()
+            allreduce.wait()
             hdp.copy_(dparams, non_blocking=True)
             torch.cuda.current_stream(dev).synchronize()
 
@@ -365,9 +384,9 @@ def main():
             tt = torch.tensor([e_ms], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e_ms = float(tt.item())
-        e2e = {"value": world * hb.K / (e_ms / 1000), "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": samples / (e_ms / 1000), "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms,
-               "note": ("cavs_train_step_host" if world == 1 else "copies + step + NCCL all-reduce") +
+               "note": ("cavs_train_step_host" if world == 1 else "copies + step + bucketed NCCL all-reduce") +
                        ": pinned host CSR/params/x/x_row/Gamma -> device, schedule, fwd, bwd, "
                        "dparams -> host, synchronised each step (host wall clock, max over ranks)"}
 
@@ -383,13 +402,14 @@ def main():
                            "train samples/s (fwd+bwd)", "inference samples/s (fwd only)" if args.inference else
                            "train samples/s (fwd+bwd)"),
             "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": args.precision, "data": "synthetic",
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
+            "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
             "config": {"workload": f"{args.config}: {_desc(args.config, b0.h)}", "h": b0.h, "d": b0.d,
-                       "batch_per_gpu": b0.K, "global_batch": samples, "precision": args.precision,
+                       "batch_per_gpu": float(np.mean([b.K for b in batches])), "global_batch": samples,
+                       "precision": args.precision,
                        "batch_pool": args.pool, "l2_flush": not args.no_flush, "parallelism": f"dp{world}",
                        "mean_vertices": float(np.mean([b.V for b in batches])),
-                       "mean_levels_T": None},
+                       "mean_levels_T": depth_T},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -182,6 +182,14 @@ cavs_status cavs_train_step_host(cavs_ctx* ctx, int32_t K, int32_t V, int32_t E,
                                  const float* x, const int32_t* x_row, const float* dh_out,
                                  float* dparams, float* dx, float* h_out);
 
+/* Data-parallel overlap hook (SURVEY §8(e) "Overlap"): `cuda_event` (a cudaEvent_t created by the
+ * caller, or NULL to clear) is recorded on the context's stream by every later cavs_backward as soon
+ * as all WEIGHT blocks of dparams (W, U_iou, U_f / W_c, W_x) are final -- right after the lazily
+ * batched weight-gradient GEMMs, before dX and db -- so a caller can start the all-reduce
+ * of those blocks on another stream while the rest of the backward runs.  The bias block is final
+ * when cavs_backward's work completes.  The event stays owned by the caller.  Errors: CAVS_E_INVALID. */
+cavs_status cavs_set_grad_event(cavs_ctx* ctx, void* cuda_event);
+
 /* Wait for all work enqueued on the context's stream and report the deferred device-side input
  * errors of the calls since the last cavs_schedule: CAVS_E_INVALID if a forward met an x_row
  * entry outside [-1, n_x).  CAVS_E_CUDA on a CUDA error.  cavs_train_step_host does this itself. */

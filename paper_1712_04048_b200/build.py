@@ -16,8 +16,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 INCLUDE = os.path.join(ROOT, "include")
-OBJ = os.path.join(HERE, "build")
-LIB = os.path.join(HERE, "libcavs.so")
+# A/B variants (tools/ab_libs.sh): CAVS_BUILD_DEFS="-DNAME ..." builds into build-<tag>/ and
+# ab_libs/<tag>.so instead of the in-tree library (CAVS_BUILD_TAG names the variant).
+_TAG = os.environ.get("CAVS_BUILD_TAG")
+OBJ = os.path.join(HERE, "build" if not _TAG else "build-" + _TAG)
+LIB = os.path.join(HERE, "libcavs.so") if not _TAG else os.path.join(ROOT, "ab_libs", _TAG + ".so")
+DEFS = os.environ.get("CAVS_BUILD_DEFS", "").split() if _TAG else []
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
@@ -41,6 +45,7 @@ def _deps_mtime() -> float:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     srcs = sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
     dep = _deps_mtime()
     jobs = []
@@ -50,7 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(OBJ, f[:-3] + ".o")
         objs.append(obj)
         if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(dep, os.path.getmtime(src)):
-            cmd = [nvcc(), *ARCH, *FLAGS, "-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj]
+            cmd = [nvcc(), *ARCH, *FLAGS, *DEFS, "-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj]
             jobs.append(cmd)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         for cmd, r in zip(jobs, ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), jobs)):

@@ -56,6 +56,7 @@ def _load():
         "cavs_train_step_host": (S, [P, I32, I32, I32, P, P, P, P, I32, P, P, P, P, P, P]),
         "cavs_kernel_launches": (I64, [P]),
         "cavs_sync": (S, [P]),
+        "cavs_set_grad_event": (S, [P, P]),
         "cavs_last_error": (ctypes.c_char_p, [P]),
         "cavs_path_info": (ctypes.c_char_p, [P]),
         "cavs_profile": (S, [P, ctypes.c_int]),
@@ -75,7 +76,7 @@ def _load():
 _lib = _load()
 EXPORTS = ["cavs_param_count", "cavs_create", "cavs_set_stream", "cavs_workspace_bytes",
            "cavs_set_workspace", "cavs_load_graphs", "cavs_schedule", "cavs_get_schedule",
-           "cavs_forward", "cavs_forward_inference", "cavs_backward", "cavs_train_step_host", "cavs_kernel_launches", "cavs_sync",
+           "cavs_forward", "cavs_forward_inference", "cavs_backward", "cavs_train_step_host", "cavs_kernel_launches", "cavs_sync", "cavs_set_grad_event",
            "cavs_last_error", "cavs_path_info", "cavs_destroy", "cavs_profile", "cavs_profile_read"]
 PHASES = ["schedule", "prep", "xproj", "fwd_levels", "bwd_roots", "bwd_levels", "lazy", "dx", "reduce"]
 
@@ -241,6 +242,16 @@ class Context:
         self._check(_lib.cavs_backward(self._ctx, _ptr(dh_out, "f32", dv), _ptr(dparams, "f32", dv),
                                        _ptr(dx, "f32", dv)))
         return dparams, dx
+
+    def set_grad_event(self, event):
+        """cavs_set_grad_event: `event` (torch.cuda.Event or None) is recorded by every later backward
+        once the weight blocks of dparams are final (before dX and db)."""
+        self._grad_event = event
+        ptr = None
+        if event is not None:
+            event.record(self.stream)                    # materialise the cudaEvent_t
+            ptr = event.cuda_event
+        self._check(_lib.cavs_set_grad_event(self._ctx, ptr))
 
     def sync(self):
         """Wait for the context's stream; raises on deferred device-side input errors (cavs_sync)."""

@@ -37,6 +37,7 @@ struct cavs_ctx {
   int *s_xrow = nullptr, *s_gp = nullptr, *s_cp = nullptr, *s_ci = nullptr;
   TcState* tc = nullptr;        // tensor-core (BF16) path state: TMA descriptors
   cudaEvent_t ev_hdr = nullptr; // recorded after the schedule header's device->host copy
+  cudaEvent_t ev_wgrad = nullptr;   // caller's event: recorded once dparams' weight blocks are final
   bool hdr_pending = false;     // header copied asynchronously, not parsed yet
 };
 
@@ -378,7 +379,7 @@ CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dp
   P.mark(CAVS_PH_BWD_LEVELS, ctx->stream);
   int split[3] = {1, 1, 1};
   if (D.prec == CAVS_BF16) {
-    tc_backward(D, ctx->tc, ctx->lp, ctx->stream, split, P);
+    tc_backward(D, ctx->tc, ctx->lp, ctx->stream, split, P, ctx->ev_wgrad);
   } else {
     simt_backward<float>(D, ctx->lp, ctx->stream, P);
   }
@@ -386,6 +387,7 @@ CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dp
   if (split[0] >= 0) {                         // split-K slots of the fallback lazy GEMMs -> dparams
     launch_pack(D, split, ctx->stream);
     P.count(1);
+    if (ctx->ev_wgrad) CK(cudaEventRecord(ctx->ev_wgrad, ctx->stream));
   }
   launch_colsum(D, ctx->lazy_db, ctx->stream);  // db -> dparams
   P.count(1);
@@ -423,6 +425,12 @@ CAVS_API cavs_status cavs_train_step_host(cavs_ctx* ctx, int32_t K, int32_t V, i
   if (dx && n_x) CK(cudaMemcpyAsync(dx, ctx->s_dx, sizeof(float) * n_x * d.d, cudaMemcpyDeviceToHost, s));
   if (h_out) CK(cudaMemcpyAsync(h_out, ctx->s_hout, sizeof(float) * V * d.h, cudaMemcpyDeviceToHost, s));
   return cavs_sync(ctx);
+}
+
+CAVS_API cavs_status cavs_set_grad_event(cavs_ctx* ctx, void* cuda_event) {
+  if (!ctx) return CAVS_E_INVALID;
+  ctx->ev_wgrad = static_cast<cudaEvent_t>(cuda_event);
+  return CAVS_OK;
 }
 
 CAVS_API cavs_status cavs_sync(cavs_ctx* ctx) {

@@ -42,7 +42,7 @@ constexpr int kBProd = 3;
 constexpr int kBMma = 3;
 constexpr int kBEpi0 = 4;
 constexpr int kBKb = 16384;        // one resident weight k-block: 128 rows x 64 bf16 (SW128)
-constexpr int kBMaxS = 12;
+constexpr int kBMaxS = 16;
 constexpr int kBKS = 4;            // K-slices per unit block
 
 struct BPlan {
@@ -177,6 +177,7 @@ k_pbwd(const __grid_constant__ CUtensorMap ma_iou, const __grid_constant__ CUten
           while (gate_get(gate) < i) { }              // task V_t+1 done cluster-wide (acquire)
           ptx::fence_proxy_async_global();            // its dZ writes -> this thread's TMA reads
         }
+        if (D.trace && w == 0) ptrace(D, 7200, blockIdx.x, i, gtime(), 0, 0, 0, 0);
         for (int j = 0; j < ntile; ++j) {
           const int p0 = lo + j * nt;
           for (int sg = 0; sg < 1 + NM; ++sg) {
@@ -218,6 +219,7 @@ k_pbwd(const __grid_constant__ CUtensorMap ma_iou, const __grid_constant__ CUten
       cl_rows(D, t, r, lo, M);
       const int nix = nt_index(M, 1, P.max_ni), nt = 16 << nix;
       const int ntile = (M + nt - 1) / nt;
+      const unsigned long long tm0 = D.trace ? gtime() : 0;
       for (int j = 0; j < ntile; ++j, ++tcount) {
         if (tcount > 0) { pwait_warp(tmem_empty, (tcount - 1) & 1); ptx::tc_fence_after(); }
         if (nix == 0) bmma_tile<16, NM>(ni, nf, P.kbb, S, stage16, acc0, b_lo, full, empty, step);
@@ -226,6 +228,7 @@ k_pbwd(const __grid_constant__ CUtensorMap ma_iou, const __grid_constant__ CUten
         if (ptx::elect_one()) ptx::mma_commit(done);
         __syncwarp();
       }
+      if (D.trace && ntile > 0 && lane == 0) ptrace(D, 7100, blockIdx.x, i, tm0, gtime(), nt, 0, 0);
     }
     __syncwarp();
   } else {
@@ -251,6 +254,8 @@ k_pbwd(const __grid_constant__ CUtensorMap ma_iou, const __grid_constant__ CUten
         if (lane == 0) while (gate_get(gate) < i) { }
         __syncwarp();
       }
+      unsigned long long tr[6] = {0, 0, 0, 0, 0, 0};
+      if (D.trace) tr[0] = gtime();
       for (int jt = 0; jt < ntile; ++jt, ++tcount) {
         const int p0 = lo + jt * nt;
         const int valid = min(nt, lo + M - p0);
@@ -266,6 +271,7 @@ k_pbwd(const __grid_constant__ CUtensorMap ma_iou, const __grid_constant__ CUten
         if (et == 0) ptx::mbar_arrive_expect_tx(rfull, (uint32_t)(kBKS * NM * nt * 32 * 4));
         pwait_warp(done, tcount & 1);
         ptx::tc_fence_after();
+        if (D.trace && jt == 0) tr[1] = gtime();
         if (tcount > 0) pwait_warp(rfree, (tcount - 1) & 1);   // receivers consumed the last tile
         // ---- partials of output units [32 q, +32) -> CTA (ub, q): P_k = acc_iou + acc_k ----
         const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)P.acc0;
@@ -291,7 +297,9 @@ k_pbwd(const __grid_constant__ CUtensorMap ma_iou, const __grid_constant__ CUten
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(tmem_empty);
         // ---- the four K-slices' partials of this CTA's units -> fused child dF ----
+        if (D.trace && jt == 0) tr[2] = gtime();
         pwait_warp(rfull, tcount & 1);
+        if (D.trace && jt == 0) tr[3] = gtime();
 #pragma unroll 1
         while (base < items) {
           const int col = base / 8;
@@ -316,6 +324,7 @@ k_pbwd(const __grid_constant__ CUtensorMap ma_iou, const __grid_constant__ CUten
         }
         ptx::named_bar_sync(1, 256);                  // recv consumed by every epilogue thread
         if (et < kBKS) cluster_arrive(rfree, ub * kBKS + et);   // release: the senders may overwrite
+        if (D.trace) tr[4] = gtime();
       }
       if (i + 1 < nlev) {                             // V_t complete cluster-wide before V_t-1
         ptx::named_bar_sync(1, 256);
@@ -327,6 +336,12 @@ k_pbwd(const __grid_constant__ CUtensorMap ma_iou, const __grid_constant__ CUten
           }
           if (et == 0) gate_set(gate, i + 1);
         }
+      }
+      if (D.trace && et == 0 && ntile > 0)
+      {
+        ptrace(D, 7000, blockIdx.x, (unsigned long long)i | ((unsigned long long)M << 16), tr[0], tr[1], tr[2], tr[3],
+               tr[4]);
+        ptrace(D, 7001, blockIdx.x, i, gtime(), 0, 0, 0, 0);
       }
     }
   }
@@ -394,8 +409,11 @@ static int pbwd_attr_clusters(const BPlan& P) {
 }
 
 PbwdState* pbwd_init(const Dev& D, int max_vertices, int* clusters, std::string* why) {
+  // Opt-in (CAVS_PBWD=1): measured on B200 at cfg4 it issues 4x fewer MMAs than the gate-grouped
+  // backward but the per-tile DSMEM exchange costs more than the MMA issue it saves (bwd levels
+  // 293 vs 252 us, profiles/r02_ablations.md), so the gate-grouped kernel stays the default.
   const char* env = std::getenv("CAVS_PBWD");
-  if (env && env[0] == '0') { *why = "disabled (CAVS_PBWD=0)"; return nullptr; }
+  if (!env || env[0] != '1') { *why = "off (opt-in: CAVS_PBWD=1)"; return nullptr; }
   const int h = D.h, N = D.N;
   if (D.cell != CAVS_CELL_TREE_LSTM || h % 128 || h < 128 || h > 512) {
     *why = "needs Tree-LSTM with h % 128 == 0, 128 <= h <= 512";
@@ -428,7 +446,9 @@ PbwdState* pbwd_init(const Dev& D, int max_vertices, int* clusters, std::string*
   P.stage = P.kbb * 64 * 128;
   const int smem_total = 232448 - 1024 - (2 * kBMaxS + 8) * 8 - 64 - 64;
   P.max_ni = -1;
-  for (int ix = 2; ix >= 0 && P.max_ni < 0; --ix) {
+  const char* mx = std::getenv("CAVS_PBWD_MAXNT");     // A/B: cap the task tile (16 / 32 / 64)
+  const int ix_cap = mx ? (std::atoi(mx) <= 16 ? 0 : std::atoi(mx) <= 32 ? 1 : 2) : 2;
+  for (int ix = ix_cap; ix >= 0 && P.max_ni < 0; --ix) {
     const int nt = 16 << ix;
     if (P.acc0 + (1 + N) * nt > 512) continue;
     const int recv = kBKS * N * nt * 32 * 4;

@@ -14,11 +14,19 @@ __device__ __forceinline__ void pwait(uint64_t* bar, uint32_t parity) {
   unsigned long long t0 = 0;
   for (;;) {
     uint32_t ok;
+#ifdef CAVS_PWAIT_SPIN
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred P;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
         "selp.b32 %0, 1, 0, P;\n\t}"
         : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+#endif
     if (ok) return;
     const unsigned long long now = gtime();
     if (t0 == 0) t0 = now;
@@ -58,7 +66,11 @@ __device__ __forceinline__ void cluster_wait(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred P;\n\t"
+#ifdef CAVS_PWAIT_SPIN
+        "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
+#else
         "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
+#endif
         "selp.b32 %0, 1, 0, P;\n\t}"
         : "=r"(ok) : "r"(a), "r"(parity) : "memory");
     if (ok) return;

@@ -779,7 +779,8 @@ static int launch_II(const CUtensorMap& a, const CUtensorMap& b, const Dev& D, P
   return P.split;
 }
 
-void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, int* split, Prof& P) {
+void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, int* split, Prof& P,
+                 cudaEvent_t wgrad_ev) {
   const int skmax = skinny_max(D);
   split[0] = split[1] = split[2] = 1;
   if (t->use_simt) { simt_backward<__nv_bfloat16>(D, lp, s, P); return; }
@@ -826,6 +827,7 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
   if (lazy_grads(D, t->ls, s)) {                      // every dU / dW block straight into dparams
     P.count(1);
     split[0] = -1;
+    if (wgrad_ev) cudaEventRecord(wgrad_ev, s);        // the weight blocks can be all-reduced from here on
   } else if (lstm) {
     PlanII A{};                                         // dU_iou = sum_k dZ_iou^T H_k  (h~ by linearity)
     A.nseg = N;

@@ -12,7 +12,10 @@ struct TcState;
 cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* err);
 // Launches are counted into P; phase marks XPROJ -> FWD_LEVELS and BWD_LEVELS -> LAZY -> DX.
 void tc_forward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, Prof& P);
-void tc_backward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, int* split /*[3]*/, Prof& P);
+// wgrad_ev (nullable): recorded on s once the lazy GEMMs wrote every weight block of dparams
+// (stream-K path; otherwise the caller records it after the split-K pack).
+void tc_backward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, int* split /*[3]*/, Prof& P,
+                 cudaEvent_t wgrad_ev = nullptr);
 void tc_destroy(TcState* tc);
 std::string tc_describe(const TcState* tc);   // which level-kernel path is active
 int tc_clusters(const TcState* tc);           // graph-range clusters of the persistent level kernels (0: none)

@@ -77,3 +77,55 @@ def test_gloo_allreduce_equals_full_batch_gradient():
     _, full, _, _ = oracle.run(_batch())
     for r in range(world):
         np.testing.assert_allclose(out[r], full, rtol=1e-10, atol=1e-12)
+
+
+def test_graph_depths_match_the_oracle_levels():
+    b = _batch()
+    lv = oracle.levels_recursive(oracle.global_children(b.graph_ptr, b.child_ptr, b.child_idx))
+    want = [int(lv[b.graph_ptr[k]:b.graph_ptr[k + 1]].max()) + 1 for k in range(b.K)]
+    assert dp.graph_depths(b.graph_ptr, b.child_ptr, b.child_idx) == want
+
+
+def test_shard_batch_covers_the_global_batch():
+    """Strong scaling: the shards of ONE global batch are disjoint, cover every graph,
+    and each is a self-contained batch whose oracle outputs equal the full batch's rows."""
+    b = _batch()
+    ho, _, _, _ = oracle.run(b, with_backward=False)
+    seen = []
+    for world in (3, 4):
+        seen = []
+        for r in range(world):
+            sb, mine = dp.shard_batch(b, world, r)
+            seen += mine
+            hs, _, _, _ = oracle.run(sb, with_backward=False)
+            rows = np.concatenate([np.arange(b.graph_ptr[k], b.graph_ptr[k + 1]) for k in mine])
+            np.testing.assert_array_equal(hs, ho[rows])
+        assert sorted(seen) == list(range(b.K))
+
+
+def _worker_bucketed(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b = _batch()
+    sb, _ = dp.shard_batch(b, world, rank)
+    _, dparams, _, _ = oracle.run(sb)
+    g = torch.from_numpy(dparams)
+    ar = dp.BucketedAllReduce(None, g, dp.bias_floats(b.cell, b.N, b.h))
+    ar.launch()
+    ar.wait()
+    out[rank] = g.numpy().copy()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gloo_bucketed_allreduce_4_uneven_ranks():
+    """world_size 4 over 9 graphs (uneven shards): the two-bucket all-reduce of the sharded
+    gradients equals the single-process full-batch gradient (graphs independent)."""
+    world = 4
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_bucketed, args=(world, _free_port(), out), nprocs=world, join=True)
+    _, full, _, _ = oracle.run(_batch())
+    for r in range(world):
+        np.testing.assert_allclose(out[r], full, rtol=1e-10, atol=1e-12)

@@ -467,8 +467,8 @@ KSPLIT_CASES = ["lstm_n2_h512_sst", "lstm_n1_h256_wide", "lstm_n3_h128", "lstm_n
 
 @pytest.mark.parametrize("case", KSPLIT_CASES)
 def test_ksplit_backward(case, monkeypatch):
-    """The K-split Tree-LSTM backward (persist_bwd.cu: 4 K-slices per 128-unit block, partials
-    reduced over DSMEM in fixed order) against the gate-grouped persistent backward (CAVS_PBWD=0):
+    """The opt-in K-split Tree-LSTM backward (CAVS_PBWD=1, persist_bwd.cu: 4 K-slices per 128-unit
+    block, partials reduced over DSMEM in fixed order) against the default gate-grouped backward:
     same bf16 operands and rounding points, another fp32 summation order; bit-identical when the
     same context runs the same batch twice."""
     b = PERSIST_CASES[case]()
@@ -478,7 +478,7 @@ def test_ksplit_backward(case, monkeypatch):
     g2 = run_gpu(b, "bf16", ctx=g["ctx"])
     assert np.array_equal(g["dparams"], g2["dparams"]) and np.array_equal(g["dx"], g2["dx"]), \
         "K-split backward not deterministic"
-    monkeypatch.setenv("CAVS_PBWD", "0")
+    monkeypatch.delenv("CAVS_PBWD")
     o = run_gpu(b, "bf16")
     assert "bwd K-split" not in o["ctx"].path_info()
     assert np.array_equal(g["h_out"], o["h_out"])          # same forward kernel
@@ -488,7 +488,7 @@ def test_ksplit_backward(case, monkeypatch):
 def test_persistent_path_is_default_for_benchmark_shape():
     b = gen.make_batch("tree_lstm", 2, 512, 512, "sst_tree", 4, seed=1)
     ctx = make_ctx(b, "bf16")
-    assert "levels: persistent" in ctx.path_info() and "bwd K-split" in ctx.path_info(), ctx.path_info()
+    assert "levels: persistent" in ctx.path_info() and "bwd gate-grouped" in ctx.path_info(), ctx.path_info()
 
 
 # ------------------------------------------------------------------ stream-K lazy gradients

@@ -78,3 +78,21 @@ for kind in sorted(set(int(k) for k in rec[:, 0] if 6000 <= k < 7000)):
         r = R6[R6[:, 2] == i]
         print(f"  i={i:3d} | {((r[:, 4] - r[:, 3]).max()) / 1e3:6.2f} | {((r[:, 5] - r[:, 3]).max()) / 1e3:6.2f} | "
               f"{((r[:, 6] - r[:, 3]).max()) / 1e3:6.2f}")
+
+# per-CTA durations (mean / max over CTAs) of the epilogue records: start->first done | done->epi end |
+# epi end->barrier out | barrier out->next start
+for kind in sorted(set(int(k) for k in rec[:, 0] if 2000 <= k < 3000)):
+    R = rec[rec[:, 0] == kind]
+    print(f"== per-CTA durations {kind}: M | start->done | done->epi end | epi end->barrier out | barrier out->next start")
+    nxt = {}
+    for c in set(R[:, 1].tolist()):
+        rows = R[R[:, 1] == c]
+        rows = rows[np.argsort(rows[:, 2])]
+        for a, b2 in zip(rows[:-1], rows[1:]):
+            nxt[(c, int(a[2]))] = int(b2[3])
+    for i in sorted(set(R[:, 2].tolist())):
+        r = R[R[:, 2] == i]
+        cols = [[(x[4] - x[3]) / 1e3 for x in r if x[4] > 0], [(x[5] - x[4]) / 1e3 for x in r if x[4] > 0],
+                [(x[6] - x[5]) / 1e3 for x in r], [(nxt[(int(x[1]), i)] - x[6]) / 1e3 for x in r if (int(x[1]), i) in nxt]]
+        txt = " | ".join(f"{np.mean(c):5.2f} {np.max(c):5.2f}" if len(c) else "  -  " for c in cols)
+        print(f"  i={i:3d} M={int(r[:, 7].max()):5d} n={len(r):3d} | {txt}")
