@@ -52,8 +52,9 @@ typedef enum cavs_status {
   CAVS_E_INVALID = 1,     /* bad argument / malformed graph (K<1, empty graph, id out of range, sizes) */
   CAVS_E_ARITY = 2,       /* a vertex has more than N children */
   CAVS_E_CYCLE = 3,       /* G is not a DAG: some vertex is never activated */
-  CAVS_E_FANOUT = 4,      /* a vertex has more than one parent: DAG fan-out is not supported
-                             in this version (forests only) */
+  CAVS_E_FANOUT = 4,      /* reserved (round 1: fan-out rejected).  DAG inputs -- a vertex with
+                             several parents, or a child listed twice -- are accepted since
+                             round 2 (NEXT-3); this code is no longer returned */
   CAVS_E_STATE = 5,       /* call out of order (e.g. backward before forward) */
   CAVS_E_CAPACITY = 6,    /* batch exceeds the context's max_* or the workspace is too small */
   CAVS_E_CUDA = 7,        /* a CUDA runtime/driver error; see cavs_last_error */
@@ -108,7 +109,12 @@ cavs_status cavs_set_workspace(cavs_ctx* ctx, void* dev, size_t bytes);
  * ("reads training samples and their associated graphs", §4).
  *   graph_ptr [K+1]: global vertex offsets, graph_ptr[0] = 0, graph_ptr[K] = V
  *   child_ptr [V+1]: CSR row pointers over global vertices, child_ptr[V] = E
- *   child_idx [E]  : children as INSTANCE-LOCAL ids (0 .. n_k-1); row order = gather index k
+ *   child_idx [E]  : children as INSTANCE-LOCAL ids (0 .. n_k-1); row order = gather index k.
+ *                    A vertex may be the child of several parents and may appear twice in one
+ *                    row (DAG inputs): its h / c are then gathered into every slot
+ *                    that lists it and the gradients of all those slots are ADDED in a
+ *                    fixed order (ascending parent position, then slot), so results are
+ *                    deterministic.  E <= N * max_vertices.
  * `on_device` != 0: the three arrays are device pointers, read (and copied into the
  * workspace) by the first kernel of the next cavs_schedule — keep them alive and unmodified
  * until that kernel ran (stream order), i.e. until any later call on the stream completes.
@@ -129,8 +135,10 @@ cavs_status cavs_load_graphs(cavs_ctx* ctx, int32_t K, int32_t V, int32_t E,
  * validation errors here.  T_out == NULL: returns after enqueueing; the validation errors
  * are then returned by the next cavs_forward / cavs_get_schedule (which consume the header)
  * and the context falls back to LOADED.
- * Errors: CAVS_E_STATE (nothing loaded), CAVS_E_INVALID, CAVS_E_ARITY, CAVS_E_CYCLE,
- *         CAVS_E_FANOUT, CAVS_E_CUDA. */
+ * A batch with fan-out anywhere runs the DAG path: per-task gather in the forward and a
+ * pull-reduce over a parent CSR before each task's dF in the backward (the fused tree path,
+ * where each child's dF runs inside its unique parent's epilogue, needs a single parent).
+ * Errors: CAVS_E_STATE (nothing loaded), CAVS_E_INVALID, CAVS_E_ARITY, CAVS_E_CYCLE, CAVS_E_CUDA. */
 cavs_status cavs_schedule(cavs_ctx* ctx, int32_t* T_out);
 
 /* Copy the schedule into HOST buffers (any may be NULL):

@@ -74,7 +74,7 @@ static size_t carve(cavs_ctx* c, char* base) {
   Dev& D = c->D;
   auto I = [&](size_t n) { return reinterpret_cast<int*>(take(n * 4)); };
   auto F = [&](size_t n) { return reinterpret_cast<float*>(take(n * 4)); };
-  D.graph_ptr = I(K + 1); D.child_ptr = I(V + 1); D.child_idx = I(V + 1);
+  D.graph_ptr = I(K + 1); D.child_ptr = I(V + 1); D.child_idx = I(N * V + 1);   // DAGs: up to N V edges
   D.level = I(V); D.pos = I(V); D.graph_of = I(V); D.parent_v = I(V); D.slot_v = I(V);
   D.pending = I(V); D.queue = I(V);
   D.hdr = I(kHdrWords + V + 1); D.level_ptr = base ? D.hdr + kHdrWords : nullptr;
@@ -101,6 +101,8 @@ static size_t carve(cavs_ctx* c, char* base) {
     D.Wa = take(2 * h * h * es); D.Wb = take(h * dd * es); D.Wc = take(2 * h * h * es);
     D.Wd = nullptr; D.We = take(dd * h * es);
   }
+  D.pptr = I(V + 1); D.pent = I(N * V + 1); D.pcur = I(V);          // DAG parent CSR (NEXT-3)
+  D.dHg = F(Vp * N * h); D.dCg = is_lstm(d) ? F(Vp * N * h) : nullptr;
   D.lazy = F(lazy_floats(D));
   c->lazy_db = F((size_t)kDbChunks * d.N * 4 * h);   // db partials [(slot, chunk)][logical column]
   const size_t P = cavs_param_count(d.cell, d.N, d.h, d.d);
@@ -186,7 +188,7 @@ CAVS_API cavs_status cavs_load_graphs(cavs_ctx* ctx, int32_t K, int32_t V, int32
   if (ctx->state < S_READY) return fail(ctx, CAVS_E_STATE, "set_workspace first");
   if (K < 1 || V < 1 || E < 0 || !graph_ptr || !child_ptr || (E > 0 && !child_idx))
     return fail(ctx, CAVS_E_INVALID, "bad sizes or null pointers");
-  if (K > ctx->desc.max_graphs || V > ctx->desc.max_vertices || E > ctx->desc.max_vertices)
+  if (K > ctx->desc.max_graphs || V > ctx->desc.max_vertices || (int64_t)E > (int64_t)ctx->desc.N * ctx->desc.max_vertices)
     return fail(ctx, CAVS_E_CAPACITY, "batch exceeds context capacity");
   CK(cudaSetDevice(ctx->device));
   Dev& D = ctx->D;
@@ -217,11 +219,15 @@ static cavs_status finish_schedule(cavs_ctx* ctx) {
     ctx->state = S_LOADED;
     if (st & ST_INVALID) return fail(ctx, CAVS_E_INVALID, "malformed graph (range/shape)");
     if (st & ST_ARITY) return fail(ctx, CAVS_E_ARITY, "a vertex has more than N children");
-    if (st & ST_FANOUT) return fail(ctx, CAVS_E_FANOUT, "a vertex has more than one parent");
     return fail(ctx, CAVS_E_CYCLE, "input graph has a cycle");
   }
   const int T = ctx->h_hdr[1];
   ctx->T = T;
+  D.dag = (ctx->h_hdr[3] & ST_DAG) ? 1 : 0;          // fan-out somewhere in the batch (NEXT-3)
+  if (D.dag) {
+    launch_dag_parents(D, ctx->stream);
+    ctx->prof.count(4);
+  }
   ctx->n_roots = ctx->h_hdr[2];
   ctx->lp.assign(T + 1, 0);
   if (T + 1 <= nread - kHdrWords) {
@@ -333,7 +339,7 @@ static cavs_status forward_impl(cavs_ctx* ctx, const float* params, int32_t n_x,
   CK(cudaSetDevice(ctx->device));
   Dev& D = ctx->D;
   D.params = params; D.x = x; D.x_row = x_row; D.h_out = h_out; D.n_x = n_x;
-  D.infer = infer ? 1 : 0;
+  D.infer = infer ? 1 : 0;                 // (a DAG batch gathers c from the leaves' saved state: see below)
   Prof& P = ctx->prof;
   P.mark(CAVS_PH_PREP, ctx->stream);
   launch_prep(D, ctx->stream);
@@ -343,6 +349,7 @@ static cavs_status forward_impl(cavs_ctx* ctx, const float* params, int32_t n_x,
     const cavs_status st = finish_schedule(ctx);
     if (st) return st;
   }
+  if (D.dag) D.infer = 0;                  // the per-task gather reads every child's saved c
   P.mark(CAVS_PH_XPROJ, ctx->stream);
   if (D.prec == CAVS_BF16) tc_forward(D, ctx->tc, ctx->lp, ctx->stream, P);
   else simt_forward<float>(D, ctx->lp, ctx->stream, P);
@@ -374,8 +381,10 @@ CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dp
   Prof& P = ctx->prof;
   if (dx && D.n_x > 0) CK(cudaMemsetAsync(dx, 0, sizeof(float) * (size_t)D.n_x * D.d, ctx->stream));   // dx is accumulated
   P.mark(CAVS_PH_BWD_ROOTS, ctx->stream);
-  launch_roots(D, ctx->n_roots, D.roots, ctx->stream);
-  P.count(1);
+  if (!D.dag) {                                // DAG batches: every vertex's dF runs in launch_dag_df
+    launch_roots(D, ctx->n_roots, D.roots, ctx->stream);
+    P.count(1);
+  }
   P.mark(CAVS_PH_BWD_LEVELS, ctx->stream);
   int split[3] = {1, 1, 1};
   if (D.prec == CAVS_BF16) {

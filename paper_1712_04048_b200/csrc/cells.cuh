@@ -366,6 +366,48 @@ template <> struct EpiK<EPI_FC_BWD> {
   }
 };
 
+// ---- DAG inputs (fan-out): the level GEMM's epilogue only sends the gradient along each edge; the
+// child's dF runs once all its parents are done (launch_dag_df: fixed-order sum over its parents).
+// Tree-LSTM at parent p, slot k: dL/dh_k = U_iou^T dz_iou + U_f^T dz_fk, dL/dc_k = dc-bar * f_k.
+template <> struct EpiK<EPI_LSTM_BWD_DAG> {
+  template <int VW, int NM = kMaxN> struct In { FV<VW> dcbp; FV<VW> fp[NM]; };
+  template <int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void load(const Dev& D, int j, const VMeta& m, In<VW, NM>& in) {
+    const int h = D.h, N = D.N;
+    in.dcbp = ldv<VW>(D.dcb + (size_t)m.p * h + j);
+    const float* g = D.gates + (size_t)m.p * (3 + N) * h + j;
+#pragma unroll
+    for (int k = 0; k < NM; ++k) in.fp[k] = k < m.deg ? ldv<VW>(g + (3 + k) * h) : zerov<VW>();
+  }
+  template <class OpT, int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const FV<VW>* acc,
+                                               const In<VW, NM>& in, const UnitC<VW>&) {
+    const int h = D.h, N = D.N;
+#pragma unroll
+    for (int k = 0; k < NM; ++k) {
+      if (k >= m.deg) break;
+      FV<VW> dh, dc;
+#pragma unroll
+      for (int e = 0; e < VW; ++e) { dh.v[e] = acc[0].v[e] + acc[1 + k].v[e]; dc.v[e] = in.dcbp.v[e] * in.fp[k].v[e]; }
+      const size_t at = ((size_t)m.p * N + k) * h + j;
+      stv<VW>(D.dHg + at, dh);
+      stv<VW>(D.dCg + at, dc);
+    }
+  }
+};
+// Tree-FC at parent p: dL/dh_k = W_k^T dz (acc[k]).
+template <> struct EpiK<EPI_FC_BWD_DAG> {
+  template <int VW, int NM = kMaxN> struct In {};
+  template <int VW, int NM = kMaxN> static __device__ __forceinline__ void load(const Dev&, int, const VMeta&, In<VW, NM>&) {}
+  template <class OpT, int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const FV<VW>* acc,
+                                               const In<VW, NM>&, const UnitC<VW>&) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (k < m.deg) stv<VW>(D.dHg + ((size_t)m.p * 2 + k) * D.h + j, acc[k]);
+  }
+};
+
 // pull's adjoint: dx[record] += W^T dz.  ADDED, not stored: several vertices may pull
 // the same record (an embedding row); dx is zeroed by cavs_backward first.  With one vertex per
 // record every element receives exactly one add onto 0 (deterministic).
@@ -390,7 +432,7 @@ template <int E> __host__ __device__ constexpr bool epi_uses_bias() {
   return E == EPI_LSTM_FWD || E == EPI_LSTM_XPROJ || E == EPI_FC_FWD || E == EPI_FC_XPROJ;
 }
 template <int E> __host__ __device__ constexpr bool epi_is_lstm() {
-  return E == EPI_LSTM_FWD || E == EPI_LSTM_XPROJ || E == EPI_LSTM_BWD;
+  return E == EPI_LSTM_FWD || E == EPI_LSTM_XPROJ || E == EPI_LSTM_BWD || E == EPI_LSTM_BWD_DAG;
 }
 
 // Does position p need this epilogue at all? (tile skipping for the x-kernels)
@@ -411,6 +453,31 @@ __device__ __forceinline__ void epilogue1(const Dev& D, int j, const VMeta& m, c
   typename EpiK<E>::template In<1, kMaxN> in;
   EpiK<E>::template load<1, kMaxN>(D, j, m, in);
   EpiK<E>::template store<OpT, 1, kMaxN>(D, j, m, a, in, uc);
+}
+
+// DAG: dF at position p once every parent sent its edge gradients (dHg / dCg at the parent-slot
+// indices pent[pptr[p] .. pptr[p+1]), ascending: a fixed summation order), plus push's adjoint.
+template <class OpT>
+__device__ __forceinline__ void dag_df(const Dev& D, int j, int p) {
+  const int vid = D.order[p];
+  const int e0 = D.pptr[p], e1 = D.pptr[p + 1];
+  if (D.cell == CAVS_CELL_TREE_LSTM) {
+    LstmChildIn<1, kMaxN> in;
+    const int deg = D.deg[p];
+    lstm_child_load<1, kMaxN>(D, j, p, vid, deg, in);
+    FV<1> dh = in.dho, dc = zerov<1>();
+    for (int e = e0; e < e1; ++e) {
+      const size_t at = (size_t)D.pent[e] * D.h + j;
+      dh.v[0] += D.dHg[at];
+      dc.v[0] += D.dCg[at];
+    }
+    lstm_child_store<OpT, 1, kMaxN>(D, j, p, deg, dh, dc, in);
+  } else {
+    float dh = D.dh_out[(size_t)vid * D.h + j];
+    for (int e = e0; e < e1; ++e) dh += D.dHg[(size_t)D.pent[e] * D.h + j];
+    const float hv = D.gates[(size_t)p * D.h + j];
+    op<OpT>(D.dZ)[(size_t)p * D.h + j] = to_op<OpT>(dh * (1.f - hv * hv));
+  }
 }
 
 // dF entry at vertices without a parent: only push's adjoint arrives (dh = Gamma, dc = 0).

@@ -15,7 +15,7 @@
 
 namespace cavs {
 
-enum : int { ST_INVALID = 1, ST_ARITY = 2, ST_CYCLE = 4, ST_FANOUT = 8, ST_XROW = 16 };
+enum : int { ST_INVALID = 1, ST_ARITY = 2, ST_CYCLE = 4, ST_FANOUT = 8, ST_XROW = 16, ST_DAG = 32 };
 
 // Device view of one context: sizes + every arena pointer.  Passed by value.
 struct Dev {
@@ -32,7 +32,7 @@ struct Dev {
   // schedule (position-indexed)
   int* order; int* level_ptr; int* child_pos; int* parent_pos; int* slot; int* deg; int* xrow_pos;
   int* tile_x;                      // per 64-position tile: 1 if any vertex has a pull record
-  int* hdr;                         // [0] status bits, [1] T, [2] #roots, [3] deferred input errors (ST_XROW), [4..] level_ptr
+  int* hdr;                         // [0] status bits, [1] T, [2] #roots, [3] ST_XROW (deferred input error) | ST_DAG, [4..] level_ptr
   int* roots;                       // positions of vertices without a parent
   int* cnt;                         // per-graph level histograms: cnt[graph_ptr[g] + t] (t < T_g)
   int* lrank;                       // rank of a vertex among the vertices of its graph and level
@@ -43,6 +43,13 @@ struct Dev {
   int ncl;                          // clusters of the persistent level kernels (0: none)
   int* crow;                        // [T][ncl + 1]: first position of task t owned by cluster >= r
   int* tile_cnt;                    // arrival counters (zero between launches): lazy tiles, then db column blocks
+  // DAG inputs (fan-out: a vertex with several parents); dag = 1 for this batch
+  int dag;
+  int* pptr;                        // [V+1] parent CSR by position: entries [pptr[p], pptr[p+1])
+  int* pent;                        // [E] parent-slot index q = parent_pos * N + k, ascending per vertex
+  int* pcur;                        // [V] fill cursors
+  float* dHg;                       // [Vp, N*h] gradient sent along edge (parent p, slot k): dL/dh_k
+  float* dCg;                       // [Vp, N*h] Tree-LSTM: dL/dc_k along the same edge
   // arenas (OpT = float in FP32 mode, __nv_bfloat16 in BF16 mode)
   void* Hk;      // [Vp, N*h] gather slots of child h (written by the child's scatter)
   void* Hs;      // [Vp, h]   child-sum h~ (Tree-LSTM, N >= 2)

@@ -14,7 +14,8 @@ constexpr int kMaxClusters = 16;     // graph-range clusters of the persistent l
 constexpr int kDbMaxBlocks = 64;      // arrival counters of the db column blocks (k_colsum)
 constexpr int kSkinnyMax = 8;     // tasks with at most this many vertices use the skinny level kernel
 
-enum Epi : int { EPI_LSTM_FWD = 0, EPI_LSTM_XPROJ, EPI_LSTM_BWD, EPI_FC_FWD, EPI_FC_XPROJ, EPI_FC_BWD, EPI_DX };
+enum Epi : int { EPI_LSTM_FWD = 0, EPI_LSTM_XPROJ, EPI_LSTM_BWD, EPI_FC_FWD, EPI_FC_XPROJ, EPI_FC_BWD, EPI_DX,
+                 EPI_LSTM_BWD_DAG, EPI_FC_BWD_DAG };
 
 enum BSrc : int { B_HK = 0, B_XP = 1, B_DZ = 2 };
 
@@ -104,5 +105,11 @@ void launch_pull(const Dev& D, cudaStream_t s);
 void launch_roots(const Dev& D, int n_roots, const int* roots, cudaStream_t s);
 void launch_colsum(const Dev& D, float* part, cudaStream_t s);   // db straight into D.dparams
 void launch_pack(const Dev& D, const int* split /*[3]*/, cudaStream_t s);   // split-K slots -> dU, dW
+// DAG inputs (D.dag): parent CSR of the schedule, the forward gather of task [lo, hi) (children's h, c
+// into the parent-slot arenas; fan-out forbids the children's scatter) and the backward pull-reduce
+// + dF of task [lo, hi) (sums the edges' gradients in parent-CSR order: deterministic)
+void launch_dag_parents(const Dev& D, cudaStream_t s);
+void launch_dag_gather(const Dev& D, int lo, int hi, cudaStream_t s);
+void launch_dag_df(const Dev& D, int lo, int hi, cudaStream_t s);
 
 }  // namespace cavs

@@ -281,6 +281,86 @@ __global__ void __launch_bounds__(256) k_pack(Dev D, PackSegs P) {
   }
 }
 
+// ---- DAG inputs (D.dag): parent CSR by position ------------------------------------------
+// count parents per child position, exclusive scan, fill, then sort every (short) list so the
+// order of the pull-reduce is fixed: ascending parent-slot index q = parent_pos * N + k.
+__global__ void k_dag_count(Dev D) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < D.V; p += gridDim.x * blockDim.x) {
+    const int deg = D.deg[p];
+    for (int k = 0; k < deg; ++k) atomicAdd(&D.pcur[D.child_pos[(size_t)p * D.N + k]], 1);
+  }
+}
+__global__ void __launch_bounds__(1024) k_dag_scan(Dev D) {   // one CTA
+  __shared__ int s_warp[32];
+  int carry = 0;
+  for (int b0 = 0; b0 < D.V; b0 += blockDim.x) {
+    const int p = b0 + threadIdx.x;
+    const int c = p < D.V ? D.pcur[p] : 0;
+    int v = c;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(~0u, v, o); if (lane >= o) v += y; }
+    if (lane == 31) s_warp[w] = v;
+    __syncthreads();
+    if (w == 0) {
+      int y = lane < nw ? s_warp[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) { const int z = __shfl_up_sync(~0u, y, o); if (lane >= o) y += z; }
+      s_warp[lane] = y;
+    }
+    __syncthreads();
+    const int excl = carry + v - c + (w ? s_warp[w - 1] : 0);
+    if (p < D.V) { D.pptr[p] = excl; D.pcur[p] = 0; }
+    carry += s_warp[nw - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) D.pptr[D.V] = carry;
+}
+__global__ void k_dag_fill(Dev D) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < D.V; p += gridDim.x * blockDim.x) {
+    const int deg = D.deg[p];
+    for (int k = 0; k < deg; ++k) {
+      const int c = D.child_pos[(size_t)p * D.N + k];
+      D.pent[D.pptr[c] + atomicAdd(&D.pcur[c], 1)] = p * D.N + k;
+    }
+  }
+}
+__global__ void k_dag_sort(Dev D) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < D.V; p += gridDim.x * blockDim.x) {
+    const int a = D.pptr[p], b = D.pptr[p + 1];
+    for (int i = a + 1; i < b; ++i) {              // insertion sort: lists are short
+      const int x = D.pent[i];
+      int j = i - 1;
+      while (j >= a && D.pent[j] > x) { D.pent[j + 1] = D.pent[j]; --j; }
+      D.pent[j + 1] = x;
+    }
+    D.pcur[p] = 0;                                 // cursors zero for the next batch
+  }
+}
+
+// Forward gather of task [lo, hi): slot k of parent p <- the child's pushed h (operand dtype) and c.
+template <class OpT>
+__global__ void k_dag_gather(Dev D, int lo, int hi) {
+  const int h = D.h, N = D.N;
+  const size_t n = (size_t)(hi - lo) * N * h;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % h);
+    const int k = (int)((i / h) % N);
+    const int p = lo + (int)(i / ((size_t)N * h));
+    if (k >= D.deg[p]) continue;                   // missing slots stay zero (k_build_maps, Z1)
+    const int c = D.child_pos[(size_t)p * N + k];
+    const size_t at = ((size_t)p * N + k) * h + j;
+    op<OpT>(D.Hk)[at] = to_op<OpT>(D.h_out[(size_t)D.order[c] * h + j]);
+    if (D.Ck) D.Ck[at] = D.cst[(size_t)c * h + j];
+  }
+}
+
+// Backward pull-reduce + dF of task [lo, hi) (cells.cuh dag_df).
+template <class OpT>
+__global__ void k_dag_df(Dev D, int lo, int hi) {
+  const size_t n = (size_t)(hi - lo) * D.h;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dag_df<OpT>(D, (int)(i % D.h), lo + (int)(i / D.h));
+}
+
 static int grid_for(size_t n, int block) { return (int)std::min<size_t>((n + block - 1) / block, 148 * 16); }
 
 void launch_prep(const Dev& D, cudaStream_t s) {
@@ -365,6 +445,28 @@ void launch_pack(const Dev& D, const int* split, cudaStream_t s) {
   }
   dim3 grid(std::min(148, cdiv(maxlen, 256 * 4)), P.n);
   k_pack<<<grid, 256, 0, s>>>(D, P);
+}
+
+void launch_dag_parents(const Dev& D, cudaStream_t s) {
+  const int g = grid_for(D.V, 256);
+  k_dag_count<<<g, 256, 0, s>>>(D);
+  k_dag_scan<<<1, 1024, 0, s>>>(D);
+  k_dag_fill<<<g, 256, 0, s>>>(D);
+  k_dag_sort<<<g, 256, 0, s>>>(D);
+}
+
+void launch_dag_gather(const Dev& D, int lo, int hi, cudaStream_t s) {
+  if (hi <= lo) return;
+  const size_t n = (size_t)(hi - lo) * D.N * D.h;
+  if (D.prec == CAVS_BF16) k_dag_gather<__nv_bfloat16><<<grid_for(n, 256), 256, 0, s>>>(D, lo, hi);
+  else k_dag_gather<float><<<grid_for(n, 256), 256, 0, s>>>(D, lo, hi);
+}
+
+void launch_dag_df(const Dev& D, int lo, int hi, cudaStream_t s) {
+  if (hi <= lo) return;
+  const size_t n = (size_t)(hi - lo) * D.h;
+  if (D.prec == CAVS_BF16) k_dag_df<__nv_bfloat16><<<grid_for(n, 256), 256, 0, s>>>(D, lo, hi);
+  else k_dag_df<float><<<grid_for(n, 256), 256, 0, s>>>(D, lo, hi);
 }
 
 }  // namespace cavs

@@ -77,10 +77,41 @@ __global__ void __launch_bounds__(256) k_graph_sched(Dev D) {
     if (bad) atomicOr(&s_bad, bad);
   }
   __syncthreads();
-  if (s_bad) {
+  const bool dag = s_bad == ST_FANOUT;               // fan-out only: a DAG (NEXT-3), not an error
+  if (s_bad && !dag) {
     if (threadIdx.x == 0) atomicOr(st, s_bad);
     return;
   }
+  int round = 0;
+  if (dag) {
+    // A vertex may have several parents, so there is no single parent to count down: level rounds
+    // by pulling instead -- in round r every unassigned vertex whose children all have levels < r
+    // gets level r (= 1 + max over its children, reading Z5); no progress with vertices left = cycle.
+    if (threadIdx.x == 0) { atomicOr(&st[3], ST_DAG); s_tail = 0; }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) lev[i] = -1;
+    __syncthreads();
+    while (true) {
+      __shared__ int s_new;
+      if (threadIdx.x == 0) s_new = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        if (lev[i] >= 0) continue;
+        const int v = lo + i;
+        bool ready = true;
+        for (int e = D.src_cp[v]; e < D.src_cp[v + 1] && ready; ++e) {
+          const int l = lev[D.src_ci[e]];
+          ready = l >= 0 && l < round;
+        }
+        if (ready) { lev[i] = round; atomicAdd(&s_new, 1); }
+      }
+      __syncthreads();
+      const int got = s_new;
+      if (threadIdx.x == 0) s_tail += got;
+      __syncthreads();
+      if (got == 0) break;
+      ++round;
+    }
+  } else {
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     if (pend[i] == 0) {
       q[atomicAdd(&s_tail, 1)] = i;
@@ -88,7 +119,6 @@ __global__ void __launch_bounds__(256) k_graph_sched(Dev D) {
     }
   }
   __syncthreads();
-  int round = 0;
   while (true) {                                     // round r activates exactly the level-r vertices
     const int qs = s_head, qe = s_tail;
     if (qs == qe) break;
@@ -104,6 +134,7 @@ __global__ void __launch_bounds__(256) k_graph_sched(Dev D) {
     if (threadIdx.x == 0) s_head = qe;
     ++round;
     __syncthreads();
+  }
   }
   if (s_tail != n) {                                 // some vertex never activated
     if (threadIdx.x == 0) atomicOr(st, ST_CYCLE);
@@ -239,7 +270,9 @@ __global__ void k_build_maps(Dev D) {
     D.deg[p] = deg;
     for (int k = 0; k < D.N; ++k)
       D.child_pos[(size_t)p * D.N + k] = k < deg ? vpos(D, lo + D.child_idx[a + k], lo) : -1;
-    const int pv = D.parent_v[v];
+    // DAG batches (fan-out anywhere): no child scatters into a parent slot (the forward gathers
+    // per task, launch_dag_gather) and the backward pulls over the parent CSR (launch_dag_df)
+    const int pv = (D.hdr[3] & ST_DAG) ? -1 : D.parent_v[v];
     D.parent_pos[p] = pv >= 0 ? vpos(D, pv, lo) : -1;
     D.slot[p] = pv >= 0 ? D.slot_v[v] : 0;
     if (pv < 0) D.roots[atomicAdd(&D.hdr[2], 1)] = p;

@@ -146,6 +146,12 @@ void simt_typeI(const Dev& D, int epi, const SegListI& L, int row_lo, int row_hi
     case EPI_FC_XPROJ: typeI<OpT, 1, EPI_FC_XPROJ>(D, L, row_lo, row_hi, units, s); break;
     case EPI_FC_FWD: typeI<OpT, 1, EPI_FC_FWD>(D, L, row_lo, row_hi, units, s); break;
     case EPI_FC_BWD: typeI<OpT, 2, EPI_FC_BWD>(D, L, row_lo, row_hi, units, s); break;
+    case EPI_LSTM_BWD_DAG:
+      if (D.N == 1) typeI<OpT, 2, EPI_LSTM_BWD_DAG>(D, L, row_lo, row_hi, units, s);
+      else if (D.N == 2) typeI<OpT, 3, EPI_LSTM_BWD_DAG>(D, L, row_lo, row_hi, units, s);
+      else typeI<OpT, 1 + kMaxN, EPI_LSTM_BWD_DAG>(D, L, row_lo, row_hi, units, s);
+      break;
+    case EPI_FC_BWD_DAG: typeI<OpT, 2, EPI_FC_BWD_DAG>(D, L, row_lo, row_hi, units, s); break;
     default: typeI<OpT, 1, EPI_DX>(D, L, row_lo, row_hi, units, s); break;
   }
 }
@@ -200,6 +206,7 @@ void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
     P.mark(CAVS_PH_FWD_LEVELS, s);
     F = fwd_segments(D);
     for (int t = 1; t < T; ++t) {
+      if (D.dag) { launch_dag_gather(D, lp[t], lp[t + 1], s); P.count(1); }
       if (lp[t + 1] - lp[t] <= skmax) skinny_typeI<OpT>(D, EPI_LSTM_FWD, F, lp[t], lp[t + 1], h, s);
       else simt_typeI<OpT>(D, EPI_LSTM_FWD, F, lp[t], lp[t + 1], h, s);
       P.count(1);
@@ -211,6 +218,7 @@ void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
     P.mark(CAVS_PH_FWD_LEVELS, s);
     F = fwd_segments(D);
     for (int t = 1; t < T; ++t) {
+      if (D.dag) { launch_dag_gather(D, lp[t], lp[t + 1], s); P.count(1); }
       if (lp[t + 1] - lp[t] <= skmax) skinny_typeI<OpT>(D, EPI_FC_FWD, F, lp[t], lp[t + 1], h, s);
       else simt_typeI<OpT>(D, EPI_FC_FWD, F, lp[t], lp[t + 1], h, s);
       P.count(1);
@@ -236,10 +244,22 @@ void simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) 
     for (int k = 0; k < 2; ++k) B.s[k] = SegI{D.Wc, h, k * h, B_DZ, 0, h, h, k};
     epi = EPI_FC_BWD;
   }
+  if (D.dag) {                      // DAG batch: pull-reduce + dF per task, then the edge gradients
+    epi = lstm ? EPI_LSTM_BWD_DAG : EPI_FC_BWD_DAG;
+    for (int t = T - 1; t >= 0; --t) {
+      launch_dag_df(D, lp[t], lp[t + 1], s);
+      P.count(1);
+      if (t == 0) break;
+      if (lp[t + 1] - lp[t] <= skmax) skinny_typeI<OpT>(D, epi, B, lp[t], lp[t + 1], h, s);
+      else simt_typeI<OpT>(D, epi, B, lp[t], lp[t + 1], h, s);
+      P.count(1);
+    }
+  } else {
   for (int t = T - 1; t >= 1; --t) {
     if (lp[t + 1] - lp[t] <= skmax) skinny_typeI<OpT>(D, epi, B, lp[t], lp[t + 1], h, s);
     else simt_typeI<OpT>(D, epi, B, lp[t], lp[t + 1], h, s);
     P.count(1);
+  }
   }
   P.mark(CAVS_PH_LAZY, s);
   // lazy batching of the parameter gradients over ALL vertices; one partial each

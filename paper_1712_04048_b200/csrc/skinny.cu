@@ -202,6 +202,12 @@ void skinny_typeI(const Dev& D, int epi, const SegListI& L, int row_lo, int row_
       break;
     case EPI_FC_FWD: sk<OpT, 1, EPI_FC_FWD>(D, L, row_lo, row_hi, units, s); break;
     case EPI_FC_BWD: sk<OpT, 2, EPI_FC_BWD>(D, L, row_lo, row_hi, units, s); break;
+    case EPI_LSTM_BWD_DAG:
+      if (D.N == 1) sk<OpT, 2, EPI_LSTM_BWD_DAG>(D, L, row_lo, row_hi, units, s);
+      else if (D.N == 2) sk<OpT, 3, EPI_LSTM_BWD_DAG>(D, L, row_lo, row_hi, units, s);
+      else sk<OpT, 1 + kMaxN, EPI_LSTM_BWD_DAG>(D, L, row_lo, row_hi, units, s);
+      break;
+    case EPI_FC_BWD_DAG: sk<OpT, 2, EPI_FC_BWD_DAG>(D, L, row_lo, row_hi, units, s); break;
     default: break;
   }
 }

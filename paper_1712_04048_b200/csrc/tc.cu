@@ -224,7 +224,7 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
     constexpr int CPT = COLS / 8;                      // columns per thread
     constexpr int CH = epi_needs_children<E>() ? 1 : (CPT < 4 ? CPT : 4);
     // children per vertex the epilogue state is sized for
-    constexpr int NM = E == EPI_LSTM_FWD ? NACC - 3 : E == EPI_LSTM_BWD ? NACC - 1 : 1;
+    constexpr int NM = E == EPI_LSTM_FWD ? NACC - 3 : (E == EPI_LSTM_BWD || E == EPI_LSTM_BWD_DAG) ? NACC - 1 : 1;
 #pragma unroll 1
     for (int i0 = 0; i0 < CPT; i0 += CH) {
       FV<4> acc[CH][NACC];
@@ -731,10 +731,11 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
       launch_level<EPI_LSTM_XPROJ, 4, 1>(t->A[1], t->A[1], t->B_xp, D, mono_lstm_xproj(h, d), 0, D.V, h, s);
     P.count(1);
     P.mark(CAVS_PH_FWD_LEVELS, s);
-    if (t->ps) { if (T > 1) { persist_forward(D, t->ps, T, s); P.count(1); } return; }
+    if (t->ps && !D.dag) { if (T > 1) { persist_forward(D, t->ps, T, s); P.count(1); } return; }
     const PlanT F = gs ? gs_lstm_fwd(h, N) : mono_lstm_fwd(h, N);
     for (int tt = 1; tt < T; ++tt) {
       const int M = lp[tt + 1] - lp[tt];
+      if (D.dag) { launch_dag_gather(D, lp[tt], lp[tt + 1], s); P.count(1); }
       if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_FWD, Fs, lp[tt], lp[tt + 1], h, s);
       else if (rows_tiles(t->rs, false, M) >= t->rows_min_tiles && rows_level(D, t->rs, false, lp[tt], lp[tt + 1], s)) {}
       else level_N<EPI_LSTM_FWD, 3>(gs, N, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
@@ -745,12 +746,13 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
       launch_level<EPI_FC_XPROJ, 1, 1>(t->A[1], t->A[1], t->B_xp, D, mono_one(d, 1, &zero, &zero), 0, D.V, h, s);
     P.count(1);
     P.mark(CAVS_PH_FWD_LEVELS, s);
-    if (t->ps) { if (T > 1) { persist_forward(D, t->ps, T, s); P.count(1); } return; }
+    if (t->ps && !D.dag) { if (T > 1) { persist_forward(D, t->ps, T, s); P.count(1); } return; }
     PlanT F;
     if (gs) { F = plan_empty(); gs_add_ksplit(F, 0, 0, 0, 0, 2 * h, 0); }
     else F = mono_one(2 * h, 1, &zero, &zero);
     for (int tt = 1; tt < T; ++tt) {
       const int M = lp[tt + 1] - lp[tt];
+      if (D.dag) { launch_dag_gather(D, lp[tt], lp[tt + 1], s); P.count(1); }
       if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_FWD, Fs, lp[tt], lp[tt + 1], h, s);
       else if (rows_tiles(t->rs, false, M) >= t->rows_min_tiles && rows_level(D, t->rs, false, lp[tt], lp[tt + 1], s)) {}
       else if (gs) launch_level<EPI_FC_FWD, 1, kCluster>(t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
@@ -791,7 +793,32 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
   const SegListI Bs = bwd_segments(D);
   // rows past V of dZ are read by the lazy GEMMs' last k-block: keep them zero
   cudaMemsetAsync(reinterpret_cast<__nv_bfloat16*>(D.dZ) + (size_t)D.V * G * h, 0, (size_t)64 * G * h * 2, s);
-  if (t->ps) {
+  if (D.dag) {
+    // DAG batch (NEXT-3): per task, the pull-reduce + dF of its vertices (every parent is in a
+    // later task, already done), then the level GEMM whose epilogue only sends the edge gradients
+    const PlanT B = lstm ? (gs ? gs_lstm_bwd(h, N) : mono_lstm_bwd(h, N)) : PlanT{};
+    PlanT Bfc;
+    const int rows[2] = {0, h}, zeros[2] = {0, 0};
+    if (!lstm) {
+      if (gs) { Bfc = plan_empty(); for (int k = 0; k < 2; ++k) gs_add_ksplit(Bfc, 0, k * h, 0, 0, h, k); }
+      else Bfc = mono_one(h, 2, rows, zeros);
+    }
+    for (int tt = T - 1; tt >= 0; --tt) {
+      launch_dag_df(D, lp[tt], lp[tt + 1], s);
+      P.count(1);
+      if (tt == 0) break;
+      const int M = lp[tt + 1] - lp[tt];
+      if (lstm) {
+        if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_BWD_DAG, Bs, lp[tt], lp[tt + 1], h, s);
+        else level_N<EPI_LSTM_BWD_DAG, 1>(gs, N, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
+      } else {
+        if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_BWD_DAG, Bs, lp[tt], lp[tt + 1], h, s);
+        else if (gs) launch_level<EPI_FC_BWD_DAG, 2, kCluster>(t->A[2], t->A[2], t->B_dz, D, Bfc, lp[tt], lp[tt + 1], h, s);
+        else launch_level<EPI_FC_BWD_DAG, 2, 1>(t->A[2], t->A[2], t->B_dz, D, Bfc, lp[tt], lp[tt + 1], h, s);
+      }
+      P.count(1);
+    }
+  } else if (t->ps) {
     if (T > 1) { persist_backward(D, t->ps, T, s); P.count(1); }
   } else if (lstm) {
     const PlanT B = gs ? gs_lstm_bwd(h, N) : mono_lstm_bwd(h, N);

@@ -84,7 +84,7 @@ def test_schedule_mixed_batch_tasks():
     ([[[], [0, 2], [1]]], 2, "E_CYCLE"),
     ([[[1, 2, 3], [], [], []]], 2, "E_ARITY"),
     ([[[5], []]], 2, "E_INVALID"),
-    ([[[1, 1], []]], 2, "E_FANOUT"),
+    ([[[1, 2], [2], [0]]], 2, "E_CYCLE"),        # fan-out (DAG path) with a cycle
 ])
 def test_schedule_errors(graphs, N, code):
     from paper_1712_04048_b200 import CavsError
@@ -616,3 +616,70 @@ def test_out_of_range_x_row_is_a_deferred_error():
     ctx.schedule()
     ctx.forward(t(b.params), t(b.x), t(b.x_row))
     ctx.sync()
+
+
+# ------------------------------------------------------------------ DAG inputs (NEXT-3)
+def _random_dags(K, N, n_max, seed, tree_frac=0.0):
+    """Random DAGs: vertices are created children-first; an internal vertex lists 1..N children drawn
+    WITH replacement from all earlier vertices (fan-out and duplicate child ids), local ids permuted.
+    A fraction of the graphs are plain trees (a batch mixing both runs the DAG path)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for g in range(K):
+        if rng.random() < tree_frac:
+            out.append(_nary_forest(1, N, int(rng.integers(1, n_max // 2 + 1)), int(rng.integers(1 << 30)))[0])
+            continue
+        n = int(rng.integers(1, n_max + 1))
+        nodes = []
+        for v in range(n):
+            if v < 2 or rng.random() < 0.3:
+                nodes.append([])
+            else:
+                k = int(rng.integers(1, N + 1))
+                nodes.append(rng.integers(0, v, size=k).tolist())
+        out.append(gen.permute(nodes, rng))
+    return out
+
+
+DAG_CASES = {
+    "lstm_n2_h64": lambda: gen.batch_from_graphs(_random_dags(20, 2, 30, 51), cell="tree_lstm", N=2, h=64, d=64,
+                                                 seed=51, x_at="all", loss_at="all"),
+    "lstm_n3_h128_mixed": lambda: gen.batch_from_graphs(_random_dags(24, 3, 40, 52, tree_frac=0.5), cell="tree_lstm",
+                                                        N=3, h=128, d=64, seed=52, x_at="all", loss_at="all"),
+    "lstm_n2_h512": lambda: gen.batch_from_graphs(_random_dags(30, 2, 60, 53), cell="tree_lstm", N=2, h=512,
+                                                  d=512, seed=53, x_at="all", loss_at="all"),
+    "fc_h128": lambda: gen.batch_from_graphs(_random_dags(20, 2, 40, 54), cell="tree_fc", N=2, h=128, d=64,
+                                             seed=54, x_at="all", loss_at="all"),
+}
+
+
+@pytest.mark.parametrize("case", list(DAG_CASES))
+def test_dag_schedule_bit_exact(case):
+    b = DAG_CASES[case]()
+    ctx = make_ctx(b, "bf16")
+    ctx.load_graphs(b.graph_ptr, b.child_ptr, b.child_idx)
+    T = ctx.schedule()
+    level, lp, order = ctx.get_schedule()
+    ch = global_children(b.graph_ptr, b.child_ptr, b.child_idx)
+    lv, lp_r, order_r = oracle.schedule(ch)
+    assert T == len(lp_r) - 1
+    assert np.array_equal(level, lv) and np.array_equal(lp, lp_r) and np.array_equal(order, order_r)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("case", list(DAG_CASES))
+def test_dag_parity(case, precision):
+    """DAG batches (fan-out, duplicate child ids, trees mixed in) against the fp64 oracle, whose
+    additive backward is pinned by finite differences on DAGs (test_oracle_pins); bit-identical
+    when run twice (fixed-order pull-reduce over the parent CSR)."""
+    b = DAG_CASES[case]()
+    g = run_gpu(b, precision)
+    r = run_oracle(b)
+    compare(b, g, r, FP32_TOL if precision == "fp32" else BF16_TOL, f"DAG {case} {precision} vs fp64")
+    g2 = run_gpu(b, precision, ctx=g["ctx"])
+    for k in ("h_out", "dparams", "dx"):
+        assert np.array_equal(g[k], g2[k]), f"DAG {case}: {k} not deterministic"
+    # a tree batch on the same context afterwards still takes the fused tree path
+    t = gen.make_batch(b.cell, b.N, b.h, b.d, "sst_tree" if b.cell == "tree_lstm" else "cbt8", 3, seed=5)
+    gt = run_gpu(t, precision, ctx=g["ctx"])
+    compare(t, gt, run_oracle(t), FP32_TOL if precision == "fp32" else BF16_TOL, f"tree after DAG {case}")

@@ -280,6 +280,21 @@ def test_finite_differences(case):
         _fd_case("tree_fc", 2, 3, 2, [tree, [[], [0]]], seed=14)
 
 
+@pytest.mark.parametrize("case", ["lstm2_dag", "lstm3_dup", "fc_dag"])
+def test_finite_differences_dag(case):
+    """DAG inputs (NEXT-3; P:L189-191 graph-structured RNNs, P:L447 gradients ADDED): a child shared
+    by two parents and a child listed twice by one parent; the oracle's additive backward must equal
+    central differences of its own forward (which evaluates a shared child once)."""
+    # 0, 1 leaves; 2 = (0, 1); 3 = (1, 2): vertex 1 has two parents; 4 = (3, 3): duplicate child
+    dag = [[], [], [0, 1], [1, 2], [3, 3]]
+    if case == "lstm2_dag":
+        _fd_case("tree_lstm", 2, 3, 2, [dag, [[]]], seed=15)
+    elif case == "lstm3_dup":
+        _fd_case("tree_lstm", 3, 2, 2, [[[], [], [0, 0, 1], [2, 0]]], seed=16)
+    else:
+        _fd_case("tree_fc", 2, 3, 2, [dag], seed=17)
+
+
 # ---------------------------------------------------------------- P7 batching invariance
 def test_batching_invariance():
     rng = np.random.default_rng(9)
