@@ -38,6 +38,7 @@ struct cavs_ctx {
   TcState* tc = nullptr;        // tensor-core (BF16) path state: TMA descriptors
   cudaEvent_t ev_hdr = nullptr; // recorded after the schedule header's device->host copy
   cudaEvent_t ev_wgrad = nullptr;   // caller's event: recorded once dparams' weight blocks are final
+  XStream xs;                   // streaming ablation: side stream + per-task events
   bool hdr_pending = false;     // header copied asynchronously, not parsed yet
 };
 
@@ -103,6 +104,8 @@ static size_t carve(cavs_ctx* c, char* base) {
   }
   D.pptr = I(V + 1); D.pent = I(N * V + 1); D.pcur = I(V);          // DAG parent CSR (NEXT-3)
   D.dHg = F(Vp * N * h); D.dCg = is_lstm(d) ? F(Vp * N * h) : nullptr;
+  D.rawld = (is_lstm(d) ? 3 + kMaxN : 2) * (int)h;
+  D.raw = D.unfused ? F(Vp * D.rawld) : nullptr;     // unfused ablation only
   D.lazy = F(lazy_floats(D));
   c->lazy_db = F((size_t)kDbChunks * d.N * 4 * h);   // db partials [(slot, chunk)][logical column]
   const size_t P = cavs_param_count(d.cell, d.N, d.h, d.d);
@@ -142,6 +145,14 @@ CAVS_API cavs_status cavs_create(const cavs_desc* desc, int device, void* stream
   c->device = device;
   c->stream = reinterpret_cast<cudaStream_t>(stream);
   c->D.cell = d.cell; c->D.N = d.N; c->D.h = d.h; c->D.d = d.d; c->D.prec = d.precision;
+  {  // engine ablations (NEXT-1), fixed for the context's lifetime
+    const char* lz = std::getenv("CAVS_LAZY_BATCH");
+    const char* uf = std::getenv("CAVS_UNFUSED");
+    const char* sx = std::getenv("CAVS_STREAMING");
+    c->D.lazy_off = lz && lz[0] == '0';
+    c->D.unfused = uf && uf[0] == '1';
+    c->D.stream_x = sx && sx[0] == '1';
+  }
   if (cudaSetDevice(device) != cudaSuccess ||
       cudaMallocHost(&c->h_hdr, sizeof(int) * (kHdrWords + kReadback)) != cudaSuccess) {
     delete c;
@@ -351,8 +362,12 @@ static cavs_status forward_impl(cavs_ctx* ctx, const float* params, int32_t n_x,
   }
   if (D.dag) D.infer = 0;                  // the per-task gather reads every child's saved c
   P.mark(CAVS_PH_XPROJ, ctx->stream);
-  if (D.prec == CAVS_BF16) tc_forward(D, ctx->tc, ctx->lp, ctx->stream, P);
-  else simt_forward<float>(D, ctx->lp, ctx->stream, P);
+  if (D.stream_x && !ctx->xs.s) {
+    CK(cudaStreamCreateWithFlags(&ctx->xs.s, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->xs.start, cudaEventDisableTiming));
+  }
+  if (D.prec == CAVS_BF16) tc_forward(D, ctx->tc, ctx->lp, ctx->stream, P, &ctx->xs);
+  else simt_forward<float>(D, ctx->lp, ctx->stream, P, &ctx->xs);
   P.mark(-1, ctx->stream);
   account_forward(ctx);
   CK(cudaGetLastError());
@@ -500,7 +515,10 @@ CAVS_API const char* cavs_path_info(const cavs_ctx* ctx) {
   if (!ctx) return "null context";
   cavs_ctx* c = const_cast<cavs_ctx*>(ctx);
   c->info = ctx->state < S_READY ? std::string("no workspace yet")
-                                 : ctx->desc.precision == CAVS_BF16 ? tc_describe(ctx->tc) : std::string("levels: FP32 FFMA");
+                                 : ctx->desc.precision == CAVS_BF16 ? tc_describe(ctx->tc) : std::string("levels: FP32 FFMA") +
+                                       (ctx->D.unfused ? "; ablation: unfused cell epilogues" : "") +
+                                       (ctx->D.stream_x ? "; ablation: streamed x-projection" : "") +
+                                       (ctx->D.lazy_off ? "; lazy batching OFF (ablation: per-task weight-gradient GEMMs)" : "");
   return c->info.c_str();
 }
 
@@ -509,6 +527,12 @@ CAVS_API void cavs_destroy(cavs_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream); else cudaDeviceSynchronize();
   tc_destroy(ctx->tc);
+  if (ctx->xs.s) {
+    cudaStreamSynchronize(ctx->xs.s);
+    cudaStreamDestroy(ctx->xs.s);
+    cudaEventDestroy(ctx->xs.start);
+    for (cudaEvent_t e : ctx->xs.ev) cudaEventDestroy(e);
+  }
   if (ctx->ev_hdr) cudaEventDestroy(ctx->ev_hdr);
   if (ctx->h_hdr) cudaFreeHost(ctx->h_hdr);
   delete ctx;

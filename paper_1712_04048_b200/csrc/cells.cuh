@@ -443,9 +443,26 @@ __device__ __forceinline__ bool row_active(const Dev& D, int p, int xrow) {
   else return true;
 }
 
+// The level-task epilogues (the ones the unfused ablation splits off the GEMM).
+template <int E> __host__ __device__ constexpr bool epi_is_level() {
+  return E == EPI_LSTM_FWD || E == EPI_LSTM_BWD || E == EPI_FC_FWD || E == EPI_FC_BWD || E == EPI_LSTM_BWD_DAG ||
+         E == EPI_FC_BWD_DAG;
+}
+// Unfused ablation: the GEMM only stores its accumulators (acc e of unit j at raw[p][e h + j]).
+template <int VW>
+__device__ __forceinline__ void store_raw(const Dev& D, int j, int p, const FV<VW>* acc, int nacc) {
+  for (int e = 0; e < nacc && e * D.h < D.rawld; ++e) stv<VW>(D.raw + (size_t)p * D.rawld + (size_t)e * D.h + j, acc[e]);
+}
+
 // Scalar entry used by the FFMA / skinny kernels: acc has NACC entries.
 template <int E, class OpT, int NACC>
 __device__ __forceinline__ void epilogue1(const Dev& D, int j, const VMeta& m, const float* acc) {
+  if constexpr (epi_is_level<E>()) {
+    if (D.unfused) {
+      for (int e = 0; e < NACC && e * D.h < D.rawld; ++e) D.raw[(size_t)m.p * D.rawld + (size_t)e * D.h + j] = acc[e];
+      return;
+    }
+  }
   const UnitC<1> uc = epi_uses_bias<E>() ? load_unit<1>(D, j, epi_is_lstm<E>()) : UnitC<1>{};
   FV<1> a[NACC];
 #pragma unroll

@@ -43,6 +43,13 @@ struct Dev {
   int ncl;                          // clusters of the persistent level kernels (0: none)
   int* crow;                        // [T][ncl + 1]: first position of task t owned by cluster >= r
   int* tile_cnt;                    // arrival counters (zero between launches): lazy tiles, then db column blocks
+  // engine ablations of the paper's optimisations, fixed at
+  // cavs_create from the environment: lazy_off (CAVS_LAZY_BATCH=0), unfused
+  // (CAVS_UNFUSED=1: the level GEMMs store raw accumulators, a separate elementwise
+  // kernel applies F / dF), stream_x (CAVS_STREAMING=1: the eager x-projection of the tasks
+  // above level 0 runs on a second stream, each task waiting only for its own rows)
+  int lazy_off, unfused, stream_x;
+  float* raw; int rawld;            // unfused: raw accumulators [Vp, rawld] fp32
   // DAG inputs (fan-out: a vertex with several parents); dag = 1 for this batch
   int dag;
   int* pptr;                        // [V+1] parent CSR by position: entries [pptr[p], pptr[p+1])

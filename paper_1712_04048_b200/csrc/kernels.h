@@ -84,8 +84,13 @@ inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// streaming ablation: the eager x-projection of the tasks above level 0 on a second stream, one
+// event per task (owned by the context)
+struct XStream { cudaStream_t s = nullptr; std::vector<cudaEvent_t> ev; cudaEvent_t start = nullptr; };
+
 void launch_schedule(const Dev& D, cudaStream_t s);
-template <class OpT> void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P);
+template <class OpT> void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P,
+                                      XStream* xs = nullptr);
 template <class OpT> void simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P);
 
 template <class OpT>
@@ -97,7 +102,8 @@ void skinny_typeI(const Dev& D, int epi, const SegListI& L, int row_lo, int row_
 SegListI fwd_segments(const Dev& D);
 SegListI bwd_segments(const Dev& D);
 template <class OpT>
-void simt_typeII(const Dev& D, const SegListII& L, float* out, int M, int Ncols, int ldo, cudaStream_t s);
+void simt_typeII(const Dev& D, const SegListII& L, float* out, int M, int Ncols, int ldo, cudaStream_t s,
+                 int accum = 0);   // accum: out += (stream-ordered per-task ablation launches)
 
 // ops.cu
 void launch_prep(const Dev& D, cudaStream_t s);
@@ -108,6 +114,8 @@ void launch_pack(const Dev& D, const int* split /*[3]*/, cudaStream_t s);   // s
 // DAG inputs (D.dag): parent CSR of the schedule, the forward gather of task [lo, hi) (children's h, c
 // into the parent-slot arenas; fan-out forbids the children's scatter) and the backward pull-reduce
 // + dF of task [lo, hi) (sums the edges' gradients in parent-CSR order: deterministic)
+// unfused ablation: the cell epilogue `epi` of task rows [lo, hi) from D.raw
+void launch_unfused(const Dev& D, int epi, int lo, int hi, cudaStream_t s);
 void launch_dag_parents(const Dev& D, cudaStream_t s);
 void launch_dag_gather(const Dev& D, int lo, int hi, cudaStream_t s);
 void launch_dag_df(const Dev& D, int lo, int hi, cudaStream_t s);

@@ -361,6 +361,39 @@ __global__ void k_dag_df(Dev D, int lo, int hi) {
     dag_df<OpT>(D, (int)(i % D.h), lo + (int)(i / D.h));
 }
 
+// Unfused ablation (CAVS_UNFUSED=1): the cell's elementwise part as its own kernel,
+// reading the level GEMM's raw accumulators (one thread per (vertex, unit)).
+template <int E, class OpT>
+__global__ void k_unfused(Dev D, int lo, int hi) {
+  const int h = D.h, nacc = D.rawld / h;
+  const size_t n = (size_t)(hi - lo) * h;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % h), p = lo + (int)(i / h);
+    VMeta m;
+    load_meta(D, p, epi_needs_children<E>(), m);
+    FV<1> acc[3 + kMaxN];
+#pragma unroll
+    for (int e = 0; e < 3 + kMaxN; ++e) acc[e].v[0] = e < nacc ? D.raw[(size_t)p * D.rawld + (size_t)e * h + j] : 0.f;
+    const UnitC<1> uc = epi_uses_bias<E>() ? load_unit<1>(D, j, epi_is_lstm<E>()) : UnitC<1>{};
+    typename EpiK<E>::template In<1, kMaxN> in;
+    EpiK<E>::template load<1, kMaxN>(D, j, m, in);
+    EpiK<E>::template store<OpT, 1, kMaxN>(D, j, m, acc, in, uc);
+  }
+}
+
+template <class OpT>
+static void unfused_t(const Dev& D, int epi, int lo, int hi, int g, cudaStream_t s) {
+  switch (epi) {
+    case EPI_LSTM_FWD: k_unfused<EPI_LSTM_FWD, OpT><<<g, 256, 0, s>>>(D, lo, hi); break;
+    case EPI_LSTM_BWD: k_unfused<EPI_LSTM_BWD, OpT><<<g, 256, 0, s>>>(D, lo, hi); break;
+    case EPI_FC_FWD: k_unfused<EPI_FC_FWD, OpT><<<g, 256, 0, s>>>(D, lo, hi); break;
+    case EPI_FC_BWD: k_unfused<EPI_FC_BWD, OpT><<<g, 256, 0, s>>>(D, lo, hi); break;
+    case EPI_LSTM_BWD_DAG: k_unfused<EPI_LSTM_BWD_DAG, OpT><<<g, 256, 0, s>>>(D, lo, hi); break;
+    case EPI_FC_BWD_DAG: k_unfused<EPI_FC_BWD_DAG, OpT><<<g, 256, 0, s>>>(D, lo, hi); break;
+    default: break;
+  }
+}
+
 static int grid_for(size_t n, int block) { return (int)std::min<size_t>((n + block - 1) / block, 148 * 16); }
 
 void launch_prep(const Dev& D, cudaStream_t s) {
@@ -467,6 +500,13 @@ void launch_dag_df(const Dev& D, int lo, int hi, cudaStream_t s) {
   const size_t n = (size_t)(hi - lo) * D.h;
   if (D.prec == CAVS_BF16) k_dag_df<__nv_bfloat16><<<grid_for(n, 256), 256, 0, s>>>(D, lo, hi);
   else k_dag_df<float><<<grid_for(n, 256), 256, 0, s>>>(D, lo, hi);
+}
+
+void launch_unfused(const Dev& D, int epi, int lo, int hi, cudaStream_t s) {
+  if (hi <= lo) return;
+  const int g = grid_for((size_t)(hi - lo) * D.h, 256);
+  if (D.prec == CAVS_BF16) unfused_t<__nv_bfloat16>(D, epi, lo, hi, g, s);
+  else unfused_t<float>(D, epi, lo, hi, g, s);
 }
 
 }  // namespace cavs

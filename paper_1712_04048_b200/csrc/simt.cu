@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(256) k_simt_typeI(Dev D, SegListI L, int row_l
 }
 
 template <class OpT>
-__global__ void __launch_bounds__(256) k_simt_typeII(Dev D, SegListII L, float* out, int M, int Ncols, int ldo) {
+__global__ void __launch_bounds__(256) k_simt_typeII(Dev D, SegListII L, float* out, int M, int Ncols, int ldo,
+                                                     int accum) {
   __shared__ float As[ST][ST + 1];   // [pos][m]
   __shared__ float Bs[ST][ST + 1];   // [pos][n]
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(256) k_simt_typeII(Dev D, SegListII L, float* 
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int n = n0 + ty + 8 * r;
-    if (n < Ncols) out[(size_t)m * ldo + n] = acc[r];
+    if (n < Ncols) out[(size_t)m * ldo + n] = accum ? out[(size_t)m * ldo + n] + acc[r] : acc[r];
   }
 }
 
@@ -157,9 +158,9 @@ void simt_typeI(const Dev& D, int epi, const SegListI& L, int row_lo, int row_hi
 }
 
 template <class OpT>
-void simt_typeII(const Dev& D, const SegListII& L, float* out, int M, int Ncols, int ldo, cudaStream_t s) {
+void simt_typeII(const Dev& D, const SegListII& L, float* out, int M, int Ncols, int ldo, cudaStream_t s, int accum) {
   dim3 grid(cdiv(M, ST), cdiv(Ncols, ST));
-  k_simt_typeII<OpT><<<grid, 256, 0, s>>>(D, L, out, M, Ncols, ldo);
+  k_simt_typeII<OpT><<<grid, 256, 0, s>>>(D, L, out, M, Ncols, ldo, accum);
 }
 
 SegListI fwd_segments(const Dev& D) {
@@ -195,34 +196,44 @@ SegListI bwd_segments(const Dev& D) {
 
 // ---- whole passes (FP32 mode; BF16 operands when CAVS_BF16_SIMT=1 for A/B checks) ----
 template <class OpT>
-void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
+void simt_forward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P, XStream* xs) {
   const int skmax = skinny_max(D);
   const int h = D.h, d = D.d, N = D.N, T = (int)lp.size() - 1;
+  const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
   SegListI L{}, F{};
-  if (D.cell == CAVS_CELL_TREE_LSTM) {
+  if (lstm) {
     L.n = 4;
     for (int g = 0; g < 4; ++g) L.s[g] = SegI{D.Wb, d, g * h, B_XP, 0, d, d, g};
-    simt_typeI<OpT>(D, EPI_LSTM_XPROJ, L, 0, D.V, h, s); P.count(1);
-    P.mark(CAVS_PH_FWD_LEVELS, s);
-    F = fwd_segments(D);
-    for (int t = 1; t < T; ++t) {
-      if (D.dag) { launch_dag_gather(D, lp[t], lp[t + 1], s); P.count(1); }
-      if (lp[t + 1] - lp[t] <= skmax) skinny_typeI<OpT>(D, EPI_LSTM_FWD, F, lp[t], lp[t + 1], h, s);
-      else simt_typeI<OpT>(D, EPI_LSTM_FWD, F, lp[t], lp[t + 1], h, s);
-      P.count(1);
-    }
   } else {
     L.n = 1;
     L.s[0] = SegI{D.Wb, d, 0, B_XP, 0, d, d, 0};
-    simt_typeI<OpT>(D, EPI_FC_XPROJ, L, 0, D.V, h, s); P.count(1);
-    P.mark(CAVS_PH_FWD_LEVELS, s);
-    F = fwd_segments(D);
+  }
+  const int xepi = lstm ? EPI_LSTM_XPROJ : EPI_FC_XPROJ, fepi = lstm ? EPI_LSTM_FWD : EPI_FC_FWD;
+  // eager x-projection; streaming ablation: the rows above level 0 on a second
+  // stream, task t waiting only for its own rows
+  const bool streamed = D.stream_x && xs && xs->s;
+  if (streamed) {
+    while ((int)xs->ev.size() < T) { cudaEvent_t e; cudaEventCreateWithFlags(&e, cudaEventDisableTiming); xs->ev.push_back(e); }
+    cudaEventRecord(xs->start, s);
+    cudaStreamWaitEvent(xs->s, xs->start, 0);
     for (int t = 1; t < T; ++t) {
-      if (D.dag) { launch_dag_gather(D, lp[t], lp[t + 1], s); P.count(1); }
-      if (lp[t + 1] - lp[t] <= skmax) skinny_typeI<OpT>(D, EPI_FC_FWD, F, lp[t], lp[t + 1], h, s);
-      else simt_typeI<OpT>(D, EPI_FC_FWD, F, lp[t], lp[t + 1], h, s);
-      P.count(1);
+      simt_typeI<OpT>(D, xepi, L, lp[t], lp[t + 1], h, xs->s);
+      cudaEventRecord(xs->ev[t], xs->s);
     }
+    simt_typeI<OpT>(D, xepi, L, 0, T > 1 ? lp[1] : D.V, h, s);
+    P.count(T);
+  } else {
+    simt_typeI<OpT>(D, xepi, L, 0, D.V, h, s); P.count(1);
+  }
+  P.mark(CAVS_PH_FWD_LEVELS, s);
+  F = fwd_segments(D);
+  for (int t = 1; t < T; ++t) {
+    if (D.dag) { launch_dag_gather(D, lp[t], lp[t + 1], s); P.count(1); }
+    if (streamed) cudaStreamWaitEvent(s, xs->ev[t], 0);
+    if (lp[t + 1] - lp[t] <= skmax) skinny_typeI<OpT>(D, fepi, F, lp[t], lp[t + 1], h, s);
+    else simt_typeI<OpT>(D, fepi, F, lp[t], lp[t + 1], h, s);
+    P.count(1);
+    if (D.unfused) { launch_unfused(D, fepi, lp[t], lp[t + 1], s); P.count(1); }
   }
 }
 
@@ -253,36 +264,73 @@ void simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) 
       if (lp[t + 1] - lp[t] <= skmax) skinny_typeI<OpT>(D, epi, B, lp[t], lp[t + 1], h, s);
       else simt_typeI<OpT>(D, epi, B, lp[t], lp[t + 1], h, s);
       P.count(1);
+      if (D.unfused) { launch_unfused(D, epi, lp[t], lp[t + 1], s); P.count(1); }
     }
   } else {
   for (int t = T - 1; t >= 1; --t) {
     if (lp[t + 1] - lp[t] <= skmax) skinny_typeI<OpT>(D, epi, B, lp[t], lp[t + 1], h, s);
     else simt_typeI<OpT>(D, epi, B, lp[t], lp[t + 1], h, s);
     P.count(1);
+    if (D.unfused) { launch_unfused(D, epi, lp[t], lp[t + 1], s); P.count(1); }
   }
   }
   P.mark(CAVS_PH_LAZY, s);
   // lazy batching of the parameter gradients over ALL vertices; one partial each
   const LazyLayout Z = lazy_layout(D);
   const int lp1 = D.lp1, V = D.V;
-  if (lstm) {
+  if (D.lazy_off) {
+    // ablation "lazy batching off": one set of weight-gradient GEMMs per task over its own
+    // rows, accumulated in stream order
+    for (int t = 0; t < T; ++t) {
+      const int lo = lp[t], hi = lp[t + 1], acc = t > 0 ? 1 : 0, accU = t > 1 ? 1 : 0;
+      if (lstm) {
+        if (t >= 1) {
+          SegListII A{}; A.n = N;
+          for (int k = 0; k < N; ++k) A.s[k] = SegII{D.dZ, G * h, 0, D.Hk, N * h, k * h, lo, hi, 0};
+          simt_typeII<OpT>(D, A, D.lazy + Z.u4, 3 * h, h, h, s, accU);
+          SegListII Bf{}; Bf.n = N;
+          for (int k = 0; k < N; ++k) Bf.s[k] = SegII{D.dZ, G * h, (3 + k) * h, D.Hk, N * h, k * h, lo, hi, 0};
+          simt_typeII<OpT>(D, Bf, D.lazy + Z.uf, h, h, h, s, accU);
+          P.count(2);
+        }
+        SegListII Cw{}; Cw.n = 1;
+        Cw.s[0] = SegII{D.dZ, G * h, 0, D.Xp, d, 0, lo, hi, 1};
+        simt_typeII<OpT>(D, Cw, D.lazy + Z.w, G * h, d, d, s, acc);
+      } else {
+        if (t >= 1) {
+          SegListII A{}; A.n = 1;
+          A.s[0] = SegII{D.dZ, h, 0, D.Hk, 2 * h, 0, lo, hi, 0};
+          simt_typeII<OpT>(D, A, D.lazy + Z.u4, h, 2 * h, 2 * h, s, accU);
+          P.count(1);
+        }
+        SegListII Cw{}; Cw.n = 1;
+        Cw.s[0] = SegII{D.dZ, h, 0, D.Xp, d, 0, lo, hi, 1};
+        simt_typeII<OpT>(D, Cw, D.lazy + Z.w, h, d, d, s, acc);
+      }
+      P.count(1);
+    }
+    if (T <= 1) {
+      cudaMemsetAsync(D.lazy + Z.u4, 0, sizeof(float) * Z.su4, s);
+      if (lstm) cudaMemsetAsync(D.lazy + Z.uf, 0, sizeof(float) * Z.suf, s);
+    }
+  } else if (lstm) {
     SegListII A{}; A.n = N;                      // dU_iou = sum_k dZ_iou^T H_k
     for (int k = 0; k < N; ++k) A.s[k] = SegII{D.dZ, G * h, 0, D.Hk, N * h, k * h, lp1, V, 0};
-    simt_typeII<OpT>(D, A, D.lazy + Z.u4, 3 * h, h, h, s);
+    simt_typeII<OpT>(D, A, D.lazy + Z.u4, 3 * h, h, h, s, 0);
     SegListII Bf{}; Bf.n = N;
     for (int k = 0; k < N; ++k) Bf.s[k] = SegII{D.dZ, G * h, (3 + k) * h, D.Hk, N * h, k * h, lp1, V, 0};
-    simt_typeII<OpT>(D, Bf, D.lazy + Z.uf, h, h, h, s);
+    simt_typeII<OpT>(D, Bf, D.lazy + Z.uf, h, h, h, s, 0);
     SegListII Cw{}; Cw.n = 1;
     Cw.s[0] = SegII{D.dZ, G * h, 0, D.Xp, d, 0, 0, V, 1};
-    simt_typeII<OpT>(D, Cw, D.lazy + Z.w, G * h, d, d, s);
+    simt_typeII<OpT>(D, Cw, D.lazy + Z.w, G * h, d, d, s, 0);
     P.count(3);
   } else {
     SegListII A{}; A.n = 1;
     A.s[0] = SegII{D.dZ, h, 0, D.Hk, 2 * h, 0, lp1, V, 0};
-    simt_typeII<OpT>(D, A, D.lazy + Z.u4, h, 2 * h, 2 * h, s);
+    simt_typeII<OpT>(D, A, D.lazy + Z.u4, h, 2 * h, 2 * h, s, 0);
     SegListII Cw{}; Cw.n = 1;
     Cw.s[0] = SegII{D.dZ, h, 0, D.Xp, d, 0, 0, V, 1};
-    simt_typeII<OpT>(D, Cw, D.lazy + Z.w, h, d, d, s);
+    simt_typeII<OpT>(D, Cw, D.lazy + Z.w, h, d, d, s, 0);
     P.count(2);
   }
   P.mark(CAVS_PH_DX, s);
@@ -293,14 +341,14 @@ void simt_backward(Dev& D, const std::vector<int>& lp, cudaStream_t s, Prof& P) 
   }
 }
 
-template void simt_forward<float>(Dev&, const std::vector<int>&, cudaStream_t, Prof&);
-template void simt_forward<__nv_bfloat16>(Dev&, const std::vector<int>&, cudaStream_t, Prof&);
+template void simt_forward<float>(Dev&, const std::vector<int>&, cudaStream_t, Prof&, XStream*);
+template void simt_forward<__nv_bfloat16>(Dev&, const std::vector<int>&, cudaStream_t, Prof&, XStream*);
 template void simt_backward<float>(Dev&, const std::vector<int>&, cudaStream_t, Prof&);
 template void simt_backward<__nv_bfloat16>(Dev&, const std::vector<int>&, cudaStream_t, Prof&);
 
 template void simt_typeI<float>(const Dev&, int, const SegListI&, int, int, int, cudaStream_t);
 template void simt_typeI<__nv_bfloat16>(const Dev&, int, const SegListI&, int, int, int, cudaStream_t);
-template void simt_typeII<float>(const Dev&, const SegListII&, float*, int, int, int, cudaStream_t);
-template void simt_typeII<__nv_bfloat16>(const Dev&, const SegListII&, float*, int, int, int, cudaStream_t);
+template void simt_typeII<float>(const Dev&, const SegListII&, float*, int, int, int, cudaStream_t, int);
+template void simt_typeII<__nv_bfloat16>(const Dev&, const SegListII&, float*, int, int, int, cudaStream_t, int);
 
 }  // namespace cavs

@@ -56,7 +56,7 @@ struct RankPlan { int nb; Bundle b[3]; int nacc; int stages; int stage_bytes; in
 struct PlanT { RankPlan r[kCluster]; int comb[8][kCluster]; int bar_off; };
 
 struct SegT2 { int a_col; int b_col; int k_lo, k_hi; int skip_no_x; };
-struct PlanII { int nseg; SegT2 s[4]; int M, Ncols, ldo; int split; size_t split_stride; int stages; };
+struct PlanII { int nseg; SegT2 s[4]; int M, Ncols, ldo; int split; size_t split_stride; int stages; int accum; };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~(uintptr_t)1023);
@@ -253,6 +253,14 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
         }
         EpiK<E>::template load<4, NM>(D, j, s_meta[r], in[i]);
       }
+      if constexpr (epi_is_level<E>()) {
+        if (D.unfused) {                               // ablation: raw accumulators only
+#pragma unroll
+          for (int i = 0; i < CH; ++i)
+            if (ok[i]) store_raw<4>(D, j, s_meta[cg + 8 * (i0 + i)].p, acc[i], NACC);
+          continue;
+        }
+      }
 #pragma unroll
       for (int i = 0; i < CH; ++i)                     // ... then the math and the stores
         if (ok[i]) EpiK<E>::template store<__nv_bfloat16, 4, NM>(D, j, s_meta[cg + 8 * (i0 + i)], acc[i], in[i], uc);
@@ -331,6 +339,19 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
           const uint32_t ph = (step / S) & 1;
           ptx::mbar_wait(&full[s], ph);
           ptx::tc_fence_after();
+          const int valid = sg.k_hi - (sg.k_lo + kb * 64);
+          if (valid < 64) {
+            // rows past k_hi belong to the next range (per-task ablation launches): zero them in
+            // the A tile -- a position row is one 128-byte line of each MN-major box, which the
+            // 128B swizzle only permutes internally
+            uint8_t* at = smem + s * STAGE;
+            for (int r = valid; r < 64; ++r)
+              for (int c = 0; c < 128; c += 16) {
+                *reinterpret_cast<uint4*>(at + r * 128 + c) = make_uint4(0, 0, 0, 0);
+                *reinterpret_cast<uint4*>(at + 8192 + r * 128 + c) = make_uint4(0, 0, 0, 0);
+              }
+            ptx::fence_proxy_async_smem();
+          }
           const uint32_t a = ptx::smem_u32(smem + s * STAGE);
           const uint32_t b = a + T2_TILE;
 #pragma unroll
@@ -387,7 +408,11 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
         if (m < P.M) {
           for (int i = 0; i < 16; ++i) {
             const int n = n0 + c + i;
-            if (n < P.Ncols) o[(size_t)m * P.ldo + n] = any ? v[i] : 0.f;
+            if (n < P.Ncols) {
+              const float x = any ? v[i] : 0.f;
+              float* dst = o + (size_t)m * P.ldo + n;
+              *dst = P.accum ? *dst + x : x;              // accum: stream-ordered launches, split 1
+            }
           }
         }
       }
@@ -481,7 +506,11 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
   if (!t->use_simt) t->ls = lazy_init(D, max_vertices);
   if (t->use_simt) t->info = "levels: SIMT FFMA (CAVS_BF16_SIMT=1)";
   else if (t->mono) t->info = "levels: per-task tcgen05, monolithic CTAs (CAVS_TC_MONO=1)";
-  else {
+  else if (D.unfused || D.stream_x) {
+    t->info = std::string("levels: per-task tcgen05 launches (ablation: ") +
+              (D.unfused ? "unfused cell epilogues" : "") + (D.unfused && D.stream_x ? ", " : "") +
+              (D.stream_x ? "streamed x-projection" : "") + ")";
+  } else {
     std::string why;
     t->ps = persist_init(D, max_vertices, &why);
     t->info = t->ps ? "levels: " + persist_describe(t->ps)
@@ -493,7 +522,8 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
       if (t->rs) t->info += "; large tasks: row-tiled tcgen05 (>= " + std::to_string(t->rows_min_tiles) + " tiles)";
     }
   }
-  t->info += t->ls ? "; lazy: stream-K tcgen05 (one launch)" : "; lazy: split-K tcgen05 + pack";
+  t->info += D.lazy_off ? "; lazy batching OFF (ablation: per-task weight-gradient GEMMs)"
+                        : t->ls ? "; lazy: stream-K tcgen05 (one launch)" : "; lazy: split-K tcgen05 + pack";
   *out = t;
   return CAVS_OK;
 }
@@ -718,33 +748,66 @@ static void level_N(bool gs, int N, const CUtensorMap& a0, const CUtensorMap& a1
   }
 }
 
-void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, Prof& P) {
+// Streaming ablation: level-0 rows of the x-projection (they finish the leaves) on the main
+// stream; the rows of every task above level 0 on the side stream, task t waiting only for its own.
+static bool xproj_streamed(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, XStream* xs, Prof& P) {
+  const int h = D.h, d = D.d, T = (int)lp.size() - 1;
+  if (!D.stream_x || !xs || !xs->s) return false;
+  const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
+  const int zero = 0;
+  const PlanT X = lstm ? mono_lstm_xproj(h, d) : mono_one(d, 1, &zero, &zero);
+  auto proj = [&](int lo, int hi, cudaStream_t st) {
+    if (lstm) launch_level<EPI_LSTM_XPROJ, 4, 1>(t->A[1], t->A[1], t->B_xp, D, X, lo, hi, h, st);
+    else launch_level<EPI_FC_XPROJ, 1, 1>(t->A[1], t->A[1], t->B_xp, D, X, lo, hi, h, st);
+  };
+  while ((int)xs->ev.size() < T) { cudaEvent_t e; cudaEventCreateWithFlags(&e, cudaEventDisableTiming); xs->ev.push_back(e); }
+  cudaEventRecord(xs->start, s);                     // prep / pull done
+  cudaStreamWaitEvent(xs->s, xs->start, 0);
+  for (int tt = 1; tt < T; ++tt) {
+    proj(lp[tt], lp[tt + 1], xs->s);
+    cudaEventRecord(xs->ev[tt], xs->s);
+  }
+  proj(0, T > 1 ? lp[1] : D.V, s);
+  P.count(T);
+  return true;
+}
+
+void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, Prof& P, XStream* xs) {
   const int skmax = skinny_max(D);
-  if (t->use_simt) { simt_forward<__nv_bfloat16>(D, lp, s, P); return; }
+  if (t->use_simt) { simt_forward<__nv_bfloat16>(D, lp, s, P, xs); return; }
   const int h = D.h, d = D.d, N = D.N, T = (int)lp.size() - 1;
   const bool gs = !t->mono;
   const SegListI Fs = fwd_segments(D);
   const int zero = 0;
+  const bool streamed = xproj_streamed(D, t, lp, s, xs, P);
+  auto wait_x = [&](int tt) { if (streamed) cudaStreamWaitEvent(s, xs->ev[tt], 0); };
+  auto unfused = [&](int epi, int tt) { if (D.unfused) { launch_unfused(D, epi, lp[tt], lp[tt + 1], s); P.count(1); } };
   if (D.cell == CAVS_CELL_TREE_LSTM) {
     // eager pull projection fused with task 0 (large: monolithic CTAs reuse the x tile for 4 gates)
-    if (!gemm_xproj(D, t->gs, s))
-      launch_level<EPI_LSTM_XPROJ, 4, 1>(t->A[1], t->A[1], t->B_xp, D, mono_lstm_xproj(h, d), 0, D.V, h, s);
-    P.count(1);
+    if (!streamed) {
+      if (!gemm_xproj(D, t->gs, s))
+        launch_level<EPI_LSTM_XPROJ, 4, 1>(t->A[1], t->A[1], t->B_xp, D, mono_lstm_xproj(h, d), 0, D.V, h, s);
+      P.count(1);
+    }
     P.mark(CAVS_PH_FWD_LEVELS, s);
     if (t->ps && !D.dag) { if (T > 1) { persist_forward(D, t->ps, T, s); P.count(1); } return; }
     const PlanT F = gs ? gs_lstm_fwd(h, N) : mono_lstm_fwd(h, N);
     for (int tt = 1; tt < T; ++tt) {
       const int M = lp[tt + 1] - lp[tt];
       if (D.dag) { launch_dag_gather(D, lp[tt], lp[tt + 1], s); P.count(1); }
+      wait_x(tt);
       if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_FWD, Fs, lp[tt], lp[tt + 1], h, s);
       else if (rows_tiles(t->rs, false, M) >= t->rows_min_tiles && rows_level(D, t->rs, false, lp[tt], lp[tt + 1], s)) {}
       else level_N<EPI_LSTM_FWD, 3>(gs, N, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       P.count(1);
+      unfused(EPI_LSTM_FWD, tt);
     }
   } else {
-    if (!gemm_xproj(D, t->gs, s))
-      launch_level<EPI_FC_XPROJ, 1, 1>(t->A[1], t->A[1], t->B_xp, D, mono_one(d, 1, &zero, &zero), 0, D.V, h, s);
-    P.count(1);
+    if (!streamed) {
+      if (!gemm_xproj(D, t->gs, s))
+        launch_level<EPI_FC_XPROJ, 1, 1>(t->A[1], t->A[1], t->B_xp, D, mono_one(d, 1, &zero, &zero), 0, D.V, h, s);
+      P.count(1);
+    }
     P.mark(CAVS_PH_FWD_LEVELS, s);
     if (t->ps && !D.dag) { if (T > 1) { persist_forward(D, t->ps, T, s); P.count(1); } return; }
     PlanT F;
@@ -753,11 +816,13 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
     for (int tt = 1; tt < T; ++tt) {
       const int M = lp[tt + 1] - lp[tt];
       if (D.dag) { launch_dag_gather(D, lp[tt], lp[tt + 1], s); P.count(1); }
+      wait_x(tt);
       if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_FWD, Fs, lp[tt], lp[tt + 1], h, s);
       else if (rows_tiles(t->rs, false, M) >= t->rows_min_tiles && rows_level(D, t->rs, false, lp[tt], lp[tt + 1], s)) {}
       else if (gs) launch_level<EPI_FC_FWD, 1, kCluster>(t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       else launch_level<EPI_FC_FWD, 1, 1>(t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
       P.count(1);
+      unfused(EPI_FC_FWD, tt);
     }
   }
 }
@@ -767,7 +832,8 @@ static int launch_II(const CUtensorMap& a, const CUtensorMap& b, const Dev& D, P
   int nkb = 0;
   for (int i = 0; i < P.nseg; ++i) nkb += cdiv(P.s[i].k_hi - P.s[i].k_lo, 64);
   const int tiles = cdiv(P.M, 128) * cdiv(P.Ncols, 128);
-  P.split = std::max(1, std::min(std::min(kSplitMax, 148 / std::max(1, tiles)), std::max(1, nkb / 4)));
+  P.split = P.split == 1 ? 1      // forced (per-task ablation launches accumulate in stream order)
+            : std::max(1, std::min(std::min(kSplitMax, 148 / std::max(1, tiles)), std::max(1, nkb / 4)));
   P.stages = 6;
   const int smem = P.stages * 2 * T2_TILE + 1024 + 2 * 8 * P.stages + 64;
   static bool attr_done[kMaxDev] = {};
@@ -817,6 +883,7 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
         else launch_level<EPI_FC_BWD_DAG, 2, 1>(t->A[2], t->A[2], t->B_dz, D, Bfc, lp[tt], lp[tt + 1], h, s);
       }
       P.count(1);
+      if (D.unfused) { launch_unfused(D, lstm ? EPI_LSTM_BWD_DAG : EPI_FC_BWD_DAG, lp[tt], lp[tt + 1], s); P.count(1); }
     }
   } else if (t->ps) {
     if (T > 1) { persist_backward(D, t->ps, T, s); P.count(1); }
@@ -828,6 +895,7 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
       else if (rows_tiles(t->rs, true, M) >= t->rows_min_tiles && rows_level(D, t->rs, true, lp[tt], lp[tt + 1], s)) {}
       else level_N<EPI_LSTM_BWD, 1>(gs, N, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       P.count(1);
+      if (D.unfused) { launch_unfused(D, EPI_LSTM_BWD, lp[tt], lp[tt + 1], s); P.count(1); }
     }
   } else {
     PlanT B;
@@ -841,6 +909,7 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
       else if (gs) launch_level<EPI_FC_BWD, 2, kCluster>(t->A[2], t->A[2], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       else launch_level<EPI_FC_BWD, 2, 1>(t->A[2], t->A[2], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
       P.count(1);
+      if (D.unfused) { launch_unfused(D, EPI_FC_BWD, lp[tt], lp[tt + 1], s); P.count(1); }
     }
   }
   P.mark(CAVS_PH_LAZY, s);
@@ -851,7 +920,47 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
   float* w = D.lazy + Z.w;
   const int lp1 = D.lp1, V = D.V;
   const int zero = 0;
-  if (lazy_grads(D, t->ls, s)) {                      // every dU / dW block straight into dparams
+  if (D.lazy_off) {
+    // ablation "lazy batching off": the weight gradients as separate GEMMs per task over
+    // that task's rows only (what Alg. 1's per-task backward would issue), accumulated in stream
+    // order into one slot (split 1; deterministic), then packed like the split-K fallback
+    const int Tn = (int)lp.size() - 1;
+    for (int tt = 0; tt < Tn; ++tt) {
+      const int lo = lp[tt], hi = lp[tt + 1];
+      const int acc = tt > 0 ? 1 : 0;
+      if (lstm) {
+        PlanII A{};                                     // dU_iou, dU_f: parents only (t >= 1)
+        A.nseg = N; A.split = 1; A.accum = acc > 0 && tt > 1 ? 1 : 0;
+        for (int k = 0; k < N; ++k) A.s[k] = SegT2{0, k * h, lo, tt >= 1 ? hi : lo, 0};
+        A.M = 3 * h; A.Ncols = h; A.ldo = h; A.split_stride = Z.su4;
+        PlanII Bf = A;
+        for (int k = 0; k < N; ++k) Bf.s[k] = SegT2{(3 + k) * h, k * h, lo, tt >= 1 ? hi : lo, 0};
+        Bf.M = h; Bf.Ncols = h; Bf.ldo = h; Bf.split_stride = Z.suf;
+        if (tt >= 1) { launch_II(t->M_dz, t->M_hk, D, A, u4, s); launch_II(t->M_dz, t->M_hk, D, Bf, uf, s); P.count(2); }
+        PlanII Cw{};                                    // dW over this task's pull records
+        Cw.nseg = 1; Cw.split = 1; Cw.accum = acc;
+        Cw.s[0] = SegT2{0, 0, lo, hi, 1};
+        Cw.M = G * h; Cw.Ncols = d; Cw.ldo = d; Cw.split_stride = Z.sw;
+        launch_II(t->M_dz, t->M_xp, D, Cw, w, s); P.count(1);
+      } else {
+        PlanII A{};
+        A.nseg = 1; A.split = 1; A.accum = tt > 1 ? 1 : 0;
+        A.s[0] = SegT2{0, 0, lo, hi, 0};
+        A.M = h; A.Ncols = 2 * h; A.ldo = 2 * h; A.split_stride = Z.su4;
+        if (tt >= 1) { launch_II(t->M_dz, t->M_hk, D, A, u4, s); P.count(1); }
+        PlanII Cw{};
+        Cw.nseg = 1; Cw.split = 1; Cw.accum = acc;
+        Cw.s[0] = SegT2{0, 0, lo, hi, 1};
+        Cw.M = h; Cw.Ncols = d; Cw.ldo = d; Cw.split_stride = Z.sw;
+        launch_II(t->M_dz, t->M_xp, D, Cw, w, s); P.count(1);
+      }
+    }
+    if (Tn <= 1) {                                      // no internal vertex: dU = 0
+      cudaMemsetAsync(u4, 0, sizeof(float) * Z.su4, s);
+      if (lstm) cudaMemsetAsync(uf, 0, sizeof(float) * Z.suf, s);
+    }
+    split[0] = split[1] = split[2] = 1;
+  } else if (lazy_grads(D, t->ls, s)) {                // every dU / dW block straight into dparams
     P.count(1);
     split[0] = -1;
     if (wgrad_ev) cudaEventRecord(wgrad_ev, s);        // the weight blocks can be all-reduced from here on

@@ -11,7 +11,7 @@ struct TcState;
 
 cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* err);
 // Launches are counted into P; phase marks XPROJ -> FWD_LEVELS and BWD_LEVELS -> LAZY -> DX.
-void tc_forward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, Prof& P);
+void tc_forward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, Prof& P, XStream* xs = nullptr);
 // wgrad_ev (nullable): recorded on s once the lazy GEMMs wrote every weight block of dparams
 // (stream-K path; otherwise the caller records it after the split-K pack).
 void tc_backward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, int* split /*[3]*/, Prof& P,

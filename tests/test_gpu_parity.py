@@ -683,3 +683,41 @@ def test_dag_parity(case, precision):
     t = gen.make_batch(b.cell, b.N, b.h, b.d, "sst_tree" if b.cell == "tree_lstm" else "cbt8", 3, seed=5)
     gt = run_gpu(t, precision, ctx=g["ctx"])
     compare(t, gt, run_oracle(t), FP32_TOL if precision == "fp32" else BF16_TOL, f"tree after DAG {case}")
+
+
+# ------------------------------------------------------------------ engine ablations (NEXT-1)
+ABLATIONS = {
+    "lazy_off": ({"CAVS_LAZY_BATCH": "0"}, "lazy batching OFF"),
+    "unfused": ({"CAVS_UNFUSED": "1"}, "unfused cell epilogues"),
+    "streaming": ({"CAVS_STREAMING": "1"}, "streamed x-projection"),
+}
+ABL_CASES = {
+    "lstm_sst_h128": lambda: gen.make_batch("tree_lstm", 2, 128, 128, "sst_tree", 12, seed=61),
+    "lstm_chains_h64": lambda: gen.batch_from_graphs([gen.chain(n) for n in (9, 30, 2, 17)], cell="tree_lstm", N=1,
+                                                     h=64, d=64, seed=62, x_at="all", loss_at="all"),
+    "fc_cbt_h128": lambda: gen.make_batch("tree_fc", 2, 128, 64, "cbt16", 6, seed=63),
+    "lstm_dag_h64": lambda: DAG_CASES["lstm_n2_h64"](),
+}
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("case", list(ABL_CASES))
+@pytest.mark.parametrize("abl", list(ABLATIONS))
+def test_ablations(abl, case, precision, monkeypatch):
+    """The paper's optimisation toggles (Fig. 10; lazy batching P:L542, fusion P:L559-562,
+    streaming P:L544) change where and when the same arithmetic runs, not the method: each ablated
+    engine against the fp64 oracle, and against the default engine (same operands and rounding
+    points; only fp32 summation order may differ)."""
+    b = ABL_CASES[case]()
+    env, marker = ABLATIONS[abl]
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = run_gpu(b, precision)
+    assert marker in g["ctx"].path_info(), g["ctx"].path_info()
+    tol = FP32_TOL if precision == "fp32" else BF16_TOL
+    compare(b, g, run_oracle(b), tol, f"{abl} {case} {precision} vs fp64")
+    for k in env:
+        monkeypatch.delenv(k)
+    o = run_gpu(b, precision)
+    assert marker not in o["ctx"].path_info()
+    compare(b, g, o, FP32_TOL if precision == "fp32" else BF16_EMU_TOL, f"{abl} {case} {precision} vs default engine")
