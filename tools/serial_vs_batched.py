@@ -3,6 +3,9 @@ cfg4 batch run as ONE level-batched step (all graphs' tasks merged) and as 256 s
 each (the serial policy: every task holds a single graph's vertices), device time by CUDA events.
 
     python tools/serial_vs_batched.py [--config cfg4] [--graphs 256]
+    python tools/serial_vs_batched.py --config cfg2 --sweep 2,4,8,16,32,64,128
+        Fig. 10's curve: for each batch size bs, one level-batched step over bs graphs vs bs
+        single-graph steps (Fixed-LSTM chains of 64, h = 512: the paper's 1.7x ... 36x axis).
 """
 import argparse
 import json
@@ -22,12 +25,27 @@ def main():
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--graphs", type=int, default=256)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--sweep", default=None, help="comma-separated batch sizes (graphs per step)")
+    ap.add_argument("--precision", default="bf16")
     a = ap.parse_args()
+    if a.sweep:
+        for bs in [int(x) for x in a.sweep.split(",")]:
+            one(a, bs)
+        return
+    one(a, a.graphs)
+
+
+def one(a, K_req):
     dev = torch.device("cuda", 0)
-    b = gen.make_config_batch(a.config, seed=0)
+    b = gen.make_config_batch(a.config, seed=0, K=K_req if a.config == "cfg2" and K_req > 64 else None)
     t = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)
-    K = min(a.graphs, b.K)
-    ctx = Context(b.cell, b.N, b.h, b.d, precision="bf16", max_graphs=b.K, max_vertices=b.V, max_x=max(1, b.n_x))
+    K = min(K_req, b.K)
+    if K < b.K:                                   # the batched step runs exactly the first K graphs
+        gp, cp, ci, rows, recs, nxr = gen.subset_csr(b.graph_ptr, b.child_ptr, b.child_idx, b.x_row, list(range(K)))
+        b = gen.Batch(cell=b.cell, N=b.N, h=b.h, d=b.d, graph_ptr=gp, child_ptr=cp, child_idx=ci, x_row=nxr,
+                      x=np.ascontiguousarray(b.x[recs]), params=b.params, gamma=np.ascontiguousarray(b.gamma[rows]))
+    ctx = Context(b.cell, b.N, b.h, b.d, precision=a.precision, max_graphs=b.K, max_vertices=b.V,
+                  max_x=max(1, b.n_x))
     params = t(b.params)
     # per-graph sub-batches (CSR slices re-based to vertex 0, x rows re-indexed)
     subs = []
@@ -64,10 +82,11 @@ def main():
 
     batched = timed(lambda: run(full))
     serial = timed(lambda: [run(s) for s in subs])
-    out = {"config": a.config, "graphs": K, "batched_ms": batched, "serial_ms": serial,
+    out = {"config": a.config, "precision": a.precision, "graphs": K, "batched_ms": batched, "serial_ms": serial,
            "batched_samples_per_s": b.K / (batched / 1e3), "serial_samples_per_s": K / (serial / 1e3),
            "speedup": serial / batched * (b.K / K)}
-    print(json.dumps(out))
+    print(json.dumps(out), flush=True)
+    ctx.close()
 
 
 if __name__ == "__main__":
