@@ -190,6 +190,20 @@ cavs_status cavs_train_step_host(cavs_ctx* ctx, int32_t K, int32_t V, int32_t E,
                                  const float* x, const int32_t* x_row, const float* dh_out,
                                  float* dparams, float* dx, float* h_out);
 
+/* Next-word softmax head (§5 P:L606 "predicts the next word"): the
+ * loss lives outside (F, G) (reading Z9) and is wired to F through push (h_out) and push's adjoint
+ * (dh_out = dL/dh).  This is its fused softmax / cross-entropy / gradient pass over the logits of
+ * M rows (the head's contractions logits = H W^T + b and dH = dlogits W are plain GEMMs):
+ *   logits  [M, vocab] device fp32 (row-major)
+ *   target  [M]        device int32: class of each row, < 0 = no loss at this row
+ *   loss    [M]        device fp32 (nullable): logsumexp(logits_m) - logits_m[target_m] (0 without target)
+ *   dlogits [M, vocab] device fp32: scale * (softmax(logits_m) - onehot(target_m)) (0 without target);
+ *                      may alias logits (in place)
+ * Enqueued on `stream` (a cudaStream_t, NULL = legacy default).  No context needed.
+ * Errors: CAVS_E_INVALID (sizes / null pointers), CAVS_E_CUDA (launch). */
+cavs_status cavs_softmax_xent(const float* logits, int32_t M, int32_t vocab, const int32_t* target, float* loss,
+                              float* dlogits, float scale, void* stream);
+
 /* Data-parallel overlap hook (SURVEY §8(e) "Overlap"): `cuda_event` (a cudaEvent_t created by the
  * caller, or NULL to clear) is recorded on the context's stream by every later cavs_backward as soon
  * as all WEIGHT blocks of dparams (W, U_iou, U_f / W_c, W_x) are final -- right after the lazily

@@ -12,6 +12,7 @@ from .cavs_oracle import (  # noqa: F401
     forward,
     global_children,
     levels_recursive,
+    lm_head,
     loss,
     pack,
     run,

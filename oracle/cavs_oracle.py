@@ -392,6 +392,26 @@ def backward(cell, N, h, d, theta, tape, x_row, n_x, gamma, emulate_bf16=False, 
     return pack(cell, N, h, d, G), dx
 
 
+def lm_head(h_out, W_out, b_out, targets):
+    """Next-word softmax head outside (F, G) (reading Z9), plain definition in fp64:
+    logits_v = W_out h_v + b_out; L = sum over vertices with a target of
+    logsumexp(logits_v) - logits_v[target_v].  Returns (L, dL/dh [V,h], dL/dW_out, dL/db_out);
+    dL/dh is the cotangent Gamma that push's adjoint hands to F's backward."""
+    H = np.asarray(h_out, dtype=np.float64)
+    W = np.asarray(W_out, dtype=np.float64)
+    b = np.asarray(b_out, dtype=np.float64)
+    t = np.asarray(targets)
+    logits = H @ W.T + b
+    mx = logits.max(axis=1, keepdims=True)
+    lse = mx[:, 0] + np.log(np.exp(logits - mx).sum(axis=1))
+    has = t >= 0
+    L = float(np.sum(lse[has] - logits[has, t[has]]))
+    dl = np.exp(logits - lse[:, None])
+    dl[has, t[has]] -= 1.0
+    dl[~has] = 0.0
+    return L, dl @ W, dl.T @ H, dl.sum(axis=0)
+
+
 def loss(h_out, gamma):
     """External linear loss L = sum_v <Gamma_v, h_v> (reading Z9)."""
     return float(np.sum(np.asarray(h_out) * np.asarray(gamma, dtype=np.float64)))

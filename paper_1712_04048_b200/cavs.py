@@ -57,6 +57,7 @@ def _load():
         "cavs_kernel_launches": (I64, [P]),
         "cavs_sync": (S, [P]),
         "cavs_set_grad_event": (S, [P, P]),
+        "cavs_softmax_xent": (S, [P, I32, I32, P, P, P, ctypes.c_float, P]),
         "cavs_last_error": (ctypes.c_char_p, [P]),
         "cavs_path_info": (ctypes.c_char_p, [P]),
         "cavs_profile": (S, [P, ctypes.c_int]),
@@ -76,7 +77,7 @@ def _load():
 _lib = _load()
 EXPORTS = ["cavs_param_count", "cavs_create", "cavs_set_stream", "cavs_workspace_bytes",
            "cavs_set_workspace", "cavs_load_graphs", "cavs_schedule", "cavs_get_schedule",
-           "cavs_forward", "cavs_forward_inference", "cavs_backward", "cavs_train_step_host", "cavs_kernel_launches", "cavs_sync", "cavs_set_grad_event",
+           "cavs_forward", "cavs_forward_inference", "cavs_backward", "cavs_train_step_host", "cavs_kernel_launches", "cavs_sync", "cavs_set_grad_event", "cavs_softmax_xent",
            "cavs_last_error", "cavs_path_info", "cavs_destroy", "cavs_profile", "cavs_profile_read"]
 PHASES = ["schedule", "prep", "xproj", "fwd_levels", "bwd_roots", "bwd_levels", "lazy", "dx", "reduce"]
 
@@ -115,6 +116,24 @@ def _ptr(a, kind=None, device=None, host_ok=False):
         elif not host_ok:
             raise TypeError("expected a CUDA tensor on the context's device, got a CPU tensor")
     return a.data_ptr()
+
+
+def softmax_xent(logits, target, dlogits=None, loss=None, scale=1.0, stream=None):
+    """cavs_softmax_xent: per-row loss and scale * (softmax - onehot) (in place when dlogits is logits).
+    logits [M, vocab] fp32 CUDA, target [M] int32 CUDA (< 0: no loss).  Returns (loss [M], dlogits)."""
+    import torch
+    M, vocab = int(logits.shape[0]), int(logits.shape[1])
+    dev = logits.device
+    if dlogits is None:
+        dlogits = torch.empty_like(logits)
+    if loss is None:
+        loss = torch.empty(M, dtype=torch.float32, device=dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    st_code = _lib.cavs_softmax_xent(_ptr(logits, "f32", dev), M, vocab, _ptr(target, "i32", dev), _ptr(loss, "f32", dev),
+                                     _ptr(dlogits, "f32", dev), float(scale), ctypes.c_void_p(st.cuda_stream))
+    if st_code != 0:
+        raise CavsError(st_code, "cavs_softmax_xent failed")
+    return loss, dlogits
 
 
 class Context:

@@ -339,19 +339,6 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
           const uint32_t ph = (step / S) & 1;
           ptx::mbar_wait(&full[s], ph);
           ptx::tc_fence_after();
-          const int valid = sg.k_hi - (sg.k_lo + kb * 64);
-          if (valid < 64) {
-            // rows past k_hi belong to the next range (per-task ablation launches): zero them in
-            // the A tile -- a position row is one 128-byte line of each MN-major box, which the
-            // 128B swizzle only permutes internally
-            uint8_t* at = smem + s * STAGE;
-            for (int r = valid; r < 64; ++r)
-              for (int c = 0; c < 128; c += 16) {
-                *reinterpret_cast<uint4*>(at + r * 128 + c) = make_uint4(0, 0, 0, 0);
-                *reinterpret_cast<uint4*>(at + 8192 + r * 128 + c) = make_uint4(0, 0, 0, 0);
-              }
-            ptx::fence_proxy_async_smem();
-          }
           const uint32_t a = ptx::smem_u32(smem + s * STAGE);
           const uint32_t b = a + T2_TILE;
 #pragma unroll
@@ -928,6 +915,9 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
     for (int tt = 0; tt < Tn; ++tt) {
       const int lo = lp[tt], hi = lp[tt + 1];
       const int acc = tt > 0 ? 1 : 0;
+      // dZ viewed with `hi` rows: the TMA zero-fills the last k-block's rows of the next task
+      CUtensorMap mdz;
+      encode(&mdz, D.dZ, (uint64_t)G * h, (uint64_t)hi, (uint64_t)G * h, 64, 64);
       if (lstm) {
         PlanII A{};                                     // dU_iou, dU_f: parents only (t >= 1)
         A.nseg = N; A.split = 1; A.accum = acc > 0 && tt > 1 ? 1 : 0;
@@ -936,23 +926,23 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
         PlanII Bf = A;
         for (int k = 0; k < N; ++k) Bf.s[k] = SegT2{(3 + k) * h, k * h, lo, tt >= 1 ? hi : lo, 0};
         Bf.M = h; Bf.Ncols = h; Bf.ldo = h; Bf.split_stride = Z.suf;
-        if (tt >= 1) { launch_II(t->M_dz, t->M_hk, D, A, u4, s); launch_II(t->M_dz, t->M_hk, D, Bf, uf, s); P.count(2); }
+        if (tt >= 1) { launch_II(mdz, t->M_hk, D, A, u4, s); launch_II(mdz, t->M_hk, D, Bf, uf, s); P.count(2); }
         PlanII Cw{};                                    // dW over this task's pull records
         Cw.nseg = 1; Cw.split = 1; Cw.accum = acc;
         Cw.s[0] = SegT2{0, 0, lo, hi, 1};
         Cw.M = G * h; Cw.Ncols = d; Cw.ldo = d; Cw.split_stride = Z.sw;
-        launch_II(t->M_dz, t->M_xp, D, Cw, w, s); P.count(1);
+        launch_II(mdz, t->M_xp, D, Cw, w, s); P.count(1);
       } else {
         PlanII A{};
         A.nseg = 1; A.split = 1; A.accum = tt > 1 ? 1 : 0;
         A.s[0] = SegT2{0, 0, lo, hi, 0};
         A.M = h; A.Ncols = 2 * h; A.ldo = 2 * h; A.split_stride = Z.su4;
-        if (tt >= 1) { launch_II(t->M_dz, t->M_hk, D, A, u4, s); P.count(1); }
+        if (tt >= 1) { launch_II(mdz, t->M_hk, D, A, u4, s); P.count(1); }
         PlanII Cw{};
         Cw.nseg = 1; Cw.split = 1; Cw.accum = acc;
         Cw.s[0] = SegT2{0, 0, lo, hi, 1};
         Cw.M = h; Cw.Ncols = d; Cw.ldo = d; Cw.split_stride = Z.sw;
-        launch_II(t->M_dz, t->M_xp, D, Cw, w, s); P.count(1);
+        launch_II(mdz, t->M_xp, D, Cw, w, s); P.count(1);
       }
     }
     if (Tn <= 1) {                                      // no internal vertex: dU = 0

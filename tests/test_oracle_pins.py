@@ -384,3 +384,27 @@ def test_bf16_hsum_rounded_is_a_bf16_rounding_of_the_exact_sum():
         assert np.all(np.abs(hr - ex) <= 2.0 ** -8 * np.abs(ex) + 1e-300)
         differ += int(np.any(te.st[v]["hs"] != hr))
     assert differ > 0
+
+
+# ---------------------------------------------------------------- NEXT-4 softmax head (outside (F, G))
+def test_lm_head_matches_finite_differences_and_closed_forms():
+    """The next-word head (reading Z9): dL/dh, dL/dW, dL/db against central differences of
+    its own loss; with all-zero logits the per-row loss is log(vocab) (uniform softmax)."""
+    rng = np.random.default_rng(3)
+    V, h, vocab = 5, 3, 7
+    H = rng.normal(size=(V, h))
+    W = rng.normal(size=(vocab, h)) * 0.5
+    b = rng.normal(size=vocab) * 0.1
+    t = np.array([1, 6, -1, 0, 3])
+    L, dH, dW, db = oracle.lm_head(H, W, b, t)
+    eps = 1e-6
+    for arr, grad in ((H, dH), (W, dW), (b, db)):
+        num = np.zeros_like(arr)
+        for j in np.ndindex(arr.shape):
+            old = arr[j]
+            arr[j] = old + eps; lp = oracle.lm_head(H, W, b, t)[0]
+            arr[j] = old - eps; lm = oracle.lm_head(H, W, b, t)[0]
+            arr[j] = old
+            num[j] = (lp - lm) / (2 * eps)
+        assert np.abs(num - grad).max() < 1e-7
+    assert np.allclose(dH[2], 0) and np.allclose(oracle.lm_head(H, W * 0, b * 0, t)[0], 4 * np.log(vocab))

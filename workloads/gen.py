@@ -246,6 +246,38 @@ def _embedding_x(n_x: int, d: int, seed: int, vocab: int = 10000) -> np.ndarray:
     return table[tok]
 
 
+@dataclass
+class LMBatch:
+    """Language-model batch: `batch` is the F-over-G part (chains, N = 1) whose
+    pull records are the rows of an embedding table (x = table [vocab, d], x_row[v] = token of
+    vertex v: the embedding pull); `targets[v]` = next token of the sequence (-1 at the last step);
+    W_out [vocab, h], b_out [vocab]: the softmax head's parameters."""
+    batch: "Batch"
+    tokens: np.ndarray
+    targets: np.ndarray
+    W_out: np.ndarray
+    b_out: np.ndarray
+
+
+def make_lm_batch(K: int, lengths, h: int, d: int, vocab: int, seed: int) -> LMBatch:
+    """K sequences (lengths: an int or one per sequence) of Zipf tokens p(r) ~ 1/r over `vocab`
+    (PTB-sized at 10k, P:L606), chains 0 -> 1 -> ... (vertex t reads token t, predicts token t+1);
+    params U(-0.1, 0.1), embedding and head U(-0.1, 0.1)."""
+    rng = np.random.default_rng(seed)
+    lens = [int(lengths)] * K if np.isscalar(lengths) else [int(x) for x in lengths]
+    p = 1.0 / np.arange(1, vocab + 1)
+    p /= p.sum()
+    seqs = [rng.choice(vocab, size=n + 1, p=p).astype(np.int32) for n in lens]
+    b = batch_from_graphs([chain(n) for n in lens], cell="tree_lstm", N=1, h=h, d=d, seed=seed, x_at="none",
+                          loss_at="all")
+    b.x = rng.uniform(-0.1, 0.1, size=(vocab, d)).astype(np.float32)
+    b.x_row = np.concatenate([q[:-1] for q in seqs]).astype(np.int32)
+    targets = np.concatenate([np.concatenate([q[1:-1], [-1]]) for q in seqs]).astype(np.int32)
+    W_out = rng.uniform(-0.1, 0.1, size=(vocab, h)).astype(np.float32)
+    b_out = rng.uniform(-0.1, 0.1, size=vocab).astype(np.float32)
+    return LMBatch(batch=b, tokens=b.x_row.copy(), targets=targets, W_out=W_out, b_out=b_out)
+
+
 def make_batch(cell: str, N: int, h: int, d: int, shape: str, K: int, seed: int,
                gamma_scale: float = 1.0) -> Batch:
     graphs = make_graphs(shape, K, seed)
