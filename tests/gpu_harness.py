@@ -111,7 +111,12 @@ def compare(b, g, r, tol, what="", row_factor=ROW_FACTOR, elem_factor=ELEM_FACTO
     plus row-wise (h_out, dx: max_v ||d_v|| / ||ref_v||) <= row_factor * tol and elementwise
     (max |d| / max |ref|) <= elem_factor * tol.  `rows`: compare only these h_out rows."""
     errs = errors(b, g, r, rows)
-    lim = {k: tol * (row_factor if k.endswith(".row") else elem_factor if k.endswith(".elem") else 1.0) for k in errs}
+    # bf16-class comparisons (tol >= 1e-3): the row / element guards never tighter than 4e-2 -- they
+    # catch O(1) errors (a wrong row or unit column); single-ulp bf16 flips amplified along deep
+    # trees reach ~1e-2 elementwise between two valid summation orders (fc_h512_sst)
+    floor = 4e-2 if tol >= 1e-3 else 0.0
+    lim = {k: max(floor, tol * row_factor) if k.endswith(".row") else max(floor, tol * elem_factor)
+           if k.endswith(".elem") else tol for k in errs}
     RECORD.append({"what": what, "tol": tol, "errs": errs})
     bad = {k: v for k, v in errs.items() if not v <= lim[k]}
     assert not bad, f"{what} errors above limits: {bad} (tol {tol}; all: {errs})"
