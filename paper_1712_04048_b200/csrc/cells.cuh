@@ -47,18 +47,38 @@ template <class OpT> __device__ __forceinline__ float act_tanh(float z) {
 // ---- VW-wide vector helpers (VW in {1, 4}) ----------------------------------------------
 template <int VW> struct FV { float v[VW]; };
 
+// VW = 8: one 256-bit access per thread (LDG/STG.E.256 on sm_100): a thread that owns one row
+// (TMEM lane = vertex, rows.cu) then touches whole 32-byte sectors instead of half sectors.
 template <int VW> __device__ __forceinline__ FV<VW> ldv(const float* p) {
   FV<VW> r;
-  if constexpr (VW == 4) { const float4 t = *reinterpret_cast<const float4*>(p); r.v[0] = t.x; r.v[1] = t.y; r.v[2] = t.z; r.v[3] = t.w; }
+  if constexpr (VW == 8) {
+    asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]), "=f"(r.v[6]),
+                   "=f"(r.v[7]) : "l"(p));
+  } else if constexpr (VW == 4) { const float4 t = *reinterpret_cast<const float4*>(p); r.v[0] = t.x; r.v[1] = t.y; r.v[2] = t.z; r.v[3] = t.w; }
   else r.v[0] = *p;
   return r;
 }
 template <int VW> __device__ __forceinline__ void stv(float* p, const FV<VW>& a) {
-  if constexpr (VW == 4) *reinterpret_cast<float4*>(p) = make_float4(a.v[0], a.v[1], a.v[2], a.v[3]);
+  if constexpr (VW == 8) {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 ::"l"(p), "f"(a.v[0]), "f"(a.v[1]), "f"(a.v[2]), "f"(a.v[3]), "f"(a.v[4]), "f"(a.v[5]), "f"(a.v[6]),
+                   "f"(a.v[7]) : "memory");
+  } else if constexpr (VW == 4) *reinterpret_cast<float4*>(p) = make_float4(a.v[0], a.v[1], a.v[2], a.v[3]);
   else *p = a.v[0];
 }
 template <class OpT, int VW> __device__ __forceinline__ void stv_op(OpT* p, const FV<VW>& a) {
-  if constexpr (VW == 4 && sizeof(OpT) == 2) {
+  if constexpr (VW == 8 && sizeof(OpT) == 2) {
+    uint4 u;
+    __nv_bfloat162 b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) b[i] = __floats2bfloat162_rn(a.v[2 * i], a.v[2 * i + 1]);
+    u.x = *reinterpret_cast<uint32_t*>(&b[0]); u.y = *reinterpret_cast<uint32_t*>(&b[1]);
+    u.z = *reinterpret_cast<uint32_t*>(&b[2]); u.w = *reinterpret_cast<uint32_t*>(&b[3]);
+    *reinterpret_cast<uint4*>(p) = u;
+  } else if constexpr (VW == 8) {
+    stv<8>(reinterpret_cast<float*>(p), a);
+  } else if constexpr (VW == 4 && sizeof(OpT) == 2) {
     __nv_bfloat162 lo = __floats2bfloat162_rn(a.v[0], a.v[1]), hi = __floats2bfloat162_rn(a.v[2], a.v[3]);
     uint2 u;
     u.x = *reinterpret_cast<uint32_t*>(&lo);

@@ -22,6 +22,13 @@
 // Epilogue: thread = task row (TMEM lane) x half of the tile's units; per 4-unit quad the
 // accumulators are read straight from TMEM and the cell (cells.cuh EpiK) runs in registers.
 //   warp 0: TMA producer, warp 1: TMEM allocator + MMA issuer, warps 2-9: epilogue.
+// CTA pairs (CG = 2, opt-in CAVS_ROWS_PAIR=1): a cluster of two CTAs on one TPC runs each tile as ONE
+// tcgen05.mma.cta_group::2 of M = 256 task rows (128 per CTA) x N = n weight rows, issued by the
+// rank-0 CTA; each CTA stages its own 128 A rows and HALF of the B rows (n/2), so a stage is
+// 16 KB + n/2 x 128 B instead of 16 KB + n x 128 B: half the weight traffic per SM and 6-8
+// pipeline stages instead of 4.  Both CTAs' TMA complete on the leader's full barrier; the
+// leader's commits multicast to both CTAs' empty / accumulator-full barriers; both epilogues
+// drain their own TMEM and arrive on the leader's accumulator-empty barrier.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -34,8 +41,9 @@
 namespace cavs {
 
 constexpr int kRThreads = 320;
-constexpr int kRS = 4;                 // pipeline stages
+constexpr int kRSMax = 8;              // pipeline stages (plan: as many as fit shared memory)
 constexpr int kRA = 128 * 128;         // A stage: 128 rows x 64 k (bf16) = 16 KB
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;   // shared::cluster address of the pair's rank-0 CTA
 
 struct RSeg { int a_col, bmap, nbox, box_rows, b_row0[4], nkb, acc_col; };
 struct RPlan {
@@ -43,11 +51,12 @@ struct RPlan {
   RSeg seg[5];
   int UG;          // units per tile
   int n;           // MMA N (nbox * box_rows), the same for every segment
-  int stage;       // bytes per stage
+  int stage;       // bytes per stage (per CTA)
+  int S;           // pipeline stages
   int acc_cols;    // TMEM columns per accumulator buffer
   int nbuf;        // accumulator buffers (1 or 2)
   int lo, hi;      // task rows
-  int nut, ntiles; // unit tiles, tiles
+  int nut, ntiles; // unit tiles, tiles (of 128 CG task rows)
 };
 
 __device__ __forceinline__ void rwait(uint64_t* bar, uint32_t parity) {
@@ -81,35 +90,40 @@ __device__ __forceinline__ void tld_wait() { asm volatile("tcgen05.wait::ld.sync
 template <int E> struct RAcc { static constexpr int NE = 1; };
 template <> struct RAcc<EPI_FC_BWD> { static constexpr int NE = 2; };
 
-// accumulators of the quad at unit offset u (within the tile) -> acc[NE]
-template <int E, int NM>
-__device__ __forceinline__ void fetch_acc(uint32_t tb, int UG, int u, FV<4>* acc) {
+// accumulators of the VW units at unit offset u (within the tile) -> acc[NE]; VW in {4, 8}
+template <int VW>
+__device__ __forceinline__ void tldv(uint32_t taddr, uint32_t* r) {
+  tld4(taddr, r);
+  if constexpr (VW == 8) tld4(taddr + 4, r + 4);
+}
+template <int E, int NM, int VW>
+__device__ __forceinline__ void fetch_acc(uint32_t tb, int UG, int u, FV<VW>* acc) {
   if constexpr (E == EPI_FC_FWD) {
-    uint32_t r[4];
-    tld4(tb + u, r);
+    uint32_t r[VW];
+    tldv<VW>(tb + u, r);
     tld_wait();
 #pragma unroll
-    for (int e = 0; e < 4; ++e) acc[0].v[e] = __uint_as_float(r[e]);
+    for (int e = 0; e < VW; ++e) acc[0].v[e] = __uint_as_float(r[e]);
   } else if constexpr (E == EPI_FC_BWD) {
-    uint32_t r[2][4];
-    tld4(tb + u, r[0]);
-    tld4(tb + UG + u, r[1]);
+    uint32_t r[2][VW];
+    tldv<VW>(tb + u, r[0]);
+    tldv<VW>(tb + UG + u, r[1]);
     tld_wait();
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[a].v[e] = __uint_as_float(r[a][e]);
+      for (int e = 0; e < VW; ++e) acc[a].v[e] = __uint_as_float(r[a][e]);
   } else if constexpr (E == EPI_LSTM_FWD) {
-    uint32_t r[NM][4][4];
+    uint32_t r[NM][4][VW];
 #pragma unroll
     for (int k = 0; k < NM; ++k)
 #pragma unroll
-      for (int g = 0; g < 4; ++g) tld4(tb + (uint32_t)(k * 4 * UG + g * UG + u), r[k][g]);
+      for (int g = 0; g < 4; ++g) tldv<VW>(tb + (uint32_t)(k * 4 * UG + g * UG + u), r[k][g]);
     tld_wait();
 #pragma unroll
     for (int g = 0; g < 3; ++g)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < VW; ++e) {
         float s = 0.f;
 #pragma unroll
         for (int k = 0; k < NM; ++k) s += __uint_as_float(r[k][g][e]);
@@ -118,100 +132,167 @@ __device__ __forceinline__ void fetch_acc(uint32_t tb, int UG, int u, FV<4>* acc
 #pragma unroll
     for (int k = 0; k < NM; ++k)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[3 + k].v[e] = __uint_as_float(r[k][3][e]);
+      for (int e = 0; e < VW; ++e) acc[3 + k].v[e] = __uint_as_float(r[k][3][e]);
   } else {   // EPI_LSTM_BWD: acc 0 = U_iou^T dz_iou, acc 1 + k = U_f^T dz_fk
-    uint32_t r[1 + NM][4];
+    uint32_t r[1 + NM][VW];
 #pragma unroll
-    for (int a = 0; a < 1 + NM; ++a) tld4(tb + (uint32_t)(a * UG + u), r[a]);
+    for (int a = 0; a < 1 + NM; ++a) tldv<VW>(tb + (uint32_t)(a * UG + u), r[a]);
     tld_wait();
 #pragma unroll
     for (int a = 0; a < 1 + NM; ++a)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[a].v[e] = __uint_as_float(r[a][e]);
+      for (int e = 0; e < VW; ++e) acc[a].v[e] = __uint_as_float(r[a][e]);
   }
 }
 
-template <int E, int NM, int QB>
+__device__ __forceinline__ uint32_t r_cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void r_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA 2-D tile load; CG = 2: completes on the pair leader's barrier (same offset, peer bit cleared)
+template <int CG>
+__device__ __forceinline__ void r_tma(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* bar) {
+  if constexpr (CG == 1) {
+    ptx::tma_load_2d(dst, m, c0, c1, bar);
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(ptx::smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1),
+          "r"(ptx::smem_u32(bar) & kPeerMask)
+        : "memory");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void r_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (CG == 1) {
+    ptx::mma_bf16(d, a, b, idesc, acc);
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  }
+}
+// arrive on `bar` of this CTA (CG = 1) or of both CTAs of the pair (CG = 2) when the issued MMAs finish
+template <int CG>
+__device__ __forceinline__ void r_commit(uint64_t* bar) {
+  if constexpr (CG == 1) {
+    ptx::mma_commit(bar);
+  } else {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}"
+        ::"r"(ptx::smem_u32(bar)) : "memory");
+  }
+}
+
+template <int E, int NM, int QB, int CG>
 __global__ void __launch_bounds__(kRThreads, 1)
 k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB0,
        const __grid_constant__ CUtensorMap mB1, Dev D, const __grid_constant__ RPlan P) {
   constexpr int NE = E == EPI_LSTM_FWD ? 3 + NM : E == EPI_LSTM_BWD ? 1 + NM : RAcc<E>::NE;
   extern __shared__ __align__(16) uint8_t r_raw[];
   uint8_t* smem = r_raw + ((1024u - (ptx::smem_u32(r_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRS * P.stage);
-  uint64_t* empty = full + kRS;
-  uint64_t* accf = empty + kRS;
+  const int S = P.S;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * P.stage);
+  uint64_t* empty = full + kRSMax;
+  uint64_t* accf = empty + kRSMax;
   uint64_t* acce = accf + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = CG == 2 ? (int)r_cluster_rank() : 0;
+  const bool leader = rank == 0;
+  const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;   // CTA pair (CG = 2) or CTA
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kRS; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { ptx::mbar_init(&accf[b], 1); ptx::mbar_init(&acce[b], 256); }
-    ptx::fence_mbar_init();
+    for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { ptx::mbar_init(&accf[b], 1); ptx::mbar_init(&acce[b], 8 * CG); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (CG == 1) {
+      ptx::tmem_alloc<512>(tmem_slot);
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(ptx::smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+  }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) r_cluster_sync();             // barriers + TMEM of both CTAs ready
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     // ---- TMA producer ----
-    // one box per lane (lane 0: A, lanes 1..nbox: B): boxes issued by one thread are serviced
-    // one after another, boxes of different threads in parallel
+    // one box per lane (lane 0: A, lanes 1..: this CTA's B boxes): boxes issued by one thread are
+    // serviced one after another, boxes of different threads in parallel
     if (lane == 0) { ptx::tma_prefetch(&mA); ptx::tma_prefetch(&mB0); ptx::tma_prefetch(&mB1); }
     ptx::griddep_wait();                                 // task rows come from the previous kernels
     if (lane <= 4) {
       int step = 0;
-      for (int j = blockIdx.x; j < P.ntiles; j += gridDim.x) {
-        const int p0 = P.lo + (j / P.nut) * 128, u0 = (j % P.nut) * P.UG;
+      for (int j = unit; j < P.ntiles; j += nunits) {
+        const int p0 = P.lo + (j / P.nut) * 128 * CG + 128 * rank, u0 = (j % P.nut) * P.UG;
         for (int sg = 0; sg < P.nseg; ++sg) {
-          const RSeg& S = P.seg[sg];
-          const CUtensorMap* mb = S.bmap ? &mB1 : &mB0;
-          for (int kb = 0; kb < S.nkb; ++kb, ++step) {
-            const int s = step % kRS;
-            if (lane > S.nbox) continue;
-            if (step >= kRS) rwait(&empty[s], ((step / kRS) & 1) ^ 1);
+          const RSeg& Sg = P.seg[sg];
+          const CUtensorMap* mb = Sg.bmap ? &mB1 : &mB0;
+          const int own = Sg.nbox / CG;                  // this CTA's B boxes: [rank own, +own)
+          for (int kb = 0; kb < Sg.nkb; ++kb, ++step) {
+            const int s = step % S;
+            if (lane > own) continue;
+            if (step >= S) rwait(&empty[s], ((step / S) & 1) ^ 1);
             uint8_t* st = smem + s * P.stage;
+#ifdef CAVS_ROWS_NOTMA
+            if (lane == 0 && leader) ptx::mbar_arrive(&full[s]);       // A/B only: MMA on stale smem
+            (void)st; (void)mb; (void)p0; (void)u0;
+#else
             if (lane == 0) {
-              ptx::mbar_arrive_expect_tx(&full[s], P.stage);
-              ptx::tma_load_2d(st, &mA, S.a_col + kb * 64, p0, &full[s]);
+              if (leader) ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)(CG * P.stage));
+              r_tma<CG>(st, &mA, Sg.a_col + kb * 64, p0, &full[s]);
             } else {
-              const int g = lane - 1;
-              ptx::tma_load_2d(st + kRA + g * S.box_rows * 128, mb, kb * 64, S.b_row0[g] + u0, &full[s]);
+              const int g = rank * own + lane - 1;
+              r_tma<CG>(st + kRA + (lane - 1) * Sg.box_rows * 128, mb, kb * 64, Sg.b_row0[g] + u0, &full[s]);
             }
+#endif
           }
         }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ---- MMA issuer ----
-    if (lane == 0) {
-      const uint32_t idesc = ptx::idesc_bf16(128, P.n, 0, 0);
+    // ---- MMA issuer (the pair's rank-0 CTA) ----
+    if (lane == 0 && leader) {
+      const uint32_t idesc = ptx::idesc_bf16(128 * CG, P.n, 0, 0);
       int step = 0;
-      for (int j = blockIdx.x, k = 0; j < P.ntiles; j += gridDim.x, ++k) {
+      for (int j = unit, k = 0; j < P.ntiles; j += nunits, ++k) {
         const int buf = P.nbuf == 2 ? (k & 1) : 0;
         const int use = P.nbuf == 2 ? (k >> 1) : k;       // earlier uses of this buffer
         if (use > 0) rwait(&acce[buf], (use - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t tb = tmem + (uint32_t)(buf * P.acc_cols);
         for (int sg = 0; sg < P.nseg; ++sg) {
-          const RSeg& S = P.seg[sg];
-          for (int kb = 0; kb < S.nkb; ++kb, ++step) {
-            const int s = step % kRS;
-            rwait(&full[s], (step / kRS) & 1);
+          const RSeg& Sg = P.seg[sg];
+          for (int kb = 0; kb < Sg.nkb; ++kb, ++step) {
+            const int s = step % S;
+            rwait(&full[s], (step / S) & 1);
             ptx::tc_fence_after();
             const uint32_t a = ptx::smem_u32(smem + s * P.stage), b = a + kRA;
+#ifndef CAVS_ROWS_NOMMA
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              ptx::mma_bf16(tb + (uint32_t)S.acc_col, r_desc(a + kk * 32), r_desc(b + kk * 32), idesc,
-                            (kb | kk) ? 1u : 0u);
-            ptx::mma_commit(&empty[s]);
+              r_mma<CG>(tb + (uint32_t)Sg.acc_col, r_desc(a + kk * 32), r_desc(b + kk * 32), idesc, (kb | kk) ? 1u : 0u);
+#else
+            (void)a; (void)b; (void)idesc;                   // A/B only: TMA stream without MMAs
+#endif
+            r_commit<CG>(&empty[s]);
           }
         }
-        ptx::mma_commit(&accf[buf]);
+        r_commit<CG>(&accf[buf]);
       }
     }
     __syncwarp();
@@ -220,9 +301,14 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
     const int q = warp & 3, hh = (warp - 2) >> 2;
     const int r = q * 32 + lane;
     const int qpt = P.UG / 8;                            // quads per thread
+    uint32_t acce_remote[2] = {0, 0};
+    if constexpr (CG == 2) {
+      for (int b = 0; b < 2; ++b)
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(acce_remote[b]) : "r"(ptx::smem_u32(&acce[b])));
+    }
     ptx::griddep_wait();
-    for (int j = blockIdx.x, k = 0; j < P.ntiles; j += gridDim.x, ++k) {
-      const int p0 = P.lo + (j / P.nut) * 128, u0 = (j % P.nut) * P.UG;
+    for (int j = unit, k = 0; j < P.ntiles; j += nunits, ++k) {
+      const int p0 = P.lo + (j / P.nut) * 128 * CG + 128 * rank, u0 = (j % P.nut) * P.UG;
       const int p = p0 + r;
       const bool valid = p < P.hi;
       VMeta m;
@@ -233,36 +319,50 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
       ptx::tc_fence_after();
       const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * P.acc_cols);
       const int ub = hh * (P.UG / 2);                    // this thread's first unit within the tile
+      // VW units per item: 8 (one 32-byte sector per row and output stream: 256-bit accesses) except
+      // for the register-heavy Tree-LSTM backward (children's state in registers)
+      constexpr int VW = E == EPI_LSTM_BWD ? 4 : 8;
+      const int ipt = P.UG / 2 / VW;                     // items per thread
 #pragma unroll 1
-      for (int qb = 0; qb < qpt; qb += QB) {
-        typename EpiK<E>::template In<4, NM> in[QB];
-        UnitC<4> uc[QB];
+      for (int qb = 0; qb < ipt; qb += QB) {
+        typename EpiK<E>::template In<VW, NM> in[QB];
+        UnitC<VW> uc[QB];
         if (valid) {
 #pragma unroll
           for (int b = 0; b < QB; ++b) {
-            const int jj = u0 + ub + (qb + b) * 4;
-            EpiK<E>::template load<4, NM>(D, jj, m, in[b]);
-            uc[b] = epi_uses_bias<E>() ? load_unit<4>(D, jj, epi_is_lstm<E>()) : UnitC<4>{};
+            const int jj = u0 + ub + (qb + b) * VW;
+            EpiK<E>::template load<VW, NM>(D, jj, m, in[b]);
+            uc[b] = epi_uses_bias<E>() ? load_unit<VW>(D, jj, epi_is_lstm<E>()) : UnitC<VW>{};
           }
         }
-        FV<4> acc[QB][NE];
+        FV<VW> acc[QB][NE];
 #pragma unroll
-        for (int b = 0; b < QB; ++b) fetch_acc<E, NM>(tb, P.UG, ub + (qb + b) * 4, acc[b]);
+        for (int b = 0; b < QB; ++b) fetch_acc<E, NM, VW>(tb, P.UG, ub + (qb + b) * VW, acc[b]);
+#ifndef CAVS_ROWS_NOEPI
         if (valid) {
 #pragma unroll
           for (int b = 0; b < QB; ++b)
-            EpiK<E>::template store<__nv_bfloat16, 4, NM>(D, u0 + ub + (qb + b) * 4, m, acc[b], in[b], uc[b]);
+            EpiK<E>::template store<__nv_bfloat16, VW, NM>(D, u0 + ub + (qb + b) * VW, m, acc[b], in[b], uc[b]);
         }
+#else
+        if (valid && acc[0][0].v[0] == 12345.f) D.h_out[0] = acc[QB - 1][NE - 1].v[3];   // A/B only: no epilogue stores
+#endif
       }
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&acce[buf]);
+      __syncwarp();
+      if (lane == 0) {                                   // this warp drained its TMEM lanes
+        if (CG == 1 || leader) ptx::mbar_arrive(&acce[buf]);
+        else asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acce_remote[buf]) : "memory");
+      }
     }
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) r_cluster_sync();             // the peer's last MMA / arrivals are done
+  else __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<512>(tmem);
+    if constexpr (CG == 1) ptx::tmem_dealloc<512>(tmem);
+    else asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
@@ -274,6 +374,7 @@ struct RowsState {
   CUtensorMap B_fwd, B_bwd0, B_bwd1;
   RPlan fwd{}, bwd{};
   int num_sms = 148;
+  int cg = 1;                          // CTAs per MMA: 2 = CTA pairs (cta_group::2, opt-in), 1 = single CTA
 };
 
 static PFN_cuTensorMapEncodeTiled_v12000 r_enc = nullptr;
@@ -296,11 +397,28 @@ static RSeg rseg(int a_col, int bmap, int nbox, int box_rows, const int* rows0, 
   return S;
 }
 
-static int r_smem(const RPlan& P) { return 1024 + kRS * P.stage + (2 * kRS + 4) * 8 + 16; }
+static int r_smem(const RPlan& P) { return 1024 + P.S * P.stage + (2 * kRSMax + 4) * 8 + 16; }
 
-template <int E, int NM, int QB>
+template <int E, int NM, int QB, int CG>
 static bool r_attr(const RPlan& P) {
-  return cudaFuncSetAttribute(k_rows<E, NM, QB>, cudaFuncAttributeMaxDynamicSharedMemorySize, r_smem(P)) == cudaSuccess;
+  return cudaFuncSetAttribute(k_rows<E, NM, QB, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, r_smem(P)) ==
+         cudaSuccess;
+}
+
+// Plan of one pass: segments, stage size and depth for CG CTAs per MMA.  CG = 2 splits every
+// segment's B rows between the pair (a single 128-row box becomes two 64-row half boxes).
+static void r_finish(RPlan& P, int h, int CG) {
+  if (CG == 2)
+    for (int sg = 0; sg < P.nseg; ++sg) {
+      RSeg& S = P.seg[sg];
+      if (S.nbox == 1) {
+        S.nbox = 2; S.b_row0[1] = S.b_row0[0] + S.box_rows / 2; S.box_rows /= 2;
+      }
+    }
+  P.stage = kRA + P.n / CG * 128;
+  P.S = std::min(kRSMax, (232448 - 2048 - (2 * kRSMax + 4) * 8 - 16) / P.stage);
+  P.nbuf = 2 * P.acc_cols <= 512 ? 2 : 1;
+  P.nut = h / P.UG;
 }
 
 RowsState* rows_init(const Dev& D, int max_vertices) {
@@ -321,6 +439,11 @@ RowsState* rows_init(const Dev& D, int max_vertices) {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&rs->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  // CTA pairs are opt-in (CAVS_ROWS_PAIR=1): measured at cfg5 they do not beat one CTA per MMA
+  // (the pair's TMA stream runs in lockstep on the slower SM; profiles/r02_rows.md)
+  const char* pe = std::getenv("CAVS_ROWS_PAIR");
+  rs->cg = (pe && pe[0] == '1') ? 2 : 1;
+  const int CG = rs->cg;
   const uint64_t Vp = (uint64_t)max_vertices + kPadRows, G = lstm ? 3 + N : 1;
   bool ok = renc(&rs->A_hk, D.Hk, (uint64_t)N * h, Vp, 128) && renc(&rs->A_dz, D.dZ, G * h, Vp, 128);
   RPlan& F = rs->fwd;
@@ -338,7 +461,8 @@ RowsState* rows_init(const Dev& D, int max_vertices) {
     B.seg[0] = rseg(0, 0, 1, 128, r0, 3 * h / 64, 0);
     for (int k = 0; k < N; ++k) B.seg[1 + k] = rseg((3 + k) * h, 1, 1, 128, r0, h / 64, (1 + k) * 128);
     B.acc_cols = 128 * (1 + N);
-    ok = ok && renc(&rs->B_bwd0, D.Wc, 3 * (uint64_t)h, h, 128) && renc(&rs->B_bwd1, D.Wd, h, h, 128);
+    const uint32_t br = CG == 2 ? 64 : 128;                                       // pair: half boxes
+    ok = ok && renc(&rs->B_bwd0, D.Wc, 3 * (uint64_t)h, h, br) && renc(&rs->B_bwd1, D.Wd, h, h, br);
   } else {
     // forward: z = [h_l | h_r] W_c^T for 256 units
     F.UG = 256; F.n = 256; F.nseg = 1;
@@ -354,17 +478,16 @@ RowsState* rows_init(const Dev& D, int max_vertices) {
     ok = ok && renc(&rs->B_bwd0, D.Wc, h, 2 * (uint64_t)h, 128);                // W_c^T [2h x h]
     rs->B_bwd1 = rs->B_bwd0;
   }
-  for (RPlan* P : {&F, &B}) {
-    P->stage = kRA + P->n * 128;
-    P->nbuf = 2 * P->acc_cols <= 512 ? 2 : 1;
-    P->nut = h / P->UG;
-  }
-  if (lstm) {
-    ok = ok && (N == 1 ? r_attr<EPI_LSTM_FWD, 1, 2>(F) && r_attr<EPI_LSTM_BWD, 1, 2>(B)
-                       : r_attr<EPI_LSTM_FWD, 2, 2>(F) && r_attr<EPI_LSTM_BWD, 2, 2>(B));
-  } else {
-    ok = ok && r_attr<EPI_FC_FWD, 1, 4>(F) && r_attr<EPI_FC_BWD, 1, 4>(B);
-  }
+  r_finish(F, h, CG);
+  r_finish(B, h, CG);
+  auto attrs = [&](auto cg) {
+    constexpr int C = decltype(cg)::value;
+    if (lstm)
+      return N == 1 ? r_attr<EPI_LSTM_FWD, 1, 1, C>(F) && r_attr<EPI_LSTM_BWD, 1, 1, C>(B)
+                    : r_attr<EPI_LSTM_FWD, 2, 1, C>(F) && r_attr<EPI_LSTM_BWD, 2, 1, C>(B);
+    return r_attr<EPI_FC_FWD, 1, 2, C>(F) && r_attr<EPI_FC_BWD, 1, 2, C>(B);
+  };
+  ok = ok && (CG == 2 ? attrs(std::integral_constant<int, 2>{}) : attrs(std::integral_constant<int, 1>{}));
   if (!ok) { delete rs; return nullptr; }
   return rs;
 }
@@ -375,7 +498,9 @@ int rows_tiles(const RowsState* rs, bool backward, int rows) {
   return rs ? cdiv(rows, 128) * (backward ? rs->bwd.nut : rs->fwd.nut) : 0;
 }
 
-template <int E, int NM, int QB>
+int rows_pair(const RowsState* rs) { return rs ? rs->cg : 0; }
+
+template <int E, int NM, int QB, int CG>
 static void r_launch(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1, const Dev& D, const RPlan& P,
                      int grid, cudaStream_t s) {
   cudaLaunchConfig_t cfg{};
@@ -383,33 +508,41 @@ static void r_launch(const CUtensorMap& a, const CUtensorMap& b0, const CUtensor
   cfg.blockDim = dim3(kRThreads, 1, 1);
   cfg.dynamicSmemBytes = r_smem(P);
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;          // CTA pair on one TPC (CG = 2)
+  at[1].val.clusterDim.x = CG; at[1].val.clusterDim.y = 1; at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_rows<E, NM, QB>, a, b0, b1, D, P);
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, k_rows<E, NM, QB, CG>, a, b0, b1, D, P);
+}
+
+template <int CG>
+static void rows_go(const Dev& D, RowsState* rs, bool backward, RPlan& P, cudaStream_t s) {
+  P.ntiles = cdiv(P.hi - P.lo, 128 * CG) * P.nut;
+  const int grid = std::min(P.ntiles * CG, rs->num_sms / CG * CG);
+  const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
+  if (lstm) {
+    if (!backward) {
+      if (D.N == 1) r_launch<EPI_LSTM_FWD, 1, 1, CG>(rs->A_hk, rs->B_fwd, rs->B_fwd, D, P, grid, s);
+      else r_launch<EPI_LSTM_FWD, 2, 1, CG>(rs->A_hk, rs->B_fwd, rs->B_fwd, D, P, grid, s);
+    } else {
+      if (D.N == 1) r_launch<EPI_LSTM_BWD, 1, 1, CG>(rs->A_dz, rs->B_bwd0, rs->B_bwd1, D, P, grid, s);
+      else r_launch<EPI_LSTM_BWD, 2, 1, CG>(rs->A_dz, rs->B_bwd0, rs->B_bwd1, D, P, grid, s);
+    }
+  } else {
+    if (!backward) r_launch<EPI_FC_FWD, 1, 2, CG>(rs->A_hk, rs->B_fwd, rs->B_fwd, D, P, grid, s);
+    else r_launch<EPI_FC_BWD, 1, 2, CG>(rs->A_dz, rs->B_bwd0, rs->B_bwd1, D, P, grid, s);
+  }
 }
 
 bool rows_level(const Dev& D, RowsState* rs, bool backward, int lo, int hi, cudaStream_t s) {
   if (!rs || hi <= lo) return false;
   RPlan P = backward ? rs->bwd : rs->fwd;
   P.lo = lo; P.hi = hi;
-  P.ntiles = cdiv(hi - lo, 128) * P.nut;
-  const int grid = std::min(P.ntiles, rs->num_sms);
-  const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
-  if (lstm) {
-    if (!backward) {
-      if (D.N == 1) r_launch<EPI_LSTM_FWD, 1, 2>(rs->A_hk, rs->B_fwd, rs->B_fwd, D, P, grid, s);
-      else r_launch<EPI_LSTM_FWD, 2, 2>(rs->A_hk, rs->B_fwd, rs->B_fwd, D, P, grid, s);
-    } else {
-      if (D.N == 1) r_launch<EPI_LSTM_BWD, 1, 2>(rs->A_dz, rs->B_bwd0, rs->B_bwd1, D, P, grid, s);
-      else r_launch<EPI_LSTM_BWD, 2, 2>(rs->A_dz, rs->B_bwd0, rs->B_bwd1, D, P, grid, s);
-    }
-  } else {
-    if (!backward) r_launch<EPI_FC_FWD, 1, 4>(rs->A_hk, rs->B_fwd, rs->B_fwd, D, P, grid, s);
-    else r_launch<EPI_FC_BWD, 1, 4>(rs->A_dz, rs->B_bwd0, rs->B_bwd1, D, P, grid, s);
-  }
+  if (rs->cg == 2) rows_go<2>(D, rs, backward, P, s);
+  else rows_go<1>(D, rs, backward, P, s);
   return true;
 }
 

@@ -506,7 +506,8 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
       t->rs = rows_init(D, max_vertices);
       const char* mt = std::getenv("CAVS_ROWS_MIN_TILES");
       if (mt) t->rows_min_tiles = std::atoi(mt);
-      if (t->rs) t->info += "; large tasks: row-tiled tcgen05 (>= " + std::to_string(t->rows_min_tiles) + " tiles)";
+      if (t->rs) t->info += "; large tasks: row-tiled tcgen05 (>= " + std::to_string(t->rows_min_tiles) + " tiles" +
+                            (rows_pair(t->rs) == 2 ? ", CTA pairs)" : ")");
     }
   }
   t->info += D.lazy_off ? "; lazy batching OFF (ablation: per-task weight-gradient GEMMs)"
