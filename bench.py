@@ -350,14 +350,22 @@ def main():
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
         hp = dict(gp=pin(hb.graph_ptr), cp=pin(hb.child_ptr), ci=pin(hb.child_idx), pr=pin(params.cpu().numpy()),
                   x=pin(hb.x), xr=pin(hb.x_row), g=pin(hb.gamma))
+        # the cotangent rows of the loss vertices (roots for trees, every step for chains): the
+        # pipelined entry takes Gamma as rows + values (cavs_train_step_host_async)
+        g_rows = np.nonzero(np.abs(hb.gamma).sum(axis=1))[0].astype(np.int32)
+        hpa = dict(hp, g=pin(hb.gamma[g_rows]), grow=pin(g_rows))
         hdp = torch.empty(ctx.P, dtype=torch.float32).pin_memory()
-        h2d = sum(v.numel() * v.element_size() for v in hp.values())
+        h2d = sum(v.numel() * v.element_size() for v in (hpa if world == 1 else hp).values())
         d2h = hdp.numel() * 4
         dv = {k: torch.empty_like(v, device=dev) for k, v in hp.items()}
 
+        def e2e_sync_step():                        # one synchronous C-ABI call: H2D, step, D2H
+            ctx.train_step_host(hp["gp"], hp["cp"], hp["ci"], hp["pr"], hp["x"], hp["xr"], hp["g"], hdp)
+
         def e2e_step():
-            if world == 1:                          # one C-ABI call: H2D, schedule, fwd, bwd, D2H
-                ctx.train_step_host(hp["gp"], hp["cp"], hp["ci"], hp["pr"], hp["x"], hp["xr"], hp["g"], hdp)
+            if world == 1:                          # pipelined C-ABI call: H2D of this step overlaps the last
+                ctx.train_step_host_async(hpa["gp"], hpa["cp"], hpa["ci"], hpa["pr"], hpa["x"], hpa["xr"], hpa["g"],
+                                          hdp, gamma_rows=hpa["grow"])
                 return
             for k, v in hp.items():                 # N > 1: the same copies around the data-parallel step
                 dv[k].copy_(v, non_blocking=True)
@@ -373,22 +381,39 @@ def main():
 
         for _ in range(max(1, args.warmup)):
             e2e_step()
+        if world == 1:
+            ctx.sync()
         e_steps = max(3, args.steps // 2)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(e_steps):
             e2e_step()
+        if world == 1:
+            ctx.sync()                              # every step's dparams are on the host
         e_ms = 1000 * (time.perf_counter() - t0) / e_steps
+        sync_ms = None
+        if world == 1:                              # context: the synchronous single-call step
+            e2e_sync_step()
+            t0 = time.perf_counter()
+            for _ in range(e_steps):
+                e2e_sync_step()
+            sync_ms = 1000 * (time.perf_counter() - t0) / e_steps
         if world > 1:
             tt = torch.tensor([e_ms], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e_ms = float(tt.item())
         e2e = {"value": samples / (e_ms / 1000), "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms,
-               "note": ("cavs_train_step_host" if world == 1 else "copies + step + bucketed NCCL all-reduce") +
+               "note": ("cavs_train_step_host_async (two steps in flight: the next step's H2D overlaps this "
+                        "step's compute; Gamma as the loss vertices' rows)" if world == 1 else
+                        "copies + step + bucketed NCCL all-reduce, synchronised each step") +
                        ": pinned host CSR/params/x/x_row/Gamma -> device, schedule, fwd, bwd, "
-                       "dparams -> host, synchronised each step (host wall clock, max over ranks)"}
+                       "dparams -> host every step (host wall clock over the steps, max over ranks)"}
+        if sync_ms:
+            e2e["sync_single_call"] = {"value": samples / (sync_ms / 1000), "ms_per_step": sync_ms,
+                                       "h2d_bytes_per_step": int(sum(v.numel() * v.element_size() for v in hp.values())),
+                                       "note": "cavs_train_step_host: dense Gamma, synchronised every step"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.inference:

@@ -190,6 +190,26 @@ cavs_status cavs_train_step_host(cavs_ctx* ctx, int32_t K, int32_t V, int32_t E,
                                  const float* x, const int32_t* x_row, const float* dh_out,
                                  float* dparams, float* dx, float* h_out);
 
+/* Pipelined end-to-end training step from HOST buffers (r02): the same work as
+ * cavs_train_step_host (H2D of this step's inputs, load / schedule / forward / backward, D2H of
+ * dparams) but ASYNCHRONOUS: the H2D copies run on the context's own copy stream and overlap the
+ * previous step's compute, the D2H of dparams on a second copy stream; two staging slots, so at most
+ * two steps are in flight and a slot is reused only after the step that last used it has copied
+ * its dparams out.  The call returns after enqueueing (it may wait for the previous step's
+ * schedule header, see cavs_schedule); call cavs_sync before reading `dparams` or reusing the host
+ * input buffers of the last two steps.  Host buffers must be pinned.
+ *   gamma_rows != NULL: the push cotangent is given for n_gamma vertices only (e.g. the roots that
+ *                       carry a loss): gamma [n_gamma, h] rows of dL/dh at global vertex ids
+ *                       gamma_rows[i]; every other vertex has dL/dh = 0.
+ *   gamma_rows == NULL: gamma is the dense [V, h] cotangent (n_gamma = V), or n_gamma = 0 (all zero).
+ *   dparams [P] host fp32: dL/dparams of this step (valid after cavs_sync).
+ * Errors: as cavs_train_step_host; CAVS_E_INVALID for inconsistent gamma arguments. */
+cavs_status cavs_train_step_host_async(cavs_ctx* ctx, int32_t K, int32_t V, int32_t E,
+                                       const int32_t* graph_ptr, const int32_t* child_ptr,
+                                       const int32_t* child_idx, const float* params, int32_t n_x,
+                                       const float* x, const int32_t* x_row, int32_t n_gamma,
+                                       const int32_t* gamma_rows, const float* gamma, float* dparams);
+
 /* Next-word softmax head (§5 P:L606 "predicts the next word"): the
  * loss lives outside (F, G) (reading Z9) and is wired to F through push (h_out) and push's adjoint
  * (dh_out = dL/dh).  This is its fused softmax / cross-entropy / gradient pass over the logits of

@@ -58,6 +58,7 @@ def _load():
         "cavs_sync": (S, [P]),
         "cavs_set_grad_event": (S, [P, P]),
         "cavs_softmax_xent": (S, [P, I32, I32, P, P, P, ctypes.c_float, P]),
+        "cavs_train_step_host_async": (S, [P, I32, I32, I32, P, P, P, P, I32, P, P, I32, P, P, P]),
         "cavs_last_error": (ctypes.c_char_p, [P]),
         "cavs_path_info": (ctypes.c_char_p, [P]),
         "cavs_profile": (S, [P, ctypes.c_int]),
@@ -77,7 +78,7 @@ def _load():
 _lib = _load()
 EXPORTS = ["cavs_param_count", "cavs_create", "cavs_set_stream", "cavs_workspace_bytes",
            "cavs_set_workspace", "cavs_load_graphs", "cavs_schedule", "cavs_get_schedule",
-           "cavs_forward", "cavs_forward_inference", "cavs_backward", "cavs_train_step_host", "cavs_kernel_launches", "cavs_sync", "cavs_set_grad_event", "cavs_softmax_xent",
+           "cavs_forward", "cavs_forward_inference", "cavs_backward", "cavs_train_step_host", "cavs_kernel_launches", "cavs_sync", "cavs_set_grad_event", "cavs_softmax_xent", "cavs_train_step_host_async",
            "cavs_last_error", "cavs_path_info", "cavs_destroy", "cavs_profile", "cavs_profile_read"]
 PHASES = ["schedule", "prep", "xproj", "fwd_levels", "bwd_roots", "bwd_levels", "lazy", "dx", "reduce"]
 
@@ -287,6 +288,23 @@ class Context:
             self._ctx, K, V, E, _ptr(graph_ptr, "i32", **H), _ptr(child_ptr, "i32", **H), _ptr(child_idx, "i32", **H),
             _ptr(params, "f32", **H), int(x.shape[0]), _ptr(x, "f32", **H), _ptr(x_row, "i32", **H),
             _ptr(dh_out, "f32", **H), _ptr(dparams, "f32", **H), _ptr(dx, "f32", **H), _ptr(h_out, "f32", **H)))
+        self.V, self.K = V, K
+
+    def train_step_host_async(self, graph_ptr, child_ptr, child_idx, params, x, x_row, gamma, dparams,
+                              gamma_rows=None):
+        """cavs_train_step_host_async: pipelined step from pinned HOST arrays; `gamma` is dense [V, h] or,
+        with `gamma_rows`, the cotangent rows of those vertices only.  Call sync() before reading dparams."""
+        K = int(graph_ptr.shape[0]) - 1
+        V = int(child_ptr.shape[0]) - 1
+        E = int(child_idx.shape[0])
+        H = dict(device=self.device, host_ok=True)
+        n_g = int(gamma.shape[0]) if gamma is not None else 0
+        self._keep_async = getattr(self, "_keep_async", [])[-3:] + [(graph_ptr, child_ptr, child_idx, params, x, x_row,
+                                                                     gamma, gamma_rows, dparams)]
+        self._check(_lib.cavs_train_step_host_async(
+            self._ctx, K, V, E, _ptr(graph_ptr, "i32", **H), _ptr(child_ptr, "i32", **H), _ptr(child_idx, "i32", **H),
+            _ptr(params, "f32", **H), int(x.shape[0]), _ptr(x, "f32", **H), _ptr(x_row, "i32", **H), n_g,
+            _ptr(gamma_rows, "i32", **H), _ptr(gamma, "f32", **H), _ptr(dparams, "f32", **H)))
         self.V, self.K = V, K
 
     def close(self):

@@ -39,6 +39,16 @@ struct cavs_ctx {
   cudaEvent_t ev_hdr = nullptr; // recorded after the schedule header's device->host copy
   cudaEvent_t ev_wgrad = nullptr;   // caller's event: recorded once dparams' weight blocks are final
   XStream xs;                   // streaming ablation: side stream + per-task events
+  // pipelined host-buffer steps (cavs_train_step_host_async): two staging slots, H2D / D2H streams
+  struct Slot {
+    int *gp = nullptr, *cp = nullptr, *ci = nullptr, *xrow = nullptr, *grow = nullptr;
+    float *params = nullptr, *x = nullptr, *gval = nullptr, *dp = nullptr;
+    cudaEvent_t copied = nullptr, done = nullptr;
+    bool used = false;
+  } slot[2];
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_bwd = nullptr;
+  int64_t n_async = 0;
   bool hdr_pending = false;     // header copied asynchronously, not parsed yet
 };
 
@@ -113,6 +123,10 @@ static size_t carve(cavs_ctx* c, char* base) {
   c->s_x = F(X * dd); c->s_dx = F(X * dd);
   c->s_dh = F(V * h); c->s_hout = F(V * h);
   c->s_xrow = I(V); c->s_gp = I(K + 1); c->s_cp = I(V + 1); c->s_ci = I(V + 1);
+  for (auto& sl : c->slot) {                  // cavs_train_step_host_async staging
+    sl.gp = I(K + 1); sl.cp = I(V + 1); sl.ci = I(N * V + 1); sl.xrow = I(V); sl.grow = I(V);
+    sl.params = F(P); sl.x = F(X * dd); sl.gval = F(V * h); sl.dp = F(P);
+  }
   return (off + 255) & ~(size_t)255;
 }
 
@@ -451,6 +465,77 @@ CAVS_API cavs_status cavs_train_step_host(cavs_ctx* ctx, int32_t K, int32_t V, i
   return cavs_sync(ctx);
 }
 
+// Pipelined end-to-end step (include/cavs.h): H2D of step i+1 on its own stream overlaps step i's
+// compute, D2H of dparams on a third stream; two staging slots, reused once the step that last
+// used the slot finished its D2H.  Cotangents may come as rows + values (the loss vertices).
+CAVS_API cavs_status cavs_train_step_host_async(cavs_ctx* ctx, int32_t K, int32_t V, int32_t E,
+                                                const int32_t* graph_ptr, const int32_t* child_ptr,
+                                                const int32_t* child_idx, const float* params, int32_t n_x,
+                                                const float* x, const int32_t* x_row, int32_t n_gamma,
+                                                const int32_t* gamma_rows, const float* gamma, float* dparams) {
+  if (!ctx) return CAVS_E_INVALID;
+  if (ctx->state < S_READY) return fail(ctx, CAVS_E_STATE, "set_workspace first");
+  const cavs_desc& d = ctx->desc;
+  if (n_x < 0 || n_x > d.max_x || V > d.max_vertices || V < 1 || K < 1 || K > d.max_graphs || E < 0 ||
+      (int64_t)E > (int64_t)d.N * d.max_vertices)
+    return fail(ctx, CAVS_E_CAPACITY, "batch exceeds capacity");
+  if (!graph_ptr || !child_ptr || (E && !child_idx) || !params || !x_row || !dparams || (n_x && !x) ||
+      n_gamma < 0 || n_gamma > V || (n_gamma && !gamma) || (!gamma_rows && n_gamma != V && n_gamma != 0))
+    return fail(ctx, CAVS_E_INVALID, "null pointer or bad sizes");
+  CK(cudaSetDevice(ctx->device));
+  if (!ctx->h2d) {
+    CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_bwd, cudaEventDisableTiming));
+    for (auto& sl : ctx->slot) {
+      CK(cudaEventCreateWithFlags(&sl.copied, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    }
+  }
+  const size_t P = cavs_param_count(d.cell, d.N, d.h, d.d);
+  auto& sl = ctx->slot[ctx->n_async & 1];
+  ++ctx->n_async;
+  // ---- H2D of this step's inputs (waits only for the step that last used this slot) ----
+  if (sl.used) CK(cudaStreamWaitEvent(ctx->h2d, sl.done, 0));
+  sl.used = true;
+  cudaStream_t c = ctx->h2d;
+  CK(cudaMemcpyAsync(sl.gp, graph_ptr, sizeof(int) * (K + 1), cudaMemcpyHostToDevice, c));
+  CK(cudaMemcpyAsync(sl.cp, child_ptr, sizeof(int) * (V + 1), cudaMemcpyHostToDevice, c));
+  if (E) CK(cudaMemcpyAsync(sl.ci, child_idx, sizeof(int) * E, cudaMemcpyHostToDevice, c));
+  CK(cudaMemcpyAsync(sl.params, params, sizeof(float) * P, cudaMemcpyHostToDevice, c));
+  if (n_x) CK(cudaMemcpyAsync(sl.x, x, sizeof(float) * n_x * d.d, cudaMemcpyHostToDevice, c));
+  CK(cudaMemcpyAsync(sl.xrow, x_row, sizeof(int) * V, cudaMemcpyHostToDevice, c));
+  if (n_gamma) CK(cudaMemcpyAsync(sl.gval, gamma, sizeof(float) * n_gamma * d.h, cudaMemcpyHostToDevice, c));
+  if (n_gamma && gamma_rows) CK(cudaMemcpyAsync(sl.grow, gamma_rows, sizeof(int) * n_gamma, cudaMemcpyHostToDevice, c));
+  CK(cudaEventRecord(sl.copied, c));
+  // ---- compute on the context's stream ----
+  cudaStream_t s = ctx->stream;
+  CK(cudaStreamWaitEvent(s, sl.copied, 0));
+  cavs_status st = cavs_load_graphs(ctx, K, V, E, sl.gp, sl.cp, sl.ci, 1);
+  if (st) return st;
+  st = cavs_schedule(ctx, nullptr);
+  if (st) return st;
+  float* dh = ctx->s_dh;                       // dense push cotangent (a single buffer: stream-ordered)
+  if (gamma_rows) {
+    CK(cudaMemsetAsync(dh, 0, sizeof(float) * (size_t)V * d.h, s));
+    launch_scatter_rows(dh, sl.gval, sl.grow, n_gamma, d.h, s);
+  } else if (n_gamma) {
+    dh = sl.gval;
+  } else {
+    CK(cudaMemsetAsync(dh, 0, sizeof(float) * (size_t)V * d.h, s));
+  }
+  st = cavs_forward(ctx, sl.params, n_x, sl.x, sl.xrow, ctx->s_hout);
+  if (st) return st;
+  st = cavs_backward(ctx, dh, sl.dp, nullptr);
+  if (st) return st;
+  CK(cudaEventRecord(ctx->ev_bwd, s));
+  // ---- D2H of the step's result ----
+  CK(cudaStreamWaitEvent(ctx->d2h, ctx->ev_bwd, 0));
+  CK(cudaMemcpyAsync(dparams, sl.dp, sizeof(float) * P, cudaMemcpyDeviceToHost, ctx->d2h));
+  CK(cudaEventRecord(sl.done, ctx->d2h));
+  return CAVS_OK;
+}
+
 CAVS_API cavs_status cavs_set_grad_event(cavs_ctx* ctx, void* cuda_event) {
   if (!ctx) return CAVS_E_INVALID;
   ctx->ev_wgrad = static_cast<cudaEvent_t>(cuda_event);
@@ -461,6 +546,7 @@ CAVS_API cavs_status cavs_sync(cavs_ctx* ctx) {
   if (!ctx) return CAVS_E_INVALID;
   if (ctx->state < S_READY) return CAVS_OK;
   CK(cudaSetDevice(ctx->device));
+  if (ctx->d2h) CK(cudaStreamSynchronize(ctx->d2h));   // pipelined host-buffer steps
   CK(cudaMemcpyAsync(ctx->h_hdr + kHdrWords + kReadback - 1, ctx->D.hdr + 3, sizeof(int), cudaMemcpyDeviceToHost,
                      ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -534,6 +620,13 @@ CAVS_API void cavs_destroy(cavs_ctx* ctx) {
     for (cudaEvent_t e : ctx->xs.ev) cudaEventDestroy(e);
   }
   if (ctx->ev_hdr) cudaEventDestroy(ctx->ev_hdr);
+  if (ctx->h2d) {
+    cudaStreamSynchronize(ctx->d2h);
+    cudaStreamDestroy(ctx->h2d);
+    cudaStreamDestroy(ctx->d2h);
+    cudaEventDestroy(ctx->ev_bwd);
+    for (auto& sl : ctx->slot) { cudaEventDestroy(sl.copied); cudaEventDestroy(sl.done); }
+  }
   if (ctx->h_hdr) cudaFreeHost(ctx->h_hdr);
   delete ctx;
 }

@@ -394,6 +394,13 @@ static void unfused_t(const Dev& D, int epi, int lo, int hi, int g, cudaStream_t
   }
 }
 
+// dst[rows[i]] = src[i] for n rows of w floats (the push cotangents of the loss vertices)
+__global__ void k_scatter_rows(float* dst, const float* src, const int* rows, int n, int w) {
+  const size_t tot = (size_t)n * w;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x)
+    dst[(size_t)rows[i / w] * w + i % w] = src[i];
+}
+
 static int grid_for(size_t n, int block) { return (int)std::min<size_t>((n + block - 1) / block, 148 * 16); }
 
 void launch_prep(const Dev& D, cudaStream_t s) {
@@ -507,6 +514,11 @@ void launch_unfused(const Dev& D, int epi, int lo, int hi, cudaStream_t s) {
   const int g = grid_for((size_t)(hi - lo) * D.h, 256);
   if (D.prec == CAVS_BF16) unfused_t<__nv_bfloat16>(D, epi, lo, hi, g, s);
   else unfused_t<float>(D, epi, lo, hi, g, s);
+}
+
+void launch_scatter_rows(float* dst, const float* src, const int* rows, int n, int w, cudaStream_t s) {
+  if (n <= 0) return;
+  k_scatter_rows<<<grid_for((size_t)n * w, 256), 256, 0, s>>>(dst, src, rows, n, w);
 }
 
 }  // namespace cavs

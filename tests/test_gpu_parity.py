@@ -721,3 +721,35 @@ def test_ablations(abl, case, precision, monkeypatch):
     o = run_gpu(b, precision)
     assert marker not in o["ctx"].path_info()
     compare(b, g, o, FP32_TOL if precision == "fp32" else BF16_EMU_TOL, f"{abl} {case} {precision} vs default engine")
+
+
+# ------------------------------------------------------------------ pipelined host-buffer steps
+def test_train_step_host_async_matches_sync():
+    """cavs_train_step_host_async (two steps in flight, sparse root cotangents) gives bit-identical
+    dparams to the synchronous host-buffer step on the same batches (same kernels, same order)."""
+    bs = [gen.make_batch("tree_lstm", 2, 128, 128, "sst_tree", 6, seed=s) for s in (71, 72, 73)]
+    for b in bs[1:]:
+        b.params = bs[0].params
+    maxV = max(b.V for b in bs)
+    ctx = make_ctx(bs[0], "bf16", max_vertices=maxV, max_x=max(b.n_x for b in bs), max_graphs=6)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    ref = []
+    for b in bs:
+        dp = torch.empty(ctx.P).pin_memory()
+        ctx.train_step_host(pin(b.graph_ptr), pin(b.child_ptr), pin(b.child_idx), pin(b.params), pin(b.x),
+                            pin(b.x_row), pin(b.gamma), dp)
+        ref.append(dp.numpy().copy())
+    outs = []
+    keep = []
+    for rep in range(2):
+        for b in bs:
+            rows = np.nonzero(np.abs(b.gamma).sum(axis=1))[0].astype(np.int32)
+            dp = torch.empty(ctx.P).pin_memory()
+            args = (pin(b.graph_ptr), pin(b.child_ptr), pin(b.child_idx), pin(b.params), pin(b.x), pin(b.x_row),
+                    pin(b.gamma[rows]), dp)
+            keep.append(args)
+            ctx.train_step_host_async(*args, gamma_rows=pin(rows))
+            outs.append(dp)
+    ctx.sync()
+    for i, dp in enumerate(outs):
+        assert np.array_equal(dp.numpy(), ref[i % 3]), f"async step {i} differs"
