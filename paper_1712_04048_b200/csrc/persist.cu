@@ -58,6 +58,8 @@ struct PPlan {
   int acc0;                          // first TMEM column of the accumulators
   int max_ni;                        // largest task tile index (NT = 16 << ni) the TMEM budget admits
   int nub, R;
+  int mc;                            // 1: B boxes multicast to the whole cluster (every CTA of a graph
+                                     //    range reads the same task rows): one TMA per box per cluster
   int xs_off, meta_off, bar_off;
 };
 
@@ -83,6 +85,16 @@ template <int E, int NM> struct PLay {
 
 // MMA issue of one task's tiles (NT compile-time: constant instruction descriptor, accumulator
 // columns and descriptor strides; only 32-bit adds per tcgen05.mma).
+// stage-free arrival: this CTA's MMAs of the stage are done -> the stage's empty barrier of this CTA,
+// or (multicast plan) of every CTA of the cluster, since any of them may issue the stage's next box
+__device__ __forceinline__ void stage_commit(uint64_t* bar, int mc, uint32_t mask) {
+  if (mc)
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(ptx::smem_u32(bar)), "h"((uint16_t)mask) : "memory");
+  else
+    ptx::mma_commit(bar);
+}
+
 template <int NT, bool TS>
 __device__ __forceinline__ void mma_level(const PPlan& P, int ntile, uint32_t a_lo, uint32_t b_lo,
                                           uint64_t* full, uint64_t* empty, uint64_t* done, uint64_t* tmem_empty,
@@ -123,7 +135,7 @@ __device__ __forceinline__ void mma_level(const PPlan& P, int ntile, uint32_t a_
           bl += (NT * 128) >> 4;
           if (++kbi == nkbA) { kbi = 0; d += NT; }
         }
-        ptx::mma_commit(&empty[s]);
+        stage_commit(&empty[s], P.mc, (1u << P.nub) - 1u);
       }
       __syncwarp();
       kba += cnt;                                     // advance (all lanes, uniform)
@@ -167,7 +179,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
   const int S = P.S;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], P.mc ? P.nub : 1); }
     ptx::mbar_init(done, 1);
     ptx::mbar_init(tmem_empty, 8);
     ptx::mbar_init(abar, P.ngrp);
@@ -220,9 +232,19 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
             const int s = step % S;
             if (s % kPProd != w) continue;
             const uint32_t ph = (step / S) & 1;
-            if (step >= S) pwait(&empty[s], ph ^ 1);
+            if (P.mc) pwait(&empty[s], ph);              // freed by every CTA of the cluster (phase 0: initial)
+            else if (step >= S) pwait(&empty[s], ph ^ 1);
             ptx::mbar_arrive_expect_tx(&full[s], bytes);
-            ptx::tma_load_3d(sB + s * P.stage, mb, 0, p0, P.seg_bcol[0] / 64 + b * sk, &full[s]);
+            if (!P.mc) {
+              ptx::tma_load_3d(sB + s * P.stage, mb, 0, p0, P.seg_bcol[0] / 64 + b * sk, &full[s]);
+            } else if (step % P.nub == ub) {             // this CTA's turn: one box for the whole cluster
+              asm volatile(
+                  "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+                  " [%0], [%1, {%2, %3, %4}], [%5], %6;"
+                  ::"r"(ptx::smem_u32(sB + s * P.stage)), "l"(reinterpret_cast<uint64_t>(mb)), "r"(0), "r"(p0),
+                    "r"(P.seg_bcol[0] / 64 + b * sk), "r"(ptx::smem_u32(&full[s])), "h"((uint16_t)((1u << P.nub) - 1u))
+                  : "memory");
+            }
           }
         }
       }
@@ -249,6 +271,14 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
         __syncwarp();
         pwait_warp(acopy, 0);
         ptx::tc_fence_after();
+      }
+      if (P.mc) {
+        // multicast plan: a peer may write this CTA's stages only once its weights left the staging
+        // area (tcgen05.cp above): the initial phase of every stage's empty barrier, in every CTA,
+        // completes with one arrival per CTA, issued when this thread's copies are done
+        if (ptx::elect_one())
+          for (int s2 = 0; s2 < S; ++s2) stage_commit(&empty[s2], 1, (1u << P.nub) - 1u);
+        __syncwarp();
       }
       const uint32_t a_lo = ((ptx::smem_u32(sA) >> 4) & 0x3FFF) | (1u << 16);
       const uint32_t b_lo = ((ptx::smem_u32(sB) >> 4) & 0x3FFF) | (1u << 16);
@@ -665,6 +695,11 @@ PersistState* persist_init(const Dev& D, int max_vertices, std::string* why) {
   }
   F.R = B.R = R = nc;
   if (ps->kbwd) pbwd_set_clusters(ps->kbwd, nc);
+  // opt-in (CAVS_PERSIST_MC=1): one multicast TMA per B box per cluster instead of one load per CTA.
+  // Parity-tested, but measured 1-3 % slower at cfg2/3/4 (the per-task chain is latency-bound and
+  // a multicast stage can be refilled only once all 16 CTAs freed it; profiles/r02_ablations.md)
+  const char* mce = std::getenv("CAVS_PERSIST_MC");
+  F.mc = B.mc = (mce && mce[0] == '1') ? 1 : 0;
   ps->fwd = F;
   ps->bwd = B;
   return ps;
@@ -683,6 +718,7 @@ std::string persist_describe(const PersistState* ps) {
   const PPlan& F = ps->fwd;
   const PPlan& B = ps->bwd;
   return "persistent: grid " + std::to_string(F.nub * F.R) + " (units/CTA " + std::to_string(F.UG) + ", " +
+         (F.mc ? "B boxes multicast per cluster, " : "") +
          std::to_string(F.R) + " clusters of " + std::to_string(F.nub) + " over graph ranges), weights in " + (F.tsA ? "TMEM" : "smem") + ", stages fwd " + std::to_string(F.S) +
          " bwd " + std::to_string(B.S) + ", max task tile fwd " + std::to_string(16 << F.max_ni) + " bwd " +
          std::to_string(16 << B.max_ni) +
