@@ -174,9 +174,11 @@ cavs_status cavs_forward_inference(cavs_ctx* ctx, const float* params, int32_t n
  * gradients are lazily batched over all vertices once after the level loop (§3.5).
  *   dh_out  [V, h]   device fp32: dL/d(push h) of every vertex (the external loss's cotangent)
  *   dparams [P]      device fp32, OVERWRITTEN with dL/dparams summed over all K graphs
- *   dx      [n_x, d] device fp32, OVERWRITTEN with dL/dx (may be NULL): zeroed, then every vertex's
- *                    pull adjoint W^T dz is added into its record's row; records no
- *                    vertex pulls stay 0.  Deterministic when each record is pulled at most once.
+ *   dx      [n_x, d] device fp32, OVERWRITTEN with dL/dx (may be NULL): row r = the sum over the
+ *                    vertices that pull record r of their pull adjoint W^T dz; rows
+ *                    of records no vertex pulls are 0.  Deterministic when each record is pulled at
+ *                    most once (then every row is written by one store; records pulled by several
+ *                    vertices are accumulated with atomic adds after a zero fill).
  * Errors: CAVS_E_STATE (no forward since the last schedule), CAVS_E_INVALID. */
 cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dparams, float* dx);
 

@@ -49,10 +49,11 @@ struct cavs_ctx {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t ev_bwd = nullptr;
   int64_t n_async = 0;
+  unsigned pull_gen = 0;
   bool hdr_pending = false;     // header copied asynchronously, not parsed yet
 };
 
-static constexpr int kHdrWords = 4;
+static constexpr int kHdrWords = 6;
 static constexpr int kReadback = 1024;
 
 static cavs_status fail(cavs_ctx* c, cavs_status s, const std::string& m) {
@@ -94,7 +95,7 @@ static size_t carve(cavs_ctx* c, char* base) {
   D.tile_cnt = I(kLazyMaxTiles + kDbMaxBlocks + 1);   // + the schedule's last-CTA counter
   D.crow = I((V + 1) * (kMaxClusters + 1));
   D.order = I(V); D.child_pos = I(V * N); D.parent_pos = I(V); D.slot = I(V); D.deg = I(V);
-  D.xrow_pos = I(Vp); D.tile_x = I(Vp / 64 + 2);
+  D.xrow_pos = I(Vp); D.tile_x = I(Vp / 64 + 2); D.xseen = I(X + 1);
   D.Hk = take(Vp * N * h * es);
   D.Hs = nullptr;                              // U h~ is accumulated as sum_k U h_k: no h~ arena
   D.Xp = take(Vp * dd * es);
@@ -365,6 +366,7 @@ static cavs_status forward_impl(cavs_ctx* ctx, const float* params, int32_t n_x,
   Dev& D = ctx->D;
   D.params = params; D.x = x; D.x_row = x_row; D.h_out = h_out; D.n_x = n_x;
   D.infer = infer ? 1 : 0;                 // (a DAG batch gathers c from the leaves' saved state: see below)
+  D.xgen = ++ctx->pull_gen;                // k_pull stamps every record it pulls (duplicates -> ST_XDUP)
   Prof& P = ctx->prof;
   P.mark(CAVS_PH_PREP, ctx->stream);
   launch_prep(D, ctx->stream);
@@ -408,7 +410,10 @@ CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dp
   Dev& D = ctx->D;
   D.dh_out = dh_out; D.dparams = dparams; D.dx = dx;
   Prof& P = ctx->prof;
-  if (dx && D.n_x > 0) CK(cudaMemsetAsync(dx, 0, sizeof(float) * (size_t)D.n_x * D.d, ctx->stream));   // dx is accumulated
+  // dx rows receive plain stores when every record is pulled exactly once (the usual case); the
+  // zeroing + atomic adds only run when some record is pulled by several vertices or by none
+  // (k_pull's ST_XDUP bit / pull count; decided on the device by k_dx_zero and the DX epilogue)
+  if (dx && D.n_x > 0) { launch_dx_zero(D, ctx->stream); P.count(1); }
   P.mark(CAVS_PH_BWD_ROOTS, ctx->stream);
   if (!D.dag) {                                // DAG batches: every vertex's dF runs in launch_dag_df
     launch_roots(D, ctx->n_roots, D.roots, ctx->stream);

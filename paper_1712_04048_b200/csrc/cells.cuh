@@ -441,7 +441,10 @@ template <> struct EpiK<EPI_DX> {
   template <class OpT, int VW, int NM = kMaxN>
   static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const FV<VW>* acc,
                                                const In<VW, NM>&, const UnitC<VW>&) {
-    if (m.xrow >= 0) addv<VW>(D.dx + (size_t)m.xrow * D.d + j, acc[0]);
+    if (m.xrow < 0) return;
+    float* dst = D.dx + (size_t)m.xrow * D.d + j;
+    if (D.hdr[3] & ST_XDUP) addv<VW>(dst, acc[0]);   // a record pulled by several vertices: add
+    else stv<VW>(dst, acc[0]);                       // each record pulled at most once: one store
   }
 };
 

@@ -117,6 +117,7 @@ void launch_pack(const Dev& D, const int* split /*[3]*/, cudaStream_t s);   // s
 // unfused ablation: the cell epilogue `epi` of task rows [lo, hi) from D.raw
 void launch_unfused(const Dev& D, int epi, int lo, int hi, cudaStream_t s);
 void launch_dag_parents(const Dev& D, cudaStream_t s);
+void launch_dx_zero(const Dev& D, cudaStream_t s);   // zero dx unless every record is pulled exactly once
 void launch_scatter_rows(float* dst, const float* src, const int* rows, int n, int w, cudaStream_t s);
 void launch_dag_gather(const Dev& D, int lo, int hi, cudaStream_t s);
 void launch_dag_df(const Dev& D, int lo, int hi, cudaStream_t s);

@@ -33,6 +33,10 @@ __device__ __forceinline__ OpT* prep_dst(const Dev& D, int sel) {
 template <class OpT>
 __global__ void __launch_bounds__(256) k_prep(Dev D, PrepJobs J) {
   pdl_wait();
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {   // k_pull's statistics of this forward
+    D.hdr[4] = 0;
+    atomicAnd(D.hdr + 3, ~ST_XDUP);
+  }
   const PrepJob& jb = J.j[blockIdx.y];
   __shared__ float tile[32][33];
   if (jb.transpose) {
@@ -94,8 +98,11 @@ __global__ void k_pull(Dev D) {
         r = -1;
       }
       D.xrow_pos[p] = r;
+      if (r >= 0 && atomicExch(D.xseen + r, (int)D.xgen) == (int)D.xgen) atomicOr(D.hdr + 3, ST_XDUP);
     }
     s_r[threadIdx.x] = r;
+    const unsigned has = __ballot_sync(0xffffffffu, r >= 0);   // warps 0-1: count this block's pulls
+    if ((threadIdx.x & 31) == 0 && has) atomicAdd(D.hdr + 4, __popc(has));
   }
   const int any = __syncthreads_or(threadIdx.x < 64 && s_r[threadIdx.x] >= 0);
   if (threadIdx.x == 0) D.tile_x[blockIdx.x] = any;
@@ -401,6 +408,14 @@ __global__ void k_scatter_rows(float* dst, const float* src, const int* rows, in
     dst[(size_t)rows[i / w] * w + i % w] = src[i];
 }
 
+// dx must be zeroed unless every record is pulled exactly once (then every row gets one store)
+__global__ void k_dx_zero(Dev D) {
+  pdl_wait();
+  if (!(D.hdr[3] & ST_XDUP) && D.hdr[4] == D.n_x) return;
+  const size_t n = (size_t)D.n_x * D.d;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) D.dx[i] = 0.f;
+}
+
 static int grid_for(size_t n, int block) { return (int)std::min<size_t>((n + block - 1) / block, 148 * 16); }
 
 void launch_prep(const Dev& D, cudaStream_t s) {
@@ -519,6 +534,10 @@ void launch_unfused(const Dev& D, int epi, int lo, int hi, cudaStream_t s) {
 void launch_scatter_rows(float* dst, const float* src, const int* rows, int n, int w, cudaStream_t s) {
   if (n <= 0) return;
   k_scatter_rows<<<grid_for((size_t)n * w, 256), 256, 0, s>>>(dst, src, rows, n, w);
+}
+
+void launch_dx_zero(const Dev& D, cudaStream_t s) {
+  launch_pdl(k_dx_zero, dim3(grid_for((size_t)D.n_x * D.d, 256)), dim3(256), 0, s, D);
 }
 
 }  // namespace cavs

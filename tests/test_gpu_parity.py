@@ -753,3 +753,28 @@ def test_train_step_host_async_matches_sync():
     ctx.sync()
     for i, dp in enumerate(outs):
         assert np.array_equal(dp.numpy(), ref[i % 3]), f"async step {i} differs"
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_dx_records_pulled_never_or_twice(precision):
+    """pull's adjoint with x_row not a bijection: some records pulled by no vertex (their dx
+    rows must be 0), some by two vertices (their adjoints ADD); and a bijective batch on the
+    same context afterwards (plain stores, no zero fill) still matches the oracle."""
+    b = gen.make_batch("tree_lstm", 2, 64, 64, "sst_tree", 5, seed=81)
+    rng = np.random.default_rng(81)
+    n_x = b.n_x + 7                                   # 7 records nobody pulls
+    x = rng.uniform(-1, 1, size=(n_x, b.d)).astype(np.float32)
+    xr = b.x_row.copy()
+    has = np.nonzero(xr >= 0)[0]
+    xr[has] = rng.permutation(n_x)[:len(has)]
+    xr[has[:3]] = xr[has[3:6]]                        # 3 records pulled twice
+    b.x, b.x_row = x, xr.astype(np.int32)
+    g = run_gpu(b, precision)
+    r = run_oracle(b)
+    tol = FP32_TOL if precision == "fp32" else BF16_TOL
+    compare(b, g, r, tol, f"non-bijective pulls {precision}")
+    unused = np.setdiff1d(np.arange(n_x), b.x_row[b.x_row >= 0])
+    assert np.all(g["dx"][unused] == 0)
+    b2 = gen.make_batch("tree_lstm", 2, 64, 64, "sst_tree", 5, seed=82)
+    g2 = run_gpu(b2, precision, ctx=g["ctx"])
+    compare(b2, g2, run_oracle(b2), tol, f"bijective pulls after {precision}")
