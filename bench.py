@@ -178,10 +178,15 @@ def cpu_baseline(args, unit_batch):
     pool = OraclePool()
     wall, cpu, used = pool.run(b, list(range(n)))
     pool.close()
+    n1 = min(4, b.K)                                  # one core, one process
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):                        # BLAS of this process on one thread
+        one = _oracle_worker(_oracle_jobs(b, list(range(n1)), 1)[0])
     return {"value": n / wall, "unit": "samples/s", "cores": used, "kind": "oracle",
             "sample": f"{n} of the {b.K} graphs of batch seed 0 ({args.config}, h={b.h}), fp64 NumPy per-vertex "
                       f"evaluator, fwd+bwd, graphs split over {used} worker processes (1 thread each); "
-                      f"{cpu:.1f} CPU-s in {wall:.2f} s wall"}
+                      f"{cpu:.1f} CPU-s in {wall:.2f} s wall",
+            "one_core": {"value": n1 / one, "unit": "samples/s", "sample": f"graphs 0..{n1 - 1}, one process"}}
 
 
 # ------------------------------------------------------------------------------ reference arm
