@@ -93,24 +93,27 @@ __global__ void __launch_bounds__(256) k_graph_sched(Dev D) {
     while (true) {
       __shared__ int s_new;
       if (threadIdx.x == 0) s_new = 0;
-      __syncthreads();
+      // decide (read every level), then commit (write): no level is read and written in one phase
       for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        if (lev[i] >= 0) continue;
+        bool ready = lev[i] < 0;
         const int v = lo + i;
-        bool ready = true;
         for (int e = D.src_cp[v]; e < D.src_cp[v + 1] && ready; ++e) {
           const int l = lev[D.src_ci[e]];
           ready = l >= 0 && l < round;
         }
-        if (ready) { lev[i] = round; atomicAdd(&s_new, 1); }
+        pend[i] = ready ? 1 : 0;
       }
       __syncthreads();
-      const int got = s_new;
-      if (threadIdx.x == 0) s_tail += got;
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+        if (pend[i]) { lev[i] = round; atomicAdd(&s_new, 1); }
       __syncthreads();
+      const int got = s_new;
+      __syncthreads();                               // every thread read s_new before its reset
+      if (threadIdx.x == 0) s_tail += got;
       if (got == 0) break;
       ++round;
     }
+    __syncthreads();
   } else {
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     if (pend[i] == 0) {

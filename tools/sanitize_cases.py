@@ -25,6 +25,14 @@ CASES = {
     "rows": (dict(cell="tree_fc", N=2, h=640, d=640, shape="cbt16", K=2), "bf16", {"CAVS_ROWS_MIN_TILES": "1"}),
     "tc_level": (dict(cell="tree_lstm", N=2, h=128, d=128, shape="sst_tree", K=5), "bf16", {"CAVS_PERSIST": "0"}),
     "fp32": (dict(cell="tree_lstm", N=2, h=64, d=64, shape="sst_tree", K=4), "fp32", {}),
+    # round 2
+    "ksplit_bwd": (dict(cell="tree_lstm", N=2, h=256, d=256, shape="sst_tree", K=6), "bf16", {"CAVS_PBWD": "1"}),
+    "multicast": (dict(cell="tree_lstm", N=2, h=256, d=256, shape="sst_tree", K=6), "bf16", {"CAVS_PERSIST_MC": "1"}),
+    "rows_pair": (dict(cell="tree_fc", N=2, h=512, d=512, shape="cbt16", K=2), "bf16",
+                  {"CAVS_ROWS_MIN_TILES": "1", "CAVS_ROWS_PAIR": "1", "CAVS_PERSIST": "0"}),
+    "dag": (dict(cell="tree_lstm", N=2, h=128, d=128, shape="dag", K=5), "bf16", {}),
+    "ablations": (dict(cell="tree_lstm", N=2, h=128, d=128, shape="sst_tree", K=5), "bf16",
+                  {"CAVS_LAZY_BATCH": "0", "CAVS_UNFUSED": "1", "CAVS_STREAMING": "1"}),
 }
 
 
@@ -33,7 +41,12 @@ def run_case(name):
     from gpu_harness import rel, run_gpu, run_oracle
     from workloads import gen
     spec, prec, _ = CASES[name]
-    b = gen.make_batch(spec["cell"], spec["N"], spec["h"], spec["d"], spec["shape"], spec["K"], seed=1)
+    if spec["shape"] == "dag":                      # shared children and duplicate child ids
+        import test_gpu_parity as T
+        b = gen.batch_from_graphs(T._random_dags(spec["K"], spec["N"], 20, 1), cell=spec["cell"], N=spec["N"],
+                                  h=spec["h"], d=spec["d"], seed=1, x_at="all", loss_at="all")
+    else:
+        b = gen.make_batch(spec["cell"], spec["N"], spec["h"], spec["d"], spec["shape"], spec["K"], seed=1)
     g = run_gpu(b, prec)
     r = run_oracle(b)
     e = max(rel(g["h_out"], r["h_out"]), rel(g["dparams"], r["dparams"]), rel(g["dx"], r["dx"]))
