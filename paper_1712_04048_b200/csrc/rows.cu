@@ -319,10 +319,41 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
       ptx::tc_fence_after();
       const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * P.acc_cols);
       const int ub = hh * (P.UG / 2);                    // this thread's first unit within the tile
-      // VW units per item: 8 (one 32-byte sector per row and output stream: 256-bit accesses) except
-      // for the register-heavy Tree-LSTM backward (children's state in registers)
-      constexpr int VW = E == EPI_LSTM_BWD ? 4 : 8;
+      // VW units per item: 8 (one 32-byte sector per row and output stream: 256-bit accesses)
+      constexpr int VW = 8;
       const int ipt = P.UG / 2 / VW;                     // items per thread
+      if constexpr (E == EPI_LSTM_BWD) {
+        // Tree-LSTM backward: the children's dF one child at a time (its state in registers, 8 units
+        // per access), the gradient sent to child k = dh~ + U_f^T dz_fk (cells.cuh EpiK)
+        const int h = D.h, G = 3 + D.N;
+#pragma unroll 1
+        for (int it = 0; it < ipt; ++it) {
+          const int uo = ub + it * VW, jj = u0 + uo;
+          FV<VW> acc[NE];
+          fetch_acc<E, NM, VW>(tb, P.UG, uo, acc);
+#ifndef CAVS_ROWS_NOEPI
+          if (valid) {
+            const FV<VW> dcbp = ldv<VW>(D.dcb + (size_t)m.p * h + jj);
+#pragma unroll
+            for (int k = 0; k < NM; ++k) {
+              if (k >= m.deg) break;
+              const FV<VW> fpk = ldv<VW>(D.gates + (size_t)m.p * G * h + (3 + k) * h + jj);
+              LstmChildIn<VW, NM> cin;
+              lstm_child_load<VW, NM>(D, jj, m.ch[k], m.ch_vid[k], m.ch_deg[k], cin);
+              FV<VW> dh, dc;
+#pragma unroll
+              for (int e = 0; e < VW; ++e) {
+                dh.v[e] = acc[0].v[e] + acc[1 + k].v[e] + cin.dho.v[e];
+                dc.v[e] = dcbp.v[e] * fpk.v[e];
+              }
+              lstm_child_store<__nv_bfloat16, VW, NM>(D, jj, m.ch[k], m.ch_deg[k], dh, dc, cin);
+            }
+          }
+#else
+          if (valid && acc[0].v[0] == 12345.f) D.h_out[0] = acc[NE - 1].v[3];
+#endif
+        }
+      } else
 #pragma unroll 1
       for (int qb = 0; qb < ipt; qb += QB) {
         typename EpiK<E>::template In<VW, NM> in[QB];
