@@ -237,10 +237,18 @@ def main():
     from paper_1712_04048_b200 import Context, dp
     from workloads import gen
 
+    # CAVS_DIST_BACKEND=gloo (test only): several ranks may then share one GPU (NCCL refuses that),
+    # which exercises the sharded / bucketed data-parallel path on a single-GPU box
+    backend = os.environ.get("CAVS_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     # ---- inputs: a pool of batches resident in HBM before the timed region ----
     # strong scaling (default): pool batch i is ONE global batch (seed i, same on every rank), sharded
