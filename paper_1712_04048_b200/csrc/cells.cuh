@@ -130,13 +130,13 @@ template <int VW> __device__ __forceinline__ UnitC<VW> load_unit(const Dev& D, i
 
 // ---- Tree-LSTM helpers -----------------------------------------------------------
 // Finish F at (j.., p) given gate pre-activations (bias included) and the children's c.
-// CHK: honour Dev::infer (skip the activations dF needs).  Only the x-projection epilogue
-// (level-0 cells, half the vertices of a tree batch) checks it; the level kernels always store
-// (the check costs the register-bound persistent kernel ~5 us per pass).
-template <class OpT, int VW, int NM, bool CHK = false>
+// CHK: 0 = store the activations dF needs; 1 = honour Dev::infer at run time (the x-projection
+// epilogue: level-0 cells); 2 = inference kind (EPI_*_FWD_INF: a separate instantiation of the
+// level kernels, so the register-bound persistent kernel carries no run-time check).
+template <class OpT, int VW, int NM, int CHK = 0>
 __device__ __forceinline__ void lstm_finish(const Dev& D, int j, const VMeta& m, const FV<VW>& zi, const FV<VW>& zo,
                                             const FV<VW>& zu, const FV<VW>* zf, const FV<VW>* ck) {
-  const bool keep = !CHK || !D.infer;
+  const bool keep = CHK == 0 || (CHK == 1 && !D.infer);
   const int h = D.h, N = D.N, G = 3 + N;
   FV<VW> i, o, u, c, hv;
 #pragma unroll
@@ -275,7 +275,7 @@ template <> struct EpiK<EPI_LSTM_XPROJ> {
 #pragma unroll
         for (int e = 0; e < VW; ++e) zf[k].v[e] = acc[3].v[e] + b.b3.v[e];
       }
-      lstm_finish<OpT, VW, NM, true>(D, j, m, zi, zo, zu, zf, ck);
+      lstm_finish<OpT, VW, NM, 1>(D, j, m, zi, zo, zu, zf, ck);
     } else if (m.xrow >= 0) {
       float* xw = D.XW + (size_t)m.p * 4 * h + j;
       stv<VW>(xw, acc[0]); stv<VW>(xw + h, acc[1]); stv<VW>(xw + 2 * h, acc[2]); stv<VW>(xw + 3 * h, acc[3]);
@@ -317,13 +317,13 @@ template <> struct EpiK<EPI_LSTM_BWD> {
 };
 
 // ---- Tree-FC ------------------------------------------------------------------------
-template <class OpT, int VW, bool CHK = false>
+template <class OpT, int VW, int CHK = 0>
 __device__ __forceinline__ void fc_finish(const Dev& D, int j, const VMeta& m, const FV<VW>& z) {
   const int h = D.h;
   FV<VW> hv;
 #pragma unroll
   for (int e = 0; e < VW; ++e) hv.v[e] = act_tanh<OpT>(z.v[e]);
-  if (!CHK || !D.infer) stv<VW>(D.gates + (size_t)m.p * h + j, hv);   // h kept for dF (1 - h^2)
+  if (CHK == 0 || (CHK == 1 && !D.infer)) stv<VW>(D.gates + (size_t)m.p * h + j, hv);   // h kept for dF (1 - h^2)
   stv<VW>(D.h_out + (size_t)m.vid * h + j, hv);
   if (m.par >= 0) stv_op<OpT, VW>(op<OpT>(D.Hk) + (size_t)m.par * 2 * h + (size_t)m.slot * h + j, hv);
 }
@@ -354,10 +354,50 @@ template <> struct EpiK<EPI_FC_XPROJ> {
       FV<VW> z;
 #pragma unroll
       for (int e = 0; e < VW; ++e) z.v[e] = acc[0].v[e] + b.b0.v[e];
-      fc_finish<OpT, VW, true>(D, j, m, z);
+      fc_finish<OpT, VW, 1>(D, j, m, z);
     } else if (m.xrow >= 0) {
       stv<VW>(D.XW + (size_t)m.p * D.h + j, acc[0]);
     }
+  }
+};
+
+// Inference-only forward kinds: the training epilogue without the activations dF needs.
+template <> struct EpiK<EPI_LSTM_FWD_INF> {
+  template <int VW, int NM = kMaxN> using In = EpiK<EPI_LSTM_FWD>::In<VW, NM>;
+  template <int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void load(const Dev& D, int j, const VMeta& m, In<VW, NM>& in) {
+    EpiK<EPI_LSTM_FWD>::load<VW, NM>(D, j, m, in);
+  }
+  template <class OpT, int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const FV<VW>* acc,
+                                               const In<VW, NM>& in, const UnitC<VW>& b) {
+    FV<VW> zi, zo, zu, zf[NM];
+#pragma unroll
+    for (int e = 0; e < VW; ++e) {
+      zi.v[e] = acc[0].v[e] + in.xi.v[e] + b.b0.v[e];
+      zo.v[e] = acc[1].v[e] + in.xo.v[e] + b.b1.v[e];
+      zu.v[e] = acc[2].v[e] + in.xu.v[e] + b.b2.v[e];
+    }
+#pragma unroll
+    for (int k = 0; k < NM; ++k)
+#pragma unroll
+      for (int e = 0; e < VW; ++e) zf[k].v[e] = (k < D.N ? acc[3 + k].v[e] : 0.f) + in.xf.v[e] + b.b3.v[e];
+    lstm_finish<OpT, VW, NM, 2>(D, j, m, zi, zo, zu, zf, in.ck);
+  }
+};
+template <> struct EpiK<EPI_FC_FWD_INF> {
+  template <int VW, int NM = kMaxN> using In = EpiK<EPI_FC_FWD>::In<VW, NM>;
+  template <int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void load(const Dev& D, int j, const VMeta& m, In<VW, NM>& in) {
+    EpiK<EPI_FC_FWD>::load<VW, NM>(D, j, m, in);
+  }
+  template <class OpT, int VW, int NM = kMaxN>
+  static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const FV<VW>* acc,
+                                               const In<VW, NM>& in, const UnitC<VW>& b) {
+    FV<VW> z;
+#pragma unroll
+    for (int e = 0; e < VW; ++e) z.v[e] = acc[0].v[e] + in.xw.v[e] + b.b0.v[e];
+    fc_finish<OpT, VW, 2>(D, j, m, z);
   }
 };
 
@@ -452,10 +492,11 @@ template <int E> __host__ __device__ constexpr bool epi_needs_children() {
   return E == EPI_LSTM_BWD || E == EPI_FC_BWD;
 }
 template <int E> __host__ __device__ constexpr bool epi_uses_bias() {
-  return E == EPI_LSTM_FWD || E == EPI_LSTM_XPROJ || E == EPI_FC_FWD || E == EPI_FC_XPROJ;
+  return E == EPI_LSTM_FWD || E == EPI_LSTM_XPROJ || E == EPI_FC_FWD || E == EPI_FC_XPROJ || E == EPI_LSTM_FWD_INF ||
+         E == EPI_FC_FWD_INF;
 }
 template <int E> __host__ __device__ constexpr bool epi_is_lstm() {
-  return E == EPI_LSTM_FWD || E == EPI_LSTM_XPROJ || E == EPI_LSTM_BWD || E == EPI_LSTM_BWD_DAG;
+  return E == EPI_LSTM_FWD || E == EPI_LSTM_XPROJ || E == EPI_LSTM_BWD || E == EPI_LSTM_BWD_DAG || E == EPI_LSTM_FWD_INF;
 }
 
 // Does position p need this epilogue at all? (tile skipping for the x-kernels)

@@ -15,7 +15,12 @@ constexpr int kDbMaxBlocks = 64;      // arrival counters of the db column block
 constexpr int kSkinnyMax = 8;     // tasks with at most this many vertices use the skinny level kernel
 
 enum Epi : int { EPI_LSTM_FWD = 0, EPI_LSTM_XPROJ, EPI_LSTM_BWD, EPI_FC_FWD, EPI_FC_XPROJ, EPI_FC_BWD, EPI_DX,
-                 EPI_LSTM_BWD_DAG, EPI_FC_BWD_DAG };
+                 EPI_LSTM_BWD_DAG, EPI_FC_BWD_DAG,
+                 EPI_LSTM_FWD_INF, EPI_FC_FWD_INF };   // inference-only forward: no activations for dF
+// the training kind an inference kind computes like (same accumulators, same plan)
+__host__ __device__ constexpr int epi_base(int E) {
+  return E == EPI_LSTM_FWD_INF ? EPI_LSTM_FWD : E == EPI_FC_FWD_INF ? EPI_FC_FWD : E;
+}
 
 enum BSrc : int { B_HK = 0, B_XP = 1, B_DZ = 2 };
 

@@ -4,26 +4,28 @@
 //
 // Why: a level-by-level launch pays, per task V_t, a kernel launch + a fresh stream of F's
 // weights (2-8 MB) through the SMs, and the small tasks at the top of the trees are pure
-// latency.  Here every CTA keeps a fixed 128-row slice of the weights resident in shared
-// memory for the whole pass, and the tasks are separated by a grid-wide barrier instead of
-// kernel boundaries.
+// latency.  Here every CTA keeps a fixed 128-row slice of the weights resident in TMEM (staged
+// once through shared memory by TMA and copied with tcgen05.cp; the MMA takes A from TMEM) for the
+// whole pass, and the tasks are separated by a cluster-local barrier instead of kernel boundaries.
 //
 // Decomposition (swap-AB, like tc.cu): D[row, task] = sum_k A[row, k] B[task, k], M = 128 weight
-// rows, N = NT task rows (16/32/64 chosen per task so that the task spreads over the R
-// replicas), accumulators in TMEM.  The 128 rows of a CTA are ngrp "row groups" of UG units
-// each, every group a different gate (Tree-LSTM: i, o, u, f of the same 32 units, UG = 32;
-// Tree-FC: the two children's blocks of the same 64 units, UG = 64), so a CTA owns ALL the
-// gates of its units and the fused cell epilogue needs no inter-CTA exchange.  A group only
-// pairs with its own operand columns; where operands differ per group (backward: dz_i, dz_o,
-// dz_u, dz_f; Tree-FC forward: h_l, h_r) each operand gets its own accumulator and the
-// epilogue keeps the matching group — the wasted MMA rows are cheap next to the latency saved.
+// rows, N = NT task rows (16/32/64 chosen per task), accumulators in TMEM after the weights.  The
+// 128 rows of a CTA are ngrp "row groups" of UG units each, every group a different gate
+// (Tree-LSTM: i, o, u, f of the same 32 units, UG = 32; Tree-FC: the two children's blocks of the
+// same 64 units, UG = 64), so a CTA owns ALL the gates of its units and the fused cell epilogue
+// needs no inter-CTA exchange.  A group only pairs with its own operand columns; where operands
+// differ per group (backward: dz_i, dz_o, dz_u, dz_f; Tree-FC forward: h_l, h_r) each operand gets
+// its own accumulator and the epilogue keeps the matching group (the Tree-LSTM backward's
+// discarded rows: see persist_bwd.cu for the K-split alternative and why it is opt-in).
 //
-//   grid = nub x R CTAs (nub = h / UG unit blocks, R = replicas, all co-resident: 1 CTA/SM);
-//   CTA (ub, r) handles tiles j = r, r + R, ... of every task.
+//   grid = nub x R CTAs: R clusters (graph ranges; the graphs of a batch are independent,
+//   P:L388-391) of nub = h / UG unit-block CTAs, one CTA per SM; cluster r runs its own rows of
+//   every task (table crow[t][r], k_build_maps) and only its CTAs synchronise between tasks
+//   (cluster-scope mbarrier, persist_common.cuh).
 //   warps 0-2: TMA producers (weights once; then B boxes {64 k, NT rows, sk k-blocks} of the
 //              task rows, one warp per pipeline stage), warp 3: TMEM allocator + MMA issuer,
 //   warps 4-11: per-vertex metadata, TMEM -> smem staging, fused cell epilogue (cells.cuh),
-//              and the grid barrier between tasks.
+//              and the cluster task barrier.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -65,7 +67,8 @@ struct PPlan {
 
 // Compile-time staging layout per epilogue kind (matches the host plan of persist_init):
 // xs slot s holds one row group's accumulator(s); epilogue accumulator e sums slots.
-template <int E, int NM> struct PLay {
+template <int E0, int NM> struct PLay {
+  static constexpr int E = epi_base(E0);             // inference kinds: the training kind's layout
   static constexpr bool lstm = E == EPI_LSTM_FWD || E == EPI_LSTM_BWD;
   static constexpr int UG = lstm ? 32 : 64;
   static constexpr int NSLOT = lstm ? 3 + NM : 2;
@@ -672,12 +675,13 @@ PersistState* persist_init(const Dev& D, int max_vertices, std::string* why) {
   auto occ = [&](int a, int b) { nc = std::min(nc, std::min(a, b)); };
   if (lstm) {
     switch (N) {
-      case 1: occ(attr_and_clusters<EPI_LSTM_FWD, 4, 1>(plan_smem(F), nub), attr_and_clusters<EPI_LSTM_BWD, 2, 1>(plan_smem(B), nub)); break;
-      case 2: occ(attr_and_clusters<EPI_LSTM_FWD, 5, 2>(plan_smem(F), nub), attr_and_clusters<EPI_LSTM_BWD, 3, 2>(plan_smem(B), nub)); break;
-      case 3: occ(attr_and_clusters<EPI_LSTM_FWD, 6, 3>(plan_smem(F), nub), attr_and_clusters<EPI_LSTM_BWD, 4, 3>(plan_smem(B), nub)); break;
-      default: occ(attr_and_clusters<EPI_LSTM_FWD, 7, 4>(plan_smem(F), nub), attr_and_clusters<EPI_LSTM_BWD, 5, 4>(plan_smem(B), nub)); break;
+      case 1: attr_and_clusters<EPI_LSTM_FWD_INF, 4, 1>(plan_smem(F), nub); occ(attr_and_clusters<EPI_LSTM_FWD, 4, 1>(plan_smem(F), nub), attr_and_clusters<EPI_LSTM_BWD, 2, 1>(plan_smem(B), nub)); break;
+      case 2: attr_and_clusters<EPI_LSTM_FWD_INF, 5, 2>(plan_smem(F), nub); occ(attr_and_clusters<EPI_LSTM_FWD, 5, 2>(plan_smem(F), nub), attr_and_clusters<EPI_LSTM_BWD, 3, 2>(plan_smem(B), nub)); break;
+      case 3: attr_and_clusters<EPI_LSTM_FWD_INF, 6, 3>(plan_smem(F), nub); occ(attr_and_clusters<EPI_LSTM_FWD, 6, 3>(plan_smem(F), nub), attr_and_clusters<EPI_LSTM_BWD, 4, 3>(plan_smem(B), nub)); break;
+      default: attr_and_clusters<EPI_LSTM_FWD_INF, 7, 4>(plan_smem(F), nub); occ(attr_and_clusters<EPI_LSTM_FWD, 7, 4>(plan_smem(F), nub), attr_and_clusters<EPI_LSTM_BWD, 5, 4>(plan_smem(B), nub)); break;
     }
   } else {
+    attr_and_clusters<EPI_FC_FWD_INF, 1, 1>(plan_smem(F), nub);
     occ(attr_and_clusters<EPI_FC_FWD, 1, 1>(plan_smem(F), nub), attr_and_clusters<EPI_FC_BWD, 2, 1>(plan_smem(B), nub));
   }
   if (lstm) {                                          // the K-split backward shares the cluster table
@@ -730,12 +734,23 @@ void persist_forward(const Dev& D, PersistState* ps, int T, cudaStream_t s) {
   if (T <= 1) return;
   const PPlan& P = ps->fwd;
   if (D.cell == CAVS_CELL_TREE_LSTM) {
+    if (D.infer) {                                    // inference-only forward: no activations for dF
+      switch (D.N) {
+        case 1: launch_p<EPI_LSTM_FWD_INF, 4, 1>(ps->A_fwd, ps->B_hk, D, P, 1, T - 1, 1, s); break;
+        case 2: launch_p<EPI_LSTM_FWD_INF, 5, 2>(ps->A_fwd, ps->B_hk, D, P, 1, T - 1, 1, s); break;
+        case 3: launch_p<EPI_LSTM_FWD_INF, 6, 3>(ps->A_fwd, ps->B_hk, D, P, 1, T - 1, 1, s); break;
+        default: launch_p<EPI_LSTM_FWD_INF, 7, 4>(ps->A_fwd, ps->B_hk, D, P, 1, T - 1, 1, s); break;
+      }
+      return;
+    }
     switch (D.N) {
       case 1: launch_p<EPI_LSTM_FWD, 4, 1>(ps->A_fwd, ps->B_hk, D, P, 1, T - 1, 1, s); break;
       case 2: launch_p<EPI_LSTM_FWD, 5, 2>(ps->A_fwd, ps->B_hk, D, P, 1, T - 1, 1, s); break;
       case 3: launch_p<EPI_LSTM_FWD, 6, 3>(ps->A_fwd, ps->B_hk, D, P, 1, T - 1, 1, s); break;
       default: launch_p<EPI_LSTM_FWD, 7, 4>(ps->A_fwd, ps->B_hk, D, P, 1, T - 1, 1, s); break;
     }
+  } else if (D.infer) {
+    launch_p<EPI_FC_FWD_INF, 1, 1>(ps->A_fwd, ps->B_hk, D, P, 1, T - 1, 1, s);
   } else {
     launch_p<EPI_FC_FWD, 1, 1>(ps->A_fwd, ps->B_hk, D, P, 1, T - 1, 1, s);
   }
