@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--weak", action="store_true",
                     help="weak scaling: an independent batch of the config's size per rank (default: strong "
                          "scaling, ONE global batch sharded over the ranks by dp.shard_batch)")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="skip the CUDA-graph measurement (sync-free mode: one captured graph per pool batch)")
     ap.add_argument("--inference", action="store_true",
                     help="forward-only (cavs_forward_inference): inference samples/s, no backward")
     a = ap.parse_args()
@@ -328,6 +330,51 @@ def main():
     samples = world * b0.K if args.weak else glob[0].K      # graphs the whole job processed per step
     value = samples / (ms / 1000.0)
 
+    # ---- the same steps as CUDA-graph replays (sync-free mode: the host never reads the schedule;
+    #      one graph per pool batch captures load + schedule + forward + backward) ----
+    graph_line = None
+    if world == 1 and not args.inference and not args.no_graph:
+        try:
+            ctx.set_sync_free(True)
+        except Exception as e:                      # path without sync-free support (e.g. h > 512)
+            graph_line = {"unavailable": str(e)[:120]}
+        if graph_line is None:
+            side = torch.cuda.Stream(dev)
+            graphs = []
+            for i in range(len(pool)):
+                g = torch.cuda.CUDAGraph()
+                side.wait_stream(stream)
+                with torch.cuda.stream(side):
+                    with torch.cuda.graph(g, stream=side):
+                        ctx.set_stream(side)
+                        step(i)
+                graphs.append(g)
+            ctx.set_stream(stream)
+            for i in range(args.warmup):
+                graphs[i % len(graphs)].replay()
+            torch.cuda.synchronize()
+            gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+            for k in range(args.steps):
+                if not args.no_flush:
+                    flush_buf.zero_()
+                gev[k][0].record(stream)
+                graphs[(args.warmup + k) % len(graphs)].replay()
+                gev[k][1].record(stream)
+            torch.cuda.synchronize()
+            ctx.sync()                              # the steps' deferred status (valid batches: OK)
+            g_ms = sum(a.elapsed_time(b) for a, b in gev) / args.steps
+            graph_line = {"value": samples / (g_ms / 1000.0), "unit": "samples/s", "ms_per_step": g_ms,
+                          "note": "cavs_set_sync_free + one CUDA graph per pool batch (load, schedule, forward, "
+                                  "backward captured); replays timed like the eager steps (CUDA events per step, "
+                                  "L2 flushed between steps)"}
+            ctx.set_sync_free(False)
+            del graphs
+    eager_line = {"value": value, "ms_per_step": ms,
+                  "note": "the same steps launched eagerly (the host reads each batch's schedule header); the "
+                          "phase split and roofline below are measured on this pass"}
+    if graph_line and "value" in graph_line:       # headline: the graph replays (same kernels, no host gaps)
+        value, ms = graph_line["value"], graph_line["ms_per_step"]
+
     # ---- roofline of the dominant tensor-core phase (per launch = totals / launches) ----
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {}
@@ -350,7 +397,8 @@ def main():
         traffic = tr.get(f"{args.config}:{args.precision}:{dom}")
     roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if peak else None, "traffic": traffic, "peak_source": peak_src,
-                "launches": P["launches"], "avg_launch_us": 1000 * P["ms"] / max(1, P["launches"])}
+                "launches": P["launches"], "avg_launch_us": 1000 * P["ms"] / max(1, P["launches"]),
+                "pass": "eager steps (library per-phase CUDA events on the launching stream)"}
     phases = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
                   "TFLOP/s": (v["flops"] / (v["ms"] / 1000) / 1e12) if v["ms"] > 0 and v["flops"] else None,
                   "GB/s": (v["bytes"] / (v["ms"] / 1000) / 1e9) if v["ms"] > 0 and v["bytes"] else None}
@@ -392,6 +440,13 @@ def main():
             hdp.copy_(dparams, non_blocking=True)
             torch.cuda.current_stream(dev).synchronize()
 
+        e2e_sync_free = False
+        if world == 1:
+            try:                                    # the pipelined steps never wait for a schedule header
+                ctx.set_sync_free(True)
+                e2e_sync_free = True
+            except Exception:
+                pass
         for _ in range(max(1, args.warmup)):
             e2e_step()
         if world == 1:
@@ -405,6 +460,8 @@ def main():
         if world == 1:
             ctx.sync()                              # every step's dparams are on the host
         e_ms = 1000 * (time.perf_counter() - t0) / e_steps
+        if e2e_sync_free:
+            ctx.set_sync_free(False)
         sync_ms = None
         if world == 1:                              # context: the synchronous single-call step
             e2e_sync_step()
@@ -419,7 +476,8 @@ def main():
         e2e = {"value": samples / (e_ms / 1000), "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms,
                "note": ("cavs_train_step_host_async (two steps in flight: the next step's H2D overlaps this "
-                        "step's compute; Gamma as the loss vertices' rows)" if world == 1 else
+                        "step's compute; Gamma as the loss vertices' rows" +
+                        ("; sync-free mode" if world == 1 and e2e_sync_free else "") + ")" if world == 1 else
                         "copies + step + bucketed NCCL all-reduce, synchronised each step") +
                        ": pinned host CSR/params/x/x_row/Gamma -> device, schedule, fwd, bwd, "
                        "dparams -> host every step (host wall clock over the steps, max over ranks)"}
@@ -452,6 +510,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
+            "graph": graph_line,
+            "eager": eager_line,
             "clocks": clk,
             "phases": phases,
             "context": "paper (Titan X GM200, CUDA 8, precision not stated, SST): Cavs Tree-LSTM bs=256 "

@@ -226,6 +226,17 @@ cavs_status cavs_train_step_host_async(cavs_ctx* ctx, int32_t K, int32_t V, int3
 cavs_status cavs_softmax_xent(const float* logits, int32_t M, int32_t vocab, const int32_t* target, float* loss,
                               float* dlogits, float scale, void* stream);
 
+/* Sync-free mode (r02): with `on` != 0 the host never reads the schedule header -- cavs_schedule
+ * (with T_out == NULL), cavs_forward and cavs_backward only enqueue work; the kernels take the
+ * number of tasks T, the first internal position level_ptr[1] and the number of roots from the
+ * device, so a whole step (load on device, schedule, forward, backward) can be captured in one
+ * CUDA graph and replayed.  Requires the BF16 persistent path (h % 64 == 0, h <= 512; not with
+ * the opt-in K-split backward).  Forests only: an invalid batch or a DAG batch makes every kernel
+ * of the step skip its work, and the next cavs_sync returns its error (CAVS_E_INVALID / ARITY /
+ * CYCLE, or CAVS_E_UNSUPPORTED for a DAG).  FLOP / byte accounting of cavs_profile_read is not
+ * kept in this mode (phase times are).  Errors: CAVS_E_UNSUPPORTED, CAVS_E_STATE. */
+cavs_status cavs_set_sync_free(cavs_ctx* ctx, int on);
+
 /* Data-parallel overlap hook (SURVEY §8(e) "Overlap"): `cuda_event` (a cudaEvent_t created by the
  * caller, or NULL to clear) is recorded on the context's stream by every later cavs_backward as soon
  * as all WEIGHT blocks of dparams (W, U_iou, U_f / W_c, W_x) are final -- right after the lazily

@@ -59,6 +59,7 @@ def _load():
         "cavs_set_grad_event": (S, [P, P]),
         "cavs_softmax_xent": (S, [P, I32, I32, P, P, P, ctypes.c_float, P]),
         "cavs_train_step_host_async": (S, [P, I32, I32, I32, P, P, P, P, I32, P, P, I32, P, P, P]),
+        "cavs_set_sync_free": (S, [P, ctypes.c_int]),
         "cavs_last_error": (ctypes.c_char_p, [P]),
         "cavs_path_info": (ctypes.c_char_p, [P]),
         "cavs_profile": (S, [P, ctypes.c_int]),
@@ -78,7 +79,7 @@ def _load():
 _lib = _load()
 EXPORTS = ["cavs_param_count", "cavs_create", "cavs_set_stream", "cavs_workspace_bytes",
            "cavs_set_workspace", "cavs_load_graphs", "cavs_schedule", "cavs_get_schedule",
-           "cavs_forward", "cavs_forward_inference", "cavs_backward", "cavs_train_step_host", "cavs_kernel_launches", "cavs_sync", "cavs_set_grad_event", "cavs_softmax_xent", "cavs_train_step_host_async",
+           "cavs_forward", "cavs_forward_inference", "cavs_backward", "cavs_train_step_host", "cavs_kernel_launches", "cavs_sync", "cavs_set_grad_event", "cavs_softmax_xent", "cavs_train_step_host_async", "cavs_set_sync_free",
            "cavs_last_error", "cavs_path_info", "cavs_destroy", "cavs_profile", "cavs_profile_read"]
 PHASES = ["schedule", "prep", "xproj", "fwd_levels", "bwd_roots", "bwd_levels", "lazy", "dx", "reduce"]
 
@@ -272,6 +273,10 @@ class Context:
             event.record(self.stream)                    # materialise the cudaEvent_t
             ptr = event.cuda_event
         self._check(_lib.cavs_set_grad_event(self._ctx, ptr))
+
+    def set_sync_free(self, on=True):
+        """cavs_set_sync_free: schedule / forward / backward never wait on the host (graph-capturable)."""
+        self._check(_lib.cavs_set_sync_free(self._ctx, 1 if on else 0))
 
     def sync(self):
         """Wait for the context's stream; raises on deferred device-side input errors (cavs_sync)."""

@@ -53,7 +53,6 @@ struct cavs_ctx {
   bool hdr_pending = false;     // header copied asynchronously, not parsed yet
 };
 
-static constexpr int kHdrWords = 6;
 static constexpr int kReadback = 1024;
 
 static cavs_status fail(cavs_ctx* c, cavs_status s, const std::string& m) {
@@ -277,12 +276,19 @@ CAVS_API cavs_status cavs_schedule(cavs_ctx* ctx, int32_t* T_out) {
   ctx->prof.count(3);
   ctx->prof.mark(-1, ctx->stream);
   CK(cudaGetLastError());
+  ctx->state = S_SCHEDULED;
+  if (D.sync_free && !T_out) {                  // sync-free mode: the header stays on the device
+    ctx->hdr_pending = false;
+    ctx->T = -1;
+    ctx->lp.clear();
+    D.dag = 0;
+    return CAVS_OK;
+  }
   const int nread = kHdrWords + std::min(D.V + 1, kReadback);
   CK(cudaMemcpyAsync(ctx->h_hdr, D.hdr, sizeof(int) * nread, cudaMemcpyDeviceToHost, ctx->stream));
   if (!ctx->ev_hdr) CK(cudaEventCreateWithFlags(&ctx->ev_hdr, cudaEventDisableTiming));
   CK(cudaEventRecord(ctx->ev_hdr, ctx->stream));
   ctx->hdr_pending = true;
-  ctx->state = S_SCHEDULED;
   if (T_out) {
     const cavs_status st = finish_schedule(ctx);
     if (st) return st;
@@ -295,6 +301,13 @@ CAVS_API cavs_status cavs_get_schedule(cavs_ctx* ctx, int32_t* level, int32_t* l
   if (!ctx) return CAVS_E_INVALID;
   if (ctx->state < S_SCHEDULED) return fail(ctx, CAVS_E_STATE, "not scheduled");
   CK(cudaSetDevice(ctx->device));
+  if (ctx->T < 0) {                             // sync-free mode: fetch the header now (synchronous call)
+    const int nread = kHdrWords + std::min(ctx->D.V + 1, kReadback);
+    CK(cudaMemcpyAsync(ctx->h_hdr, ctx->D.hdr, sizeof(int) * nread, cudaMemcpyDeviceToHost, ctx->stream));
+    if (!ctx->ev_hdr) CK(cudaEventCreateWithFlags(&ctx->ev_hdr, cudaEventDisableTiming));
+    CK(cudaEventRecord(ctx->ev_hdr, ctx->stream));
+    ctx->hdr_pending = true;
+  }
   const cavs_status st = finish_schedule(ctx);
   if (st) return st;
   CK(cudaStreamSynchronize(ctx->stream));
@@ -385,7 +398,7 @@ static cavs_status forward_impl(cavs_ctx* ctx, const float* params, int32_t n_x,
   if (D.prec == CAVS_BF16) tc_forward(D, ctx->tc, ctx->lp, ctx->stream, P, &ctx->xs);
   else simt_forward<float>(D, ctx->lp, ctx->stream, P, &ctx->xs);
   P.mark(-1, ctx->stream);
-  account_forward(ctx);
+  if (ctx->T >= 0) account_forward(ctx);        // (sync-free mode: the host does not know I / T)
   CK(cudaGetLastError());
   ctx->state = infer ? S_SCHEDULED : S_FORWARDED;   // no activations for dF after an inference pass
   return CAVS_OK;
@@ -416,7 +429,7 @@ CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dp
   if (dx && D.n_x > 0) { launch_dx_zero(D, ctx->stream); P.count(1); }
   P.mark(CAVS_PH_BWD_ROOTS, ctx->stream);
   if (!D.dag) {                                // DAG batches: every vertex's dF runs in launch_dag_df
-    launch_roots(D, ctx->n_roots, D.roots, ctx->stream);
+    launch_roots(D, ctx->T >= 0 ? ctx->n_roots : -1, D.roots, ctx->stream);   // -1: count on the device
     P.count(1);
   }
   P.mark(CAVS_PH_BWD_LEVELS, ctx->stream);
@@ -435,7 +448,7 @@ CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dp
   launch_colsum(D, ctx->lazy_db, ctx->stream);  // db -> dparams
   P.count(1);
   P.mark(-1, ctx->stream);
-  account_backward(ctx);
+  if (ctx->T >= 0) account_backward(ctx);
   CK(cudaGetLastError());
   return CAVS_OK;
 }
@@ -541,6 +554,15 @@ CAVS_API cavs_status cavs_train_step_host_async(cavs_ctx* ctx, int32_t K, int32_
   return CAVS_OK;
 }
 
+CAVS_API cavs_status cavs_set_sync_free(cavs_ctx* ctx, int on) {
+  if (!ctx) return CAVS_E_INVALID;
+  if (ctx->state < S_READY) return fail(ctx, CAVS_E_STATE, "set_workspace first");
+  if (on && !(ctx->desc.precision == CAVS_BF16 && tc_sync_free_capable(ctx->tc)))
+    return fail(ctx, CAVS_E_UNSUPPORTED, "sync-free mode needs the BF16 persistent path (h % 64 == 0, h <= 512)");
+  ctx->D.sync_free = on ? 1 : 0;
+  return CAVS_OK;
+}
+
 CAVS_API cavs_status cavs_set_grad_event(cavs_ctx* ctx, void* cuda_event) {
   if (!ctx) return CAVS_E_INVALID;
   ctx->ev_wgrad = static_cast<cudaEvent_t>(cuda_event);
@@ -554,7 +576,19 @@ CAVS_API cavs_status cavs_sync(cavs_ctx* ctx) {
   if (ctx->d2h) CK(cudaStreamSynchronize(ctx->d2h));   // pipelined host-buffer steps
   CK(cudaMemcpyAsync(ctx->h_hdr + kHdrWords + kReadback - 1, ctx->D.hdr + 3, sizeof(int), cudaMemcpyDeviceToHost,
                      ctx->stream));
+  if (ctx->D.sync_free) {                       // the schedule's own status, never read on the host before
+    CK(cudaMemcpyAsync(ctx->h_hdr + kHdrWords + kReadback - 2, ctx->D.hdr, sizeof(int), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  }
   CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->D.sync_free) {
+    const int st = ctx->h_hdr[kHdrWords + kReadback - 2], fl = ctx->h_hdr[kHdrWords + kReadback - 1];
+    if (st & ST_INVALID) return fail(ctx, CAVS_E_INVALID, "malformed graph (range/shape); the step did nothing");
+    if (st & ST_ARITY) return fail(ctx, CAVS_E_ARITY, "a vertex has more than N children; the step did nothing");
+    if (st & ST_CYCLE) return fail(ctx, CAVS_E_CYCLE, "input graph has a cycle; the step did nothing");
+    if (fl & ST_DAG)
+      return fail(ctx, CAVS_E_UNSUPPORTED, "DAG batch (fan-out) in sync-free mode; the step did nothing");
+  }
   if (ctx->h_hdr[kHdrWords + kReadback - 1] & ST_XROW)
     return fail(ctx, CAVS_E_INVALID, "x_row entry outside [-1, n_x) (the vertex pulled nothing)");
   return CAVS_OK;

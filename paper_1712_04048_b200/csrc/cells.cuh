@@ -263,7 +263,7 @@ template <> struct EpiK<EPI_LSTM_XPROJ> {
   static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const FV<VW>* acc,
                                                const In<VW, NM>&, const UnitC<VW>& b) {
     const int h = D.h;
-    if (m.p < D.lp1) {
+    if (m.p < dev_lp1(D)) {
       FV<VW> zi, zo, zu, zf[NM], ck[NM];
 #pragma unroll
       for (int e = 0; e < VW; ++e) {
@@ -350,7 +350,7 @@ template <> struct EpiK<EPI_FC_XPROJ> {
   template <class OpT, int VW, int NM = kMaxN>
   static __device__ __forceinline__ void store(const Dev& D, int j, const VMeta& m, const FV<VW>* acc,
                                                const In<VW, NM>&, const UnitC<VW>& b) {
-    if (m.p < D.lp1) {
+    if (m.p < dev_lp1(D)) {
       FV<VW> z;
 #pragma unroll
       for (int e = 0; e < VW; ++e) z.v[e] = acc[0].v[e] + b.b0.v[e];
@@ -502,7 +502,7 @@ template <int E> __host__ __device__ constexpr bool epi_is_lstm() {
 // Does position p need this epilogue at all? (tile skipping for the x-kernels)
 template <int E>
 __device__ __forceinline__ bool row_active(const Dev& D, int p, int xrow) {
-  if constexpr (E == EPI_LSTM_XPROJ || E == EPI_FC_XPROJ) return p < D.lp1 || xrow >= 0;
+  if constexpr (E == EPI_LSTM_XPROJ || E == EPI_FC_XPROJ) return p < dev_lp1(D) || xrow >= 0;
   else if constexpr (E == EPI_DX) return xrow >= 0;
   else return true;
 }

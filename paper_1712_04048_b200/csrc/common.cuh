@@ -51,6 +51,10 @@ struct Dev {
   // kernel applies F / dF), stream_x (CAVS_STREAMING=1: the eager x-projection of the tasks
   // above level 0 runs on a second stream, each task waiting only for its own rows)
   int lazy_off, unfused, stream_x;
+  // sync-free mode (cavs_set_sync_free): the host never reads the schedule header; the kernels
+  // take T, level_ptr[1] and #roots from the device header (dev_T / dev_lp1), and skip their work
+  // for an invalid or DAG batch (reported by cavs_sync)
+  int sync_free;
   float* raw; int rawld;            // unfused: raw accumulators [Vp, rawld] fp32
   // DAG inputs (fan-out: a vertex with several parents); dag = 1 for this batch
   int dag;
@@ -81,6 +85,10 @@ struct Dev {
 };
 
 constexpr int kPadRows = 128;   // extra zero rows after V for TMA/K-block over-reach
+constexpr int kHdrWords = 6;    // header words before level_ptr (cavs_api.cu carve)
+
+// Schedule facts on the device (sync-free mode) or from the host copy.  Read after the PDL wait.
+__device__ __forceinline__ bool dev_skip(const struct Dev& D);
 
 // cudaFuncSetAttribute is per device: launchers cache "attribute already set" per device id.
 constexpr int kMaxDev = 64;
@@ -106,5 +114,15 @@ template <> __device__ __forceinline__ float to_op<float>(float v) { return v; }
 template <> __device__ __forceinline__ __nv_bfloat16 to_op<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 __device__ __forceinline__ float from_op(float v) { return v; }
 __device__ __forceinline__ float from_op(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+__device__ __forceinline__ bool dev_skip(const Dev& D) {
+  return D.sync_free && (D.hdr[0] != 0 || (D.hdr[3] & ST_DAG) != 0);
+}
+__device__ __forceinline__ int dev_T(const Dev& D) { return D.sync_free ? (dev_skip(D) ? 0 : D.hdr[1]) : D.T; }
+__device__ __forceinline__ int dev_lp1(const Dev& D) {
+  if (!D.sync_free) return D.lp1;
+  const int T = dev_T(D);
+  return T > 1 ? D.hdr[kHdrWords + 1] : D.V;
+}
 
 }  // namespace cavs

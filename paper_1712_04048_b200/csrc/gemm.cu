@@ -66,11 +66,12 @@ k_gemm_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
   const int p0 = blockIdx.x * kGRows;
   const int u0 = blockIdx.y * UGN;
   ptx::griddep_wait();                                   // flags / arenas of the previous kernels
+  if (dev_skip(D)) return;                               // sync-free mode: invalid / DAG batch
   // rows needing the epilogue: level-0 vertices (x-projection) or pull records (k_pull's flags)
   {
     const int f0 = p0 >> 6;
     bool act = D.tile_x[f0] || (p0 + 64 < D.V && D.tile_x[f0 + 1]);
-    if constexpr (E == EPI_LSTM_XPROJ || E == EPI_FC_XPROJ) act = act || p0 < D.lp1;
+    if constexpr (E == EPI_LSTM_XPROJ || E == EPI_FC_XPROJ) act = act || p0 < dev_lp1(D);
     if (!act || p0 >= D.V) return;
   }
   if (threadIdx.x == 0) {

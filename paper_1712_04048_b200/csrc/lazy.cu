@@ -57,6 +57,7 @@ struct LJob {
   long long out;         // dparams offset of the block
   int hblk, rowmap[4];   // internal row m -> packed row rowmap[m / hblk] + m % hblk
   int nkb;               // k-blocks per segment in the host plan (estimate for skip jobs)
+  int dev_lo;            // 1 (sync-free mode): k_lo = level_ptr[1] read on the device, nkb an estimate
 };
 struct LItem {
   unsigned short gtile, ltile;   // tile id (counter index) / job-local tile
@@ -88,11 +89,13 @@ __device__ __forceinline__ void lwait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-// actual k-block range [a, b) of an item and k-blocks per segment
-__device__ __forceinline__ void item_range(const LJob& J, const LItem& it, int n_act, int& a, int& b, int& kps) {
-  if (J.skip) {
-    kps = n_act;
-    const long long est = (long long)J.nseg * J.nkb, act = (long long)J.nseg * n_act;
+// actual k-block range [a, b) of an item and k-blocks per segment; the host plan's estimate is
+// mapped proportionally onto the device count (pull-record blocks; internal rows in sync-free mode)
+__device__ __forceinline__ void item_range(const LJob& J, const LItem& it, int n_act, int nkb_in, int& a, int& b,
+                                           int& kps) {
+  if (J.skip || J.dev_lo) {
+    kps = J.skip ? n_act : nkb_in;
+    const long long est = (long long)J.nseg * J.nkb, act = (long long)J.nseg * kps;
     a = est ? (int)((long long)it.g0 * act / est) : 0;
     b = est ? (int)((long long)it.g1 * act / est) : 0;
   } else {
@@ -120,7 +123,8 @@ k_lazy(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
   int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);             // [0] n_act, [1] last arrival
   unsigned short* s_act = reinterpret_cast<unsigned short*>(s_flag + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i0 = P.cta_start[blockIdx.x], i1 = P.cta_start[blockIdx.x + 1];
+  const int i0 = P.cta_start[blockIdx.x];
+  int i1 = P.cta_start[blockIdx.x + 1];
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kLS; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
@@ -131,6 +135,9 @@ k_lazy(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
   bool need_act = false;
   for (int i = i0; i < i1; ++i) need_act |= P.job[P.item[i].job].skip != 0;
   ptx::griddep_wait();                                   // dZ of the backward pass, k_pull's flags
+  if (dev_skip(D)) i1 = i0;                              // sync-free mode: invalid / DAG batch, no work
+  const int lp1d = dev_lp1(D);                           // internal rows [lp1d, V) (dU jobs)
+  const int nkb_in = lp1d < D.V ? cdiv(D.V - lp1d, 64) : 0;
   if (warp == 0) {
     int n = 0;
     if (need_act) {                                      // ascending list of 64-row blocks with a pull record
@@ -162,12 +169,12 @@ k_lazy(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
         const int tm = it.ltile / J.ntn, tn = it.ltile % J.ntn;
         const CUtensorMap* mB = J.bsrc ? &mXp : &mHk;
         int a, b, kps;
-        item_range(J, it, n_act, a, b, kps);
+        item_range(J, it, n_act, nkb_in, a, b, kps);
         for (int g = a; g < b; ++g, ++step) {
           const int s = step % kLS;
           if (s != warp) continue;
           const int seg = g / kps, j = g - seg * kps;
-          const int r0 = J.skip ? 64 * (int)s_act[j] : J.k_lo + 64 * j;
+          const int r0 = J.skip ? 64 * (int)s_act[j] : (J.dev_lo ? lp1d : J.k_lo) + 64 * j;
           if (step >= kLS) lwait(&empty[s], ((step / kLS) & 1) ^ 1);
           uint8_t* st = smem + s * kLStage;
           if (lane == 0) {
@@ -190,7 +197,7 @@ k_lazy(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
         const LItem& it = P.item[i];
         const LJob& J = P.job[it.job];
         int a, b, kps;
-        item_range(J, it, n_act, a, b, kps);
+        item_range(J, it, n_act, nkb_in, a, b, kps);
         const int buf = k & 1;
         if (k >= 2) lwait(&acce[buf], ((k - 2) >> 1) & 1);
         ptx::tc_fence_after();
@@ -220,7 +227,7 @@ k_lazy(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
       const LJob& J = P.job[it.job];
       const int tm = it.ltile / J.ntn, tn = it.ltile % J.ntn;
       int a, b, kps;
-      item_range(J, it, n_act, a, b, kps);
+      item_range(J, it, n_act, nkb_in, a, b, kps);
       const int buf = k & 1;
       lwait(&accf[buf], (k >> 1) & 1);
       ptx::tc_fence_after();
@@ -373,12 +380,18 @@ static LJob job(int nseg, const int* a_col, const int* b_col, int k_lo, int k_hi
   J.nkb = nkb;
   return J;
 }
+static LJob dev_rows(LJob J, bool on) {              // sync-free mode: internal rows from the device
+  J.dev_lo = (on && !J.skip) ? 1 : 0;
+  return J;
+}
 
 bool lazy_grads(const Dev& D, LazyState* l, cudaStream_t s) {
   if (!l || !D.dparams || (reinterpret_cast<uintptr_t>(D.dparams) & 15)) return false;
   const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
-  const int h = D.h, d = D.d, N = D.N, V = D.V, lp1 = D.lp1;
-  const int nkb_in = lp1 < V ? cdiv(V - lp1, 64) : 0;                      // internal rows [lp1, V)
+  const int h = D.h, d = D.d, N = D.N, V = D.V, lp1 = D.sync_free ? 0 : D.lp1;
+  // internal rows [lp1, V); sync-free mode: level_ptr[1] is read on the device, the plan assumes
+  // every row (the device maps it onto the actual count, item_range)
+  const int nkb_in = lp1 < V ? cdiv(V - lp1, 64) : 0;
   // dW rows: the 64-row blocks holding a pull record; the plan assumes they are packed (trees:
   // the leaves [0, lp1); chains: every row); the device maps the plan onto the actual count
   const int nkb_x = std::min(cdiv(V, 64), cdiv(std::max(D.n_x, 0), 64));
@@ -389,12 +402,12 @@ bool lazy_grads(const Dev& D, LazyState* l, cudaStream_t s) {
     const long long nW = 4LL * h * d, nU = 3LL * h * h;
     int bk[4], af[4], ident[4] = {0, 0, 0, 0}, iou[4] = {0, 2 * h, 3 * h, 3 * h};
     for (int k = 0; k < N; ++k) { bk[k] = k * h; af[k] = (3 + k) * h; }
-    P.job[nj++] = job(N, zero4, bk, lp1, V, 0, 0, 3 * h, h, h, nW, 3 * h, ident, nkb_in);        // dU_iou
-    P.job[nj++] = job(N, af, bk, lp1, V, 0, 0, h, h, h, nW + nU, h, ident, nkb_in);              // dU_f
+    P.job[nj++] = dev_rows(job(N, zero4, bk, lp1, V, 0, 0, 3 * h, h, h, nW, 3 * h, ident, nkb_in), D.sync_free);  // dU_iou
+    P.job[nj++] = dev_rows(job(N, af, bk, lp1, V, 0, 0, h, h, h, nW + nU, h, ident, nkb_in), D.sync_free);        // dU_f
     P.job[nj++] = job(1, zero4, zero4, 0, V, 1, 1, 3 * h, d, d, 0, h, iou, nkb_x);               // dW_i,o,u
     P.job[nj++] = job(N, af, zero4, 0, V, 1, 1, h, d, d, (long long)h * d, h, ident, nkb_x);     // dW_f
   } else {
-    P.job[nj++] = job(1, zero4, zero4, lp1, V, 0, 0, h, 2 * h, 2 * h, 0, h, zero4, nkb_in);      // dW_c
+    P.job[nj++] = dev_rows(job(1, zero4, zero4, lp1, V, 0, 0, h, 2 * h, 2 * h, 0, h, zero4, nkb_in), D.sync_free);  // dW_c
     P.job[nj++] = job(1, zero4, zero4, 0, V, 1, 1, h, d, d, 2LL * h * h, h, zero4, nkb_x);       // dW_x
   }
   // stream-K partition of the (tile, k-block) work

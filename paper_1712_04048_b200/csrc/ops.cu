@@ -141,6 +141,8 @@ __global__ void k_pull(Dev D) {
 template <class OpT>
 __global__ void k_roots(Dev D, int n_roots, const int* roots) {
   pdl_wait();
+  if (dev_skip(D)) return;
+  if (n_roots < 0) n_roots = D.hdr[2];                      // sync-free mode: the device count
   const size_t n = (size_t)n_roots * D.h;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     root_bwd<OpT>(D, (int)(i % D.h), roots[i / D.h]);
@@ -157,6 +159,7 @@ __global__ void k_roots(Dev D, int n_roots, const int* roots) {
 template <class OpT>
 __global__ void __launch_bounds__(256) k_colsum(Dev D, float* part, int lcols) {
   pdl_wait();
+  if (dev_skip(D)) return;
   __shared__ float red[8][256];
   __shared__ int s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -461,7 +464,7 @@ void launch_pull(const Dev& D, cudaStream_t s) {
 }
 
 void launch_roots(const Dev& D, int n_roots, const int* roots, cudaStream_t s) {
-  const size_t n = (size_t)n_roots * D.h;
+  const size_t n = (size_t)(n_roots < 0 ? D.V : n_roots) * D.h;   // < 0: device count, grid for V
   if (D.prec == CAVS_BF16) launch_pdl(k_roots<__nv_bfloat16>, dim3(grid_for(n, 256)), dim3(256), 0, s, D, n_roots, roots);
   else launch_pdl(k_roots<float>, dim3(grid_for(n, 256)), dim3(256), 0, s, D, n_roots, roots);
 }

@@ -150,6 +150,15 @@ __device__ __forceinline__ void mma_level(const PPlan& P, int ntile, uint32_t a_
   }
 }
 
+// nlev < 0 (sync-free mode): the tasks of the pass from the device header (t_first = 1 forward,
+// T - 1 backward); an invalid or DAG batch runs no task.  Call after the PDL wait.
+__device__ __forceinline__ void resolve_tasks(const Dev& D, int dir, int& t_first, int& nlev) {
+  if (nlev >= 0) return;
+  const int T = dev_T(D);
+  nlev = T > 1 ? T - 1 : 0;
+  t_first = dir > 0 ? 1 : T - 1;
+}
+
 template <int E, int NE, int NM>
 __global__ void __launch_bounds__(kPThreads, 1)
 k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUtensorMap ma1,
@@ -211,6 +220,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
       ptx::tma_prefetch(&mb16); ptx::tma_prefetch(&mb32); ptx::tma_prefetch(&mb64);
       if (P.tsA) pwait(acopy, 0);                     // stages overlay the weights' staging area
       ptx::griddep_wait();                            // task rows come from the previous kernels
+      resolve_tasks(D, dir, t_first, nlev);
       int step = 0;
       for (int i = 0; i < nlev; ++i) {
         const int t = t_first + i * dir;
@@ -285,6 +295,8 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
       }
       const uint32_t a_lo = ((ptx::smem_u32(sA) >> 4) & 0x3FFF) | (1u << 16);
       const uint32_t b_lo = ((ptx::smem_u32(sB) >> 4) & 0x3FFF) | (1u << 16);
+      ptx::griddep_wait();
+      resolve_tasks(D, dir, t_first, nlev);
       int step = 0, tcount = 0;
       for (int i = 0; i < nlev; ++i) {
         const int t = t_first + i * dir;
@@ -315,6 +327,7 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
     const int quad = et % quads;                       // constant: 256 % quads == 0
     const int j = u0 + quad * 4;
     ptx::griddep_wait();
+    resolve_tasks(D, dir, t_first, nlev);
     const UnitC<4> uc = epi_uses_bias<E>() ? load_unit<4>(D, j, epi_is_lstm<E>()) : UnitC<4>{};
     constexpr int CH = epi_needs_children<E>() ? 1 : 2;
     int tcount = 0, nbar = 0;
@@ -715,6 +728,7 @@ void persist_destroy(PersistState* ps) {
 }
 
 int persist_clusters(const PersistState* ps) { return ps ? ps->fwd.R : 0; }
+bool persist_has_kbwd(const PersistState* ps) { return ps && ps->kbwd; }
 
 static bool D_is_lstm(const PersistState* ps) { return ps->fwd.ngrp == 4; }
 
@@ -731,7 +745,8 @@ std::string persist_describe(const PersistState* ps) {
 }
 
 void persist_forward(const Dev& D, PersistState* ps, int T, cudaStream_t s) {
-  if (T <= 1) return;
+  if (T <= 1 && !D.sync_free) return;
+  if (D.sync_free) T = 0;                             // launch args (1, T - 1) = (1, -1): tasks from the device
   const PPlan& P = ps->fwd;
   if (D.cell == CAVS_CELL_TREE_LSTM) {
     if (D.infer) {                                    // inference-only forward: no activations for dF
@@ -757,7 +772,8 @@ void persist_forward(const Dev& D, PersistState* ps, int T, cudaStream_t s) {
 }
 
 void persist_backward(const Dev& D, PersistState* ps, int T, cudaStream_t s) {
-  if (T <= 1) return;
+  if (T <= 1 && !D.sync_free) return;
+  if (D.sync_free) T = 0;                             // launch args (T - 1, T - 1) = (-1, -1): from the device
   if (ps->kbwd) { pbwd_launch(D, ps->kbwd, T, s); return; }
   const PPlan& P = ps->bwd;
   if (D.cell == CAVS_CELL_TREE_LSTM) {

@@ -12,6 +12,8 @@ PersistState* persist_init(const Dev& D, int max_vertices, std::string* why);
 void persist_destroy(PersistState* ps);
 // clusters (graph ranges) of the persistent kernels: Dev::ncl, the width of the Dev::crow table
 int persist_clusters(const PersistState* ps);
+// the backward runs the (opt-in) K-split kernel, which takes its task count from the host
+bool persist_has_kbwd(const PersistState* ps);
 // All tasks t = 1 .. T-1 (forward) / T-1 .. 1 (backward) in one launch.
 void persist_forward(const Dev& D, PersistState* ps, int T, cudaStream_t s);
 void persist_backward(const Dev& D, PersistState* ps, int T, cudaStream_t s);

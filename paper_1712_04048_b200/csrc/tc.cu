@@ -519,6 +519,9 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
 std::string tc_describe(const TcState* tc) { return tc ? tc->info : std::string("levels: FP32 FFMA"); }
 
 int tc_clusters(const TcState* tc) { return tc && tc->ps ? persist_clusters(tc->ps) : 0; }
+bool tc_sync_free_capable(const TcState* tc) {
+  return tc && tc->ps && !persist_has_kbwd(tc->ps) && tc->ls && tc->gs && !tc->use_simt && !tc->mono;
+}
 
 void tc_destroy(TcState* tc) {
   if (tc && tc->ps) persist_destroy(tc->ps);
@@ -778,7 +781,7 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
       P.count(1);
     }
     P.mark(CAVS_PH_FWD_LEVELS, s);
-    if (t->ps && !D.dag) { if (T > 1) { persist_forward(D, t->ps, T, s); P.count(1); } return; }
+    if (t->ps && !D.dag) { if (T > 1 || D.sync_free) { persist_forward(D, t->ps, T, s); P.count(1); } return; }
     const PlanT F = gs ? gs_lstm_fwd(h, N) : mono_lstm_fwd(h, N);
     for (int tt = 1; tt < T; ++tt) {
       const int M = lp[tt + 1] - lp[tt];
@@ -797,7 +800,7 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
       P.count(1);
     }
     P.mark(CAVS_PH_FWD_LEVELS, s);
-    if (t->ps && !D.dag) { if (T > 1) { persist_forward(D, t->ps, T, s); P.count(1); } return; }
+    if (t->ps && !D.dag) { if (T > 1 || D.sync_free) { persist_forward(D, t->ps, T, s); P.count(1); } return; }
     PlanT F;
     if (gs) { F = plan_empty(); gs_add_ksplit(F, 0, 0, 0, 0, 2 * h, 0); }
     else F = mono_one(2 * h, 1, &zero, &zero);
@@ -874,7 +877,7 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
       if (D.unfused) { launch_unfused(D, lstm ? EPI_LSTM_BWD_DAG : EPI_FC_BWD_DAG, lp[tt], lp[tt + 1], s); P.count(1); }
     }
   } else if (t->ps) {
-    if (T > 1) { persist_backward(D, t->ps, T, s); P.count(1); }
+    if (T > 1 || D.sync_free) { persist_backward(D, t->ps, T, s); P.count(1); }
   } else if (lstm) {
     const PlanT B = gs ? gs_lstm_bwd(h, N) : mono_lstm_bwd(h, N);
     for (int tt = T - 1; tt >= 1; --tt) {

@@ -19,5 +19,8 @@ void tc_backward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s
 void tc_destroy(TcState* tc);
 std::string tc_describe(const TcState* tc);   // which level-kernel path is active
 int tc_clusters(const TcState* tc);           // graph-range clusters of the persistent level kernels (0: none)
+// the whole step runs without host knowledge of the schedule: persistent level kernels (device task
+// count), stream-K lazy kernel (device row count), row GEMMs -- the sync-free mode's requirement
+bool tc_sync_free_capable(const TcState* tc);
 
 }  // namespace cavs

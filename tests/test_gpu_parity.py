@@ -778,3 +778,75 @@ def test_dx_records_pulled_never_or_twice(precision):
     b2 = gen.make_batch("tree_lstm", 2, 64, 64, "sst_tree", 5, seed=82)
     g2 = run_gpu(b2, precision, ctx=g["ctx"])
     compare(b2, g2, run_oracle(b2), tol, f"bijective pulls after {precision}")
+
+
+# ------------------------------------------------------------------ sync-free mode + CUDA graphs
+def _dev_step(ctx, b, params_t, x_t, xr_t, g_t, csr, h_out, dp, dx):
+    ctx.load_graphs(*csr)
+    ctx.schedule(wait=False)
+    ctx.forward(params_t, x_t, xr_t, h_out)
+    ctx.backward(g_t, dp, dx)
+
+
+def test_sync_free_step_and_cuda_graph_replay():
+    """Sync-free mode: the host never reads the schedule header; the step equals the normal step
+    (h_out bit for bit; dparams up to the lazy GEMMs' split order) and a whole step captured in ONE
+    CUDA graph replays to the same bits as the uncaptured sync-free step, on two batches."""
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    bs = [gen.make_batch("tree_lstm", 2, 256, 256, "sst_tree", 24, seed=s) for s in (91, 92)]
+    for b in bs[1:]:
+        b.params = bs[0].params
+    maxV = max(b.V for b in bs)
+    maxX = max(b.n_x for b in bs)
+    ref = [run_gpu(b, "bf16") for b in bs]
+    ctx = make_ctx(bs[0], "bf16", max_vertices=maxV, max_x=maxX, max_graphs=24)
+    ctx.set_sync_free(True)
+    params = t(bs[0].params)
+    ins = [(t(b.x), t(b.x_row), t(b.gamma), (t(b.graph_ptr), t(b.child_ptr), t(b.child_idx))) for b in bs]
+    outs = [(torch.empty(b.V, b.h, device=dev), torch.empty(ctx.P, device=dev), torch.empty(b.n_x, b.d, device=dev))
+            for b in bs]
+    for i, b in enumerate(bs):                          # uncaptured sync-free steps
+        _dev_step(ctx, b, params, ins[i][0], ins[i][1], ins[i][2], ins[i][3], *outs[i])
+        ctx.sync()
+        assert np.array_equal(outs[i][0].cpu().numpy(), ref[i]["h_out"])
+        compare(b, dict(h_out=outs[i][0].cpu().numpy(), dparams=outs[i][1].cpu().numpy(),
+                        dx=outs[i][2].cpu().numpy()), ref[i], 1e-5, f"sync-free vs normal step {i}")
+    first = [(o[0].clone(), o[1].clone(), o[2].clone()) for o in outs]
+    graphs = []
+    side = torch.cuda.Stream(dev)
+    for i, b in enumerate(bs):                          # one graph per batch
+        g = torch.cuda.CUDAGraph()
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                ctx.set_stream(side)
+                _dev_step(ctx, b, params, ins[i][0], ins[i][1], ins[i][2], ins[i][3], *outs[i])
+        graphs.append(g)
+    ctx.set_stream(torch.cuda.current_stream(dev))
+    for rep in range(2):
+        for i, g in enumerate(graphs):
+            for o in outs[i]:
+                o.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            for a, r in zip(outs[i], first[i]):
+                assert torch.equal(a, r), f"graph replay {rep} batch {i} differs"
+    ctx.sync()
+
+
+def test_sync_free_reports_errors_at_sync():
+    from paper_1712_04048_b200 import CavsError
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    for graphs, code in (([[[1, 2], [2], [0]]], "E_CYCLE"), ([[[], [0, 0], [1, 0]]], "E_UNSUPPORTED")):
+        b = gen.batch_from_graphs(graphs, cell="tree_lstm", N=2, h=128, d=128, seed=0, x_at="all", loss_at="all")
+        ctx = make_ctx(b, "bf16", max_vertices=16, max_graphs=4, max_x=16)
+        ctx.set_sync_free(True)
+        ctx.load_graphs(t(b.graph_ptr), t(b.child_ptr), t(b.child_idx))
+        ctx.schedule(wait=False)
+        ctx.forward(t(b.params), t(b.x), t(b.x_row))
+        ctx.backward(t(b.gamma))
+        with pytest.raises(CavsError) as e:
+            ctx.sync()
+        assert e.value.name == code
