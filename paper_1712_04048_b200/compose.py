@@ -23,20 +23,27 @@ from .cavs import Context, softmax_xent
 
 
 class LMHead:
-    """Softmax head W_out [vocab, h], b_out [vocab] (fp32 device tensors)."""
+    """Softmax head W_out [vocab, h], b_out [vocab] (fp32 device tensors).  `tf32=True` lets the
+    head's three GEMMs run on the tensor cores with TF32 inputs (fp32 accumulation and outputs) --
+    the precision class of the bf16 mode; the fp32 parity mode keeps exact fp32 GEMMs."""
 
-    def __init__(self, W_out, b_out):
-        self.W, self.b = W_out, b_out
+    def __init__(self, W_out, b_out, tf32=False):
+        self.W, self.b, self.tf32 = W_out, b_out, tf32
 
     def loss_and_grad(self, H, targets):
         """H [V, h] (F's push buffer), targets [V] int32 (-1: no loss).  Returns the summed loss (0-dim
         tensor), dL/dH [V, h] (F's push cotangent), dL/dW_out, dL/db_out."""
         import torch
-        logits = torch.addmm(self.b, H, self.W.t())                       # library GEMM
-        loss, dlog = softmax_xent(logits, targets, dlogits=logits)         # fused, in place
-        dH = dlog @ self.W                                                 # library GEMM
-        dW = dlog.t() @ H
-        db = dlog.t() @ torch.ones(dlog.shape[0], device=dlog.device, dtype=dlog.dtype)
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = self.tf32
+        try:
+            logits = torch.addmm(self.b, H, self.W.t())                   # library GEMM
+            loss, dlog = softmax_xent(logits, targets, dlogits=logits)     # fused, in place
+            dH = dlog @ self.W                                             # library GEMM
+            dW = dlog.t() @ H
+            db = dlog.sum(0)
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = prev
         return loss.sum(), dH, dW, db
 
 

@@ -43,7 +43,7 @@ def test_lm_train_step(precision, tol):
     lm = gen.make_lm_batch(3, [5, 9, 3], h=64, d=64, vocab=50, seed=4)
     b = lm.batch
     ctx = make_ctx(b, precision, max_x=lm.batch.x.shape[0])
-    head = compose.LMHead(t(lm.W_out), t(lm.b_out))
+    head = compose.LMHead(t(lm.W_out), t(lm.b_out), tf32=precision == "bf16")
     loss, h_out, dp, demb, dW, db = compose.lm_train_step(
         ctx, t(b.params), t(b.x), t(b.x_row), head, t(lm.targets), graph=(t(b.graph_ptr), t(b.child_ptr), t(b.child_idx)))
     torch.cuda.synchronize()
