@@ -273,6 +273,7 @@ def main():
     maxX = max(b.n_x for b in batches)
     ctx = Context(b0.cell, b0.N, b0.h, b0.d, precision=args.precision, max_graphs=max(b.K for b in batches),
                   max_vertices=maxV, max_x=maxX, device=local)
+    path_info = ctx.path_info()
     h_out = torch.empty(maxV, b0.h, device=dev)
     dparams = torch.empty(ctx.P, device=dev)
     dx = torch.empty(maxX, b0.d, device=dev)
@@ -386,6 +387,13 @@ def main():
         peak_src = "measured (MEASURED_PEAKS.json bf16_tflops_sustained)" if peak else None
         if not peak:
             peak, peak_src = 1400.0, "fallback (B200_PROFILING.md sustained 1.4 PFLOP/s)"
+    elif "bf16x3" in path_info:
+        # FP32 mode on the tensor cores: every fp32 product is six bf16 tcgen05 MMAs (bf16x3 split
+        # operands), so the fp32 roofline is the measured bf16 peak / 6
+        bp = peaks.get("bf16_tflops_sustained") or peaks.get("bf16_tflops") or 1400.0
+        peak = bp / 6.0
+        peak_src = ("measured bf16 sustained peak (MEASURED_PEAKS.json) / 6: six bf16 MMAs per fp32 product "
+                    "(bf16x3 split)")
     else:
         # FFMA fp32 peak: 148 SMs x 128 FP32 lanes x 2 FLOP x measured max SM clock
         mhz = peaks.get("sm_max_mhz", 1965.0)
@@ -502,7 +510,7 @@ def main():
             "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
             "config": {"workload": f"{args.config}: {_desc(args.config, b0.h)}", "h": b0.h, "d": b0.d,
                        "batch_per_gpu": float(np.mean([b.K for b in batches])), "global_batch": samples,
-                       "precision": args.precision,
+                       "precision": args.precision, "engine": path_info,
                        "batch_pool": args.pool, "l2_flush": not args.no_flush, "parallelism": f"dp{world}",
                        "mean_vertices": float(np.mean([b.V for b in batches])),
                        "mean_levels_T": depth_T},

@@ -68,7 +68,8 @@ static cavs_status cuda_check(cavs_ctx* c, cudaError_t e, const char* where) {
 
 static bool is_lstm(const cavs_desc& d) { return d.cell == CAVS_CELL_TREE_LSTM; }
 static int gates(const cavs_desc& d) { return is_lstm(d) ? 3 + d.N : 1; }
-static size_t esize(const cavs_desc& d) { return d.precision == CAVS_BF16 ? 2 : 4; }
+// bytes per operand element as stored: bf16, fp32, or (FP32 split mode) three bf16 planes
+static size_t esize(const cavs_ctx* c) { return c->desc.precision == CAVS_BF16 ? 2 : c->D.split ? 6 : 4; }
 
 // Carve the workspace; with base == nullptr only computes the size.
 static size_t carve(cavs_ctx* c, char* base) {
@@ -81,7 +82,7 @@ static size_t carve(cavs_ctx* c, char* base) {
     return p;
   };
   const size_t V = d.max_vertices, K = d.max_graphs, X = d.max_x, N = d.N, h = d.h, dd = d.d;
-  const size_t Vp = V + kPadRows, G = gates(d), es = esize(d);
+  const size_t Vp = V + kPadRows, G = gates(d), es = esize(c);
   Dev& D = c->D;
   auto I = [&](size_t n) { return reinterpret_cast<int*>(take(n * 4)); };
   auto F = [&](size_t n) { return reinterpret_cast<float*>(take(n * 4)); };
@@ -99,6 +100,9 @@ static size_t carve(cavs_ctx* c, char* base) {
   D.Hs = nullptr;                              // U h~ is accumulated as sum_k U h_k: no h~ arena
   D.Xp = take(Vp * dd * es);
   D.dZ = take(Vp * G * h * es);
+  // FP32 split mode: plane q of an arena / weight copy starts q * (plane elements) after plane 0
+  const size_t sp = D.split ? 1 : 0;
+  D.ps_hk = sp * Vp * N * h; D.ps_xp = sp * Vp * dd; D.ps_dz = sp * Vp * G * h;
   D.Ck = is_lstm(d) ? F(Vp * N * h) : nullptr;
   D.XW = F(Vp * (is_lstm(d) ? 4 : 1) * h);
   D.gates = F(Vp * G * h);
@@ -108,15 +112,25 @@ static size_t carve(cavs_ctx* c, char* base) {
   if (is_lstm(d)) {
     D.Wa = take(4 * h * h * es); D.Wb = take(4 * h * dd * es); D.Wc = take(3 * h * h * es);
     D.Wd = take(h * h * es); D.We = take(dd * G * h * es);
+    const size_t pw[5] = {4 * h * h, 4 * h * dd, 3 * h * h, h * h, dd * G * h};
+    for (int i = 0; i < 5; ++i) D.ps_w[i] = sp * pw[i];
   } else {
     D.Wa = take(2 * h * h * es); D.Wb = take(h * dd * es); D.Wc = take(2 * h * h * es);
     D.Wd = nullptr; D.We = take(dd * h * es);
+    const size_t pw[5] = {2 * h * h, h * dd, 2 * h * h, 0, dd * h};
+    for (int i = 0; i < 5; ++i) D.ps_w[i] = sp * pw[i];
   }
   D.pptr = I(V + 1); D.pent = I(N * V + 1); D.pcur = I(V);          // DAG parent CSR (NEXT-3)
   D.dHg = F(Vp * N * h); D.dCg = is_lstm(d) ? F(Vp * N * h) : nullptr;
   D.rawld = (is_lstm(d) ? 3 + kMaxN : 2) * (int)h;
   D.raw = D.unfused ? F(Vp * D.rawld) : nullptr;     // unfused ablation only
   D.lazy = F(lazy_floats(D));
+  // row-tiled level GEMMs (h > 512, BF16): split-K partial slots [296 items][acc columns][128 rows]
+  const char* pe = std::getenv("CAVS_PERSIST");
+  const bool rows_path = d.precision == CAVS_BF16 && (h > 512 || (pe && pe[0] == '0'));
+  const size_t acc_cols = is_lstm(d) ? std::max<size_t>(256 * std::min<size_t>(N, 2), 128 * (1 + std::min<size_t>(N, 2))) : 256;
+  D.rows_part = rows_path ? F((size_t)296 * acc_cols * 128) : nullptr;
+  D.rows_cnt = rows_path ? I(1024) : nullptr;
   c->lazy_db = F((size_t)kDbChunks * d.N * 4 * h);   // db partials [(slot, chunk)][logical column]
   const size_t P = cavs_param_count(d.cell, d.N, d.h, d.d);
   c->s_params = F(P); c->s_dp = F(P);
@@ -166,6 +180,11 @@ CAVS_API cavs_status cavs_create(const cavs_desc* desc, int device, void* stream
     c->D.lazy_off = lz && lz[0] == '0';
     c->D.unfused = uf && uf[0] == '1';
     c->D.stream_x = sx && sx[0] == '1';
+    // FP32 mode on the tensor cores (bf16x3 split operands, six MMAs per product) unless the shape
+    // or an ablation needs the FFMA path, or CAVS_FP32_FFMA=1 asks for it
+    const char* ff = std::getenv("CAVS_FP32_FFMA");
+    c->D.split = d.precision == CAVS_FP32 && !(ff && ff[0] == '1') && d.h % 64 == 0 && d.d % 64 == 0 &&
+                 !c->D.lazy_off && !c->D.unfused && !c->D.stream_x;
   }
   if (cudaSetDevice(device) != cudaSuccess ||
       cudaMallocHost(&c->h_hdr, sizeof(int) * (kHdrWords + kReadback)) != cudaSuccess) {
@@ -198,7 +217,7 @@ CAVS_API cavs_status cavs_set_workspace(cavs_ctx* ctx, void* dev, size_t bytes) 
   ctx->D.trace = (tr && tr[0] == '1') ? reinterpret_cast<unsigned long long*>(ctx->ws + ctx->ws_bytes - (4u << 20))
                                       : nullptr;
   CK(cudaMemsetAsync(ctx->ws, 0, ctx->ws_bytes, ctx->stream));   // arenas start finite (zero)
-  if (ctx->desc.precision == CAVS_BF16) {
+  if (ctx->desc.precision == CAVS_BF16 || ctx->D.split) {
     cavs_status s = tc_init(ctx->D, ctx->desc.max_vertices, &ctx->tc, &ctx->err);
     if (s) return s;
     ctx->D.ncl = tc_clusters(ctx->tc);
@@ -326,7 +345,7 @@ CAVS_API cavs_status cavs_get_schedule(cavs_ctx* ctx, int32_t* level, int32_t* l
 static void account_forward(cavs_ctx* ctx) {
   Prof& P = ctx->prof;
   const Dev& D = ctx->D;
-  const double h = D.h, d = D.d, I = D.V - D.lp1, E = D.E, nx = D.n_x, O = esize(ctx->desc), S = 4;
+  const double h = D.h, d = D.d, I = D.V - D.lp1, E = D.E, nx = D.n_x, O = esize(ctx), S = 4;
   const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
   const double G = lstm ? 3 + D.N : 1;
   if (lstm) {
@@ -347,7 +366,7 @@ static void account_forward(cavs_ctx* ctx) {
 static void account_backward(cavs_ctx* ctx) {
   Prof& P = ctx->prof;
   const Dev& D = ctx->D;
-  const double h = D.h, d = D.d, I = D.V - D.lp1, E = D.E, nx = D.n_x, O = esize(ctx->desc), S = 4;
+  const double h = D.h, d = D.d, I = D.V - D.lp1, E = D.E, nx = D.n_x, O = esize(ctx), S = 4;
   const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
   const double G = lstm ? 3 + D.N : 1;
   if (lstm) {
@@ -395,7 +414,7 @@ static cavs_status forward_impl(cavs_ctx* ctx, const float* params, int32_t n_x,
     CK(cudaStreamCreateWithFlags(&ctx->xs.s, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->xs.start, cudaEventDisableTiming));
   }
-  if (D.prec == CAVS_BF16) tc_forward(D, ctx->tc, ctx->lp, ctx->stream, P, &ctx->xs);
+  if (ctx->tc) tc_forward(D, ctx->tc, ctx->lp, ctx->stream, P, &ctx->xs);
   else simt_forward<float>(D, ctx->lp, ctx->stream, P, &ctx->xs);
   P.mark(-1, ctx->stream);
   if (ctx->T >= 0) account_forward(ctx);        // (sync-free mode: the host does not know I / T)
@@ -434,7 +453,7 @@ CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dp
   }
   P.mark(CAVS_PH_BWD_LEVELS, ctx->stream);
   int split[3] = {1, 1, 1};
-  if (D.prec == CAVS_BF16) {
+  if (ctx->tc) {
     tc_backward(D, ctx->tc, ctx->lp, ctx->stream, split, P, ctx->ev_wgrad);
   } else {
     simt_backward<float>(D, ctx->lp, ctx->stream, P);
@@ -640,7 +659,7 @@ CAVS_API const char* cavs_path_info(const cavs_ctx* ctx) {
   if (!ctx) return "null context";
   cavs_ctx* c = const_cast<cavs_ctx*>(ctx);
   c->info = ctx->state < S_READY ? std::string("no workspace yet")
-                                 : ctx->desc.precision == CAVS_BF16 ? tc_describe(ctx->tc) : std::string("levels: FP32 FFMA") +
+                                 : ctx->tc ? tc_describe(ctx->tc) : std::string("levels: FP32 FFMA") +
                                        (ctx->D.unfused ? "; ablation: unfused cell epilogues" : "") +
                                        (ctx->D.stream_x ? "; ablation: streamed x-projection" : "") +
                                        (ctx->D.lazy_off ? "; lazy batching OFF (ablation: per-task weight-gradient GEMMs)" : "");

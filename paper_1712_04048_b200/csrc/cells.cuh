@@ -35,12 +35,13 @@ __device__ __forceinline__ float tanh_fast(float x) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// (FP32 mode on tensor cores, OpT = S3, keeps the accurate functions: its parity bar is 1e-5)
 template <class OpT> __device__ __forceinline__ float act_sig(float z) {
-  if constexpr (sizeof(OpT) == 2) return fmaf(0.5f, tanh_fast(0.5f * z), 0.5f);
+  if constexpr (sizeof(OpT) == 2 && !is_s3<OpT>::value) return fmaf(0.5f, tanh_fast(0.5f * z), 0.5f);
   else return sigm(z);
 }
 template <class OpT> __device__ __forceinline__ float act_tanh(float z) {
-  if constexpr (sizeof(OpT) == 2) return tanh_fast(z);
+  if constexpr (sizeof(OpT) == 2 && !is_s3<OpT>::value) return tanh_fast(z);
   else return tanhf(z);
 }
 
@@ -67,8 +68,17 @@ template <int VW> __device__ __forceinline__ void stv(float* p, const FV<VW>& a)
   } else if constexpr (VW == 4) *reinterpret_cast<float4*>(p) = make_float4(a.v[0], a.v[1], a.v[2], a.v[3]);
   else *p = a.v[0];
 }
-template <class OpT, int VW> __device__ __forceinline__ void stv_op(OpT* p, const FV<VW>& a) {
-  if constexpr (VW == 8 && sizeof(OpT) == 2) {
+// ps: plane stride (elements) of the destination arena, used by the split operand type S3 only
+template <class OpT, int VW> __device__ __forceinline__ void stv_op(OpT* p, const FV<VW>& a, size_t ps = 0) {
+  if constexpr (is_s3<OpT>::value) {
+    __nv_bfloat16* q = reinterpret_cast<__nv_bfloat16*>(p);
+#pragma unroll
+    for (int e = 0; e < VW; ++e) {
+      __nv_bfloat16 b0, b1, b2;
+      split3(a.v[e], b0, b1, b2);
+      q[e] = b0; q[ps + e] = b1; q[2 * ps + e] = b2;
+    }
+  } else if constexpr (VW == 8 && sizeof(OpT) == 2) {
     uint4 u;
     __nv_bfloat162 b[4];
 #pragma unroll
@@ -165,7 +175,7 @@ __device__ __forceinline__ void lstm_finish(const Dev& D, int j, const VMeta& m,
   stv<VW>(D.h_out + (size_t)m.vid * h + j, hv);                   // push(h)
   if (m.par >= 0) {                                                // scatter([c,h]) into the parent's gather slot
     const size_t at = (size_t)m.par * N * h + (size_t)m.slot * h + j;
-    stv_op<OpT, VW>(op<OpT>(D.Hk) + at, hv);
+    stv_op<OpT, VW>(op<OpT>(D.Hk) + at, hv, D.ps_hk);
     stv<VW>(D.Ck + at, c);
   }
 }
@@ -204,7 +214,7 @@ __device__ __forceinline__ void lstm_child_store(const Dev& D, int j, int c, int
     dzu.v[e] = dcb.v[e] * i * (1.f - u * u);
   }
   OpT* dz = op<OpT>(D.dZ) + (size_t)c * G * h + j;
-  stv_op<OpT, VW>(dz, dzi); stv_op<OpT, VW>(dz + h, dzo); stv_op<OpT, VW>(dz + 2 * h, dzu);
+  stv_op<OpT, VW>(dz, dzi, D.ps_dz); stv_op<OpT, VW>(dz + h, dzo, D.ps_dz); stv_op<OpT, VW>(dz + 2 * h, dzu, D.ps_dz);
 #pragma unroll
   for (int k = 0; k < NM; ++k) {
     if (k >= N) break;
@@ -212,7 +222,7 @@ __device__ __forceinline__ void lstm_child_store(const Dev& D, int j, int c, int
 #pragma unroll
     for (int e = 0; e < VW; ++e)
       v.v[e] = k < c_deg ? dcb.v[e] * in.ck[k].v[e] * in.f[k].v[e] * (1.f - in.f[k].v[e]) : 0.f;
-    stv_op<OpT, VW>(dz + (3 + k) * h, v);
+    stv_op<OpT, VW>(dz + (3 + k) * h, v, D.ps_dz);
   }
   stv<VW>(D.dcb + (size_t)c * h + j, dcb);
 }
@@ -325,7 +335,7 @@ __device__ __forceinline__ void fc_finish(const Dev& D, int j, const VMeta& m, c
   for (int e = 0; e < VW; ++e) hv.v[e] = act_tanh<OpT>(z.v[e]);
   if (CHK == 0 || (CHK == 1 && !D.infer)) stv<VW>(D.gates + (size_t)m.p * h + j, hv);   // h kept for dF (1 - h^2)
   stv<VW>(D.h_out + (size_t)m.vid * h + j, hv);
-  if (m.par >= 0) stv_op<OpT, VW>(op<OpT>(D.Hk) + (size_t)m.par * 2 * h + (size_t)m.slot * h + j, hv);
+  if (m.par >= 0) stv_op<OpT, VW>(op<OpT>(D.Hk) + (size_t)m.par * 2 * h + (size_t)m.slot * h + j, hv, D.ps_hk);
 }
 
 template <> struct EpiK<EPI_FC_FWD> {
@@ -421,7 +431,7 @@ template <> struct EpiK<EPI_FC_BWD> {
       FV<VW> dz;
 #pragma unroll
       for (int e = 0; e < VW; ++e) dz.v[e] = (acc[k].v[e] + in.dho[k].v[e]) * (1.f - in.hc[k].v[e] * in.hc[k].v[e]);
-      stv_op<OpT, VW>(op<OpT>(D.dZ) + (size_t)m.ch[k] * D.h + j, dz);
+      stv_op<OpT, VW>(op<OpT>(D.dZ) + (size_t)m.ch[k] * D.h + j, dz, D.ps_dz);
     }
   }
 };
@@ -557,7 +567,7 @@ __device__ __forceinline__ void dag_df(const Dev& D, int j, int p) {
     float dh = D.dh_out[(size_t)vid * D.h + j];
     for (int e = e0; e < e1; ++e) dh += D.dHg[(size_t)D.pent[e] * D.h + j];
     const float hv = D.gates[(size_t)p * D.h + j];
-    op<OpT>(D.dZ)[(size_t)p * D.h + j] = to_op<OpT>(dh * (1.f - hv * hv));
+    st_op1<OpT>(op<OpT>(D.dZ) + (size_t)p * D.h + j, dh * (1.f - hv * hv), D.ps_dz);
   }
 }
 
@@ -572,7 +582,7 @@ __device__ __forceinline__ void root_bwd(const Dev& D, int j, int p) {
     lstm_child_store<OpT, 1, kMaxN>(D, j, p, deg, in.dho, zerov<1>(), in);
   } else {
     const float hv = D.gates[(size_t)p * D.h + j];
-    op<OpT>(D.dZ)[(size_t)p * D.h + j] = to_op<OpT>(D.dh_out[(size_t)vid * D.h + j] * (1.f - hv * hv));
+    st_op1<OpT>(op<OpT>(D.dZ) + (size_t)p * D.h + j, D.dh_out[(size_t)vid * D.h + j] * (1.f - hv * hv), D.ps_dz);
   }
 }
 

@@ -45,6 +45,8 @@ struct Dev {
   int ncl;                          // clusters of the persistent level kernels (0: none)
   int* crow;                        // [T][ncl + 1]: first position of task t owned by cluster >= r
   int* tile_cnt;                    // arrival counters (zero between launches): lazy tiles, then db column blocks
+  float* rows_part;                 // split-K partial accumulators of the row-tiled level GEMMs (rows.cu), or null
+  int* rows_cnt;                    // their per-tile arrival counters (zero between launches)
   // engine ablations of the paper's optimisations, fixed at
   // cavs_create from the environment: lazy_off (CAVS_LAZY_BATCH=0), unfused
   // (CAVS_UNFUSED=1: the level GEMMs store raw accumulators, a separate elementwise
@@ -78,6 +80,12 @@ struct Dev {
   void* Wa; void* Wb; void* Wc; void* Wd; void* We;
   // lazy outputs (fp32 scratch)
   float* lazy;
+  // FP32 mode on tensor cores (bf16x3 split): split = 1 stores every operand
+  // arena / weight copy as three bf16 planes x = b0 + b1 + b2; plane q of an arena lives q * ps_*
+  // elements after plane 0 (plane-major: the row arithmetic of plane 0 is unchanged)
+  int split;
+  size_t ps_hk, ps_xp, ps_dz;       // plane strides (elements) of Hk, Xp, dZ
+  size_t ps_w[5];                   // plane strides of the weight copies Wa..We
   unsigned long long* trace;   // debug (CAVS_TRACE=1): per-CTA globaltimer records, else null
   // caller buffers of the current call
   const float* params; const float* x; const int* x_row; const float* dh_out;
@@ -114,6 +122,41 @@ template <> __device__ __forceinline__ float to_op<float>(float v) { return v; }
 template <> __device__ __forceinline__ __nv_bfloat16 to_op<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 __device__ __forceinline__ float from_op(float v) { return v; }
 __device__ __forceinline__ float from_op(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+// Operand type of the FP32-on-tensor-core mode: plane 0 of a bf16x3 split value (the bf16 bits of
+// b0 = rn(x); planes 1, 2 hold b1 = rn(x - b0), b2 = rn(x - b0 - b1) one plane stride further).
+// Both differences are exact in fp32 (Sterbenz), so b0 + b1 + b2 = x to within 2^-24 |x|, and the
+// six products a_s b_t (s + t <= 2) of two split operands give x y to ~2^-22 relative.
+struct S3 { __nv_bfloat16 b; };
+template <class T> struct is_s3 { static constexpr bool value = false; };
+template <> struct is_s3<S3> { static constexpr bool value = true; };
+__device__ __forceinline__ void split3(float x, __nv_bfloat16& b0, __nv_bfloat16& b1, __nv_bfloat16& b2) {
+  b0 = __float2bfloat16_rn(x);
+  const float r1 = x - __bfloat162float(b0);
+  b1 = __float2bfloat16_rn(r1);
+  b2 = __float2bfloat16_rn(r1 - __bfloat162float(b1));
+}
+// one operand value: plain store (fp32 / bf16) or the three planes (S3, plane stride ps)
+template <class OpT> __device__ __forceinline__ void st_op1(OpT* p, float v, size_t ps) {
+  if constexpr (is_s3<OpT>::value) {
+    __nv_bfloat16 b0, b1, b2;
+    split3(v, b0, b1, b2);
+    __nv_bfloat16* q = reinterpret_cast<__nv_bfloat16*>(p);
+    q[0] = b0; q[ps] = b1; q[2 * ps] = b2;
+  } else {
+    (void)ps;
+    *p = to_op<OpT>(v);
+  }
+}
+template <class OpT> __device__ __forceinline__ float ld_op1(const OpT* p, size_t ps) {
+  if constexpr (is_s3<OpT>::value) {
+    const __nv_bfloat16* q = reinterpret_cast<const __nv_bfloat16*>(p);
+    return (__bfloat162float(q[0]) + __bfloat162float(q[ps])) + __bfloat162float(q[2 * ps]);
+  } else {
+    (void)ps;
+    return from_op(*p);
+  }
+}
 
 __device__ __forceinline__ bool dev_skip(const Dev& D) {
   return D.sync_free && (D.hdr[0] != 0 || (D.hdr[3] & ST_DAG) != 0);

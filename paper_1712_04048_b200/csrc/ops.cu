@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(256) k_prep(Dev D, PrepJobs J) {
 #pragma unroll
       for (int k = 0; k < 32; k += 8) {
         const int c = c0 + ty + k, r = r0 + tx;                    // dst row = source column
-        if (r < jb.rows && c < jb.cols) dst[(size_t)c * jb.dpitch + r] = to_op<OpT>(tile[tx][ty + k]);
+        if (r < jb.rows && c < jb.cols) st_op1<OpT>(dst + (size_t)c * jb.dpitch + r, tile[tx][ty + k], D.ps_w[jb.dst_sel]);
       }
       __syncthreads();
     }
@@ -72,11 +72,11 @@ __global__ void __launch_bounds__(256) k_prep(Dev D, PrepJobs J) {
         const float4 v = s4[i];
         FV<4> f;
         f.v[0] = v.x; f.v[1] = v.y; f.v[2] = v.z; f.v[3] = v.w;
-        stv_op<OpT, 4>(dst + 4 * i, f);
+        stv_op<OpT, 4>(dst + 4 * i, f, D.ps_w[jb.dst_sel]);
       }
     } else {
       for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        dst[i] = to_op<OpT>(jb.src[i]);
+        st_op1<OpT>(dst + i, jb.src[i], D.ps_w[jb.dst_sel]);
     }
   }
 }
@@ -125,7 +125,7 @@ __global__ void k_pull(Dev D) {
         if (e >= n || p0 + rr >= D.V) continue;
         FV<4> f;
         f.v[0] = v[u].x; f.v[1] = v[u].y; f.v[2] = v[u].z; f.v[3] = v[u].w;
-        stv_op<OpT, 4>(X + (size_t)(p0 + rr) * d + k, f);
+        stv_op<OpT, 4>(X + (size_t)(p0 + rr) * d + k, f, D.ps_xp);
       }
     }
   } else {
@@ -133,7 +133,7 @@ __global__ void k_pull(Dev D) {
       const int rr = e / d, k = e % d, p = p0 + rr;
       if (p >= D.V) break;
       const int r = s_r[rr];
-      X[(size_t)p * d + k] = to_op<OpT>(r >= 0 ? D.x[(size_t)r * d + k] : 0.f);
+      st_op1<OpT>(X + (size_t)p * d + k, r >= 0 ? D.x[(size_t)r * d + k] : 0.f, D.ps_xp);
     }
   }
 }
@@ -182,7 +182,13 @@ __global__ void __launch_bounds__(256) k_colsum(Dev D, float* part, int lcols) {
     const int pc = (lstm && gl == 3) ? 3 * h + j : gl * h + j;
     for (int k = kk; k < min(nk, kk + 1); ++k) {
       const OpT* col = dz + pc + k * h;
-      if constexpr (sizeof(OpT) == 2) {
+      if constexpr (is_s3<OpT>::value) {                     // FP32 split mode: b0 + b1 + b2 per element
+        for (int r = r0 + warp; r < r1; r += 8) {
+          const OpT* rowp = col + (size_t)r * cols;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] += ld_op1<OpT>(rowp + e, D.ps_dz);
+        }
+      } else if constexpr (sizeof(OpT) == 2) {
         int r = r0 + warp;
         for (; r + 56 < r1; r += 64) {                      // 8 rows in flight
           uint4 u[8];
@@ -215,7 +221,7 @@ __global__ void __launch_bounds__(256) k_colsum(Dev D, float* part, int lcols) {
       const int nk = (lstm && gl == 3) ? D.N : 1;
       const int pc = (lstm && gl == 3) ? 3 * h + j : gl * h + j;
       for (int k = kk; k < min(nk, kk + 1); ++k)
-        for (int r = r0 + warp; r < r1; r += 8) acc[e] += from_op(dz[(size_t)r * cols + pc + k * h]);
+        for (int r = r0 + warp; r < r1; r += 8) acc[e] += ld_op1<OpT>(dz + (size_t)r * cols + pc + k * h, D.ps_dz);
     }
   }
 #pragma unroll
@@ -358,7 +364,7 @@ __global__ void k_dag_gather(Dev D, int lo, int hi) {
     if (k >= D.deg[p]) continue;                   // missing slots stay zero (k_build_maps, Z1)
     const int c = D.child_pos[(size_t)p * N + k];
     const size_t at = ((size_t)p * N + k) * h + j;
-    op<OpT>(D.Hk)[at] = to_op<OpT>(D.h_out[(size_t)D.order[c] * h + j]);
+    st_op1<OpT>(op<OpT>(D.Hk) + at, D.h_out[(size_t)D.order[c] * h + j], D.ps_hk);
     if (D.Ck) D.Ck[at] = D.cst[(size_t)c * h + j];
   }
 }
@@ -455,17 +461,20 @@ void launch_prep(const Dev& D, cudaStream_t s) {
   }
   dim3 grid(148, J.n);
   if (D.prec == CAVS_BF16) launch_pdl(k_prep<__nv_bfloat16>, grid, dim3(256), 0, s, D, J);
+  else if (D.split) launch_pdl(k_prep<S3>, grid, dim3(256), 0, s, D, J);
   else launch_pdl(k_prep<float>, grid, dim3(256), 0, s, D, J);
 }
 
 void launch_pull(const Dev& D, cudaStream_t s) {
   if (D.prec == CAVS_BF16) launch_pdl(k_pull<__nv_bfloat16>, dim3(cdiv(D.V, 64)), dim3(256), 0, s, D);
+  else if (D.split) launch_pdl(k_pull<S3>, dim3(cdiv(D.V, 64)), dim3(256), 0, s, D);
   else launch_pdl(k_pull<float>, dim3(cdiv(D.V, 64)), dim3(256), 0, s, D);
 }
 
 void launch_roots(const Dev& D, int n_roots, const int* roots, cudaStream_t s) {
   const size_t n = (size_t)(n_roots < 0 ? D.V : n_roots) * D.h;   // < 0: device count, grid for V
   if (D.prec == CAVS_BF16) launch_pdl(k_roots<__nv_bfloat16>, dim3(grid_for(n, 256)), dim3(256), 0, s, D, n_roots, roots);
+  else if (D.split) launch_pdl(k_roots<S3>, dim3(grid_for(n, 256)), dim3(256), 0, s, D, n_roots, roots);
   else launch_pdl(k_roots<float>, dim3(grid_for(n, 256)), dim3(256), 0, s, D, n_roots, roots);
 }
 
@@ -473,6 +482,7 @@ void launch_colsum(const Dev& D, float* part, cudaStream_t s) {
   const int lcols = (D.cell == CAVS_CELL_TREE_LSTM ? 4 : 1) * D.h;
   dim3 grid(cdiv(lcols, 256), kDbChunks * (D.cell == CAVS_CELL_TREE_LSTM ? D.N : 1));   // (slot, row chunk)
   if (D.prec == CAVS_BF16) launch_pdl(k_colsum<__nv_bfloat16>, grid, dim3(256), 0, s, D, part, lcols);
+  else if (D.split) launch_pdl(k_colsum<S3>, grid, dim3(256), 0, s, D, part, lcols);
   else launch_pdl(k_colsum<float>, grid, dim3(256), 0, s, D, part, lcols);
 }
 
@@ -517,6 +527,7 @@ void launch_dag_gather(const Dev& D, int lo, int hi, cudaStream_t s) {
   if (hi <= lo) return;
   const size_t n = (size_t)(hi - lo) * D.N * D.h;
   if (D.prec == CAVS_BF16) k_dag_gather<__nv_bfloat16><<<grid_for(n, 256), 256, 0, s>>>(D, lo, hi);
+  else if (D.split) k_dag_gather<S3><<<grid_for(n, 256), 256, 0, s>>>(D, lo, hi);
   else k_dag_gather<float><<<grid_for(n, 256), 256, 0, s>>>(D, lo, hi);
 }
 
@@ -524,6 +535,7 @@ void launch_dag_df(const Dev& D, int lo, int hi, cudaStream_t s) {
   if (hi <= lo) return;
   const size_t n = (size_t)(hi - lo) * D.h;
   if (D.prec == CAVS_BF16) k_dag_df<__nv_bfloat16><<<grid_for(n, 256), 256, 0, s>>>(D, lo, hi);
+  else if (D.split) k_dag_df<S3><<<grid_for(n, 256), 256, 0, s>>>(D, lo, hi);
   else k_dag_df<float><<<grid_for(n, 256), 256, 0, s>>>(D, lo, hi);
 }
 

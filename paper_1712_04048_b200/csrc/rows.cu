@@ -57,7 +57,18 @@ struct RPlan {
   int nbuf;        // accumulator buffers (1 or 2)
   int lo, hi;      // task rows
   int nut, ntiles; // unit tiles, tiles (of 128 CG task rows)
+  int ks;          // split-K: work item w = (tile w / ks, K share w % ks); ks > 1 only when the tiles do not
+                   // fill the GPU (CG = 1): the shares' fp32 partials meet in D.rows_part (counters
+                   // D.rows_cnt), each share sums one slice of the tile's units in share order and runs the
+                   // cell epilogue on it (r_split_reduce)
 };
+constexpr int kRowsMaxItems = 296;     // split work items (tiles x shares) with partial slots
+constexpr int kRowsMaxKs = 8;
+// K share q of ks over nkb k-blocks: [lo, hi)
+__host__ __device__ __forceinline__ void r_kshare(int nkb, int q, int ks, int& lo, int& hi) {
+  lo = (int)(((long long)nkb * q) / ks);
+  hi = (int)(((long long)nkb * (q + 1)) / ks);
+}
 
 __device__ __forceinline__ void rwait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = ptx::smem_u32(bar);
@@ -191,6 +202,72 @@ __device__ __forceinline__ void r_commit(uint64_t* bar) {
   }
 }
 
+__device__ __forceinline__ void tst16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+      ::"r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+        "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])),
+        "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
+        "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+        "r"(__float_as_uint(v[15])) : "memory");
+}
+
+// Split-K meeting point of work item (tile j, share kq), called by the 8 epilogue warps (thread = TMEM
+// lane r x column half hh) once the share's accumulator is complete.  Every share stores its fp32
+// partial (slot layout [item][column][128 lanes]: a warp writes 128 contiguous bytes per column), the
+// ks shares of the tile wait for each other (all work items are co-resident: ks x tiles <= #SMs, one
+// CTA per SM), then share kq sums the slots in share order (deterministic) for its own slice of the
+// tile's units -- columns blk UG + [kq UG/ks, (kq+1) UG/ks) of every accumulator block -- into its TMEM,
+// and runs the cell epilogue on that slice: the reduction and the epilogue are spread over all shares.
+template <class P_t>
+__device__ __forceinline__ void r_split_reduce(const Dev& D, const P_t& P, uint32_t tb, int j, int kq, int r, int hh) {
+  const int half = P.acc_cols / 2, c0 = hh * half;
+  float* part = D.rows_part;
+  for (int c = c0; c < c0 + half; c += 16) {
+    float v[16];
+    ptx::tmem_ld16(tb + (uint32_t)c, v);
+    float* dst = part + ((size_t)(j * P.ks + kq) * P.acc_cols + c) * 128 + r;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) __stcg(dst + (size_t)i * 128, v[i]);
+  }
+  __threadfence();
+  ptx::named_bar_sync(1, 256);
+  if (threadIdx.x == 64) {                             // arrive, then wait for the tile's other shares
+    int* arrive = D.rows_cnt + 2 * j;
+    atomicAdd(arrive, 1);
+    unsigned long long t0 = 0;
+    while (ptx::ld_acquire_gpu(reinterpret_cast<const uint32_t*>(arrive)) < (uint32_t)P.ks) {
+      const unsigned long long now = gtime();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 4000000000ull) __trap();
+    }
+  }
+  ptx::named_bar_sync(1, 256);
+  __threadfence();
+  const int sw = P.UG / P.ks, s0 = kq * sw;            // this share's units [s0, s0 + sw)
+  const int nblk = P.acc_cols / P.UG, nch = nblk * (sw / 16);
+  for (int ch = hh; ch < nch; ch += 2) {
+    const int c = (ch / (sw / 16)) * P.UG + s0 + (ch % (sw / 16)) * 16;
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = 0.f;
+    for (int qq = 0; qq < P.ks; ++qq) {
+      const float* src = part + ((size_t)(j * P.ks + qq) * P.acc_cols + c) * 128 + r;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] += __ldcg(src + (size_t)i * 128);
+    }
+    tst16(tb + (uint32_t)c, v);
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  ptx::tc_fence_before();
+  ptx::named_bar_sync(1, 256);                         // both halves' columns stored; partials all read
+  ptx::tc_fence_after();
+  if (threadIdx.x == 64) {                             // the last share out resets the tile's counters
+    int* arrive = D.rows_cnt + 2 * j;
+    if (atomicAdd(arrive + 1, 1) == P.ks - 1) { arrive[0] = 0; arrive[1] = 0; }
+  }
+}
+
 template <int E, int NM, int QB, int CG>
 __global__ void __launch_bounds__(kRThreads, 1)
 k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB0,
@@ -236,13 +313,16 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
     ptx::griddep_wait();                                 // task rows come from the previous kernels
     if (lane <= 4) {
       int step = 0;
-      for (int j = unit; j < P.ntiles; j += nunits) {
+      for (int w = unit; w < P.ntiles * P.ks; w += nunits) {
+        const int j = w / P.ks, kq = w % P.ks;
         const int p0 = P.lo + (j / P.nut) * 128 * CG + 128 * rank, u0 = (j % P.nut) * P.UG;
         for (int sg = 0; sg < P.nseg; ++sg) {
           const RSeg& Sg = P.seg[sg];
           const CUtensorMap* mb = Sg.bmap ? &mB1 : &mB0;
           const int own = Sg.nbox / CG;                  // this CTA's B boxes: [rank own, +own)
-          for (int kb = 0; kb < Sg.nkb; ++kb, ++step) {
+          int kb0, kb1;
+          r_kshare(Sg.nkb, kq, P.ks, kb0, kb1);
+          for (int kb = kb0; kb < kb1; ++kb, ++step) {
             const int s = step % S;
             if (lane > own) continue;
             if (step >= S) rwait(&empty[s], ((step / S) & 1) ^ 1);
@@ -269,7 +349,8 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
     if (lane == 0 && leader) {
       const uint32_t idesc = ptx::idesc_bf16(128 * CG, P.n, 0, 0);
       int step = 0;
-      for (int j = unit, k = 0; j < P.ntiles; j += nunits, ++k) {
+      for (int w = unit, k = 0; w < P.ntiles * P.ks; w += nunits, ++k) {
+        const int kq = w % P.ks;
         const int buf = P.nbuf == 2 ? (k & 1) : 0;
         const int use = P.nbuf == 2 ? (k >> 1) : k;       // earlier uses of this buffer
         if (use > 0) rwait(&acce[buf], (use - 1) & 1);
@@ -277,7 +358,9 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
         const uint32_t tb = tmem + (uint32_t)(buf * P.acc_cols);
         for (int sg = 0; sg < P.nseg; ++sg) {
           const RSeg& Sg = P.seg[sg];
-          for (int kb = 0; kb < Sg.nkb; ++kb, ++step) {
+          int kb0, kb1;
+          r_kshare(Sg.nkb, kq, P.ks, kb0, kb1);
+          for (int kb = kb0; kb < kb1; ++kb, ++step) {
             const int s = step % S;
             rwait(&full[s], (step / S) & 1);
             ptx::tc_fence_after();
@@ -285,7 +368,8 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
 #ifndef CAVS_ROWS_NOMMA
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              r_mma<CG>(tb + (uint32_t)Sg.acc_col, r_desc(a + kk * 32), r_desc(b + kk * 32), idesc, (kb | kk) ? 1u : 0u);
+              r_mma<CG>(tb + (uint32_t)Sg.acc_col, r_desc(a + kk * 32), r_desc(b + kk * 32), idesc,
+                        (kb != kb0 || kk) ? 1u : 0u);
 #else
             (void)a; (void)b; (void)idesc;                   // A/B only: TMA stream without MMAs
 #endif
@@ -307,7 +391,8 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
         asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(acce_remote[b]) : "r"(ptx::smem_u32(&acce[b])));
     }
     ptx::griddep_wait();
-    for (int j = unit, k = 0; j < P.ntiles; j += nunits, ++k) {
+    for (int w = unit, k = 0; w < P.ntiles * P.ks; w += nunits, ++k) {
+      const int j = w / P.ks;
       const int p0 = P.lo + (j / P.nut) * 128 * CG + 128 * rank, u0 = (j % P.nut) * P.UG;
       const int p = p0 + r;
       const bool valid = p < P.hi;
@@ -318,10 +403,13 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
       rwait(&accf[buf], use & 1);
       ptx::tc_fence_after();
       const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * P.acc_cols);
-      const int ub = hh * (P.UG / 2);                    // this thread's first unit within the tile
+      // split-K: the shares of the tile meet, share kq finishes the units [kq UG/ks, (kq+1) UG/ks)
+      if (P.ks > 1) r_split_reduce(D, P, tb, j, w % P.ks, r, hh);
+      const int sw = P.UG / P.ks;                        // units finished by this work item
+      const int ub = (w % P.ks) * sw + hh * (sw / 2);    // this thread's first unit within the tile
       // VW units per item: 8 (one 32-byte sector per row and output stream: 256-bit accesses)
       constexpr int VW = 8;
-      const int ipt = P.UG / 2 / VW;                     // items per thread
+      const int ipt = sw / 2 / VW;                       // items per thread
       if constexpr (E == EPI_LSTM_BWD) {
         // Tree-LSTM backward: the children's dF one child at a time (its state in registers, 8 units
         // per access), the gradient sent to child k = dh~ + U_f^T dz_fk (cells.cuh EpiK)
@@ -406,7 +494,24 @@ struct RowsState {
   RPlan fwd{}, bwd{};
   int num_sms = 148;
   int cg = 1;                          // CTAs per MMA: 2 = CTA pairs (cta_group::2, opt-in), 1 = single CTA
+  bool can_split = false;              // split-K partial slots carved (D.rows_part) and not disabled
+  bool lstm = false;
+  bool sel_items = false;              // rows_tiles counts work items (tiles x shares) instead of tiles
 };
+
+// split-K shares of a task of ntiles tiles: only when the tiles leave SMs idle (CG = 1); every segment
+// keeps >= 2 k-blocks per share; at most kRowsMaxItems work items (partial slots)
+static int r_ks(const RowsState* rs, const RPlan& P, int ntiles) {
+  if (rs->cg != 1 || !rs->can_split || ntiles >= rs->num_sms || ntiles < 1) return 1;
+  int min_nkb = 1 << 30;
+  for (int sg = 0; sg < P.nseg; ++sg) min_nkb = std::min(min_nkb, P.seg[sg].nkb);
+  int ks = std::max(1, std::min({kRowsMaxKs, rs->num_sms / ntiles, min_nkb / 2, kRowsMaxItems / ntiles}));
+  // every share finishes a slice of UG / ks units: a whole number of 16-column chunks per column half
+  // and of epilogue rounds (QB items of 8 units: 2 for Tree-FC, 1 for Tree-LSTM)
+  const int qb = rs->lstm ? 1 : 2;
+  while (ks > 1 && (P.UG % ks || (P.UG / ks) % (16 * qb))) --ks;
+  return ks;
+}
 
 static PFN_cuTensorMapEncodeTiled_v12000 r_enc = nullptr;
 
@@ -474,6 +579,11 @@ RowsState* rows_init(const Dev& D, int max_vertices) {
   // (the pair's TMA stream runs in lockstep on the slower SM; profiles/r02_rows.md)
   const char* pe = std::getenv("CAVS_ROWS_PAIR");
   rs->cg = (pe && pe[0] == '1') ? 2 : 1;
+  const char* ke = std::getenv("CAVS_ROWS_KSPLIT");
+  rs->can_split = D.rows_part && D.rows_cnt && !(ke && ke[0] == '0');
+  rs->lstm = D.cell == CAVS_CELL_TREE_LSTM;
+  const char* se = std::getenv("CAVS_ROWS_SEL");
+  rs->sel_items = se ? se[0] == 'i' : !rs->lstm;
   const int CG = rs->cg;
   const uint64_t Vp = (uint64_t)max_vertices + kPadRows, G = lstm ? 3 + N : 1;
   bool ok = renc(&rs->A_hk, D.Hk, (uint64_t)N * h, Vp, 128) && renc(&rs->A_dz, D.dZ, G * h, Vp, 128);
@@ -525,8 +635,13 @@ RowsState* rows_init(const Dev& D, int max_vertices) {
 
 void rows_destroy(RowsState* rs) { delete rs; }
 
+// a task's size measure for the caller's "use the row-tiled kernel" threshold: its tiles, or (Tree-FC,
+// or CAVS_ROWS_SEL=items) its work items = tiles x split-K shares
 int rows_tiles(const RowsState* rs, bool backward, int rows) {
-  return rs ? cdiv(rows, 128) * (backward ? rs->bwd.nut : rs->fwd.nut) : 0;
+  if (!rs) return 0;
+  const RPlan& P = backward ? rs->bwd : rs->fwd;
+  const int nt = cdiv(rows, 128 * rs->cg) * P.nut;
+  return rs->sel_items ? nt * r_ks(rs, P, nt) : nt;
 }
 
 int rows_pair(const RowsState* rs) { return rs ? rs->cg : 0; }
@@ -552,7 +667,10 @@ static void r_launch(const CUtensorMap& a, const CUtensorMap& b0, const CUtensor
 template <int CG>
 static void rows_go(const Dev& D, RowsState* rs, bool backward, RPlan& P, cudaStream_t s) {
   P.ntiles = cdiv(P.hi - P.lo, 128 * CG) * P.nut;
-  const int grid = std::min(P.ntiles * CG, rs->num_sms / CG * CG);
+  // split-K when the tiles leave SMs idle: ks shares per tile (every segment keeps >= 2 k-blocks
+  // per share), at most kRowsMaxItems work items (partial slots)
+  P.ks = r_ks(rs, P, P.ntiles);
+  const int grid = std::min(P.ntiles * P.ks * CG, rs->num_sms / CG * CG);
   const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
   if (lstm) {
     if (!backward) {

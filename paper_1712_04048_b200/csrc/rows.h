@@ -7,7 +7,7 @@ namespace cavs {
 struct RowsState;
 RowsState* rows_init(const Dev& D, int max_vertices);   // nullptr: shape not supported / disabled
 void rows_destroy(RowsState* rs);
-int rows_tiles(const RowsState* rs, bool backward, int rows);   // tiles of a task of `rows` rows
+int rows_tiles(const RowsState* rs, bool backward, int rows);   // size of a task in tiles (or work items, see rows.cu)
 int rows_pair(const RowsState* rs);                             // CTAs per MMA (2: cta_group::2 pairs)
 // one task V_t = rows [lo, hi) of the forward (or backward) level step; false: caller falls back
 bool rows_level(const Dev& D, RowsState* rs, bool backward, int lo, int hi, cudaStream_t s);

@@ -282,7 +282,7 @@ __global__ void k_build_maps(Dev D) {
     // an internal vertex with fewer than N children reads zero in its missing slots (Z1)
     if (deg > 0 && deg < D.N) {
       OpT* hk = reinterpret_cast<OpT*>(D.Hk) + (size_t)p * D.N * D.h;
-      for (int i = deg * D.h; i < D.N * D.h; ++i) hk[i] = to_op<OpT>(0.f);
+      for (int i = deg * D.h; i < D.N * D.h; ++i) st_op1<OpT>(hk + i, 0.f, D.ps_hk);
       if (D.Ck) for (int i = deg * D.h; i < D.N * D.h; ++i) D.Ck[(size_t)p * D.N * D.h + i] = 0.f;
     }
   }
@@ -300,6 +300,7 @@ void launch_schedule(const Dev& D, cudaStream_t s) {
   launch_pdl(k_level_offsets, dim3(148), dim3(1024), 0, s, D);
   const int g = std::min(cdiv(D.V, 256), 148 * 8);
   if (D.prec == CAVS_BF16) launch_pdl(k_build_maps<__nv_bfloat16>, dim3(g), dim3(256), 0, s, D);
+  else if (D.split) launch_pdl(k_build_maps<S3>, dim3(g), dim3(256), 0, s, D);
   else launch_pdl(k_build_maps<float>, dim3(g), dim3(256), 0, s, D);
 }
 

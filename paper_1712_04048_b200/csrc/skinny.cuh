@@ -1,4 +1,4 @@
-// skinny.cu — level kernel for SMALL tasks (M_t <= kSkinnyMax vertices), both precisions.
+// skinny.cuh — level kernel for SMALL tasks (M_t <= kSkinnyMax vertices), both precisions.
 //
 // A task of a few vertices is bound by streaming F's weights (2-8 MB) through the SMs, not by
 // math: the tensor-core kernel puts 128 units per CTA, i.e. only h/128 CTAs each pulling
@@ -8,6 +8,9 @@
 // tensor-core path), every warp loads its whole weight rows up front (one latency), and
 // the K dot products run with fp32 accumulation and a shuffle reduction.  The fused
 // epilogue is the same cells.cuh code as every other level kernel.
+#pragma once
+// (implementation shared by skinny_f32.cu / skinny_bf16.cu: one instantiation per translation unit,
+// so the two heavily unrolled kernel sets compile in parallel)
 #include "cells.cuh"
 #include "kernels.h"
 
@@ -173,19 +176,6 @@ static void sk(const Dev& D, const SegListI& L, int row_lo, int row_hi, int unit
   else sk_mv<OpT, NACC, E, 32>(D, L, row_lo, row_hi, units, s);
 }
 
-int skinny_max(const Dev& D) {
-  // 16-byte vector access needs every row width / column offset to be a multiple of the vector
-  const int es = D.prec == CAVS_BF16 ? 2 : 4;
-  const int ve = 16 / es;
-  if (D.h % ve || D.d % ve) return 0;
-  // staged rows must fit shared memory: widest source row (+ h~) x MV operands
-  const int G = D.cell == CAVS_CELL_TREE_LSTM ? 3 + D.N : 1;
-  const int W = std::max(D.N * D.h, G * D.h);
-  int mv = kSkinnyMax;
-  while (mv > 4 && (size_t)mv * W * es > 180 * 1024) mv /= 2;
-  return mv;
-}
-
 template <class OpT>
 void skinny_typeI(const Dev& D, int epi, const SegListI& L, int row_lo, int row_hi, int units, cudaStream_t s) {
   if (row_hi <= row_lo) return;
@@ -212,7 +202,5 @@ void skinny_typeI(const Dev& D, int epi, const SegListI& L, int row_lo, int row_
   }
 }
 
-template void skinny_typeI<float>(const Dev&, int, const SegListI&, int, int, int, cudaStream_t);
-template void skinny_typeI<__nv_bfloat16>(const Dev&, int, const SegListI&, int, int, int, cudaStream_t);
 
 }  // namespace cavs

@@ -53,10 +53,16 @@ struct Bundle {
 struct RankPlan { int nb; Bundle b[3]; int nacc; int stages; int stage_bytes; int offB; };
 // CL = 1: rank 0 only; CL = kCluster: one plan per rank.  comb[e][r] = accumulator of rank r
 // summed into epilogue slot e (-1: none).
-struct PlanT { RankPlan r[kCluster]; int comb[8][kCluster]; int bar_off; };
+// npair = 6 in the FP32 split mode (bf16x3 operands): every bundle's k-loop runs
+// once per plane pair (s, t) with s + t <= 2, A plane s at A row + s a_prow[map], B plane t at task
+// row + t b_prow (plane-major arenas); npair = 1: plain bf16.
+struct PlanT { RankPlan r[kCluster]; int comb[8][kCluster]; int bar_off; int npair; int a_prow[2]; int b_prow; };
+__device__ __constant__ const int kPairS[6] = {0, 0, 1, 0, 1, 2};
+__device__ __constant__ const int kPairT[6] = {0, 1, 0, 2, 1, 0};
 
-struct SegT2 { int a_col; int b_col; int k_lo, k_hi; int skip_no_x; };
-struct PlanII { int nseg; SegT2 s[4]; int M, Ncols, ldo; int split; size_t split_stride; int stages; int accum; };
+// a_roff / b_roff: row (vertex) offset of the operand plane (FP32 split mode: plane q at q * Vp)
+struct SegT2 { int a_col; int b_col; int k_lo, k_hi; int skip_no_x; int a_roff = 0, b_roff = 0; int corr = 0; };
+struct PlanII { int nseg; SegT2 s[24]; int M, Ncols, ldo; int split; size_t split_stride; int stages; int accum; };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~(uintptr_t)1023);
@@ -83,7 +89,7 @@ __device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
 
 // ------------------------------------------------------------------------------------
 // Type-I kernel.  CL = 1 (monolithic) or kCluster (gate split).
-template <int E, int NACC, int CL>
+template <int E, int NACC, int CL, class OpT>
 __global__ void __launch_bounds__(kThreads, 1)
 k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
            const __grid_constant__ CUtensorMap mB, Dev D, PlanT P, int row_lo, int row_hi, int units) {
@@ -135,7 +141,8 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
       constexpr uint32_t idesc = ptx::idesc_bf16(128, NT, 0, 0);
       uint32_t written = 0;                            // accumulators already initialised
       int step = 0;
-      for (int bi = 0; bi < R.nb; ++bi) {
+      for (int bi = 0; bi < R.nb; ++bi)
+      for (int pr = 0; pr < P.npair; ++pr) {
         const Bundle& b = R.b[bi];
         for (int kb = 0; kb < b.nk; ++kb, ++step) {
           const int s = step % S;
@@ -146,7 +153,10 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
           for (int m = 0; m < b.nmma; ++m) {
             const uint32_t a = st + b.mma_a[m] * A_TILE;
             const uint32_t bb = st + R.offB + b.mma_b[m] * B_TILE;
-            const int acc = b.mma_acc[m];
+            // split mode: the five correction products (pairs 1..5, ~2^-8 of the main one) accumulate
+            // separately (acc + nacc): the tensor core's fp32 accumulation then adds them into a small
+            // sum, and the main chain a0 b0 keeps plain bf16 MMA's number of accumulation steps
+            const int acc = b.mma_acc[m] + (pr > 0 ? R.nacc : 0);
             const uint32_t d = tmem + acc * NT;
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk)
@@ -169,9 +179,11 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
       const int w = warp - 2;
       bool waited = false;
       int step = 0;
-      for (int bi = 0; bi < R.nb; ++bi) {
+      for (int bi = 0; bi < R.nb; ++bi)
+      for (int pr = 0; pr < P.npair; ++pr) {
         const Bundle& b = R.b[bi];
         const CUtensorMap* ma = b.map_a ? &mA1 : &mA0;
+        const int arow = m0 + kPairS[pr] * P.a_prow[b.map_a], brow = p0 + kPairT[pr] * P.b_prow;
         for (int kb = 0; kb < b.nk; ++kb, ++step) {
           if (step % S != w) continue;
           const int s = step % S;
@@ -180,10 +192,10 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
           if (step >= S) ptx::mbar_wait(&empty[s], ph ^ 1);
           ptx::mbar_arrive_expect_tx(&full[s], b.nA * A_TILE + b.nB * B_TILE);
           for (int i = 0; i < b.nA; ++i)
-            ptx::tma_load_2d(st + i * A_TILE, ma, b.a_col0 + kb * BK, b.a_row[i] + m0, &full[s]);
+            ptx::tma_load_2d(st + i * A_TILE, ma, b.a_col0 + kb * BK, b.a_row[i] + arow, &full[s]);
           if (!waited) { ptx::griddep_wait(); waited = true; }
           for (int i = 0; i < b.nB; ++i)
-            ptx::tma_load_2d(st + R.offB + i * B_TILE, &mB, b.b_col[i] + kb * BK, p0, &full[s]);
+            ptx::tma_load_2d(st + R.offB + i * B_TILE, &mB, b.b_col[i] + kb * BK, brow, &full[s]);
         }
       }
     } else {
@@ -206,6 +218,12 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
       for (int c0 = grp * 32; c0 < grp * 32 + 32; c0 += 8) {
         float v[8];
         ptx::tmem_ld<8>(tq + a * NT + c0, v);
+        if (P.npair > 1) {                               // split mode: main + corrections (fp32, RN)
+          float w[8];
+          ptx::tmem_ld<8>(tq + (a + R.nacc) * NT + c0, w);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] += w[i];
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) xs[((size_t)a * NT + c0 + i) * 128 + qd * 32 + lane] = v[i];
       }
@@ -263,7 +281,7 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
       }
 #pragma unroll
       for (int i = 0; i < CH; ++i)                     // ... then the math and the stores
-        if (ok[i]) EpiK<E>::template store<__nv_bfloat16, 4, NM>(D, j, s_meta[cg + 8 * (i0 + i)], acc[i], in[i], uc);
+        if (ok[i]) EpiK<E>::template store<OpT, 4, NM>(D, j, s_meta[cg + 8 * (i0 + i)], acc[i], in[i], uc);
     }
   }
   if constexpr (CL > 1) cluster_sync_all();            // remote reads done before smem is released
@@ -303,6 +321,8 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
   uint64_t* done = empty + S;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
   int* s_count = reinterpret_cast<int*>(tmem_slot + 1);
+  int& s_main = s_count[1];                           // the main / correction accumulator was written
+  int& s_corr = s_count[2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * 128, n0 = blockIdx.y * 128, z = blockIdx.z;
   int nkb_total = 0;
@@ -316,7 +336,7 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
     ptx::fence_mbar_init();
     *s_count = 0;
   }
-  if (warp == 1) ptx::tmem_alloc<128>(tmem_slot);
+  if (warp == 1) ptx::tmem_alloc<256>(tmem_slot);      // [0,128): main, [128,256): split-mode corrections
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -329,6 +349,7 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_bf16(128, 128, 1, 1);
       int step = 0, g = 0;
+      uint32_t wrote = 0;                              // accumulators initialised (bit 0 main, bit 1 corr)
       for (int si = 0; si < P.nseg; ++si) {
         const SegT2 sg = P.s[si];
         const int nkb = cdiv(sg.k_hi - sg.k_lo, 64);
@@ -341,15 +362,19 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
           ptx::tc_fence_after();
           const uint32_t a = ptx::smem_u32(smem + s * STAGE);
           const uint32_t b = a + T2_TILE;
+          const uint32_t ac = (uint32_t)sg.corr;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            ptx::mma_bf16(tmem, ptx::sdesc_sw128(a + kk * 2048, 8192, 1024), ptx::sdesc_sw128(b + kk * 2048, 8192, 1024),
-                          idesc, (step > 0 || kk > 0) ? 1u : 0u);
+            ptx::mma_bf16(tmem + ac * 128, ptx::sdesc_sw128(a + kk * 2048, 8192, 1024),
+                          ptx::sdesc_sw128(b + kk * 2048, 8192, 1024), idesc, ((wrote >> ac) & 1u) | (kk > 0 ? 1u : 0u));
+          wrote |= 1u << ac;
           ptx::mma_commit(&empty[s]);
           ++step;
         }
       }
       *s_count = step;
+      s_main = wrote & 1u;
+      s_corr = (wrote >> 1) & 1u;
       ptx::mma_commit(done);
     }
     __syncwarp();
@@ -371,10 +396,10 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
             if (step >= S) ptx::mbar_wait(&empty[s], ph ^ 1);
             uint8_t* st = smem + s * STAGE;
             ptx::mbar_arrive_expect_tx(&full[s], STAGE);
-            ptx::tma_load_2d(st, &mA, sg.a_col + m0, r0, &full[s]);
-            ptx::tma_load_2d(st + T2_TILE / 2, &mA, sg.a_col + m0 + 64, r0, &full[s]);
-            ptx::tma_load_2d(st + T2_TILE, &mB, sg.b_col + n0, r0, &full[s]);
-            ptx::tma_load_2d(st + T2_TILE + T2_TILE / 2, &mB, sg.b_col + n0 + 64, r0, &full[s]);
+            ptx::tma_load_2d(st, &mA, sg.a_col + m0, r0 + sg.a_roff, &full[s]);
+            ptx::tma_load_2d(st + T2_TILE / 2, &mA, sg.a_col + m0 + 64, r0 + sg.a_roff, &full[s]);
+            ptx::tma_load_2d(st + T2_TILE, &mB, sg.b_col + n0, r0 + sg.b_roff, &full[s]);
+            ptx::tma_load_2d(st + T2_TILE + T2_TILE / 2, &mB, sg.b_col + n0 + 64, r0 + sg.b_roff, &full[s]);
           }
           ++step;
         }
@@ -392,6 +417,16 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
       for (int c = 0; c < 128; c += 16) {
         float v[16];
         ptx::tmem_ld16(tq + c, v);
+        if (!s_main) {                                 // (a split-K slot with correction blocks only)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        if (s_corr) {                                  // split mode: main + corrections (fp32, RN)
+          float w[16];
+          ptx::tmem_ld16(tq + 128 + c, w);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += w[i];
+        }
         if (m < P.M) {
           for (int i = 0; i < 16; ++i) {
             const int n = n0 + c + i;
@@ -409,7 +444,7 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
   __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<128>(tmem);
+    ptx::tmem_dealloc<256>(tmem);
   }
 }
 
@@ -428,8 +463,40 @@ struct TcState {
   LazyState* ls = nullptr;      // stream-K lazy weight-gradient GEMMs (lazy.cu)
   RowsState* rs = nullptr;      // row-tiled level GEMMs for large tasks when the persistent path is off (rows.cu)
   int rows_min_tiles = 64;      // a task uses the row-tiled kernel from this many tiles on
+  // FP32 split mode (bf16x3 operands): rows between the planes of each A map (the weight copy's
+  // row count) and of the arenas (Vp); 0 = plain bf16
+  int split = 0;
+  int prow[5] = {0, 0, 0, 0, 0};
+  int vp = 0;
   std::string info;
 };
+
+// The launch's plane pairs (FP32 split mode: six products a_s b_t, s + t <= 2, of the bf16x3
+// operands; PlanT::npair) for a plan whose A tiles come from A maps ia0 / ia1.
+static PlanT pl(const TcState* t, PlanT P, int ia0, int ia1) {
+  P.npair = t->split ? 6 : 1;
+  P.a_prow[0] = t->split ? t->prow[ia0] : 0;
+  P.a_prow[1] = t->split ? t->prow[ia1] : 0;
+  P.b_prow = t->split ? t->vp : 0;
+  return P;
+}
+// Type II in the split mode: every segment becomes the six plane-pair segments (rows of plane q of
+// an arena start q * Vp rows after plane 0: the MN-major maps span all three planes)
+static PlanII pl2(const TcState* t, PlanII P) {
+  if (!t->split) return P;
+  static const int ps[6] = {0, 0, 1, 0, 1, 2}, pt[6] = {0, 1, 0, 2, 1, 0};
+  PlanII Q = P;
+  Q.nseg = 0;
+  for (int i = 0; i < P.nseg; ++i)
+    for (int q = 0; q < 6; ++q) {
+      SegT2 sg = P.s[i];
+      sg.a_roff = ps[q] * t->vp;
+      sg.b_roff = pt[q] * t->vp;
+      sg.corr = q > 0 ? 1 : 0;
+      Q.s[Q.nseg++] = sg;
+    }
+  return Q;
+}
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
@@ -464,30 +531,49 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
   const uint64_t h = D.h, d = D.d, N = D.N, Vp = (uint64_t)max_vertices + kPadRows;
   const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
   const uint64_t G = lstm ? 3 + N : 1;
+  // FP32 split mode: each map spans the three bf16 planes (plane-major: plane q starts q x the
+  // plane's row count after plane 0), the plans add the plane row offsets (pl / pl2)
+  const uint64_t np = D.split ? 3 : 1;
+  t->split = D.split;
+  t->vp = (int)Vp;
   bool ok = true;
   if (lstm) {
-    ok &= encode(&t->A[0], D.Wa, h, 4 * h, h, BK, 128);          // U4   [4h x h]
-    ok &= encode(&t->A[1], D.Wb, d, 4 * h, d, BK, 128);          // W4   [4h x d]
-    ok &= encode(&t->A[2], D.Wc, 3 * h, h, 3 * h, BK, 128);      // UTiou[h x 3h]
-    ok &= encode(&t->A[3], D.Wd, h, h, h, BK, 128);              // UTf  [h x h]
-    ok &= encode(&t->A[4], D.We, G * h, d, G * h, BK, 128);      // WT   [d x G h]
+    ok &= encode(&t->A[0], D.Wa, h, np * 4 * h, h, BK, 128);          // U4   [4h x h]
+    ok &= encode(&t->A[1], D.Wb, d, np * 4 * h, d, BK, 128);          // W4   [4h x d]
+    ok &= encode(&t->A[2], D.Wc, 3 * h, np * h, 3 * h, BK, 128);      // UTiou[h x 3h]
+    ok &= encode(&t->A[3], D.Wd, h, np * h, h, BK, 128);              // UTf  [h x h]
+    ok &= encode(&t->A[4], D.We, G * h, np * d, G * h, BK, 128);      // WT   [d x G h]
+    const int pr[5] = {(int)(4 * h), (int)(4 * h), (int)h, (int)h, (int)d};
+    for (int i = 0; i < 5; ++i) t->prow[i] = pr[i];
   } else {
-    ok &= encode(&t->A[0], D.Wa, 2 * h, h, 2 * h, BK, 128);      // Wc   [h x 2h]
-    ok &= encode(&t->A[1], D.Wb, d, h, d, BK, 128);              // Wx   [h x d]
-    ok &= encode(&t->A[2], D.Wc, h, 2 * h, h, BK, 128);          // WcT  [2h x h]
+    ok &= encode(&t->A[0], D.Wa, 2 * h, np * h, 2 * h, BK, 128);      // Wc   [h x 2h]
+    ok &= encode(&t->A[1], D.Wb, d, np * h, d, BK, 128);              // Wx   [h x d]
+    ok &= encode(&t->A[2], D.Wc, h, np * 2 * h, h, BK, 128);          // WcT  [2h x h]
     t->A[3] = t->A[2];
-    ok &= encode(&t->A[4], D.We, h, d, h, BK, 128);              // WxT  [d x h]
+    ok &= encode(&t->A[4], D.We, h, np * d, h, BK, 128);              // WxT  [d x h]
+    const int pr[5] = {(int)h, (int)h, (int)(2 * h), (int)(2 * h), (int)d};
+    for (int i = 0; i < 5; ++i) t->prow[i] = pr[i];
   }
-  ok &= encode(&t->B_hk, D.Hk, N * h, Vp, N * h, BK, NT);
-  ok &= encode(&t->B_xp, D.Xp, d, Vp, d, BK, NT);
-  ok &= encode(&t->B_dz, D.dZ, G * h, Vp, G * h, BK, NT);
-  ok &= encode(&t->M_dz, D.dZ, G * h, Vp, G * h, 64, 64);
-  ok &= encode(&t->M_hk, D.Hk, N * h, Vp, N * h, 64, 64);
-  ok &= encode(&t->M_xp, D.Xp, d, Vp, d, 64, 64);
+  ok &= encode(&t->B_hk, D.Hk, N * h, np * Vp, N * h, BK, NT);
+  ok &= encode(&t->B_xp, D.Xp, d, np * Vp, d, BK, NT);
+  ok &= encode(&t->B_dz, D.dZ, G * h, np * Vp, G * h, BK, NT);
+  ok &= encode(&t->M_dz, D.dZ, G * h, np * Vp, G * h, 64, 64);
+  ok &= encode(&t->M_hk, D.Hk, N * h, np * Vp, N * h, 64, 64);
+  ok &= encode(&t->M_xp, D.Xp, d, np * Vp, d, 64, 64);
   if (!ok) {
     *err = "cuTensorMapEncodeTiled failed";
     delete t;
     return CAVS_E_CUDA;
+  }
+  if (D.split) {
+    // FP32 mode on the tensor cores: the per-task type-I kernels (gate-split clusters, monolithic
+    // x-projection / dX) and the split-K type-II lazy GEMMs, six bf16 MMAs per fp32 product
+    t->use_simt = false;
+    t->mono = false;
+    t->info = "levels: FP32 on tcgen05 (bf16x3 split operands, 6 MMAs per product), per-task launches; "
+              "lazy: split-K tcgen05 + pack";
+    *out = t;
+    return CAVS_OK;
   }
   if (!t->use_simt) t->gs = gemm_init(D, max_vertices);
   if (!t->use_simt) t->ls = lazy_init(D, max_vertices);
@@ -534,6 +620,7 @@ void tc_destroy(TcState* tc) {
 // ---- type-I plans ---------------------------------------------------------------------
 static PlanT plan_empty() {
   PlanT P{};
+  P.npair = 1;
   for (int e = 0; e < 8; ++e)
     for (int r = 0; r < kCluster; ++r) P.comb[e][r] = -1;
   return P;
@@ -693,7 +780,7 @@ static PlanT mono_one(int K, int e_count, const int* a_rows, const int* b_cols) 
   return P;
 }
 
-template <int E, int NACC, int CL>
+template <int E, int NACC, int CL, class OpT>
 static void launch_level(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const Dev& D, PlanT P,
                          int row_lo, int row_hi, int units, cudaStream_t s) {
   if (row_hi <= row_lo) return;
@@ -701,7 +788,7 @@ static void launch_level(const CUtensorMap& a0, const CUtensorMap& a1, const CUt
   static int attr_set[kMaxDev] = {};                   // dynamic + static smem must stay <= 227 KB
   const int dv = cur_device();
   if (smem > attr_set[dv]) {
-    cudaFuncSetAttribute(k_tc_level<E, NACC, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_tc_level<E, NACC, CL, OpT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr_set[dv] = smem;
   }
   cudaLaunchConfig_t cfg{};
@@ -720,22 +807,22 @@ static void launch_level(const CUtensorMap& a0, const CUtensorMap& a1, const CUt
   ++na;
   cfg.attrs = at2;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, k_tc_level<E, NACC, CL>, a0, a1, b, D, P, row_lo, row_hi, units);
+  cudaLaunchKernelEx(&cfg, k_tc_level<E, NACC, CL, OpT>, a0, a1, b, D, P, row_lo, row_hi, units);
 }
 
 // per-task dispatch on the arity N (NACC = BASE + N)
-template <int E, int BASE>
+template <int E, int BASE, class OpT>
 static void level_N(bool gs, int N, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const Dev& D,
                     const PlanT& P, int lo, int hi, int units, cudaStream_t s) {
   switch (N) {
-    case 1: gs ? launch_level<E, BASE + 1, kCluster>(a0, a1, b, D, P, lo, hi, units, s)
-               : launch_level<E, BASE + 1, 1>(a0, a1, b, D, P, lo, hi, units, s); break;
-    case 2: gs ? launch_level<E, BASE + 2, kCluster>(a0, a1, b, D, P, lo, hi, units, s)
-               : launch_level<E, BASE + 2, 1>(a0, a1, b, D, P, lo, hi, units, s); break;
-    case 3: gs ? launch_level<E, BASE + 3, kCluster>(a0, a1, b, D, P, lo, hi, units, s)
-               : launch_level<E, BASE + 3, 1>(a0, a1, b, D, P, lo, hi, units, s); break;
-    default: gs ? launch_level<E, BASE + 4, kCluster>(a0, a1, b, D, P, lo, hi, units, s)
-                : launch_level<E, BASE + 4, 1>(a0, a1, b, D, P, lo, hi, units, s); break;
+    case 1: gs ? launch_level<E, BASE + 1, kCluster, OpT>(a0, a1, b, D, P, lo, hi, units, s)
+               : launch_level<E, BASE + 1, 1, OpT>(a0, a1, b, D, P, lo, hi, units, s); break;
+    case 2: gs ? launch_level<E, BASE + 2, kCluster, OpT>(a0, a1, b, D, P, lo, hi, units, s)
+               : launch_level<E, BASE + 2, 1, OpT>(a0, a1, b, D, P, lo, hi, units, s); break;
+    case 3: gs ? launch_level<E, BASE + 3, kCluster, OpT>(a0, a1, b, D, P, lo, hi, units, s)
+               : launch_level<E, BASE + 3, 1, OpT>(a0, a1, b, D, P, lo, hi, units, s); break;
+    default: gs ? launch_level<E, BASE + 4, kCluster, OpT>(a0, a1, b, D, P, lo, hi, units, s)
+                : launch_level<E, BASE + 4, 1, OpT>(a0, a1, b, D, P, lo, hi, units, s); break;
   }
 }
 
@@ -748,8 +835,8 @@ static bool xproj_streamed(Dev& D, TcState* t, const std::vector<int>& lp, cudaS
   const int zero = 0;
   const PlanT X = lstm ? mono_lstm_xproj(h, d) : mono_one(d, 1, &zero, &zero);
   auto proj = [&](int lo, int hi, cudaStream_t st) {
-    if (lstm) launch_level<EPI_LSTM_XPROJ, 4, 1>(t->A[1], t->A[1], t->B_xp, D, X, lo, hi, h, st);
-    else launch_level<EPI_FC_XPROJ, 1, 1>(t->A[1], t->A[1], t->B_xp, D, X, lo, hi, h, st);
+    if (lstm) launch_level<EPI_LSTM_XPROJ, 4, 1, __nv_bfloat16>(t->A[1], t->A[1], t->B_xp, D, X, lo, hi, h, st);
+    else launch_level<EPI_FC_XPROJ, 1, 1, __nv_bfloat16>(t->A[1], t->A[1], t->B_xp, D, X, lo, hi, h, st);
   };
   while ((int)xs->ev.size() < T) { cudaEvent_t e; cudaEventCreateWithFlags(&e, cudaEventDisableTiming); xs->ev.push_back(e); }
   cudaEventRecord(xs->start, s);                     // prep / pull done
@@ -763,7 +850,8 @@ static bool xproj_streamed(Dev& D, TcState* t, const std::vector<int>& lp, cudaS
   return true;
 }
 
-void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, Prof& P, XStream* xs) {
+template <class OpT>
+static void fwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, Prof& P, XStream* xs) {
   const int skmax = skinny_max(D);
   if (t->use_simt) { simt_forward<__nv_bfloat16>(D, lp, s, P, xs); return; }
   const int h = D.h, d = D.d, N = D.N, T = (int)lp.size() - 1;
@@ -777,7 +865,7 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
     // eager pull projection fused with task 0 (large: monolithic CTAs reuse the x tile for 4 gates)
     if (!streamed) {
       if (!gemm_xproj(D, t->gs, s))
-        launch_level<EPI_LSTM_XPROJ, 4, 1>(t->A[1], t->A[1], t->B_xp, D, mono_lstm_xproj(h, d), 0, D.V, h, s);
+        launch_level<EPI_LSTM_XPROJ, 4, 1, OpT>(t->A[1], t->A[1], t->B_xp, D, pl(t, mono_lstm_xproj(h, d), 1, 1), 0, D.V, h, s);
       P.count(1);
     }
     P.mark(CAVS_PH_FWD_LEVELS, s);
@@ -789,14 +877,14 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
       wait_x(tt);
       if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_FWD, Fs, lp[tt], lp[tt + 1], h, s);
       else if (rows_tiles(t->rs, false, M) >= t->rows_min_tiles && rows_level(D, t->rs, false, lp[tt], lp[tt + 1], s)) {}
-      else level_N<EPI_LSTM_FWD, 3>(gs, N, t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
+      else level_N<EPI_LSTM_FWD, 3, OpT>(gs, N, t->A[0], t->A[0], t->B_hk, D, pl(t, F, 0, 0), lp[tt], lp[tt + 1], h, s);
       P.count(1);
       unfused(EPI_LSTM_FWD, tt);
     }
   } else {
     if (!streamed) {
       if (!gemm_xproj(D, t->gs, s))
-        launch_level<EPI_FC_XPROJ, 1, 1>(t->A[1], t->A[1], t->B_xp, D, mono_one(d, 1, &zero, &zero), 0, D.V, h, s);
+        launch_level<EPI_FC_XPROJ, 1, 1, OpT>(t->A[1], t->A[1], t->B_xp, D, pl(t, mono_one(d, 1, &zero, &zero), 1, 1), 0, D.V, h, s);
       P.count(1);
     }
     P.mark(CAVS_PH_FWD_LEVELS, s);
@@ -810,8 +898,8 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
       wait_x(tt);
       if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_FWD, Fs, lp[tt], lp[tt + 1], h, s);
       else if (rows_tiles(t->rs, false, M) >= t->rows_min_tiles && rows_level(D, t->rs, false, lp[tt], lp[tt + 1], s)) {}
-      else if (gs) launch_level<EPI_FC_FWD, 1, kCluster>(t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
-      else launch_level<EPI_FC_FWD, 1, 1>(t->A[0], t->A[0], t->B_hk, D, F, lp[tt], lp[tt + 1], h, s);
+      else if (gs) launch_level<EPI_FC_FWD, 1, kCluster, OpT>(t->A[0], t->A[0], t->B_hk, D, pl(t, F, 0, 0), lp[tt], lp[tt + 1], h, s);
+      else launch_level<EPI_FC_FWD, 1, 1, OpT>(t->A[0], t->A[0], t->B_hk, D, pl(t, F, 0, 0), lp[tt], lp[tt + 1], h, s);
       P.count(1);
       unfused(EPI_FC_FWD, tt);
     }
@@ -838,8 +926,9 @@ static int launch_II(const CUtensorMap& a, const CUtensorMap& b, const Dev& D, P
   return P.split;
 }
 
-void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, int* split, Prof& P,
-                 cudaEvent_t wgrad_ev) {
+template <class OpT>
+static void bwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, int* split, Prof& P,
+                  cudaEvent_t wgrad_ev) {
   const int skmax = skinny_max(D);
   split[0] = split[1] = split[2] = 1;
   if (t->use_simt) { simt_backward<__nv_bfloat16>(D, lp, s, P); return; }
@@ -849,7 +938,8 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
   const bool gs = !t->mono;
   const SegListI Bs = bwd_segments(D);
   // rows past V of dZ are read by the lazy GEMMs' last k-block: keep them zero
-  cudaMemsetAsync(reinterpret_cast<__nv_bfloat16*>(D.dZ) + (size_t)D.V * G * h, 0, (size_t)64 * G * h * 2, s);
+  for (int q = 0; q < (D.split ? 3 : 1); ++q)
+    cudaMemsetAsync(reinterpret_cast<__nv_bfloat16*>(D.dZ) + q * D.ps_dz + (size_t)D.V * G * h, 0, (size_t)64 * G * h * 2, s);
   if (D.dag) {
     // DAG batch (NEXT-3): per task, the pull-reduce + dF of its vertices (every parent is in a
     // later task, already done), then the level GEMM whose epilogue only sends the edge gradients
@@ -867,11 +957,11 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
       const int M = lp[tt + 1] - lp[tt];
       if (lstm) {
         if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_BWD_DAG, Bs, lp[tt], lp[tt + 1], h, s);
-        else level_N<EPI_LSTM_BWD_DAG, 1>(gs, N, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
+        else level_N<EPI_LSTM_BWD_DAG, 1, OpT>(gs, N, t->A[2], t->A[3], t->B_dz, D, pl(t, B, 2, 3), lp[tt], lp[tt + 1], h, s);
       } else {
         if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_BWD_DAG, Bs, lp[tt], lp[tt + 1], h, s);
-        else if (gs) launch_level<EPI_FC_BWD_DAG, 2, kCluster>(t->A[2], t->A[2], t->B_dz, D, Bfc, lp[tt], lp[tt + 1], h, s);
-        else launch_level<EPI_FC_BWD_DAG, 2, 1>(t->A[2], t->A[2], t->B_dz, D, Bfc, lp[tt], lp[tt + 1], h, s);
+        else if (gs) launch_level<EPI_FC_BWD_DAG, 2, kCluster, OpT>(t->A[2], t->A[2], t->B_dz, D, pl(t, Bfc, 2, 2), lp[tt], lp[tt + 1], h, s);
+        else launch_level<EPI_FC_BWD_DAG, 2, 1, OpT>(t->A[2], t->A[2], t->B_dz, D, pl(t, Bfc, 2, 2), lp[tt], lp[tt + 1], h, s);
       }
       P.count(1);
       if (D.unfused) { launch_unfused(D, lstm ? EPI_LSTM_BWD_DAG : EPI_FC_BWD_DAG, lp[tt], lp[tt + 1], s); P.count(1); }
@@ -884,7 +974,7 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
       const int M = lp[tt + 1] - lp[tt];
       if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_BWD, Bs, lp[tt], lp[tt + 1], h, s);
       else if (rows_tiles(t->rs, true, M) >= t->rows_min_tiles && rows_level(D, t->rs, true, lp[tt], lp[tt + 1], s)) {}
-      else level_N<EPI_LSTM_BWD, 1>(gs, N, t->A[2], t->A[3], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
+      else level_N<EPI_LSTM_BWD, 1, OpT>(gs, N, t->A[2], t->A[3], t->B_dz, D, pl(t, B, 2, 3), lp[tt], lp[tt + 1], h, s);
       P.count(1);
       if (D.unfused) { launch_unfused(D, EPI_LSTM_BWD, lp[tt], lp[tt + 1], s); P.count(1); }
     }
@@ -897,8 +987,8 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
       const int M = lp[tt + 1] - lp[tt];
       if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_BWD, Bs, lp[tt], lp[tt + 1], h, s);
       else if (rows_tiles(t->rs, true, M) >= t->rows_min_tiles && rows_level(D, t->rs, true, lp[tt], lp[tt + 1], s)) {}
-      else if (gs) launch_level<EPI_FC_BWD, 2, kCluster>(t->A[2], t->A[2], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
-      else launch_level<EPI_FC_BWD, 2, 1>(t->A[2], t->A[2], t->B_dz, D, B, lp[tt], lp[tt + 1], h, s);
+      else if (gs) launch_level<EPI_FC_BWD, 2, kCluster, OpT>(t->A[2], t->A[2], t->B_dz, D, pl(t, B, 2, 2), lp[tt], lp[tt + 1], h, s);
+      else launch_level<EPI_FC_BWD, 2, 1, OpT>(t->A[2], t->A[2], t->B_dz, D, pl(t, B, 2, 2), lp[tt], lp[tt + 1], h, s);
       P.count(1);
       if (D.unfused) { launch_unfused(D, EPI_FC_BWD, lp[tt], lp[tt + 1], s); P.count(1); }
     }
@@ -930,23 +1020,23 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
         PlanII Bf = A;
         for (int k = 0; k < N; ++k) Bf.s[k] = SegT2{(3 + k) * h, k * h, lo, tt >= 1 ? hi : lo, 0};
         Bf.M = h; Bf.Ncols = h; Bf.ldo = h; Bf.split_stride = Z.suf;
-        if (tt >= 1) { launch_II(mdz, t->M_hk, D, A, u4, s); launch_II(mdz, t->M_hk, D, Bf, uf, s); P.count(2); }
+        if (tt >= 1) { launch_II(mdz, t->M_hk, D, pl2(t, A), u4, s); launch_II(mdz, t->M_hk, D, pl2(t, Bf), uf, s); P.count(2); }
         PlanII Cw{};                                    // dW over this task's pull records
         Cw.nseg = 1; Cw.split = 1; Cw.accum = acc;
         Cw.s[0] = SegT2{0, 0, lo, hi, 1};
         Cw.M = G * h; Cw.Ncols = d; Cw.ldo = d; Cw.split_stride = Z.sw;
-        launch_II(mdz, t->M_xp, D, Cw, w, s); P.count(1);
+        launch_II(mdz, t->M_xp, D, pl2(t, Cw), w, s); P.count(1);
       } else {
         PlanII A{};
         A.nseg = 1; A.split = 1; A.accum = tt > 1 ? 1 : 0;
         A.s[0] = SegT2{0, 0, lo, hi, 0};
         A.M = h; A.Ncols = 2 * h; A.ldo = 2 * h; A.split_stride = Z.su4;
-        if (tt >= 1) { launch_II(mdz, t->M_hk, D, A, u4, s); P.count(1); }
+        if (tt >= 1) { launch_II(mdz, t->M_hk, D, pl2(t, A), u4, s); P.count(1); }
         PlanII Cw{};
         Cw.nseg = 1; Cw.split = 1; Cw.accum = acc;
         Cw.s[0] = SegT2{0, 0, lo, hi, 1};
         Cw.M = h; Cw.Ncols = d; Cw.ldo = d; Cw.split_stride = Z.sw;
-        launch_II(mdz, t->M_xp, D, Cw, w, s); P.count(1);
+        launch_II(mdz, t->M_xp, D, pl2(t, Cw), w, s); P.count(1);
       }
     }
     if (Tn <= 1) {                                      // no internal vertex: dU = 0
@@ -963,40 +1053,51 @@ void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s,
     A.nseg = N;
     for (int k = 0; k < N; ++k) A.s[k] = SegT2{0, k * h, lp1, V, 0};
     A.M = 3 * h; A.Ncols = h; A.ldo = h; A.split_stride = Z.su4;
-    if (lp1 < V) { split[0] = launch_II(t->M_dz, t->M_hk, D, A, u4, s); P.count(1); }
+    if (lp1 < V) { split[0] = launch_II(t->M_dz, t->M_hk, D, pl2(t, A), u4, s); P.count(1); }
     else cudaMemsetAsync(u4, 0, sizeof(float) * Z.su4, s);
     PlanII Bf{};                                        // dU_f = sum_k dZ_fk^T H_k
     Bf.nseg = N;
     for (int k = 0; k < N; ++k) Bf.s[k] = SegT2{(3 + k) * h, k * h, lp1, V, 0};
     Bf.M = h; Bf.Ncols = h; Bf.ldo = h; Bf.split_stride = Z.suf;
-    if (lp1 < V) { split[1] = launch_II(t->M_dz, t->M_hk, D, Bf, uf, s); P.count(1); }
+    if (lp1 < V) { split[1] = launch_II(t->M_dz, t->M_hk, D, pl2(t, Bf), uf, s); P.count(1); }
     else cudaMemsetAsync(uf, 0, sizeof(float) * Z.suf, s);
     PlanII Cw{};                                        // dW = dZ^T X over the pull records
     Cw.nseg = 1;
     Cw.s[0] = SegT2{0, 0, 0, V, 1};
     Cw.M = G * h; Cw.Ncols = d; Cw.ldo = d; Cw.split_stride = Z.sw;
-    split[2] = launch_II(t->M_dz, t->M_xp, D, Cw, w, s); P.count(1);
+    split[2] = launch_II(t->M_dz, t->M_xp, D, pl2(t, Cw), w, s); P.count(1);
   } else {
     PlanII A{};
     A.nseg = 1;
     A.s[0] = SegT2{0, 0, lp1, V, 0};
     A.M = h; A.Ncols = 2 * h; A.ldo = 2 * h; A.split_stride = Z.su4;
-    if (lp1 < V) { split[0] = launch_II(t->M_dz, t->M_hk, D, A, u4, s); P.count(1); }
+    if (lp1 < V) { split[0] = launch_II(t->M_dz, t->M_hk, D, pl2(t, A), u4, s); P.count(1); }
     else cudaMemsetAsync(u4, 0, sizeof(float) * Z.su4, s);
     PlanII Cw{};
     Cw.nseg = 1;
     Cw.s[0] = SegT2{0, 0, 0, V, 1};
     Cw.M = h; Cw.Ncols = d; Cw.ldo = d; Cw.split_stride = Z.sw;
-    split[2] = launch_II(t->M_dz, t->M_xp, D, Cw, w, s); P.count(1);
+    split[2] = launch_II(t->M_dz, t->M_xp, D, pl2(t, Cw), w, s); P.count(1);
   }
   P.mark(CAVS_PH_DX, s);
   if (D.dx) {                                         // pull's adjoint: dX = dZ W
     if (!gemm_dx(D, t->gs, s)) {
-      if (lstm) launch_level<EPI_DX, 1, 1>(t->A[4], t->A[4], t->B_dz, D, mono_lstm_dx(h, N), 0, V, d, s);
-      else launch_level<EPI_DX, 1, 1>(t->A[4], t->A[4], t->B_dz, D, mono_one(h, 1, &zero, &zero), 0, V, d, s);
+      if (lstm) launch_level<EPI_DX, 1, 1, OpT>(t->A[4], t->A[4], t->B_dz, D, pl(t, mono_lstm_dx(h, N), 4, 4), 0, V, d, s);
+      else launch_level<EPI_DX, 1, 1, OpT>(t->A[4], t->A[4], t->B_dz, D, pl(t, mono_one(h, 1, &zero, &zero), 4, 4), 0, V, d, s);
     }
     P.count(1);
   }
+}
+
+void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, Prof& P, XStream* xs) {
+  if (D.split) fwd_t<S3>(D, t, lp, s, P, xs);
+  else fwd_t<__nv_bfloat16>(D, t, lp, s, P, xs);
+}
+
+void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, int* split, Prof& P,
+                 cudaEvent_t wgrad_ev) {
+  if (D.split) bwd_t<S3>(D, t, lp, s, split, P, wgrad_ev);
+  else bwd_t<__nv_bfloat16>(D, t, lp, s, split, P, wgrad_ev);
 }
 
 }  // namespace cavs

@@ -178,6 +178,45 @@ def test_fp32_parity(case):
     compare(b, g, r, FP32_TOL, case)
 
 
+# FP32 mode on the tensor cores (h, d multiples of 64): bf16x3 split operands, six tcgen05 MMAs per
+# product; the 1e-5 bar of the fp32 mode is unchanged
+FP32_TC_CASES = {
+    "lstm_sst_h64": lambda: gen.make_batch("tree_lstm", 2, 64, 64, "sst_tree", 24, seed=81),
+    "lstm_chain_h128": lambda: gen.make_batch("tree_lstm", 1, 128, 64, "sst_chain", 12, seed=82),
+    "lstm_N3_h64": lambda: gen.batch_from_graphs(
+        [[[], [], [], [0, 1, 2], [3], [], [4, 5]] for _ in range(5)] + [[[]]],
+        cell="tree_lstm", N=3, h=64, d=64, seed=83, x_at="all", loss_at="all"),
+    "fc_cbt_h128": lambda: gen.make_batch("tree_fc", 2, 128, 64, "cbt32", 5, seed=84),
+    "lstm_sst_h256_d128": lambda: gen.make_batch("tree_lstm", 2, 256, 128, "sst_tree", 16, seed=85),
+}
+
+
+@pytest.mark.parametrize("case", list(FP32_TC_CASES))
+def test_fp32_tensor_core_parity(case):
+    """FP32 mode on tcgen05 against the fp64 oracle at the fp32 bar (1e-5), bit-reproducible."""
+    b = FP32_TC_CASES[case]()
+    g = run_gpu(b, "fp32")
+    assert "bf16x3" in g["ctx"].path_info(), g["ctx"].path_info()
+    compare(b, g, run_oracle(b), FP32_TOL, f"fp32 tcgen05 {case}")
+    g2 = run_gpu(b, "fp32", ctx=g["ctx"])
+    for k in ("h_out", "dparams", "dx"):
+        assert np.array_equal(g[k], g2[k]), f"{case}: {k} not deterministic"
+
+
+def test_fp32_ffma_path_on_request(monkeypatch):
+    """CAVS_FP32_FFMA=1 keeps the FFMA kernels; both fp32 engines agree with the oracle and with
+    each other at the fp32 bar."""
+    b = FP32_TC_CASES["lstm_sst_h64"]()
+    monkeypatch.setenv("CAVS_FP32_FFMA", "1")
+    f = run_gpu(b, "fp32")
+    assert "FFMA" in f["ctx"].path_info(), f["ctx"].path_info()
+    monkeypatch.delenv("CAVS_FP32_FFMA")
+    t = run_gpu(b, "fp32")
+    assert "bf16x3" in t["ctx"].path_info()
+    compare(b, f, run_oracle(b), FP32_TOL, "fp32 FFMA vs fp64")
+    compare(b, t, f, FP32_TOL, "fp32 tcgen05 vs FFMA")
+
+
 def test_host_and_device_inputs_agree():
     b = gen.make_config_batch("cfg1", seed=1)
     g1 = run_gpu(b, "fp32", on_device=True)
@@ -557,6 +596,24 @@ def test_rows_level_kernels(case, monkeypatch):
     o = run_gpu(b, "bf16")
     assert "row-tiled" not in o["ctx"].path_info()
     compare(b, g, o, BF16_EMU_TOL, case + " row-tiled vs per-task")
+
+
+@pytest.mark.parametrize("case", ["fc_h256_cbt", "lstm_n2_h256_sst", "lstm_n1_h128_chain"])
+def test_rows_split_k(case, monkeypatch):
+    """Split-K of the row-tiled kernel (tasks whose tiles leave SMs idle: K shares, fp32 partials summed
+    in share order by the last share to arrive): against the oracle, bit-reproducible, and against the
+    unsplit kernel (CAVS_ROWS_KSPLIT=0: same bf16 operands, another fp32 summation order)."""
+    b = ROWS_CASES[case]()
+    monkeypatch.setenv("CAVS_PERSIST", "0")
+    monkeypatch.setenv("CAVS_ROWS_MIN_TILES", "1")
+    g = run_gpu(b, "bf16")
+    compare(b, g, run_oracle(b), BF16_TOL, case + " split-K vs fp64 oracle")
+    g2 = run_gpu(b, "bf16", ctx=g["ctx"])
+    for k in ("h_out", "dparams", "dx"):
+        assert np.array_equal(g[k], g2[k]), f"{case}: split-K {k} not deterministic"
+    monkeypatch.setenv("CAVS_ROWS_KSPLIT", "0")
+    o = run_gpu(b, "bf16")
+    compare(b, g, o, BF16_EMU_TOL, case + " split-K vs unsplit")
 
 
 # ------------------------------------------------------------------ inference-only forward

@@ -35,7 +35,12 @@ def test_csr_wellformed_and_x_policy():
     assert b.child_ptr[-1] == b.child_idx.size == b.V - b.K
     deg = np.diff(b.child_ptr)
     assert np.array_equal(b.x_row >= 0, deg == 0)          # x at leaves
-    assert np.all(b.gamma[np.diff(b.child_ptr) > 0].any(axis=1) | True)
+    is_child = np.zeros(b.V, bool)                          # the loss is at the roots (Z9)
+    for g in range(b.K):
+        lo, hi = b.graph_ptr[g], b.graph_ptr[g + 1]
+        for v in range(lo, hi):
+            is_child[lo + b.child_idx[b.child_ptr[v]:b.child_ptr[v + 1]]] = True
+    assert b.gamma[~is_child].any(axis=1).all() and not b.gamma[is_child].any()
     c = gen.make_config_batch("cfg3", seed=0, K=8, h=8)
     assert np.all(c.x_row >= 0)                               # chains: x everywhere
     lens = gen.sst_lengths(10000, np.random.default_rng(1))
