@@ -40,7 +40,8 @@ constexpr int A_TILE = 128 * BK * 2;       // 16 KB
 constexpr int B_TILE = NT * BK * 2;        // 8 KB
 constexpr int kThreads = 320;              // 10 warps
 constexpr int kSmemBudget = 196 * 1024;    // pipeline stages (+ static metadata <= 227 KB)
-constexpr int kCluster = 4;
+constexpr int kCluster = 4;                // gate-split cluster: one rank per gate group
+constexpr int kClMax = 16;                 // K-sliced gate split: kCluster x ksl ranks (ksl in {1, 2, 4})
 
 struct Bundle {
   int map_a;                 // which A tensor map (0/1)
@@ -56,7 +57,7 @@ struct RankPlan { int nb; Bundle b[3]; int nacc; int stages; int stage_bytes; in
 // npair = 6 in the FP32 split mode (bf16x3 operands): every bundle's k-loop runs
 // once per plane pair (s, t) with s + t <= 2, A plane s at A row + s a_prow[map], B plane t at task
 // row + t b_prow (plane-major arenas); npair = 1: plain bf16.
-struct PlanT { RankPlan r[kCluster]; int comb[8][kCluster]; int bar_off; int npair; int a_prow[2]; int b_prow; };
+struct PlanT { RankPlan r[kClMax]; int comb[8][kClMax]; int bar_off; int npair; int a_prow[2]; int b_prow; };
 __device__ __constant__ const int kPairS[6] = {0, 0, 1, 0, 1, 2};
 __device__ __constant__ const int kPairT[6] = {0, 1, 0, 2, 1, 0};
 
@@ -239,7 +240,7 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
     const int j = m0 + uq * 4;
     const UnitC<4> uc = (epi_uses_bias<E>() && j < units) ? load_unit<4>(D, j, epi_is_lstm<E>()) : UnitC<4>{};
     const uint32_t xs_base = ptx::smem_u32(xs) + (uint32_t)(uq * 4) * 4u;
-    constexpr int CPT = COLS / 8;                      // columns per thread
+    constexpr int CPT = (COLS + 7) / 8;                // columns per thread (CL = 16: 4 columns, half the threads)
     constexpr int CH = epi_needs_children<E>() ? 1 : (CPT < 4 ? CPT : 4);
     // children per vertex the epilogue state is sized for
     constexpr int NM = E == EPI_LSTM_FWD ? NACC - 3 : (E == EPI_LSTM_BWD || E == EPI_LSTM_BWD_DAG) ? NACC - 1 : 1;
@@ -253,7 +254,7 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
         const int r = cg + 8 * (i0 + i);               // own column index
         const int c = c_own + r;                       // column in the task tile
         const int p = p0 + c;
-        ok[i] = j < units && p < row_hi && row_active<E>(D, p, s_meta[r].xrow);
+        ok[i] = r < COLS && j < units && p < row_hi && row_active<E>(D, p, s_meta[r].xrow);
         if (!ok[i]) continue;
 #pragma unroll
         for (int e = 0; e < NACC; ++e) {
@@ -468,6 +469,8 @@ struct TcState {
   int split = 0;
   int prow[5] = {0, 0, 0, 0, 0};
   int vp = 0;
+  int num_sms = 148;
+  int ksl_force = 0;            // CAVS_TC_KSL=1|2|4: K slices per gate rank of the per-task kernels (0: by size)
   std::string info;
 };
 
@@ -518,6 +521,12 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
   t->use_simt = env && env[0] == '1';
   const char* mono = std::getenv("CAVS_TC_MONO");
   t->mono = mono && mono[0] == '1';
+  if (const char* k = std::getenv("CAVS_TC_KSL")) t->ksl_force = std::atoi(k);
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   if (!g_encode) {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
@@ -622,7 +631,7 @@ static PlanT plan_empty() {
   PlanT P{};
   P.npair = 1;
   for (int e = 0; e < 8; ++e)
-    for (int r = 0; r < kCluster; ++r) P.comb[e][r] = -1;
+    for (int r = 0; r < kClMax; ++r) P.comb[e][r] = -1;
   return P;
 }
 
@@ -677,6 +686,32 @@ static void gs_add_ksplit(PlanT& P, int map_a, int a_row, int a_col, int b_col, 
     R.b[R.nb++] = b;
     P.comb[e][r] = R.nacc++;
   }
+}
+
+// K-sliced gate split (small tasks: spread F's weight stream over more SMs): rank g of a kCluster
+// gate-split plan becomes ranks g ksl + q, q < ksl, each running k-blocks [q nk / ksl, (q + 1) nk / ksl)
+// of every bundle of g into its own accumulators; the epilogue sums the slices like the gate ranks
+// (comb).  nullopt-like: returns false if some bundle has fewer than ksl k-blocks.
+static bool kslice(const PlanT& G, int ksl, PlanT* out) {
+  PlanT P = G;
+  for (int g = 0; g < kCluster; ++g)
+    for (int q = 0; q < ksl; ++q) {
+      RankPlan R = G.r[g];
+      for (int bi = 0; bi < R.nb; ++bi) {
+        Bundle& b = R.b[bi];
+        if (b.nk < ksl) return false;
+        const int k0 = (b.nk * q) / ksl, k1 = (b.nk * (q + 1)) / ksl;
+        b.a_col0 += k0 * BK;
+        for (int i = 0; i < b.nB; ++i) b.b_col[i] += k0 * BK;
+        b.nk = k1 - k0;
+      }
+      P.r[g * ksl + q] = R;
+    }
+  for (int e = 0; e < 8; ++e)
+    for (int g = 0; g < kCluster; ++g)
+      for (int q = 0; q < ksl; ++q) P.comb[e][g * ksl + q] = G.comb[e][g];
+  *out = P;
+  return true;
 }
 
 // ---- Tree-LSTM, forward task: gate g over every child slot (U h~ = sum_k U h_k) ----
@@ -789,6 +824,7 @@ static void launch_level(const CUtensorMap& a0, const CUtensorMap& a1, const CUt
   const int dv = cur_device();
   if (smem > attr_set[dv]) {
     cudaFuncSetAttribute(k_tc_level<E, NACC, CL, OpT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (CL > 8) cudaFuncSetAttribute(k_tc_level<E, NACC, CL, OpT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr_set[dv] = smem;
   }
   cudaLaunchConfig_t cfg{};
@@ -810,20 +846,47 @@ static void launch_level(const CUtensorMap& a0, const CUtensorMap& a1, const CUt
   cudaLaunchKernelEx(&cfg, k_tc_level<E, NACC, CL, OpT>, a0, a1, b, D, P, row_lo, row_hi, units);
 }
 
-// per-task dispatch on the arity N (NACC = BASE + N)
+// per-task dispatch on the arity N (NACC = BASE + N) and the cluster size cl (1: monolithic, 4: gate
+// split, 8 / 16: K-sliced gate split, N <= 2)
+template <int E, int NACC, class OpT>
+static void level_cl(int cl, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const Dev& D,
+                     const PlanT& P, int lo, int hi, int units, cudaStream_t s) {
+  if (cl == 1) launch_level<E, NACC, 1, OpT>(a0, a1, b, D, P, lo, hi, units, s);
+  else if (cl == kCluster) launch_level<E, NACC, kCluster, OpT>(a0, a1, b, D, P, lo, hi, units, s);
+  else if constexpr (NACC <= 5) {
+    if (cl == 8) launch_level<E, NACC, 8, OpT>(a0, a1, b, D, P, lo, hi, units, s);
+    else launch_level<E, NACC, 16, OpT>(a0, a1, b, D, P, lo, hi, units, s);
+  }
+}
 template <int E, int BASE, class OpT>
-static void level_N(bool gs, int N, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const Dev& D,
+static void level_N(int cl, int N, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const Dev& D,
                     const PlanT& P, int lo, int hi, int units, cudaStream_t s) {
   switch (N) {
-    case 1: gs ? launch_level<E, BASE + 1, kCluster, OpT>(a0, a1, b, D, P, lo, hi, units, s)
-               : launch_level<E, BASE + 1, 1, OpT>(a0, a1, b, D, P, lo, hi, units, s); break;
-    case 2: gs ? launch_level<E, BASE + 2, kCluster, OpT>(a0, a1, b, D, P, lo, hi, units, s)
-               : launch_level<E, BASE + 2, 1, OpT>(a0, a1, b, D, P, lo, hi, units, s); break;
-    case 3: gs ? launch_level<E, BASE + 3, kCluster, OpT>(a0, a1, b, D, P, lo, hi, units, s)
-               : launch_level<E, BASE + 3, 1, OpT>(a0, a1, b, D, P, lo, hi, units, s); break;
-    default: gs ? launch_level<E, BASE + 4, kCluster, OpT>(a0, a1, b, D, P, lo, hi, units, s)
-                : launch_level<E, BASE + 4, 1, OpT>(a0, a1, b, D, P, lo, hi, units, s); break;
+    case 1: level_cl<E, BASE + 1, OpT>(cl, a0, a1, b, D, P, lo, hi, units, s); break;
+    case 2: level_cl<E, BASE + 2, OpT>(cl, a0, a1, b, D, P, lo, hi, units, s); break;
+    case 3: level_cl<E, BASE + 3, OpT>(cl, a0, a1, b, D, P, lo, hi, units, s); break;
+    default: level_cl<E, BASE + 4, OpT>(cl, a0, a1, b, D, P, lo, hi, units, s); break;
   }
+}
+
+// K slices per gate rank for a task of M rows (cluster = kCluster x ksl CTAs per 128-unit block): the
+// weight stream of a small task spread over more SMs while every cluster stays resident
+static int pick_ksl(const TcState* t, int M, int units) {
+  if (t->ksl_force > 0) return t->ksl_force;
+  const int nclu = cdiv(units, 128) * cdiv(M, NT);   // clusters of the task
+  if (nclu * kCluster * 4 <= t->num_sms && nclu <= 7) return 4;
+  if (nclu * kCluster * 2 <= t->num_sms) return 2;
+  return 1;
+}
+
+// the task's plan and cluster size: gate split (K-sliced for small tasks, arity <= 2) or monolithic
+static PlanT gsplan(const TcState* t, const Dev& D, bool gs, const PlanT& G, int M, int units, int* cl) {
+  if (!gs) { *cl = 1; return G; }
+  int ksl = D.N <= 2 ? pick_ksl(t, M, units) : 1;
+  PlanT K;
+  while (ksl > 1 && !kslice(G, ksl, &K)) ksl /= 2;
+  *cl = kCluster * ksl;
+  return ksl > 1 ? K : G;
 }
 
 // Streaming ablation: level-0 rows of the x-projection (they finish the leaves) on the main
@@ -877,7 +940,11 @@ static void fwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
       wait_x(tt);
       if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_FWD, Fs, lp[tt], lp[tt + 1], h, s);
       else if (rows_tiles(t->rs, false, M) >= t->rows_min_tiles && rows_level(D, t->rs, false, lp[tt], lp[tt + 1], s)) {}
-      else level_N<EPI_LSTM_FWD, 3, OpT>(gs, N, t->A[0], t->A[0], t->B_hk, D, pl(t, F, 0, 0), lp[tt], lp[tt + 1], h, s);
+      else {
+        int cl;
+        const PlanT Fk = gsplan(t, D, gs, F, M, h, &cl);
+        level_N<EPI_LSTM_FWD, 3, OpT>(cl, N, t->A[0], t->A[0], t->B_hk, D, pl(t, Fk, 0, 0), lp[tt], lp[tt + 1], h, s);
+      }
       P.count(1);
       unfused(EPI_LSTM_FWD, tt);
     }
@@ -898,7 +965,11 @@ static void fwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
       wait_x(tt);
       if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_FWD, Fs, lp[tt], lp[tt + 1], h, s);
       else if (rows_tiles(t->rs, false, M) >= t->rows_min_tiles && rows_level(D, t->rs, false, lp[tt], lp[tt + 1], s)) {}
-      else if (gs) launch_level<EPI_FC_FWD, 1, kCluster, OpT>(t->A[0], t->A[0], t->B_hk, D, pl(t, F, 0, 0), lp[tt], lp[tt + 1], h, s);
+      else if (gs) {
+        int cl;
+        const PlanT Fk = gsplan(t, D, gs, F, M, h, &cl);
+        level_cl<EPI_FC_FWD, 1, OpT>(cl, t->A[0], t->A[0], t->B_hk, D, pl(t, Fk, 0, 0), lp[tt], lp[tt + 1], h, s);
+      }
       else launch_level<EPI_FC_FWD, 1, 1, OpT>(t->A[0], t->A[0], t->B_hk, D, pl(t, F, 0, 0), lp[tt], lp[tt + 1], h, s);
       P.count(1);
       unfused(EPI_FC_FWD, tt);
@@ -957,10 +1028,18 @@ static void bwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
       const int M = lp[tt + 1] - lp[tt];
       if (lstm) {
         if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_BWD_DAG, Bs, lp[tt], lp[tt + 1], h, s);
-        else level_N<EPI_LSTM_BWD_DAG, 1, OpT>(gs, N, t->A[2], t->A[3], t->B_dz, D, pl(t, B, 2, 3), lp[tt], lp[tt + 1], h, s);
+        else {
+          int cl;
+          const PlanT Bk = gsplan(t, D, gs, B, M, h, &cl);
+          level_N<EPI_LSTM_BWD_DAG, 1, OpT>(cl, N, t->A[2], t->A[3], t->B_dz, D, pl(t, Bk, 2, 3), lp[tt], lp[tt + 1], h, s);
+        }
       } else {
         if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_BWD_DAG, Bs, lp[tt], lp[tt + 1], h, s);
-        else if (gs) launch_level<EPI_FC_BWD_DAG, 2, kCluster, OpT>(t->A[2], t->A[2], t->B_dz, D, pl(t, Bfc, 2, 2), lp[tt], lp[tt + 1], h, s);
+        else if (gs) {
+          int cl;
+          const PlanT Bk = gsplan(t, D, gs, Bfc, M, h, &cl);
+          level_cl<EPI_FC_BWD_DAG, 2, OpT>(cl, t->A[2], t->A[2], t->B_dz, D, pl(t, Bk, 2, 2), lp[tt], lp[tt + 1], h, s);
+        }
         else launch_level<EPI_FC_BWD_DAG, 2, 1, OpT>(t->A[2], t->A[2], t->B_dz, D, pl(t, Bfc, 2, 2), lp[tt], lp[tt + 1], h, s);
       }
       P.count(1);
@@ -974,7 +1053,11 @@ static void bwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
       const int M = lp[tt + 1] - lp[tt];
       if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_LSTM_BWD, Bs, lp[tt], lp[tt + 1], h, s);
       else if (rows_tiles(t->rs, true, M) >= t->rows_min_tiles && rows_level(D, t->rs, true, lp[tt], lp[tt + 1], s)) {}
-      else level_N<EPI_LSTM_BWD, 1, OpT>(gs, N, t->A[2], t->A[3], t->B_dz, D, pl(t, B, 2, 3), lp[tt], lp[tt + 1], h, s);
+      else {
+        int cl;
+        const PlanT Bk = gsplan(t, D, gs, B, M, h, &cl);
+        level_N<EPI_LSTM_BWD, 1, OpT>(cl, N, t->A[2], t->A[3], t->B_dz, D, pl(t, Bk, 2, 3), lp[tt], lp[tt + 1], h, s);
+      }
       P.count(1);
       if (D.unfused) { launch_unfused(D, EPI_LSTM_BWD, lp[tt], lp[tt + 1], s); P.count(1); }
     }
@@ -987,7 +1070,11 @@ static void bwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
       const int M = lp[tt + 1] - lp[tt];
       if (M <= skmax) skinny_typeI<__nv_bfloat16>(D, EPI_FC_BWD, Bs, lp[tt], lp[tt + 1], h, s);
       else if (rows_tiles(t->rs, true, M) >= t->rows_min_tiles && rows_level(D, t->rs, true, lp[tt], lp[tt + 1], s)) {}
-      else if (gs) launch_level<EPI_FC_BWD, 2, kCluster, OpT>(t->A[2], t->A[2], t->B_dz, D, pl(t, B, 2, 2), lp[tt], lp[tt + 1], h, s);
+      else if (gs) {
+        int cl;
+        const PlanT Bk = gsplan(t, D, gs, B, M, h, &cl);
+        level_cl<EPI_FC_BWD, 2, OpT>(cl, t->A[2], t->A[2], t->B_dz, D, pl(t, Bk, 2, 2), lp[tt], lp[tt + 1], h, s);
+      }
       else launch_level<EPI_FC_BWD, 2, 1, OpT>(t->A[2], t->A[2], t->B_dz, D, pl(t, B, 2, 2), lp[tt], lp[tt + 1], h, s);
       P.count(1);
       if (D.unfused) { launch_unfused(D, EPI_FC_BWD, lp[tt], lp[tt + 1], s); P.count(1); }

@@ -616,6 +616,36 @@ def test_rows_split_k(case, monkeypatch):
     compare(b, g, o, BF16_EMU_TOL, case + " split-K vs unsplit")
 
 
+KSL_CASES = {
+    "lstm_n2_h128_sst": lambda: gen.make_batch("tree_lstm", 2, 128, 64, "sst_tree", 10, seed=91),
+    "lstm_n1_h256_chain": lambda: gen.batch_from_graphs([gen.chain(n) for n in (9, 30, 2, 17)], cell="tree_lstm", N=1,
+                                                        h=256, d=128, seed=92, x_at="all", loss_at="all"),
+    "fc_h256_cbt": lambda: gen.make_batch("tree_fc", 2, 256, 128, "cbt16", 6, seed=93),
+}
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+@pytest.mark.parametrize("ksl", ["2", "4"])
+@pytest.mark.parametrize("case", list(KSL_CASES))
+def test_ksliced_gate_split(case, ksl, precision, monkeypatch):
+    """Per-task kernels with K-sliced gate-split clusters (4 x ksl CTAs per 128-unit block, the slices'
+    accumulators summed through DSMEM like the gate ranks) against the oracle, bit-reproducible, and
+    against the plain gate split (same operands, another fp32 summation order)."""
+    b = KSL_CASES[case]()
+    monkeypatch.setenv("CAVS_PERSIST", "0")
+    monkeypatch.setenv("CAVS_ROWS", "0")
+    monkeypatch.setenv("CAVS_TC_KSL", ksl)
+    g = run_gpu(b, precision)
+    tol = FP32_TOL if precision == "fp32" else BF16_TOL
+    compare(b, g, run_oracle(b), tol, f"ksl {ksl} {case} {precision} vs fp64")
+    g2 = run_gpu(b, precision, ctx=g["ctx"])
+    for k in ("h_out", "dparams", "dx"):
+        assert np.array_equal(g[k], g2[k]), f"{case}: {k} not deterministic"
+    monkeypatch.setenv("CAVS_TC_KSL", "1")
+    o = run_gpu(b, precision)
+    compare(b, g, o, FP32_TOL if precision == "fp32" else BF16_EMU_TOL, f"ksl {ksl} vs 1 {case} {precision}")
+
+
 # ------------------------------------------------------------------ inference-only forward
 @pytest.mark.parametrize("case", ["lstm_n2_h512_sst", "fc_h256_cbt"])
 @pytest.mark.parametrize("precision", ["bf16", "fp32"])
