@@ -39,6 +39,11 @@ struct cavs_ctx {
   cudaEvent_t ev_hdr = nullptr; // recorded after the schedule header's device->host copy
   cudaEvent_t ev_wgrad = nullptr;   // caller's event: recorded once dparams' weight blocks are final
   XStream xs;                   // streaming ablation: side stream + per-task events
+  // db (k_colsum) beside the lazy GEMMs and dX: side stream forked after the level tasks, joined at the
+  // end of the backward (CAVS_DB_SIDE=0: on the main stream)
+  cudaStream_t db_s = nullptr;
+  cudaEvent_t ev_lv = nullptr, ev_db = nullptr;
+  bool db_side = true;
   // pipelined host-buffer steps (cavs_train_step_host_async): two staging slots, H2D / D2H streams
   struct Slot {
     int *gp = nullptr, *cp = nullptr, *ci = nullptr, *xrow = nullptr, *grow = nullptr;
@@ -177,6 +182,8 @@ CAVS_API cavs_status cavs_create(const cavs_desc* desc, int device, void* stream
     const char* lz = std::getenv("CAVS_LAZY_BATCH");
     const char* uf = std::getenv("CAVS_UNFUSED");
     const char* sx = std::getenv("CAVS_STREAMING");
+    const char* dbs = std::getenv("CAVS_DB_SIDE");
+    c->db_side = !(dbs && dbs[0] == '0');
     c->D.lazy_off = lz && lz[0] == '0';
     c->D.unfused = uf && uf[0] == '1';
     c->D.stream_x = sx && sx[0] == '1';
@@ -454,7 +461,12 @@ CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dp
   P.mark(CAVS_PH_BWD_LEVELS, ctx->stream);
   int split[3] = {1, 1, 1};
   if (ctx->tc) {
-    tc_backward(D, ctx->tc, ctx->lp, ctx->stream, split, P, ctx->ev_wgrad);
+    if (ctx->db_side && !ctx->db_s) {
+      CK(cudaStreamCreateWithFlags(&ctx->db_s, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ctx->ev_lv, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_db, cudaEventDisableTiming));
+    }
+    tc_backward(D, ctx->tc, ctx->lp, ctx->stream, split, P, ctx->ev_wgrad, ctx->db_side ? ctx->ev_lv : nullptr);
   } else {
     simt_backward<float>(D, ctx->lp, ctx->stream, P);
   }
@@ -464,7 +476,14 @@ CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dp
     P.count(1);
     if (ctx->ev_wgrad) CK(cudaEventRecord(ctx->ev_wgrad, ctx->stream));
   }
-  launch_colsum(D, ctx->lazy_db, ctx->stream);  // db -> dparams
+  if (ctx->tc && ctx->db_side) {                 // db -> dparams, beside the lazy GEMMs / dX (same dZ, disjoint outputs)
+    CK(cudaStreamWaitEvent(ctx->db_s, ctx->ev_lv, 0));
+    launch_colsum(D, ctx->lazy_db, ctx->db_s);
+    CK(cudaEventRecord(ctx->ev_db, ctx->db_s));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_db, 0));
+  } else {
+    launch_colsum(D, ctx->lazy_db, ctx->stream);
+  }
   P.count(1);
   P.mark(-1, ctx->stream);
   if (ctx->T >= 0) account_backward(ctx);
@@ -678,6 +697,12 @@ CAVS_API void cavs_destroy(cavs_ctx* ctx) {
     for (cudaEvent_t e : ctx->xs.ev) cudaEventDestroy(e);
   }
   if (ctx->ev_hdr) cudaEventDestroy(ctx->ev_hdr);
+  if (ctx->db_s) {
+    cudaStreamSynchronize(ctx->db_s);
+    cudaStreamDestroy(ctx->db_s);
+    cudaEventDestroy(ctx->ev_lv);
+    cudaEventDestroy(ctx->ev_db);
+  }
   if (ctx->h2d) {
     cudaStreamSynchronize(ctx->d2h);
     cudaStreamDestroy(ctx->h2d);

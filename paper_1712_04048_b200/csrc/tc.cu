@@ -999,7 +999,7 @@ static int launch_II(const CUtensorMap& a, const CUtensorMap& b, const Dev& D, P
 
 template <class OpT>
 static void bwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, int* split, Prof& P,
-                  cudaEvent_t wgrad_ev) {
+                  cudaEvent_t wgrad_ev, cudaEvent_t levels_ev) {
   const int skmax = skinny_max(D);
   split[0] = split[1] = split[2] = 1;
   if (t->use_simt) { simt_backward<__nv_bfloat16>(D, lp, s, P); return; }
@@ -1080,6 +1080,7 @@ static void bwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
       if (D.unfused) { launch_unfused(D, EPI_FC_BWD, lp[tt], lp[tt + 1], s); P.count(1); }
     }
   }
+  if (levels_ev) cudaEventRecord(levels_ev, s);      // every dZ row final: db may run beside the lazy GEMMs
   P.mark(CAVS_PH_LAZY, s);
   // ---- lazy batching of the parameter gradients ----
   const LazyLayout Z = lazy_layout(D);
@@ -1182,9 +1183,9 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
 }
 
 void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, int* split, Prof& P,
-                 cudaEvent_t wgrad_ev) {
-  if (D.split) bwd_t<S3>(D, t, lp, s, split, P, wgrad_ev);
-  else bwd_t<__nv_bfloat16>(D, t, lp, s, split, P, wgrad_ev);
+                 cudaEvent_t wgrad_ev, cudaEvent_t levels_ev) {
+  if (D.split) bwd_t<S3>(D, t, lp, s, split, P, wgrad_ev, levels_ev);
+  else bwd_t<__nv_bfloat16>(D, t, lp, s, split, P, wgrad_ev, levels_ev);
 }
 
 }  // namespace cavs
