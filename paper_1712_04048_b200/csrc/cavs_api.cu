@@ -405,11 +405,28 @@ static cavs_status forward_impl(cavs_ctx* ctx, const float* params, int32_t n_x,
   Dev& D = ctx->D;
   D.params = params; D.x = x; D.x_row = x_row; D.h_out = h_out; D.n_x = n_x;
   D.infer = infer ? 1 : 0;                 // (a DAG batch gathers c from the leaves' saved state: see below)
-  D.xgen = ++ctx->pull_gen;                // k_pull stamps every record it pulls (duplicates -> ST_XDUP)
+  D.xgen = ++ctx->pull_gen;                // k_pull stamps every record it pulls (duplicates -> hdr[5])
   Prof& P = ctx->prof;
   P.mark(CAVS_PH_PREP, ctx->stream);
-  launch_prep(D, ctx->stream);
+  // the parameter repack (weights only) runs on a side stream beside the pull; the forward's tensor-core
+  // kernels wait for both (fork / join: a parallel branch in a CUDA-graph capture)
+  const bool side = ctx->db_side;
+  if (side && !ctx->db_s) {
+    CK(cudaStreamCreateWithFlags(&ctx->db_s, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_lv, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_db, cudaEventDisableTiming));
+  }
+  if (side) {
+    CK(cudaEventRecord(ctx->ev_lv, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->db_s, ctx->ev_lv, 0));
+    launch_prep(D, ctx->db_s);
+    CK(cudaEventRecord(ctx->ev_db, ctx->db_s));
+  } else {
+    launch_prep(D, ctx->stream);
+  }
+  CK(cudaMemsetAsync(D.hdr + 4, 0, 2 * sizeof(int), ctx->stream));   // k_pull's statistics of this forward
   launch_pull(D, ctx->stream);
+  if (side) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_db, 0));
   P.count(2);
   {  // a deferred schedule header is consumed here, while prep / pull run on the device
     const cavs_status st = finish_schedule(ctx);
@@ -451,7 +468,7 @@ CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dp
   Prof& P = ctx->prof;
   // dx rows receive plain stores when every record is pulled exactly once (the usual case); the
   // zeroing + atomic adds only run when some record is pulled by several vertices or by none
-  // (k_pull's ST_XDUP bit / pull count; decided on the device by k_dx_zero and the DX epilogue)
+  // (k_pull.s duplicate flag / pull count; decided on the device by k_dx_zero and the DX epilogue)
   if (dx && D.n_x > 0) { launch_dx_zero(D, ctx->stream); P.count(1); }
   P.mark(CAVS_PH_BWD_ROOTS, ctx->stream);
   if (!D.dag) {                                // DAG batches: every vertex's dF runs in launch_dag_df

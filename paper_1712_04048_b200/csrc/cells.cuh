@@ -493,7 +493,7 @@ template <> struct EpiK<EPI_DX> {
                                                const In<VW, NM>&, const UnitC<VW>&) {
     if (m.xrow < 0) return;
     float* dst = D.dx + (size_t)m.xrow * D.d + j;
-    if (D.hdr[3] & ST_XDUP) addv<VW>(dst, acc[0]);   // a record pulled by several vertices: add
+    if (D.hdr[5]) addv<VW>(dst, acc[0]);             // a record pulled by several vertices: add
     else stv<VW>(dst, acc[0]);                       // each record pulled at most once: one store
   }
 };

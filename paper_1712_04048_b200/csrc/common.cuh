@@ -15,7 +15,7 @@
 
 namespace cavs {
 
-enum : int { ST_INVALID = 1, ST_ARITY = 2, ST_CYCLE = 4, ST_FANOUT = 8, ST_XROW = 16, ST_DAG = 32, ST_XDUP = 64 };
+enum : int { ST_INVALID = 1, ST_ARITY = 2, ST_CYCLE = 4, ST_FANOUT = 8, ST_XROW = 16, ST_DAG = 32 };
 
 // Device view of one context: sizes + every arena pointer.  Passed by value.
 struct Dev {
@@ -32,8 +32,9 @@ struct Dev {
   // schedule (position-indexed)
   int* order; int* level_ptr; int* child_pos; int* parent_pos; int* slot; int* deg; int* xrow_pos;
   int* tile_x;                      // per 64-position tile: 1 if any vertex has a pull record
-  int* hdr;                         // [0] status bits, [1] T, [2] #roots, [3] ST_XROW (deferred input error) | ST_DAG |
-                                    // ST_XDUP (a record pulled twice), [4] vertices with a record, [5] -, [6..] level_ptr
+  int* hdr;                         // [0] status bits, [1] T, [2] #roots, [3] ST_XROW (deferred input error) | ST_DAG,
+                                    // [4] vertices with a record, [5] 1: a record pulled twice (both reset by the
+                                    // forward before k_pull), [6..] level_ptr
   int* xseen; unsigned xgen;        // per record: generation of the last forward that pulled it (duplicate pulls)
   int* roots;                       // positions of vertices without a parent
   int* cnt;                         // per-graph level histograms: cnt[graph_ptr[g] + t] (t < T_g)

@@ -33,10 +33,6 @@ __device__ __forceinline__ OpT* prep_dst(const Dev& D, int sel) {
 template <class OpT>
 __global__ void __launch_bounds__(256) k_prep(Dev D, PrepJobs J) {
   pdl_wait();
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {   // k_pull's statistics of this forward
-    D.hdr[4] = 0;
-    atomicAnd(D.hdr + 3, ~ST_XDUP);
-  }
   const PrepJob& jb = J.j[blockIdx.y];
   __shared__ float tile[32][33];
   if (jb.transpose) {
@@ -98,7 +94,7 @@ __global__ void k_pull(Dev D) {
         r = -1;
       }
       D.xrow_pos[p] = r;
-      if (r >= 0 && atomicExch(D.xseen + r, (int)D.xgen) == (int)D.xgen) atomicOr(D.hdr + 3, ST_XDUP);
+      if (r >= 0 && atomicExch(D.xseen + r, (int)D.xgen) == (int)D.xgen) D.hdr[5] = 1;   // a record pulled twice
     }
     s_r[threadIdx.x] = r;
     const unsigned has = __ballot_sync(0xffffffffu, r >= 0);   // warps 0-1: count this block's pulls
@@ -420,7 +416,7 @@ __global__ void k_scatter_rows(float* dst, const float* src, const int* rows, in
 // dx must be zeroed unless every record is pulled exactly once (then every row gets one store)
 __global__ void k_dx_zero(Dev D) {
   pdl_wait();
-  if (!(D.hdr[3] & ST_XDUP) && D.hdr[4] == D.n_x) return;
+  if (!D.hdr[5] && D.hdr[4] == D.n_x) return;
   const size_t n = (size_t)D.n_x * D.d;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) D.dx[i] = 0.f;
 }

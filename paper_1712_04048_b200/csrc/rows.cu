@@ -299,6 +299,10 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KS = SPLIT ? P.ks : 1;                      // split-K shares per tile
+  // debug trace (CAVS_TRACE=1): [0] start, [1] producer past the PDL wait, [2] first stage landed,
+  // [3] first accumulator complete, [4] split-K reduction done, [5] first epilogue done
+  __shared__ unsigned long long s_tr[6];
+  if (D.trace && threadIdx.x == 0) { s_tr[0] = gtime(); s_tr[1] = s_tr[2] = s_tr[3] = s_tr[4] = s_tr[5] = 0; }
   const int rank = CG == 2 ? (int)r_cluster_rank() : 0;
   const bool leader = rank == 0;
   const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;   // CTA pair (CG = 2) or CTA
@@ -329,6 +333,7 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
     if (lane == 0) { ptx::tma_prefetch(&mA); ptx::tma_prefetch(&mB0); ptx::tma_prefetch(&mB1); }
     ptx::griddep_wait();                                 // task rows come from the previous kernels
     if (lane == 0) ptx::griddep_launch();                // PDL: the next task's CTAs may start their prologue
+    if (D.trace && lane == 0) s_tr[1] = gtime();
     if (lane <= 4) {
       int step = 0;
       for (int w = unit; w < P.ntiles * KS; w += nunits) {
@@ -382,6 +387,7 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
             const int s = step % S;
             rwait(&full[s], (step / S) & 1);
             ptx::tc_fence_after();
+            if (D.trace && step == 0) s_tr[2] = gtime();
             const uint32_t a = ptx::smem_u32(smem + s * P.stage), b = a + kRA;
 #ifndef CAVS_ROWS_NOMMA
 #pragma unroll
@@ -422,7 +428,9 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
       ptx::tc_fence_after();
       const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * P.acc_cols);
       // split-K: the shares of the tile meet, share kq finishes the units [kq UG/ks, (kq+1) UG/ks)
+      if (D.trace && threadIdx.x == 64 && k == 0) s_tr[3] = gtime();
       if constexpr (SPLIT) r_split_reduce(D, P, tb, j, w % KS, r, hh);
+      if (D.trace && threadIdx.x == 64 && k == 0) s_tr[4] = gtime();
       const int sw = P.UG / KS;                        // units finished by this work item
       const int ub = (w % KS) * sw + hh * (sw / 2);    // this thread's first unit within the tile
       // VW units per item: 8 (one 32-byte sector per row and output stream: 256-bit accesses)
@@ -485,6 +493,7 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
         if (valid && acc[0][0].v[0] == 12345.f) D.h_out[0] = acc[QB - 1][NE - 1].v[3];   // A/B only: no epilogue stores
 #endif
       }
+      if (D.trace && threadIdx.x == 64 && k == 0) s_tr[5] = gtime();
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {                                   // this warp drained its TMEM lanes
@@ -496,6 +505,14 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
   ptx::tc_fence_before();
   if constexpr (CG == 2) r_cluster_sync();             // the peer's last MMA / arrivals are done
   else __syncthreads();
+  if (D.trace && threadIdx.x == 0) {
+    const unsigned long long at = 8 + 8 * atomicAdd(D.trace, 1ull);
+    if (at + 8 < (4u << 20) / 8) {
+      D.trace[at] = 7000 + E; D.trace[at + 1] = blockIdx.x | ((unsigned long long)P.lo << 20);
+      for (int i = 0; i < 5; ++i) D.trace[at + 2 + i] = s_tr[i + 1] ? s_tr[i + 1] - s_tr[0] : 0;
+      D.trace[at + 7] = s_tr[0] | 0;  // start (absolute)
+    }
+  }
   if (warp == 1) {
     ptx::tc_fence_after();
     if constexpr (CG == 1) ptx::tmem_dealloc<512>(tmem);

@@ -61,9 +61,12 @@ struct PlanT { RankPlan r[kClMax]; int comb[8][kClMax]; int bar_off; int npair; 
 __device__ __constant__ const int kPairS[6] = {0, 0, 1, 0, 1, 2};
 __device__ __constant__ const int kPairT[6] = {0, 1, 0, 2, 1, 0};
 
-// a_roff / b_roff: row (vertex) offset of the operand plane (FP32 split mode: plane q at q * Vp)
-struct SegT2 { int a_col; int b_col; int k_lo, k_hi; int skip_no_x; int a_roff = 0, b_roff = 0; int corr = 0; };
-struct PlanII { int nseg; SegT2 s[24]; int M, Ncols, ldo; int split; size_t split_stride; int stages; int accum; };
+struct SegT2 { int a_col; int b_col; int k_lo, k_hi; int skip_no_x; };
+// planes = 3 (split mode): a stage holds the three planes of the A and B tiles (plane q of an arena starts
+// q * vp rows after plane 0), the six plane-pair products are issued from it, corrections into a
+// second accumulator
+struct PlanII { int nseg; SegT2 s[4]; int M, Ncols, ldo; int split; size_t split_stride; int stages; int accum;
+                int planes; int vp; };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~(uintptr_t)1023);
@@ -95,6 +98,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
            const __grid_constant__ CUtensorMap mB, Dev D, PlanT P, int row_lo, int row_hi, int units) {
   constexpr int COLS = NT / CL;                        // task columns finished by this CTA
+  constexpr bool PM = is_s3<OpT>::value;               // split mode: plane-major stages (P.npair == 6)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const uint32_t rank = CL > 1 ? cluster_rank() : 0;
@@ -142,6 +146,35 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
       constexpr uint32_t idesc = ptx::idesc_bf16(128, NT, 0, 0);
       uint32_t written = 0;                            // accumulators already initialised
       int step = 0;
+      if constexpr (PM) {
+        // split mode: a stage holds the three planes of every A and B tile of the k-block, the six
+        // plane-pair products a_s b_t (s + t <= 2) are issued from it (each plane loaded once)
+        constexpr int PS[6] = {0, 0, 1, 0, 1, 2}, PT[6] = {0, 1, 0, 2, 1, 0};
+        for (int bi = 0; bi < R.nb; ++bi) {
+          const Bundle& b = R.b[bi];
+          for (int kb = 0; kb < b.nk; ++kb, ++step) {
+            const int s = step % S;
+            ptx::mbar_wait(&full[s], (step / S) & 1);
+            ptx::tc_fence_after();
+            const uint32_t st = ptx::smem_u32(smem + s * R.stage_bytes);
+            for (int m = 0; m < b.nmma; ++m) {
+#pragma unroll
+              for (int pr = 0; pr < 6; ++pr) {
+                const uint32_t a = st + (PS[pr] * b.nA + b.mma_a[m]) * A_TILE;
+                const uint32_t bb = st + R.offB + (PT[pr] * b.nB + b.mma_b[m]) * B_TILE;
+                const int acc = b.mma_acc[m] + (pr > 0 ? R.nacc : 0);
+                const uint32_t d = tmem + acc * NT;
+#pragma unroll
+                for (int kk = 0; kk < BK / 16; ++kk)
+                  ptx::mma_bf16(d, ptx::sdesc_sw128(a + kk * 32, 16, 1024), ptx::sdesc_sw128(bb + kk * 32, 16, 1024),
+                                idesc, ((written >> acc) & 1u) | (kk > 0 ? 1u : 0u));
+                written |= 1u << acc;
+              }
+            }
+            ptx::mma_commit(&empty[s]);
+          }
+        }
+      } else
       for (int bi = 0; bi < R.nb; ++bi)
       for (int pr = 0; pr < P.npair; ++pr) {
         const Bundle& b = R.b[bi];
@@ -180,6 +213,28 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
       const int w = warp - 2;
       bool waited = false;
       int step = 0;
+      if constexpr (PM) {
+        for (int bi = 0; bi < R.nb; ++bi) {
+          const Bundle& b = R.b[bi];
+          const CUtensorMap* ma = b.map_a ? &mA1 : &mA0;
+          for (int kb = 0; kb < b.nk; ++kb, ++step) {
+            if (step % S != w) continue;
+            const int s = step % S;
+            uint8_t* st = smem + s * R.stage_bytes;
+            if (step >= S) ptx::mbar_wait(&empty[s], ((step / S) & 1) ^ 1);
+            ptx::mbar_arrive_expect_tx(&full[s], 3 * (b.nA * A_TILE + b.nB * B_TILE));
+            for (int q = 0; q < 3; ++q)
+              for (int i = 0; i < b.nA; ++i)
+                ptx::tma_load_2d(st + (q * b.nA + i) * A_TILE, ma, b.a_col0 + kb * BK,
+                                 b.a_row[i] + m0 + q * P.a_prow[b.map_a], &full[s]);
+            if (!waited) { ptx::griddep_wait(); waited = true; }
+            for (int q = 0; q < 3; ++q)
+              for (int i = 0; i < b.nB; ++i)
+                ptx::tma_load_2d(st + R.offB + (q * b.nB + i) * B_TILE, &mB, b.b_col[i] + kb * BK,
+                                 p0 + q * P.b_prow, &full[s]);
+          }
+        }
+      } else
       for (int bi = 0; bi < R.nb; ++bi)
       for (int pr = 0; pr < P.npair; ++pr) {
         const Bundle& b = R.b[bi];
@@ -316,7 +371,8 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const int S = P.stages;
-  constexpr int STAGE = 2 * T2_TILE;
+  const int STAGE = 2 * T2_TILE * P.planes;            // A then B, each planes x (128 MN x 64 K)
+  const int offBp = T2_TILE * P.planes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE);
   uint64_t* empty = full + S;
   uint64_t* done = empty + S;
@@ -361,14 +417,18 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
           const uint32_t ph = (step / S) & 1;
           ptx::mbar_wait(&full[s], ph);
           ptx::tc_fence_after();
-          const uint32_t a = ptx::smem_u32(smem + s * STAGE);
-          const uint32_t b = a + T2_TILE;
-          const uint32_t ac = (uint32_t)sg.corr;
+          const uint32_t a0 = ptx::smem_u32(smem + s * STAGE);
+          const uint32_t b0 = a0 + offBp;
+          constexpr int PS[6] = {0, 0, 1, 0, 1, 2}, PT[6] = {0, 1, 0, 2, 1, 0};
+          for (int pr = 0; pr < (P.planes > 1 ? 6 : 1); ++pr) {
+            const uint32_t a = a0 + PS[pr] * T2_TILE, b = b0 + PT[pr] * T2_TILE;
+            const uint32_t ac = pr > 0 ? 1u : 0u;        // split mode: corrections in their own accumulator
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            ptx::mma_bf16(tmem + ac * 128, ptx::sdesc_sw128(a + kk * 2048, 8192, 1024),
-                          ptx::sdesc_sw128(b + kk * 2048, 8192, 1024), idesc, ((wrote >> ac) & 1u) | (kk > 0 ? 1u : 0u));
-          wrote |= 1u << ac;
+            for (int kk = 0; kk < 4; ++kk)
+              ptx::mma_bf16(tmem + ac * 128, ptx::sdesc_sw128(a + kk * 2048, 8192, 1024),
+                            ptx::sdesc_sw128(b + kk * 2048, 8192, 1024), idesc, ((wrote >> ac) & 1u) | (kk > 0 ? 1u : 0u));
+            wrote |= 1u << ac;
+          }
           ptx::mma_commit(&empty[s]);
           ++step;
         }
@@ -397,10 +457,15 @@ k_tc_typeII(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
             if (step >= S) ptx::mbar_wait(&empty[s], ph ^ 1);
             uint8_t* st = smem + s * STAGE;
             ptx::mbar_arrive_expect_tx(&full[s], STAGE);
-            ptx::tma_load_2d(st, &mA, sg.a_col + m0, r0 + sg.a_roff, &full[s]);
-            ptx::tma_load_2d(st + T2_TILE / 2, &mA, sg.a_col + m0 + 64, r0 + sg.a_roff, &full[s]);
-            ptx::tma_load_2d(st + T2_TILE, &mB, sg.b_col + n0, r0 + sg.b_roff, &full[s]);
-            ptx::tma_load_2d(st + T2_TILE + T2_TILE / 2, &mB, sg.b_col + n0 + 64, r0 + sg.b_roff, &full[s]);
+            for (int q = 0; q < P.planes; ++q) {
+              const int ra = r0 + q * P.vp;
+              uint8_t* sa = st + q * T2_TILE;
+              uint8_t* sb = st + offBp + q * T2_TILE;
+              ptx::tma_load_2d(sa, &mA, sg.a_col + m0, ra, &full[s]);
+              ptx::tma_load_2d(sa + T2_TILE / 2, &mA, sg.a_col + m0 + 64, ra, &full[s]);
+              ptx::tma_load_2d(sb, &mB, sg.b_col + n0, ra, &full[s]);
+              ptx::tma_load_2d(sb + T2_TILE / 2, &mB, sg.b_col + n0 + 64, ra, &full[s]);
+            }
           }
           ++step;
         }
@@ -486,19 +551,9 @@ static PlanT pl(const TcState* t, PlanT P, int ia0, int ia1) {
 // Type II in the split mode: every segment becomes the six plane-pair segments (rows of plane q of
 // an arena start q * Vp rows after plane 0: the MN-major maps span all three planes)
 static PlanII pl2(const TcState* t, PlanII P) {
-  if (!t->split) return P;
-  static const int ps[6] = {0, 0, 1, 0, 1, 2}, pt[6] = {0, 1, 0, 2, 1, 0};
-  PlanII Q = P;
-  Q.nseg = 0;
-  for (int i = 0; i < P.nseg; ++i)
-    for (int q = 0; q < 6; ++q) {
-      SegT2 sg = P.s[i];
-      sg.a_roff = ps[q] * t->vp;
-      sg.b_roff = pt[q] * t->vp;
-      sg.corr = q > 0 ? 1 : 0;
-      Q.s[Q.nseg++] = sg;
-    }
-  return Q;
+  P.planes = t->split ? 3 : 1;
+  P.vp = t->vp;
+  return P;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -655,8 +710,9 @@ static int plan_finalize(PlanT& P, int CL) {
     RankPlan& R = P.r[r];
     int maxA = 1, maxB = 1;
     for (int i = 0; i < R.nb; ++i) { maxA = std::max(maxA, R.b[i].nA); maxB = std::max(maxB, R.b[i].nB); }
-    R.offB = maxA * A_TILE;
-    R.stage_bytes = R.offB + maxB * B_TILE;
+    const int np = P.npair > 1 ? 3 : 1;                // split mode: three planes of every tile per stage
+    R.offB = np * maxA * A_TILE;
+    R.stage_bytes = R.offB + np * maxB * B_TILE;
     R.stages = std::max(1, std::min(6, kSmemBudget / R.stage_bytes));
     pipe = std::max(pipe, R.stages * R.stage_bytes);
     xs = std::max(xs, R.nacc * NT * 128 * 4);
@@ -757,6 +813,19 @@ static PlanT mono_lstm_xproj(int h, int d) {
   Bundle b = bundle(0, 4, rows, 0, 1, &zero, d / BK);
   for (int g = 0; g < 4; ++g) { add_mma(b, g, 0, g); P.comb[g][0] = g; }
   P.r[0].b[0] = b; P.r[0].nb = 1; P.r[0].nacc = 4;
+  return P;
+}
+// gate-split variant (split mode: the four gates' A tiles x three planes do not fit one stage)
+static PlanT gs_lstm_xproj(int h, int d) {
+  PlanT P = plan_empty();
+  const int zero = 0;
+  for (int g = 0; g < 4; ++g) {
+    const int row = g * h;
+    Bundle b = bundle(0, 1, &row, 0, 1, &zero, d / BK);
+    add_mma(b, 0, 0, 0);
+    P.r[g].b[0] = b; P.r[g].nb = 1; P.r[g].nacc = 1;
+    P.comb[g][g] = 0;
+  }
   return P;
 }
 // ---- Tree-LSTM backward task: slot 0 = U_iou^T dz_iou, slot 1+k = U_f^T dz_fk ----
@@ -927,7 +996,10 @@ static void fwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
   if (D.cell == CAVS_CELL_TREE_LSTM) {
     // eager pull projection fused with task 0 (large: monolithic CTAs reuse the x tile for 4 gates)
     if (!streamed) {
-      if (!gemm_xproj(D, t->gs, s))
+      if (D.split)
+        launch_level<EPI_LSTM_XPROJ, 4, kCluster, OpT>(t->A[1], t->A[1], t->B_xp, D, pl(t, gs_lstm_xproj(h, d), 1, 1),
+                                                        0, D.V, h, s);
+      else if (!gemm_xproj(D, t->gs, s))
         launch_level<EPI_LSTM_XPROJ, 4, 1, OpT>(t->A[1], t->A[1], t->B_xp, D, pl(t, mono_lstm_xproj(h, d), 1, 1), 0, D.V, h, s);
       P.count(1);
     }
@@ -984,8 +1056,9 @@ static int launch_II(const CUtensorMap& a, const CUtensorMap& b, const Dev& D, P
   const int tiles = cdiv(P.M, 128) * cdiv(P.Ncols, 128);
   P.split = P.split == 1 ? 1      // forced (per-task ablation launches accumulate in stream order)
             : std::max(1, std::min(std::min(kSplitMax, 148 / std::max(1, tiles)), std::max(1, nkb / 4)));
-  P.stages = 6;
-  const int smem = P.stages * 2 * T2_TILE + 1024 + 2 * 8 * P.stages + 64;
+  if (P.planes < 1) P.planes = 1;
+  P.stages = P.planes > 1 ? 2 : 6;
+  const int smem = P.stages * 2 * T2_TILE * P.planes + 1024 + 2 * 8 * P.stages + 64;
   static bool attr_done[kMaxDev] = {};
   const int dv = cur_device();
   if (!attr_done[dv]) {
@@ -1002,7 +1075,11 @@ static void bwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
                   cudaEvent_t wgrad_ev, cudaEvent_t levels_ev) {
   const int skmax = skinny_max(D);
   split[0] = split[1] = split[2] = 1;
-  if (t->use_simt) { simt_backward<__nv_bfloat16>(D, lp, s, P); return; }
+  if (t->use_simt) {
+    simt_backward<__nv_bfloat16>(D, lp, s, P);
+    if (levels_ev) cudaEventRecord(levels_ev, s);      // (db after the whole FFMA backward)
+    return;
+  }
   const int h = D.h, d = D.d, N = D.N, T = (int)lp.size() - 1;
   const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
   const int G = lstm ? 3 + N : 1;

@@ -9,7 +9,10 @@ Cases (path forced by the library's environment switches, set per case in a chil
   persist_fc   Tree-FC h=128 bf16 (persistent Tree-FC plans)
   rows         Tree-FC h=640 bf16 with CAVS_ROWS_MIN_TILES=1: row-tiled k_rows level GEMMs
   tc_level     Tree-LSTM h=128 bf16, CAVS_PERSIST=0: per-task swap-AB / skinny kernels
-  fp32         Tree-LSTM h=64 fp32: FFMA tiles
+  fp32         Tree-LSTM h=64 fp32 (CAVS_FP32_FFMA=1 in round 1; round 2: the tcgen05 bf16x3 path)
+  fp32_tc*     FP32 mode on tcgen05 (bf16x3 split operands), Tree-LSTM and Tree-FC
+  rows_splitk* split-K row-tiled kernels (shares meet at a per-tile counter)
+  ksl4         per-task kernels with 16-CTA K-sliced gate-split clusters
 """
 import os
 import subprocess
@@ -33,6 +36,15 @@ CASES = {
     "dag": (dict(cell="tree_lstm", N=2, h=128, d=128, shape="dag", K=5), "bf16", {}),
     "ablations": (dict(cell="tree_lstm", N=2, h=128, d=128, shape="sst_tree", K=5), "bf16",
                   {"CAVS_LAZY_BATCH": "0", "CAVS_UNFUSED": "1", "CAVS_STREAMING": "1"}),
+    # round 2, second half: FP32 on tcgen05 (bf16x3), split-K row kernel, K-sliced gate split
+    "fp32_tc": (dict(cell="tree_lstm", N=2, h=64, d=64, shape="sst_tree", K=4), "fp32", {}),
+    "fp32_tc_fc": (dict(cell="tree_fc", N=2, h=128, d=64, shape="cbt8", K=3), "fp32", {}),
+    "rows_splitk": (dict(cell="tree_fc", N=2, h=256, d=128, shape="cbt16", K=3), "bf16",
+                    {"CAVS_ROWS_MIN_TILES": "1", "CAVS_PERSIST": "0"}),
+    "rows_splitk_lstm": (dict(cell="tree_lstm", N=2, h=256, d=128, shape="sst_tree", K=6), "bf16",
+                         {"CAVS_ROWS_MIN_TILES": "1", "CAVS_PERSIST": "0", "CAVS_ROWS_SEL": "i"}),
+    "ksl4": (dict(cell="tree_lstm", N=2, h=128, d=64, shape="sst_tree", K=4), "bf16",
+             {"CAVS_PERSIST": "0", "CAVS_ROWS": "0", "CAVS_TC_KSL": "4"}),
 }
 
 
