@@ -57,6 +57,8 @@ struct RPlan {
   int nbuf;        // accumulator buffers (1 or 2)
   int lo, hi;      // task rows
   int nut, ntiles; // unit tiles, tiles (of 128 CG task rows)
+  int dsm;         // split-K through DSMEM: the ks shares of a tile form a cluster and exchange partials in
+                   // shared memory (when a partial fits the pipeline area), else through D.rows_part
   int ks;          // split-K: work item w = (tile w / ks, K share w % ks); ks > 1 only when the tiles do not
                    // fill the GPU (CG = 1): the shares' fp32 partials meet in D.rows_part (counters
                    // D.rows_cnt), each share sums one slice of the tile's units in share order and runs the
@@ -283,6 +285,71 @@ __device__ __forceinline__ void r_split_reduce(const Dev& D, const P_t& P, uint3
   }
 }
 
+// Split-K meeting point through distributed shared memory: the ks shares of tile j are one cluster
+// (rank = share).  Each share stages its fp32 partial in its own (drained) pipeline smem as
+// [column][128 lanes], the shares meet at a cluster-scope mbarrier (one release-arrive per peer), then
+// share kq sums its unit slice over the shares' smem in share order (ld.shared::cluster) into its TMEM.
+// The CTAs leave through a full cluster barrier at the end of the kernel (no peer reads a departed CTA).
+template <class P_t>
+__device__ __forceinline__ void r_split_dsmem(const P_t& P, uint8_t* smem, uint64_t* xbar, uint32_t tb, int kq, int r,
+                                              int hh) {
+  const int half = P.acc_cols / 2, c0 = hh * half;
+  float* sp = reinterpret_cast<float*>(smem);
+  for (int c = c0; c < c0 + half; c += 16) {
+    float v[16];
+    ptx::tmem_ld16(tb + (uint32_t)c, v);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sp[(size_t)(c + i) * 128 + r] = v[i];
+  }
+  ptx::named_bar_sync(1, 256);
+  if (threadIdx.x == 64) {
+    for (int q = 0; q < P.ks; ++q) {
+      uint32_t ra;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(ptx::smem_u32(xbar)), "r"(q));
+      asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+    }
+    const uint32_t a = ptx::smem_u32(xbar);
+    unsigned long long t0 = 0;
+    for (;;) {
+      uint32_t ok;
+      asm volatile(
+          "{\n\t.reg .pred P;\n\t"
+          "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
+          "selp.b32 %0, 1, 0, P;\n\t}"
+          : "=r"(ok) : "r"(a), "r"(0) : "memory");
+      if (ok) break;
+      const unsigned long long now = gtime();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 4000000000ull) __trap();
+    }
+  }
+  ptx::named_bar_sync(1, 256);
+  const int sw = P.UG / P.ks, s0 = kq * sw;            // this share's units [s0, s0 + sw)
+  const int nblk = P.acc_cols / P.UG, nch = nblk * (sw / 16);
+  const uint32_t base = ptx::smem_u32(sp) + (uint32_t)r * 4u;
+  for (int ch = hh; ch < nch; ch += 2) {
+    const int c = (ch / (sw / 16)) * P.UG + s0 + (ch % (sw / 16)) * 16;
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = 0.f;
+    for (int qq = 0; qq < P.ks; ++qq) {                 // share order: deterministic
+      uint32_t ra;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(base + (uint32_t)c * 512u), "r"(qq));
+      float x[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x[i]) : "r"(ra + (uint32_t)i * 512u) : "memory");
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] += x[i];
+    }
+    tst16(tb + (uint32_t)c, v);
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  ptx::tc_fence_before();
+  ptx::named_bar_sync(1, 256);
+  ptx::tc_fence_after();
+}
+
 // SPLIT: the split-K instantiation (P.ks > 1); the plain one keeps ks = 1 at compile time
 template <int E, int NM, int QB, int CG, bool SPLIT>
 __global__ void __launch_bounds__(kRThreads, 1)
@@ -296,7 +363,8 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
   uint64_t* empty = full + kRSMax;
   uint64_t* accf = empty + kRSMax;
   uint64_t* acce = accf + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+  uint64_t* xbar = acce + 2;                            // split-K DSMEM exchange (cluster scope)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KS = SPLIT ? P.ks : 1;                      // split-K shares per tile
   // debug trace (CAVS_TRACE=1): [0] start, [1] producer past the PDL wait, [2] first stage landed,
@@ -310,6 +378,7 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { ptx::mbar_init(&accf[b], 1); ptx::mbar_init(&acce[b], 8 * CG); }
+    if (SPLIT) ptx::mbar_init(xbar, P.ks);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -322,6 +391,7 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
   }
   ptx::tc_fence_before();
   if constexpr (CG == 2) r_cluster_sync();             // barriers + TMEM of both CTAs ready
+  else if (SPLIT && P.dsm) r_cluster_sync();           // the shares' exchange barriers ready
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
@@ -429,7 +499,10 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
       const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * P.acc_cols);
       // split-K: the shares of the tile meet, share kq finishes the units [kq UG/ks, (kq+1) UG/ks)
       if (D.trace && threadIdx.x == 64 && k == 0) s_tr[3] = gtime();
-      if constexpr (SPLIT) r_split_reduce(D, P, tb, j, w % KS, r, hh);
+      if constexpr (SPLIT) {
+        if (P.dsm) r_split_dsmem(P, smem, xbar, tb, w % KS, r, hh);
+        else r_split_reduce(D, P, tb, j, w % KS, r, hh);
+      }
       if (D.trace && threadIdx.x == 64 && k == 0) s_tr[4] = gtime();
       const int sw = P.UG / KS;                        // units finished by this work item
       const int ub = (w % KS) * sw + hh * (sw / 2);    // this thread's first unit within the tile
@@ -504,6 +577,7 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
   }
   ptx::tc_fence_before();
   if constexpr (CG == 2) r_cluster_sync();             // the peer's last MMA / arrivals are done
+  else if (SPLIT && P.dsm) r_cluster_sync();           // no share leaves while a peer reads its smem
   else __syncthreads();
   if (D.trace && threadIdx.x == 0) {
     const unsigned long long at = 8 + 8 * atomicAdd(D.trace, 1ull);
@@ -531,6 +605,8 @@ struct RowsState {
   int cg = 1;                          // CTAs per MMA: 2 = CTA pairs (cta_group::2, opt-in), 1 = single CTA
   bool can_split = false;              // split-K partial slots carved (D.rows_part) and not disabled
   bool lstm = false;
+  bool dsm = false;                    // split-K partials through DSMEM (CAVS_ROWS_DSM=1; measured no faster
+                                       // than the global slots at cfg5, profiles/r02_fp32tc.md)
   bool sel_items = false;              // rows_tiles counts work items (tiles x shares) instead of tiles
 };
 
@@ -568,7 +644,7 @@ static RSeg rseg(int a_col, int bmap, int nbox, int box_rows, const int* rows0, 
   return S;
 }
 
-static int r_smem(const RPlan& P) { return 1024 + P.S * P.stage + (2 * kRSMax + 4) * 8 + 16; }
+static int r_smem(const RPlan& P) { return 1024 + P.S * P.stage + (2 * kRSMax + 5) * 8 + 16; }
 
 template <int E, int NM, int QB, int CG>
 static bool r_attr(const RPlan& P) {
@@ -591,7 +667,7 @@ static void r_finish(RPlan& P, int h, int CG) {
       }
     }
   P.stage = kRA + P.n / CG * 128;
-  P.S = std::min(kRSMax, (232448 - 2048 - (2 * kRSMax + 4) * 8 - 16) / P.stage);
+  P.S = std::min(kRSMax, (232448 - 2048 - (2 * kRSMax + 5) * 8 - 16) / P.stage);
   P.nbuf = 2 * P.acc_cols <= 512 ? 2 : 1;
   P.nut = h / P.UG;
 }
@@ -621,6 +697,8 @@ RowsState* rows_init(const Dev& D, int max_vertices) {
   const char* ke = std::getenv("CAVS_ROWS_KSPLIT");
   rs->can_split = D.rows_part && D.rows_cnt && !(ke && ke[0] == '0');
   rs->lstm = D.cell == CAVS_CELL_TREE_LSTM;
+  const char* de = std::getenv("CAVS_ROWS_DSM");
+  rs->dsm = de && de[0] == '1';
   const char* se = std::getenv("CAVS_ROWS_SEL");
   rs->sel_items = se ? se[0] == 'i' : !rs->lstm;
   const int CG = rs->cg;
@@ -696,8 +774,9 @@ static void r_launch(const CUtensorMap& a, const CUtensorMap& b0, const CUtensor
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
-  at[1].id = cudaLaunchAttributeClusterDimension;          // CTA pair on one TPC (CG = 2)
-  at[1].val.clusterDim.x = CG; at[1].val.clusterDim.y = 1; at[1].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;          // CTA pair on one TPC (CG = 2); split-K shares (DSMEM)
+  at[1].val.clusterDim.x = (CG == 1 && P.ks > 1 && P.dsm) ? P.ks : CG;
+  at[1].val.clusterDim.y = 1; at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
   if constexpr (CG == 1) {
@@ -712,6 +791,8 @@ static void rows_go(const Dev& D, RowsState* rs, bool backward, RPlan& P, cudaSt
   // split-K when the tiles leave SMs idle: ks shares per tile (every segment keeps >= 2 k-blocks
   // per share), at most kRowsMaxItems work items (partial slots)
   P.ks = r_ks(rs, P, P.ntiles);
+  // the DSMEM exchange needs the partial ([acc_cols][128] fp32) to fit the drained pipeline area
+  P.dsm = P.ks > 1 && rs->dsm && (size_t)P.acc_cols * 128 * 4 <= (size_t)P.S * P.stage;
   const int grid = std::min(P.ntiles * P.ks * CG, rs->num_sms / CG * CG);
   const bool lstm = D.cell == CAVS_CELL_TREE_LSTM;
   if (lstm) {

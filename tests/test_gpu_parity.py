@@ -613,6 +613,11 @@ def test_rows_split_k(case, monkeypatch):
     g2 = run_gpu(b, "bf16", ctx=g["ctx"])
     for k in ("h_out", "dparams", "dx"):
         assert np.array_equal(g[k], g2[k]), f"{case}: split-K {k} not deterministic"
+    monkeypatch.setenv("CAVS_ROWS_DSM", "1")               # partials exchanged through DSMEM (opt-in)
+    q = run_gpu(b, "bf16")
+    for k in ("h_out", "dparams", "dx"):                   # same partials, same share order
+        assert np.array_equal(g[k], q[k]), f"{case}: DSMEM vs global split-K {k} differ"
+    monkeypatch.delenv("CAVS_ROWS_DSM")
     monkeypatch.setenv("CAVS_ROWS_KSPLIT", "0")
     o = run_gpu(b, "bf16")
     compare(b, g, o, BF16_EMU_TOL, case + " split-K vs unsplit")

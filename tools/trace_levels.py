@@ -10,7 +10,7 @@ dev = torch.device("cuda", 0)
 t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
 ctx = Context(b.cell, b.N, b.h, b.d, precision="bf16", max_graphs=b.K, max_vertices=b.V, max_x=b.n_x)
 ws = ctx.workspace[ctx._ws_off + ctx._ws_bytes - (4 << 20): ctx._ws_off + ctx._ws_bytes]
-for it in range(20):
+for it in range(int(os.environ.get('TRACE_ITERS', '20'))):
     torch.cuda.synchronize()
     ws.zero_()
     ctx.load_graphs(t(b.graph_ptr), t(b.child_ptr), t(b.child_idx)); ctx.schedule()
@@ -19,6 +19,7 @@ for it in range(20):
 tail = ws.view(torch.int64).cpu().numpy()
 n = tail[0]
 rec = tail[8:8 + 8 * n].reshape(n, 8)
+rec = rec[rec[:, 0] < 2000]          # k_tc_level records (kind 100 CL + E); k_rows writes 7000 + E
 t0 = rec[:, 3].min()
 print("records", n)
 # per launch (kind, row_lo): CTAs, first start, last end, max per-CTA phase times
