@@ -482,8 +482,14 @@ template <> struct EpiK<EPI_FC_BWD_DAG> {
 // the same record (an embedding row); dx is zeroed by cavs_backward first.  With one vertex per
 // record every element receives exactly one add onto 0 (deterministic).
 template <int VW> __device__ __forceinline__ void addv(float* p, const FV<VW>& a) {
-  if constexpr (VW == 4) atomicAdd(reinterpret_cast<float4*>(p), make_float4(a.v[0], a.v[1], a.v[2], a.v[3]));
-  else atomicAdd(p, a.v[0]);
+  if constexpr (VW == 8) {
+    atomicAdd(reinterpret_cast<float4*>(p), make_float4(a.v[0], a.v[1], a.v[2], a.v[3]));
+    atomicAdd(reinterpret_cast<float4*>(p + 4), make_float4(a.v[4], a.v[5], a.v[6], a.v[7]));
+  } else if constexpr (VW == 4) {
+    atomicAdd(reinterpret_cast<float4*>(p), make_float4(a.v[0], a.v[1], a.v[2], a.v[3]));
+  } else {
+    atomicAdd(p, a.v[0]);
+  }
 }
 template <> struct EpiK<EPI_DX> {
   template <int VW, int NM = kMaxN> struct In {};

@@ -102,6 +102,12 @@ __device__ __forceinline__ void tld_wait() { asm volatile("tcgen05.wait::ld.sync
 
 template <int E> struct RAcc { static constexpr int NE = 1; };
 template <> struct RAcc<EPI_FC_BWD> { static constexpr int NE = 2; };
+template <> struct RAcc<EPI_LSTM_XPROJ> { static constexpr int NE = 4; };
+// accumulator layout kind of an epilogue: the eager x-projection (r02) is laid out like one child slot of
+// the Tree-LSTM forward (i, o, u, f blocks of UG units) or like the Tree-FC forward (one block); dX too
+template <int E> __host__ __device__ constexpr int r_fetch_kind() {
+  return E == EPI_LSTM_XPROJ ? EPI_LSTM_FWD : (E == EPI_FC_XPROJ || E == EPI_DX) ? EPI_FC_FWD : E;
+}
 
 // accumulators of the VW units at unit offset u (within the tile) -> acc[NE]; VW in {4, 8}
 template <int VW>
@@ -350,12 +356,28 @@ __device__ __forceinline__ void r_split_dsmem(const P_t& P, uint8_t* smem, uint6
   ptx::tc_fence_after();
 }
 
+// x-projection / dX: does row tile [p0, p0 + 128) hold a row that needs the epilogue (a level-0 vertex
+// for the x-projection, a pull record for both; k_pull's per-64-row flags)
+template <int E>
+__device__ __forceinline__ bool r_tile_active(const Dev& D, int p0) {
+  if constexpr (E == EPI_LSTM_XPROJ || E == EPI_FC_XPROJ || E == EPI_DX) {
+    if (E != EPI_DX && p0 < dev_lp1(D)) return true;
+    return D.tile_x[p0 >> 6] || D.tile_x[(p0 >> 6) + 1];
+  } else {
+    return true;
+  }
+}
+
 // SPLIT: the split-K instantiation (P.ks > 1); the plain one keeps ks = 1 at compile time
 template <int E, int NM, int QB, int CG, bool SPLIT>
 __global__ void __launch_bounds__(kRThreads, 1)
 k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB0,
        const __grid_constant__ CUtensorMap mB1, Dev D, const __grid_constant__ RPlan P) {
   constexpr int NE = E == EPI_LSTM_FWD ? 3 + NM : E == EPI_LSTM_BWD ? 1 + NM : RAcc<E>::NE;
+  constexpr int FE = r_fetch_kind<E>();                 // accumulator layout
+  constexpr int FNM = E == EPI_LSTM_XPROJ ? 1 : NM;      // (x-projection: one "child slot" of 4 gates)
+  // x-projection / dX (r02): row tiles without any row needing the epilogue are skipped by every role
+  constexpr bool XD = E == EPI_LSTM_XPROJ || E == EPI_FC_XPROJ || E == EPI_DX;
   extern __shared__ __align__(16) uint8_t r_raw[];
   uint8_t* smem = r_raw + ((1024u - (ptx::smem_u32(r_raw) & 1023u)) & 1023u);
   const int S = P.S;
@@ -409,6 +431,7 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
       for (int w = unit; w < P.ntiles * KS; w += nunits) {
         const int j = w / KS, kq = w % KS;
         const int p0 = P.lo + (j / P.nut) * 128 * CG + 128 * rank, u0 = (j % P.nut) * P.UG;
+        if (XD && !r_tile_active<E>(D, p0)) continue;
         for (int sg = 0; sg < P.nseg; ++sg) {
           const RSeg& Sg = P.seg[sg];
           const CUtensorMap* mb = Sg.bmap ? &mB1 : &mB0;
@@ -442,8 +465,10 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
     if (lane == 0 && leader) {
       const uint32_t idesc = ptx::idesc_bf16(128 * CG, P.n, 0, 0);
       int step = 0;
-      for (int w = unit, k = 0; w < P.ntiles * KS; w += nunits, ++k) {
+      if (XD) ptx::griddep_wait();                       // k_pull's tile flags
+      for (int w = unit, k = 0; w < P.ntiles * KS; w += nunits) {
         const int kq = w % KS;
+        if (XD && !r_tile_active<E>(D, P.lo + (w / KS / P.nut) * 128 * CG + 128 * rank)) continue;
         const int buf = P.nbuf == 2 ? (k & 1) : 0;
         const int use = P.nbuf == 2 ? (k >> 1) : k;       // earlier uses of this buffer
         if (use > 0) rwait(&acce[buf], (use - 1) & 1);
@@ -471,6 +496,7 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
           }
         }
         r_commit<CG>(&accf[buf]);
+        ++k;
       }
     }
     __syncwarp();
@@ -485,13 +511,16 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
         asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(acce_remote[b]) : "r"(ptx::smem_u32(&acce[b])));
     }
     ptx::griddep_wait();
-    for (int w = unit, k = 0; w < P.ntiles * KS; w += nunits, ++k) {
+    for (int w = unit, k = -1; w < P.ntiles * KS; w += nunits) {
       const int j = w / KS;
       const int p0 = P.lo + (j / P.nut) * 128 * CG + 128 * rank, u0 = (j % P.nut) * P.UG;
+      if (XD && !r_tile_active<E>(D, p0)) continue;
+      ++k;
       const int p = p0 + r;
-      const bool valid = p < P.hi;
+      bool valid = p < P.hi;
       VMeta m;
       if (valid) load_meta(D, p, epi_needs_children<E>(), m);
+      if (XD && valid) valid = row_active<E>(D, p, m.xrow);
       const int buf = P.nbuf == 2 ? (k & 1) : 0;
       const int use = P.nbuf == 2 ? (k >> 1) : k;
       rwait(&accf[buf], use & 1);
@@ -517,7 +546,7 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
         for (int it = 0; it < ipt; ++it) {
           const int uo = ub + it * VW, jj = u0 + uo;
           FV<VW> acc[NE];
-          fetch_acc<E, NM, VW>(tb, P.UG, uo, acc);
+          fetch_acc<FE, FNM, VW>(tb, P.UG, uo, acc);
 #ifndef CAVS_ROWS_NOEPI
           if (valid) {
             const FV<VW> dcbp = ldv<VW>(D.dcb + (size_t)m.p * h + jj);
@@ -555,7 +584,7 @@ k_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorM
         }
         FV<VW> acc[QB][NE];
 #pragma unroll
-        for (int b = 0; b < QB; ++b) fetch_acc<E, NM, VW>(tb, P.UG, ub + (qb + b) * VW, acc[b]);
+        for (int b = 0; b < QB; ++b) fetch_acc<FE, FNM, VW>(tb, P.UG, ub + (qb + b) * VW, acc[b]);
 #ifndef CAVS_ROWS_NOEPI
         if (valid) {
 #pragma unroll
@@ -601,6 +630,11 @@ struct RowsState {
   CUtensorMap A_hk, A_dz;
   CUtensorMap B_fwd, B_bwd0, B_bwd1;
   RPlan fwd{}, bwd{};
+  // r02: the eager x-projection and pull's adjoint dX on the same kernel (persistent over row tiles,
+  // double-buffered accumulators, 256-bit epilogue), rows without an epilogue skipped per 128-row tile
+  CUtensorMap A_xp, B_x, B_dx;
+  RPlan xp{}, dx{};
+  bool xd = false;
   int num_sms = 148;
   int cg = 1;                          // CTAs per MMA: 2 = CTA pairs (cta_group::2, opt-in), 1 = single CTA
   bool can_split = false;              // split-K partial slots carved (D.rows_part) and not disabled
@@ -658,7 +692,7 @@ static bool r_attr(const RPlan& P) {
 
 // Plan of one pass: segments, stage size and depth for CG CTAs per MMA.  CG = 2 splits every
 // segment's B rows between the pair (a single 128-row box becomes two 64-row half boxes).
-static void r_finish(RPlan& P, int h, int CG) {
+static void r_finish(RPlan& P, int h, int CG) {   // h: the units the tiles cover (the output width)
   if (CG == 2)
     for (int sg = 0; sg < P.nseg; ++sg) {
       RSeg& S = P.seg[sg];
@@ -738,6 +772,36 @@ RowsState* rows_init(const Dev& D, int max_vertices) {
   }
   r_finish(F, h, CG);
   r_finish(B, h, CG);
+  // x-projection (Z = X W^T over the pulled rows) and dX = dZ W: single-CTA tiles (CG = 1 only)
+  const int d = D.d;
+  const char* xe = std::getenv("CAVS_ROWS_XD");
+  rs->xd = CG == 1 && !(xe && xe[0] == '0') && d % 256 == 0 && d % 64 == 0;
+  if (rs->xd) {
+    RPlan& X = rs->xp;
+    RPlan& Q = rs->dx;
+    bool okx = renc(&rs->A_xp, D.Xp, (uint64_t)d, Vp, 128);
+    if (lstm) {
+      X.UG = 64; X.n = 256; X.nseg = 1;
+      const int rows4[4] = {0, h, 2 * h, 3 * h};
+      X.seg[0] = rseg(0, 0, 4, 64, rows4, d / 64, 0);
+      okx = okx && renc(&rs->B_x, D.Wb, (uint64_t)d, 4 * (uint64_t)h, 64);          // W4 [4h x d]
+      okx = okx && renc(&rs->B_dx, D.We, G * h, (uint64_t)d, 128);                   // WT [d x G h]
+    } else {
+      X.UG = 256; X.n = 256; X.nseg = 1;
+      const int r01[2] = {0, 128};
+      X.seg[0] = rseg(0, 0, 2, 128, r01, d / 64, 0);
+      okx = okx && renc(&rs->B_x, D.Wb, (uint64_t)d, h, 128);                        // Wx [h x d]
+      okx = okx && renc(&rs->B_dx, D.We, (uint64_t)h, (uint64_t)d, 128);             // WxT [d x h]
+    }
+    X.acc_cols = 256;
+    Q.UG = 256; Q.n = 256; Q.nseg = 1;
+    const int r01[2] = {0, 128};
+    Q.seg[0] = rseg(0, 0, 2, 128, r01, (int)(G * h) / 64, 0);
+    Q.acc_cols = 256;
+    r_finish(X, h, 1);
+    r_finish(Q, d, 1);
+    rs->xd = okx;
+  }
   auto attrs = [&](auto cg) {
     constexpr int C = decltype(cg)::value;
     if (lstm)
@@ -746,6 +810,15 @@ RowsState* rows_init(const Dev& D, int max_vertices) {
     return r_attr<EPI_FC_FWD, 1, 2, C>(F) && r_attr<EPI_FC_BWD, 1, 2, C>(B);
   };
   ok = ok && (CG == 2 ? attrs(std::integral_constant<int, 2>{}) : attrs(std::integral_constant<int, 1>{}));
+  if (ok && rs->xd) {
+    bool okx;
+    if (lstm)
+      okx = (N == 1 ? r_attr<EPI_LSTM_XPROJ, 1, 1, 1>(rs->xp) : r_attr<EPI_LSTM_XPROJ, 2, 1, 1>(rs->xp)) &&
+            r_attr<EPI_DX, 1, 2, 1>(rs->dx);
+    else
+      okx = r_attr<EPI_FC_XPROJ, 1, 2, 1>(rs->xp) && r_attr<EPI_DX, 1, 2, 1>(rs->dx);
+    rs->xd = okx;
+  }
   if (!ok) { delete rs; return nullptr; }
   return rs;
 }
@@ -807,6 +880,33 @@ static void rows_go(const Dev& D, RowsState* rs, bool backward, RPlan& P, cudaSt
     if (!backward) r_launch<EPI_FC_FWD, 1, 2, CG>(rs->A_hk, rs->B_fwd, rs->B_fwd, D, P, grid, s);
     else r_launch<EPI_FC_BWD, 1, 2, CG>(rs->A_dz, rs->B_bwd0, rs->B_bwd1, D, P, grid, s);
   }
+}
+
+bool rows_xd(const RowsState* rs) { return rs && rs->xd; }
+
+bool rows_xproj(const Dev& D, RowsState* rs, cudaStream_t s) {
+  if (!rs || !rs->xd || D.V < 1) return false;
+  RPlan P = rs->xp;
+  P.lo = 0; P.hi = D.V; P.ks = 1; P.dsm = 0;
+  P.ntiles = cdiv(P.hi, 128) * P.nut;
+  const int grid = std::min(P.ntiles, rs->num_sms);
+  if (D.cell == CAVS_CELL_TREE_LSTM) {
+    if (D.N == 1) r_launch<EPI_LSTM_XPROJ, 1, 1, 1>(rs->A_xp, rs->B_x, rs->B_x, D, P, grid, s);
+    else r_launch<EPI_LSTM_XPROJ, 2, 1, 1>(rs->A_xp, rs->B_x, rs->B_x, D, P, grid, s);
+  } else {
+    r_launch<EPI_FC_XPROJ, 1, 2, 1>(rs->A_xp, rs->B_x, rs->B_x, D, P, grid, s);
+  }
+  return true;
+}
+
+bool rows_dx(const Dev& D, RowsState* rs, cudaStream_t s) {
+  if (!rs || !rs->xd || !D.dx || D.V < 1) return false;
+  RPlan P = rs->dx;
+  P.lo = 0; P.hi = D.V; P.ks = 1; P.dsm = 0;
+  P.ntiles = cdiv(P.hi, 128) * P.nut;
+  const int grid = std::min(P.ntiles, rs->num_sms);
+  r_launch<EPI_DX, 1, 2, 1>(rs->A_dz, rs->B_dx, rs->B_dx, D, P, grid, s);
+  return true;
 }
 
 bool rows_level(const Dev& D, RowsState* rs, bool backward, int lo, int hi, cudaStream_t s) {

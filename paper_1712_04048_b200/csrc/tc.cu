@@ -528,6 +528,7 @@ struct TcState {
   GemmState* gs = nullptr;      // row-tiled x-projection / dX GEMMs (gemm.cu)
   LazyState* ls = nullptr;      // stream-K lazy weight-gradient GEMMs (lazy.cu)
   RowsState* rs = nullptr;      // row-tiled level GEMMs for large tasks when the persistent path is off (rows.cu)
+  RowsState* rx = nullptr;      // the row-tiled kernel for the x-projection / dX (= rs, or its own state)
   int rows_min_tiles = 64;      // a task uses the row-tiled kernel from this many tiles on
   // FP32 split mode (bf16x3 operands): rows between the planes of each A map (the weight copy's
   // row count) and of the arenas (Vp); 0 = plain bf16
@@ -659,6 +660,12 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
       if (t->rs) t->info += "; large tasks: row-tiled tcgen05 (>= " + std::to_string(t->rows_min_tiles) + " tiles" +
                             (rows_pair(t->rs) == 2 ? ", CTA pairs)" : ")");
     }
+    t->rx = t->rs ? t->rs : rows_init(D, max_vertices);
+    if (t->rx && !rows_xd(t->rx)) {
+      if (t->rx != t->rs) rows_destroy(t->rx);
+      t->rx = nullptr;
+    }
+    if (t->rx) t->info += "; x-projection / dX: row-tiled tcgen05";
   }
   t->info += D.lazy_off ? "; lazy batching OFF (ablation: per-task weight-gradient GEMMs)"
                         : t->ls ? "; lazy: stream-K tcgen05 (one launch)" : "; lazy: split-K tcgen05 + pack";
@@ -677,6 +684,7 @@ void tc_destroy(TcState* tc) {
   if (tc && tc->ps) persist_destroy(tc->ps);
   if (tc && tc->gs) gemm_destroy(tc->gs);
   if (tc && tc->ls) lazy_destroy(tc->ls);
+  if (tc && tc->rx && tc->rx != tc->rs) rows_destroy(tc->rx);
   if (tc && tc->rs) rows_destroy(tc->rs);
   delete tc;
 }
@@ -999,7 +1007,7 @@ static void fwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
       if (D.split)
         launch_level<EPI_LSTM_XPROJ, 4, kCluster, OpT>(t->A[1], t->A[1], t->B_xp, D, pl(t, gs_lstm_xproj(h, d), 1, 1),
                                                         0, D.V, h, s);
-      else if (!gemm_xproj(D, t->gs, s))
+      else if (!rows_xproj(D, t->rx, s) && !gemm_xproj(D, t->gs, s))
         launch_level<EPI_LSTM_XPROJ, 4, 1, OpT>(t->A[1], t->A[1], t->B_xp, D, pl(t, mono_lstm_xproj(h, d), 1, 1), 0, D.V, h, s);
       P.count(1);
     }
@@ -1022,7 +1030,7 @@ static void fwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
     }
   } else {
     if (!streamed) {
-      if (!gemm_xproj(D, t->gs, s))
+      if (!rows_xproj(D, t->rx, s) && !gemm_xproj(D, t->gs, s))
         launch_level<EPI_FC_XPROJ, 1, 1, OpT>(t->A[1], t->A[1], t->B_xp, D, pl(t, mono_one(d, 1, &zero, &zero), 1, 1), 0, D.V, h, s);
       P.count(1);
     }
@@ -1246,7 +1254,7 @@ static void bwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
   }
   P.mark(CAVS_PH_DX, s);
   if (D.dx) {                                         // pull's adjoint: dX = dZ W
-    if (!gemm_dx(D, t->gs, s)) {
+    if (!rows_dx(D, t->rx, s) && !gemm_dx(D, t->gs, s)) {
       if (lstm) launch_level<EPI_DX, 1, 1, OpT>(t->A[4], t->A[4], t->B_dz, D, pl(t, mono_lstm_dx(h, N), 4, 4), 0, V, d, s);
       else launch_level<EPI_DX, 1, 1, OpT>(t->A[4], t->A[4], t->B_dz, D, pl(t, mono_one(h, 1, &zero, &zero), 4, 4), 0, V, d, s);
     }

@@ -653,6 +653,34 @@ def test_ksliced_gate_split(case, ksl, precision, monkeypatch):
     compare(b, g, o, FP32_TOL if precision == "fp32" else BF16_EMU_TOL, f"ksl {ksl} vs 1 {case} {precision}")
 
 
+XD_CASES = {   # d % 256 == 0: dX tiles of 256 input columns
+    "lstm_n2_h256_d256_sst": lambda: gen.make_batch("tree_lstm", 2, 256, 256, "sst_tree", 24, seed=95),
+    "lstm_n1_h128_d256_chain": lambda: gen.batch_from_graphs([gen.chain(n) for n in (30, 200, 7)] * 20,
+                                                             cell="tree_lstm", N=1, h=128, d=256, seed=96, x_at="all",
+                                                             loss_at="all"),
+    "fc_h256_d256_cbt": lambda: gen.make_batch("tree_fc", 2, 256, 256, "cbt32", 20, seed=97),
+    "fc_h512_sst": lambda: ROWS_CASES["fc_h512_sst"](),
+}
+
+
+@pytest.mark.parametrize("case", list(XD_CASES))
+def test_rows_xproj_dx(case, monkeypatch):
+    """The eager x-projection and dX on the row-tiled kernel (row tiles without an epilogue row skipped)
+    against the oracle and against the row GEMMs of gemm.cu (CAVS_ROWS_XD=0: same bf16 operands, another
+    fp32 summation order); bit-reproducible."""
+    b = XD_CASES[case]()
+    g = run_gpu(b, "bf16")
+    assert "x-projection / dX: row-tiled" in g["ctx"].path_info(), g["ctx"].path_info()
+    compare(b, g, run_oracle(b), BF16_TOL, case + " rows x-projection / dX vs fp64 oracle")
+    g2 = run_gpu(b, "bf16", ctx=g["ctx"])
+    for k in ("h_out", "dparams", "dx"):
+        assert np.array_equal(g[k], g2[k]), f"{case}: {k} not deterministic"
+    monkeypatch.setenv("CAVS_ROWS_XD", "0")
+    o = run_gpu(b, "bf16")
+    assert "x-projection / dX: row-tiled" not in o["ctx"].path_info()
+    compare(b, g, o, 2 * BF16_EMU_TOL, case + " rows vs gemm_rows x-projection / dX")
+
+
 # ------------------------------------------------------------------ inference-only forward
 @pytest.mark.parametrize("case", ["lstm_n2_h512_sst", "fc_h256_cbt"])
 @pytest.mark.parametrize("precision", ["bf16", "fp32"])
