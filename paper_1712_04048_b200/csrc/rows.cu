@@ -774,8 +774,12 @@ RowsState* rows_init(const Dev& D, int max_vertices) {
   r_finish(B, h, CG);
   // x-projection (Z = X W^T over the pulled rows) and dX = dZ W: single-CTA tiles (CG = 1 only)
   const int d = D.d;
+  // default on for Tree-FC (cfg5: x-projection 210 -> 167 us, dX 176 -> 125 us); the Tree-LSTM
+  // x-projection measured slower than gemm.cu's (its epilogue writes five arenas per unit, and the
+  // 2-CTA-per-SM row GEMM overlaps two epilogues), so CAVS_ROWS_XD=1 opts it in, =0 turns both off
   const char* xe = std::getenv("CAVS_ROWS_XD");
-  rs->xd = CG == 1 && !(xe && xe[0] == '0') && d % 256 == 0 && d % 64 == 0;
+  const bool xd_on = xe ? xe[0] == '1' : !lstm;
+  rs->xd = CG == 1 && xd_on && d % 256 == 0;
   if (rs->xd) {
     RPlan& X = rs->xp;
     RPlan& Q = rs->dx;

@@ -669,6 +669,7 @@ def test_rows_xproj_dx(case, monkeypatch):
     against the oracle and against the row GEMMs of gemm.cu (CAVS_ROWS_XD=0: same bf16 operands, another
     fp32 summation order); bit-reproducible."""
     b = XD_CASES[case]()
+    monkeypatch.setenv("CAVS_ROWS_XD", "1")               # (default on for Tree-FC, opt-in for Tree-LSTM)
     g = run_gpu(b, "bf16")
     assert "x-projection / dX: row-tiled" in g["ctx"].path_info(), g["ctx"].path_info()
     compare(b, g, run_oracle(b), BF16_TOL, case + " rows x-projection / dX vs fp64 oracle")

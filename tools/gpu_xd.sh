@@ -1,0 +1,16 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests/test_gpu_parity.py -q -k "rows or persistent or full_size or fp32_tensor or dx_records or shared_pull" > gpurun_out/pytest_xd.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_xd.log; grep -E "^FAILED" gpurun_out/pytest_xd.log | head -8
+run() {  # name env args
+  env $2 timeout 300 python bench.py $3 --steps 20 --warmup 3 --no-cpu-baseline 2>gpurun_out/b.err | tail -1 > gpurun_out/b.json
+  python -c "
+import json; b=json.load(open('gpurun_out/b.json')); print('$1', round(b['value']), round(b['ms_per_step'],4), 'e2e', round(b['e2e']['value']), {k: round(v['ms_per_step'],4) for k,v in b['phases'].items()})" || tail -3 gpurun_out/b.err
+}
+run cfg4 "X=1" "--config cfg4"
+run cfg4_noxd "CAVS_ROWS_XD=0" "--config cfg4"
+run cfg4_noside "CAVS_DB_SIDE=0" "--config cfg4"
+run cfg3 "X=1" "--config cfg3"
+run cfg3_noside "CAVS_DB_SIDE=0" "--config cfg3"
+run cfg5 "X=1" "--config cfg5"
+run cfg5_noxd "CAVS_ROWS_XD=0" "--config cfg5"
+run cfg4_h1024 "X=1" "--config cfg4_h1024"
