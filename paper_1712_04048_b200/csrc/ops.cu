@@ -461,15 +461,7 @@ void launch_prep(const Dev& D, cudaStream_t s) {
     add(Wx, (int)h, (int)d, (int)d, 4, 0, (int)h, 1);                                // WxT = W_x^T [d x h]
     add(b, 1, (int)h, 0, 5, 0, 0, 0);
   }
-  // enough CTAs per job that the largest one (a 32x32-tile transpose at h = 2048: 8k tiles) is not
-  // latency-bound on one tile round trip after another
-  size_t work = 1;
-  for (int i = 0; i < J.n; ++i) {
-    const PrepJob& jb = J.j[i];
-    work = std::max(work, jb.transpose ? (size_t)cdiv(jb.rows, 32) * cdiv(jb.cols, 32)
-                                       : ((size_t)jb.rows * jb.cols + 1023) / 1024);
-  }
-  dim3 grid((unsigned)std::min<size_t>(std::max<size_t>(work / 4, 148), 148 * 8), J.n);
+  dim3 grid(148, J.n);
   if (D.prec == CAVS_BF16) launch_pdl(k_prep<__nv_bfloat16>, grid, dim3(256), 0, s, D, J);
   else if (D.split) launch_pdl(k_prep<S3>, grid, dim3(256), 0, s, D, J);
   else launch_pdl(k_prep<float>, grid, dim3(256), 0, s, D, J);
