@@ -56,6 +56,65 @@ __global__ void k_rate(int iters, unsigned long long* out) {
   if (warp == 0) { ptx::tc_fence_after(); ptx::tmem_dealloc<512>(tmem); }
 }
 
+// k_rows-like issue (r02): SS M = 128 x N x 16 MMAs in k-blocks of 4, a tcgen05.commit to one of S
+// rotating stage barriers after every `every` k-blocks (0: none), nothing waiting on them; is the
+// commit itself a bubble in the tensor pipe?
+template <int N>
+__global__ void k_commit(int iters, int every, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar, st[4];
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    for (int i = 0; i < 4; ++i) ptx::mbar_init(&st[i], 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0) ptx::tmem_alloc<512>(&slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = slot;
+  const uint32_t a = ptx::smem_u32(smem), b = a + 16384;
+  constexpr uint32_t idesc = ptx::idesc_bf16(128, N, 0, 0);
+  if (warp == 0) {
+    unsigned long long t0 = 0;
+    if (ptx::elect_one()) {
+      t0 = clock64();
+      for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          ptx::mma_bf16(tmem, desc(a + kk * 32), desc(b + kk * 32), idesc, it | kk ? 1u : 0u);
+        if (every && (it + 1) % every == 0) ptx::mma_commit(&st[it & 3]);
+      }
+      ptx::mma_commit(&bar);
+    }
+    __syncwarp();
+    ptx::mbar_wait(&bar, 0);
+    if (threadIdx.x == 0) out[blockIdx.x] = clock64() - t0;
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { ptx::tc_fence_after(); ptx::tmem_dealloc<512>(tmem); }
+}
+
+template <int N>
+void run_commit(int every) {
+  unsigned long long* d;
+  cudaMalloc(&d, 8);
+  const int smem = 16384 + N * 128 + 1024;
+  cudaFuncSetAttribute(k_commit<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int iters = 512;
+  k_commit<N><<<1, 128, smem>>>(iters, every, d);
+  k_commit<N><<<1, 128, smem>>>(iters, every, d);
+  cudaDeviceSynchronize();
+  unsigned long long h = 0;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  printf("SS N=%3d commit every %d k-blocks: %6.1f cycles/MMA (floor %d)  err=%s\n", N, every, (double)h / (iters * 4),
+         128 * N / 256, cudaGetErrorString(cudaGetLastError()));
+  cudaFree(d);
+}
+
 // persist-like issue: per tile 2 segments x 8 k-blocks x 4 MMAs (TS, N = 16), A walking 256 TMEM
 // columns, B walking a 32 KB box (16 k-blocks of 16 rows), 2 accumulators; one commit per tile.
 template <int N>
@@ -158,7 +217,11 @@ void run(int grid) {
   cudaFree(d);
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1 && argv[1][0] == 'c') {       // ./mma_rate commit
+    for (int e : {0, 1, 2, 4}) { run_commit<256>(e); run_commit<128>(e); run_commit<64>(e); }
+    return 0;
+  }
   for (int w : {0, 1}) { run_tile<16>(w); run_tile<32>(w); run_tile<64>(w); }
   for (int nz : {1, 2, 3}) { run_tile<16>(1, nz); run_tile<32>(1, nz); }
   return 0;
