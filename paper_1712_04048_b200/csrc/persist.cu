@@ -63,6 +63,7 @@ struct PPlan {
   int mc;                            // 1: B boxes multicast to the whole cluster (every CTA of a graph
                                      //    range reads the same task rows): one TMA per box per cluster
   int xs_off, meta_off, bar_off;
+  int is_bwd;                        // host: backward plan (stage-size override)
 };
 
 // Compile-time staging layout per epilogue kind (matches the host plan of persist_init):
@@ -234,7 +235,14 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
         const uint32_t bytes = (uint32_t)nt * 128u * (uint32_t)sk;
         if (i > 0) {                                  // previous task finished grid-wide
           const unsigned long long tw = D.trace ? gtime() : 0;
-          while (gate_get(gate) < i) { }         // acquire: the cluster's task writes are visible
+          // acquire: the cluster's task writes are visible.  Back off between polls: the producers wait
+          // here through the MMA and epilogue of the previous task, and a tight ld.shared spin competes
+          // with the MMAs' shared-memory operand reads (CAVS_GATE_SPIN=1 build: tight spin, A/B)
+#ifdef CAVS_GATE_SPIN
+          while (gate_get(gate) < i) { }
+#else
+          while (gate_get(gate) < i) __nanosleep(128);
+#endif
           ptx::fence_proxy_async_global();     // ... to this thread's TMA (async proxy) reads
           if (D.trace && w == 0) ptrace(D, 3000 + E, blockIdx.x, i, tw, gtime(), 0, 0, 0);
         }
@@ -340,7 +348,11 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
       unsigned long long tr0 = 0, tr1 = 0, tr2 = 0, tr3 = 0;
       if (D.trace && et == 0) tr0 = gtime();
       if (i > 0 && ntile > 0) {                         // inputs of V_t are final once the barrier passed
+#ifdef CAVS_GATE_SPIN
         if (lane == 0) while (gate_get(gate) < i) { }
+#else
+        if (lane == 0) while (gate_get(gate) < i) __nanosleep(32);
+#endif
         __syncwarp();
       }
       for (int jt = 0; jt < ntile; ++jt, ++tcount) {
@@ -521,11 +533,22 @@ static bool plan_layout(PPlan& P, bool tsA) {
     for (int e = 0; e < sg; ++e)
       if (P.seg_acc[e] == P.seg_acc[sg]) P.seg_init[sg] = 0;
   }
-  // stage size: a 16-row tile of the task in one or two boxes (fewer, larger TMA boxes: the
-  // boxes of one SM are serviced one after another), multiple of 8 KB, <= 48 KB
+  // stage size: as few, large TMA boxes per tile as the pipeline admits -- one SM's boxes are serviced
+  // one after another, ~1 us each (tools/trace_persist.py: a 5-box tile's last box lands 5.5 us after
+  // its first, a 1-box tile's in one), so a 16-row tile is ONE box and larger tiles take few: up to
+  // 2 x the 16-row tile (>= 64 KB), two stages at least, multiples of 16 KB (r02: cfg4 bwd levels
+  // 0.258 -> 0.224 ms with the 80 KB Tree-LSTM backward box, fwd 0.185 -> 0.172 ms with 64 KB)
   const int tile16 = 16 * 128 * P.nseg * P.nkbA;
-  int stage = tile16 <= 32768 ? tile16 : (tile16 / 2 + 8191) / 8192 * 8192;
-  stage = std::max(kPStageMin, std::min(stage, 49152));
+  int stage = std::min({avail / 2, std::max(tile16, 65536), 2 * tile16});
+  stage = std::max(kPStageMin, stage / kPStageMin * kPStageMin);
+  // A/B: B stage bytes (multiple of 16 KB), per pass / both passes
+  if (const char* e = std::getenv(P.is_bwd ? "CAVS_PERSIST_STAGE_BWD" : "CAVS_PERSIST_STAGE_FWD")) {
+    const int v = std::atoi(e);
+    if (v >= kPStageMin && v <= 98304 && v % kPStageMin == 0) stage = v;
+  } else if (const char* e2 = std::getenv("CAVS_PERSIST_STAGE")) {
+    const int v = std::atoi(e2);
+    if (v >= kPStageMin && v <= 98304 && v % kPStageMin == 0) stage = v;
+  }
   P.tsA = tsA ? 1 : 0;
   int S;
   if (tsA) {
@@ -676,6 +699,7 @@ PersistState* persist_init(const Dev& D, int max_vertices, std::string* why) {
   }
   const char* ss = std::getenv("CAVS_PERSIST_SS");    // 1: weights in smem (SS MMA) instead of TMEM
   const bool tsA = !(ss && ss[0] == '1');
+  B.is_bwd = 1;
   if (!plan_layout(F, tsA) || !plan_layout(B, tsA)) { delete ps; *why = "does not fit shared memory / TMEM"; return nullptr; }
   for (int i = 0; i < 3; ++i) {
     ok &= enc3(&ps->B_hk[i], D.Hk, (uint64_t)N * h, Vp, 16u << i, F.sk[i]);
