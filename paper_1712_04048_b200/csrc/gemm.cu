@@ -94,8 +94,10 @@ k_gemm_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
         if (kb >= S) pwait_g(&empty[s], ((kb / S) & 1) ^ 1);
         uint8_t* st = smem + s * STAGE;
         ptx::mbar_arrive_expect_tx(&full[s], STAGE);
-        for (int g = 0; g < NG; ++g)
-          ptx::tma_load_2d(st + kGA + g * UGN * 128, &mB, kb * 64, g * b_gate_stride + u0, &full[s]);
+        if constexpr (NG > 1)                            // all NG gate-row groups in ONE 4-D box (r02):
+          ptx::tma_load_4d(st + kGA, &mB, 0, u0, kb, 0, &full[s]);   // an SM's boxes are serviced serially
+        else
+          ptx::tma_load_2d(st + kGA, &mB, kb * 64, u0, &full[s]);
         ptx::tma_load_2d(st, &mA, a_col0 + kb * 64, p0, &full[s]);
       }
     }
@@ -178,11 +180,23 @@ k_gemm_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
 // =====================================================================================
 struct GemmState {
   CUtensorMap A_xp, A_dz;       // arena rows, box {64, 128}
-  CUtensorMap B_xp, B_dx;       // weight rows: x-projection (box {64, UGN}), dX (box {64, BN})
+  CUtensorMap B_xp, B_dx;       // weight rows: x-projection (Tree-LSTM: 4-D, all gates in one box), dX
   bool ok = false;
 };
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_enc = nullptr;
+
+// [NG x rows x K] weight rows viewed as {64 k, rows, k-block, gate}: box {64, box_rows, 1, NG} = the NG gate
+// groups of box_rows rows of one k-block, smem order [gate][row][64] (the B tile of NG x box_rows rows)
+static bool genc4(CUtensorMap* m, const void* base, uint64_t K, uint64_t rows, uint32_t ng, uint32_t box_rows) {
+  cuuint64_t dims[4] = {64, rows, K / 64, ng};
+  cuuint64_t strides[3] = {K * 2, 128, rows * K * 2};
+  cuuint32_t box[4] = {64, box_rows, 1, ng};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return g_enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 static bool genc(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
   cuuint64_t dims[2] = {cols, rows};
@@ -239,7 +253,7 @@ GemmState* gemm_init(const Dev& D, int max_vertices) {
   if (h % 32 || d % 128 || h % 128) return nullptr;
   GemmState* g = new GemmState();
   bool ok = genc(&g->A_xp, D.Xp, d, Vp, kGRows) && genc(&g->A_dz, D.dZ, G * h, Vp, kGRows);
-  if (lstm) ok = ok && genc(&g->B_xp, D.Wb, d, 4 * h, kXpBN / 4);     // W4 [4h x d]: gate rows g*h + u
+  if (lstm) ok = ok && genc4(&g->B_xp, D.Wb, d, h, 4, kXpBN / 4);    // W4 [4h x d]: gate rows g*h + u
   else ok = ok && genc(&g->B_xp, D.Wb, d, h, kXpBN);                  // W_x [h x d]
   ok = ok && genc(&g->B_dx, D.We, G * h, d, kDxBN);                   // W^T [d x G h]
   if (!ok) { delete g; return nullptr; }

@@ -57,7 +57,11 @@ struct RankPlan { int nb; Bundle b[3]; int nacc; int stages; int stage_bytes; in
 // npair = 6 in the FP32 split mode (bf16x3 operands): every bundle's k-loop runs
 // once per plane pair (s, t) with s + t <= 2, A plane s at A row + s a_prow[map], B plane t at task
 // row + t b_prow (plane-major arenas); npair = 1: plain bf16.
-struct PlanT { RankPlan r[kClMax]; int comb[8][kClMax]; int bar_off; int npair; int a_prow[2]; int b_prow; };
+// kpb > 0 (grouped stages, r02): the maps are 4-D {64 k, rows, k-block, plane} and a stage holds kpb
+// consecutive k-blocks of every A and B tile in all planes, ONE TMA box per tile (one SM's boxes are
+// serviced one after another, ~0.3 us each: fewer, larger boxes; tools/tma_tile).  kpb = 0: the 2-D
+// per-k-block maps (legacy path).
+struct PlanT { RankPlan r[kClMax]; int comb[8][kClMax]; int bar_off; int npair; int a_prow[2]; int b_prow; int kpb; };
 __device__ __constant__ const int kPairS[6] = {0, 0, 1, 0, 1, 2};
 __device__ __constant__ const int kPairT[6] = {0, 1, 0, 2, 1, 0};
 
@@ -146,10 +150,37 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
       constexpr uint32_t idesc = ptx::idesc_bf16(128, NT, 0, 0);
       uint32_t written = 0;                            // accumulators already initialised
       int step = 0;
-      if constexpr (PM) {
+      constexpr int PS[6] = {0, 0, 1, 0, 1, 2}, PT[6] = {0, 1, 0, 2, 1, 0};
+      if (P.kpb > 0) {
+        // grouped stages: tile (plane q, k-block j) of operand i at base_i + (q kpb + j) * TILE
+        const int kpb = P.kpb, np = P.npair > 1 ? 3 : 1;
+        for (int bi = 0; bi < R.nb; ++bi) {
+          const Bundle& b = R.b[bi];
+          for (int g0 = 0; g0 < b.nk; g0 += kpb, ++step) {
+            const int s = step % S;
+            ptx::mbar_wait(&full[s], (step / S) & 1);
+            ptx::tc_fence_after();
+            const uint32_t st = ptx::smem_u32(smem + s * R.stage_bytes);
+            const int kn = min(kpb, b.nk - g0);
+            for (int jj = 0; jj < kn; ++jj)
+              for (int m = 0; m < b.nmma; ++m)
+                for (int pr = 0; pr < P.npair; ++pr) {
+                  const uint32_t a = st + ((b.mma_a[m] * np + PS[pr]) * kpb + jj) * A_TILE;
+                  const uint32_t bb = st + R.offB + ((b.mma_b[m] * np + PT[pr]) * kpb + jj) * B_TILE;
+                  const int acc = b.mma_acc[m] + (pr > 0 ? R.nacc : 0);
+                  const uint32_t d = tmem + acc * NT;
+#pragma unroll
+                  for (int kk = 0; kk < BK / 16; ++kk)
+                    ptx::mma_bf16(d, ptx::sdesc_sw128(a + kk * 32, 16, 1024), ptx::sdesc_sw128(bb + kk * 32, 16, 1024),
+                                  idesc, ((written >> acc) & 1u) | (kk > 0 ? 1u : 0u));
+                  written |= 1u << acc;
+                }
+            ptx::mma_commit(&empty[s]);
+          }
+        }
+      } else if constexpr (PM) {
         // split mode: a stage holds the three planes of every A and B tile of the k-block, the six
         // plane-pair products a_s b_t (s + t <= 2) are issued from it (each plane loaded once)
-        constexpr int PS[6] = {0, 0, 1, 0, 1, 2}, PT[6] = {0, 1, 0, 2, 1, 0};
         for (int bi = 0; bi < R.nb; ++bi) {
           const Bundle& b = R.b[bi];
           for (int kb = 0; kb < b.nk; ++kb, ++step) {
@@ -213,7 +244,26 @@ k_tc_level(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUte
       const int w = warp - 2;
       bool waited = false;
       int step = 0;
-      if constexpr (PM) {
+      if (P.kpb > 0) {
+        // grouped stages: ONE 4-D box {64, rows, kpb, planes} per A / B tile of the stage
+        const int kpb = P.kpb, np = P.npair > 1 ? 3 : 1;
+        for (int bi = 0; bi < R.nb; ++bi) {
+          const Bundle& b = R.b[bi];
+          const CUtensorMap* ma = b.map_a ? &mA1 : &mA0;
+          for (int g0 = 0; g0 < b.nk; g0 += kpb, ++step) {
+            if (step % S != w) continue;
+            const int s = step % S;
+            uint8_t* st = smem + s * R.stage_bytes;
+            if (step >= S) ptx::mbar_wait(&empty[s], ((step / S) & 1) ^ 1);
+            ptx::mbar_arrive_expect_tx(&full[s], np * kpb * (b.nA * A_TILE + b.nB * B_TILE));
+            for (int i = 0; i < b.nA; ++i)
+              ptx::tma_load_4d(st + i * np * kpb * A_TILE, ma, 0, b.a_row[i] + m0, b.a_col0 / BK + g0, 0, &full[s]);
+            if (!waited) { ptx::griddep_wait(); waited = true; }
+            for (int i = 0; i < b.nB; ++i)
+              ptx::tma_load_4d(st + R.offB + i * np * kpb * B_TILE, &mB, 0, p0, b.b_col[i] / BK + g0, 0, &full[s]);
+          }
+        }
+      } else if constexpr (PM) {
         for (int bi = 0; bi < R.nb; ++bi) {
           const Bundle& b = R.b[bi];
           const CUtensorMap* ma = b.map_a ? &mA1 : &mA0;
@@ -537,6 +587,10 @@ struct TcState {
   int vp = 0;
   int num_sms = 148;
   int ksl_force = 0;            // CAVS_TC_KSL=1|2|4: K slices per gate rank of the per-task kernels (0: by size)
+  // grouped-stage maps (PlanT::kpb): 4-D {64 k, rows, k-block, plane} views of the same tensors, one per
+  // kpb in {1, 2, 4} (the box covers kpb k-blocks x all planes); grp = 0: CAVS_TC_GROUP=0 (legacy maps)
+  bool grp = false;
+  CUtensorMap A4[5][3], B4_hk[3], B4_xp[3], B4_dz[3];
   std::string info;
 };
 
@@ -569,6 +623,34 @@ static bool encode(CUtensorMap* m, const void* base, uint64_t cols, uint64_t row
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+// 4-D view {64 k, rows, k-block, plane} of a row-major [planes x rows x K] bf16 tensor (plane q
+// plane_rows rows after plane 0), box {64, box_rows, kpb, np}: one box = kpb k-block tiles of box_rows
+// rows in every plane, smem order [plane][k-block][row][64] (each tile SW128, K-major)
+static bool encode4(CUtensorMap* m, const void* base, uint64_t K, uint64_t rows, uint64_t np, uint64_t plane_rows,
+                    uint32_t box_rows, uint32_t kpb) {
+  cuuint64_t dims[4] = {64, rows, K / 64, np};
+  cuuint64_t strides[3] = {K * 2, 128, plane_rows * K * 2};
+  cuuint32_t box[4] = {64, box_rows, kpb, (cuuint32_t)np};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// the grouped-stage map of a legacy map of this context (nullptr: none)
+static thread_local const TcState* g_tc = nullptr;
+static const CUtensorMap* map4(const CUtensorMap* m, int kidx) {
+  const TcState* t = g_tc;
+  if (!t || !t->grp) return nullptr;
+  for (int i = 0; i < 5; ++i)
+    if (m == &t->A[i]) return &t->A4[i][kidx];
+  if (m == &t->B_hk) return &t->B4_hk[kidx];
+  if (m == &t->B_xp) return &t->B4_xp[kidx];
+  if (m == &t->B_dz) return &t->B4_dz[kidx];
+  return nullptr;
 }
 
 cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* err) {
@@ -625,6 +707,29 @@ cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* 
   ok &= encode(&t->M_dz, D.dZ, G * h, np * Vp, G * h, 64, 64);
   ok &= encode(&t->M_hk, D.Hk, N * h, np * Vp, N * h, 64, 64);
   ok &= encode(&t->M_xp, D.Xp, d, np * Vp, d, 64, 64);
+  {
+    // opt-in (CAVS_TC_GROUP=1): measured slower than the per-k-block boxes issued by one warp per stage
+    // (cfg4 h = 1024 155.8k vs 157.2k, fp32 113.4k vs 120.7k samples/s; profiles/r02_ablations.md)
+    const char* ge = std::getenv("CAVS_TC_GROUP");
+    t->grp = ge && ge[0] == '1';
+    // A maps: (base, K = row width, rows per plane) as the 2-D maps above
+    const void* ab[5] = {D.Wa, D.Wb, D.Wc, lstm ? D.Wd : D.Wc, D.We};
+    uint64_t ak[5], am[5];
+    if (lstm) {
+      const uint64_t k5[5] = {h, d, 3 * h, h, G * h}, m5[5] = {4 * h, 4 * h, h, h, d};
+      for (int i = 0; i < 5; ++i) { ak[i] = k5[i]; am[i] = m5[i]; }
+    } else {
+      const uint64_t k5[5] = {2 * h, d, h, h, h}, m5[5] = {h, h, 2 * h, 2 * h, d};
+      for (int i = 0; i < 5; ++i) { ak[i] = k5[i]; am[i] = m5[i]; }
+    }
+    for (int kx = 0; kx < 3 && t->grp; ++kx) {
+      const uint32_t kpb = 1u << kx;
+      for (int i = 0; i < 5; ++i) t->grp &= encode4(&t->A4[i][kx], ab[i], ak[i], am[i], np, am[i], 128, kpb);
+      t->grp &= encode4(&t->B4_hk[kx], D.Hk, N * h, Vp, np, Vp, NT, kpb);
+      t->grp &= encode4(&t->B4_xp[kx], D.Xp, d, Vp, np, Vp, NT, kpb);
+      t->grp &= encode4(&t->B4_dz[kx], D.dZ, G * h, Vp, np, Vp, NT, kpb);
+    }
+  }
   if (!ok) {
     *err = "cuTensorMapEncodeTiled failed";
     delete t;
@@ -714,13 +819,28 @@ static void add_mma(Bundle& b, int a, int bt, int acc) {
 
 static int plan_finalize(PlanT& P, int CL) {
   int pipe = 0, xs = 0;
+  const int np = P.npair > 1 ? 3 : 1;                  // split mode: three planes of every tile per stage
+  if (P.kpb > 0) {                                     // grouped stages: the largest kpb with >= 2 stages
+    int per = 0, maxnk = 1;
+    for (int r = 0; r < CL; ++r) {
+      const RankPlan& R = P.r[r];
+      int maxA = 1, maxB = 1;
+      for (int i = 0; i < R.nb; ++i) {
+        maxA = std::max(maxA, R.b[i].nA); maxB = std::max(maxB, R.b[i].nB); maxnk = std::max(maxnk, R.b[i].nk);
+      }
+      per = std::max(per, np * (maxA * A_TILE + maxB * B_TILE));
+    }
+    int kpb = 4;
+    while (kpb > 1 && (2 * kpb * per > kSmemBudget || kpb > maxnk)) kpb /= 2;
+    P.kpb = kpb;
+  }
+  const int kg = P.kpb > 0 ? P.kpb : 1;
   for (int r = 0; r < CL; ++r) {
     RankPlan& R = P.r[r];
     int maxA = 1, maxB = 1;
     for (int i = 0; i < R.nb; ++i) { maxA = std::max(maxA, R.b[i].nA); maxB = std::max(maxB, R.b[i].nB); }
-    const int np = P.npair > 1 ? 3 : 1;                // split mode: three planes of every tile per stage
-    R.offB = np * maxA * A_TILE;
-    R.stage_bytes = R.offB + np * maxB * B_TILE;
+    R.offB = kg * np * maxA * A_TILE;
+    R.stage_bytes = R.offB + kg * np * maxB * B_TILE;
     R.stages = std::max(1, std::min(6, kSmemBudget / R.stage_bytes));
     pipe = std::max(pipe, R.stages * R.stage_bytes);
     xs = std::max(xs, R.nacc * NT * 128 * 4);
@@ -896,7 +1016,14 @@ template <int E, int NACC, int CL, class OpT>
 static void launch_level(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const Dev& D, PlanT P,
                          int row_lo, int row_hi, int units, cudaStream_t s) {
   if (row_hi <= row_lo) return;
+  // grouped stages when this context has the 4-D views of the three maps (kpb chosen by plan_finalize)
+  const CUtensorMap *ga0 = map4(&a0, 0), *ga1 = map4(&a1, 0), *gb = map4(&b, 0);
+  P.kpb = (ga0 && ga1 && gb) ? 1 : 0;
   const int smem = plan_finalize(P, CL);
+  const int kx = P.kpb == 4 ? 2 : P.kpb == 2 ? 1 : 0;
+  const CUtensorMap& A0 = P.kpb > 0 ? *map4(&a0, kx) : a0;
+  const CUtensorMap& A1 = P.kpb > 0 ? *map4(&a1, kx) : a1;
+  const CUtensorMap& B0 = P.kpb > 0 ? *map4(&b, kx) : b;
   static int attr_set[kMaxDev] = {};                   // dynamic + static smem must stay <= 227 KB
   const int dv = cur_device();
   if (smem > attr_set[dv]) {
@@ -920,7 +1047,7 @@ static void launch_level(const CUtensorMap& a0, const CUtensorMap& a1, const CUt
   ++na;
   cfg.attrs = at2;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, k_tc_level<E, NACC, CL, OpT>, a0, a1, b, D, P, row_lo, row_hi, units);
+  cudaLaunchKernelEx(&cfg, k_tc_level<E, NACC, CL, OpT>, A0, A1, B0, D, P, row_lo, row_hi, units);
 }
 
 // per-task dispatch on the arity N (NACC = BASE + N) and the cluster size cl (1: monolithic, 4: gate
@@ -1263,12 +1390,14 @@ static void bwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
 }
 
 void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, Prof& P, XStream* xs) {
+  g_tc = t;
   if (D.split) fwd_t<S3>(D, t, lp, s, P, xs);
   else fwd_t<__nv_bfloat16>(D, t, lp, s, P, xs);
 }
 
 void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, int* split, Prof& P,
                  cudaEvent_t wgrad_ev, cudaEvent_t levels_ev) {
+  g_tc = t;
   if (D.split) bwd_t<S3>(D, t, lp, s, split, P, wgrad_ev, levels_ev);
   else bwd_t<__nv_bfloat16>(D, t, lp, s, split, P, wgrad_ev, levels_ev);
 }

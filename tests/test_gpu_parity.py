@@ -682,6 +682,22 @@ def test_rows_xproj_dx(case, monkeypatch):
     compare(b, g, o, 2 * BF16_EMU_TOL, case + " rows vs gemm_rows x-projection / dX")
 
 
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+@pytest.mark.parametrize("case", ["lstm_n2_h128_sst", "fc_h256_cbt"])
+def test_grouped_stages(case, precision, monkeypatch):
+    """Opt-in grouped pipeline stages of the per-task kernels (CAVS_TC_GROUP=1: 4-D TMA boxes over k-blocks
+    and planes) against the per-k-block boxes: same operands, same summation order -> bit-identical."""
+    b = KSL_CASES[case]()
+    monkeypatch.setenv("CAVS_PERSIST", "0")
+    monkeypatch.setenv("CAVS_ROWS", "0")
+    o = run_gpu(b, precision)
+    monkeypatch.setenv("CAVS_TC_GROUP", "1")
+    g = run_gpu(b, precision)
+    compare(b, g, run_oracle(b), FP32_TOL if precision == "fp32" else BF16_TOL, f"grouped {case} {precision}")
+    for k in ("h_out", "dparams", "dx"):
+        assert np.array_equal(g[k], o[k]), f"{case} {precision}: grouped stages change {k}"
+
+
 # ------------------------------------------------------------------ inference-only forward
 @pytest.mark.parametrize("case", ["lstm_n2_h512_sst", "fc_h256_cbt"])
 @pytest.mark.parametrize("precision", ["bf16", "fp32"])
