@@ -570,7 +570,9 @@ static bool plan_layout(PPlan& P, bool tsA) {
   if (P.max_ni < 0) return false;
   P.meta_off = P.xs_off + xs;
   P.bar_off = (P.meta_off + 15) & ~15;
-  for (int i = 0; i < 3; ++i) P.sk[i] = stage / ((16 << i) * 128);   // k-blocks per box (<= 256)
+  // k-blocks per box (<= 256), never more than a tile has (a box past the arena's last k-block would be
+  // zero-filled by the TMA: bytes moved for nothing)
+  for (int i = 0; i < 3; ++i) P.sk[i] = std::min(stage / ((16 << i) * 128), P.nseg * P.nkbA);
   return true;
 }
 static int plan_smem(const PPlan& P) { return 1024 + P.bar_off + 2 * kPMaxS * 8 + 64; }
