@@ -44,6 +44,7 @@ struct cavs_ctx {
   cudaStream_t db_s = nullptr;
   cudaEvent_t ev_lv = nullptr, ev_db = nullptr;
   bool db_side = true;
+  bool dx_side = true;                  // dX = dZ W on db_s too (CAVS_DX_SIDE=0: on the main stream)
   // pipelined host-buffer steps (cavs_train_step_host_async): two staging slots, H2D / D2H streams
   struct Slot {
     int *gp = nullptr, *cp = nullptr, *ci = nullptr, *xrow = nullptr, *grow = nullptr;
@@ -184,6 +185,8 @@ CAVS_API cavs_status cavs_create(const cavs_desc* desc, int device, void* stream
     const char* sx = std::getenv("CAVS_STREAMING");
     const char* dbs = std::getenv("CAVS_DB_SIDE");
     c->db_side = !(dbs && dbs[0] == '0');
+    const char* dxs = std::getenv("CAVS_DX_SIDE");
+    c->dx_side = !(dxs && dxs[0] == '0');
     c->D.lazy_off = lz && lz[0] == '0';
     c->D.unfused = uf && uf[0] == '1';
     c->D.stream_x = sx && sx[0] == '1';
@@ -483,7 +486,9 @@ CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dp
       CK(cudaEventCreateWithFlags(&ctx->ev_lv, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&ctx->ev_db, cudaEventDisableTiming));
     }
-    tc_backward(D, ctx->tc, ctx->lp, ctx->stream, split, P, ctx->ev_wgrad, ctx->db_side ? ctx->ev_lv : nullptr);
+    // dX on the side stream (before db there) beside the lazy GEMMs unless CAVS_DX_SIDE=0
+    tc_backward(D, ctx->tc, ctx->lp, ctx->stream, split, P, ctx->ev_wgrad, ctx->db_side ? ctx->ev_lv : nullptr,
+                ctx->db_side && ctx->dx_side ? ctx->db_s : nullptr);
   } else {
     simt_backward<float>(D, ctx->lp, ctx->stream, P);
   }

@@ -1205,9 +1205,21 @@ static int launch_II(const CUtensorMap& a, const CUtensorMap& b, const Dev& D, P
   return P.split;
 }
 
+// pull's adjoint: dX = dZ W
+template <class OpT>
+static void launch_dx(Dev& D, TcState* t, cudaStream_t s) {
+  const int h = D.h, N = D.N, V = D.V, d = D.d;
+  const int zero = 0;
+  if (rows_dx(D, t->rx, s) || gemm_dx(D, t->gs, s)) return;
+  if (D.cell == CAVS_CELL_TREE_LSTM)
+    launch_level<EPI_DX, 1, 1, OpT>(t->A[4], t->A[4], t->B_dz, D, pl(t, mono_lstm_dx(h, N), 4, 4), 0, V, d, s);
+  else
+    launch_level<EPI_DX, 1, 1, OpT>(t->A[4], t->A[4], t->B_dz, D, pl(t, mono_one(h, 1, &zero, &zero), 4, 4), 0, V, d, s);
+}
+
 template <class OpT>
 static void bwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, int* split, Prof& P,
-                  cudaEvent_t wgrad_ev, cudaEvent_t levels_ev) {
+                  cudaEvent_t wgrad_ev, cudaEvent_t levels_ev, cudaStream_t dx_s) {
   const int skmax = skinny_max(D);
   split[0] = split[1] = split[2] = 1;
   if (t->use_simt) {
@@ -1293,6 +1305,13 @@ static void bwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
     }
   }
   if (levels_ev) cudaEventRecord(levels_ev, s);      // every dZ row final: db may run beside the lazy GEMMs
+  // dX = dZ W only reads dZ and the weights: on dx_s it overlaps the lazy GEMMs (disjoint outputs)
+  const bool dx_side = dx_s && levels_ev && D.dx && !D.lazy_off;
+  if (dx_side) {
+    cudaStreamWaitEvent(dx_s, levels_ev, 0);
+    launch_dx<OpT>(D, t, dx_s);
+    P.count(1);
+  }
   P.mark(CAVS_PH_LAZY, s);
   // ---- lazy batching of the parameter gradients ----
   const LazyLayout Z = lazy_layout(D);
@@ -1380,13 +1399,7 @@ static void bwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
     split[2] = launch_II(t->M_dz, t->M_xp, D, pl2(t, Cw), w, s); P.count(1);
   }
   P.mark(CAVS_PH_DX, s);
-  if (D.dx) {                                         // pull's adjoint: dX = dZ W
-    if (!rows_dx(D, t->rx, s) && !gemm_dx(D, t->gs, s)) {
-      if (lstm) launch_level<EPI_DX, 1, 1, OpT>(t->A[4], t->A[4], t->B_dz, D, pl(t, mono_lstm_dx(h, N), 4, 4), 0, V, d, s);
-      else launch_level<EPI_DX, 1, 1, OpT>(t->A[4], t->A[4], t->B_dz, D, pl(t, mono_one(h, 1, &zero, &zero), 4, 4), 0, V, d, s);
-    }
-    P.count(1);
-  }
+  if (D.dx && !dx_side) { launch_dx<OpT>(D, t, s); P.count(1); }
 }
 
 void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, Prof& P, XStream* xs) {
@@ -1396,10 +1409,10 @@ void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, 
 }
 
 void tc_backward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, int* split, Prof& P,
-                 cudaEvent_t wgrad_ev, cudaEvent_t levels_ev) {
+                 cudaEvent_t wgrad_ev, cudaEvent_t levels_ev, cudaStream_t dx_s) {
   g_tc = t;
-  if (D.split) bwd_t<S3>(D, t, lp, s, split, P, wgrad_ev, levels_ev);
-  else bwd_t<__nv_bfloat16>(D, t, lp, s, split, P, wgrad_ev, levels_ev);
+  if (D.split) bwd_t<S3>(D, t, lp, s, split, P, wgrad_ev, levels_ev, dx_s);
+  else bwd_t<__nv_bfloat16>(D, t, lp, s, split, P, wgrad_ev, levels_ev, dx_s);
 }
 
 }  // namespace cavs

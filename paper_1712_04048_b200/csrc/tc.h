@@ -15,8 +15,9 @@ void tc_forward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s,
 // wgrad_ev (nullable): recorded on s once the lazy GEMMs wrote every weight block of dparams
 // (stream-K path; otherwise the caller records it after the split-K pack).
 void tc_backward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, int* split /*[3]*/, Prof& P,
-                 cudaEvent_t wgrad_ev = nullptr, cudaEvent_t levels_ev = nullptr);
+                 cudaEvent_t wgrad_ev = nullptr, cudaEvent_t levels_ev = nullptr, cudaStream_t dx_s = nullptr);
 // levels_ev (nullable): recorded on s once the level tasks wrote every dZ row (db can start)
+// dx_s (nullable, needs levels_ev): dX = dZ W runs there, beside the lazy weight-gradient GEMMs on s
 void tc_destroy(TcState* tc);
 std::string tc_describe(const TcState* tc);   // which level-kernel path is active
 int tc_clusters(const TcState* tc);           // graph-range clusters of the persistent level kernels (0: none)
