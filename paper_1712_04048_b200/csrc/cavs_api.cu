@@ -423,9 +423,11 @@ static cavs_status forward_impl(cavs_ctx* ctx, const float* params, int32_t n_x,
     CK(cudaEventRecord(ctx->ev_lv, ctx->stream));
     CK(cudaStreamWaitEvent(ctx->db_s, ctx->ev_lv, 0));
     launch_prep(D, ctx->db_s);
+    if (ctx->tc) tc_zero_dz_tail(D, ctx->tc, ctx->db_s);
     CK(cudaEventRecord(ctx->ev_db, ctx->db_s));
   } else {
     launch_prep(D, ctx->stream);
+    if (ctx->tc) tc_zero_dz_tail(D, ctx->tc, ctx->stream);
   }
   CK(cudaMemsetAsync(D.hdr + 4, 0, 2 * sizeof(int), ctx->stream));   // k_pull's statistics of this forward
   launch_pull(D, ctx->stream);
@@ -472,7 +474,7 @@ CAVS_API cavs_status cavs_backward(cavs_ctx* ctx, const float* dh_out, float* dp
   // dx rows receive plain stores when every record is pulled exactly once (the usual case); the
   // zeroing + atomic adds only run when some record is pulled by several vertices or by none
   // (k_pull.s duplicate flag / pull count; decided on the device by k_dx_zero and the DX epilogue)
-  if (dx && D.n_x > 0) { launch_dx_zero(D, ctx->stream); P.count(1); }
+  if (dx && D.n_x > 0 && !ctx->tc) { launch_dx_zero(D, ctx->stream); P.count(1); }   // (tc: in tc_backward)
   P.mark(CAVS_PH_BWD_ROOTS, ctx->stream);
   if (!D.dag) {                                // DAG batches: every vertex's dF runs in launch_dag_df
     launch_roots(D, ctx->T >= 0 ? ctx->n_roots : -1, D.roots, ctx->stream);   // -1: count on the device

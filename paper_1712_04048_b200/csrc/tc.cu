@@ -1222,6 +1222,10 @@ static void bwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
                   cudaEvent_t wgrad_ev, cudaEvent_t levels_ev, cudaStream_t dx_s) {
   const int skmax = skinny_max(D);
   split[0] = split[1] = split[2] = 1;
+  // dX = dZ W only reads dZ and the weights: on dx_s it overlaps the lazy GEMMs (disjoint outputs);
+  // the dx zeroing (usually an early exit) goes with it
+  const bool dx_side = dx_s && levels_ev && D.dx && !D.lazy_off && !t->use_simt;
+  if (D.dx && D.n_x > 0 && !dx_side) { launch_dx_zero(D, s); P.count(1); }
   if (t->use_simt) {
     simt_backward<__nv_bfloat16>(D, lp, s, P);
     if (levels_ev) cudaEventRecord(levels_ev, s);      // (db after the whole FFMA backward)
@@ -1232,9 +1236,6 @@ static void bwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
   const int G = lstm ? 3 + N : 1;
   const bool gs = !t->mono;
   const SegListI Bs = bwd_segments(D);
-  // rows past V of dZ are read by the lazy GEMMs' last k-block: keep them zero
-  for (int q = 0; q < (D.split ? 3 : 1); ++q)
-    cudaMemsetAsync(reinterpret_cast<__nv_bfloat16*>(D.dZ) + q * D.ps_dz + (size_t)D.V * G * h, 0, (size_t)64 * G * h * 2, s);
   if (D.dag) {
     // DAG batch (NEXT-3): per task, the pull-reduce + dF of its vertices (every parent is in a
     // later task, already done), then the level GEMM whose epilogue only sends the edge gradients
@@ -1305,10 +1306,9 @@ static void bwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
     }
   }
   if (levels_ev) cudaEventRecord(levels_ev, s);      // every dZ row final: db may run beside the lazy GEMMs
-  // dX = dZ W only reads dZ and the weights: on dx_s it overlaps the lazy GEMMs (disjoint outputs)
-  const bool dx_side = dx_s && levels_ev && D.dx && !D.lazy_off;
   if (dx_side) {
     cudaStreamWaitEvent(dx_s, levels_ev, 0);
+    if (D.n_x > 0) { launch_dx_zero(D, dx_s); P.count(1); }
     launch_dx<OpT>(D, t, dx_s);
     P.count(1);
   }
@@ -1400,6 +1400,13 @@ static void bwd_t(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s
   }
   P.mark(CAVS_PH_DX, s);
   if (D.dx && !dx_side) { launch_dx<OpT>(D, t, s); P.count(1); }
+}
+
+void tc_zero_dz_tail(const Dev& D, const TcState* t, cudaStream_t s) {
+  if (t->use_simt) return;                            // (the FFMA backward reads no row past V)
+  const size_t Gh = (size_t)(D.cell == CAVS_CELL_TREE_LSTM ? 3 + D.N : 1) * D.h;
+  for (int q = 0; q < (D.split ? 3 : 1); ++q)
+    cudaMemsetAsync(reinterpret_cast<__nv_bfloat16*>(D.dZ) + q * D.ps_dz + (size_t)D.V * Gh, 0, 64 * Gh * 2, s);
 }
 
 void tc_forward(Dev& D, TcState* t, const std::vector<int>& lp, cudaStream_t s, Prof& P, XStream* xs) {

@@ -12,6 +12,9 @@ struct TcState;
 cavs_status tc_init(const Dev& D, int max_vertices, TcState** out, std::string* err);
 // Launches are counted into P; phase marks XPROJ -> FWD_LEVELS and BWD_LEVELS -> LAZY -> DX.
 void tc_forward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, Prof& P, XStream* xs = nullptr);
+// the 64 dZ rows past V read by the lazy GEMMs' last k-block -> 0 (any time between the last backward's
+// lazy GEMMs and the next one's: cavs_forward issues it beside the pull)
+void tc_zero_dz_tail(const Dev& D, const TcState* tc, cudaStream_t s);
 // wgrad_ev (nullable): recorded on s once the lazy GEMMs wrote every weight block of dparams
 // (stream-K path; otherwise the caller records it after the split-K pack).
 void tc_backward(Dev& D, TcState* tc, const std::vector<int>& lp, cudaStream_t s, int* split /*[3]*/, Prof& P,
