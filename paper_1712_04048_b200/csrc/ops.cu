@@ -78,6 +78,9 @@ __global__ void __launch_bounds__(256) k_prep(Dev D, PrepJobs J) {
 }
 
 // One CTA per 64-position tile; 4 consecutive x values per thread and step (16-byte loads).
+// A grid of at most two tiles per SM (cfg4: ~148 tiles) runs 512 threads (8 loads of 16 B each in
+// flight: ~64 KB per SM, what HBM latency x bandwidth asks for); larger grids keep 256 (several
+// CTAs per SM already; 512 measured slower on cfg5's 511 tiles)
 template <class OpT>
 __global__ void k_pull(Dev D) {
   pdl_wait();
@@ -468,9 +471,13 @@ void launch_prep(const Dev& D, cudaStream_t s) {
 }
 
 void launch_pull(const Dev& D, cudaStream_t s) {
-  if (D.prec == CAVS_BF16) launch_pdl(k_pull<__nv_bfloat16>, dim3(cdiv(D.V, 64)), dim3(256), 0, s, D);
-  else if (D.split) launch_pdl(k_pull<S3>, dim3(cdiv(D.V, 64)), dim3(256), 0, s, D);
-  else launch_pdl(k_pull<float>, dim3(cdiv(D.V, 64)), dim3(256), 0, s, D);
+  static int n_sm[kMaxDev] = {};
+  const int dv = cur_device();
+  if (!n_sm[dv]) cudaDeviceGetAttribute(&n_sm[dv], cudaDevAttrMultiProcessorCount, dv);
+  const int nt = cdiv(D.V, 64) <= 2 * n_sm[dv] ? 512 : 256;
+  if (D.prec == CAVS_BF16) launch_pdl(k_pull<__nv_bfloat16>, dim3(cdiv(D.V, 64)), dim3(nt), 0, s, D);
+  else if (D.split) launch_pdl(k_pull<S3>, dim3(cdiv(D.V, 64)), dim3(nt), 0, s, D);
+  else launch_pdl(k_pull<float>, dim3(cdiv(D.V, 64)), dim3(nt), 0, s, D);
 }
 
 void launch_roots(const Dev& D, int n_roots, const int* roots, cudaStream_t s) {
