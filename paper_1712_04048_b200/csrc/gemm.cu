@@ -66,6 +66,10 @@ k_gemm_rows(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUte
   const int p0 = blockIdx.x * kGRows;
   const int u0 = blockIdx.y * UGN;
   ptx::griddep_wait();                                   // flags / arenas of the previous kernels
+  // PDL: the next kernel (the persistent forward after the x-projection) may launch once every CTA
+  // of this grid is resident, so its prologue (weights -> TMEM) overlaps this grid's last wave; its
+  // own griddepcontrol.wait still orders every read of this grid's outputs
+  if (threadIdx.x == 0) ptx::griddep_launch();
   if (dev_skip(D)) return;                               // sync-free mode: invalid / DAG batch
   // rows needing the epilogue: level-0 vertices (x-projection) or pull records (k_pull's flags)
   {

@@ -140,6 +140,9 @@ __global__ void k_pull(Dev D) {
 template <class OpT>
 __global__ void k_roots(Dev D, int n_roots, const int* roots) {
   pdl_wait();
+  // PDL: the persistent backward's prologue (weights -> TMEM) may overlap this kernel (its
+  // griddepcontrol.wait orders the reads of these dZ rows)
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (dev_skip(D)) return;
   if (n_roots < 0) n_roots = D.hdr[2];                      // sync-free mode: the device count
   const size_t n = (size_t)n_roots * D.h;
