@@ -204,6 +204,10 @@ k_persist(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUten
   if (warp == kPMma) ptx::tmem_alloc<512>(tmem_slot);
   ptx::tc_fence_before();
   cluster_sync_all();                                 // peers' barriers initialised before any remote arrive
+  // PDL: every CTA of this persistent grid is resident from here on, so the next kernel (k_roots after
+  // the forward, the lazy GEMMs after the backward) may launch onto the idle SMs and run its prologue;
+  // its griddepcontrol.wait still orders every read of this grid's outputs
+  if (threadIdx.x == 0) ptx::griddep_launch();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
